@@ -1,0 +1,231 @@
+/*
+ * uot_b200.h -- C-ABI of the B200 (sm_100a) implementation of the two hot
+ * paths of arXiv 2201.00730: translation-invariant (H-) Sinkhorn for entropic
+ * unbalanced OT, and 1-D Frank-Wolfe UOT with its multimarginal barycenter.
+ *
+ * The reference (uotkit, /root/reference/pkg/src/uotkit) is pure Python; its
+ * "plugin boundary" is the public solver API re-exported by
+ * src/__init__.py:10-70.  Each entry point below names the reference
+ * interface it replaces (file:line, relative to that package).
+ *
+ * Conventions:
+ *  - Plain pointers and sizes.  Array arguments are DEVICE pointers unless
+ *    stated; dtype is given per call (fp32 or fp64).  Batched arrays are
+ *    dense row-major with the batch index outermost.
+ *  - No allocation inside: the caller provides a device workspace whose size
+ *    is returned by the matching *_workspace_size query.
+ *  - Work is enqueued on the caller's cudaStream_t (passed as void*); calls
+ *    are reentrant per stream.
+ *  - Every call returns a status.  Codes map onto the reference exceptions
+ *    (src/exceptions.py:4-25): 1 MassBalanceError, 2 UnsupportedEntropyError,
+ *    3 ValueError, 6 InfeasibleDualError; 4/5 are CUDA / NCCL failures.
+ *    uot_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef UOT_B200_H
+#define UOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  UOT_OK = 0,
+  UOT_ERR_MASS_BALANCE = 1,
+  UOT_ERR_UNSUPPORTED_ENTROPY = 2,
+  UOT_ERR_INVALID = 3,
+  UOT_ERR_CUDA = 4,
+  UOT_ERR_NCCL = 5,
+  UOT_ERR_INFEASIBLE = 6
+};
+
+enum { UOT_F32 = 0, UOT_F64 = 1 };
+enum { UOT_SINKHORN_F = 0, UOT_SINKHORN_H = 1 };
+/* Ground costs: squared Euclidean between d-dim point clouds; |x-y|^p on 1-D
+ * points (src/measures.py:93-105 PowerDistance); dense explicit matrix
+ * (src/measures.py:108-122 ExplicitMatrix). */
+enum { UOT_COST_SQEUCLID = 0, UOT_COST_POWER = 1, UOT_COST_EXPLICIT = 2 };
+enum { UOT_STEP_HARMONIC = 0, UOT_STEP_LINESEARCH = 1 };
+
+/* Library identity / diagnostics. */
+const char* uot_version(void);
+const char* uot_last_error(void);
+int uot_device_arch(int device, int* sm_major, int* sm_minor);
+
+/* ------------------------------------------------------------------------
+ * Sinkhorn: replaces src/sinkhorn.py:246-315 `run(prob, config, init)` for
+ * variants "f" (f_sinkhorn_step, :103-114) and "h" (h_sinkhorn_step,
+ * :137-163) with KL marginals (KL(rho1), KL(rho2)), for a batch of
+ * independent problems, with a fixed iteration budget and the reference's
+ * optional `delta_f < tol` stop (:304-306) evaluated per problem.
+ *
+ * Inputs (dtype elements): x [batch][n][d], y [batch][m][d] (d = 1 for
+ * UOT_COST_POWER); explicit costs c [batch][n][m] and its transpose
+ * ct [batch][m][n]; weights a [batch][n], b [batch][m].  f [batch][n] holds
+ * the initial f when init_given (the g input is unused by both variants,
+ * exactly as in the reference) and receives the final pair with g.
+ * trace_delta [batch][iters] (fp64) receives ||f_t - f_{t-1}||_inf,
+ * iterations [batch] the number of steps taken.
+ *
+ * Row sharding (BASELINE cfg3): with nccl_comm != NULL the n rows given are
+ * this rank's slice of a problem whose target side (y, b, g) is replicated;
+ * column partial log-sum-exps are exchanged with one ncclAllGather per
+ * iteration.  nranks > 1 with nccl_comm == NULL emulates the same protocol
+ * in one process on one GPU (x, a, f then hold all shards back to back and
+ * shard_rows[nranks] gives the row count of each shard).
+ * ------------------------------------------------------------------------ */
+typedef struct uot_sinkhorn_desc {
+  int32_t variant, dtype, cost;
+  int32_t batch, n, m, d;
+  double p;
+  double eps, rho1, rho2;
+  const void* x;
+  const void* y;
+  const void* c;
+  const void* ct;
+  const void* a;
+  const void* b;
+  void* f;
+  void* g;
+  int32_t init_given;
+  int32_t iters;
+  double tol;
+  int32_t use_tol;
+  double* trace_delta;
+  int32_t* iterations;
+  void* nccl_comm;
+  int32_t nranks, rank;
+  const int32_t* shard_rows; /* host array [nranks] (emulation only) */
+} uot_sinkhorn_desc;
+
+int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);
+int uot_sinkhorn_run(const uot_sinkhorn_desc* desc, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* Softmin / log-sum-exp reductions used by the API mirror:
+ * replaces src/duality.py:160-178 `lambda_star` (KL closed form),
+ * src/entropies.py:187-200 `softmin` and src/duality.py:279-290 `_eval_h_kl`
+ * for a batch: out[b*3 + 0] = lambda*, out[b*3 + 1] = H_0 (no eps term),
+ * out[b*3 + 2] = Smin_a^{rho1}(f).  fp64, device pointers, out [batch][3]. */
+int uot_kl_scalars(int32_t batch, int32_t n, int32_t m, const double* a, const double* b,
+                   const double* f, const double* g, double rho1, double rho2, double* out,
+                   void* stream);
+
+/* ------------------------------------------------------------------------
+ * Balanced 1-D OT (Algorithm 1): replaces src/ot1d.py:112-172
+ * `solve_ot_1d(a, b, cost)` for a batch of problems with sorted supports.
+ * fp64.  Costs: UOT_COST_POWER with exponent p, or UOT_COST_EXPLICIT with
+ * c [batch][n][m].  Outputs: f [batch][n], g [batch][m]; plan entries
+ * (ei, ej int32, em fp64) [batch][n+m-1] with count [batch]; entries are in
+ * sweep order.  status [batch] gets 1 for a mass mismatch above 1e-9
+ * relative (src/ot1d.py:133-136).
+ * ------------------------------------------------------------------------ */
+int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
+                     const double* a, const double* b, int32_t cost, double p, const double* c,
+                     double* f, double* g, int32_t* ei, int32_t* ej, double* em, int32_t* count,
+                     int32_t* status, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Batched 1-D Frank-Wolfe UOT at eps = 0: replaces src/fw.py:176-232
+ * `fw_solve(prob, FwConfig(step, max_iters, gap_tol))` (+ `_lmo` :159-173,
+ * `_h0` :106-115, `eval_primal` src/duality.py:320-344, line search
+ * :131-148, `_finalize` :235-252) for KL(rho1)/KL(rho2) marginals and
+ * |x-y|^p costs on sorted supports.  fp64.
+ *
+ * f, g [batch][n|m]: in = initial pair (must be dual feasible), out = the
+ * final iterate TRANSLATED by lambda* (report.final).  Traces
+ * [batch][max_iters] h0, fw_gap, pd_gap; iterations [batch]; the last
+ * oracle plan (ei, ej, em, count) as for uot_ot1d_batched; final primal /
+ * dual / lambda* in summary [batch][3]; status [batch] (1 = reweighted
+ * masses disagree, fw.py:161-166).  With early_exit != 0 a problem stops at
+ * the first pd_gap < gap_tol (fw.py:220-222).
+ * ------------------------------------------------------------------------ */
+typedef struct uot_fw_desc {
+  int32_t batch, n, m;
+  double p;
+  double rho1, rho2;
+  int32_t step;       /* UOT_STEP_* */
+  int32_t max_iters;
+  double gap_tol;
+  int32_t early_exit;
+  const double* x;
+  const double* y;
+  const double* a;
+  const double* b;
+  double* f;
+  double* g;
+  double* h0;
+  double* fw_gap;
+  double* pd_gap;
+  int32_t* iterations;
+  int32_t* ei;
+  int32_t* ej;
+  double* em;
+  int32_t* count;
+  double* summary;
+  int32_t* status;
+} uot_fw_desc;
+
+int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);
+int uot_fw1d_run(const uot_fw_desc* desc, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Dense feasibility check max(0, max_ij f_i + g_j - C_ij) for 1-D power
+ * costs: replaces src/duality.py:117-121 `dual_feasibility_violation`.
+ * out [batch] fp64. */
+int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
+                       double p, const double* f, const double* g, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Balanced K-marginal sweep (Algorithm 3) and the KL barycenter FW:
+ * replace src/barycenter.py:169-233 `solve_mot_1d(inputs, w)` and
+ * :330-430 `fw_barycenter(problem, config)` for a batch of problems with K
+ * sorted inputs of equal length n (fp64).  x, a, f [batch][K][n]; omega
+ * [K] barycentric weights.  Plans are returned as (tuple indices
+ * [batch][E][K] int32, mass [batch][E]) with E <= K*(n-1)+1.
+ * ------------------------------------------------------------------------ */
+typedef struct uot_bary_desc {
+  int32_t batch, k, n;
+  const double* omega;  /* host array [k] */
+  double rho;
+  int32_t step;
+  int32_t max_iters;
+  double gap_tol;
+  int32_t early_exit;
+  const double* x;
+  const double* a;
+  double* f;           /* in: initial potentials; out: translated final potentials */
+  double* h0;
+  double* fw_gap;
+  double* pd_gap;
+  int32_t* iterations;
+  int32_t* idx;        /* [batch][k*(n-1)+1][k] */
+  double* mass;        /* [batch][k*(n-1)+1] */
+  int32_t* count;
+  double* summary;     /* [batch][2]: primal, dual of the last iteration */
+  int32_t* status;
+} uot_bary_desc;
+
+int uot_mot1d_workspace_size(int32_t batch, int32_t k, int32_t n, size_t* bytes);
+int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const double* x, const double* a,
+                      const double* omega_host, double* f, int32_t* idx, double* mass,
+                      int32_t* count, int32_t* status, void* workspace, size_t workspace_bytes,
+                      void* stream);
+int uot_bary_workspace_size(const uot_bary_desc* desc, size_t* bytes);
+int uot_bary_run(const uot_bary_desc* desc, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* ------------------------------------------------------------------------
+ * NCCL plumbing for the row-sharded Sinkhorn (one process per GPU).  The
+ * unique id is 128 opaque bytes broadcast by the host (torch.distributed).
+ * ------------------------------------------------------------------------ */
+int uot_nccl_unique_id(char out[128]);
+int uot_nccl_comm_init(const char id[128], int32_t nranks, int32_t rank, void** comm);
+int uot_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UOT_B200_H */

@@ -1,0 +1,31 @@
+/*
+ * uot_b200_bench.h -- measurement hooks used by bench.py (not part of the
+ * reference-facing boundary in uot_b200.h).
+ */
+#ifndef UOT_B200_BENCH_H
+#define UOT_B200_BENCH_H
+
+#include <stddef.h>
+#include "uot_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Runs the descriptor once, then times `reps` launches of the g-direction and
+ * f-direction log-sum-exp kernels (CUDA events on `stream`): ms_out[0..1]. */
+int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* workspace, size_t workspace_bytes,
+                           void* stream, int reps, float* ms_out);
+
+/* MUFU ex2.approx.ftz.f32 throughput probe: independent ex2 chains on every
+ * SM; returns ex2 results per second (measured with CUDA events). */
+int uot_probe_mufu_ex2(void* stream, double* ex2_per_s);
+
+/* FP64 DFMA throughput probe (DFMA per second). */
+int uot_probe_dfma(void* stream, double* dfma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

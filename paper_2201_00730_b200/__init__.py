@@ -1,0 +1,31 @@
+"""B200-native (sm_100a) implementation of the hot paths of arXiv 2201.00730.
+
+Mirrors the reference package's public solver API (uotkit, src/__init__.py:10-70)
+for the paths in SURVEY.md §8: TI/F-Sinkhorn, the 1-D OT oracle, batched 1-D
+Frank-Wolfe, and the multimarginal barycenter.  All arithmetic runs in the
+CUDA kernels of ``csrc/`` through the C-ABI declared in ``include/uot_b200.h``;
+there is no CPU fallback.
+"""
+
+from .duality import DualPair, UotProblem, kl_scalars, lambda_star, translate
+from .entropies import KL, Balanced, Berg
+from .exceptions import (
+    InfeasibleDualError,
+    MassBalanceError,
+    NewtonError,
+    SubmodularityError,
+    UnsupportedEntropyError,
+    UotError,
+)
+from .measures import DiscreteMeasure, ExplicitMatrix, PowerDistance, SqEuclideanPoints
+from .sinkhorn import (
+    AndersonConfig,
+    SinkhornConfig,
+    SolverReport,
+    f_sinkhorn_step,
+    h_sinkhorn_step,
+    run,
+    sinkhorn_batched,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,892 @@
+// sinkhorn.cu -- F/H-Sinkhorn engine for sm_100a (see sinkhorn.cuh for the
+// structure).  Reference: src/sinkhorn.py:93-163, src/entropies.py:67-92,
+// :187-214, src/duality.py:175-178.
+#include <algorithm>
+#include <vector>
+
+#include "../../include/uot_b200.h"
+#include "sinkhorn.cuh"
+
+#if defined(UOT_WITH_NCCL)
+#include <nccl.h>
+#endif
+
+namespace uot {
+
+// ---------------------------------------------------------------------------
+// Exponent domains.  fp32 kernels work in log2 units so that each pair costs a
+// single MUFU.EX2; fp64 kernels use natural units (libdevice exp/log).
+
+template <typename T>
+struct Dom;
+
+template <>
+struct Dom<float> {
+  static constexpr double unit = LN2;  // natural = unit * domain
+  static __device__ __forceinline__ float ex(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  static __device__ __forceinline__ float lg(float x) { return __log2f(x); }
+  static __device__ __forceinline__ double exd(double x) { return exp2(x); }
+  static __device__ __forceinline__ double lgd(double x) { return log2(x); }
+  static constexpr float HI = 24.0f, LO = -48.0f, TINY = 3.5527136788005009e-15f;  // 2^-48
+};
+
+template <>
+struct Dom<double> {
+  static constexpr double unit = 1.0;
+  static __device__ __forceinline__ double ex(double x) { return exp(x); }
+  static __device__ __forceinline__ double lg(double x) { return log(x); }
+  static __device__ __forceinline__ double exd(double x) { return exp(x); }
+  static __device__ __forceinline__ double lgd(double x) { return log(x); }
+  static constexpr double HI = 64.0, LO = -256.0, TINY = 6.6e-112;  // ~e^-256
+};
+
+// ---------------------------------------------------------------------------
+// Cost policies.  Each defines the packed record of a reduced-side index
+// (written by the tail of the previous half-step), the per-output registers,
+// and arg(r, o) = (pot_r - C(r,o))/eps + log w_r in domain units, split as
+// arg_nov(rec, out) + bias(out) so the per-output bias folds into the shift.
+
+// fp32 squared Euclidean, expanded form |x|^2 + |y|^2 - 2 x.y (d = D).
+//   rec = [U, X_0..X_{D-1}, pad], U = (pot - |x|^2) L + log2 w, X = 2 L x
+//   out: y[D], bias = -|y|^2 L
+template <int D>
+struct SqE32 {
+  using T = float;
+  static constexpr int RW = (D + 1 + 3) / 4 * 4;
+  struct Out {
+    float y[D];
+    float bias;
+  };
+  static __device__ __forceinline__ void load(Out& o, const DirGeo<float>& g, int b, int idx) {
+    const float* p = g.out_pts + b * g.out_pts_bstride + (long)idx * D;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      o.y[k] = p[k];
+      s = fmaf(o.y[k], o.y[k], s);
+    }
+    o.bias = -s * g.L;
+  }
+  static __device__ __forceinline__ float arg(const float* rec, long, const Out& o,
+                                              const DirGeo<float>&, int) {
+    if constexpr (D == 2) {
+      const float4 r = *reinterpret_cast<const float4*>(rec);
+      return fmaf(r.z, o.y[1], fmaf(r.y, o.y[0], r.x));
+    } else {
+      float a = rec[0];
+#pragma unroll
+      for (int k = 0; k < D; ++k) a = fmaf(rec[1 + k], o.y[k], a);
+      return a;
+    }
+  }
+  static __device__ __forceinline__ void pack(float* rec, double hat, const float* pt, double w,
+                                              double L, double, int) {
+    double s = 0.0;
+    for (int k = 0; k < D; ++k) s += (double)pt[k] * (double)pt[k];
+    rec[0] = (float)((hat - s) * L + log2(w));
+    for (int k = 0; k < D; ++k) rec[1 + k] = (float)(2.0 * L * (double)pt[k]);
+    for (int k = D + 1; k < RW; ++k) rec[k] = 0.f;
+  }
+  static int rw(int) { return RW; }
+};
+
+// fp32 squared Euclidean with runtime d (SIMT fallback for d > 3; the d >= 32
+// tensor-core path replaces it for throughput).
+struct SqE32N {
+  using T = float;
+  struct Out {
+    const float* y;
+    float bias;
+  };
+  static __device__ __forceinline__ void load(Out& o, const DirGeo<float>& g, int b, int idx) {
+    o.y = g.out_pts + b * g.out_pts_bstride + (long)idx * g.d;
+    float s = 0.f;
+    for (int k = 0; k < g.d; ++k) s = fmaf(o.y[k], o.y[k], s);
+    o.bias = -s * g.L;
+  }
+  static __device__ __forceinline__ float arg(const float* rec, long, const Out& o,
+                                              const DirGeo<float>& g, int) {
+    float a = rec[0];
+    for (int k = 0; k < g.d; ++k) a = fmaf(rec[1 + k], __ldg(o.y + k), a);
+    return a;
+  }
+  static __device__ __forceinline__ void pack(float* rec, double hat, const float* pt, double w,
+                                              double L, double, int d) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += (double)pt[k] * (double)pt[k];
+    rec[0] = (float)((hat - s) * L + log2(w));
+    for (int k = 0; k < d; ++k) rec[1 + k] = (float)(2.0 * L * (double)pt[k]);
+  }
+  static int rw(int d) { return d + 1; }
+};
+
+// |x - y|^p on 1-D points (src/measures.py:228-234), any dtype.
+//   rec = [P, x], P = pot * L + log w ; arg = P - L * |x - y|^p
+template <typename TT>
+struct Pow1D {
+  using T = TT;
+  struct Out {
+    T y;
+    T bias;
+  };
+  static __device__ __forceinline__ void load(Out& o, const DirGeo<T>& g, int b, int idx) {
+    o.y = g.out_pts[b * g.out_pts_bstride + idx];
+    o.bias = T(0);
+  }
+  static __device__ __forceinline__ T cost(T x, T y, T p) {
+    T d = x - y;
+    if (p == T(2)) return d * d;
+    d = d < T(0) ? -d : d;
+    if (p == T(1)) return d;
+    return pow(d, p);
+  }
+  static __device__ __forceinline__ T arg(const T* rec, long, const Out& o, const DirGeo<T>& g,
+                                          int) {
+    return rec[0] - g.L * cost(rec[1], o.y, g.p);
+  }
+  static __device__ __forceinline__ void pack(T* rec, double hat, const T* pt, double w, double L,
+                                              double, int) {
+    rec[0] = (T)(hat * L + (Dom<T>::unit == 1.0 ? log(w) : log2(w)));
+    rec[1] = pt[0];
+  }
+  static int rw(int) { return 2; }
+};
+
+// fp64 squared Euclidean, direct form sum_k (x_k - y_k)^2 (runtime d): the
+// fp64 parity path for point clouds.  rec = [P, x_0..x_{d-1}].
+struct SqE64 {
+  using T = double;
+  struct Out {
+    const double* y;
+    double bias;
+  };
+  static __device__ __forceinline__ void load(Out& o, const DirGeo<double>& g, int b, int idx) {
+    o.y = g.out_pts + b * g.out_pts_bstride + (long)idx * g.d;
+    o.bias = 0.0;
+  }
+  static __device__ __forceinline__ double arg(const double* rec, long, const Out& o,
+                                               const DirGeo<double>& g, int) {
+    double c = 0.0;
+    for (int k = 0; k < g.d; ++k) {
+      double t = rec[1 + k] - __ldg(o.y + k);
+      c = fma(t, t, c);
+    }
+    return rec[0] - g.L * c;
+  }
+  static __device__ __forceinline__ void pack(double* rec, double hat, const double* pt, double w,
+                                              double L, double, int d) {
+    rec[0] = hat * L + log(w);
+    for (int k = 0; k < d; ++k) rec[1 + k] = pt[k];
+  }
+  static int rw(int d) { return d + 1; }
+};
+
+// Dense explicit cost (src/measures.py:108-122).  rec = [P].
+template <typename TT>
+struct Explicit {
+  using T = TT;
+  struct Out {
+    int o;
+    T bias;
+  };
+  static __device__ __forceinline__ void load(Out& o, const DirGeo<T>&, int, int idx) {
+    o.o = idx;
+    o.bias = T(0);
+  }
+  static __device__ __forceinline__ T arg(const T* rec, long r, const Out& o, const DirGeo<T>& g,
+                                          int b) {
+    return rec[0] - g.L * __ldg(g.cmat + b * g.cm_bstride + r * g.ld_r + (long)o.o * g.ld_o);
+  }
+  static __device__ __forceinline__ void pack(T* rec, double hat, const T*, double w, double L,
+                                              double, int) {
+    rec[0] = (T)(hat * L + (Dom<T>::unit == 1.0 ? log(w) : log2(w)));
+  }
+  static int rw(int) { return 1; }
+};
+
+template <class P>
+__device__ __forceinline__ void pack_rec(typename P::T* rec, double hat, const typename P::T* pt,
+                                         double w, double L, double p, int d) {
+  P::pack(rec, hat, pt, w, L, p, d);
+}
+
+// One register tile: RT reduced records x COLS outputs.  Exponents are
+// formed first, their max checked against the safe window of the current
+// shift (conditional rescale, rarely taken), then exponentiated and summed.
+template <class P, int COLS, int RT, bool CHECK>
+__device__ __forceinline__ void tile(const typename P::T* srec, int rw, int rr, int clen, long rbase,
+                                     const typename P::Out (&out)[COLS],
+                                     const DirGeo<typename P::T>& g, int b,
+                                     typename P::T (&cc)[COLS], typename P::T (&mm)[COLS],
+                                     typename P::T (&acc)[COLS]) {
+  using T = typename P::T;
+  using D = Dom<T>;
+  T t[RT][COLS];
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const bool ok = !CHECK || rr + i < clen;
+    const T* rc = srec + (ok ? (rr + i) : 0) * rw;
+#pragma unroll
+    for (int c = 0; c < COLS; ++c) {
+      const T v = P::arg(rc, rbase + rr + i, out[c], g, b) + cc[c];
+      t[i][c] = ok ? v : T(-INFINITY);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < COLS; ++c) {
+    T mx = t[0][c];
+#pragma unroll
+    for (int i = 1; i < RT; ++i) mx = fmax(mx, t[i][c]);
+    if (mx > D::HI || (mx < D::LO && acc[c] < D::TINY)) {
+      // Rare: the stale shift is off by more than the safe window.  Move the
+      // shift to the current maximum (FA-style conditional rescale).
+      T mn = mx;
+      if (acc[c] > T(0)) mn = fmax(mn, D::lg(acc[c]));
+      if (mn > T(-INFINITY) && mn < T(INFINITY)) {
+        if (acc[c] > T(0)) acc[c] *= D::ex(-mn);
+        mm[c] += mn;
+        cc[c] -= mn;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) t[i][c] -= mn;
+      }
+    }
+    T s = D::ex(t[0][c]);
+#pragma unroll
+    for (int i = 1; i < RT; ++i) s += D::ex(t[i][c]);
+    acc[c] += s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Main kernel: partial online log-sum-exp over a split of the reduced index.
+
+template <class P, int THREADS, int COLS, int RT>
+__global__ void __launch_bounds__(THREADS) sk_main(MainArgs<typename P::T> A) {
+  using T = typename P::T;
+  using D = Dom<T>;
+  const int b = blockIdx.z;
+  if (A.done != nullptr && A.done[b]) return;
+  const int split = blockIdx.y, S = gridDim.y;
+  const long r0 = (long)A.nred * split / S;
+  const long r1 = (long)A.nred * (split + 1) / S;
+  const int rw = A.g.rw;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* srec = reinterpret_cast<T*>(smem_raw);
+
+  typename P::Out out[COLS];
+  T cc[COLS], mm[COLS], acc[COLS];
+  const int obase = blockIdx.x * THREADS * COLS + threadIdx.x;
+#pragma unroll
+  for (int c = 0; c < COLS; ++c) {
+    const int o = obase + c * THREADS;
+    const bool ok = o < A.nout;
+    P::load(out[c], A.g, b, ok ? o : 0);
+    mm[c] = ok ? A.shift_in[(long)b * A.nout + o] : T(0);
+    cc[c] = out[c].bias - mm[c];
+    acc[c] = T(0);
+  }
+
+  const T* rec_g = A.g.red_rec + b * A.g.red_bstride;
+  for (long cs = r0; cs < r1; cs += A.chunk) {
+    const int clen = (int)min((long)A.chunk, r1 - cs);
+    {
+      const long base = (cs + A.red_offset) * rw;
+      const int nel = clen * rw;
+      for (int e = threadIdx.x; e < nel; e += THREADS) srec[e] = rec_g[base + e];
+    }
+    __syncthreads();
+    // Full tiles run without bounds checks; the ragged tail of the chunk
+    // takes the checked path.
+    const int full = clen / RT * RT;
+    for (int rr = 0; rr < full; rr += RT)
+      tile<P, COLS, RT, false>(srec, rw, rr, clen, cs + A.red_offset, out, A.g, b, cc, mm, acc);
+    if (full < clen)
+      tile<P, COLS, RT, true>(srec, rw, full, clen, cs + A.red_offset, out, A.g, b, cc, mm, acc);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < COLS; ++c) {
+    const int o = obase + c * THREADS;
+    if (o < A.nout) {
+      const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
+      A.part_m[idx] = mm[c];
+      A.part_a[idx] = acc[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tail kernel.
+
+constexpr int TAIL_THREADS = 256;
+
+template <class P>
+__global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> A) {
+  using T = typename P::T;
+  using D = Dom<T>;
+  const int b = blockIdx.y;
+  if (A.done != nullptr && A.done[b]) return;
+  __shared__ double s_m[32], s_s[32], s_x[32];
+  __shared__ int s_last;
+  const int o = blockIdx.x * TAIL_THREADS + threadIdx.x;
+  const bool ok = o < A.nout;
+  const SkScalars sc = A.sc[b];
+  const double tau_red = sc.tau[A.red_side];
+  const double smin_red = sc.shat[A.red_side] + tau_red;
+  const double tau_old = sc.tau[A.out_side];
+
+  LsePair pr{-CUDART_INF, 0.0};
+  double dmax = -CUDART_INF, dmin = CUDART_INF;
+  if (ok) {
+    double hat;
+    if (A.mode == 1) {
+      hat = (double)A.pot_in[(long)b * A.nout + o];
+    } else {
+      double M = -CUDART_INF;
+      const long pbase = (long)b * A.nparts * A.nout + o;
+      for (int s = 0; s < A.nparts; ++s) {
+        const double a = (double)A.part_a[pbase + (long)s * A.nout];
+        if (a > 0.0) M = fmax(M, (double)A.part_m[pbase + (long)s * A.nout]);
+      }
+      double acc = 0.0;
+      for (int s = 0; s < A.nparts; ++s) {
+        const double a = (double)A.part_a[pbase + (long)s * A.nout];
+        if (a > 0.0) acc += a * D::exd((double)A.part_m[pbase + (long)s * A.nout] - M);
+      }
+      const double lse = M + D::lgd(acc);  // domain units, excluding tau_red
+      A.shift_out[(long)b * A.nout + o] = (T)lse;
+      const double smin = -A.eps * A.unit * (lse + tau_red * A.inv_eu);
+      hat = A.a_coef * smin - A.k_coef * smin_red;
+    }
+    const T hat_t = (T)hat;
+    hat = (double)hat_t;
+    A.hat_out[(long)b * A.nout + o] = hat_t;
+    const double w = (double)A.out_w[(long)b * A.nout + o];
+    pack_rec<P>(A.rec_out + ((long)b * A.nout + o) * A.rw, hat,
+                A.out_pts + ((long)b * A.nout + o) * A.d, w, (double)A.L, (double)A.p, A.d);
+    if (w > 0.0) pr = LsePair{-hat / A.rho_out, w};
+    if (A.hat_old != nullptr) {
+      const double dl = hat - ((double)A.hat_old[(long)b * A.nout + o] + tau_old);
+      dmax = dl;
+      dmin = dl;
+    }
+  }
+  // Block partials: log-sum-exp of -hat/rho weighted by w, and delta bounds.
+  pr = block_lse(pr, s_m, s_s);
+  dmax = block_reduce(dmax, s_x, MaxOp(), -CUDART_INF);
+  dmin = block_reduce(dmin, s_x, MinOp(), CUDART_INF);
+  double* blk = A.blk + (long)b * gridDim.x * 4;
+  if (threadIdx.x == 0) {
+    blk[blockIdx.x * 4 + 0] = pr.m;
+    blk[blockIdx.x * 4 + 1] = pr.s;
+    blk[blockIdx.x * 4 + 2] = dmax;
+    blk[blockIdx.x * 4 + 3] = dmin;
+  }
+  if (!last_block_arrive(A.counter + b, gridDim.x, &s_last)) return;
+  // Last block: fold the per-block partials (fixed order -> deterministic).
+  LsePair q{-CUDART_INF, 0.0};
+  double qmax = -CUDART_INF, qmin = CUDART_INF;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += TAIL_THREADS) {
+    q = lse_merge(q, LsePair{blk[k * 4 + 0], blk[k * 4 + 1]});
+    qmax = fmax(qmax, blk[k * 4 + 2]);
+    qmin = fmin(qmin, blk[k * 4 + 3]);
+  }
+  q = block_lse(q, s_m, s_s);
+  qmax = block_reduce(qmax, s_x, MaxOp(), -CUDART_INF);
+  qmin = block_reduce(qmin, s_x, MinOp(), CUDART_INF);
+  if (threadIdx.x == 0) {
+    const double shat = -A.rho_out * (q.m + log(q.s));
+    const double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
+    A.sc[b].shat[A.out_side] = shat;
+    A.sc[b].tau[A.out_side] = tau;
+    if (A.hat_old != nullptr && A.trace != nullptr) {
+      const double delta = fmax(qmax + tau, -(qmin + tau));
+      A.trace[(long)b * A.trace_len + A.t] = delta;
+      A.iters_done[b] = A.t + 1;
+      if (A.use_tol && delta < A.tol) A.done[b] = 1;
+    }
+    A.counter[b] = 0u;
+  }
+}
+
+// Final pair: f = hat_f + tau_f, g = hat_g + tau_g (src/sinkhorn.py returns
+// the plain potentials, :163).
+template <typename T>
+__global__ void sk_finalize(int n, int m, const T* hatA0, const T* hatA1, const T* hatB,
+                            const SkScalars* sc, const int* iters_done, T* f, T* g) {
+  const int b = blockIdx.y;
+  const T* hatA = (iters_done[b] & 1) ? hatA1 : hatA0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max(n, m); i += gridDim.x * blockDim.x) {
+    if (i < n) f[(long)b * n + i] = (T)((double)hatA[(long)b * n + i] + sc[b].tau[0]);
+    if (i < m) g[(long)b * m + i] = (T)((double)hatB[(long)b * m + i] + sc[b].tau[1]);
+  }
+}
+
+__global__ void sk_reset(int batch, SkScalars* sc, unsigned int* counters, int* done,
+                         int* iters_done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) {
+    sc[b] = SkScalars{{0.0, 0.0}, {0.0, 0.0}};
+    counters[b] = 0u;
+    done[b] = 0;
+    iters_done[b] = 0;
+  }
+}
+
+template <typename T>
+__global__ void sk_zero(long n, T* p) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    p[i] = T(0);
+}
+
+// ---------------------------------------------------------------------------
+// Host engine.
+
+namespace {
+
+struct WsLayout {
+  size_t off[16];
+  size_t total;
+};
+
+template <typename T>
+struct Buffers {
+  T* recA;
+  T* recB;
+  T* hatA0;
+  T* hatA1;
+  T* hatB;
+  T* shiftA;
+  T* shiftB;
+  T* part_m;
+  T* part_a;
+  T* zeros;  // [B][max(n,m)] initial potential when none is given
+  SkScalars* sc;
+  double* blk;
+  unsigned int* counter;
+  int* done;
+  int* iters_done;
+  double* trace;  // scratch trace when the caller passes none
+};
+
+struct Shape {
+  int B, n, m, d, rwA, rwB, S, nblk;
+  int total_n;  // all shards (emulation)
+};
+
+template <typename T>
+size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* base) {
+  size_t sizes[16];
+  const long nm = std::max(s.total_n, s.m);
+  sizes[0] = sizeof(T) * (size_t)s.B * s.total_n * s.rwA;
+  sizes[1] = sizeof(T) * (size_t)s.B * s.m * s.rwB;
+  sizes[2] = sizeof(T) * (size_t)s.B * s.total_n;
+  sizes[3] = sizes[2];
+  sizes[4] = sizeof(T) * (size_t)s.B * s.m;
+  sizes[5] = sizes[2];
+  sizes[6] = sizes[4];
+  sizes[7] = sizeof(T) * (size_t)s.B * s.S * nm;
+  sizes[8] = sizes[7];
+  sizes[9] = sizeof(T) * (size_t)s.B * nm;
+  sizes[10] = sizeof(SkScalars) * (size_t)s.B;
+  sizes[11] = sizeof(double) * 4 * (size_t)s.B * s.nblk;
+  sizes[12] = sizeof(unsigned int) * (size_t)s.B;
+  sizes[13] = sizeof(int) * (size_t)s.B;
+  sizes[14] = sizeof(int) * (size_t)s.B;
+  sizes[15] = sizeof(double) * (size_t)s.B * std::max(iters, 1);
+  size_t off = 0;
+  for (int k = 0; k < 16; ++k) {
+    L.off[k] = off;
+    off += (sizes[k] + 255) / 256 * 256;
+  }
+  L.total = off;
+  if (buf != nullptr) {
+    buf->recA = (T*)(base + L.off[0]);
+    buf->recB = (T*)(base + L.off[1]);
+    buf->hatA0 = (T*)(base + L.off[2]);
+    buf->hatA1 = (T*)(base + L.off[3]);
+    buf->hatB = (T*)(base + L.off[4]);
+    buf->shiftA = (T*)(base + L.off[5]);
+    buf->shiftB = (T*)(base + L.off[6]);
+    buf->part_m = (T*)(base + L.off[7]);
+    buf->part_a = (T*)(base + L.off[8]);
+    buf->zeros = (T*)(base + L.off[9]);
+    buf->sc = (SkScalars*)(base + L.off[10]);
+    buf->blk = (double*)(base + L.off[11]);
+    buf->counter = (unsigned int*)(base + L.off[12]);
+    buf->done = (int*)(base + L.off[13]);
+    buf->iters_done = (int*)(base + L.off[14]);
+    buf->trace = (double*)(base + L.off[15]);
+  }
+  return L.total;
+}
+
+template <class P>
+struct Cfg;
+template <int D>
+struct Cfg<SqE32<D>> {
+  static constexpr int THREADS = 128, COLS = 4, RT = 8;
+};
+template <>
+struct Cfg<SqE32N> {
+  static constexpr int THREADS = 128, COLS = 2, RT = 4;
+};
+template <>
+struct Cfg<Pow1D<float>> {
+  static constexpr int THREADS = 128, COLS = 4, RT = 8;
+};
+template <>
+struct Cfg<Pow1D<double>> {
+  static constexpr int THREADS = 128, COLS = 2, RT = 4;
+};
+template <>
+struct Cfg<SqE64> {
+  static constexpr int THREADS = 128, COLS = 2, RT = 4;
+};
+template <typename TT>
+struct Cfg<Explicit<TT>> {
+  static constexpr int THREADS = 128, COLS = 2, RT = 4;
+};
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Splits of the reduced index so the main grid fills the chip several times
+// over (grid = out_blocks x splits x batch) while keeping >= 16 reduced
+// indices per split.
+int choose_splits(int B, long nout, long nred, int out_per_block) {
+  const long out_blocks = (nout + out_per_block - 1) / out_per_block;
+  const long target = (long)num_sms() * 24;
+  long s = (target + out_blocks * B - 1) / (out_blocks * B);
+  s = std::min(s, std::max(1L, nred / 16));
+  s = std::min(s, 4096L);
+  return (int)std::max(1L, s);
+}
+
+template <class P>
+struct Engine {
+  using T = typename P::T;
+  using C = Cfg<P>;
+  static constexpr int OUT_PER_BLOCK = C::THREADS * C::COLS;
+
+  static int chunk_for(int rw) {
+    int ch = (int)(32768 / (rw * sizeof(T)));
+    ch = std::max(16, std::min(1024, ch));
+    return ch / 8 * 8;
+  }
+
+  static Shape shape(const uot_sinkhorn_desc& d) {
+    Shape s;
+    s.B = d.batch;
+    s.n = d.n;
+    s.m = d.m;
+    s.d = d.d;
+    s.rwA = P::rw(d.d);
+    s.rwB = P::rw(d.d);
+    s.total_n = d.n;
+    const int sA = choose_splits(d.batch, d.m, d.n, OUT_PER_BLOCK);
+    const int sB = choose_splits(d.batch, d.n, d.m, OUT_PER_BLOCK);
+    s.S = std::max(sA, sB);
+    if (d.nranks > 1 && d.nccl_comm == nullptr) s.S = std::max(s.S, d.nranks);
+    s.nblk = (int)ceil_div(std::max(d.n, d.m), TAIL_THREADS);
+    return s;
+  }
+
+  static size_t ws_size(const uot_sinkhorn_desc& d) {
+    WsLayout L;
+    Shape s = shape(d);
+    return layout<T>(s, d.iters, L, nullptr, nullptr);
+  }
+
+  static int launch_main(const uot_sinkhorn_desc& d, const Buffers<T>& bf, cudaStream_t st,
+                         bool to_target, int splits, int red_offset, int nred, int split_base,
+                         int splits_total) {
+    MainArgs<T> a{};
+    const double L = 1.0 / (d.eps * Dom<T>::unit);
+    a.g.rw = P::rw(d.d);
+    a.g.d = d.d;
+    a.g.L = (T)L;
+    a.g.p = (T)d.p;
+    if (to_target) {  // g-update: reduce over the source side, outputs = targets
+      a.g.red_rec = bf.recA;
+      a.g.red_bstride = (long)d.n * a.g.rw;
+      a.g.out_pts = (const T*)d.y;
+      a.g.out_pts_bstride = (long)d.m * d.d;
+      a.g.cmat = (const T*)d.c;
+      a.g.cm_bstride = (long)d.n * d.m;
+      a.g.ld_r = d.m;
+      a.g.ld_o = 1;
+      a.nout = d.m;
+      a.shift_in = bf.shiftB;
+    } else {  // f-update: reduce over the target side, outputs = sources
+      a.g.red_rec = bf.recB;
+      a.g.red_bstride = (long)d.m * a.g.rw;
+      a.g.out_pts = (const T*)d.x;
+      a.g.out_pts_bstride = (long)d.n * d.d;
+      a.g.cmat = (const T*)d.ct;
+      a.g.cm_bstride = (long)d.n * d.m;
+      a.g.ld_r = d.n;
+      a.g.ld_o = 1;
+      a.nout = d.n;
+      a.shift_in = bf.shiftA;
+    }
+    a.nred = nred;
+    a.red_offset = red_offset;
+    a.part_m = bf.part_m;
+    a.part_a = bf.part_a;
+    a.done = bf.done;
+    a.chunk = chunk_for(a.g.rw);
+    a.split_base = split_base;
+    a.splits_total = splits_total;
+    dim3 grid(ceil_div(a.nout, OUT_PER_BLOCK), splits, d.batch);
+    const size_t smem = (size_t)a.chunk * a.g.rw * sizeof(T);
+    sk_main<P, C::THREADS, C::COLS, C::RT><<<grid, C::THREADS, smem, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  }
+
+  static int launch_tail(const uot_sinkhorn_desc& d, const Buffers<T>& bf, cudaStream_t st,
+                         bool to_target, int mode, int nparts, const T* hat_old, T* hat_out,
+                         const T* pot_in, int t, double* trace, int trace_len) {
+    TailArgs<T> a{};
+    const bool H = d.variant == UOT_SINKHORN_H;
+    const double eps = d.eps, r1 = d.rho1, r2 = d.rho2;
+    const double ro = to_target ? r2 : r1;        // own marginal strength
+    const double rother = to_target ? r1 : r2;    // the other marginal
+    a.nout = to_target ? d.m : d.n;
+    a.nparts = nparts;
+    a.mode = mode;
+    a.out_side = to_target ? 1 : 0;
+    a.red_side = to_target ? 0 : 1;
+    a.part_m = bf.part_m;
+    a.part_a = bf.part_a;
+    a.pot_in = pot_in;
+    a.sc = bf.sc;
+    a.eps = eps;
+    a.unit = Dom<T>::unit;
+    a.inv_eu = 1.0 / (eps * Dom<T>::unit);
+    // src/sinkhorn.py:154-162: hat = rho/(rho+eps) smin - (eps/(eps+rho)) (rho/(r1+r2)) Smin_other
+    a.a_coef = ro / (ro + eps);
+    a.k_coef = H ? (eps / (eps + ro)) * (ro / (r1 + r2)) : 0.0;
+    const double kk = (eps / (eps + ro)) * (rother / (r1 + r2));
+    a.tau_fac = H ? kk / (1.0 - kk) : 0.0;
+    a.rho_out = ro;
+    a.hat_out = hat_out;
+    a.hat_old = hat_old;
+    a.shift_out = to_target ? bf.shiftB : bf.shiftA;
+    a.rec_out = to_target ? bf.recB : bf.recA;
+    a.rw = P::rw(d.d);
+    a.out_pts = (const T*)(to_target ? d.y : d.x);
+    a.d = d.d;
+    a.out_w = (const T*)(to_target ? d.b : d.a);
+    a.L = (T)(1.0 / (eps * Dom<T>::unit));
+    a.p = (T)d.p;
+    a.blk = bf.blk;
+    a.counter = bf.counter;
+    a.trace = trace;
+    a.trace_len = trace_len;
+    a.t = t;
+    a.iters_done = bf.iters_done;
+    a.done = bf.done;
+    a.tol = d.tol;
+    a.use_tol = d.use_tol;
+    dim3 grid(ceil_div(a.nout, TAIL_THREADS), d.batch);
+    sk_tail<P><<<grid, TAIL_THREADS, 0, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  }
+
+  static int run(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_t st) {
+    Shape s = shape(d);
+    WsLayout L;
+    Buffers<T> bf;
+    const size_t need = layout<T>(s, d.iters, L, &bf, (char*)ws);
+    if (ws_bytes < need) {
+      set_error("sinkhorn workspace too small: %zu < %zu", ws_bytes, need);
+      return UOT_INVALID;
+    }
+    if (d.nranks > 1) {
+      set_error("row-sharded sinkhorn is not available in this build");
+      return UOT_INVALID;
+    }
+    sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
+                                                      bf.iters_done);
+    UOT_CHECK_LAUNCH();
+    const long nm = std::max(d.n, d.m);
+    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
+    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.m, bf.shiftB);
+    UOT_CHECK_LAUNCH();
+    const T* f0 = (const T*)d.f;
+    if (!d.init_given) {
+      sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * nm, bf.zeros);
+      UOT_CHECK_LAUNCH();
+      f0 = bf.zeros;
+    }
+    double* trace = d.trace_delta != nullptr ? d.trace_delta : bf.trace;
+    const int trace_len = std::max(d.iters, 1);
+    // init: hat_f = f0, Smin_a(f0), pack source records.
+    UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, f0, 0, nullptr, trace_len));
+    const int sB = choose_splits(d.batch, d.m, d.n, OUT_PER_BLOCK);  // g-update splits
+    const int sA = choose_splits(d.batch, d.n, d.m, OUT_PER_BLOCK);  // f-update splits
+    for (int t = 0; t < d.iters; ++t) {
+      T* hat_old = (t & 1) ? bf.hatA1 : bf.hatA0;
+      T* hat_new = (t & 1) ? bf.hatA0 : bf.hatA1;
+      UOT_TRY(launch_main(d, bf, st, true, sB, 0, d.n, 0, sB));
+      UOT_TRY(launch_tail(d, bf, st, true, 0, sB, nullptr, bf.hatB, nullptr, t, nullptr,
+                          trace_len));
+      UOT_TRY(launch_main(d, bf, st, false, sA, 0, d.m, 0, sA));
+      UOT_TRY(launch_tail(d, bf, st, false, 0, sA, hat_old, hat_new, nullptr, t, trace,
+                          trace_len));
+    }
+    sk_finalize<T><<<dim3(ceil_div(nm, 256), d.batch), 256, 0, st>>>(
+        d.n, d.m, bf.hatA0, bf.hatA1, bf.hatB, bf.sc, bf.iters_done, (T*)d.f, (T*)d.g);
+    UOT_CHECK_LAUNCH();
+    if (d.iterations != nullptr) {
+      UOT_CUDA_TRY(cudaMemcpyAsync(d.iterations, bf.iters_done, sizeof(int) * d.batch,
+                                   cudaMemcpyDeviceToDevice, st));
+    }
+    return UOT_OK;
+  }
+};
+
+// Bench hook: after a normal run (which leaves the workspace holding a valid
+// state), time `reps` launches of each direction's main kernel with CUDA
+// events on the caller's stream; returns the mean per-launch milliseconds of
+// the g-direction and f-direction kernels.
+template <class E>
+int time_main(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_t st, int reps,
+              float* ms) {
+  using T = typename E::T;
+  UOT_TRY(E::run(d, ws, ws_bytes, st));
+  Shape s = E::shape(d);
+  WsLayout L;
+  Buffers<T> bf;
+  layout<T>(s, d.iters, L, &bf, (char*)ws);
+  const int sB = choose_splits(d.batch, d.m, d.n, E::OUT_PER_BLOCK);
+  const int sA = choose_splits(d.batch, d.n, d.m, E::OUT_PER_BLOCK);
+  cudaEvent_t e0, e1;
+  UOT_CUDA_TRY(cudaEventCreate(&e0));
+  UOT_CUDA_TRY(cudaEventCreate(&e1));
+  for (int dir = 0; dir < 2; ++dir) {
+    UOT_TRY(E::launch_main(d, bf, st, dir == 0, dir == 0 ? sB : sA, 0, dir == 0 ? d.n : d.m, 0,
+                           dir == 0 ? sB : sA));
+    UOT_CUDA_TRY(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r)
+      UOT_TRY(E::launch_main(d, bf, st, dir == 0, dir == 0 ? sB : sA, 0, dir == 0 ? d.n : d.m, 0,
+                             dir == 0 ? sB : sA));
+    UOT_CUDA_TRY(cudaEventRecord(e1, st));
+    UOT_CUDA_TRY(cudaEventSynchronize(e1));
+    float t = 0.f;
+    UOT_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+    ms[dir] = t / (float)reps;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return UOT_OK;
+}
+
+template <class Fn>
+int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
+  if (d.dtype == UOT_F32) {
+    switch (d.cost) {
+      case UOT_COST_SQEUCLID:
+        if (d.d == 1) return fn(Engine<SqE32<1>>());
+        if (d.d == 2) return fn(Engine<SqE32<2>>());
+        if (d.d == 3) return fn(Engine<SqE32<3>>());
+        return fn(Engine<SqE32N>());
+      case UOT_COST_POWER:
+        return fn(Engine<Pow1D<float>>());
+      case UOT_COST_EXPLICIT:
+        return fn(Engine<Explicit<float>>());
+    }
+  } else if (d.dtype == UOT_F64) {
+    switch (d.cost) {
+      case UOT_COST_SQEUCLID:
+        return fn(Engine<SqE64>());
+      case UOT_COST_POWER:
+        return fn(Engine<Pow1D<double>>());
+      case UOT_COST_EXPLICIT:
+        return fn(Engine<Explicit<double>>());
+    }
+  }
+  set_error("unsupported sinkhorn dtype/cost combination (%d, %d)", d.dtype, d.cost);
+  return UOT_INVALID;
+}
+
+int validate(const uot_sinkhorn_desc* d) {
+  if (d == nullptr) {
+    set_error("null descriptor");
+    return UOT_INVALID;
+  }
+  if (d->batch < 1 || d->n < 1 || d->m < 1 || d->d < 1 || d->iters < 1) {
+    set_error("invalid sizes (batch=%d n=%d m=%d d=%d iters=%d)", d->batch, d->n, d->m, d->d,
+              d->iters);
+    return UOT_INVALID;
+  }
+  if (!(d->eps > 0.0) || !std::isfinite(d->eps)) {
+    set_error("sinkhorn iterations need eps > 0");  // src/sinkhorn.py:192-194
+    return UOT_INVALID;
+  }
+  if (!(d->rho1 > 0.0) || !(d->rho2 > 0.0) || !std::isfinite(d->rho1) || !std::isfinite(d->rho2)) {
+    set_error("rho must be positive and finite");  // src/entropies.py:46-48
+    return UOT_INVALID;
+  }
+  if (d->variant != UOT_SINKHORN_F && d->variant != UOT_SINKHORN_H) {
+    set_error("variant must be F (0) or H (1)");
+    return UOT_INVALID;
+  }
+  if (d->cost == UOT_COST_POWER && (d->d != 1 || !(d->p >= 1.0))) {
+    set_error("power cost needs d == 1 and p >= 1");  // src/measures.py:200-202
+    return UOT_INVALID;
+  }
+  if (d->cost == UOT_COST_EXPLICIT && (d->c == nullptr || d->ct == nullptr)) {
+    set_error("explicit cost needs c and its transpose ct");
+    return UOT_INVALID;
+  }
+  return UOT_OK;
+}
+
+}  // namespace
+
+}  // namespace uot
+
+extern "C" int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes) {
+  using namespace uot;
+  UOT_TRY(validate(desc));
+  return dispatch(*desc, [&](auto eng) {
+    *bytes = decltype(eng)::ws_size(*desc);
+    return (int)UOT_OK;
+  });
+}
+
+extern "C" int uot_sinkhorn_run(const uot_sinkhorn_desc* desc, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  using namespace uot;
+  UOT_TRY(validate(desc));
+  return dispatch(*desc, [&](auto eng) {
+    return decltype(eng)::run(*desc, workspace, workspace_bytes, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* workspace,
+                                      size_t workspace_bytes, void* stream, int reps,
+                                      float* ms_out) {
+  using namespace uot;
+  UOT_TRY(validate(desc));
+  return dispatch(*desc, [&](auto eng) {
+    return time_main<decltype(eng)>(*desc, workspace, workspace_bytes, (cudaStream_t)stream,
+                                    reps, ms_out);
+  });
+}

@@ -1,0 +1,101 @@
+"""Dual-pair / problem value types and the closed-form KL translation
+(src/duality.py:42-91, :160-178, :250-253, :279-303).  The reductions run in
+the ``uot_kl_scalars`` kernel."""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .entropies import KL, Berg, require_kl
+from .exceptions import UnsupportedEntropyError
+from .measures import DiscreteMeasure
+
+
+@dataclass(frozen=True)
+class DualPair:
+    """Potentials (f, g) attached to the two marginals; read-only fp64."""
+
+    f: np.ndarray
+    g: np.ndarray
+
+    def __post_init__(self):
+        f = np.array(self.f, dtype=np.float64, copy=True)
+        g = np.array(self.g, dtype=np.float64, copy=True)
+        if f.ndim != 1 or g.ndim != 1:
+            raise ValueError("potentials must be vectors")
+        if not (np.isfinite(f).all() and np.isfinite(g).all()):
+            raise ValueError("potentials must be finite")
+        f.flags.writeable = False
+        g.flags.writeable = False
+        object.__setattr__(self, "f", f)
+        object.__setattr__(self, "g", g)
+
+    @staticmethod
+    def zeros(n, m):
+        return DualPair(np.zeros(n), np.zeros(m))
+
+
+@dataclass(frozen=True)
+class UotProblem:
+    """One unbalanced transport instance (alpha, beta, cost, ent1, ent2, eps)."""
+
+    alpha: DiscreteMeasure
+    beta: DiscreteMeasure
+    cost: object
+    ent1: object
+    ent2: object
+    eps: float = 0.0
+
+    def __post_init__(self):
+        if not (math.isfinite(self.eps) and self.eps >= 0):
+            raise ValueError("eps must be nonnegative and finite")
+
+    def check_pair(self, d):
+        if d.f.size != len(self.alpha) or d.g.size != len(self.beta):
+            raise ValueError("potential lengths do not match the marginals")
+
+
+def kl_scalars(a, b, f, g, rho1, rho2):
+    """Batched (lambda*, H_0, Smin_a^{rho1}(f)) on device tensors [B, N]/[B, M]."""
+    t = D.torch()
+    lib = _lib.load()
+    a, b, f, g = (D.to_dev(v, t.float64) for v in (a, b, f, g))
+    if a.ndim == 1:
+        a, b, f, g = (v.unsqueeze(0) for v in (a, b, f, g))
+    out = D.empty((a.shape[0], 3), t.float64)
+    st = lib.uot_kl_scalars(a.shape[0], a.shape[1], b.shape[1], _lib.ptr(a), _lib.ptr(b),
+                            _lib.ptr(f), _lib.ptr(g), ctypes.c_double(rho1),
+                            ctypes.c_double(rho2), _lib.ptr(out), _lib.stream_handle())
+    _lib.check(st, "uot_kl_scalars")
+    return out
+
+
+def _strictly_convex(spec):
+    return isinstance(spec, (KL, Berg))
+
+
+def lambda_star(prob, d, tol=1e-11, max_iters=100, initial=0.0):
+    """Optimal translation t* maximising G(f + t, g - t) (src/duality.py:160-179).
+
+    KL/KL has the closed form rho1 rho2/(rho1+rho2) (LSE_a(-f/rho1) -
+    LSE_b(-g/rho2)), evaluated on the GPU.  Balanced is rejected like the
+    reference; Berg (Newton branch, :182-247) is not on the B200 path."""
+    prob.check_pair(d)
+    if not (_strictly_convex(prob.ent1) and _strictly_convex(prob.ent2)):
+        raise UnsupportedEntropyError(
+            "optimal translation needs strictly convex conjugates (KL or Berg)")
+    require_kl(prob.ent1, prob.ent2, what="lambda_star")
+    out = kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.ent1.rho, prob.ent2.rho)
+    return float(out[0, 0].item())
+
+
+def translate(prob, d):
+    """(f + t*, g - t*) (src/duality.py:250-253)."""
+    lam = lambda_star(prob, d)
+    return DualPair(d.f + lam, d.g - lam)

@@ -1,0 +1,236 @@
+"""F- and H-Sinkhorn on the B200 (mirror of src/sinkhorn.py:59-163, :246-315).
+
+``run(prob, config, init, reference)`` keeps the reference signature and
+report; the iterations execute in the fused sm_100a kernels of
+``csrc/sinkhorn.cu`` through ``uot_sinkhorn_run``.  ``sinkhorn_batched`` is
+the new batched / point-cloud entry point (BASELINE configs 3 and 4).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .duality import DualPair, UotProblem, kl_scalars
+from .entropies import KL, require_kl
+from .exceptions import UnsupportedEntropyError
+from .measures import ExplicitMatrix, PowerDistance, SqEuclideanPoints, check_submodular  # noqa: F401
+
+
+@dataclass(frozen=True)
+class AndersonConfig:
+    """Anderson window (src/sinkhorn.py:45-56); accepted, not on the B200 path."""
+
+    depth: int = 4
+    reg: float = 1e-7
+
+    def __post_init__(self):
+        if self.depth < 1:
+            raise ValueError("depth must be at least 1")
+        if self.reg < 0:
+            raise ValueError("regularization must be nonnegative")
+
+
+@dataclass(frozen=True)
+class SinkhornConfig:
+    """variant in {"f", "g", "h"}, iteration budget, delta_f tolerance.
+
+    ``precision`` is new: "fp64" (default, the reference's arithmetic) or
+    "fp32" (log2-domain MUFU kernels; tolerance 1e-4 * eps on potentials)."""
+
+    variant: str = "f"
+    max_iters: int = 100_000
+    tol: float = 1e-9
+    anderson: AndersonConfig | None = None
+    precision: str = "fp64"
+
+    def __post_init__(self):
+        if self.variant not in ("f", "g", "h"):
+            raise ValueError("variant must be one of 'f', 'g', 'h'")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be positive")
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+
+
+@dataclass
+class SolverReport:
+    """Outcome of an iterative run plus its per-iteration trace."""
+
+    final: DualPair
+    iterations: int
+    converged: bool
+    trace: dict = field(default_factory=dict)
+    certificate: object = None
+    plan: object = None
+
+
+def _geometry(prob):
+    """(cost kind, d, p, x, y, C) of a problem for the kernels."""
+    cost = prob.cost
+    if isinstance(cost, PowerDistance):
+        return _lib.COST_POWER, 1, float(cost.p), prob.alpha.points, prob.beta.points, None
+    if isinstance(cost, ExplicitMatrix):
+        if cost.matrix.shape != (len(prob.alpha), len(prob.beta)):
+            raise ValueError(f"explicit cost shape {cost.matrix.shape} does not match supports "
+                             f"({len(prob.alpha)}, {len(prob.beta)})")
+        return (_lib.COST_EXPLICIT, 1, 2.0, prob.alpha.points, prob.beta.points, cost.matrix)
+    if isinstance(cost, SqEuclideanPoints):
+        if cost.X.shape[0] != len(prob.alpha) or cost.Y.shape[0] != len(prob.beta):
+            raise ValueError("point clouds do not match the measures")
+        return _lib.COST_SQEUCLID, cost.d, 2.0, cost.X, cost.Y, None
+    raise TypeError(f"unknown cost specification {cost!r}")
+
+
+def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
+                     c=None, f0=None, tol=None, precision="fp32", stream=None):
+    """Batched Sinkhorn on device.
+
+    x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
+    b [B, M]; ``cost`` in {"sqeuclid", "power", "explicit"} (explicit needs
+    c [B, N, M]).  Returns (f [B, N], g [B, M], delta [B, iters] fp64,
+    iterations [B] int32) as device tensors; f and g are in ``precision``.
+    """
+    t = D.torch()
+    lib = _lib.load()
+    dt = t.float32 if precision == "fp32" else t.float64
+    kind = {"sqeuclid": _lib.COST_SQEUCLID, "power": _lib.COST_POWER,
+            "explicit": _lib.COST_EXPLICIT}[cost]
+    a = D.to_dev(a, dt)
+    b = D.to_dev(b, dt)
+    if a.ndim == 1:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    B, n = a.shape
+    m = b.shape[1]
+    x = D.to_dev(x, dt).reshape(B, n, -1)
+    y = D.to_dev(y, dt).reshape(B, m, -1)
+    d = x.shape[2]
+    cm = ct = None
+    if kind == _lib.COST_EXPLICIT:
+        cm = D.to_dev(c, dt).reshape(B, n, m)
+        ct = cm.transpose(1, 2).contiguous()
+    f = D.empty((B, n), dt)
+    g = D.empty((B, m), dt)
+    if f0 is not None:
+        f.copy_(D.to_dev(f0, dt).reshape(B, n))
+    trace = D.empty((B, iters), t.float64)
+    its = D.empty((B,), t.int32)
+    desc = _lib.SinkhornDesc(
+        variant=_lib.SINKHORN_H if variant == "h" else _lib.SINKHORN_F,
+        dtype=_lib.F32 if dt == t.float32 else _lib.F64, cost=kind, batch=B, n=n, m=m,
+        d=1 if kind != _lib.COST_SQEUCLID else d, p=float(p), eps=float(eps),
+        rho1=float(rho1), rho2=float(rho2), x=_lib.ptr(x), y=_lib.ptr(y), c=_lib.ptr(cm),
+        ct=_lib.ptr(ct), a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(f), g=_lib.ptr(g),
+        init_given=1 if f0 is not None else 0, iters=int(iters),
+        tol=float(tol) if tol is not None else 0.0, use_tol=1 if tol is not None else 0,
+        trace_delta=_lib.ptr(trace), iterations=_lib.ptr(its), nccl_comm=None, nranks=1, rank=0,
+        shard_rows=None)
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)),
+               "sinkhorn workspace")
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_sinkhorn_run(ctypes.byref(desc), _lib.ptr(ws), ctypes.c_size_t(size.value),
+                                    _lib.stream_handle(stream)), "uot_sinkhorn_run")
+    return f, g, trace, its
+
+
+def _require_positive_eps(prob):
+    if prob.eps <= 0:
+        raise ValueError("sinkhorn iterations need eps > 0")
+
+
+def _step_inputs(prob):
+    kind, d, p, x, y, C = _geometry(prob)
+    costname = {_lib.COST_POWER: "power", _lib.COST_EXPLICIT: "explicit",
+                _lib.COST_SQEUCLID: "sqeuclid"}[kind]
+    return costname, p, x, y, C
+
+
+def _one_step(prob, d, variant):
+    _require_positive_eps(prob)
+    prob.check_pair(d)
+    require_kl(prob.ent1, prob.ent2, what=f"{variant}-sinkhorn")
+    costname, p, x, y, C = _step_inputs(prob)
+    f, g, _, _ = sinkhorn_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.eps,
+                                  prob.ent1.rho, prob.ent2.rho, 1, variant=variant, cost=costname,
+                                  p=p, c=C, f0=d.f, precision="fp64")
+    return DualPair(D.to_np(f[0]), D.to_np(g[0]))
+
+
+def f_sinkhorn_step(prob, d):
+    """One plain step, g then f (src/sinkhorn.py:103-114), KL marginals."""
+    return _one_step(prob, d, "f")
+
+
+def h_sinkhorn_step(prob, d):
+    """One translation-invariant step, g then f (src/sinkhorn.py:137-163)."""
+    _require_positive_eps(prob)
+    if not (isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)):
+        raise UnsupportedEntropyError("h-sinkhorn requires kl penalties on both marginals")
+    return _one_step(prob, d, "h")
+
+
+def run(prob, config, init=None, reference=None):
+    """Iterate the configured variant until ||f_t - f_{t-1}||_inf < tol
+    (src/sinkhorn.py:246-315).  ``wall_ns`` holds the mean device time per
+    iteration of each launch chunk.  With ``reference`` the iterates are
+    advanced one step per launch so that err_f / err_g (translated iterates
+    vs the reference pair) can be traced exactly like the reference."""
+    _require_positive_eps(prob)
+    n, m = len(prob.alpha), len(prob.beta)
+    d = init if init is not None else DualPair.zeros(n, m)
+    prob.check_pair(d)
+    if config.variant == "h" and not (isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)):
+        raise UnsupportedEntropyError("h-sinkhorn requires kl penalties on both marginals")
+    require_kl(prob.ent1, prob.ent2, what="sinkhorn")
+    if config.variant == "g":
+        raise UnsupportedEntropyError("the g variant is not on the B200 path (use 'h')")
+    if config.anderson is not None:
+        raise UnsupportedEntropyError("Anderson extrapolation is not on the B200 path")
+    t = D.torch()
+    costname, p, x, y, C = _step_inputs(prob)
+    deltas, walls, err_f, err_g = [], [], [], []
+    f_cur = d.f
+    g_cur = d.g
+    done = 0
+    converged = False
+    chunk = 1 if reference is not None else 256
+    while done < config.max_iters and not converged:
+        k = min(chunk, config.max_iters - done)
+        t0 = time.perf_counter_ns()
+        f, g, tr, its = sinkhorn_batched(
+            x, y, prob.alpha.weights, prob.beta.weights, prob.eps, prob.ent1.rho, prob.ent2.rho,
+            k, variant=config.variant, cost=costname, p=p, c=C, f0=f_cur, tol=config.tol,
+            precision=config.precision)
+        t.cuda.synchronize()
+        el = time.perf_counter_ns() - t0
+        got = int(its[0].item())
+        dl = D.to_np(tr[0, :got], readonly=False)
+        deltas.extend(dl.tolist())
+        walls.extend([el // max(got, 1)] * got)
+        f_cur = D.to_np(f[0]).astype(np.float64)
+        g_cur = D.to_np(g[0]).astype(np.float64)
+        done += got
+        if got < k or (got > 0 and dl[-1] < config.tol):
+            converged = True
+        if reference is not None:
+            if config.variant == "f":
+                lam = 0.0
+            else:
+                lam = float(kl_scalars(prob.alpha.weights, prob.beta.weights, f_cur, g_cur,
+                                       prob.ent1.rho, prob.ent2.rho)[0, 0].item())
+            err_f.append(float(np.abs(f_cur + lam - reference.f).max()))
+            err_g.append(float(np.abs(g_cur - lam - reference.g).max()))
+    trace = {"delta_f": np.asarray(deltas), "wall_ns": np.asarray(walls, dtype=np.int64)}
+    if reference is not None:
+        trace["err_f"] = np.asarray(err_f)
+        trace["err_g"] = np.asarray(err_g)
+    return SolverReport(final=DualPair(f_cur, g_cur), iterations=len(deltas), converged=converged,
+                        trace=trace)

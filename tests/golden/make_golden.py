@@ -1,0 +1,369 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``uotkit`` read-only from /root/reference/pkg/src and drives the
+reference's own step / oracle functions with fixed iteration counts (the
+reference's ``run``/``fw_solve``/``fw_barycenter`` exit early once a gap or
+delta tolerance is met -- sinkhorn.py:304-306, fw.py:220-222,
+barycenter.py:394-396 -- so the loops below call the step functions
+directly, as SURVEY.md §8c prescribes).  The fixtures are small .npz files
+(no pickles); tests/test_oracle_golden.py pins the oracle against them and
+the GPU parity tests compare the CUDA path against them.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import uotkit as U  # noqa: E402
+from uotkit import barycenter as UB  # noqa: E402
+from uotkit import fw as UF  # noqa: E402
+from uotkit import sinkhorn as US  # noqa: E402
+
+from paper_2201_00730_b200 import synthetic as S  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def ref_sinkhorn(prob, variant, iters):
+    d = U.DualPair.zeros(len(prob.alpha), len(prob.beta))
+    deltas = []
+    step = US.h_sinkhorn_step if variant == "h" else US.f_sinkhorn_step
+    for _ in range(iters):
+        new = step(prob, d)
+        deltas.append(float(np.abs(new.f - d.f).max()))
+        d = new
+    return d.f, d.g, np.asarray(deltas)
+
+
+def gen_cfg1():
+    c = S.cfg1_inputs()
+    a = U.DiscreteMeasure(c.x, c.alpha)
+    b = U.DiscreteMeasure(c.y, c.beta)
+    prob = U.UotProblem(a, b, U.PowerDistance(2.0), U.KL(c.rho), U.KL(c.rho), eps=c.eps)
+    out = dict(x=c.x, y=c.y, alpha=c.alpha, beta=c.beta, eps=c.eps, rho=c.rho)
+    for v in ("h", "f"):
+        f, g, dl = ref_sinkhorn(prob, v, c.iters)
+        out[f"{v}_f"], out[f"{v}_g"], out[f"{v}_delta"] = f, g, dl
+        lam = U.lambda_star(prob, U.DualPair(f, g))
+        out[f"{v}_lam"] = lam
+        out[f"{v}_dual"] = U.eval_H(prob, U.DualPair(f, g))
+    save("cfg1.npz", **out)
+
+
+def gen_sinkhorn_small():
+    rng = np.random.default_rng(7)
+    out = {}
+    cases = []
+    for k in range(12):
+        n, m = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+        p = [1.0, 2.0, 1.5][k % 3]
+        eps = [0.05, 0.5, 0.2][k % 3]
+        r1, r2 = float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.3, 2.0))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m) * 1.7
+        if k % 4 == 3:  # zero-weight atoms are masked out of every reduction
+            wa[rng.integers(0, n)] = 0.0
+            wb[rng.integers(0, m)] = 0.0
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=eps)
+        iters = 40
+        for v in ("h", "f"):
+            f, g, dl = ref_sinkhorn(prob, v, iters)
+            out[f"c{k}_{v}_f"], out[f"c{k}_{v}_g"], out[f"c{k}_{v}_delta"] = f, g, dl
+            out[f"c{k}_{v}_dual"] = U.eval_H(prob, U.DualPair(f, g))
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([p, eps, r1, r2, iters])
+        cases.append(k)
+    out["cases"] = np.array(cases)
+    save("sinkhorn_small.npz", **out)
+
+
+def gen_points_sinkhorn(name, x, y, wa, wb, eps, rho, iters):
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(axis=2)
+    n, m = len(x), len(y)
+    prob = U.UotProblem(U.DiscreteMeasure(np.arange(n, dtype=float), wa),
+                        U.DiscreteMeasure(np.arange(m, dtype=float), wb),
+                        U.ExplicitMatrix(C), U.KL(rho), U.KL(rho), eps=eps)
+    t0 = time.time()
+    f, g, dl = ref_sinkhorn(prob, "h", iters)
+    dual = U.eval_H(prob, U.DualPair(f, g))
+    print(f"  {name}: reference H-sinkhorn {n}x{m} x{iters} in {time.time() - t0:.1f}s")
+    save(name, x=x, y=y, alpha=wa, beta=wb, eps=eps, rho=rho, iters=iters, f=f, g=g,
+         delta=dl, dual=dual)
+
+
+def gen_cfg3_small():
+    c = S.cfg3_inputs(n=384, seed=2023)
+    gen_points_sinkhorn("cfg3_small.npz", c.x, c.y, c.alpha, c.beta, c.eps, c.rho, c.iters)
+
+
+def gen_cfg4_small():
+    x, y, a, b = S.cfg4_batch(batch=2, n=256, m=256, d=64)
+    gen_points_sinkhorn("cfg4_small.npz", x[0], y[0], a[0], b[0], S.CFG4_EPS, S.CFG4_RHO, 300)
+
+
+def gen_ot1d():
+    rng = np.random.default_rng(11)
+    out = {}
+    cases = []
+
+    def add(k, x, y, wa, wb, p):
+        a = U.DiscreteMeasure(x, wa)
+        b = U.DiscreteMeasure(y, wb)
+        plan, d = U.solve_ot_1d(a, b, U.PowerDistance(p))
+        out[f"c{k}_x"], out[f"c{k}_y"] = a.points, b.points
+        out[f"c{k}_a"], out[f"c{k}_b"] = a.weights, b.weights
+        out[f"c{k}_p"] = np.array(p)
+        out[f"c{k}_i"], out[f"c{k}_j"], out[f"c{k}_m"] = plan.source_idx, plan.target_idx, plan.mass
+        out[f"c{k}_f"], out[f"c{k}_g"] = d.f, d.g
+        cases.append(k)
+
+    # reference known-answer cases: tests/test_ot1d.py:32-38, :47-58, :71-76
+    add(0, [0.0], [1.0], [1.0], [1.0], 1.0)
+    add(1, [0.0, 1.0], [0.0, 1.0], [0.7, 0.3], [0.4, 0.6], 1.0)
+    add(2, [0.0, 0.5, 1.0], [0.2, 0.9], [0.5, 0.0, 0.5], [0.6, 0.4], 2.0)
+    k = 3
+    for _ in range(60):  # tests/test_ot1d.py:60-69 style, zero weights allowed
+        n, m = rng.integers(1, 51, 2)
+        p = float(rng.choice([1.0, 2.0]))
+        wa = rng.uniform(0.0, 1.0, n)
+        wb = rng.uniform(0.0, 1.0, m)
+        wb *= wa.sum() / wb.sum()
+        add(k, np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m)), wa, wb, p)
+        k += 1
+    for n, m in ((1024, 1024), (1000, 777), (4096, 4096)):  # cfg2-scale sweeps
+        wa = rng.exponential(1.0, n)
+        wb = rng.exponential(1.0, m)
+        wb *= wa.sum() / wb.sum()
+        add(k, np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m)), wa, wb, 2.0)
+        k += 1
+    out["cases"] = np.array(cases)
+    save("ot1d.npz", **out)
+
+
+def ref_fw(prob, iters, step):
+    """fw.py:176-232 loop body with the early exit removed."""
+    d = UF._default_init(prob)
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap")}
+    plan = None
+    for t in range(iters):
+        ta, tb, plan, atom, fw_gap = UF._lmo(prob, d)
+        dual = UF._h0(prob, d.f, d.g)
+        primal = U.eval_primal(prob, plan)
+        tr["h0"].append(dual)
+        tr["fw_gap"].append(fw_gap)
+        tr["pd_gap"].append(primal - dual)
+        gamma = 2.0 / (2.0 + t) if step == "harmonic" else UF.line_search_h0(prob, d, atom)
+        d = U.DualPair((1.0 - gamma) * d.f + gamma * atom.f, (1.0 - gamma) * d.g + gamma * atom.g)
+    lam = U.lambda_star(prob, d)
+    return d, lam, plan, {k: np.asarray(v) for k, v in tr.items()}
+
+
+def gen_fw():
+    out = {}
+    cases = []
+    rng = np.random.default_rng(13)
+    specs = []
+    for k in range(6):  # small random problems, both step rules
+        n, m = int(rng.integers(20, 70)), int(rng.integers(20, 70))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.exponential(1.0, n)
+        wa *= rng.uniform(0.5, 2.0) / wa.sum()
+        wb = rng.exponential(1.0, m)
+        wb *= rng.uniform(0.5, 2.0) / wb.sum()
+        r1, r2 = float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.3, 2.0))
+        p = [2.0, 1.0][k % 2]
+        specs.append((x, y, wa, wb, r1, r2, p, 120, ["linesearch", "harmonic"][k % 2]))
+    x2, y2, a2, b2 = S.cfg2_batch(count=3)
+    for q in range(3):  # the first problems of the seeded cfg2 batch, full shape
+        specs.append((x2[q], y2[q], a2[q], b2[q], 1.0, 1.0, 2.0, 500,
+                      "harmonic" if q == 2 else "linesearch"))
+    for k, (x, y, wa, wb, r1, r2, p, iters, step) in enumerate(specs):
+        t0 = time.time()
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=0.0)
+        d, lam, plan, tr = ref_fw(prob, iters, step)
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([r1, r2, p, iters, 1.0 if step == "linesearch" else 0.0])
+        out[f"c{k}_f_raw"], out[f"c{k}_g_raw"] = d.f, d.g
+        out[f"c{k}_f"], out[f"c{k}_g"] = d.f + lam, d.g - lam
+        out[f"c{k}_i"], out[f"c{k}_j"], out[f"c{k}_m"] = plan.source_idx, plan.target_idx, plan.mass
+        for kk, v in tr.items():
+            out[f"c{k}_{kk}"] = v
+        cases.append(k)
+        print(f"  fw case {k}: {len(x)}x{len(y)} {step} x{iters} in {time.time() - t0:.1f}s")
+    out["cases"] = np.array(cases)
+    save("fw.npz", **out)
+
+
+def gen_mot():
+    rng = np.random.default_rng(17)
+    out = {}
+    cases = []
+
+    def add(k, inputs, w):
+        plan, duals = U.solve_mot_1d(inputs, w)
+        kk = len(inputs)
+        out[f"c{k}_k"] = np.array(kk)
+        out[f"c{k}_w"] = np.asarray(w, dtype=float)
+        for q, mq in enumerate(inputs):
+            out[f"c{k}_x{q}"], out[f"c{k}_a{q}"] = mq.points, mq.weights
+            out[f"c{k}_f{q}"] = duals.potentials[q]
+        out[f"c{k}_idx"], out[f"c{k}_m"] = plan.indices, plan.mass
+        cases.append(k)
+
+    # tests/test_barycenter.py:58-66 (single atoms) and :95-105 (zero weights)
+    add(0, [U.DiscreteMeasure([float(q)], [1.0]) for q in range(3)], np.full(3, 1 / 3))
+    add(1, [U.DiscreteMeasure([0.0, 0.4, 1.0], [0.5, 0.0, 0.5]),
+            U.DiscreteMeasure([0.1, 0.9], [0.6, 0.4]),
+            U.DiscreteMeasure([0.2, 0.8], [0.3, 0.7])], np.full(3, 1 / 3))
+    k = 2
+    for _ in range(40):  # random families, K in 2..5, ragged sizes
+        kk = int(rng.integers(2, 6))
+        inputs = []
+        for _q in range(kk):
+            n = int(rng.integers(2, 30))
+            wq = rng.uniform(0.1, 1.0, n)
+            wq *= 1.3 / wq.sum()
+            inputs.append(U.DiscreteMeasure(np.sort(rng.uniform(0, 1, n)), wq))
+        w = rng.uniform(0.2, 1.0, kk)
+        w /= w.sum()
+        add(k, inputs, w)
+        k += 1
+    # one cfg5-shaped family (K = 16) at reduced N
+    xs, ws = S.cfg5_batch(count=1, n=256)
+    inputs = [U.DiscreteMeasure(xs[0, q], ws[0, q] * (1.0 / ws[0, q].sum())) for q in range(16)]
+    add(k, inputs, np.full(16, 1 / 16))
+    out["cases"] = np.array(cases + [k])
+    save("mot.npz", **out)
+
+
+def ref_barycenter(problem, iters, step):
+    """barycenter.py:361-414 with the early exit removed and no _finalize."""
+    inputs, w = problem.inputs, problem.omega
+    rhos = problem.rhos()
+    costfn = UB.barycentric_cost_fn(w)
+    pots = [np.zeros(len(a)) for a in inputs]
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap")}
+    plan = None
+    for t in range(iters):
+        lam = UB.multimarginal_lambda(UB.MultiDual(tuple(pots)), inputs, w, problem.rho)
+        tilted = [a.weights * np.exp(-(f + lk) / rk) for a, f, lk, rk in zip(inputs, pots, lam, rhos)]
+        plan, atoms = UB.solve_mot_1d([U.DiscreteMeasure(a.points, tw) for a, tw in zip(inputs, tilted)],
+                                      w, costfn)
+        fw_gap = float(sum(np.dot(tw, r - f) for tw, r, f in zip(tilted, atoms.potentials, pots)))
+        dual = UB._h_value(inputs, rhos, pots)
+        primal = UB.plan_cost(plan, inputs, costfn) + float(sum(
+            U.divergence(U.KL(rk), plan.marginal(q, len(a)), a.weights)
+            for q, (a, rk) in enumerate(zip(inputs, rhos))))
+        tr["h0"].append(dual)
+        tr["fw_gap"].append(fw_gap)
+        tr["pd_gap"].append(primal - dual)
+        if step == "harmonic":
+            gamma = 2.0 / (2.0 + t)
+        else:
+            def value(g):
+                return UB._h_value(inputs, rhos, [(1.0 - g) * f + g * r for f, r in zip(pots, atoms.potentials)])
+            gamma = UF.ternary_max(value, 0.0, 1.0, iters=60)
+            gamma = max(((value(c), c) for c in (gamma, 0.0, 1.0)), key=lambda z: z[0])[1]
+        pots = [(1.0 - gamma) * f + gamma * r for f, r in zip(pots, atoms.potentials)]
+    lam = UB.multimarginal_lambda(UB.MultiDual(tuple(pots)), inputs, w, problem.rho)
+    return pots, lam, plan, {k: np.asarray(v) for k, v in tr.items()}
+
+
+def gen_barycenter():
+    rng = np.random.default_rng(19)
+    out = {}
+    specs = []
+    for k in range(4):
+        kk = [3, 4, 2, 5][k]
+        inputs = []
+        for _q in range(kk):
+            n = int(rng.integers(8, 40))
+            wq = rng.uniform(0.05, 1.0, n)
+            wq *= rng.uniform(0.5, 2.0) / wq.sum()
+            inputs.append(U.DiscreteMeasure(np.sort(rng.uniform(0, 1, n)), wq))
+        w = rng.uniform(0.2, 1.0, kk)
+        w /= w.sum()
+        specs.append((inputs, w, float(rng.uniform(0.5, 2.0)), 60, ["linesearch", "harmonic"][k % 2]))
+    xs, ws = S.cfg5_batch(count=1, n=128)
+    specs.append(([U.DiscreteMeasure(xs[0, q], ws[0, q]) for q in range(16)], np.full(16, 1 / 16),
+                  1.0, 40, "linesearch"))
+    cases = []
+    for k, (inputs, w, rho, iters, step) in enumerate(specs):
+        t0 = time.time()
+        problem = U.BarycenterProblem(tuple(inputs), w, rho)
+        pots, lam, plan, tr = ref_barycenter(problem, iters, step)
+        out[f"c{k}_k"] = np.array(len(inputs))
+        out[f"c{k}_w"] = w
+        out[f"c{k}_par"] = np.array([rho, iters, 1.0 if step == "linesearch" else 0.0])
+        for q, mq in enumerate(inputs):
+            out[f"c{k}_x{q}"], out[f"c{k}_a{q}"] = mq.points, mq.weights
+            out[f"c{k}_f{q}"] = pots[q] + lam[q]
+            out[f"c{k}_fraw{q}"] = pots[q]
+        out[f"c{k}_idx"], out[f"c{k}_m"] = plan.indices, plan.mass
+        bar = U.extract_barycenter(plan, inputs, w)
+        out[f"c{k}_bar_x"], out[f"c{k}_bar_w"] = bar.points, bar.weights
+        for kk_, v in tr.items():
+            out[f"c{k}_{kk_}"] = v
+        cases.append(k)
+        print(f"  barycenter case {k}: K={len(inputs)} x{iters} {step} in {time.time() - t0:.1f}s")
+    out["cases"] = np.array(cases)
+    save("barycenter.npz", **out)
+
+
+def gen_duality():
+    """Known answers: tests/test_duality.py:64-75, :134-144, :185-200 style."""
+    rng = np.random.default_rng(23)
+    out = {}
+    for k in range(8):
+        n, m = int(rng.integers(2, 30)), int(rng.integers(2, 30))
+        wa = rng.uniform(0.0, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m)
+        f = rng.normal(0, 1, n)
+        g = rng.normal(0, 1, m)
+        r1, r2 = float(rng.uniform(0.2, 3.0)), float(rng.uniform(0.2, 3.0))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb), U.PowerDistance(2.0),
+                            U.KL(r1), U.KL(r2), eps=0.3)
+        d = U.DualPair(f, g)
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_f"], out[f"c{k}_g"] = f, g
+        out[f"c{k}_par"] = np.array([r1, r2, 0.3])
+        out[f"c{k}_lam"] = U.lambda_star(prob, d)
+        out[f"c{k}_H"] = U.eval_H(prob, d)
+        ta, tb = U.updated_marginals(prob, d)
+        out[f"c{k}_ta"], out[f"c{k}_tb"] = ta, tb
+        out[f"c{k}_sa"] = U.softmin(prob.alpha, r1, f)
+    out["cases"] = np.arange(8)
+    save("duality.npz", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
+                             "mot", "barycenter", "duality"]
+    for w in which:
+        t0 = time.time()
+        globals()[f"gen_{w}"]()
+        print(f"[{w}] {time.time() - t0:.1f}s")

@@ -1,0 +1,112 @@
+"""GPU parity of the fused Sinkhorn kernels against the reference goldens
+and the CPU oracle.  Tolerances (north star): 1e-9 relative in fp64,
+1e-4 * eps absolute in fp32."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2201_00730_b200 as P
+from conftest import cases, golden, rel_err
+from paper_2201_00730_b200 import _device as D
+from paper_2201_00730_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def run_dev(x, y, a, b, eps, rho, iters, variant="h", cost="sqeuclid", p=2.0, c=None,
+            precision="fp64", rho2=None, f0=None):
+    f, g, tr, its = P.sinkhorn_batched(x, y, a, b, eps, rho, rho if rho2 is None else rho2, iters,
+                                       variant=variant, cost=cost, p=p, c=c,
+                                       precision=precision, f0=f0)
+    return (D.to_np(f).astype(np.float64), D.to_np(g).astype(np.float64), D.to_np(tr),
+            D.to_np(its))
+
+
+@pytest.mark.parametrize("variant", ["h", "f"])
+def test_cfg1_fp64_1000_iterations(variant):
+    z = golden("cfg1.npz")
+    f, g, tr, its = run_dev(z["x"][None], z["y"][None], z["alpha"][None], z["beta"][None],
+                            float(z["eps"]), 1.0, 1000, variant=variant, cost="power")
+    assert its[0] == 1000
+    assert rel_err(f[0], g[0], z[f"{variant}_f"], z[f"{variant}_g"]) < 1e-9
+    np.testing.assert_allclose(tr[0], z[f"{variant}_delta"], rtol=1e-6,
+                               atol=1e-12 * np.abs(z[f"{variant}_f"]).max())
+
+
+def test_small_cases_fp64_power_costs_and_zero_weights():
+    z = golden("sinkhorn_small.npz")
+    for k in cases(z):
+        p, eps, r1, r2, iters = z[f"c{k}_par"]
+        for v in ("h", "f"):
+            f, g, _, _ = run_dev(z[f"c{k}_x"][None], z[f"c{k}_y"][None], z[f"c{k}_a"][None],
+                                 z[f"c{k}_b"][None], eps, r1, int(iters), variant=v, cost="power",
+                                 p=p, rho2=r2)
+            assert rel_err(f[0], g[0], z[f"c{k}_{v}_f"], z[f"c{k}_{v}_g"]) < 1e-9, (k, v)
+
+
+def test_small_cases_explicit_cost_fp64():
+    z = golden("sinkhorn_small.npz")
+    for k in cases(z)[:6]:
+        p, eps, r1, r2, iters = z[f"c{k}_par"]
+        C = np.abs(z[f"c{k}_x"][:, None] - z[f"c{k}_y"][None, :]) ** p
+        f, g, _, _ = run_dev(z[f"c{k}_x"][None], z[f"c{k}_y"][None], z[f"c{k}_a"][None],
+                             z[f"c{k}_b"][None], eps, r1, int(iters), variant="h", cost="explicit",
+                             c=C[None], rho2=r2)
+        assert rel_err(f[0], g[0], z[f"c{k}_h_f"], z[f"c{k}_h_g"]) < 1e-9, k
+
+
+@pytest.mark.parametrize("name", ["cfg3_small.npz", "cfg4_small.npz"])
+def test_point_clouds_fp64(name):
+    z = golden(name)
+    f, g, _, _ = run_dev(z["x"][None], z["y"][None], z["alpha"][None], z["beta"][None],
+                         float(z["eps"]), float(z["rho"]), int(z["iters"]))
+    assert rel_err(f[0], g[0], z["f"], z["g"]) < 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg3_small.npz", "cfg4_small.npz"])
+def test_point_clouds_fp32_tolerance(name):
+    z = golden(name)
+    eps = float(z["eps"])
+    f, g, _, _ = run_dev(z["x"][None], z["y"][None], z["alpha"][None], z["beta"][None], eps,
+                         float(z["rho"]), int(z["iters"]), precision="fp32")
+    assert np.abs(f[0] - z["f"]).max() <= 1e-4 * eps
+    assert np.abs(g[0] - z["g"]).max() <= 1e-4 * eps
+
+
+def test_batched_equals_individual():
+    x, y, a, b = S.cfg4_batch(batch=3, n=96, m=80, d=3)
+    fb, gb, _, _ = run_dev(x, y, a, b, 0.05, 0.5, 30)
+    for k in range(3):
+        f1, g1, _, _ = run_dev(x[k:k + 1], y[k:k + 1], a[k:k + 1], b[k:k + 1], 0.05, 0.5, 30)
+        assert rel_err(fb[k], gb[k], f1[0], g1[0]) < 1e-13
+
+
+def test_cfg3_shape_fp32_vs_oracle_2048():
+    c = S.cfg3_inputs(n=2048, seed=99)
+    f, g, _, _ = run_dev(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, c.rho, 200,
+                         precision="fp32")
+    cost = O.PointCost(c.x, c.y)
+    fo, go, _ = O.sinkhorn_fixed(cost, c.alpha, c.beta, c.eps, c.rho, c.rho, "h", 200)
+    assert np.abs(f[0] - fo).max() <= 1e-4 * c.eps
+    assert np.abs(g[0] - go).max() <= 1e-4 * c.eps
+
+
+def test_full_cfg3_one_step_sampled_columns():
+    """Size-independent check at the full BASELINE size (N = M = 65536): the
+    column differences of one GPU g-update equal the oracle's softmin
+    differences on sampled columns (translation-free, so the global Smin
+    shift cancels), from a GPU-produced f."""
+    c = S.cfg3_inputs()
+    f, g, _, _ = run_dev(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, c.rho, 3,
+                         precision="fp32")
+    f2, g2, _, _ = run_dev(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, c.rho, 1,
+                           precision="fp32", f0=f)
+    rng = np.random.default_rng(0)
+    cols = np.sort(rng.choice(len(c.y), 256, replace=False))
+    cost = O.PointCost(c.x, c.y[cols])
+    smin = cost.smin_cols(f[0], c.eps, c.alpha)
+    a_coef = c.rho / (c.rho + c.eps)
+    ref = a_coef * (smin - smin[0])
+    got = g2[0][cols] - g2[0][cols[0]]
+    assert np.abs(got - ref).max() <= 1e-4 * c.eps
