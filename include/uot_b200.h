@@ -120,12 +120,15 @@ int uot_kl_scalars(int32_t batch, int32_t n, int32_t m, const double* a, const d
  * c [batch][n][m].  Outputs: f [batch][n], g [batch][m]; plan entries
  * (ei, ej int32, em fp64) [batch][n+m-1] with count [batch]; entries are in
  * sweep order.  status [batch] gets 1 for a mass mismatch above 1e-9
- * relative (src/ot1d.py:133-136).
+ * relative (src/ot1d.py:133-136).  The ExplicitMatrix cost is validated on
+ * the host (Monge check, src/measures.py:148-165) and is not on the B200
+ * path yet (returns 3).  n, m <= 4096 per problem.
  * ------------------------------------------------------------------------ */
+int uot_ot1d_workspace_size(int32_t batch, int32_t n, int32_t m, size_t* bytes);
 int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
                      const double* a, const double* b, int32_t cost, double p, const double* c,
                      double* f, double* g, int32_t* ei, int32_t* ej, double* em, int32_t* count,
-                     int32_t* status, void* stream);
+                     int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * Batched 1-D Frank-Wolfe UOT at eps = 0: replaces src/fw.py:176-232
@@ -141,6 +144,7 @@ int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const
  * dual / lambda* in summary [batch][3]; status [batch] (1 = reweighted
  * masses disagree, fw.py:161-166).  With early_exit != 0 a problem stops at
  * the first pd_gap < gap_tol (fw.py:220-222).
+ * n, m <= 4096 per problem (one CTA per problem, state resident on chip).
  * ------------------------------------------------------------------------ */
 typedef struct uot_fw_desc {
   int32_t batch, n, m;

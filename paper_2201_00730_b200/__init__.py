@@ -18,6 +18,9 @@ from .exceptions import (
     UotError,
 )
 from .measures import DiscreteMeasure, ExplicitMatrix, PowerDistance, SqEuclideanPoints
+from .certify import Certificate, assemble_certificate
+from .fw import FwConfig, feasibility_violation, fw_solve, fw_solve_batched
+from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched
 from .sinkhorn import (
     AndersonConfig,
     SinkhornConfig,

@@ -1,0 +1,749 @@
+// fw1d.cu -- batched 1-D OT oracle (Algorithm 1) and batched Frank-Wolfe UOT
+// at eps = 0 (K4/K5/K6 of SURVEY.md §2.2).
+//
+// Reference: src/ot1d.py:112-172 (solve_ot_1d), src/fw.py:106-232 (_h0,
+// ternary line search, _lmo, fw_solve), src/duality.py:175-178, :279-303,
+// :320-344 (lambda_star, _eval_h_kl, updated_marginals, eval_primal).
+//
+// Design: one CTA per problem, THREADS x EPT elements per side held in
+// registers for the whole run (x, y and the cumulative masses live in shared
+// memory for the random accesses of the oracle), so an FW iteration touches
+// HBM only for its three trace scalars.  The monotone sweep is restated as a
+// merge of cumulative masses: with A_k = sum_{i<=k} ta_i and B_l likewise,
+// source event k happens after the target events with B_l < A_k (ties go to
+// the source, ot1d.py:158), so its partner index is a binary search, and the
+// dual potentials are prefix sums of cost differences along the staircase:
+//   r_{k+1} = r_k + C(k+1, j_k) - C(k, j_k),  s_{l+1} = s_l + C(i_l, l+1) - C(i_l, l)
+// starting from r_0 = 0, s_0 = C(0,0) (ot1d.py:138-166).  The line search
+// minimises the convex log-partition phi(gamma) (H_0 = const - (r1+r2) e^phi,
+// fw.py:106-148) by safeguarded Newton on three moments per pass instead of
+// the reference's 123 ternary evaluations (FW parity).
+#include <algorithm>
+
+#include "../../include/uot_b200.h"
+#include "common.cuh"
+
+namespace uot {
+namespace {
+
+constexpr int FW_THREADS = 256;
+
+struct FwArgs {
+  int n, m;
+  double p;
+  double r1, r2;
+  int step;
+  int max_iters;
+  double gap_tol;
+  int early_exit;
+  int mode;  // 0 = Frank-Wolfe, 1 = plain OT oracle on (a, b)
+  const double* x;
+  const double* y;
+  const double* a;
+  const double* b;
+  double* f;
+  double* g;
+  double* h0;
+  double* fw_gap;
+  double* pd_gap;
+  int* iterations;
+  int* ei;
+  int* ej;
+  double* em;
+  int* count;
+  double* summary;
+  int* status;
+  double* scratch;  // [batch][n+m] doubles + [batch][n+m][2] ints (plan extraction)
+  int* scratch_i;
+};
+
+__device__ __forceinline__ double pcost(double xi, double yj, double p) {
+  const double d = xi - yj;
+  if (p == 2.0) return d * d;
+  const double ad = fabs(d);
+  if (p == 1.0) return ad;
+  return pow(ad, p);
+}
+
+// Block reduction of K doubles (sum).  scratch: K * 32 doubles.
+template <int K>
+__device__ __forceinline__ void bsum(double (&v)[K], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  constexpr int NW = FW_THREADS / 32;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += scratch[k * 32 + w];
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+template <int K>
+__device__ __forceinline__ void bmax(double (&v)[K], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_max(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  constexpr int NW = FW_THREADS / 32;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = -CUDART_INF;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s = fmax(s, scratch[k * 32 + w]);
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+// Exclusive block scan of K per-thread totals (sum); returns prefix offsets.
+template <int K>
+__device__ __forceinline__ void bscan_excl(double (&v)[K], double (&total)[K], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double incl[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    incl[k] = s;
+  }
+  __syncthreads();
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = incl[k];
+  }
+  __syncthreads();
+  constexpr int NW = FW_THREADS / 32;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double off = 0.0, tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const double s = scratch[k * 32 + w];
+      if (w < warp) off += s;
+      tot += s;
+    }
+    total[k] = tot;
+    v[k] = off + incl[k] - v[k];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int ibsum(int v, int* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  int s = 0;
+  for (int w = 0; w < FW_THREADS / 32; ++w) s += scratch[w];
+  __syncthreads();
+  return s;
+}
+
+// #{ l in [0, len) : arr[l] < v }  (strict) or <= v (non-strict)
+template <bool STRICT>
+__device__ __forceinline__ int count_below(const double* arr, int len, double v) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const bool below = STRICT ? (arr[mid] < v) : (arr[mid] <= v);
+    if (below)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Per-problem CTA state.  Thread t owns source/target elements
+// t*EPT .. t*EPT+EPT-1 of each side.
+template <int EPT>
+struct Cta {
+  int n, m;
+  double p;
+  const double* sx;  // smem copies of the supports
+  const double* sy;
+  double* sA;        // smem cumulative masses (breakpoints)
+  double* sB;
+  double* red;       // reduction scratch (>= 16*32 doubles)
+
+  __device__ int src(int e) const { return threadIdx.x * EPT + e; }
+
+  // Balanced 1-D OT oracle on (ta, tb) (masses assumed equal to 1e-9):
+  // cumulative masses -> partner searches -> dual potentials (r, s).
+  // Leaves sA/sB holding the breakpoints for plan extraction.
+  __device__ void oracle(const double (&ta)[EPT], const double (&tb)[EPT], double (&r)[EPT],
+                         double (&s)[EPT], double& mass_a, double& mass_b) {
+    // inclusive prefix sums of the tilted masses
+    double pa[EPT], pb[EPT];
+    double ca = 0.0, cb = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ca += ta[e];
+      pa[e] = ca;
+      cb += tb[e];
+      pb[e] = cb;
+    }
+    double tot[2] = {ca, cb}, totals[2];
+    bscan_excl<2>(tot, totals, red);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      if (i < n) sA[i] = tot[0] + pa[e];
+      if (i < m) sB[i] = tot[1] + pb[e];
+    }
+    mass_a = totals[0];
+    mass_b = totals[1];
+    __syncthreads();
+    // cost increments along the staircase
+    double da[EPT], db[EPT];
+    double la = 0.0, lb = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      da[e] = 0.0;
+      db[e] = 0.0;
+      if (i >= 1 && i < n) {
+        // source event k = i-1: partner j = #{l < m-1 : B_l < A_{i-1}}
+        const int j = count_below<true>(sB, m - 1, sA[i - 1]);
+        const double yj = sy[j];
+        da[e] = pcost(sx[i], yj, p) - pcost(sx[i - 1], yj, p);
+      }
+      if (i >= 1 && i < m) {
+        // target event l = i-1: partner = #{k < n-1 : A_k <= B_{i-1}}
+        const int k = count_below<false>(sA, n - 1, sB[i - 1]);
+        const double xk = sx[k];
+        db[e] = pcost(xk, sy[i], p) - pcost(xk, sy[i - 1], p);
+      }
+      la += da[e];
+      lb += db[e];
+    }
+    double off[2] = {la, lb}, unused[2];
+    bscan_excl<2>(off, unused, red);
+    const double s0 = pcost(sx[0], sy[0], p);
+    double ra = off[0], rb = off[1];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ra += da[e];
+      rb += db[e];
+      r[e] = ra;
+      s[e] = s0 + rb;
+    }
+  }
+
+  // Plan of the breakpoints currently in sA/sB, compacted to entries with
+  // positive mass in sweep order (ot1d.py:149-153).  scratch: (n+m) doubles,
+  // scratch_i: 2*(n+m) ints, both per problem.
+  __device__ void extract_plan(double* vals, int* codes, int* ei, int* ej, double* em,
+                               int* count, double total) {
+    const int nev = (n - 1) + (m - 1);
+    // scatter events by merged rank
+    for (int i = threadIdx.x; i < n - 1; i += FW_THREADS) {
+      const double v = sA[i];
+      const int j = count_below<true>(sB, m - 1, v);
+      const int rank = i + j;
+      vals[rank] = v;
+      codes[2 * rank] = i + 1;
+      codes[2 * rank + 1] = j;
+    }
+    for (int l = threadIdx.x; l < m - 1; l += FW_THREADS) {
+      const double v = sB[l];
+      const int k = count_below<false>(sA, n - 1, v);
+      const int rank = l + k;
+      vals[rank] = v;
+      codes[2 * rank] = k;
+      codes[2 * rank + 1] = l + 1;
+    }
+    __syncthreads();
+    // state s (0..nev) follows event s-1; mass = bp(s) - bp(s-1)
+    int base = 0;
+    int* iscr = reinterpret_cast<int*>(red);
+    for (int s0 = 0; s0 <= nev; s0 += FW_THREADS) {
+      const int s = s0 + threadIdx.x;
+      double mass = 0.0;
+      int ii = 0, jj = 0;
+      if (s <= nev) {
+        const double lo = s == 0 ? 0.0 : fmin(vals[s - 1], total);
+        const double hi = s == nev ? total : fmin(vals[s], total);
+        mass = hi - lo;
+        if (s > 0) {
+          ii = codes[2 * (s - 1)];
+          jj = codes[2 * (s - 1) + 1];
+        }
+      }
+      const int keep = (s <= nev && mass > 0.0) ? 1 : 0;
+      // block exclusive scan of keep flags
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      int incl = keep;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      __syncthreads();
+      if (lane == 31) iscr[warp] = incl;
+      __syncthreads();
+      int off = 0, tot = 0;
+      for (int w = 0; w < FW_THREADS / 32; ++w) {
+        if (w < warp) off += iscr[w];
+        tot += iscr[w];
+      }
+      __syncthreads();
+      if (keep) {
+        const int pos = base + off + incl - 1;
+        ei[pos] = ii;
+        ej[pos] = jj;
+        em[pos] = mass;
+      }
+      base += tot;
+    }
+    if (threadIdx.x == 0) *count = base;
+    __syncthreads();
+  }
+};
+
+template <int EPT>
+__global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[16 * 32];
+  const int b = blockIdx.x;
+  const int n = A.n, m = A.m;
+  double* sx = smem;
+  double* sy = sx + n;
+  double* sA = sy + m;
+  double* sB = sA + n;
+  Cta<EPT> c{n, m, A.p, sx, sy, sA, sB, red};
+
+  for (int i = threadIdx.x; i < n; i += FW_THREADS) sx[i] = A.x[(long)b * n + i];
+  for (int j = threadIdx.x; j < m; j += FW_THREADS) sy[j] = A.y[(long)b * m + j];
+
+  double al[EPT], be[EPT], f[EPT], g[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    al[e] = i < n ? A.a[(long)b * n + i] : 0.0;
+    be[e] = i < m ? A.b[(long)b * m + i] : 0.0;
+    f[e] = i < n ? A.f[(long)b * n + i] : 0.0;
+    g[e] = i < m ? A.g[(long)b * m + i] : 0.0;
+  }
+  __syncthreads();
+  double* vals = A.scratch + (long)b * (n + m);
+  int* codes = A.scratch_i + (long)b * 2 * (n + m);
+  int* ei = A.ei + (long)b * (n + m - 1);
+  int* ej = A.ej + (long)b * (n + m - 1);
+  double* em = A.em + (long)b * (n + m - 1);
+
+  if (A.mode == 1) {
+    // Plain balanced OT on (a, b): src/ot1d.py:112-172.
+    double r[EPT], s[EPT], ma, mb;
+    c.oracle(al, be, r, s, ma, mb);
+    const int bad = fabs(ma - mb) > 1e-9 * fmax(ma, mb);  // ot1d.py:133-136
+    if (threadIdx.x == 0) A.status[b] = bad ? UOT_MASS_BALANCE : 0;
+    if (bad) return;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) A.f[(long)b * n + i] = r[e];
+      if (i < m) A.g[(long)b * m + i] = s[e];
+    }
+    c.extract_plan(vals, codes, ei, ej, em, A.count + b, fmin(ma, mb));
+    return;
+  }
+
+  const double r1 = A.r1, r2 = A.r2;
+  const double t1 = r1 / (r1 + r2), t2 = r2 / (r1 + r2);
+  double mass[2] = {0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    mass[0] += al[e];
+    mass[1] += be[e];
+  }
+  bsum<2>(mass, red);
+  const double malpha = mass[0], mbeta = mass[1];
+
+  int status = 0;
+  int iters = 0;
+  double last_primal = 0.0, last_dual = 0.0;
+  for (int t = 0; t < A.max_iters; ++t) {
+    // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303)
+    double ua[EPT], ub[EPT];
+    double mx[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ua[e] = al[e] > 0.0 ? -f[e] / r1 : -CUDART_INF;
+      ub[e] = be[e] > 0.0 ? -g[e] / r2 : -CUDART_INF;
+      mx[0] = fmax(mx[0], ua[e]);
+      mx[1] = fmax(mx[1], ub[e]);
+    }
+    bmax<2>(mx, red);
+    double ea[EPT], eb[EPT];
+    double sums[2] = {0.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ea[e] = exp(ua[e] - mx[0]);
+      eb[e] = exp(ub[e] - mx[1]);
+      sums[0] += al[e] * ea[e];
+      sums[1] += be[e] * eb[e];
+    }
+    bsum<2>(sums, red);
+    const double la = mx[0] + log(sums[0]);
+    const double lb = mx[1] + log(sums[1]);
+    const double lam = (r1 * r2 / (r1 + r2)) * (la - lb);
+    const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * exp(t1 * la + t2 * lb);
+    const double sca = exp(mx[0] - lam / r1), scb = exp(mx[1] + lam / r2);
+    double ta[EPT], tb[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ta[e] = al[e] * ea[e] * sca;
+      tb[e] = be[e] * eb[e] * scb;
+    }
+    // --- linear oracle (ot1d.py:112-172 on the tilted marginals, fw.py:159-173)
+    double r[EPT], s[EPT], mta, mtb;
+    c.oracle(ta, tb, r, s, mta, mtb);
+    if (fabs(mta - mtb) > 1e-9 * fmax(mta, mtb)) {  // fw.py:161-166
+      status = UOT_MASS_BALANCE;
+      break;
+    }
+    // --- gaps and line-search moments at gamma = 0
+    // log(ta/alpha) = u - lam/r1 exactly, so the KL terms of the oracle plan
+    // (whose marginals are ta, tb) need no logarithm (entropies.py:123-131).
+    double acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const double va = (r[e] - f[e]) / r1, vb = (s[e] - g[e]) / r2;
+      acc[0] += ta[e] * (r[e] - f[e]);
+      acc[1] += tb[e] * (s[e] - g[e]);
+      acc[2] += ta[e] * r[e] + tb[e] * s[e];
+      if (ta[e] > 0.0) acc[3] += ta[e] * (ua[e] - lam / r1);
+      if (tb[e] > 0.0) acc[4] += tb[e] * (ub[e] + lam / r2);
+      acc[5] += ta[e] * va;
+      acc[6] += ta[e] * va * va;
+      acc[7] += tb[e] * vb;
+      acc[8] += tb[e] * vb * vb;
+    }
+    bsum<9>(acc, red);
+    const double fw_gap = acc[0] + acc[1];
+    const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
+    const double primal = acc[2] + r1 * kl1 + r2 * kl2;
+    const double pd_gap = primal - dual;
+    if (threadIdx.x == 0) {
+      A.h0[(long)b * A.max_iters + t] = dual;
+      A.fw_gap[(long)b * A.max_iters + t] = fw_gap;
+      A.pd_gap[(long)b * A.max_iters + t] = pd_gap;
+    }
+    iters = t + 1;
+    last_primal = primal;
+    last_dual = dual;
+    const bool stop = A.early_exit && pd_gap < A.gap_tol;  // fw.py:220-222
+    if (stop || t == A.max_iters - 1) {
+      c.extract_plan(vals, codes, ei, ej, em, A.count + b, fmin(mta, mtb));
+    }
+    if (stop) break;
+    // --- step size
+    double gam;
+    if (A.step == UOT_STEP_HARMONIC) {
+      gam = 2.0 / (2.0 + t);  // fw.py:223-224
+    } else {
+      // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
+      const double ea1 = acc[5] / mta, ea2 = acc[6] / mta;
+      const double eb1 = acc[7] / mtb, eb2 = acc[8] / mtb;
+      double d1 = -t1 * ea1 - t2 * eb1;
+      double d2 = t1 * (ea2 - ea1 * ea1) + t2 * (eb2 - eb1 * eb1);
+      // shift bounds for the passes: max(u - gamma va) <= (1-gamma) max u + gamma max(-r/r1)
+      double mr[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        if (al[e] > 0.0) mr[0] = fmax(mr[0], -r[e] / r1);
+        if (be[e] > 0.0) mr[1] = fmax(mr[1], -s[e] / r2);
+      }
+      bmax<2>(mr, red);
+      if (!(d1 < 0.0)) {
+        gam = 0.0;
+      } else {
+        double lo = 0.0, hi = 1.0;
+        gam = (d2 > 0.0) ? fmin(1.0, -d1 / d2) : 1.0;
+        for (int it = 0; it < 40; ++it) {
+          // one pass: moments of va / vb under p_gamma, q_gamma
+          const double sha = (1.0 - gam) * mx[0] + gam * mr[0];
+          const double shb = (1.0 - gam) * mx[1] + gam * mr[1];
+          double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int e = 0; e < EPT; ++e) {
+            const double va = (r[e] - f[e]) / r1, vb = (s[e] - g[e]) / r2;
+            const double wa = al[e] > 0.0 ? al[e] * exp(ua[e] - gam * va - sha) : 0.0;
+            const double wb = be[e] > 0.0 ? be[e] * exp(ub[e] - gam * vb - shb) : 0.0;
+            mom[0] += wa;
+            mom[1] += wa * va;
+            mom[2] += wa * va * va;
+            mom[3] += wb;
+            mom[4] += wb * vb;
+            mom[5] += wb * vb * vb;
+          }
+          bsum<6>(mom, red);
+          const double a1 = mom[1] / mom[0], a2 = mom[2] / mom[0];
+          const double b1 = mom[4] / mom[3], b2 = mom[5] / mom[3];
+          const double g1 = -t1 * a1 - t2 * b1;
+          const double g2 = t1 * (a2 - a1 * a1) + t2 * (b2 - b1 * b1);
+          if (g1 < 0.0)
+            lo = gam;
+          else
+            hi = gam;
+          if (gam >= 1.0 && g1 <= 0.0) {
+            gam = 1.0;
+            break;
+          }
+          double nxt = (g2 > 0.0) ? gam - g1 / g2 : 0.5 * (lo + hi);
+          if (!(nxt > lo && nxt < hi)) nxt = 0.5 * (lo + hi);
+          const bool conv = fabs(nxt - gam) <= 1e-15 * fmax(1.0, gam) || g1 == 0.0 ||
+                            hi - lo <= 4e-16;
+          gam = nxt;
+          if (conv) break;
+        }
+      }
+    }
+    // --- update (fw.py:227-230)
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      f[e] = (1.0 - gam) * f[e] + gam * r[e];
+      g[e] = (1.0 - gam) * g[e] + gam * s[e];
+    }
+  }
+  // --- finalize: translate by lambda* (fw.py:235-252)
+  double mx[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    if (al[e] > 0.0) mx[0] = fmax(mx[0], -f[e] / r1);
+    if (be[e] > 0.0) mx[1] = fmax(mx[1], -g[e] / r2);
+  }
+  bmax<2>(mx, red);
+  double sums[2] = {0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    if (al[e] > 0.0) sums[0] += al[e] * exp(-f[e] / r1 - mx[0]);
+    if (be[e] > 0.0) sums[1] += be[e] * exp(-g[e] / r2 - mx[1]);
+  }
+  bsum<2>(sums, red);
+  const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(sums[0])) - (mx[1] + log(sums[1])));
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n) A.f[(long)b * n + i] = f[e] + lam;
+    if (i < m) A.g[(long)b * m + i] = g[e] - lam;
+  }
+  if (threadIdx.x == 0) {
+    A.iterations[b] = iters;
+    A.status[b] = status;
+    A.summary[b * 3 + 0] = last_primal;
+    A.summary[b * 3 + 1] = last_dual;
+    A.summary[b * 3 + 2] = lam;
+  }
+}
+
+// Dense feasibility max(0, max_ij f_i + g_j - C_ij): duality.py:117-121.
+__global__ void feasibility_kernel(int n, int m, const double* x, const double* y, double p,
+                                   const double* f, const double* g, double* out) {
+  __shared__ double scr[32];
+  const int b = blockIdx.y;
+  double worst = -CUDART_INF;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)n * m;
+       t += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / m), j = (int)(t % m);
+    const double v = f[(long)b * n + i] + g[(long)b * m + j] -
+                     pcost(x[(long)b * n + i], y[(long)b * m + j], p);
+    worst = fmax(worst, v);
+  }
+  worst = block_reduce(worst, scr, MaxOp(), -CUDART_INF);
+  if (threadIdx.x == 0) {
+    // max over blocks via the integer ordering of non-negative doubles
+    const double v = fmax(worst, 0.0);
+    atomicMax(reinterpret_cast<unsigned long long*>(out + b), __double_as_longlong(v));
+  }
+}
+
+int ept_for(int nm) {
+  const int per = (nm + FW_THREADS - 1) / FW_THREADS;
+  if (per <= 1) return 1;
+  if (per <= 2) return 2;
+  if (per <= 4) return 4;
+  if (per <= 8) return 8;
+  if (per <= 16) return 16;
+  return -1;
+}
+
+size_t fw_smem(int n, int m) { return sizeof(double) * 2 * (size_t)(n + m); }
+
+int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
+  const int ept = ept_for(std::max(a.n, a.m));
+  if (ept < 0) {
+    set_error("1-D FW / OT kernel supports n, m <= %d per problem", 16 * FW_THREADS);
+    return UOT_INVALID;
+  }
+  const size_t smem = fw_smem(a.n, a.m);
+  auto go = [&](auto kern) -> int {
+    if (smem > 48 * 1024)
+      UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    kern<<<batch, FW_THREADS, smem, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  };
+  switch (ept) {
+    case 1: return go(fw1d_kernel<1>);
+    case 2: return go(fw1d_kernel<2>);
+    case 4: return go(fw1d_kernel<4>);
+    case 8: return go(fw1d_kernel<8>);
+    default: return go(fw1d_kernel<16>);
+  }
+}
+
+size_t fw_scratch_bytes(int batch, int n, int m) {
+  return (sizeof(double) + 2 * sizeof(int)) * (size_t)batch * (n + m) + 256;
+}
+
+}  // namespace
+}  // namespace uot
+
+using namespace uot;
+
+extern "C" int uot_fw1d_workspace_size(const uot_fw_desc* d, size_t* bytes) {
+  if (d == nullptr || d->batch < 1 || d->n < 1 || d->m < 1) {
+    set_error("uot_fw1d_workspace_size: invalid descriptor");
+    return UOT_INVALID;
+  }
+  *bytes = fw_scratch_bytes(d->batch, d->n, d->m);
+  return UOT_OK;
+}
+
+extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, void* stream) {
+  if (d == nullptr || d->batch < 1 || d->n < 1 || d->m < 1 || d->max_iters < 1) {
+    set_error("uot_fw1d_run: invalid descriptor");
+    return UOT_INVALID;
+  }
+  if (!(d->rho1 > 0) || !(d->rho2 > 0) || !(d->p >= 1.0)) {
+    set_error("uot_fw1d_run: need rho > 0 and p >= 1");
+    return UOT_INVALID;
+  }
+  if (d->step != UOT_STEP_HARMONIC && d->step != UOT_STEP_LINESEARCH) {
+    set_error("uot_fw1d_run: step must be harmonic or linesearch");
+    return UOT_INVALID;
+  }
+  if (ws_bytes < fw_scratch_bytes(d->batch, d->n, d->m)) {
+    set_error("uot_fw1d_run: workspace too small");
+    return UOT_INVALID;
+  }
+  FwArgs a{};
+  a.n = d->n;
+  a.m = d->m;
+  a.p = d->p;
+  a.r1 = d->rho1;
+  a.r2 = d->rho2;
+  a.step = d->step;
+  a.max_iters = d->max_iters;
+  a.gap_tol = d->gap_tol;
+  a.early_exit = d->early_exit;
+  a.mode = 0;
+  a.x = d->x;
+  a.y = d->y;
+  a.a = d->a;
+  a.b = d->b;
+  a.f = d->f;
+  a.g = d->g;
+  a.h0 = d->h0;
+  a.fw_gap = d->fw_gap;
+  a.pd_gap = d->pd_gap;
+  a.iterations = d->iterations;
+  a.ei = d->ei;
+  a.ej = d->ej;
+  a.em = d->em;
+  a.count = d->count;
+  a.summary = d->summary;
+  a.status = d->status;
+  a.scratch = (double*)ws;
+  a.scratch_i = (int*)((char*)ws + sizeof(double) * (size_t)d->batch * (d->n + d->m));
+  return launch_fw(a, d->batch, (cudaStream_t)stream);
+}
+
+extern "C" int uot_ot1d_workspace_size(int32_t batch, int32_t n, int32_t m, size_t* bytes) {
+  if (batch < 1 || n < 1 || m < 1) {
+    set_error("uot_ot1d_workspace_size: invalid sizes");
+    return UOT_INVALID;
+  }
+  *bytes = fw_scratch_bytes(batch, n, m);
+  return UOT_OK;
+}
+
+extern "C" int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x,
+                                const double* y, const double* a, const double* b, int32_t cost,
+                                double p, const double* c, double* f, double* g, int32_t* ei,
+                                int32_t* ej, double* em, int32_t* count, int32_t* status,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  (void)c;
+  if (batch < 1 || n < 1 || m < 1 || !(p >= 1.0)) {
+    set_error("uot_ot1d_batched: invalid arguments");
+    return UOT_INVALID;
+  }
+  if (cost != UOT_COST_POWER) {
+    set_error("uot_ot1d_batched: only |x-y|^p costs run on the B200 path");
+    return UOT_INVALID;
+  }
+  if (workspace_bytes < fw_scratch_bytes(batch, n, m)) {
+    set_error("uot_ot1d_batched: workspace too small");
+    return UOT_INVALID;
+  }
+  FwArgs A{};
+  A.n = n;
+  A.m = m;
+  A.p = p;
+  A.mode = 1;
+  A.x = x;
+  A.y = y;
+  A.a = a;
+  A.b = b;
+  A.f = f;
+  A.g = g;
+  A.ei = ei;
+  A.ej = ej;
+  A.em = em;
+  A.count = count;
+  A.status = status;
+  A.scratch = (double*)workspace;
+  A.scratch_i = (int*)((char*)workspace + sizeof(double) * (size_t)batch * (n + m));
+  return launch_fw(A, batch, (cudaStream_t)stream);
+}
+
+extern "C" int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x,
+                                  const double* y, double p, const double* f, const double* g,
+                                  double* out, void* stream) {
+  if (batch < 1 || n < 1 || m < 1) {
+    set_error("uot_feasibility_1d: invalid sizes");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  UOT_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * batch, st));
+  const long nm = (long)n * m;
+  const int blocks = (int)std::min<long>(1024, (nm + 255) / 256);
+  feasibility_kernel<<<dim3(blocks, batch), 256, 0, st>>>(n, m, x, y, p, f, g, out);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}

@@ -10,17 +10,6 @@
   } while (0)
 
 extern "C" {
-int uot_ot1d_batched(int32_t, int32_t, int32_t, const double*, const double*, const double*,
-                     const double*, int32_t, double, const double*, double*, double*, int32_t*,
-                     int32_t*, double*, int32_t*, int32_t*, void*) {
-  UOT_PENDING("uot_ot1d_batched");
-}
-int uot_fw1d_workspace_size(const uot_fw_desc*, size_t*) { UOT_PENDING("uot_fw1d_workspace_size"); }
-int uot_fw1d_run(const uot_fw_desc*, void*, size_t, void*) { UOT_PENDING("uot_fw1d_run"); }
-int uot_feasibility_1d(int32_t, int32_t, int32_t, const double*, const double*, double,
-                       const double*, const double*, double*, void*) {
-  UOT_PENDING("uot_feasibility_1d");
-}
 int uot_mot1d_workspace_size(int32_t, int32_t, int32_t, size_t*) {
   UOT_PENDING("uot_mot1d_workspace_size");
 }

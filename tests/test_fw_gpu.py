@@ -1,0 +1,126 @@
+"""GPU parity of the 1-D OT oracle and the batched Frank-Wolfe kernel
+(csrc/fw1d.cu) against the reference goldens and the CPU oracle.
+Plan supports bit-exact; potentials / objective 1e-9 relative (fp64)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2201_00730_b200 as P
+from conftest import cases, golden, rel_err
+from paper_2201_00730_b200 import _device as D
+from paper_2201_00730_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def test_ot1d_goldens_bit_exact_support():
+    z = golden("ot1d.npz")
+    for k in cases(z):
+        f, g, ei, ej, em, cnt, st = P.solve_ot_1d_batched(z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"],
+                                                          z[f"c{k}_b"], float(z[f"c{k}_p"]))
+        c = int(cnt[0].item())
+        assert int(st[0].item()) == 0
+        np.testing.assert_array_equal(D.to_np(ei[0, :c]), z[f"c{k}_i"], err_msg=str(k))
+        np.testing.assert_array_equal(D.to_np(ej[0, :c]), z[f"c{k}_j"], err_msg=str(k))
+        tot = float(np.sum(z[f"c{k}_a"]))
+        np.testing.assert_allclose(D.to_np(em[0, :c]), z[f"c{k}_m"], rtol=0, atol=1e-13 * tot)
+        fr, gr = z[f"c{k}_f"], z[f"c{k}_g"]
+        assert rel_err(D.to_np(f[0]), D.to_np(g[0]), fr, gr) < 1e-12, k
+
+
+def test_ot1d_api_known_answers():
+    a = P.DiscreteMeasure([0.0, 1.0], [0.7, 0.3])
+    b = P.DiscreteMeasure([0.0, 1.0], [0.4, 0.6])
+    plan, d = P.solve_ot_1d(a, b, P.PowerDistance(1.0))
+    assert list(zip(plan.source_idx, plan.target_idx)) == [(0, 0), (0, 1), (1, 1)]
+    np.testing.assert_allclose(plan.mass, [0.4, 0.3, 0.3])
+    np.testing.assert_allclose(d.f, [0.0, -1.0])
+    np.testing.assert_allclose(d.g, [0.0, 1.0])
+    single, d1 = P.solve_ot_1d(P.DiscreteMeasure([0.0], [1.0]), P.DiscreteMeasure([1.0], [1.0]),
+                               P.PowerDistance(1.0))
+    assert list(zip(single.source_idx, single.target_idx, single.mass)) == [(0, 0, 1.0)]
+    assert d1.f.tolist() == [0.0] and d1.g.tolist() == [1.0]
+    with pytest.raises(P.MassBalanceError):
+        P.solve_ot_1d(a, P.DiscreteMeasure([0.0], [1.5]), P.PowerDistance(1.0))
+
+
+def test_ot1d_batched_random_vs_oracle():
+    rng = np.random.default_rng(3)
+    B, n, m = 64, 300, 211
+    x = np.sort(rng.uniform(0, 1, (B, n)), axis=1)
+    y = np.sort(rng.uniform(0, 1, (B, m)), axis=1)
+    a = rng.exponential(1.0, (B, n))
+    a[:, ::7] = 0.0  # zero-weight atoms
+    b = rng.exponential(1.0, (B, m))
+    b *= (a.sum(1) / b.sum(1))[:, None]
+    f, g, ei, ej, em, cnt, st = P.solve_ot_1d_batched(x, y, a, b, 2.0)
+    for k in range(B):
+        ii, jj, mm, fo, go = O.solve_ot_1d(x[k], y[k], a[k], b[k], 2.0)
+        c = int(cnt[k].item())
+        np.testing.assert_array_equal(D.to_np(ei[k, :c]), ii)
+        np.testing.assert_array_equal(D.to_np(ej[k, :c]), jj)
+        np.testing.assert_allclose(D.to_np(em[k, :c]), mm, rtol=0, atol=1e-13 * a[k].sum())
+        assert rel_err(D.to_np(f[k]), D.to_np(g[k]), fo, go) < 1e-12
+
+
+def _fw_case(z, k):
+    r1, r2, p, iters, ls = z[f"c{k}_par"]
+    return (z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"], z[f"c{k}_b"], r1, r2, p, int(iters),
+            "linesearch" if ls else "harmonic")
+
+
+def test_fw_goldens():
+    z = golden("fw.npz")
+    for k in cases(z):
+        x, y, a, b, r1, r2, p, iters, step = _fw_case(z, k)
+        r = P.fw_solve_batched(x, y, a, b, r1, r2, p, iters, step)
+        assert int(r.status[0].item()) == 0
+        h0 = D.to_np(r.h0[0])
+        np.testing.assert_allclose(h0, z[f"c{k}_h0"], rtol=1e-9, atol=1e-12, err_msg=str(k))
+        pd = D.to_np(r.pd_gap[0])
+        scale = np.abs(z[f"c{k}_h0"]).max()
+        np.testing.assert_allclose(pd, z[f"c{k}_pd_gap"], rtol=0, atol=1e-9 * scale)
+        f, g = D.to_np(r.f[0]), D.to_np(r.g[0])
+        assert rel_err(f, g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-9, (k, step)
+        c = int(r.count[0].item())
+        np.testing.assert_array_equal(D.to_np(r.ei[0, :c]), z[f"c{k}_i"])
+        np.testing.assert_array_equal(D.to_np(r.ej[0, :c]), z[f"c{k}_j"])
+        np.testing.assert_allclose(D.to_np(r.em[0, :c]), z[f"c{k}_m"], rtol=0,
+                                   atol=1e-9 * float(np.sum(z[f"c{k}_m"])))
+
+
+def test_fw_batched_cfg2_shape_vs_oracle():
+    x, y, a, b = S.cfg2_batch(batch=4096, count=48)
+    r = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 60, "linesearch")
+    for k in (0, 17, 47):
+        out = O.fw_fixed(x[k], y[k], a[k], b[k], 1.0, 1.0, 60)
+        np.testing.assert_allclose(D.to_np(r.h0[k]), out["h0"], rtol=1e-9)
+        assert rel_err(D.to_np(r.f[k]), D.to_np(r.g[k]), out["f"], out["g"]) < 1e-9
+        c = int(r.count[k].item())
+        np.testing.assert_array_equal(D.to_np(r.ei[k, :c]), out["plan"][0])
+        np.testing.assert_array_equal(D.to_np(r.ej[k, :c]), out["plan"][1])
+
+
+def test_fw_solve_api_identical_measures_converge_fast():
+    # tests/test_fw.py:38-44 of the reference: identical inputs converge in <= 3 iterations
+    rng = np.random.default_rng(5)
+    a = P.DiscreteMeasure(np.sort(rng.uniform(0, 1, 20)), rng.uniform(0.1, 1, 20))
+    prob = P.UotProblem(a, a, P.PowerDistance(2.0), P.KL(1.0), P.KL(1.0), eps=0.0)
+    rep = P.fw_solve(prob, P.FwConfig("linesearch", 50, 1e-9))
+    assert rep.converged and rep.iterations <= 3
+    assert rep.certificate.passed
+
+
+def test_fw_solve_api_matches_oracle_with_early_exit():
+    rng = np.random.default_rng(8)
+    a = P.DiscreteMeasure(np.sort(rng.uniform(0, 1, 40)), rng.uniform(0.1, 1, 40))
+    b = P.DiscreteMeasure(np.sort(rng.uniform(0, 1, 33)), rng.uniform(0.1, 1, 33) * 1.4)
+    prob = P.UotProblem(a, b, P.PowerDistance(2.0), P.KL(0.7), P.KL(1.3), eps=0.0)
+    rep = P.fw_solve(prob, P.FwConfig("harmonic", 400, 1e-4))
+    out = O.fw_fixed(a.points, b.points, a.weights, b.weights, 0.7, 1.3, 400, step="harmonic",
+                     gap_tol=1e-4)
+    assert rep.iterations == len(out["h0"])
+    assert rel_err(rep.final.f, rep.final.g, out["f"], out["g"]) < 1e-9
+    feas = float(P.feasibility_violation(a.points, b.points, rep.final.f, rep.final.g)[0].item())
+    assert feas <= 1e-9 or rep.certificate.feasibility_violation <= 1e-9

@@ -64,14 +64,32 @@ def test_point_clouds_fp64(name):
     assert rel_err(f[0], g[0], z["f"], z["g"]) < 1e-9
 
 
+def translated(a, b, f, g, r1, r2):
+    """Canonical representative (f + t*, g - t*) of the H-iterate.  H is
+    exactly invariant along (f + c, g - c) (src/duality.py:256-276), so the
+    H-Sinkhorn iterate's translation is a neutral direction in which fp32
+    rounding bias accumulates linearly (measured: -5e-6 after 300 iterations
+    at cfg4 with eps = 0.05; scripts/exp_fp32_cfg4.py); parity in fp32 is
+    therefore stated on the translated pair and on the (translation
+    invariant) dual objective."""
+    lam = O.lambda_star_kl(a, b, f, g, r1, r2)
+    return f + lam, g - lam
+
+
 @pytest.mark.parametrize("name", ["cfg3_small.npz", "cfg4_small.npz"])
 def test_point_clouds_fp32_tolerance(name):
     z = golden(name)
-    eps = float(z["eps"])
+    eps, rho = float(z["eps"]), float(z["rho"])
     f, g, _, _ = run_dev(z["x"][None], z["y"][None], z["alpha"][None], z["beta"][None], eps,
-                         float(z["rho"]), int(z["iters"]), precision="fp32")
-    assert np.abs(f[0] - z["f"]).max() <= 1e-4 * eps
-    assert np.abs(g[0] - z["g"]).max() <= 1e-4 * eps
+                         rho, int(z["iters"]), precision="fp32")
+    ft, gt = translated(z["alpha"], z["beta"], f[0], g[0], rho, rho)
+    fr, gr = translated(z["alpha"], z["beta"], z["f"], z["g"], rho, rho)
+    assert np.abs(ft - fr).max() <= 1e-4 * eps
+    assert np.abs(gt - gr).max() <= 1e-4 * eps
+    cost = O.PointCost(z["x"], z["y"])
+    H = O.eval_h_kl(z["alpha"], z["beta"], f[0], g[0], rho, rho, eps,
+                    smin_fn=lambda ff, e: cost.smin_cols(ff, e, z["alpha"]))
+    assert abs(H - float(z["dual"])) <= 1e-4 * eps
 
 
 def test_batched_equals_individual():
@@ -88,8 +106,10 @@ def test_cfg3_shape_fp32_vs_oracle_2048():
                          precision="fp32")
     cost = O.PointCost(c.x, c.y)
     fo, go, _ = O.sinkhorn_fixed(cost, c.alpha, c.beta, c.eps, c.rho, c.rho, "h", 200)
-    assert np.abs(f[0] - fo).max() <= 1e-4 * c.eps
-    assert np.abs(g[0] - go).max() <= 1e-4 * c.eps
+    ft, gt = translated(c.alpha, c.beta, f[0], g[0], c.rho, c.rho)
+    fr, gr = translated(c.alpha, c.beta, fo, go, c.rho, c.rho)
+    assert np.abs(ft - fr).max() <= 1e-4 * c.eps
+    assert np.abs(gt - gr).max() <= 1e-4 * c.eps
 
 
 def test_full_cfg3_one_step_sampled_columns():
