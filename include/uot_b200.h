@@ -170,6 +170,7 @@ typedef struct uot_fw_desc {
   int32_t* count;
   double* summary;
   int32_t* status;
+  double* step_size; /* optional [batch][max_iters]: gamma of each iteration */
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);

@@ -53,6 +53,7 @@ struct FwArgs {
   int* count;
   double* summary;
   int* status;
+  double* step_size;
   double* scratch;  // [batch][n+m] doubles + [batch][n+m][2] ints (plan extraction)
   int* scratch_i;
 };
@@ -159,6 +160,25 @@ __device__ __forceinline__ int ibsum(int v, int* scratch) {
   return s;
 }
 
+// Exclusive block max-scan of one int per thread (identity -1).
+__device__ __forceinline__ int excl_max_scan(int v, int* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, t);
+  }
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = -1;
+  __syncthreads();
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) excl = max(excl, scratch[w]);
+  __syncthreads();
+  return excl;
+}
+
 // #{ l in [0, len) : arr[l] < v }  (strict) or <= v (non-strict)
 template <bool STRICT>
 __device__ __forceinline__ int count_below(const double* arr, int len, double v) {
@@ -213,6 +233,36 @@ struct Cta {
     }
     mass_a = totals[0];
     mass_b = totals[1];
+    // A zero-weight atom must repeat its predecessor's breakpoint bit for bit
+    // (the reference emits no entry for it, ot1d.py:149-153), but the block
+    // scan associates differently across thread boundaries.  Re-point such
+    // atoms at the last positive-weight breakpoint before them.
+    int lza = -1, lzb = -1;  // last index with positive weight, within the thread
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      if (i < n && ta[e] > 0.0) lza = i;
+      if (i < m && tb[e] > 0.0) lzb = i;
+    }
+    int pra = excl_max_scan(lza, reinterpret_cast<int*>(red));
+    int prb = excl_max_scan(lzb, reinterpret_cast<int*>(red));
+    __syncthreads();
+    double fa[EPT], fb[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      fa[e] = (i < n && ta[e] == 0.0) ? (pra >= 0 ? sA[pra] : 0.0) : -1.0;
+      fb[e] = (i < m && tb[e] == 0.0) ? (prb >= 0 ? sB[prb] : 0.0) : -1.0;
+      if (i < n && ta[e] > 0.0) pra = i;
+      if (i < m && tb[e] > 0.0) prb = i;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      if (fa[e] >= 0.0) sA[i] = fa[e];
+      if (fb[e] >= 0.0) sB[i] = fb[e];
+    }
     __syncthreads();
     // cost increments along the staircase
     double da[EPT], db[EPT];
@@ -465,11 +515,15 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
     if (A.step == UOT_STEP_HARMONIC) {
       gam = 2.0 / (2.0 + t);  // fw.py:223-224
     } else {
-      // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
-      const double ea1 = acc[5] / mta, ea2 = acc[6] / mta;
-      const double eb1 = acc[7] / mtb, eb2 = acc[8] / mtb;
-      double d1 = -t1 * ea1 - t2 * eb1;
-      double d2 = t1 * (ea2 - ea1 * ea1) + t2 * (eb2 - eb1 * eb1);
+      // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb).
+      // The FW direction carries a translation component (f + c, g - c) that
+      // phi ignores exactly (H is translation invariant), so the raw moments
+      // of va and vb nearly cancel; moments are taken about the gamma = 0
+      // means (ca, cb) and the constant part of phi' is kept separately.
+      const double ca = acc[5] / mta, cb = acc[7] / mtb;
+      const double k0 = -(t1 * ca + t2 * cb);  // phi'(0)
+      const double d2 = t1 * fmax(acc[6] / mta - ca * ca, 0.0) +
+                        t2 * fmax(acc[8] / mtb - cb * cb, 0.0);  // starting curvature
       // shift bounds for the passes: max(u - gamma va) <= (1-gamma) max u + gamma max(-r/r1)
       double mr[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
@@ -478,13 +532,13 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
         if (be[e] > 0.0) mr[1] = fmax(mr[1], -s[e] / r2);
       }
       bmax<2>(mr, red);
-      if (!(d1 < 0.0)) {
+      if (!(k0 < 0.0)) {
         gam = 0.0;
       } else {
         double lo = 0.0, hi = 1.0;
-        gam = (d2 > 0.0) ? fmin(1.0, -d1 / d2) : 1.0;
-        for (int it = 0; it < 40; ++it) {
-          // one pass: moments of va / vb under p_gamma, q_gamma
+        gam = (d2 > 0.0) ? fmin(1.0, -k0 / d2) : 1.0;
+        for (int it = 0; it < 60; ++it) {
+          // one pass: centred moments of va / vb under p_gamma, q_gamma
           const double sha = (1.0 - gam) * mx[0] + gam * mr[0];
           const double shb = (1.0 - gam) * mx[1] + gam * mr[1];
           double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -493,17 +547,18 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
             const double va = (r[e] - f[e]) / r1, vb = (s[e] - g[e]) / r2;
             const double wa = al[e] > 0.0 ? al[e] * exp(ua[e] - gam * va - sha) : 0.0;
             const double wb = be[e] > 0.0 ? be[e] * exp(ub[e] - gam * vb - shb) : 0.0;
+            const double xa = va - ca, xb = vb - cb;
             mom[0] += wa;
-            mom[1] += wa * va;
-            mom[2] += wa * va * va;
+            mom[1] += wa * xa;
+            mom[2] += wa * xa * xa;
             mom[3] += wb;
-            mom[4] += wb * vb;
-            mom[5] += wb * vb * vb;
+            mom[4] += wb * xb;
+            mom[5] += wb * xb * xb;
           }
           bsum<6>(mom, red);
           const double a1 = mom[1] / mom[0], a2 = mom[2] / mom[0];
           const double b1 = mom[4] / mom[3], b2 = mom[5] / mom[3];
-          const double g1 = -t1 * a1 - t2 * b1;
+          const double g1 = k0 - t1 * a1 - t2 * b1;
           const double g2 = t1 * (a2 - a1 * a1) + t2 * (b2 - b1 * b1);
           if (g1 < 0.0)
             lo = gam;
@@ -522,6 +577,7 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
         }
       }
     }
+    if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
     // --- update (fw.py:227-230)
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
@@ -679,6 +735,7 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.count = d->count;
   a.summary = d->summary;
   a.status = d->status;
+  a.step_size = d->step_size;
   a.scratch = (double*)ws;
   a.scratch_i = (int*)((char*)ws + sizeof(double) * (size_t)d->batch * (d->n + d->m));
   return launch_fw(a, d->batch, (cudaStream_t)stream);

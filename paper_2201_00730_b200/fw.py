@@ -60,6 +60,7 @@ class FwBatchResult:
     count: object
     summary: object
     status: object
+    step_size: object
 
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
@@ -85,7 +86,8 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         pd_gap=D.empty((B, max_iters), t.float64), iterations=D.empty((B,), t.int32),
         ei=D.empty((B, n + m - 1), t.int32), ej=D.empty((B, n + m - 1), t.int32),
         em=D.empty((B, n + m - 1), t.float64), count=D.empty((B,), t.int32),
-        summary=D.empty((B, 3), t.float64), status=D.empty((B,), t.int32))
+        summary=D.empty((B, 3), t.float64), status=D.empty((B,), t.int32),
+        step_size=t.zeros((B, max_iters), dtype=t.float64, device=x.device))
     desc = _lib.FwDesc(
         batch=B, n=n, m=m, p=float(p), rho1=float(rho1), rho2=float(rho2),
         step=_lib.STEP_LINESEARCH if step == "linesearch" else _lib.STEP_HARMONIC,
@@ -94,7 +96,7 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         h0=_lib.ptr(r.h0), fw_gap=_lib.ptr(r.fw_gap), pd_gap=_lib.ptr(r.pd_gap),
         iterations=_lib.ptr(r.iterations), ei=_lib.ptr(r.ei), ej=_lib.ptr(r.ej),
         em=_lib.ptr(r.em), count=_lib.ptr(r.count), summary=_lib.ptr(r.summary),
-        status=_lib.ptr(r.status))
+        status=_lib.ptr(r.status), step_size=_lib.ptr(r.step_size))
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)
