@@ -27,6 +27,9 @@ namespace uot {
 namespace {
 
 constexpr int FW_THREADS = 256;
+#ifndef FW_MINB
+#define FW_MINB 2
+#endif
 
 struct FwArgs {
   int n, m;
@@ -57,6 +60,34 @@ struct FwArgs {
   double* scratch;  // [batch][n+m] doubles + [batch][n+m][2] ints (plan extraction)
   int* scratch_i;
 };
+
+// exp(x) for x <= 0 (arguments are shifted by their maximum): Cody-Waite
+// reduction by ln 2 and a degree-13 Taylor polynomial on |r| <= ln2/2
+// (truncation < 0.05 ulp); results below 2^-1022 flush to 0 (they are
+// negligible next to the unit maximum term).  ~20 instructions versus the
+// libdevice routine's special-case handling.
+__device__ __forceinline__ double exp_nonpos(double x) {
+  if (x < -708.0) return 0.0;
+  const double n = rint(x * 1.4426950408889634074);
+  double r = fma(n, -6.93147180369123816490e-01, x);
+  r = fma(n, -1.90821492927058770002e-10, r);
+  double q = 1.6059043836821614599e-10;  // 1/13!
+  q = fma(q, r, 2.0876756987868098979e-09);
+  q = fma(q, r, 2.5052108385441718775e-08);
+  q = fma(q, r, 2.7557319223985890653e-07);
+  q = fma(q, r, 2.7557319223985890653e-06);
+  q = fma(q, r, 2.4801587301587301587e-05);
+  q = fma(q, r, 1.9841269841269841270e-04);
+  q = fma(q, r, 1.3888888888888888889e-03);
+  q = fma(q, r, 8.3333333333333333333e-03);
+  q = fma(q, r, 4.1666666666666666667e-02);
+  q = fma(q, r, 1.6666666666666666667e-01);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const long long e = (long long)((int)n + 1023) << 52;
+  return q * __longlong_as_double(e);
+}
 
 __device__ __forceinline__ double pcost(double xi, double yj, double p) {
   const double d = xi - yj;
@@ -194,26 +225,97 @@ __device__ __forceinline__ int count_below(const double* arr, int len, double v)
   return lo;
 }
 
-// Per-problem CTA state.  Thread t owns source/target elements
-// t*EPT .. t*EPT+EPT-1 of each side.
+// Block reduction of KS sums and KM maxima in one pass.  scratch: (KS+KM)*32.
+template <int KS, int KM>
+__device__ __forceinline__ void bred(double (&sv)[KS], double (&mv)[KM], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < KS; ++k) sv[k] = warp_sum(sv[k]);
+#pragma unroll
+  for (int k = 0; k < KM; ++k) mv[k] = warp_max(mv[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < KS; ++k) scratch[k * 32 + warp] = sv[k];
+#pragma unroll
+    for (int k = 0; k < KM; ++k) scratch[(KS + k) * 32 + warp] = mv[k];
+  }
+  __syncthreads();
+  constexpr int NW = FW_THREADS / 32;
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += scratch[k * 32 + w];
+    sv[k] = t;
+  }
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    double t = -CUDART_INF;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t = fmax(t, scratch[(KS + k) * 32 + w]);
+    mv[k] = t;
+  }
+  __syncthreads();
+}
+
+// Two (max, sum) log-sum-exp pairs reduced over the block in one pass.
+__device__ __forceinline__ void block_lse2(LsePair& a, LsePair& b, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_lse(a);
+  b = warp_lse(b);
+  __syncthreads();
+  if (lane == 0) {
+    scratch[warp] = a.m;
+    scratch[32 + warp] = a.s;
+    scratch[64 + warp] = b.m;
+    scratch[96 + warp] = b.s;
+  }
+  __syncthreads();
+  LsePair ra{-CUDART_INF, 0.0}, rb{-CUDART_INF, 0.0};
+  for (int w = 0; w < FW_THREADS / 32; ++w) {
+    ra = lse_merge(ra, LsePair{scratch[w], scratch[32 + w]});
+    rb = lse_merge(rb, LsePair{scratch[64 + w], scratch[96 + w]});
+  }
+  a = ra;
+  b = rb;
+  __syncthreads();
+}
+
+// Galloping search: first index in [j, len) with !(arr[idx] < v) (STRICT) or
+// !(arr[idx] <= v), starting from a known lower bound j.
+template <bool STRICT>
+__device__ __forceinline__ int advance_below(const double* arr, int len, int j, double v) {
+#pragma unroll 1
+  for (int step = 0; step < 6; ++step) {
+    if (j >= len) return len;
+    const bool below = STRICT ? (arr[j] < v) : (arr[j] <= v);
+    if (!below) return j;
+    ++j;
+  }
+  return j + count_below<STRICT>(arr + j, len - j, v);
+}
+
+// Per-problem CTA.  Thread t owns source/target elements t*EPT .. t*EPT+EPT-1
+// of each side.  Shared memory holds the supports, the constant weights, the
+// breakpoints and the tilted weights; registers hold the potentials.
 template <int EPT>
 struct Cta {
   int n, m;
   double p;
-  const double* sx;  // smem copies of the supports
+  const double* sx;
   const double* sy;
-  double* sA;        // smem cumulative masses (breakpoints)
+  double* sA;
   double* sB;
-  double* red;       // reduction scratch (>= 16*32 doubles)
+  double* red;
+  bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
 
   __device__ int src(int e) const { return threadIdx.x * EPT + e; }
 
-  // Balanced 1-D OT oracle on (ta, tb) (masses assumed equal to 1e-9):
-  // cumulative masses -> partner searches -> dual potentials (r, s).
-  // Leaves sA/sB holding the breakpoints for plan extraction.
+  // Balanced 1-D OT oracle on (ta, tb): cumulative masses -> partner searches
+  // -> dual potentials (r, s).  Leaves sA/sB holding the breakpoints.
   __device__ void oracle(const double (&ta)[EPT], const double (&tb)[EPT], double (&r)[EPT],
                          double (&s)[EPT], double& mass_a, double& mass_b) {
-    // inclusive prefix sums of the tilted masses
     double pa[EPT], pb[EPT];
     double ca = 0.0, cb = 0.0;
 #pragma unroll
@@ -233,54 +335,62 @@ struct Cta {
     }
     mass_a = totals[0];
     mass_b = totals[1];
-    // A zero-weight atom must repeat its predecessor's breakpoint bit for bit
-    // (the reference emits no entry for it, ot1d.py:149-153), but the block
-    // scan associates differently across thread boundaries.  Re-point such
-    // atoms at the last positive-weight breakpoint before them.
-    int lza = -1, lzb = -1;  // last index with positive weight, within the thread
+    if (zeros) {
+      // A zero-weight atom must repeat its predecessor's breakpoint bit for
+      // bit (the reference emits no entry for it, ot1d.py:149-153), but the
+      // block scan associates differently across thread boundaries.
+      int lza = -1, lzb = -1;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = src(e);
-      if (i < n && ta[e] > 0.0) lza = i;
-      if (i < m && tb[e] > 0.0) lzb = i;
-    }
-    int pra = excl_max_scan(lza, reinterpret_cast<int*>(red));
-    int prb = excl_max_scan(lzb, reinterpret_cast<int*>(red));
-    __syncthreads();
-    double fa[EPT], fb[EPT];
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        if (i < n && ta[e] > 0.0) lza = i;
+        if (i < m && tb[e] > 0.0) lzb = i;
+      }
+      int pra = excl_max_scan(lza, reinterpret_cast<int*>(red));
+      int prb = excl_max_scan(lzb, reinterpret_cast<int*>(red));
+      __syncthreads();
+      double fa[EPT], fb[EPT];
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = src(e);
-      fa[e] = (i < n && ta[e] == 0.0) ? (pra >= 0 ? sA[pra] : 0.0) : -1.0;
-      fb[e] = (i < m && tb[e] == 0.0) ? (prb >= 0 ? sB[prb] : 0.0) : -1.0;
-      if (i < n && ta[e] > 0.0) pra = i;
-      if (i < m && tb[e] > 0.0) prb = i;
-    }
-    __syncthreads();
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        fa[e] = (i < n && ta[e] == 0.0) ? (pra >= 0 ? sA[pra] : 0.0) : -1.0;
+        fb[e] = (i < m && tb[e] == 0.0) ? (prb >= 0 ? sB[prb] : 0.0) : -1.0;
+        if (i < n && ta[e] > 0.0) pra = i;
+        if (i < m && tb[e] > 0.0) prb = i;
+      }
+      __syncthreads();
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = src(e);
-      if (fa[e] >= 0.0) sA[i] = fa[e];
-      if (fb[e] >= 0.0) sB[i] = fb[e];
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        if (fa[e] >= 0.0) sA[i] = fa[e];
+        if (fb[e] >= 0.0) sB[i] = fb[e];
+      }
     }
     __syncthreads();
-    // cost increments along the staircase
+    // cost increments along the staircase; partners of this thread's
+    // consecutive events are monotone, so search once and gallop.
     double da[EPT], db[EPT];
     double la = 0.0, lb = 0.0;
+    int j = 0, k = 0;
+    bool fj = true, fk = true;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
       da[e] = 0.0;
       db[e] = 0.0;
       if (i >= 1 && i < n) {
-        // source event k = i-1: partner j = #{l < m-1 : B_l < A_{i-1}}
-        const int j = count_below<true>(sB, m - 1, sA[i - 1]);
+        // source event i-1: partner j = #{l < m-1 : B_l < A_{i-1}}
+        const double v = sA[i - 1];
+        j = fj ? count_below<true>(sB, m - 1, v) : advance_below<true>(sB, m - 1, j, v);
+        fj = false;
         const double yj = sy[j];
         da[e] = pcost(sx[i], yj, p) - pcost(sx[i - 1], yj, p);
       }
       if (i >= 1 && i < m) {
-        // target event l = i-1: partner = #{k < n-1 : A_k <= B_{i-1}}
-        const int k = count_below<false>(sA, n - 1, sB[i - 1]);
+        // target event i-1: partner = #{k < n-1 : A_k <= B_{i-1}}
+        const double v = sB[i - 1];
+        k = fk ? count_below<false>(sA, n - 1, v) : advance_below<false>(sA, n - 1, k, v);
+        fk = false;
         const double xk = sx[k];
         db[e] = pcost(xk, sy[i], p) - pcost(xk, sy[i - 1], p);
       }
@@ -300,13 +410,11 @@ struct Cta {
     }
   }
 
-  // Plan of the breakpoints currently in sA/sB, compacted to entries with
-  // positive mass in sweep order (ot1d.py:149-153).  scratch: (n+m) doubles,
-  // scratch_i: 2*(n+m) ints, both per problem.
+  // Plan of the breakpoints in sA/sB, compacted to positive-mass entries in
+  // sweep order (ot1d.py:149-153).  vals: n+m doubles, codes: 2(n+m) ints.
   __device__ void extract_plan(double* vals, int* codes, int* ei, int* ej, double* em,
                                int* count, double total) {
     const int nev = (n - 1) + (m - 1);
-    // scatter events by merged rank
     for (int i = threadIdx.x; i < n - 1; i += FW_THREADS) {
       const double v = sA[i];
       const int j = count_below<true>(sB, m - 1, v);
@@ -324,7 +432,6 @@ struct Cta {
       codes[2 * rank + 1] = l + 1;
     }
     __syncthreads();
-    // state s (0..nev) follows event s-1; mass = bp(s) - bp(s-1)
     int base = 0;
     int* iscr = reinterpret_cast<int*>(red);
     for (int s0 = 0; s0 <= nev; s0 += FW_THREADS) {
@@ -341,7 +448,6 @@ struct Cta {
         }
       }
       const int keep = (s <= nev && mass > 0.0) ? 1 : 0;
-      // block exclusive scan of keep flags
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       int incl = keep;
 #pragma unroll
@@ -372,7 +478,7 @@ struct Cta {
 };
 
 template <int EPT>
-__global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
+__global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[16 * 32];
   const int b = blockIdx.x;
@@ -381,21 +487,32 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
   double* sy = sx + n;
   double* sA = sy + m;
   double* sB = sA + n;
-  Cta<EPT> c{n, m, A.p, sx, sy, sA, sB, red};
+  double* sal = sB + m;  // constant weights
+  double* sbe = sal + n;
+  Cta<EPT> c{n, m, A.p, sx, sy, sA, sB, red, false};
 
-  for (int i = threadIdx.x; i < n; i += FW_THREADS) sx[i] = A.x[(long)b * n + i];
-  for (int j = threadIdx.x; j < m; j += FW_THREADS) sy[j] = A.y[(long)b * m + j];
+  int nz = 0;
+  for (int i = threadIdx.x; i < n; i += FW_THREADS) {
+    sx[i] = A.x[(long)b * n + i];
+    const double w = A.a[(long)b * n + i];
+    sal[i] = w;
+    nz += (w == 0.0);
+  }
+  for (int j = threadIdx.x; j < m; j += FW_THREADS) {
+    sy[j] = A.y[(long)b * m + j];
+    const double w = A.b[(long)b * m + j];
+    sbe[j] = w;
+    nz += (w == 0.0);
+  }
+  c.zeros = ibsum(nz, reinterpret_cast<int*>(red)) > 0;  // (syncs: smem now visible)
 
-  double al[EPT], be[EPT], f[EPT], g[EPT];
+  double f[EPT], g[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
-    al[e] = i < n ? A.a[(long)b * n + i] : 0.0;
-    be[e] = i < m ? A.b[(long)b * m + i] : 0.0;
     f[e] = i < n ? A.f[(long)b * n + i] : 0.0;
     g[e] = i < m ? A.g[(long)b * m + i] : 0.0;
   }
-  __syncthreads();
   double* vals = A.scratch + (long)b * (n + m);
   int* codes = A.scratch_i + (long)b * 2 * (n + m);
   int* ei = A.ei + (long)b * (n + m - 1);
@@ -404,8 +521,14 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
 
   if (A.mode == 1) {
     // Plain balanced OT on (a, b): src/ot1d.py:112-172.
-    double r[EPT], s[EPT], ma, mb;
-    c.oracle(al, be, r, s, ma, mb);
+    double ta[EPT], tb[EPT], r[EPT], s[EPT], ma, mb;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      ta[e] = i < n ? sal[i] : 0.0;
+      tb[e] = i < m ? sbe[i] : 0.0;
+    }
+    c.oracle(ta, tb, r, s, ma, mb);
     const int bad = fabs(ma - mb) > 1e-9 * fmax(ma, mb);  // ot1d.py:133-136
     if (threadIdx.x == 0) A.status[b] = bad ? UOT_MASS_BALANCE : 0;
     if (bad) return;
@@ -420,51 +543,69 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
   }
 
   const double r1 = A.r1, r2 = A.r2;
+  const double i1 = 1.0 / r1, i2 = 1.0 / r2;
   const double t1 = r1 / (r1 + r2), t2 = r2 / (r1 + r2);
-  double mass[2] = {0.0, 0.0};
+  double malpha, mbeta;
+  {
+    double ms[2] = {0.0, 0.0}, mm0[1] = {0.0};
 #pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    mass[0] += al[e];
-    mass[1] += be[e];
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) ms[0] += sal[i];
+      if (i < m) ms[1] += sbe[i];
+    }
+    bred<2, 1>(ms, mm0, red);
+    malpha = ms[0];
+    mbeta = ms[1];
   }
-  bsum<2>(mass, red);
-  const double malpha = mass[0], mbeta = mass[1];
 
   int status = 0;
   int iters = 0;
   double last_primal = 0.0, last_dual = 0.0;
   for (int t = 0; t < A.max_iters; ++t) {
-    // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303)
-    double ua[EPT], ub[EPT];
-    double mx[2] = {-CUDART_INF, -CUDART_INF};
+    // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303).
+    // Thread-local (max, sum) pairs merged over the block in one pass; the
+    // exponentials are shared between the log-sum-exps and the tilt.
+    double ta[EPT], tb[EPT];
+    double mxa = -CUDART_INF, mxb = -CUDART_INF;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      ua[e] = al[e] > 0.0 ? -f[e] / r1 : -CUDART_INF;
-      ub[e] = be[e] > 0.0 ? -g[e] / r2 : -CUDART_INF;
-      mx[0] = fmax(mx[0], ua[e]);
-      mx[1] = fmax(mx[1], ub[e]);
+      const int i = c.src(e);
+      if (i < n && sal[i] > 0.0) mxa = fmax(mxa, -f[e] * i1);
+      if (i < m && sbe[i] > 0.0) mxb = fmax(mxb, -g[e] * i2);
     }
-    bmax<2>(mx, red);
-    double ea[EPT], eb[EPT];
-    double sums[2] = {0.0, 0.0};
+    {
+      double mxs[2] = {mxa, mxb};
+      bmax<2>(mxs, red);
+      mxa = mxs[0];
+      mxb = mxs[1];
+    }
+    LsePair pa{mxa, 0.0}, pb{mxb, 0.0};
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      ea[e] = exp(ua[e] - mx[0]);
-      eb[e] = exp(ub[e] - mx[1]);
-      sums[0] += al[e] * ea[e];
-      sums[1] += be[e] * eb[e];
+      const int i = c.src(e);
+      const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
+      ta[e] = wa > 0.0 ? wa * exp_nonpos(-f[e] * i1 - mxa) : 0.0;
+      tb[e] = wb > 0.0 ? wb * exp_nonpos(-g[e] * i2 - mxb) : 0.0;
+      pa.s += ta[e];
+      pb.s += tb[e];
     }
-    bsum<2>(sums, red);
-    const double la = mx[0] + log(sums[0]);
-    const double lb = mx[1] + log(sums[1]);
+    {
+      double sums[2] = {pa.s, pb.s};
+      bsum<2>(sums, red);
+      pa.s = sums[0];
+      pb.s = sums[1];
+    }
+    const double la = pa.m + log(pa.s);
+    const double lb = pb.m + log(pb.s);
     const double lam = (r1 * r2 / (r1 + r2)) * (la - lb);
     const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * exp(t1 * la + t2 * lb);
-    const double sca = exp(mx[0] - lam / r1), scb = exp(mx[1] + lam / r2);
-    double ta[EPT], tb[EPT];
+    const double sca = mxa > -CUDART_INF ? exp(mxa - lam / r1) : 0.0;
+    const double scb = mxb > -CUDART_INF ? exp(mxb + lam / r2) : 0.0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      ta[e] = al[e] * ea[e] * sca;
-      tb[e] = be[e] * eb[e] * scb;
+      ta[e] *= sca;
+      tb[e] *= scb;
     }
     // --- linear oracle (ot1d.py:112-172 on the tilted marginals, fw.py:159-173)
     double r[EPT], s[EPT], mta, mtb;
@@ -473,26 +614,32 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
       status = UOT_MASS_BALANCE;
       break;
     }
-    // --- gaps and line-search moments at gamma = 0
-    // log(ta/alpha) = u - lam/r1 exactly, so the KL terms of the oracle plan
-    // (whose marginals are ta, tb) need no logarithm (entropies.py:123-131).
-    double acc[9];
+    // --- gaps, primal and line-search moments at gamma = 0.  log(ta/alpha)
+    // = -(f + lam)/r1 exactly, so the KL terms of the oracle plan (whose
+    // marginals are ta, tb) need no logarithm (entropies.py:123-131).
+    double acc[9], mr[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      const double va = (r[e] - f[e]) / r1, vb = (s[e] - g[e]) / r2;
+      const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
       acc[0] += ta[e] * (r[e] - f[e]);
       acc[1] += tb[e] * (s[e] - g[e]);
       acc[2] += ta[e] * r[e] + tb[e] * s[e];
-      if (ta[e] > 0.0) acc[3] += ta[e] * (ua[e] - lam / r1);
-      if (tb[e] > 0.0) acc[4] += tb[e] * (ub[e] + lam / r2);
+      if (ta[e] > 0.0) {
+        acc[3] += ta[e] * ((-f[e] - lam) * i1);
+        mr[0] = fmax(mr[0], -r[e] * i1);
+      }
+      if (tb[e] > 0.0) {
+        acc[4] += tb[e] * ((-g[e] + lam) * i2);
+        mr[1] = fmax(mr[1], -s[e] * i2);
+      }
       acc[5] += ta[e] * va;
       acc[6] += ta[e] * va * va;
       acc[7] += tb[e] * vb;
       acc[8] += tb[e] * vb * vb;
     }
-    bsum<9>(acc, red);
+    bred<9, 2>(acc, mr, red);
     const double fw_gap = acc[0] + acc[1];
     const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
     const double primal = acc[2] + r1 * kl1 + r2 * kl2;
@@ -517,36 +664,31 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
     } else {
       // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb).
       // The FW direction carries a translation component (f + c, g - c) that
-      // phi ignores exactly (H is translation invariant), so the raw moments
-      // of va and vb nearly cancel; moments are taken about the gamma = 0
-      // means (ca, cb) and the constant part of phi' is kept separately.
+      // phi ignores exactly (H is translation invariant), so raw moments of
+      // va and vb nearly cancel; moments are taken about the gamma = 0 means
+      // (ca, cb) and the constant part of phi' is kept separately.
       const double ca = acc[5] / mta, cb = acc[7] / mtb;
       const double k0 = -(t1 * ca + t2 * cb);  // phi'(0)
       const double d2 = t1 * fmax(acc[6] / mta - ca * ca, 0.0) +
                         t2 * fmax(acc[8] / mtb - cb * cb, 0.0);  // starting curvature
-      // shift bounds for the passes: max(u - gamma va) <= (1-gamma) max u + gamma max(-r/r1)
-      double mr[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        if (al[e] > 0.0) mr[0] = fmax(mr[0], -r[e] / r1);
-        if (be[e] > 0.0) mr[1] = fmax(mr[1], -s[e] / r2);
-      }
-      bmax<2>(mr, red);
       if (!(k0 < 0.0)) {
         gam = 0.0;
       } else {
         double lo = 0.0, hi = 1.0;
         gam = (d2 > 0.0) ? fmin(1.0, -k0 / d2) : 1.0;
-        for (int it = 0; it < 60; ++it) {
-          // one pass: centred moments of va / vb under p_gamma, q_gamma
-          const double sha = (1.0 - gam) * mx[0] + gam * mr[0];
-          const double shb = (1.0 - gam) * mx[1] + gam * mr[1];
+        for (int it = 0; it < 24; ++it) {
+          // one pass: centred moments of va / vb under p_gamma, q_gamma; the
+          // shift (1-gamma) max(u) + gamma max(-r/r1) bounds every exponent.
+          const double sha = (1.0 - gam) * pa.m + gam * mr[0];
+          const double shb = (1.0 - gam) * pb.m + gam * mr[1];
           double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int e = 0; e < EPT; ++e) {
-            const double va = (r[e] - f[e]) / r1, vb = (s[e] - g[e]) / r2;
-            const double wa = al[e] > 0.0 ? al[e] * exp(ua[e] - gam * va - sha) : 0.0;
-            const double wb = be[e] > 0.0 ? be[e] * exp(ub[e] - gam * vb - shb) : 0.0;
+            const int i = c.src(e);
+            const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
+            const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
+            const double wa = wa0 > 0.0 ? wa0 * exp_nonpos(-f[e] * i1 - gam * va - sha) : 0.0;
+            const double wb = wb0 > 0.0 ? wb0 * exp_nonpos(-g[e] * i2 - gam * vb - shb) : 0.0;
             const double xa = va - ca, xb = vb - cb;
             mom[0] += wa;
             mom[1] += wa * xa;
@@ -569,9 +711,13 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
             break;
           }
           double nxt = (g2 > 0.0) ? gam - g1 / g2 : 0.5 * (lo + hi);
-          if (!(nxt > lo && nxt < hi)) nxt = 0.5 * (lo + hi);
-          const bool conv = fabs(nxt - gam) <= 1e-15 * fmax(1.0, gam) || g1 == 0.0 ||
-                            hi - lo <= 4e-16;
+          const bool newton = nxt > lo && nxt < hi;
+          if (!newton) nxt = 0.5 * (lo + hi);
+          // Newton converges quadratically: once a Newton step is below
+          // 1e-9 the next iterate is exact to rounding (the reference's
+          // ternary search resolves gamma to ~1e-5 on flat problems).
+          const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(1.0, gam)) ||
+                            g1 == 0.0 || hi - lo <= 1e-15;
           gam = nxt;
           if (conv) break;
         }
@@ -586,21 +732,22 @@ __global__ void __launch_bounds__(FW_THREADS) fw1d_kernel(FwArgs A) {
     }
   }
   // --- finalize: translate by lambda* (fw.py:235-252)
-  double mx[2] = {-CUDART_INF, -CUDART_INF};
+  double mxa = -CUDART_INF, mxb = -CUDART_INF;
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    if (al[e] > 0.0) mx[0] = fmax(mx[0], -f[e] / r1);
-    if (be[e] > 0.0) mx[1] = fmax(mx[1], -g[e] / r2);
+    const int i = c.src(e);
+    if (i < n && sal[i] > 0.0) mxa = fmax(mxa, -f[e] / r1);
+    if (i < m && sbe[i] > 0.0) mxb = fmax(mxb, -g[e] / r2);
   }
-  bmax<2>(mx, red);
-  double sums[2] = {0.0, 0.0};
+  LsePair pa{mxa, 0.0}, pb{mxb, 0.0};
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    if (al[e] > 0.0) sums[0] += al[e] * exp(-f[e] / r1 - mx[0]);
-    if (be[e] > 0.0) sums[1] += be[e] * exp(-g[e] / r2 - mx[1]);
+    const int i = c.src(e);
+    if (i < n && sal[i] > 0.0) pa.s += sal[i] * exp(-f[e] / r1 - mxa);
+    if (i < m && sbe[i] > 0.0) pb.s += sbe[i] * exp(-g[e] / r2 - mxb);
   }
-  bsum<2>(sums, red);
-  const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(sums[0])) - (mx[1] + log(sums[1])));
+  block_lse2(pa, pb, red);
+  const double lam = (r1 * r2 / (r1 + r2)) * ((pa.m + log(pa.s)) - (pb.m + log(pb.s)));
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
@@ -647,7 +794,7 @@ int ept_for(int nm) {
   return -1;
 }
 
-size_t fw_smem(int n, int m) { return sizeof(double) * 2 * (size_t)(n + m); }
+size_t fw_smem(int n, int m) { return sizeof(double) * 3 * (size_t)(n + m); }
 
 int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
   const int ept = ept_for(std::max(a.n, a.m));
@@ -657,9 +804,8 @@ int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
   }
   const size_t smem = fw_smem(a.n, a.m);
   auto go = [&](auto kern) -> int {
-    if (smem > 48 * 1024)
-      UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+    UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
     kern<<<batch, FW_THREADS, smem, st>>>(a);
     UOT_CHECK_LAUNCH();
     return UOT_OK;
