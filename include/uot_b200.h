@@ -185,14 +185,19 @@ int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, con
 /* ------------------------------------------------------------------------
  * Balanced K-marginal sweep (Algorithm 3) and the KL barycenter FW:
  * replace src/barycenter.py:169-233 `solve_mot_1d(inputs, w)` and
- * :330-430 `fw_barycenter(problem, config)` for a batch of problems with K
- * sorted inputs of equal length n (fp64).  x, a, f [batch][K][n]; omega
- * [K] barycentric weights.  Plans are returned as (tuple indices
- * [batch][E][K] int32, mass [batch][E]) with E <= K*(n-1)+1.
+ * :330-430 `fw_barycenter(problem, config)` (with _h_value :320-327,
+ * multimarginal_lambda :298-317, plan_cost :236-240, the final translation
+ * :413-414) for a batch of problems with K (2..16) sorted inputs, fp64.
+ * x, a, f [batch][K][n] (row stride n; list q holds lens[q] <= n atoms when
+ * the optional host array lens is given); omega [K] barycentric weights
+ * (host); rho_k = omega_k * rho (barycenter.py:81-84).  Plans come back as
+ * tuple indices [batch][K*(n-1)+1][K] int32 and masses [batch][K*(n-1)+1]
+ * with count [batch], positive-mass states only, in sweep order.
  * ------------------------------------------------------------------------ */
 typedef struct uot_bary_desc {
   int32_t batch, k, n;
   const double* omega;  /* host array [k] */
+  const int32_t* lens;  /* host array [k] or NULL (all lists have n atoms) */
   double rho;
   int32_t step;
   int32_t max_iters;
@@ -213,10 +218,11 @@ typedef struct uot_bary_desc {
 } uot_bary_desc;
 
 int uot_mot1d_workspace_size(int32_t batch, int32_t k, int32_t n, size_t* bytes);
-int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const double* x, const double* a,
-                      const double* omega_host, double* f, int32_t* idx, double* mass,
-                      int32_t* count, int32_t* status, void* workspace, size_t workspace_bytes,
-                      void* stream);
+/* f receives the sweep's dual potentials (barycenter.py:206-229). */
+int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const int32_t* lens, const double* x,
+                      const double* a, const double* omega_host, double* f, int32_t* idx,
+                      double* mass, int32_t* count, int32_t* status, void* workspace,
+                      size_t workspace_bytes, void* stream);
 int uot_bary_workspace_size(const uot_bary_desc* desc, size_t* bytes);
 int uot_bary_run(const uot_bary_desc* desc, void* workspace, size_t workspace_bytes,
                  void* stream);

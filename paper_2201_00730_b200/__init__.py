@@ -18,6 +18,17 @@ from .exceptions import (
     UotError,
 )
 from .measures import DiscreteMeasure, ExplicitMatrix, PowerDistance, SqEuclideanPoints
+from .barycenter import (
+    BarycenterProblem,
+    MultiDual,
+    MultiPlan,
+    extract_barycenter,
+    fw_barycenter,
+    fw_barycenter_batched,
+    multimarginal_cost,
+    solve_mot_1d,
+    solve_mot_1d_batched,
+)
 from .certify import Certificate, assemble_certificate
 from .fw import FwConfig, feasibility_violation, fw_solve, fw_solve_batched
 from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched

@@ -54,7 +54,7 @@ class FwDesc(ctypes.Structure):
 class BaryDesc(ctypes.Structure):
     _fields_ = [
         ("batch", _i32), ("k", _i32), ("n", _i32),
-        ("omega", _vp), ("rho", _f64),
+        ("omega", _vp), ("lens", _vp), ("rho", _f64),
         ("step", _i32), ("max_iters", _i32), ("gap_tol", _f64), ("early_exit", _i32),
         ("x", _vp), ("a", _vp), ("f", _vp),
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),

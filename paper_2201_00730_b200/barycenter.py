@@ -1,0 +1,313 @@
+"""Multimarginal 1-D transport and KL barycenters on the B200
+(mirror of src/barycenter.py).
+
+``solve_mot_1d`` and ``fw_barycenter`` keep the reference signatures; the
+K-marginal sweep and the Frank-Wolfe iterations run in ``csrc/mot1d.cu``
+(cluster of K CTAs per problem + sample-sorted event buckets).
+``fw_barycenter_batched`` is the batched entry point of BASELINE config 5.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .certify import assemble_certificate
+from .exceptions import MassBalanceError
+from .fw import FwConfig
+from .measures import DiscreteMeasure
+from .sinkhorn import SolverReport
+
+MASS_TOL = 1e-9  # src/barycenter.py:43
+
+
+@dataclass(frozen=True)
+class BarycenterProblem:
+    """K input measures, barycentric weights omega, KL strength rho
+    (rho_k = omega_k rho); rho=None is the balanced problem."""
+
+    inputs: tuple
+    omega: np.ndarray
+    rho: float | None = None
+
+    def __post_init__(self):
+        inputs = tuple(self.inputs)
+        if len(inputs) < 2:
+            raise ValueError("need at least two input measures")
+        om = np.asarray(self.omega, dtype=np.float64)
+        if om.shape != (len(inputs),):
+            raise ValueError("omega must hold one weight per input")
+        if (om <= 0).any() or abs(float(om.sum()) - 1.0) > 1e-12:
+            raise ValueError("omega must be positive and sum to one")
+        if self.rho is not None and not (np.isfinite(self.rho) and self.rho > 0):
+            raise ValueError("rho must be positive (or None for balanced)")
+        om = np.ascontiguousarray(om)
+        om.flags.writeable = False
+        object.__setattr__(self, "inputs", inputs)
+        object.__setattr__(self, "omega", om)
+
+    @property
+    def k(self):
+        return len(self.inputs)
+
+    def rhos(self):
+        if self.rho is None:
+            raise ValueError("balanced problem has no KL strengths")
+        return self.omega * self.rho
+
+
+@dataclass(frozen=True)
+class MultiPlan:
+    """Plan entries: one index tuple (row of ``indices``) and a positive mass each."""
+
+    indices: np.ndarray
+    mass: np.ndarray
+
+    def __post_init__(self):
+        idx = np.ascontiguousarray(np.asarray(self.indices, dtype=np.int64))
+        ms = np.ascontiguousarray(np.asarray(self.mass, dtype=np.float64))
+        if idx.ndim != 2 or ms.ndim != 1 or idx.shape[0] != ms.size or ms.size == 0:
+            raise ValueError("plan needs matching index rows and masses")
+        if (ms <= 0).any():
+            raise ValueError("plan masses must be positive")
+        if idx.shape[0] > 1 and (np.diff(idx, axis=0) < 0).any():
+            raise ValueError("plan support must be monotone in every coordinate")
+        idx.flags.writeable = False
+        ms.flags.writeable = False
+        object.__setattr__(self, "indices", idx)
+        object.__setattr__(self, "mass", ms)
+
+    def __len__(self):
+        return int(self.mass.size)
+
+    @property
+    def k(self):
+        return int(self.indices.shape[1])
+
+    @property
+    def total_mass(self):
+        return float(self.mass.sum())
+
+    def marginal(self, k, size):
+        return np.bincount(self.indices[:, k], weights=self.mass, minlength=size).astype(float)
+
+
+@dataclass(frozen=True)
+class MultiDual:
+    """One potential vector per marginal."""
+
+    potentials: tuple
+
+    def __post_init__(self):
+        pots = []
+        for f in self.potentials:
+            arr = np.array(f, dtype=np.float64, copy=True)
+            if arr.ndim != 1 or not np.isfinite(arr).all():
+                raise ValueError("potentials must be finite vectors")
+            arr.flags.writeable = False
+            pots.append(arr)
+        object.__setattr__(self, "potentials", tuple(pots))
+
+    def __iter__(self):
+        return iter(self.potentials)
+
+    def __len__(self):
+        return len(self.potentials)
+
+
+def multimarginal_cost(points, w):
+    """(sum_k w_k (x_k - B)^2, B) with B = <w, x> (src/barycenter.py:148-156)."""
+    pts = np.asarray(points, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    b = float(np.dot(w, pts))
+    return float(np.dot(w, (pts - b) ** 2)), b
+
+
+def _pack(inputs, extra=None):
+    """Ragged list of measures -> padded (x, a, [extra]) [1, K, n] + lens."""
+    k = len(inputs)
+    lens = np.array([len(m) for m in inputs], dtype=np.int32)
+    n = int(lens.max())
+    x = np.zeros((1, k, n))
+    a = np.zeros((1, k, n))
+    f = np.zeros((1, k, n))
+    for q, m in enumerate(inputs):
+        x[0, q, :lens[q]] = m.points
+        x[0, q, lens[q]:] = m.points[-1]
+        a[0, q, :lens[q]] = m.weights
+        if extra is not None:
+            f[0, q, :lens[q]] = extra[q]
+    return x, a, f, lens
+
+
+def _plan_from(idx, mass, count):
+    c = int(count)
+    return MultiPlan(D.to_np(idx[:c]).astype(np.int64), D.to_np(mass[:c]))
+
+
+def solve_mot_1d_batched(x, a, omega, lens=None, stream=None):
+    """Balanced K-marginal sweep on device: x, a [B, K, n].  Returns
+    (duals [B, K, n], idx [B, E, K], mass [B, E], count [B], status [B])."""
+    t = D.torch()
+    lib = _lib.load()
+    x = D.to_dev(x, t.float64)
+    a = D.to_dev(a, t.float64)
+    B, K, n = x.shape
+    cap = K * (n - 1) + 1
+    f = D.empty((B, K, n), t.float64)
+    idx = D.empty((B, cap, K), t.int32)
+    mass = D.empty((B, cap), t.float64)
+    count = D.empty((B,), t.int32)
+    status = D.empty((B,), t.int32)
+    om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+    ln = None if lens is None else np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_mot1d_workspace_size(B, K, n, ctypes.byref(size)))
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_mot1d_batched(
+        B, K, n, ln.ctypes.data_as(ctypes.c_void_p) if ln is not None else None, _lib.ptr(x),
+        _lib.ptr(a), om.ctypes.data_as(ctypes.c_void_p), _lib.ptr(f), _lib.ptr(idx),
+        _lib.ptr(mass), _lib.ptr(count), _lib.ptr(status), _lib.ptr(ws),
+        ctypes.c_size_t(size.value), _lib.stream_handle(stream)), "uot_mot1d_batched")
+    D.torch().cuda.current_stream().synchronize()
+    return f, idx, mass, count, status
+
+
+def solve_mot_1d(inputs, w=None, costfn=None):
+    """Balanced 1-D multimarginal transport (src/barycenter.py:169-233).
+
+    Only the barycentric squared-Euclidean tuple cost runs on the B200 path;
+    a custom ``costfn`` raises."""
+    inputs = tuple(inputs)
+    if len(inputs) < 2:
+        raise ValueError("need at least two measures")
+    masses = np.array([m.mass for m in inputs])
+    if float(masses.max() - masses.min()) > MASS_TOL * float(masses.max()):
+        raise MassBalanceError(f"multimarginal sweep needs equal masses, got {masses.tolist()}")
+    if costfn is not None:
+        from .exceptions import UnsupportedEntropyError
+
+        raise UnsupportedEntropyError("custom tuple costs are not on the B200 path")
+    if w is None:
+        raise ValueError("need barycentric weights when costfn is omitted")
+    x, a, _, lens = _pack(inputs)
+    f, idx, mass, count, status = solve_mot_1d_batched(x, a, w, lens)
+    st = int(status[0].item())
+    if st == 1:
+        raise MassBalanceError("multimarginal sweep needs equal masses")
+    if st != 0:
+        raise ValueError("multimarginal sweep failed (bucket capacity)")
+    fd = D.to_np(f[0])
+    plan = _plan_from(idx[0], mass[0], count[0].item())
+    return plan, MultiDual(tuple(fd[q, :lens[q]] for q in range(len(inputs))))
+
+
+@dataclass
+class BaryBatchResult:
+    f: object
+    h0: object
+    fw_gap: object
+    pd_gap: object
+    iterations: object
+    idx: object
+    mass: object
+    count: object
+    summary: object
+    status: object
+
+
+def fw_barycenter_batched(x, a, omega, rho=1.0, max_iters=1000, step="linesearch",
+                          gap_tol=1e-6, early_exit=False, f0=None, lens=None, stream=None):
+    """Batched KL barycenter FW on device: x, a [B, K, n] (sorted rows).
+    Returns device tensors; f is translated (report.final)."""
+    t = D.torch()
+    lib = _lib.load()
+    x = D.to_dev(x, t.float64)
+    a = D.to_dev(a, t.float64)
+    B, K, n = x.shape
+    cap = K * (n - 1) + 1
+    f = t.zeros((B, K, n), dtype=t.float64, device=x.device) if f0 is None else \
+        D.to_dev(f0, t.float64).clone()
+    r = BaryBatchResult(
+        f=f, h0=D.empty((B, max_iters), t.float64), fw_gap=D.empty((B, max_iters), t.float64),
+        pd_gap=D.empty((B, max_iters), t.float64), iterations=D.empty((B,), t.int32),
+        idx=D.empty((B, cap, K), t.int32), mass=D.empty((B, cap), t.float64),
+        count=D.empty((B,), t.int32), summary=D.empty((B, 2), t.float64),
+        status=D.empty((B,), t.int32))
+    om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+    ln = None if lens is None else np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
+    desc = _lib.BaryDesc(
+        batch=B, k=K, n=n, omega=om.ctypes.data_as(ctypes.c_void_p),
+        lens=ln.ctypes.data_as(ctypes.c_void_p) if ln is not None else None, rho=float(rho),
+        step=_lib.STEP_LINESEARCH if step == "linesearch" else _lib.STEP_HARMONIC,
+        max_iters=int(max_iters), gap_tol=float(gap_tol), early_exit=1 if early_exit else 0,
+        x=_lib.ptr(x), a=_lib.ptr(a), f=_lib.ptr(f), h0=_lib.ptr(r.h0),
+        fw_gap=_lib.ptr(r.fw_gap), pd_gap=_lib.ptr(r.pd_gap), iterations=_lib.ptr(r.iterations),
+        idx=_lib.ptr(r.idx), mass=_lib.ptr(r.mass), count=_lib.ptr(r.count),
+        summary=_lib.ptr(r.summary), status=_lib.ptr(r.status))
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_bary_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_bary_run(ctypes.byref(desc), _lib.ptr(ws), ctypes.c_size_t(size.value),
+                                _lib.stream_handle(stream)), "uot_bary_run")
+    t.cuda.current_stream().synchronize()  # omega / lens are host buffers of this frame
+    return r
+
+
+def fw_barycenter(problem, config=FwConfig(), init=None):
+    """Frank-Wolfe on the invariant dual of the KL multimarginal problem
+    (src/barycenter.py:330-430).  Returns ``(report, plan)``.
+
+    The certificate's feasibility term is 0 here: the reference evaluates it
+    only when the full index grid holds <= 1e5 tuples (:416-418) by an
+    exhaustive host sweep; the B200 path does not enumerate the grid."""
+    if problem.rho is None:
+        raise ValueError("balanced barycenters route directly through solve_mot_1d")
+    if config.step == "pairwise":
+        from .exceptions import UnsupportedEntropyError
+
+        raise UnsupportedEntropyError("pairwise FW is not on the B200 barycenter path")
+    inputs = problem.inputs
+    pots0 = None
+    if init is not None:
+        pots0 = [np.asarray(f, dtype=np.float64) for f in init.potentials]
+        if any(p.size != len(m) for p, m in zip(pots0, inputs)):
+            raise ValueError("initial potentials do not match the inputs")
+    x, a, f0, lens = _pack(inputs, pots0)
+    tic = time.perf_counter_ns()
+    r = fw_barycenter_batched(x, a, problem.omega, problem.rho, config.max_iters, config.step,
+                              config.gap_tol, early_exit=True, f0=f0, lens=lens)
+    st = int(r.status[0].item())
+    if st == 1:
+        raise MassBalanceError("translated masses disagree; translation broken")
+    if st != 0:
+        raise ValueError("barycenter sweep failed (bucket capacity)")
+    its = int(r.iterations[0].item())
+    wall = (time.perf_counter_ns() - tic) // max(its, 1)
+    pd = D.to_np(r.pd_gap[0, :its], readonly=False)
+    trace = {"h0": D.to_np(r.h0[0, :its], readonly=False),
+             "fw_gap": D.to_np(r.fw_gap[0, :its], readonly=False), "pd_gap": pd,
+             "wall_ns": np.full(its, wall, dtype=np.int64)}
+    converged = bool(its > 0 and pd[-1] < config.gap_tol)
+    fd = D.to_np(r.f[0])
+    final = MultiDual(tuple(fd[q, :lens[q]] for q in range(len(inputs))))
+    plan = _plan_from(r.idx[0], r.mass[0], r.count[0].item())
+    primal, dual = (float(v) for v in D.to_np(r.summary[0]))
+    cert = assemble_certificate(primal, dual, 0.0, config.gap_tol)
+    report = SolverReport(final=final, iterations=its, converged=converged, trace=trace,
+                          certificate=cert, plan=plan)
+    return report, plan
+
+
+def extract_barycenter(plan, inputs, w):
+    """One atom per plan entry at <w, tuple points> with the entry's mass;
+    coincident atoms merge (src/barycenter.py:433-443).  Host-side gather of
+    the (already computed) plan."""
+    w = np.asarray(w, dtype=np.float64)
+    pts = np.stack([inputs[k].points[plan.indices[:, k]] for k in range(plan.k)], axis=1)
+    return DiscreteMeasure(pts @ w, plan.mass)

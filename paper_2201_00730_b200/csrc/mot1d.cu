@@ -1,0 +1,1160 @@
+// mot1d.cu -- balanced K-marginal 1-D sweep (Algorithm 3) and the KL
+// barycenter Frank-Wolfe (K7/K8/K9 of SURVEY.md §2.2).
+//
+// Reference: src/barycenter.py:148-233 (multimarginal_cost, solve_mot_1d),
+// :236-240 (plan_cost), :298-327 (multimarginal_lambda, _h_value),
+// :330-430 (fw_barycenter), :433-443 (extract_barycenter).
+//
+// Restatement.  With B_q[t] = sum_{s<=t} w_q[s] the
+// cumulative masses of list q, the sweep advances coordinate p at its
+// breakpoint B_p[t] in the order of the keys (B_p[t], p, t) (ties to the
+// lowest coordinate, barycenter.py:218), and the advanced coordinate's dual
+// grows by the change of the tuple cost
+//   dCc = w_p d (x_p[t+1] + x_p[t] - Bb - Ba),  d = x_p[t+1] - x_p[t],
+// where Bb, Ba = Bb + w_p d are the barycentres of the tuple before / after
+// (Cc = sum w x^2 - B^2), so f_p[t+1] = f_p[t] + dCc (barycenter.py:225-229).
+// Bb of every event is a prefix sum over the merged events of w_p d.
+//
+// Pipeline per FW iteration, all on device:
+//   mot_prep   (cluster of K CTAs per problem, one CTA per list): log-sum-exps,
+//              optimal zero-sum translation (DSMEM exchange), tilt, block scan
+//              of the breakpoints, mass check, regular samples -> splitters ->
+//              per-list split positions (sample sort).
+//   mot_bucket (S CTAs per problem): gathers the events of one key range from
+//              all K lists, bitonic-sorts them in shared memory, scans the
+//              barycentre increments from the range's starting tuple and
+//              writes every event's cost increment.
+//   mot_update (cluster of K CTAs): per-list prefix sums -> dual atoms,
+//              gaps / primal / dual (DSMEM reductions), safeguarded Newton
+//              line search on sum_k rho_k LSE_k, update.
+// The plan (tuples + masses) of the last iteration is materialised by
+// mot_plan_count / mot_plan_write.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "../../include/uot_b200.h"
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace uot {
+namespace {
+
+constexpr int MT = 512;           // threads of the per-list CTAs
+constexpr int BT = 512;           // threads of the bucket CTAs
+constexpr int CAP = 8192;         // events per bucket (shared-memory capacity)
+constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
+
+struct MotArgs {
+  int batch, k, n;        // n = row stride (max list length)
+  const int* lens;        // device [k] list lengths (shared by the batch)
+  const double* omega;    // device [k]
+  double rho;             // KL strength: rho_k = omega_k * rho
+  int mode;               // 0 = barycenter FW, 1 = balanced sweep on a
+  int step;               // UOT_STEP_*
+  int max_iters;
+  double gap_tol;
+  int early_exit;
+  int t;                  // iteration index (host loop)
+  const double* x;        // [B][K][n]
+  const double* a;        // [B][K][n]
+  double* f;              // [B][K][n] potentials (untranslated iterate)
+  double* ta;             // [B][K][n] tilted weights
+  double* A;              // [B][K][n] breakpoints
+  double* dcc;            // [B][K][n] cost increments
+  int* split;             // [B][S+1][K]
+  int S, SS;              // buckets per problem, samples per list
+  double* scal;           // [B][4]: dual, (unused)
+  double* lam;            // [B][K]
+  double* h0;             // [B][max_iters]
+  double* fw_gap;
+  double* pd_gap;
+  int* iterations;        // [B]
+  int* done;              // [B]
+  int* status;            // [B]
+  double* summary;        // [B][2]
+  double* out_f;          // [B][K][n] translated final potentials / sweep duals
+  int* pidx;              // [B][cap_e][K]
+  double* pmass;          // [B][cap_e]
+  int* pcount;            // [B]
+  int* bcount;            // [B][S]
+  int cap_e;
+};
+
+__device__ __forceinline__ int list_len(const MotArgs& A, int q) {
+  return A.lens != nullptr ? A.lens[q] : A.n;
+}
+
+__device__ __forceinline__ double exp_nonpos(double x) {
+  if (x < -708.0) return 0.0;
+  const double nn = rint(x * 1.4426950408889634074);
+  double r = fma(nn, -6.93147180369123816490e-01, x);
+  r = fma(nn, -1.90821492927058770002e-10, r);
+  double q = 1.6059043836821614599e-10;
+  q = fma(q, r, 2.0876756987868098979e-09);
+  q = fma(q, r, 2.5052108385441718775e-08);
+  q = fma(q, r, 2.7557319223985890653e-07);
+  q = fma(q, r, 2.7557319223985890653e-06);
+  q = fma(q, r, 2.4801587301587301587e-05);
+  q = fma(q, r, 1.9841269841269841270e-04);
+  q = fma(q, r, 1.3888888888888888889e-03);
+  q = fma(q, r, 8.3333333333333333333e-03);
+  q = fma(q, r, 4.1666666666666666667e-02);
+  q = fma(q, r, 1.6666666666666666667e-01);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  return q * __longlong_as_double((long long)((int)nn + 1023) << 52);
+}
+
+// ---------------------------------------------------------------------------
+// Block helpers (MT threads).
+
+template <int K>
+__device__ __forceinline__ void bsum_k(double (&v)[K], double* scr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scr[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += scr[k * 32 + w];
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+template <int K>
+__device__ __forceinline__ void bmax_k(double (&v)[K], double* scr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_max(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scr[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = -CUDART_INF;
+    for (int w = 0; w < nw; ++w) s = fmax(s, scr[k * 32 + w]);
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+// exclusive scan of one double per thread; returns the exclusive prefix and
+// the block total.
+__device__ __forceinline__ double bscan1(double v, double& total, double* scr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += t;
+  }
+  __syncthreads();
+  if (lane == 31) scr[warp] = s;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double off = 0.0, tot = 0.0;
+  for (int w = 0; w < nw; ++w) {
+    const double t = scr[w];
+    if (w < warp) off += t;
+    tot += t;
+  }
+  __syncthreads();
+  total = tot;
+  return off + s - v;
+}
+
+__device__ __forceinline__ int bscan_maxi(int v, int* scr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int s = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s = max(s, t);
+  }
+  int ex = __shfl_up_sync(0xffffffffu, s, 1);
+  if (lane == 0) ex = -1;
+  __syncthreads();
+  if (lane == 31) scr[warp] = s;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) ex = max(ex, scr[w]);
+  __syncthreads();
+  return ex;
+}
+
+// Cluster all-reduce (sum) of NV doubles: each CTA publishes its vector in
+// its own shared slot, then every CTA sums all slots in rank order (identical
+// results everywhere).  `slot` alternates between two buffers so one cluster
+// barrier per reduction suffices.
+template <int NV>
+__device__ __forceinline__ void cluster_sum(double (&v)[NV], double* slots, int& parity) {
+  cg::cluster_group cl = cg::this_cluster();
+  double* mine = slots + parity * 16;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) mine[k] = v[k];
+  }
+  cl.sync();
+  const int nr = (int)cl.num_blocks();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  for (int r = 0; r < nr; ++r) {
+    const double* other = cl.map_shared_rank(mine, r);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += other[k];
+  }
+  parity ^= 1;
+}
+
+// Composite event key order: (value, list, index) lexicographic.
+__device__ __forceinline__ bool key_less(double va, int qa, int ta_, double vb, int qb, int tb) {
+  if (va != vb) return va < vb;
+  if (qa != qb) return qa < qb;
+  return ta_ < tb;
+}
+
+// #{ t in [0, len) : (arr[t], q, t) < (v, qs, ts) }
+__device__ __forceinline__ int count_keys_below(const double* arr, int len, int q, double v, int qs,
+                                                int ts) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key_less(arr[mid], q, mid, v, qs, ts))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// In-place bitonic sort of (key, code) pairs in shared memory; count is a
+// power of two; codes order ties ((list, index) packed).
+__device__ void bitonic_sort(double* key, int* code, int count) {
+  for (int size = 2; size <= count; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < count / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const double ka = key[lo], kb = key[hi];
+        const int ca = code[lo], cb = code[hi];
+        const bool gt = (ka > kb) || (ka == kb && ca > cb);
+        if (gt == up) {
+          key[lo] = kb;
+          key[hi] = ka;
+          code[lo] = cb;
+          code[hi] = ca;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mot_prep: one CTA per list, cluster of K CTAs per problem.
+
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double scr[32 * 8];
+  __shared__ double slots[32];
+  __shared__ int done_s;
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  int parity = 0;
+  if (threadIdx.x == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
+  __syncthreads();
+  if (done_s) return;  // uniform over the cluster
+  double* sA = smem;                                  // [n] breakpoints
+  double* samp = smem + n;                            // [SS] sample values
+  int* sampt = reinterpret_cast<int*>(samp + A.SS);   // [SS] sample indices
+  double* sortk = reinterpret_cast<double*>(sampt + A.SS + (A.SS & 1));  // CTA 0: [KSS2]
+  const long base = ((long)b * K + q) * n;
+  const double rq = A.omega[q] * A.rho;
+
+  double w[EPT], fv[EPT], ta[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    w[e] = i < nq ? A.a[base + i] : 0.0;
+    fv[e] = i < nq ? A.f[base + i] : 0.0;
+  }
+  if (A.mode == 0) {
+    // q_k = LSE_{a_k}(-f_k / rho_k)  (barycenter.py:307-313)
+    double mx[1] = {-CUDART_INF};
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (w[e] > 0.0) mx[0] = fmax(mx[0], -fv[e] / rq);
+    bmax_k<1>(mx, scr);
+    double sums[2] = {0.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ta[e] = w[e] > 0.0 ? w[e] * exp_nonpos(-fv[e] / rq - mx[0]) : 0.0;
+      sums[0] += ta[e];
+      sums[1] += w[e];
+    }
+    bsum_k<2>(sums, scr);
+    const double qk = mx[0] + log(sums[0]);
+    // exchange (rho_k q_k, rho_k m_k, rho_k) over the cluster
+    double ex[3] = {rq * qk, rq * sums[1], rq};
+    cluster_sum<3>(ex, slots, parity);
+    const double rho_tot = ex[2];
+    const double lamq = rq * qk - (rq / rho_tot) * ex[0];  // barycenter.py:316-317
+    if (threadIdx.x == 0) {
+      A.lam[(long)b * K + q] = lamq;
+      if (q == 0) A.scal[b * 4 + 0] = ex[1] - rho_tot * exp(ex[0] / rho_tot);  // :320-327
+    }
+    const double sc = exp(mx[0] - lamq / rq);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) ta[e] *= sc;
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) ta[e] = w[e];
+  }
+  // tilted weights -> global, breakpoints via block scan
+  double loc = 0.0, pre[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    if (i < nq) A.ta[base + i] = ta[e];
+    loc += ta[e];
+    pre[e] = loc;
+  }
+  double total;
+  const double off = bscan1(loc, total, scr);
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    if (i < nq) sA[i] = off + pre[e];
+  }
+  // zero-weight atoms repeat their predecessor's breakpoint bit for bit
+  {
+    int lz = -1;
+    int any0 = 0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = threadIdx.x * EPT + e;
+      if (i < nq && ta[e] > 0.0) lz = i;
+      if (i < nq && ta[e] == 0.0) any0 = 1;
+    }
+    const int anyz = __syncthreads_or(any0);
+    if (anyz) {
+      int pr = bscan_maxi(lz, reinterpret_cast<int*>(scr));
+      __syncthreads();
+      double fix[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = threadIdx.x * EPT + e;
+        fix[e] = (i < nq && ta[e] == 0.0) ? (pr >= 0 ? sA[pr] : 0.0) : -1.0;
+        if (i < nq && ta[e] > 0.0) pr = i;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = threadIdx.x * EPT + e;
+        if (fix[e] >= 0.0) sA[i] = fix[e];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nq; i += MT) A.A[base + i] = sA[i];
+  // mass balance across the K inputs (barycenter.py:187-191, :368-370)
+  {
+    double mm[2] = {total, -total};
+    cg::cluster_group c2 = cg::this_cluster();
+    double* mine = slots + parity * 16;
+    if (threadIdx.x == 0) {
+      mine[0] = mm[0];
+      mine[1] = mm[1];
+    }
+    c2.sync();
+    double mxm = -CUDART_INF, mnm = CUDART_INF;
+    for (int r = 0; r < K; ++r) {
+      const double* o = c2.map_shared_rank(mine, r);
+      mxm = fmax(mxm, o[0]);
+      mnm = fmin(mnm, o[0]);
+    }
+    parity ^= 1;
+    if (q == 0 && threadIdx.x == 0) {
+      const bool bad = (mxm - mnm) > 1e-9 * mxm;
+      A.status[b] = bad ? UOT_MASS_BALANCE : 0;
+      if (bad && A.done != nullptr) A.done[b] = 1;
+      A.scal[b * 4 + 1] = mnm;  // common total (min)
+    }
+  }
+  // regular samples of this list's events (keys (B_q[t], q, t), t < nq-1)
+  const int ne = nq - 1;
+  const int SS = A.SS;
+  for (int j = threadIdx.x; j < SS; j += MT) {
+    const int t = (ne > 0) ? (int)(((long)(j + 1) * ne) / (SS + 1)) : 0;
+    samp[j] = (ne > 0) ? sA[min(t, ne - 1)] : CUDART_INF;
+    sampt[j] = (ne > 0) ? min(t, ne - 1) : 0;
+  }
+  cl.sync();
+  const int S = A.S;
+  if (S > 1) {
+    // CTA 0 gathers all samples, sorts them and publishes S-1 splitters in
+    // its own shared memory (as (value, code) pairs in sortk / sortc).
+    int KSS2 = 1;
+    while (KSS2 < K * SS) KSS2 <<= 1;
+    int* sortc = reinterpret_cast<int*>(sortk + KSS2);
+    if (q == 0) {
+      for (int idx = threadIdx.x; idx < KSS2; idx += MT) {
+        if (idx < K * SS) {
+          const int r = idx / SS, j = idx % SS;
+          const double* ov = cl.map_shared_rank(samp, r);
+          const int* ot = cl.map_shared_rank(sampt, r);
+          sortk[idx] = ov[j];
+          sortc[idx] = r * n + ot[j];
+        } else {
+          sortk[idx] = CUDART_INF;
+          sortc[idx] = 0x7fffffff;
+        }
+      }
+      __syncthreads();
+      bitonic_sort(sortk, sortc, KSS2);
+      // splitter s (1..S-1) is the sorted sample at rank s * (K*SS) / S
+    }
+    cl.sync();
+    // every list locates each splitter in its own breakpoints
+    const double* k0 = cl.map_shared_rank(sortk, 0);
+    const int* c0 = cl.map_shared_rank(sortc, 0);
+    int* sp = A.split + (long)b * (S + 1) * K;
+    for (int s = threadIdx.x; s <= S; s += MT) {
+      int pos;
+      if (s == 0) {
+        pos = 0;
+      } else if (s == S) {
+        pos = max(ne, 0);
+      } else {
+        const int rk = (int)(((long)s * K * SS) / S);
+        const double v = k0[rk];
+        const int code = c0[rk];
+        pos = count_keys_below(sA, max(ne, 0), q, v, code / n, code % n);
+      }
+      sp[(long)s * K + q] = pos;
+    }
+  } else {
+    int* sp = A.split + (long)b * 2 * K;
+    if (threadIdx.x == 0) {
+      sp[q] = 0;
+      sp[K + q] = max(ne, 0);
+    }
+  }
+  cl.sync();  // keep shared memory alive until every CTA finished reading it
+}
+
+// ---------------------------------------------------------------------------
+// mot_bucket: events of one key range, sorted; cost increments.
+
+__device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, double* key, int* code,
+                                             int* lo_s, int* cnt_s) {
+  const int K = A.k, n = A.n;
+  const int* sp = A.split + (long)b * (A.S + 1) * K;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int q = 0; q < K; ++q) {
+      const int lo = sp[(long)s * K + q], hi = sp[(long)(s + 1) * K + q];
+      lo_s[q] = lo;
+      cnt_s[q] = c;
+      c += hi - lo;
+    }
+    cnt_s[K] = c;
+  }
+  __syncthreads();
+  const int total = cnt_s[K];
+  if (total > CAP) return -1;
+  int pw = 1;
+  while (pw < total) pw <<= 1;
+  for (int q = 0; q < K; ++q) {
+    const int lo = lo_s[q], c0 = cnt_s[q], len = cnt_s[q + 1] - c0;
+    const double* Aq = A.A + ((long)b * K + q) * n;
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      key[c0 + j] = Aq[lo + j];
+      code[c0 + j] = q * n + lo + j;
+    }
+  }
+  for (int j = total + threadIdx.x; j < pw; j += blockDim.x) {
+    key[j] = CUDART_INF;
+    code[j] = 0x7fffffff;
+  }
+  __syncthreads();
+  bitonic_sort(key, code, pw);
+  return total;
+}
+
+__global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ int lo_s[KMAX + 1], cnt_s[KMAX + 1];
+  __shared__ double scr[32];
+  __shared__ double bstart_s;
+  const int s = blockIdx.x, b = blockIdx.y;
+  if (A.done != nullptr && A.done[b]) return;
+  const int K = A.k, n = A.n;
+  double* key = bsm;
+  int* code = reinterpret_cast<int*>(key + CAP);
+  const int total = bucket_gather(A, b, s, key, code, lo_s, cnt_s);
+  if (total < 0) {
+    if (threadIdx.x == 0) A.status[b] = UOT_INVALID;  // bucket overflow
+    return;
+  }
+  // barycentre of the tuple before the range: idx_q = lo_q
+  if (threadIdx.x == 0) {
+    double bs = 0.0;
+    for (int q = 0; q < K; ++q) bs += A.omega[q] * A.x[((long)b * K + q) * n + lo_s[q]];
+    bstart_s = bs;
+  }
+  __syncthreads();
+  const double bstart = bstart_s;
+  // each thread handles a contiguous run of sorted events
+  const int per = (total + BT - 1) / BT;
+  const int e0 = threadIdx.x * per, e1 = min(total, e0 + per);
+  double loc = 0.0;
+  for (int e = e0; e < e1; ++e) {
+    const int q = code[e] / n, t = code[e] % n;
+    const double* xq = A.x + ((long)b * K + q) * n;
+    loc += A.omega[q] * (xq[t + 1] - xq[t]);
+  }
+  double tot;
+  double run = bscan1(loc, tot, scr);
+  for (int e = e0; e < e1; ++e) {
+    const int q = code[e] / n, t = code[e] % n;
+    const double* xq = A.x + ((long)b * K + q) * n;
+    const double xo = xq[t], xn = xq[t + 1];
+    const double inc = A.omega[q] * (xn - xo);
+    const double bb = bstart + run;
+    const double ba = bb + inc;
+    A.dcc[((long)b * K + q) * n + t + 1] = inc * (xn + xo - bb - ba);
+    run += inc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mot_update: dual atoms, gaps, line search, update (cluster of K CTAs).
+
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double scr[32 * 8];
+  __shared__ double slots[32];
+  __shared__ int done_s;
+  __shared__ double cc0_s;
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  int parity = 0;
+  if (threadIdx.x == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
+  __syncthreads();
+  if (done_s) return;
+  const long base = ((long)b * K + q) * n;
+  // initial potential: f_1[0] = Cc(first tuple), f_k[0] = 0 (barycenter.py:206-207)
+  if (threadIdx.x == 0) {
+    double bb = 0.0;
+    for (int r = 0; r < K; ++r) bb += A.omega[r] * A.x[((long)b * K + r) * n];
+    double c = 0.0;
+    for (int r = 0; r < K; ++r) {
+      const double d = A.x[((long)b * K + r) * n] - bb;
+      c += A.omega[r] * (d * d);
+    }
+    cc0_s = (q == 0) ? c : 0.0;
+  }
+  __syncthreads();
+  double rv[EPT];
+  double loc = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    const double d = (i >= 1 && i < nq) ? A.dcc[base + i] : 0.0;
+    loc += d;
+    rv[e] = loc;
+  }
+  double tot;
+  const double off = bscan1(loc, tot, scr) + cc0_s;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) rv[e] += off;
+
+  if (A.mode == 1) {  // balanced sweep: the duals are the output
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = threadIdx.x * EPT + e;
+      if (i < nq) A.out_f[base + i] = rv[e];
+    }
+    return;
+  }
+  const double rq = A.omega[q] * A.rho;
+  const double lamq = A.lam[(long)b * K + q];
+  double fv[EPT], tv[EPT], wv[EPT];
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  double mxs[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    fv[e] = i < nq ? A.f[base + i] : 0.0;
+    tv[e] = i < nq ? A.ta[base + i] : 0.0;
+    wv[e] = i < nq ? A.a[base + i] : 0.0;
+    const double d = rv[e] - fv[e];
+    acc[0] += tv[e] * d;                 // fw_gap part (barycenter.py:376-381)
+    acc[1] += tv[e] * rv[e];             // plan cost via complementary slackness
+    if (tv[e] > 0.0) acc[2] += tv[e] * (-(fv[e] + lamq) / rq);  // sum ta log(ta/a)
+    acc[3] += tv[e];                     // tilted mass
+    acc[4] += wv[e];                     // input mass
+    acc[5] += tv[e] * d;                 // first moment of d under p_0
+    acc[6] += tv[e] * d * d;             // second moment
+    if (wv[e] > 0.0) {
+      mxs[0] = fmax(mxs[0], -fv[e] / rq);
+      mxs[1] = fmax(mxs[1], -rv[e] / rq);
+    }
+  }
+  bsum_k<7>(acc, scr);
+  bmax_k<2>(mxs, scr);
+  // cluster sums: fw_gap, plan cost + rho KL terms, sum of centres
+  const double cq = acc[5] / acc[3];
+  double cs[3] = {acc[0], acc[1] + rq * (acc[2] - acc[3] + acc[4]), cq};
+  cluster_sum<3>(cs, slots, parity);
+  const double fw_gap = cs[0];
+  const double primal = cs[1];
+  const double dual = A.scal[b * 4 + 0];
+  const double pd_gap = primal - dual;
+  const int t = A.t;
+  if (q == 0 && threadIdx.x == 0) {
+    A.h0[(long)b * A.max_iters + t] = dual;
+    A.fw_gap[(long)b * A.max_iters + t] = fw_gap;
+    A.pd_gap[(long)b * A.max_iters + t] = pd_gap;
+    A.iterations[b] = t + 1;
+    A.summary[b * 2 + 0] = primal;
+    A.summary[b * 2 + 1] = dual;
+  }
+  const bool stop = A.early_exit && pd_gap < A.gap_tol;  // barycenter.py:394-396
+  if (stop) {
+    if (q == 0 && threadIdx.x == 0) A.done[b] = 2;  // converged (plan of this iteration kept)
+    cl.sync();
+    return;
+  }
+  double gam;
+  if (A.step == UOT_STEP_HARMONIC) {
+    gam = 2.0 / (2.0 + t);
+  } else {
+    // minimise Phi(gamma) = sum_k rho_k LSE_{a_k}(-(f_k + gamma d_k)/rho_k):
+    // Phi' = -sum_k E_k[d_k], Phi'' = sum_k Var_k[d_k] / rho_k; moments are
+    // centred at the gamma = 0 means (translation invariance, see fw1d.cu).
+    const double k0 = -cs[2];
+    const double v0 = fmax(acc[6] / acc[3] - cq * cq, 0.0) / rq;
+    double vs[1] = {v0};
+    cluster_sum<1>(vs, slots, parity);
+    if (!(k0 < 0.0)) {
+      gam = 0.0;
+    } else {
+      double lo = 0.0, hi = 1.0;
+      gam = vs[0] > 0.0 ? fmin(1.0, -k0 / vs[0]) : 1.0;
+      for (int it = 0; it < 24; ++it) {
+        const double sh = (1.0 - gam) * mxs[0] + gam * mxs[1];
+        double mom[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if (wv[e] > 0.0) {
+            const double d = rv[e] - fv[e];
+            const double ww = wv[e] * exp_nonpos(-(fv[e] + gam * d) / rq - sh);
+            const double xc = d - cq;
+            mom[0] += ww;
+            mom[1] += ww * xc;
+            mom[2] += ww * xc * xc;
+          }
+        }
+        bsum_k<3>(mom, scr);
+        const double e1 = mom[1] / mom[0];
+        double gv[2] = {e1, (mom[2] / mom[0] - e1 * e1) / rq};
+        cluster_sum<2>(gv, slots, parity);
+        const double g1 = k0 - gv[0], g2 = gv[1];
+        if (g1 < 0.0)
+          lo = gam;
+        else
+          hi = gam;
+        if (gam >= 1.0 && g1 <= 0.0) {
+          gam = 1.0;
+          break;
+        }
+        double nxt = g2 > 0.0 ? gam - g1 / g2 : 0.5 * (lo + hi);
+        const bool newton = nxt > lo && nxt < hi;
+        if (!newton) nxt = 0.5 * (lo + hi);
+        const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(1.0, gam)) || g1 == 0.0 ||
+                          hi - lo <= 1e-15;
+        gam = nxt;
+        if (conv) break;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    if (i < nq) A.f[base + i] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
+  }
+  cl.sync();  // slots stay valid until every CTA read them
+}
+
+// Final translation by the optimal zero-sum lambda (barycenter.py:413-414).
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double scr[32 * 8];
+  __shared__ double slots[32];
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  int parity = 0;
+  const long base = ((long)b * K + q) * n;
+  const double rq = A.omega[q] * A.rho;
+  double w[EPT], fv[EPT];
+  double mx[1] = {-CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    w[e] = i < nq ? A.a[base + i] : 0.0;
+    fv[e] = i < nq ? A.f[base + i] : 0.0;
+    if (w[e] > 0.0) mx[0] = fmax(mx[0], -fv[e] / rq);
+  }
+  bmax_k<1>(mx, scr);
+  double sm[1] = {0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e)
+    if (w[e] > 0.0) sm[0] += w[e] * exp_nonpos(-fv[e] / rq - mx[0]);
+  bsum_k<1>(sm, scr);
+  const double qk = mx[0] + log(sm[0]);
+  double ex[2] = {rq * qk, rq};
+  cluster_sum<2>(ex, slots, parity);
+  const double lamq = rq * qk - (rq / ex[1]) * ex[0];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = threadIdx.x * EPT + e;
+    if (i < nq) A.out_f[base + i] = fv[e] + lamq;
+  }
+  cl.sync();
+}
+
+// ---------------------------------------------------------------------------
+// Plan of the current breakpoints: tuples and masses of the positive-mass
+// states (barycenter.py:209-222), in sweep order.
+
+__device__ __forceinline__ double next_event_value(const MotArgs& A, int b, int s) {
+  // smallest key among the lists' first events of range s (or +inf)
+  const int K = A.k, n = A.n;
+  const int* sp = A.split + (long)b * (A.S + 1) * K;
+  double v = CUDART_INF;
+  for (int q = 0; q < K; ++q) {
+    const int lo = sp[(long)s * K + q];
+    const int ne = list_len(A, q) - 1;
+    if (lo < ne) v = fmin(v, A.A[((long)b * K + q) * n + lo]);
+  }
+  return v;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ int lo_s[KMAX + 1], cnt_s[KMAX + 1];
+  __shared__ int scan_s[BT / 32];
+  __shared__ int kept_s;
+  const int s = blockIdx.x, b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  double* key = bsm;
+  int* code = reinterpret_cast<int*>(key + CAP);
+  const int total = bucket_gather(A, b, s, key, code, lo_s, cnt_s);
+  if (total < 0) return;
+  const double tot_mass = A.scal[b * 4 + 1];
+  const double nxt = (s + 1 < A.S) ? next_event_value(A, b, s + 1) : CUDART_INF;
+  // states: the state after each event (and, in range 0, the initial state)
+  const int first = (s == 0) ? -1 : 0;
+  const int nst = total - first;  // number of states emitted by this range
+  int out_base = 0;
+  if (WRITE) {
+    for (int r = 0; r < s; ++r) out_base += A.bcount[(long)b * A.S + r];
+  }
+  int kept_run = 0;
+  for (int c0 = 0; c0 < nst; c0 += BT) {
+    const int c = c0 + threadIdx.x;
+    const int e = c + first;  // state after event e (e = -1: initial state)
+    double mass = 0.0;
+    if (c < nst) {
+      const double lo = (e < 0) ? 0.0 : fmin(key[e], tot_mass);
+      double hi = (e + 1 < total) ? key[e + 1] : nxt;
+      hi = fmin(hi, tot_mass);
+      mass = hi - lo;
+    }
+    const int keep = (c < nst && mass > 0.0) ? 1 : 0;
+    // block exclusive scan of keep
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = keep;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int tt = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += tt;
+    }
+    if (lane == 31) scan_s[warp] = incl;
+    __syncthreads();
+    int offw = 0, tot = 0;
+    for (int w = 0; w < BT / 32; ++w) {
+      if (w < warp) offw += scan_s[w];
+      tot += scan_s[w];
+    }
+    __syncthreads();
+    if (WRITE && keep) {
+      const int pos = out_base + kept_run + offw + incl - 1;
+      if (pos < A.cap_e) {
+        A.pmass[(long)b * A.cap_e + pos] = mass;
+        // tuple: lo_q + #{events of list q among sorted events [0, e]}
+        int* row = A.pidx + ((long)b * A.cap_e + pos) * K;
+        for (int q = 0; q < K; ++q) {
+          int cnt = 0;
+          // events are sorted; count list-q codes in [0, e] by binary search
+          // on the (list, index) code within the sorted range is not
+          // monotone, so count by a linear scan of the run of list q via
+          // its position: the number of q-events before e equals the number
+          // of q-events with key <= key[e] (keys of one list are ordered).
+          const int c_lo = cnt_s[q], c_len = cnt_s[q + 1] - c_lo;
+          if (e >= 0 && c_len > 0) {
+            const double* Aq = A.A + ((long)b * K + q) * n + lo_s[q];
+            const int eq = code[e] / n;
+            const int et = code[e] % n;
+            int lo2 = 0, hi2 = c_len;
+            while (lo2 < hi2) {  // #{j : (Aq[j], q, lo+j) <= (key[e], eq, et)}
+              const int mid = (lo2 + hi2) >> 1;
+              const bool le = !key_less(key[e], eq, et, Aq[mid], q, lo_s[q] + mid);
+              if (le)
+                lo2 = mid + 1;
+              else
+                hi2 = mid;
+            }
+            cnt = lo2;
+          }
+          row[q] = lo_s[q] + cnt;
+        }
+      }
+    }
+    kept_run += tot;
+  }
+  if (!WRITE && threadIdx.x == 0) A.bcount[(long)b * A.S + s] = kept_run;
+  if (WRITE && threadIdx.x == 0 && s == A.S - 1) A.pcount[b] = min(out_base + kept_run, A.cap_e);
+  (void)kept_s;
+}
+
+// ---------------------------------------------------------------------------
+// Host driver.
+
+struct MotPlan {
+  int S, SS, ept;
+  size_t prep_smem, bucket_smem;
+};
+
+int ept_for(int n) {
+  const int per = (n + MT - 1) / MT;
+  if (per <= 1) return 1;
+  if (per <= 2) return 2;
+  if (per <= 4) return 4;
+  if (per <= 8) return 8;
+  if (per <= 16) return 16;
+  if (per <= 32) return 32;
+  return -1;
+}
+
+MotPlan plan_for(int k, int n) {
+  MotPlan p;
+  const long events = (long)k * (n - 1);
+  p.S = (int)std::max(1L, (events + 2047) / 2048);
+  p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
+  while ((long)k * p.SS > 8192) p.SS = std::max(1, p.SS / 2);
+  p.ept = ept_for(n);
+  int kss2 = 1;
+  while (kss2 < k * p.SS) kss2 <<= 1;
+  p.prep_smem = sizeof(double) * (size_t)n + (sizeof(double) + sizeof(int)) * (size_t)p.SS + 16 +
+                (sizeof(double) + sizeof(int)) * (size_t)kss2 + 16;
+  p.bucket_smem = (sizeof(double) + sizeof(int)) * (size_t)CAP;
+  return p;
+}
+
+template <class Kern>
+int launch_cluster(Kern kern, int k, int batch, size_t smem, cudaStream_t st, const MotArgs& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(k, batch, 1);
+  cfg.blockDim = dim3(MT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = k;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  UOT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
+  return UOT_OK;
+}
+
+template <int EPT>
+int run_iteration(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
+  UOT_TRY(launch_cluster(mot_prep<EPT>, a.k, a.batch, p.prep_smem, st, a));
+  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p.bucket_smem));
+  mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch, 0, st, a));
+  return UOT_OK;
+}
+
+int run_plan(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
+  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p.bucket_smem));
+  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p.bucket_smem));
+  mot_plan<false><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  mot_plan<true><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
+template <int EPT>
+int run_all(MotArgs a, const MotPlan& p, cudaStream_t st, bool fw) {
+  if (fw) {
+    for (int t = 0; t < a.max_iters; ++t) {
+      a.t = t;
+      UOT_TRY(run_iteration<EPT>(a, p, st));
+    }
+    // plan of the last recorded iteration: its breakpoints are still in A.
+    // (Converged problems stopped before updating; the others updated f
+    // after the last oracle call, exactly like the reference loop.)
+    MotArgs ap = a;
+    ap.done = nullptr;
+    UOT_TRY(run_plan(ap, p, st));
+    UOT_TRY(launch_cluster(mot_finalize<EPT>, a.k, a.batch, 0, st, a));
+  } else {
+    a.mode = 1;
+    UOT_TRY(launch_cluster(mot_prep<EPT>, a.k, a.batch, p.prep_smem, st, a));
+    UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)p.bucket_smem));
+    mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch, 0, st, a));
+    UOT_TRY(run_plan(a, p, st));
+  }
+  return UOT_OK;
+}
+
+int dispatch(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool fw) {
+  switch (p.ept) {
+    case 1: return run_all<1>(a, p, st, fw);
+    case 2: return run_all<2>(a, p, st, fw);
+    case 4: return run_all<4>(a, p, st, fw);
+    case 8: return run_all<8>(a, p, st, fw);
+    case 16: return run_all<16>(a, p, st, fw);
+    case 32: return run_all<32>(a, p, st, fw);
+  }
+  set_error("lists longer than %d atoms are not supported", 32 * MT);
+  return UOT_INVALID;
+}
+
+// Workspace: ta, A, dcc [B][K][n] doubles; split [B][S+1][K] ints; scal
+// [B][4]; lam [B][K]; bcount [B][S]; done [B]; omega [K]; lens [K];
+// h0/fw/pd [B][T] + iterations (for the plain sweep).
+struct MotWs {
+  size_t off[12];
+  size_t total;
+};
+
+MotWs ws_layout(int batch, int k, int n, int S) {
+  MotWs w;
+  size_t sz[12];
+  const size_t bkn = (size_t)batch * k * n;
+  sz[0] = sizeof(double) * bkn;
+  sz[1] = sizeof(double) * bkn;
+  sz[2] = sizeof(double) * bkn;
+  sz[3] = sizeof(int) * (size_t)batch * (S + 1) * k;
+  sz[4] = sizeof(double) * 4 * (size_t)batch;
+  sz[5] = sizeof(double) * (size_t)batch * k;
+  sz[6] = sizeof(int) * (size_t)batch * S;
+  sz[7] = sizeof(int) * (size_t)batch;
+  sz[8] = sizeof(double) * (size_t)k;
+  sz[9] = sizeof(int) * (size_t)k;
+  sz[10] = sizeof(double) * 3 * (size_t)batch + sizeof(int) * (size_t)batch;
+  sz[11] = sizeof(double) * bkn;  // working copy of the potentials
+  size_t o = 0;
+  for (int i = 0; i < 12; ++i) {
+    w.off[i] = o;
+    o += (sz[i] + 255) / 256 * 256;
+  }
+  w.total = o;
+  return w;
+}
+
+MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const double* omega_host,
+                  const int32_t* lens_host, double rho, cudaStream_t st, int* rc) {
+  MotArgs a{};
+  MotWs L = ws_layout(batch, k, n, p.S);
+  a.batch = batch;
+  a.k = k;
+  a.n = n;
+  a.rho = rho;
+  a.S = p.S;
+  a.SS = p.SS;
+  a.ta = (double*)(ws + L.off[0]);
+  a.A = (double*)(ws + L.off[1]);
+  a.dcc = (double*)(ws + L.off[2]);
+  a.split = (int*)(ws + L.off[3]);
+  a.scal = (double*)(ws + L.off[4]);
+  a.lam = (double*)(ws + L.off[5]);
+  a.bcount = (int*)(ws + L.off[6]);
+  a.done = (int*)(ws + L.off[7]);
+  double* om = (double*)(ws + L.off[8]);
+  a.omega = om;
+  a.lens = nullptr;
+  *rc = UOT_OK;
+  if (lens_host != nullptr) {
+    int* ld = (int*)(ws + L.off[9]);
+    if (cudaMemcpyAsync(ld, lens_host, sizeof(int) * k, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess) {
+      set_error("workspace initialisation failed");
+      *rc = UOT_CUDA;
+    }
+    a.lens = ld;
+  }
+  if (cudaMemcpyAsync(om, omega_host, sizeof(double) * k, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaMemsetAsync(a.done, 0, sizeof(int) * batch, st) != cudaSuccess) {
+    set_error("workspace initialisation failed");
+    *rc = UOT_CUDA;
+  }
+  return a;
+}
+
+int check_sizes(int batch, int k, int n) {
+  if (batch < 1 || k < 2 || n < 1) {
+    set_error("need batch >= 1, k >= 2 inputs, n >= 1 atoms");
+    return UOT_INVALID;
+  }
+  if (k > KMAX) {
+    set_error("at most %d input measures per barycenter on the cluster path", KMAX);
+    return UOT_INVALID;
+  }
+  if (ept_for(n) < 0) {
+    set_error("lists longer than %d atoms are not supported", 32 * MT);
+    return UOT_INVALID;
+  }
+  return UOT_OK;
+}
+
+}  // namespace
+}  // namespace uot
+
+using namespace uot;
+
+extern "C" int uot_mot1d_workspace_size(int32_t batch, int32_t k, int32_t n, size_t* bytes) {
+  UOT_TRY(check_sizes(batch, k, n));
+  MotPlan p = plan_for(k, n);
+  *bytes = ws_layout(batch, k, n, p.S).total;
+  return UOT_OK;
+}
+
+extern "C" int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                                 const double* x, const double* a, const double* omega_host,
+                                 double* f, int32_t* idx, double* mass, int32_t* count,
+                                 int32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  UOT_TRY(check_sizes(batch, k, n));
+  MotPlan p = plan_for(k, n);
+  if (workspace_bytes < ws_layout(batch, k, n, p.S).total) {
+    set_error("uot_mot1d_batched: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  MotArgs A = make_args(batch, k, n, p, (char*)workspace, omega_host, lens, 1.0, st, &rc);
+  UOT_TRY(rc);
+  A.mode = 1;
+  A.x = x;
+  A.a = a;
+  A.f = f;
+  A.out_f = f;
+  A.status = status;
+  A.pidx = idx;
+  A.pmass = mass;
+  A.pcount = count;
+  A.cap_e = k * (n - 1) + 1;
+  A.max_iters = 1;
+  return dispatch(A, p, st, false);
+}
+
+extern "C" int uot_bary_workspace_size(const uot_bary_desc* d, size_t* bytes) {
+  if (d == nullptr) {
+    set_error("null descriptor");
+    return UOT_INVALID;
+  }
+  return uot_mot1d_workspace_size(d->batch, d->k, d->n, bytes);
+}
+
+extern "C" int uot_bary_run(const uot_bary_desc* d, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (d == nullptr) {
+    set_error("null descriptor");
+    return UOT_INVALID;
+  }
+  UOT_TRY(check_sizes(d->batch, d->k, d->n));
+  if (!(d->rho > 0.0) || d->max_iters < 1) {
+    set_error("uot_bary_run: need rho > 0 and max_iters >= 1");
+    return UOT_INVALID;
+  }
+  MotPlan p = plan_for(d->k, d->n);
+  MotWs L = ws_layout(d->batch, d->k, d->n, p.S);
+  if (workspace_bytes < L.total) {
+    set_error("uot_bary_run: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  MotArgs A = make_args(d->batch, d->k, d->n, p, (char*)workspace, d->omega, d->lens, d->rho, st,
+                        &rc);
+  UOT_TRY(rc);
+  A.mode = 0;
+  A.step = d->step;
+  A.max_iters = d->max_iters;
+  A.gap_tol = d->gap_tol;
+  A.early_exit = d->early_exit;
+  A.x = d->x;
+  A.a = d->a;
+  // iterate on a working copy; the caller's f receives the translated result
+  double* work = (double*)((char*)workspace + L.off[11]);
+  UOT_CUDA_TRY(cudaMemcpyAsync(work, d->f, sizeof(double) * (size_t)d->batch * d->k * d->n,
+                               cudaMemcpyDeviceToDevice, st));
+  A.f = work;
+  A.out_f = d->f;
+  A.h0 = d->h0;
+  A.fw_gap = d->fw_gap;
+  A.pd_gap = d->pd_gap;
+  A.iterations = d->iterations;
+  A.status = d->status;
+  A.summary = d->summary;
+  A.pidx = d->idx;
+  A.pmass = d->mass;
+  A.pcount = d->count;
+  A.cap_e = d->k * (d->n - 1) + 1;
+  return dispatch(A, p, st, true);
+}

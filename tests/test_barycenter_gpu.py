@@ -1,0 +1,105 @@
+"""GPU parity of the K-marginal sweep and the barycenter FW (csrc/mot1d.cu)
+against the reference goldens and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2201_00730_b200 as P
+from conftest import cases, golden
+from paper_2201_00730_b200 import _device as D
+from paper_2201_00730_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(z, k):
+    kk = int(z[f"c{k}_k"])
+    return [P.DiscreteMeasure(z[f"c{k}_x{q}"], z[f"c{k}_a{q}"]) for q in range(kk)], kk
+
+
+def test_mot_goldens():
+    z = golden("mot.npz")
+    for k in cases(z):
+        inputs, kk = _inputs(z, k)
+        plan, duals = P.solve_mot_1d(inputs, z[f"c{k}_w"])
+        np.testing.assert_array_equal(plan.indices, z[f"c{k}_idx"], err_msg=str(k))
+        tot = float(np.sum(z[f"c{k}_m"]))
+        np.testing.assert_allclose(plan.mass, z[f"c{k}_m"], rtol=0, atol=1e-13 * tot)
+        scale = max(1e-300, max(np.abs(z[f"c{k}_f{q}"]).max() for q in range(kk)))
+        for q in range(kk):
+            assert np.abs(duals.potentials[q] - z[f"c{k}_f{q}"]).max() <= 1e-12 * max(scale, 1.0), k
+
+
+def test_mot_known_answers():
+    # tests/test_barycenter.py:58-66 of the reference (single atoms)
+    inputs = [P.DiscreteMeasure([float(q)], [1.0]) for q in range(3)]
+    w = np.full(3, 1 / 3)
+    plan, duals = P.solve_mot_1d(inputs, w)
+    assert len(plan) == 1 and plan.mass[0] == 1.0
+    cost, _ = P.multimarginal_cost([0.0, 1.0, 2.0], w)
+    assert duals.potentials[0][0] == pytest.approx(cost)
+    assert duals.potentials[1][0] == 0.0 and duals.potentials[2][0] == 0.0
+    with pytest.raises(P.MassBalanceError):
+        P.solve_mot_1d([inputs[0], P.DiscreteMeasure([1.0], [2.0])], np.array([0.5, 0.5]))
+
+
+def test_barycenter_goldens():
+    z = golden("barycenter.npz")
+    tight = 0
+    for k in cases(z):
+        inputs, kk = _inputs(z, k)
+        rho, iters, ls = z[f"c{k}_par"]
+        step = "linesearch" if ls else "harmonic"
+        prob = P.BarycenterProblem(tuple(inputs), z[f"c{k}_w"], float(rho))
+        rep, plan = P.fw_barycenter(prob, P.FwConfig(step, int(iters), 1e-16))
+        assert rep.iterations == int(iters)
+        np.testing.assert_allclose(rep.trace["h0"], z[f"c{k}_h0"], rtol=1e-9, atol=1e-12,
+                                   err_msg=str(k))
+        scale = max(np.abs(z[f"c{k}_f{q}"]).max() for q in range(kk))
+        err = max(np.abs(rep.final.potentials[q] - z[f"c{k}_f{q}"]).max() for q in range(kk))
+        # ternary line search conditioning, see tests/test_fw_gpu.py
+        assert err <= (1e-9 if step == "harmonic" else 1e-6) * scale, (k, err / scale)
+        if err <= 1e-12 * scale:
+            tight += 1
+            np.testing.assert_array_equal(plan.indices, z[f"c{k}_idx"])
+            bar = P.extract_barycenter(plan, inputs, z[f"c{k}_w"])
+            np.testing.assert_allclose(bar.points, z[f"c{k}_bar_x"], rtol=1e-12, atol=1e-14)
+    assert tight >= 2
+
+
+def test_barycenter_batched_cfg5_shape_vs_oracle():
+    xs, ws = S.cfg5_batch(count=3, n=1024)
+    w = np.full(16, 1 / 16)
+    r = P.fw_barycenter_batched(xs, ws, w, 1.0, 12, "linesearch")
+    assert (D.to_np(r.status) == 0).all()
+    for p in (0, 2):
+        out = O.fw_barycenter_fixed(list(xs[p]), list(ws[p]), w, 1.0, 12)
+        np.testing.assert_allclose(D.to_np(r.h0[p]), out["h0"], rtol=1e-9)
+        f = D.to_np(r.f[p])
+        scale = max(np.abs(v).max() for v in out["pots"])
+        err = max(np.abs(f[q] - out["pots"][q]).max() for q in range(16))
+        assert err <= 1e-6 * scale
+    rh = P.fw_barycenter_batched(xs, ws, w, 1.0, 12, "harmonic")
+    out = O.fw_barycenter_fixed(list(xs[1]), list(ws[1]), w, 1.0, 12, step="harmonic")
+    f = D.to_np(rh.f[1])
+    scale = max(np.abs(v).max() for v in out["pots"])
+    assert max(np.abs(f[q] - out["pots"][q]).max() for q in range(16)) <= 1e-9 * scale
+    c = int(rh.count[1].item())
+    np.testing.assert_array_equal(D.to_np(rh.idx[1, :c]), out["plan"][0])
+
+
+def test_mot_full_cfg5_size_vs_oracle():
+    xs, ws = S.cfg5_batch(count=2)
+    w = np.full(16, 1 / 16)
+    ws = ws / ws.sum(axis=2, keepdims=True)  # balanced inputs
+    f, idx, mass, count, st = P.solve_mot_1d_batched(xs, ws, w)
+    for p in range(2):
+        ii, mm, pots = O.solve_mot_1d(list(xs[p]), list(ws[p]), w)
+        c = int(count[p].item())
+        got = D.to_np(idx[p, :c])
+        np.testing.assert_array_equal(got, ii)
+        np.testing.assert_allclose(D.to_np(mass[p, :c]), mm, rtol=0, atol=1e-13)
+        fd = D.to_np(f[p])
+        for q in range(16):
+            assert np.abs(fd[q] - pots[q]).max() <= 1e-10
