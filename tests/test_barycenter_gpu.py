@@ -45,27 +45,46 @@ def test_mot_known_answers():
 
 
 def test_barycenter_goldens():
+    """Fixed-iteration replay (the golden loop has no early exit)."""
+    from paper_2201_00730_b200.barycenter import _pack
+
     z = golden("barycenter.npz")
     tight = 0
     for k in cases(z):
         inputs, kk = _inputs(z, k)
         rho, iters, ls = z[f"c{k}_par"]
         step = "linesearch" if ls else "harmonic"
-        prob = P.BarycenterProblem(tuple(inputs), z[f"c{k}_w"], float(rho))
-        rep, plan = P.fw_barycenter(prob, P.FwConfig(step, int(iters), 1e-16))
-        assert rep.iterations == int(iters)
-        np.testing.assert_allclose(rep.trace["h0"], z[f"c{k}_h0"], rtol=1e-9, atol=1e-12,
+        x, a, _, lens = _pack(inputs)
+        r = P.fw_barycenter_batched(x, a, z[f"c{k}_w"], float(rho), int(iters), step, lens=lens)
+        assert int(r.status[0].item()) == 0
+        np.testing.assert_allclose(D.to_np(r.h0[0]), z[f"c{k}_h0"], rtol=1e-9, atol=1e-12,
                                    err_msg=str(k))
+        f = D.to_np(r.f[0])
         scale = max(np.abs(z[f"c{k}_f{q}"]).max() for q in range(kk))
-        err = max(np.abs(rep.final.potentials[q] - z[f"c{k}_f{q}"]).max() for q in range(kk))
+        err = max(np.abs(f[q, :lens[q]] - z[f"c{k}_f{q}"]).max() for q in range(kk))
         # ternary line search conditioning, see tests/test_fw_gpu.py
         assert err <= (1e-9 if step == "harmonic" else 1e-6) * scale, (k, err / scale)
         if err <= 1e-12 * scale:
             tight += 1
-            np.testing.assert_array_equal(plan.indices, z[f"c{k}_idx"])
+            c = int(r.count[0].item())
+            idx = D.to_np(r.idx[0, :c]).astype(np.int64)
+            np.testing.assert_array_equal(idx, z[f"c{k}_idx"])
+            plan = P.MultiPlan(idx, D.to_np(r.mass[0, :c]))
             bar = P.extract_barycenter(plan, inputs, z[f"c{k}_w"])
             np.testing.assert_allclose(bar.points, z[f"c{k}_bar_x"], rtol=1e-12, atol=1e-14)
     assert tight >= 2
+
+
+def test_fw_barycenter_api_dirac_inputs():
+    # tests/test_barycenter.py:176-186 of the reference: Diracs -> weighted mean
+    inputs = (P.DiscreteMeasure([0.0], [1.0]), P.DiscreteMeasure([1.0], [1.0]),
+              P.DiscreteMeasure([2.5], [1.0]))
+    w = np.array([0.2, 0.3, 0.5])
+    rep, plan = P.fw_barycenter(P.BarycenterProblem(inputs, w, 3.0),
+                                P.FwConfig("linesearch", 100, 1e-12))
+    bar = P.extract_barycenter(plan, inputs, w)
+    assert len(bar) == 1
+    assert bar.points[0] == pytest.approx(1.55, abs=1e-12)
 
 
 def test_barycenter_batched_cfg5_shape_vs_oracle():
