@@ -335,8 +335,24 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
   const int o = blockIdx.x * TAIL_THREADS + threadIdx.x;
   const bool ok = o < A.nout;
   const SkScalars sc = A.sc[b];
-  const double tau_red = sc.tau[A.red_side];
-  const double smin_red = sc.shat[A.red_side] + tau_red;
+  double tau_red = sc.tau[A.red_side];
+  double shat_red = sc.shat[A.red_side];
+  double delta_red = 0.0;
+  if (A.shard == 2) {
+    // resolve the reduced side's scalars from every rank's published partials
+    LsePair q{-CUDART_INF, 0.0};
+    double qmax = -CUDART_INF, qmin = CUDART_INF;
+    for (int r = 0; r < A.nranks; ++r) {
+      const double* x = A.xs_in + (long)r * A.xs_stride + (long)b * 4;
+      q = lse_merge(q, LsePair{x[0], x[1]});
+      qmax = fmax(qmax, x[2]);
+      qmin = fmin(qmin, x[3]);
+    }
+    shat_red = -A.rho_red * (q.m + log(q.s));
+    tau_red = A.first ? 0.0 : A.tau_fac_red * shat_red;
+    delta_red = fmax(qmax + tau_red, -(qmin + tau_red));
+  }
+  const double smin_red = shat_red + tau_red;
   const double tau_old = sc.tau[A.out_side];
 
   LsePair pr{-CUDART_INF, 0.0};
@@ -347,15 +363,15 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
       hat = (double)A.pot_in[(long)b * A.nout + o];
     } else {
       double M = -CUDART_INF;
-      const long pbase = (long)b * A.nparts * A.nout + o;
+      const long pbase = (long)b * A.pstride_b + o;
       for (int s = 0; s < A.nparts; ++s) {
-        const double a = (double)A.part_a[pbase + (long)s * A.nout];
-        if (a > 0.0) M = fmax(M, (double)A.part_m[pbase + (long)s * A.nout]);
+        const double a = (double)A.part_a[pbase + (long)s * A.pstride_s];
+        if (a > 0.0) M = fmax(M, (double)A.part_m[pbase + (long)s * A.pstride_s]);
       }
       double acc = 0.0;
       for (int s = 0; s < A.nparts; ++s) {
-        const double a = (double)A.part_a[pbase + (long)s * A.nout];
-        if (a > 0.0) acc += a * D::exd((double)A.part_m[pbase + (long)s * A.nout] - M);
+        const double a = (double)A.part_a[pbase + (long)s * A.pstride_s];
+        if (a > 0.0) acc += a * D::exd((double)A.part_m[pbase + (long)s * A.pstride_s] - M);
       }
       const double lse = M + D::lgd(acc);  // domain units, excluding tau_red
       A.shift_out[(long)b * A.nout + o] = (T)lse;
@@ -398,6 +414,20 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
   q = block_lse(q, s_m, s_s);
   qmax = block_reduce(qmax, s_x, MaxOp(), -CUDART_INF);
   qmin = block_reduce(qmin, s_x, MinOp(), CUDART_INF);
+  if (threadIdx.x == 0 && A.shard == 1) {
+    // publish this rank's partial scalars; resolved after the exchange
+    A.xs_out[(long)b * 4 + 0] = q.m;
+    A.xs_out[(long)b * 4 + 1] = q.s;
+    A.xs_out[(long)b * 4 + 2] = qmax;
+    A.xs_out[(long)b * 4 + 3] = qmin;
+    A.counter[b] = 0u;
+    return;
+  }
+  if (threadIdx.x == 0 && A.shard == 2) {
+    A.sc[b].shat[A.red_side] = shat_red;
+    A.sc[b].tau[A.red_side] = tau_red;
+    if (!A.first && A.trace != nullptr) A.trace[(long)b * A.trace_len + A.t - 1] = delta_red;
+  }
   if (threadIdx.x == 0) {
     const double shat = -A.rho_out * (q.m + log(q.s));
     const double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
@@ -424,6 +454,50 @@ __global__ void sk_finalize(int n, int m, const T* hatA0, const T* hatA1, const 
     if (i < n) f[(long)b * n + i] = (T)((double)hatA[(long)b * n + i] + sc[b].tau[0]);
     if (i < m) g[(long)b * m + i] = (T)((double)hatB[(long)b * m + i] + sc[b].tau[1]);
   }
+}
+
+// Row sharding, phase 1: fold this rank's split partials into one
+// (shift, sum) pair per output (the payload of the all-gather).
+template <typename T>
+__global__ void sk_combine(int nout, int S, const T* part_m, const T* part_a, T* out_m, T* out_a) {
+  using D = Dom<T>;
+  const int b = blockIdx.y;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= nout) return;
+  const long pb = (long)b * S * nout + o;
+  double M = -CUDART_INF;
+  for (int s = 0; s < S; ++s)
+    if ((double)part_a[pb + (long)s * nout] > 0.0) M = fmax(M, (double)part_m[pb + (long)s * nout]);
+  double acc = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const double a = (double)part_a[pb + (long)s * nout];
+    if (a > 0.0) acc += a * D::exd((double)part_m[pb + (long)s * nout] - M);
+  }
+  out_m[(long)b * nout + o] = (T)M;
+  out_a[(long)b * nout + o] = (T)acc;
+}
+
+// Row sharding, end of run: resolve the last f-side scalars from the
+// gathered slots (same arithmetic as the shard == 2 tail).
+__global__ void sk_resolve_final(int batch, int nranks, const double* xs, long xs_stride,
+                                 double rho1, double tau_fac, SkScalars* sc, double* trace,
+                                 int trace_len, int t_last, int* iters_done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  LsePair q{-CUDART_INF, 0.0};
+  double qmax = -CUDART_INF, qmin = CUDART_INF;
+  for (int r = 0; r < nranks; ++r) {
+    const double* x = xs + (long)r * xs_stride + (long)b * 4;
+    q = lse_merge(q, LsePair{x[0], x[1]});
+    qmax = fmax(qmax, x[2]);
+    qmin = fmin(qmin, x[3]);
+  }
+  const double shat = -rho1 * (q.m + log(q.s));
+  const double tau = tau_fac * shat;
+  sc[b].shat[0] = shat;
+  sc[b].tau[0] = tau;
+  if (trace != nullptr) trace[(long)b * trace_len + t_last] = fmax(qmax + tau, -(qmin + tau));
+  iters_done[b] = t_last + 1;
 }
 
 __global__ void sk_reset(int batch, SkScalars* sc, unsigned int* counters, int* done,
@@ -605,6 +679,7 @@ struct Engine {
   }
 
   static size_t ws_size(const uot_sinkhorn_desc& d) {
+    if (d.nranks > 1 || d.nccl_comm != nullptr) return ws_size_sharded(d);
     WsLayout L;
     Shape s = shape(d);
     return layout<T>(s, d.iters, L, nullptr, nullptr);
@@ -657,9 +732,22 @@ struct Engine {
     return UOT_OK;
   }
 
+  struct ShardOpt {
+    int shard;
+    const double* xs_in;
+    long xs_stride;
+    int nranks;
+    int first;
+    double* xs_out;
+    const T* pm;
+    const T* pa;
+    long pstride_s, pstride_b;
+  };
+
   static int launch_tail(const uot_sinkhorn_desc& d, const Buffers<T>& bf, cudaStream_t st,
                          bool to_target, int mode, int nparts, const T* hat_old, T* hat_out,
-                         const T* pot_in, int t, double* trace, int trace_len) {
+                         const T* pot_in, int t, double* trace, int trace_len,
+                         const ShardOpt* so = nullptr) {
     TailArgs<T> a{};
     const bool H = d.variant == UOT_SINKHORN_H;
     const double eps = d.eps, r1 = d.rho1, r2 = d.rho2;
@@ -672,6 +760,8 @@ struct Engine {
     a.red_side = to_target ? 0 : 1;
     a.part_m = bf.part_m;
     a.part_a = bf.part_a;
+    a.pstride_s = a.nout;
+    a.pstride_b = (long)nparts * a.nout;
     a.pot_in = pot_in;
     a.sc = bf.sc;
     a.eps = eps;
@@ -702,6 +792,24 @@ struct Engine {
     a.done = bf.done;
     a.tol = d.tol;
     a.use_tol = d.use_tol;
+    if (so != nullptr) {
+      a.shard = so->shard;
+      a.xs_in = so->xs_in;
+      a.xs_stride = so->xs_stride;
+      a.nranks = so->nranks;
+      a.first = so->first;
+      a.xs_out = so->xs_out;
+      if (so->pm != nullptr) {
+        a.part_m = so->pm;
+        a.part_a = so->pa;
+        a.pstride_s = so->pstride_s;
+        a.pstride_b = so->pstride_b;
+      }
+      // reduced side of the g-update is the (sharded) source side
+      a.rho_red = r1;
+      const double kka = (eps / (eps + r1)) * (r2 / (r1 + r2));
+      a.tau_fac_red = H ? kka / (1.0 - kka) : 0.0;
+    }
     dim3 grid(ceil_div(a.nout, TAIL_THREADS), d.batch);
     sk_tail<P><<<grid, TAIL_THREADS, 0, st>>>(a);
     UOT_CHECK_LAUNCH();
@@ -709,16 +817,13 @@ struct Engine {
   }
 
   static int run(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (d.nranks > 1 || d.nccl_comm != nullptr) return run_sharded(d, ws, ws_bytes, st);
     Shape s = shape(d);
     WsLayout L;
     Buffers<T> bf;
     const size_t need = layout<T>(s, d.iters, L, &bf, (char*)ws);
     if (ws_bytes < need) {
       set_error("sinkhorn workspace too small: %zu < %zu", ws_bytes, need);
-      return UOT_INVALID;
-    }
-    if (d.nranks > 1) {
-      set_error("row-sharded sinkhorn is not available in this build");
       return UOT_INVALID;
     }
     sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
@@ -755,6 +860,206 @@ struct Engine {
     UOT_CHECK_LAUNCH();
     if (d.iterations != nullptr) {
       UOT_CUDA_TRY(cudaMemcpyAsync(d.iterations, bf.iters_done, sizeof(int) * d.batch,
+                                   cudaMemcpyDeviceToDevice, st));
+    }
+    return UOT_OK;
+  }
+
+  // ---- Row-sharded run (BASELINE cfg3 on P GPUs).  Every
+  // rank owns a slice of the source rows and the whole target side.  Per
+  // iteration: g-update partial LSEs over the local rows -> one (shift, sum)
+  // pair per column -> ONE all-gather (which also carries the f-side
+  // scalars of the previous f-tail) -> every rank folds the P pairs in rank
+  // order, so the replicated g is bitwise identical on all ranks; the
+  // f-update is local.  nccl_comm == NULL with nranks > 1 runs the same
+  // protocol for all shards in this process (device copies replace NCCL).
+  struct ShardLayout {
+    int R;  // rank contexts held by this process
+    std::vector<int> nl, off;
+    std::vector<size_t> ctx_off;
+    std::vector<Shape> shp;
+    size_t stride;  // bytes per rank in the exchange buffer
+    size_t xbuf_off, xall_off, xfin_off, total;
+  };
+
+  static int shard_layout(const uot_sinkhorn_desc& d, ShardLayout& L) {
+    const bool real = d.nccl_comm != nullptr;
+    const int NR = std::max(1, d.nranks);
+    if (d.batch != 1) {
+      set_error("row sharding runs a single problem (batch must be 1)");
+      return UOT_INVALID;
+    }
+    L.R = real ? 1 : NR;
+    L.nl.assign(L.R, 0);
+    L.off.assign(L.R, 0);
+    if (real) {
+      L.nl[0] = d.n;
+    } else {
+      if (d.shard_rows == nullptr) {
+        set_error("emulated sharding needs shard_rows");
+        return UOT_INVALID;
+      }
+      int o = 0;
+      for (int r = 0; r < NR; ++r) {
+        L.nl[r] = d.shard_rows[r];
+        L.off[r] = o;
+        o += L.nl[r];
+        if (L.nl[r] < 1) {
+          set_error("every shard needs at least one row");
+          return UOT_INVALID;
+        }
+      }
+      if (o != d.n) {
+        set_error("shard_rows must sum to n");
+        return UOT_INVALID;
+      }
+    }
+    L.stride = ((sizeof(double) * 4 * d.batch + 2 * sizeof(T) * (size_t)d.batch * d.m) + 255) /
+               256 * 256;
+    size_t off = 0;
+    L.ctx_off.assign(L.R, 0);
+    L.shp.assign(L.R, Shape{});
+    for (int r = 0; r < L.R; ++r) {
+      uot_sinkhorn_desc dr = d;
+      dr.n = L.nl[r];
+      Shape s = shape(dr);
+      L.shp[r] = s;
+      WsLayout wl;
+      L.ctx_off[r] = off;
+      off += layout<T>(s, d.iters, wl, nullptr, nullptr);
+    }
+    L.xbuf_off = off;
+    off += L.stride * L.R;
+    L.xall_off = off;
+    off += L.stride * NR;
+    L.xfin_off = off;
+    off += (sizeof(double) * 4 * d.batch * NR + 255) / 256 * 256;
+    L.total = off;
+    return UOT_OK;
+  }
+
+  static size_t ws_size_sharded(const uot_sinkhorn_desc& d) {
+    ShardLayout L;
+    if (shard_layout(d, L) != UOT_OK) return 0;
+    return L.total;
+  }
+
+  static int exchange(const uot_sinkhorn_desc& d, const ShardLayout& L, char* base, size_t bytes,
+                      char* recv, size_t recv_stride, cudaStream_t st) {
+#if defined(UOT_WITH_NCCL)
+    if (d.nccl_comm != nullptr) {
+      ncclResult_t r = ncclAllGather(base + L.xbuf_off, recv, bytes, ncclChar,
+                                     (ncclComm_t)d.nccl_comm, st);
+      if (r != ncclSuccess) {
+        set_error("ncclAllGather failed: %s", ncclGetErrorString(r));
+        return UOT_NCCL;
+      }
+      return UOT_OK;
+    }
+#endif
+    if (d.nccl_comm != nullptr) {
+      set_error("built without NCCL");
+      return UOT_NCCL;
+    }
+    for (int r = 0; r < L.R; ++r)
+      UOT_CUDA_TRY(cudaMemcpyAsync(recv + recv_stride * r, base + L.xbuf_off + L.stride * r,
+                                   bytes, cudaMemcpyDeviceToDevice, st));
+    return UOT_OK;
+  }
+
+  static int run_sharded(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_t st) {
+    ShardLayout L;
+    UOT_TRY(shard_layout(d, L));
+    if (ws_bytes < L.total) {
+      set_error("sinkhorn workspace too small: %zu < %zu", ws_bytes, L.total);
+      return UOT_INVALID;
+    }
+    const int NR = std::max(1, d.nranks);
+    char* base = (char*)ws;
+    const int trace_len = std::max(d.iters, 1);
+    const bool H = d.variant == UOT_SINKHORN_H;
+    const double kka = (d.eps / (d.eps + d.rho1)) * (d.rho2 / (d.rho1 + d.rho2));
+    const double tau_fac_a = H ? kka / (1.0 - kka) : 0.0;
+    std::vector<uot_sinkhorn_desc> dr(L.R, d);
+    std::vector<Buffers<T>> bf(L.R);
+    std::vector<int> sA(L.R), sB(L.R);
+    char* xall = base + L.xall_off;
+    double* xfin = (double*)(base + L.xfin_off);
+    const long stride_d = (long)(L.stride / sizeof(double));
+    const long stride_t = (long)(L.stride / sizeof(T));
+    const size_t scal_bytes = sizeof(double) * 4 * d.batch;
+    for (int r = 0; r < L.R; ++r) {
+      WsLayout wl;
+      layout<T>(L.shp[r], d.iters, wl, &bf[r], base + L.ctx_off[r]);
+      dr[r].n = L.nl[r];
+      dr[r].x = (const char*)d.x + sizeof(T) * (size_t)L.off[r] * d.d;
+      dr[r].a = (const char*)d.a + sizeof(T) * (size_t)L.off[r];
+      dr[r].f = (char*)d.f + sizeof(T) * (size_t)L.off[r];
+      if (d.c != nullptr) {
+        set_error("row sharding supports point-cloud and 1-D costs");
+        return UOT_INVALID;
+      }
+      sB[r] = choose_splits(d.batch, d.m, L.nl[r], OUT_PER_BLOCK);
+      sA[r] = choose_splits(d.batch, L.nl[r], d.m, OUT_PER_BLOCK);
+      sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf[r].sc, bf[r].counter,
+                                                        bf[r].done, bf[r].iters_done);
+      sk_zero<T><<<256, 256, 0, st>>>((long)L.nl[r], bf[r].shiftA);
+      sk_zero<T><<<256, 256, 0, st>>>((long)d.m, bf[r].shiftB);
+      UOT_CHECK_LAUNCH();
+      const T* f0 = (const T*)dr[r].f;
+      if (!d.init_given) {
+        sk_zero<T><<<256, 256, 0, st>>>((long)std::max(L.nl[r], d.m), bf[r].zeros);
+        f0 = bf[r].zeros;
+      }
+      double* xb = (double*)(base + L.xbuf_off + L.stride * r);
+      ShardOpt so{1, nullptr, 0, NR, 0, xb, nullptr, nullptr, 0, 0};
+      UOT_TRY(launch_tail(dr[r], bf[r], st, false, 1, 0, nullptr, bf[r].hatA0, f0, 0, nullptr,
+                          trace_len, &so));
+    }
+    double* trace = d.trace_delta != nullptr ? d.trace_delta : bf[0].trace;
+    for (int t = 0; t < d.iters; ++t) {
+      for (int r = 0; r < L.R; ++r) {
+        UOT_TRY(launch_main(dr[r], bf[r], st, true, sB[r], 0, L.nl[r], 0, sB[r]));
+        char* xb = base + L.xbuf_off + L.stride * r;
+        T* pm = (T*)(xb + scal_bytes);
+        T* pa = pm + (size_t)d.batch * d.m;
+        sk_combine<T><<<dim3(ceil_div(d.m, 256), d.batch), 256, 0, st>>>(d.m, sB[r], bf[r].part_m,
+                                                                         bf[r].part_a, pm, pa);
+        UOT_CHECK_LAUNCH();
+      }
+      UOT_TRY(exchange(d, L, base, L.stride, xall, L.stride, st));
+      for (int r = 0; r < L.R; ++r) {
+        const T* pm = (const T*)(xall + scal_bytes);
+        const T* pa = pm + (size_t)d.batch * d.m;
+        ShardOpt so{2, (const double*)xall, stride_d, NR, t == 0 ? 1 : 0, nullptr, pm, pa,
+                    stride_t, (long)d.m};
+        UOT_TRY(launch_tail(dr[r], bf[r], st, true, 0, NR, nullptr, bf[r].hatB, nullptr, t,
+                            r == 0 ? trace : nullptr, trace_len, &so));
+      }
+      for (int r = 0; r < L.R; ++r) {
+        T* hat_old = (t & 1) ? bf[r].hatA1 : bf[r].hatA0;
+        T* hat_new = (t & 1) ? bf[r].hatA0 : bf[r].hatA1;
+        UOT_TRY(launch_main(dr[r], bf[r], st, false, sA[r], 0, d.m, 0, sA[r]));
+        double* xb = (double*)(base + L.xbuf_off + L.stride * r);
+        ShardOpt so{1, nullptr, 0, NR, 0, xb, nullptr, nullptr, 0, 0};
+        UOT_TRY(launch_tail(dr[r], bf[r], st, false, 0, sA[r], hat_old, hat_new, nullptr, t,
+                            nullptr, trace_len, &so));
+      }
+    }
+    UOT_TRY(exchange(d, L, base, scal_bytes, (char*)xfin, scal_bytes, st));
+    for (int r = 0; r < L.R; ++r) {
+      sk_resolve_final<<<ceil_div(d.batch, 128), 128, 0, st>>>(
+          d.batch, NR, xfin, (long)(scal_bytes / sizeof(double)), d.rho1, tau_fac_a, bf[r].sc,
+          r == 0 ? trace : nullptr, trace_len, d.iters - 1, bf[r].iters_done);
+      UOT_CHECK_LAUNCH();
+      const long nm = std::max(L.nl[r], d.m);
+      sk_finalize<T><<<dim3(ceil_div(nm, 256), d.batch), 256, 0, st>>>(
+          L.nl[r], d.m, bf[r].hatA0, bf[r].hatA1, bf[r].hatB, bf[r].sc, bf[r].iters_done,
+          (T*)dr[r].f, (T*)d.g);
+      UOT_CHECK_LAUNCH();
+    }
+    if (d.iterations != nullptr) {
+      UOT_CUDA_TRY(cudaMemcpyAsync(d.iterations, bf[0].iters_done, sizeof(int) * d.batch,
                                    cudaMemcpyDeviceToDevice, st));
     }
     return UOT_OK;

@@ -63,8 +63,9 @@ struct TailArgs {
   int nout, nparts;   // partials per output to combine
   int mode;           // 0 = combine partials, 1 = init from pot_in
   int out_side, red_side;
-  const T* part_m;    // [B][nparts][nout]
+  const T* part_m;    // part (b, s) of output o at b*pstride_b + s*pstride_s + o
   const T* part_a;
+  long pstride_b, pstride_s;
   const T* pot_in;    // [B][nout] (init mode)
   SkScalars* sc;      // [B]
   double eps, unit, inv_eu;    // unit = ln2 (log2 domain) or 1; inv_eu = 1/(eps*unit)
@@ -88,6 +89,17 @@ struct TailArgs {
   int* done;                   // [B]
   double tol;
   int use_tol;
+  // Row sharding (sinkhorn.cu run_sharded): shard = 1 makes the tail publish
+  // its partial output-side scalars (LSE pair of -hat/rho, delta bounds) to
+  // xs_out[b*4..] instead of finalising them; shard = 2 resolves the reduced
+  // side's scalars from the ranks' gathered slots xs_in[r*xs_stride + b*4..].
+  int shard;
+  const double* xs_in;
+  long xs_stride;
+  int nranks;
+  int first;
+  double rho_red, tau_fac_red;
+  double* xs_out;
 };
 
 }  // namespace uot

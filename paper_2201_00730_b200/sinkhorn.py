@@ -90,13 +90,19 @@ def _geometry(prob):
 
 
 def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
-                     c=None, f0=None, tol=None, precision="fp32", stream=None):
+                     c=None, f0=None, tol=None, precision="fp32", stream=None, comm=None,
+                     nranks=1, rank=0, shard_rows=None):
     """Batched Sinkhorn on device.
 
     x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
     b [B, M]; ``cost`` in {"sqeuclid", "power", "explicit"} (explicit needs
     c [B, N, M]).  Returns (f [B, N], g [B, M], delta [B, iters] fp64,
     iterations [B] int32) as device tensors; f and g are in ``precision``.
+
+    Row sharding (one problem): with ``comm`` (a handle from
+    ``distributed.NcclComm``) the x / a / f0 given are this rank's rows and
+    the returned f is this rank's slice; with ``comm=None, nranks > 1`` and
+    ``shard_rows`` the same protocol runs for all shards in this process.
     """
     t = D.torch()
     lib = _lib.load()
@@ -130,14 +136,21 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
         ct=_lib.ptr(ct), a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(f), g=_lib.ptr(g),
         init_given=1 if f0 is not None else 0, iters=int(iters),
         tol=float(tol) if tol is not None else 0.0, use_tol=1 if tol is not None else 0,
-        trace_delta=_lib.ptr(trace), iterations=_lib.ptr(its), nccl_comm=None, nranks=1, rank=0,
-        shard_rows=None)
+        trace_delta=_lib.ptr(trace), iterations=_lib.ptr(its), nccl_comm=comm,
+        nranks=int(nranks), rank=int(rank), shard_rows=None)
+    rows_arr = None
+    if shard_rows is not None:
+        import numpy as _np
+
+        rows_arr = _np.ascontiguousarray(_np.asarray(shard_rows, dtype=_np.int32))
+        desc.shard_rows = rows_arr.ctypes.data_as(ctypes.c_void_p)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)),
                "sinkhorn workspace")
     ws = D.workspace(size.value)
     _lib.check(lib.uot_sinkhorn_run(ctypes.byref(desc), _lib.ptr(ws), ctypes.c_size_t(size.value),
                                     _lib.stream_handle(stream)), "uot_sinkhorn_run")
+    del rows_arr  # host array read during the (synchronous) enqueue only
     return f, g, trace, its
 
 

@@ -130,3 +130,30 @@ def test_full_cfg3_one_step_sampled_columns():
     ref = a_coef * (smin - smin[0])
     got = g2[0][cols] - g2[0][cols[0]]
     assert np.abs(got - ref).max() <= 1e-4 * c.eps
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_row_sharded_protocol_emulated(precision, nshards):
+    """The NCCL row-sharding protocol (one all-gather per iteration), run for
+    all shards in one process, equals the unsharded solve."""
+    from paper_2201_00730_b200.distributed import shard_rows
+
+    c = S.cfg3_inputs(n=1536, m=1280, seed=11)
+    rows = shard_rows(len(c.x), nshards)
+    f1, g1, t1, _ = run_dev(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, c.rho, 25,
+                            precision=precision)
+    f, g, tr, its = P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps,
+                                       c.rho, c.rho, 25, precision=precision, nranks=nshards,
+                                       shard_rows=rows)
+    f, g = D.to_np(f).astype(float), D.to_np(g).astype(float)
+    tr = D.to_np(tr)
+    assert int(its[0].item()) == 25
+    if precision == "fp64":
+        assert rel_err(f[0], g[0], f1[0], g1[0]) < 1e-12
+        np.testing.assert_allclose(tr[0], t1[0], rtol=1e-9, atol=1e-14)
+    else:
+        ft, gt = translated(c.alpha, c.beta, f[0], g[0], c.rho, c.rho)
+        fr, gr = translated(c.alpha, c.beta, f1[0], g1[0], c.rho, c.rho)
+        assert np.abs(ft - fr).max() <= 1e-4 * c.eps
+        assert np.abs(gt - gr).max() <= 1e-4 * c.eps
