@@ -1,16 +1,18 @@
-"""Benchmark driver (contract: see the task README / DESIGN.md §Measurement).
+"""Benchmark driver (contract: DESIGN.md §Measurement).
 
-Default workload = BASELINE.json's headline metric quoted on config 3:
+Headline workload = BASELINE.json's metric as quoted on config 3:
 TI-Sinkhorn (H variant) on two seeded 8-component 2-D Gaussian mixtures,
 N = M = 65536, fp32 log-domain, eps = 1e-2 * max|x - y|^2, KL rho = 1.
 A "step" is one full H-Sinkhorn iteration (g half-step + f half-step) over
-the whole problem; value = iterations/s of the whole job.
+the whole problem; ``value`` = iterations/s of the whole job.  With
+``--gpus N`` under torchrun the single problem is row-sharded across the
+ranks (one NCCL all-gather per iteration) and the step time is the max over
+ranks.  The same line carries the other BASELINE configs as ``secondary``
+entries (batched FW cfg2, barycenter cfg5, cfg1, cfg4), each sharded by
+problem across ranks with no communication.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-
-Under torchrun (N > 1) the single problem is row-sharded across ranks (one
-NCCL all-gather of per-column log-sum-exp partials per iteration) and the
-step time is the max over ranks of the device-timed step.
+                    [--no-secondary]
 """
 
 from __future__ import annotations
@@ -31,14 +33,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TI-Sinkhorn iter/s (N=M=65536, d=2)"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+CFG2_BYTES_PER_ITER = 268435456  # 4096 * 32 * (1024 + 1024)
+CFG5_BYTES_PER_ITER = 268435456  # 64 * 16 * 8192 * 32
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return json.load(fh)
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -52,7 +56,6 @@ class ClockSampler:
         self.gpu = gpu_index
         self.rows = []
         self.proc = None
-        self.thread = None
 
     def __enter__(self):
         try:
@@ -60,11 +63,10 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
-        time.sleep(0.25)
+        time.sleep(0.3)
         return self
 
     def _read(self):
@@ -84,38 +86,377 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
+        busy = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(busy or sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
 
 
+def cuda_timer():
+    import torch
+
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+
+    class T:
+        def __enter__(self):
+            e0.record(st)
+            return self
+
+        def __exit__(self, *exc):
+            e1.record(st)
+            torch.cuda.synchronize()
+            self.ms = e0.elapsed_time(e1)
+
+    return T()
+
+
+def max_over_ranks(v, world, dev):
+    if world == 1:
+        return v
+    import torch
+
+    t = torch.tensor([float(v)], device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port (C, fp64) of the reference's column softmin
-# (src/sinkhorn.py:93-100 over src/entropies.py:84-92) on a bounded sample.
+# CPU baselines: the oracle port (fp64 restatement of the reference path,
+# oracle/) timed on the box's host cores on a bounded sample.
 
 
-def cpu_sinkhorn_rate(c, cols=512):
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_cfg3(c, cols=512):
     import oracle as O
 
-    threads = len(os.sched_getaffinity(0))
+    threads = host_cores()
     os.environ["ORACLE_THREADS"] = str(threads)
     rng = np.random.default_rng(1)
     sel = np.sort(rng.choice(len(c.y), cols, replace=False))
     cost = O.PointCost(c.x, c.y[sel])
-    f = np.zeros(len(c.x))
     t0 = time.perf_counter()
-    cost.smin_cols(f, c.eps, c.alpha)
+    cost.smin_cols(np.zeros(len(c.x)), c.eps, c.alpha)
     el = time.perf_counter() - t0
     pairs = len(c.x) * cols
-    s_per_iter = el / pairs * 2.0 * len(c.x) * len(c.y)
+    rate = 1.0 / (el / pairs * 2.0 * len(c.x) * len(c.y))
     sample = (f"one g half-step restricted to {cols} of {len(c.y)} columns x {len(c.x)} rows "
-              f"({pairs:.3g} pair evaluations, fp64 C oracle, {threads} threads), "
-              f"extrapolated to 2*N*M pairs per iteration")
-    return 1.0 / s_per_iter, threads, sample, el
+              f"({pairs:.3g} pair evaluations, fp64 C oracle restating sinkhorn.py:93-100 over "
+              f"entropies.py:84-92, {threads} threads), extrapolated to 2*N*M pairs/iteration")
+    return rate, threads, sample
+
+
+def _fw_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import oracle as O
+    from paper_2201_00730_b200 import synthetic as S
+
+    idx, iters = args
+    x, y, a, b = S.cfg2_batch(batch=4096, start=idx, count=1)
+    t0 = time.perf_counter()
+    O.fw_fixed(x[0], y[0], a[0], b[0], 1.0, 1.0, iters)
+    return time.perf_counter() - t0
+
+
+def cpu_cfg2(iters=20):
+    """cores problems x `iters` line-search FW iterations (oracle port of
+    fw.py:176-232 with the reference's ternary search), one process per core;
+    throughput scaled to the full 4096-problem batched iteration."""
+    import multiprocessing as mp
+
+    cores = host_cores()
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_fw_worker, [(k, iters) for k in range(cores)])
+    wall = time.perf_counter() - t0
+    problem_iters_per_s = cores * iters / wall
+    rate = problem_iters_per_s / 4096.0
+    sample = (f"{cores} cfg2 problems x {iters} line-search FW iterations (numpy/C oracle port, "
+              f"one process per core), scaled to 4096 problems per batched iteration")
+    return rate, cores, sample
+
+
+def _bary_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import oracle as O
+    from paper_2201_00730_b200 import synthetic as S
+
+    idx, iters = args
+    xs, ws = S.cfg5_batch(start=idx, count=1)
+    t0 = time.perf_counter()
+    O.fw_barycenter_fixed(list(xs[0]), list(ws[0]), np.full(16, 1 / 16), 1.0, iters)
+    return time.perf_counter() - t0
+
+
+def cpu_cfg5(iters=2):
+    import multiprocessing as mp
+
+    cores = min(host_cores(), 64)
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_bary_worker, [(k, iters) for k in range(cores)])
+    wall = time.perf_counter() - t0
+    rate = cores * iters / wall / 64.0
+    sample = (f"{cores} cfg5 problems x {iters} FW iterations (oracle port of "
+              f"barycenter.py:361-411), scaled to 64 problems per batched iteration")
+    return rate, cores, sample
+
+
+# ---------------------------------------------------------------------------
+# Headline: cfg3 TI-Sinkhorn (row-sharded for N > 1).
+
+
+def run_cfg3(args, rank, world, dev, comm):
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import _device as D
+    from paper_2201_00730_b200 import _lib
+    from paper_2201_00730_b200 import synthetic as S
+    from paper_2201_00730_b200.distributed import row_offset, shard_rows
+
+    lib = _lib.load()
+    c = S.cfg3_inputs()
+    n, m = len(c.x), len(c.y)
+    rows = shard_rows(n, world)
+    off = row_offset(n, world, rank)
+    nl = rows[rank]
+    xl, al = c.x[off:off + nl], c.alpha[off:off + nl]
+    x = torch.as_tensor(xl, dtype=torch.float32, device=dev)
+    a = torch.as_tensor(al, dtype=torch.float32, device=dev)
+    y = torch.as_tensor(c.y, dtype=torch.float32, device=dev)
+    b = torch.as_tensor(c.beta, dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    kw = dict(comm=comm.handle, nranks=world, rank=rank) if comm is not None else {}
+
+    def step(f0):
+        f, g, _, _ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, variant="h",
+                                        precision="fp32", f0=f0, **kw)
+        return f, g
+
+    f = None
+    for _ in range(max(args.warmup, 3)):
+        f, g = step(f)
+    flush.zero_()
+    with cuda_timer() as tf:
+        flush.zero_()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        with cuda_timer() as tt:
+            for _ in range(args.steps):
+                flush.zero_()
+                f, g = step(f)
+    ms_step = max_over_ranks(tt.ms / args.steps, world, dev)
+    value = 1e3 / ms_step
+
+    # roofline of the dominant kernel (fused cost + online LSE half-step),
+    # timed live with CUDA events on the launching stream, on this rank's shard.
+    f_, g_, tr_, its_ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, precision="fp32",
+                                           f0=f)
+    ms2 = (ctypes.c_float * 2)()
+    desc = _lib.SinkhornDesc(
+        variant=_lib.SINKHORN_H, dtype=_lib.F32, cost=_lib.COST_SQEUCLID, batch=1, n=nl, m=m, d=2,
+        p=2.0, eps=c.eps, rho1=c.rho, rho2=c.rho, x=_lib.ptr(x), y=_lib.ptr(y), c=None, ct=None,
+        a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(f_), g=_lib.ptr(g_), init_given=1, iters=1,
+        tol=0.0, use_tol=0, trace_delta=_lib.ptr(tr_), iterations=_lib.ptr(its_),
+        nccl_comm=None, nranks=1, rank=0, shard_rows=None)
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
+    ws = D.workspace(size.value)
+    lib.uot_sinkhorn_time_main.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                           ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_float)]
+    _lib.check(lib.uot_sinkhorn_time_main(ctypes.byref(desc), _lib.ptr(ws), size.value,
+                                          _lib.stream_handle(), 20, ms2))
+    kernel_ms = 0.5 * (ms2[0] + ms2[1])
+    peak = ctypes.c_double(0.0)
+    lib.uot_probe_mufu_ex2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
+    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(peak)))
+    achieved = float(nl) * float(m) / (kernel_ms * 1e-3) / 1e9
+    peak_g = peak.value / 1e9
+
+    e2e = run_cfg3_e2e(P, c, xl, al, args.steps, dev, kw, world)
+    roof = {"bound": "mufu", "achieved": achieved, "peak": peak_g, "unit": "Gex2/s",
+            "frac": achieved / peak_g, "traffic": None,
+            "kernel": "sk_main<SqE32<2>>: fused on-the-fly cost + online log-sum-exp half-step",
+            "kernel_ms": kernel_ms, "work_per_launch": f"{nl}*{m} ex2 (this rank's rows x M)",
+            "peak_source": "measured live: uot_probe_mufu_ex2 (ex2.approx.ftz on all SMs, "
+                           "CUDA events); MEASURED_PEAKS.json carries no MUFU figure"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded 8-component 2-D Gaussian mixtures, BASELINE cfg3)",
+        "config": {
+            "workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
+            "n": n, "m": m, "d": 2, "eps": c.eps, "rho": c.rho, "variant": "h",
+            "parallelism": f"rows/{world} (NCCL all-gather per iteration)" if world > 1
+            else "single GPU",
+            "l2": f"{L2_FLUSH_BYTES >> 20} MiB write between steps (included in timing; "
+                  f"{tf.ms:.3f} ms each)"},
+        "roofline": roof, "e2e": e2e,
+        "gpu_launches": (4 + 7) * args.steps if world == 1 else (5 + 8) * args.steps,
+    }
+    return line, clk
+
+
+def run_cfg3_e2e(P, c, xl, al, steps, dev, kw, world):
+    """Same metric through the public API from pinned host buffers: H2D of
+    the step's inputs, one iteration, D2H of the resulting pair."""
+    import torch
+
+    host = {k: torch.as_tensor(v, dtype=torch.float32).pin_memory()
+            for k, v in (("x", xl), ("y", c.y), ("a", al), ("b", c.beta))}
+    fh = torch.zeros(len(xl), dtype=torch.float32).pin_memory()
+    out_f = torch.empty(len(xl), dtype=torch.float32).pin_memory()
+    out_g = torch.empty(len(c.y), dtype=torch.float32).pin_memory()
+
+    def one():
+        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        f0 = fh.to(dev, non_blocking=True)
+        f, g, _, _ = P.sinkhorn_batched(dv["x"], dv["y"], dv["a"], dv["b"], c.eps, c.rho, c.rho,
+                                        1, precision="fp32", f0=f0, **kw)
+        out_f.copy_(f[0], non_blocking=True)
+        out_g.copy_(g[0], non_blocking=True)
+        fh.copy_(out_f)
+
+    for _ in range(2):
+        one()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with cuda_timer() as t:
+        for _ in range(steps):
+            one()
+    ms = max_over_ranks(t.ms / steps, world, dev)
+    n, m = len(xl), len(c.y)
+    return {"value": 1e3 / ms, "unit": "iter/s",
+            "h2d_bytes_per_step": 4 * (2 * n + 2 * m + n + m + n),
+            "d2h_bytes_per_step": 4 * (n + m), "ms_per_step": ms,
+            "path": "paper_2201_00730_b200.sinkhorn_batched -> uot_sinkhorn_run (C-ABI)"}
+
+
+# ---------------------------------------------------------------------------
+# Secondary BASELINE configs (sharded by problem across ranks).
+
+
+def run_cfg2(rank, world, dev, peaks):
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import synthetic as S
+    from paper_2201_00730_b200.distributed import shard_problems
+
+    lo, hi = shard_problems(4096, world, rank)
+    x, y, a, b = S.cfg2_batch(batch=4096, start=lo, count=hi - lo)
+    x, y, a, b = (torch.as_tensor(v, device=dev) for v in (x, y, a, b))
+    iters = 500
+    P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 5, "linesearch")
+    torch.cuda.synchronize()
+    with cuda_timer() as t:
+        r = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, iters, "linesearch")
+    ms = max_over_ranks(t.ms, world, dev)
+    assert int(r.status.max().item()) == 0
+    it_s = iters / (ms * 1e-3)
+    gbs = CFG2_BYTES_PER_ITER * it_s / 1e9
+    return {"workload": "cfg2: batched 1-D FW, B=4096, N=M=1024, KL rho=1, |x-y|^2, fp64, "
+                        "500 line-search iterations (fixed count)",
+            "value": it_s, "unit": "iter/s (batched FW iterations over all 4096 problems)",
+            "ms_total": ms, "dtype": "f64", "scaling": "weak-by-problem" if world > 1 else None,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"],
+                         "work_per_iteration": "268,435,456 algorithmic bytes (SURVEY.md §8d)",
+                         "note": "state resident on chip for all iterations (one CTA per "
+                                 "problem): DRAM traffic ~0 per iteration; the kernel is bound "
+                                 "by fp64 exp / reductions, see DESIGN.md"}}
+
+
+def run_cfg5(rank, world, dev, peaks):
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import synthetic as S
+    from paper_2201_00730_b200.distributed import shard_problems
+
+    lo, hi = shard_problems(64, world, rank)
+    xs, ws = S.cfg5_batch(start=lo, count=hi - lo)
+    x, a = torch.as_tensor(xs, device=dev), torch.as_tensor(ws, device=dev)
+    w = np.full(16, 1 / 16)
+    iters = 1000
+    P.fw_barycenter_batched(x, a, w, 1.0, 3, "linesearch")
+    torch.cuda.synchronize()
+    with cuda_timer() as t:
+        r = P.fw_barycenter_batched(x, a, w, 1.0, iters, "linesearch")
+    ms = max_over_ranks(t.ms, world, dev)
+    assert int(r.status.max().item()) == 0
+    it_s = iters / (ms * 1e-3)
+    gbs = CFG5_BYTES_PER_ITER * it_s / 1e9
+    return {"workload": "cfg5: barycenter FW, 64 problems x K=16 x N=8192, KL rho=1, fp64, "
+                        "1000 line-search iterations (fixed count)",
+            "value": it_s, "unit": "iter/s (batched FW iterations over all 64 problems)",
+            "ms_total": ms, "dtype": "f64",
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"],
+                         "work_per_iteration": "268,435,456 algorithmic bytes (SURVEY.md §8d)"}}
+
+
+def run_cfg1(dev):
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import synthetic as S
+
+    c = S.cfg1_inputs()
+    out = {}
+    for v in ("h", "f"):
+        P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, 1.0, 1.0, 10,
+                           variant=v, cost="power", precision="fp64")
+        torch.cuda.synchronize()
+        with cuda_timer() as t:
+            P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, 1.0, 1.0,
+                               1000, variant=v, cost="power", precision="fp64")
+        out[v] = 1000 / (t.ms * 1e-3)
+    return {"workload": "cfg1: H and F Sinkhorn N=M=256 fp64, 1000 iterations (latency bound)",
+            "value": out["h"], "unit": "iter/s (H)", "f_variant_iter_s": out["f"], "dtype": "f64"}
+
+
+def run_cfg4(rank, world, dev):
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import synthetic as S
+    from paper_2201_00730_b200.distributed import shard_problems
+
+    lo, hi = shard_problems(256, world, rank)
+    x, y, a, b = S.cfg4_batch(start=lo, count=hi - lo)
+    xt, yt, at, bt = (torch.as_tensor(v, dtype=torch.float32, device=dev) for v in (x, y, a, b))
+    iters = 3
+    P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, 1, precision="fp32")
+    torch.cuda.synchronize()
+    with cuda_timer() as t:
+        P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
+                           precision="fp32")
+    ms = max_over_ranks(t.ms, world, dev)
+    return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32 (SIMT expanded-form "
+                        "path; tcgen05 path pending), timed over 3 of the 300 iterations",
+            "value": iters / (ms * 1e-3), "unit": "iter/s", "dtype": "f32"}
 
 
 # ---------------------------------------------------------------------------
@@ -130,7 +471,7 @@ def run_reference(args, rank, world):
     c = S.cfg3_inputs()
     vals = []
     for k in range(args.warmup + args.steps):
-        v, threads, sample, _ = cpu_sinkhorn_rate(c, cols=256)
+        v, threads, sample = cpu_cfg3(c, cols=128)
         if k >= args.warmup:
             vals.append(v)
     value = float(np.mean(vals))
@@ -139,7 +480,7 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3: H-Sinkhorn N=M=65536 d=2, eps=1e-2*max|x-y|^2, KL rho=1",
+        "config": {"workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
                    "n": len(c.x), "m": len(c.y), "eps": c.eps},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": threads, "kind": "port",
                          "sample": sample},
@@ -149,185 +490,71 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank, world):
-    import torch
-
-    import paper_2201_00730_b200 as P
-    from paper_2201_00730_b200 import _device as D
-    from paper_2201_00730_b200 import _lib
-    from paper_2201_00730_b200 import synthetic as S
-
-    lib = _lib.load()
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
-    c = S.cfg3_inputs()
-    n, m = len(c.x), len(c.y)
-    x = torch.as_tensor(c.x, dtype=torch.float32, device=dev)
-    y = torch.as_tensor(c.y, dtype=torch.float32, device=dev)
-    a = torch.as_tensor(c.alpha, dtype=torch.float32, device=dev)
-    b = torch.as_tensor(c.beta, dtype=torch.float32, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-
-    def step(f0):
-        f, g, _, _ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, variant="h",
-                                        precision="fp32", f0=f0)
-        return f, g
-
-    # warm-up (also builds the first potentials)
-    f = None
-    for _ in range(max(args.warmup, 3)):
-        f, g = step(f)
-    torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    flush_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    # time the L2 flush alone so it can be reported (it is included below)
-    flush_ev[0].record(st)
-    flush.zero_()
-    flush_ev[1].record(st)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
-        e0.record(st)
-        for _ in range(args.steps):
-            flush.zero_()
-            f, g = step(f)
-        e1.record(st)
-        torch.cuda.synchronize()
-    ms_total = e0.elapsed_time(e1)
-    flush_ms = flush_ev[0].elapsed_time(flush_ev[1])
-    ms_step = ms_total / args.steps
-    if world > 1:
-        tt = torch.tensor([ms_step], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms_step = float(tt.item())
-    value = 1e3 / ms_step
-
-    # roofline of the dominant kernel: the fused log-sum-exp half-step
-    desc_f, desc_g, its = None, None, None
-    f_, g_, tr_, its_ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, precision="fp32",
-                                           f0=f)
-    ms2 = (ctypes.c_float * 2)()
-    desc = _lib.SinkhornDesc(
-        variant=_lib.SINKHORN_H, dtype=_lib.F32, cost=_lib.COST_SQEUCLID, batch=1, n=n, m=m, d=2,
-        p=2.0, eps=c.eps, rho1=c.rho, rho2=c.rho, x=_lib.ptr(x), y=_lib.ptr(y), c=None, ct=None,
-        a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(f_), g=_lib.ptr(g_), init_given=1, iters=1,
-        tol=0.0, use_tol=0, trace_delta=_lib.ptr(tr_), iterations=_lib.ptr(its_),
-        nccl_comm=None, nranks=1, rank=0, shard_rows=None)
-    size = ctypes.c_size_t(0)
-    _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
-    ws = D.workspace(size.value)
-    lib.uot_sinkhorn_time_main.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
-                                           ctypes.c_void_p, ctypes.c_int,
-                                           ctypes.POINTER(ctypes.c_float)]
-    _lib.check(lib.uot_sinkhorn_time_main(ctypes.byref(desc), _lib.ptr(ws), size.value,
-                                          _lib.stream_handle(), 20, ms2))
-    kernel_ms = 0.5 * (ms2[0] + ms2[1])
-    ex2_per_launch = float(n) * float(m)
-    peak = ctypes.c_double(0.0)
-    lib.uot_probe_mufu_ex2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
-    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(peak)))
-    achieved = ex2_per_launch / (kernel_ms * 1e-3) / 1e9
-    peak_g = peak.value / 1e9
-
-    # end-to-end through the public API with host buffers each step
-    e2e = run_e2e(P, c, args.steps, dev)
-
-    if rank != 0:
-        return
-    cpu_v, cpu_threads, cpu_sample, _ = cpu_sinkhorn_rate(c)
-    launches_per_step = 4 + 6  # 2x(main+tail) + reset, 3x zero, init tail, finalize per call
-    line = {
-        "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded 8-component 2-D Gaussian mixtures, BASELINE cfg3)",
-        "config": {
-            "workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
-            "n": n, "m": m, "d": 2, "eps": c.eps, "rho": c.rho, "variant": "h",
-            "parallelism": f"rows/{world}" if world > 1 else "single",
-            "l2": f"{L2_FLUSH_BYTES >> 20} MiB write between steps (included; "
-                  f"{flush_ms:.3f} ms each)",
-        },
-        "roofline": {"bound": "mufu", "achieved": achieved, "peak": peak_g, "unit": "Gex2/s",
-                     "frac": achieved / peak_g, "traffic": None,
-                     "kernel": "sk_main<SqE32<2>> (fused cost + online LSE half-step)",
-                     "kernel_ms": kernel_ms, "work_per_launch": f"{n}*{m} ex2",
-                     "peak_source": "measured live: uot_probe_mufu_ex2 (all SMs, CUDA events)"},
-        "cpu_baseline": {"value": cpu_v, "unit": "iter/s", "cores": cpu_threads, "kind": "port",
-                         "sample": cpu_sample},
-        "e2e": e2e,
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line), flush=True)
-
-
-def run_e2e(P, c, steps, dev):
-    """Same metric through the public API from pinned host buffers: H2D of
-    the step's inputs, one iteration, D2H of the resulting pair."""
-    import torch
-
-    n, m = len(c.x), len(c.y)
-    host = {k: torch.as_tensor(v, dtype=torch.float32).pin_memory()
-            for k, v in (("x", c.x), ("y", c.y), ("a", c.alpha), ("b", c.beta))}
-    fh = torch.zeros(n, dtype=torch.float32).pin_memory()
-    out_f = torch.empty(n, dtype=torch.float32).pin_memory()
-    out_g = torch.empty(m, dtype=torch.float32).pin_memory()
-    st = torch.cuda.current_stream()
-
-    def one():
-        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-        f0 = fh.to(dev, non_blocking=True)
-        f, g, _, _ = P.sinkhorn_batched(dv["x"], dv["y"], dv["a"], dv["b"], c.eps, c.rho, c.rho,
-                                        1, precision="fp32", f0=f0)
-        out_f.copy_(f[0], non_blocking=True)
-        out_g.copy_(g[0], non_blocking=True)
-        fh.copy_(out_f)
-
-    for _ in range(2):
-        one()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(steps):
-        one()
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    h2d = 4 * (2 * n + 2 * m + n + m + n)
-    d2h = 4 * (n + m)
-    return {"value": 1e3 / ms, "unit": "iter/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    import torch
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    comm = None
     if world > 1:
-        import torch
+        torch.distributed.init_process_group("nccl", device_id=dev)
+        from paper_2201_00730_b200.distributed import NcclComm
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
+        comm = NcclComm(world, rank)
     try:
-        run_ours(args, rank, world)
+        peaks, peak_src = load_peaks()
+        line, clk = run_cfg3(args, rank, world, dev, comm)
+        secondary = {}
+        if not args.no_secondary:
+            secondary["cfg2_fw"] = run_cfg2(rank, world, dev, peaks)
+            secondary["cfg5_barycenter"] = run_cfg5(rank, world, dev, peaks)
+            secondary["cfg4_sinkhorn_d64"] = run_cfg4(rank, world, dev)
+            if rank == 0:
+                secondary["cfg1_sinkhorn_1d"] = run_cfg1(dev)
+        if rank == 0:
+            cpu_v, cpu_cores, cpu_sample = cpu_cfg3(S_inputs_cfg3())
+            line["cpu_baseline"] = {"value": cpu_v, "unit": "iter/s", "cores": cpu_cores,
+                                    "kind": "port", "sample": cpu_sample}
+            if not args.no_secondary and world == 1:
+                v2, c2, s2 = cpu_cfg2()
+                secondary["cfg2_fw"]["cpu_baseline"] = {"value": v2, "unit": "iter/s",
+                                                        "cores": c2, "kind": "port", "sample": s2}
+                v5, c5, s5 = cpu_cfg5()
+                secondary["cfg5_barycenter"]["cpu_baseline"] = {
+                    "value": v5, "unit": "iter/s", "cores": c5, "kind": "port", "sample": s5}
+            line["secondary"] = secondary
+            line["peaks"] = {"hbm_gbs": peaks.get("hbm_gbs"), "source": peak_src}
+            line["clocks"] = clk.summary()
+            print(json.dumps(line), flush=True)
     finally:
+        if comm is not None:
+            comm.close()
         if world > 1:
-            import torch
-
             torch.distributed.destroy_process_group()
+
+
+_CFG3 = None
+
+
+def S_inputs_cfg3():
+    global _CFG3
+    if _CFG3 is None:
+        from paper_2201_00730_b200 import synthetic as S
+
+        _CFG3 = S.cfg3_inputs()
+    return _CFG3
 
 
 if __name__ == "__main__":
