@@ -2,6 +2,7 @@
 // structure).  Reference: src/sinkhorn.py:93-163, src/entropies.py:67-92,
 // :187-214, src/duality.py:175-178.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/uot_b200.h"
@@ -315,6 +316,195 @@ __global__ void __launch_bounds__(THREADS) sk_main(MainArgs<typename P::T> A) {
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
       A.part_m[idx] = mm[c];
       A.part_a[idx] = acc[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packed fp32x2 main kernel for the 2-D squared-Euclidean cost (BASELINE
+// cfg3).  Blackwell's FFMA2 / FADD2 process two output columns per
+// instruction with the row record broadcast as a scalar operand, so a pair
+// costs ~3.5 issued instructions (FADD2 + 2 FFMA2 per two pairs, FMNMX3 for
+// the shift check, one MUFU.EX2, half an FADD2 for the sum) and the kernel is
+// bound by the MUFU pipe (16 ex2 / clk / SM) rather than by issue.
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 p2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void u2(u64 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Slow path of a packed tile (stale shift outside the safe window): redo
+// the tile column by column with an explicit maximum and rescale.
+template <int CP, int RT, bool CHECK>
+__device__ __forceinline__ void tile_sq2_slow(const float* srec, int rr, int clen, const u64 (&y0)[CP],
+                                           const u64 (&y1)[CP], u64 (&cc)[CP],
+                                           float (&mm)[2 * CP], u64 (&acc)[CP]) {
+  using D = Dom<float>;
+#pragma unroll
+  for (int j = 0; j < CP; ++j) {
+    float yy0[2], yy1[2], c2[2], a2[2];
+    u2(y0[j], yy0[0], yy0[1]);
+    u2(y1[j], yy1[0], yy1[1]);
+    u2(cc[j], c2[0], c2[1]);
+    u2(acc[j], a2[0], a2[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float t[RT];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const bool ok = !CHECK || rr + i < clen;
+        const float4 r = *reinterpret_cast<const float4*>(srec + (ok ? (rr + i) : 0) * 4);
+        t[i] = ok ? fmaf(r.z, yy1[h], fmaf(r.y, yy0[h], r.x + c2[h])) : -INFINITY;
+        mx = fmaxf(mx, t[i]);
+      }
+      if (mx > D::HI || (mx < D::LO && a2[h] < D::TINY)) {
+        float mn = mx;
+        if (a2[h] > 0.f) mn = fmaxf(mn, D::lg(a2[h]));
+        if (mn > -INFINITY && mn < INFINITY) {
+          if (a2[h] > 0.f) a2[h] *= D::ex(-mn);
+          mm[2 * j + h] += mn;
+          c2[h] -= mn;
+#pragma unroll
+          for (int i = 0; i < RT; ++i) t[i] -= mn;
+        }
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) sum += D::ex(t[i]);
+      a2[h] += sum;
+    }
+    cc[j] = p2(c2[0], c2[1]);
+    acc[j] = p2(a2[0], a2[1]);
+  }
+}
+
+// Fast path: packed exponents, no per-pair maximum.  The accumulated sums are
+// range-checked after the tile instead (overflow -> inf / > 2^100, or
+// everything so far below 2^-100); a failing tile is redone by the slow path
+// from the pre-tile state.  In steady state the stale shift (the previous
+// iteration's log-sum-exp of the same output) keeps every tile in range.
+template <int CP, int RT, bool CHECK>
+__device__ __forceinline__ void tile_sq2(const float* srec, int rr, int clen, const u64 (&y0)[CP],
+                                         const u64 (&y1)[CP], u64 (&cc)[CP], float (&mm)[2 * CP],
+                                         u64 (&acc)[CP]) {
+  u64 t[RT][CP];
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const bool ok = !CHECK || rr + i < clen;
+    const float4 r = *reinterpret_cast<const float4*>(srec + (ok ? (rr + i) : 0) * 4);
+    const float uu = ok ? r.x : -INFINITY;
+    const u64 U = p2(uu, uu);
+    const u64 X0 = p2(r.y, r.y), X1 = p2(r.z, r.z);
+#pragma unroll
+    for (int j = 0; j < CP; ++j) t[i][j] = fma2(X1, y1[j], fma2(X0, y0[j], add2(U, cc[j])));
+  }
+  u64 na[CP];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CP; ++j) {
+    float lo, hi;
+    u2(t[0][j], lo, hi);
+    u64 s = p2(ex2f(lo), ex2f(hi));
+#pragma unroll
+    for (int i = 1; i < RT; ++i) {
+      u2(t[i][j], lo, hi);
+      s = add2(s, p2(ex2f(lo), ex2f(hi)));
+    }
+    na[j] = add2(acc[j], s);
+    float alo, ahi;
+    u2(na[j], alo, ahi);
+    bad |= !(alo < 1.2676506e30f && ahi < 1.2676506e30f && alo > 7.8886091e-31f &&
+             ahi > 7.8886091e-31f);  // (2^-100, 2^100)
+  }
+  if (bad) {
+    tile_sq2_slow<CP, RT, CHECK>(srec, rr, clen, y0, y1, cc, mm, acc);
+  } else {
+#pragma unroll
+    for (int j = 0; j < CP; ++j) acc[j] = na[j];
+  }
+}
+
+template <int THREADS, int CP, int RT>
+__global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
+  const int b = blockIdx.z;
+  if (A.done != nullptr && A.done[b]) return;
+  const int split = blockIdx.y, S = gridDim.y;
+  const long r0 = (long)A.nred * split / S;
+  const long r1 = (long)A.nred * (split + 1) / S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* srec = reinterpret_cast<float*>(smem_raw);
+  constexpr int COLS = 2 * CP;
+  u64 y0[CP], y1[CP], cc[CP], acc[CP];
+  float mm[COLS];
+  const int obase = blockIdx.x * THREADS * COLS + threadIdx.x;
+  const float L = A.g.L;
+  const float* pts = A.g.out_pts + b * A.g.out_pts_bstride;
+#pragma unroll
+  for (int j = 0; j < CP; ++j) {
+    float ya0[2], ya1[2], c[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = obase + (2 * j + h) * THREADS;
+      const bool ok = o < A.nout;
+      const float q0 = ok ? pts[(long)o * 2] : 0.f, q1 = ok ? pts[(long)o * 2 + 1] : 0.f;
+      ya0[h] = q0;
+      ya1[h] = q1;
+      mm[2 * j + h] = ok ? A.shift_in[(long)b * A.nout + o] : 0.f;
+      c[h] = -fmaf(q0, q0, q1 * q1) * L - mm[2 * j + h];
+    }
+    y0[j] = p2(ya0[0], ya0[1]);
+    y1[j] = p2(ya1[0], ya1[1]);
+    cc[j] = p2(c[0], c[1]);
+    acc[j] = p2(0.f, 0.f);
+  }
+  const float* rec_g = A.g.red_rec + b * A.g.red_bstride;
+  for (long cs = r0; cs < r1; cs += A.chunk) {
+    const int clen = (int)min((long)A.chunk, r1 - cs);
+    {
+      const float4* src = reinterpret_cast<const float4*>(rec_g + (cs + A.red_offset) * 4);
+      float4* dst = reinterpret_cast<float4*>(srec);
+      for (int e = threadIdx.x; e < clen; e += THREADS) dst[e] = src[e];
+    }
+    __syncthreads();
+    const int full = clen / RT * RT;
+    for (int rr = 0; rr < full; rr += RT) tile_sq2<CP, RT, false>(srec, rr, clen, y0, y1, cc, mm, acc);
+    if (full < clen) tile_sq2<CP, RT, true>(srec, full, clen, y0, y1, cc, mm, acc);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < CP; ++j) {
+    float a2[2];
+    u2(acc[j], a2[0], a2[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = obase + (2 * j + h) * THREADS;
+      if (o < A.nout) {
+        const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
+        A.part_m[idx] = mm[2 * j + h];
+        A.part_a[idx] = a2[h];
+      }
     }
   }
 }
@@ -637,16 +827,31 @@ int num_sms() {
   return g_num_sms;
 }
 
-// Splits of the reduced index so the main grid fills the chip several times
-// over (grid = out_blocks x splits x batch) while keeping >= 16 reduced
-// indices per split.
-int choose_splits(int B, long nout, long nred, int out_per_block) {
+// Splits of the reduced index: the main grid (out_blocks x splits x batch)
+// should fill the chip about four times over with whole waves of
+// (SMs x resident CTAs per SM), while keeping >= 16 reduced indices per split.
+int choose_splits(int B, long nout, long nred, int out_per_block, int occ = 0) {
   const long out_blocks = (nout + out_per_block - 1) / out_per_block;
-  const long target = (long)num_sms() * 24;
-  long s = (target + out_blocks * B - 1) / (out_blocks * B);
-  s = std::min(s, std::max(1L, nred / 16));
-  s = std::min(s, 4096L);
-  return (int)std::max(1L, s);
+  const long s_max = std::min(4096L, std::max(1L, nred / 16));
+  if (occ <= 0) {
+    const long target = (long)num_sms() * 24;
+    long s = (target + out_blocks * B - 1) / (out_blocks * B);
+    return (int)std::max(1L, std::min(s, s_max));
+  }
+  const long wave = (long)num_sms() * occ;
+  const long s0 = std::max(1L, (4 * wave + out_blocks * B - 1) / (out_blocks * B));
+  long best_s = std::min(s0, s_max);
+  double best_eff = -1.0;
+  for (long sv = std::max(1L, s0 / 2); sv <= std::min(s_max, 2 * s0); ++sv) {
+    const long total = out_blocks * sv * B;
+    const long waves = (total + wave - 1) / wave;
+    const double eff = (double)total / (double)(waves * wave);
+    if (eff > best_eff + 0.005) {
+      best_eff = eff;
+      best_s = sv;
+    }
+  }
+  return (int)best_s;
 }
 
 template <class P>
@@ -654,6 +859,33 @@ struct Engine {
   using T = typename P::T;
   using C = Cfg<P>;
   static constexpr int OUT_PER_BLOCK = C::THREADS * C::COLS;
+
+  static int occupancy(int d) {
+    static int cached = -1;
+    static int cached_d = -1;
+    if (cached >= 0 && cached_d == d) return cached;
+    const int rw = P::rw(d);
+    const size_t smem = (size_t)chunk_for(rw) * rw * sizeof(T);
+    int occ = 0;
+    cudaError_t e;
+    if constexpr (std::is_same<P, SqE32<2>>::value)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &occ, sk_main_sq2<C::THREADS, C::COLS / 2, C::RT>, C::THREADS, smem);
+    else
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sk_main<P, C::THREADS, C::COLS, C::RT>,
+                                                        C::THREADS, smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      occ = 0;
+    }
+    cached = occ;
+    cached_d = d;
+    return occ;
+  }
+
+  static int splits(int B, long nout, long nred, int d) {
+    return choose_splits(B, nout, nred, OUT_PER_BLOCK, occupancy(d));
+  }
 
   static int chunk_for(int rw) {
     int ch = (int)(32768 / (rw * sizeof(T)));
@@ -670,8 +902,8 @@ struct Engine {
     s.rwA = P::rw(d.d);
     s.rwB = P::rw(d.d);
     s.total_n = d.n;
-    const int sA = choose_splits(d.batch, d.m, d.n, OUT_PER_BLOCK);
-    const int sB = choose_splits(d.batch, d.n, d.m, OUT_PER_BLOCK);
+    const int sA = splits(d.batch, d.m, d.n, d.d);
+    const int sB = splits(d.batch, d.n, d.m, d.d);
     s.S = std::max(sA, sB);
     if (d.nranks > 1 && d.nccl_comm == nullptr) s.S = std::max(s.S, d.nranks);
     s.nblk = (int)ceil_div(std::max(d.n, d.m), TAIL_THREADS);
@@ -727,7 +959,12 @@ struct Engine {
     a.splits_total = splits_total;
     dim3 grid(ceil_div(a.nout, OUT_PER_BLOCK), splits, d.batch);
     const size_t smem = (size_t)a.chunk * a.g.rw * sizeof(T);
-    sk_main<P, C::THREADS, C::COLS, C::RT><<<grid, C::THREADS, smem, st>>>(a);
+    if constexpr (std::is_same<P, SqE32<2>>::value) {
+      static_assert(C::COLS % 2 == 0, "packed kernel needs an even column count");
+      sk_main_sq2<C::THREADS, C::COLS / 2, C::RT><<<grid, C::THREADS, smem, st>>>(a);
+    } else {
+      sk_main<P, C::THREADS, C::COLS, C::RT><<<grid, C::THREADS, smem, st>>>(a);
+    }
     UOT_CHECK_LAUNCH();
     return UOT_OK;
   }
@@ -843,8 +1080,8 @@ struct Engine {
     const int trace_len = std::max(d.iters, 1);
     // init: hat_f = f0, Smin_a(f0), pack source records.
     UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, f0, 0, nullptr, trace_len));
-    const int sB = choose_splits(d.batch, d.m, d.n, OUT_PER_BLOCK);  // g-update splits
-    const int sA = choose_splits(d.batch, d.n, d.m, OUT_PER_BLOCK);  // f-update splits
+    const int sB = splits(d.batch, d.m, d.n, d.d);  // g-update splits
+    const int sA = splits(d.batch, d.n, d.m, d.d);  // f-update splits
     for (int t = 0; t < d.iters; ++t) {
       T* hat_old = (t & 1) ? bf.hatA1 : bf.hatA0;
       T* hat_new = (t & 1) ? bf.hatA0 : bf.hatA1;
@@ -999,8 +1236,8 @@ struct Engine {
         set_error("row sharding supports point-cloud and 1-D costs");
         return UOT_INVALID;
       }
-      sB[r] = choose_splits(d.batch, d.m, L.nl[r], OUT_PER_BLOCK);
-      sA[r] = choose_splits(d.batch, L.nl[r], d.m, OUT_PER_BLOCK);
+      sB[r] = splits(d.batch, d.m, L.nl[r], d.d);
+      sA[r] = splits(d.batch, L.nl[r], d.m, d.d);
       sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf[r].sc, bf[r].counter,
                                                         bf[r].done, bf[r].iters_done);
       sk_zero<T><<<256, 256, 0, st>>>((long)L.nl[r], bf[r].shiftA);
@@ -1079,8 +1316,8 @@ int time_main(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_
   WsLayout L;
   Buffers<T> bf;
   layout<T>(s, d.iters, L, &bf, (char*)ws);
-  const int sB = choose_splits(d.batch, d.m, d.n, E::OUT_PER_BLOCK);
-  const int sA = choose_splits(d.batch, d.n, d.m, E::OUT_PER_BLOCK);
+  const int sB = E::splits(d.batch, d.m, d.n, d.d);
+  const int sA = E::splits(d.batch, d.n, d.m, d.d);
   cudaEvent_t e0, e1;
   UOT_CUDA_TRY(cudaEventCreate(&e0));
   UOT_CUDA_TRY(cudaEventCreate(&e1));
