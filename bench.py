@@ -293,8 +293,16 @@ def run_cfg3(args, rank, world, dev, comm):
     peak_g = peak.value / 1e9
 
     e2e = run_cfg3_e2e(P, c, xl, al, args.steps, dev, kw, world)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh)["sk_main_sq2"]["dram_bytes_per_launch"] if world == 1 else None
+    except (OSError, KeyError, ValueError):
+        traffic = None
     roof = {"bound": "mufu", "achieved": achieved, "peak": peak_g, "unit": "Gex2/s",
-            "frac": achieved / peak_g, "traffic": None,
+            "frac": achieved / peak_g, "traffic": traffic,
+            "traffic_note": "DRAM bytes per launch from the committed ncu capture; algorithmic "
+                            "input per launch = 65536 x 16 B records + 65536 x 12 B columns",
             "kernel": "sk_main<SqE32<2>>: fused on-the-fly cost + online log-sum-exp half-step",
             "kernel_ms": kernel_ms, "work_per_launch": f"{nl}*{m} ex2 (this rank's rows x M)",
             "peak_source": "measured live: uot_probe_mufu_ex2 (ex2.approx.ftz on all SMs, "
