@@ -21,6 +21,10 @@ int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* workspace, size_
  * SM; returns ex2 results per second (measured with CUDA events). */
 int uot_probe_mufu_ex2(void* stream, double* ex2_per_s);
 
+/* One-tile tcgen05 check: D[128x128] = A[128xK] * B[128xK]^T (kind::tf32,
+ * A from TMEM, B from shared memory); device pointers, row-major. */
+int uot_tc_selftest(const float* A, const float* B, int K, float* D, void* stream);
+
 /* FP64 DFMA throughput probe (DFMA per second). */
 int uot_probe_dfma(void* stream, double* dfma_per_s);
 

@@ -1,0 +1,88 @@
+// tc_selftest.cu -- one-tile check of the tcgen05 path used by the d >= 32
+// Sinkhorn kernel: D[128x128] = A[128xK] * B[128xK]^T with A written to TMEM
+// (tcgen05.st), B staged in shared memory in the canonical K-major layout,
+// kind::tf32 MMAs issued by one thread, D read back with tcgen05.ld.
+// Exported as uot_tc_selftest (include/uot_b200_bench.h); tests compare it
+// with an fp64 host product.
+#include "../../include/uot_b200_bench.h"
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace uot {
+
+__global__ void __launch_bounds__(128) tc_selftest_kernel(const float* A, const float* B, int K,
+                                                          float* D) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  constexpr int N = 128, M = 128;
+  const int t = threadIdx.x, warp = t >> 5;
+  float* sB = reinterpret_cast<float*>(smem);
+  const uint32_t LBO = (N / 8) * 128, SBO = 128;
+  // B -> shared memory, canonical K-major no-swizzle layout
+  for (int idx = t; idx < N * K; idx += blockDim.x) {
+    const int n = idx / K, k = idx % K;
+    const uint32_t off = (k / 4) * LBO + (n / 8) * SBO + (n % 8) * 16 + (k % 4) * 4;
+    sB[off / 4] = B[idx];
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) tc::tmem_alloc(&tbase_s, 512);
+  if (t == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = tbase_s;
+  // A -> TMEM: lane = row, column = K element
+  const int row = t;
+  for (int c = 0; c < K; c += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(A[row * K + c + e]);
+    tc::tmem_st8(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
+  }
+  tc::wait_st();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t d_col = 256;
+  if (t == 0) {
+    const uint32_t idesc = tc::idesc_tf32(M, N);
+    for (int s = 0; s < K / 8; ++s) {
+      const uint64_t bd = tc::sdesc(sB + (2 * s * LBO) / 4, LBO, SBO);
+      tc::mma_tf32_ts(tbase + d_col, tbase + 8 * s, bd, idesc, s > 0 ? 1u : 0u);
+    }
+    tc::mma_commit(&bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after();
+  for (int c = 0; c < N; c += 32) {
+    uint32_t v[32];
+    tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + d_col + c, v);
+    tc::wait_ld();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) D[row * N + c + e] = __uint_as_float(v[e]);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tbase, 512);
+}
+
+}  // namespace uot
+
+extern "C" int uot_tc_selftest(const float* A, const float* B, int K, float* D, void* stream) {
+  using namespace uot;
+  if (K < 8 || K % 8 != 0 || K > 256) {
+    set_error("uot_tc_selftest: K must be a multiple of 8 in [8, 256]");
+    return UOT_INVALID;
+  }
+  const size_t smem = (size_t)128 * K * 4;
+  UOT_CUDA_TRY(cudaFuncSetAttribute(tc_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  tc_selftest_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, K, D);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
