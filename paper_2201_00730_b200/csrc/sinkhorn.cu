@@ -45,6 +45,12 @@ struct Dom<double> {
   static constexpr double HI = 64.0, LO = -256.0, TINY = 6.6e-112;  // ~e^-256
 };
 
+}  // namespace uot
+
+#include "sinkhorn_tc.cuh"
+
+namespace uot {
+
 // ---------------------------------------------------------------------------
 // Cost policies.  Each defines the packed record of a reduced-side index
 // (written by the tail of the previous half-step), the per-output registers,
@@ -209,11 +215,63 @@ struct Explicit {
   static int rw(int) { return 1; }
 };
 
+// fp32 squared Euclidean on d >= 32 features via tcgen05 (sinkhorn_tc.cuh).
+// Records are written straight into the canonical K-major tile layout that
+// the main kernel bulk-copies into shared memory.
+struct SqE32TC {
+  using T = float;
+  struct Out {
+    float bias;
+  };
+  static int rw(int d) { return tc_kp(d); }
+  static __device__ __forceinline__ void pack_tile(float* base, long r, int KP, double hat,
+                                                   const float* pt, double w, double L, int d) {
+    float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
+    const int rl = (int)(r % TC_TILE);
+    double s2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const float x = (float)(2.0 * L * (double)pt[k]);
+      const float xh = tf32_hi(x);
+      tile[tc_tile_index(rl, k)] = xh;
+      tile[tc_tile_index(rl, d + k)] = x - xh;
+      tile[tc_tile_index(rl, 2 * d + k)] = xh;
+      s2 += (double)pt[k] * (double)pt[k];
+    }
+    const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
+    const float uh = tf32_hi((float)u);
+    const double u1 = u - (double)uh;
+    const float um = tf32_hi((float)u1);
+    tile[tc_tile_index(rl, 3 * d)] = uh;
+    tile[tc_tile_index(rl, 3 * d + 1)] = um;
+    tile[tc_tile_index(rl, 3 * d + 2)] = (float)(u1 - (double)um);
+    tile[tc_tile_index(rl, 3 * d + 3)] = 1.f;
+    tile[tc_tile_index(rl, 3 * d + 4)] = 1.f;
+    tile[tc_tile_index(rl, 3 * d + 5)] = 1.f;
+    for (int k = 3 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k)] = 0.f;
+  }
+};
+
+// Record layout of a side: `rw` elements per index, or the tiled layout.
 template <class P>
-__device__ __forceinline__ void pack_rec(typename P::T* rec, double hat, const typename P::T* pt,
-                                         double w, double L, double p, int d) {
-  P::pack(rec, hat, pt, w, L, p, d);
-}
+struct RecLayout {
+  static long stride(int n, int d) { return (long)n * P::rw(d); }
+  static __device__ __forceinline__ void pack(typename P::T* base, long o, int rw, double hat,
+                                              const typename P::T* pt, double w, double L,
+                                              double p, int d) {
+    P::pack(base + o * rw, hat, pt, w, L, p, d);
+  }
+};
+template <>
+struct RecLayout<SqE32TC> {
+  static long stride(int n, int d) {
+    return (long)((n + TC_TILE - 1) / TC_TILE) * TC_TILE * tc_kp(d);
+  }
+  static __device__ __forceinline__ void pack(float* base, long o, int rw, double hat,
+                                              const float* pt, double w, double L, double,
+                                              int d) {
+    SqE32TC::pack_tile(base, o, rw, hat, pt, w, L, d);
+  }
+};
 
 // One register tile: RT reduced records x COLS outputs.  Exponents are
 // formed first, their max checked against the safe window of the current
@@ -572,8 +630,9 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     hat = (double)hat_t;
     A.hat_out[(long)b * A.nout + o] = hat_t;
     const double w = (double)A.out_w[(long)b * A.nout + o];
-    pack_rec<P>(A.rec_out + ((long)b * A.nout + o) * A.rw, hat,
-                A.out_pts + ((long)b * A.nout + o) * A.d, w, (double)A.L, (double)A.p, A.d);
+    RecLayout<P>::pack(A.rec_out + (long)b * A.rec_bstride, o, A.rw, hat,
+                       A.out_pts + ((long)b * A.nout + o) * A.d, w, (double)A.L, (double)A.p,
+                       A.d);
     if (w > 0.0) pr = LsePair{-hat / A.rho_out, w};
     if (A.hat_old != nullptr) {
       const double dl = hat - ((double)A.hat_old[(long)b * A.nout + o] + tau_old);
@@ -740,14 +799,15 @@ struct Buffers {
 struct Shape {
   int B, n, m, d, rwA, rwB, S, nblk;
   int total_n;  // all shards (emulation)
+  long recA, recB;  // record elements per problem
 };
 
 template <typename T>
 size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* base) {
   size_t sizes[16];
   const long nm = std::max(s.total_n, s.m);
-  sizes[0] = sizeof(T) * (size_t)s.B * s.total_n * s.rwA;
-  sizes[1] = sizeof(T) * (size_t)s.B * s.m * s.rwB;
+  sizes[0] = sizeof(T) * (size_t)s.B * s.recA;
+  sizes[1] = sizeof(T) * (size_t)s.B * s.recB;
   sizes[2] = sizeof(T) * (size_t)s.B * s.total_n;
   sizes[3] = sizes[2];
   sizes[4] = sizeof(T) * (size_t)s.B * s.m;
@@ -811,6 +871,10 @@ template <>
 struct Cfg<SqE64> {
   static constexpr int THREADS = 128, COLS = 2, RT = 4;
 };
+template <>
+struct Cfg<SqE32TC> {
+  static constexpr int THREADS = 128, COLS = 1, RT = 1;  // 128 outputs per CTA (one MMA tile)
+};
 template <typename TT>
 struct Cfg<Explicit<TT>> {
   static constexpr int THREADS = 128, COLS = 2, RT = 4;
@@ -868,7 +932,11 @@ struct Engine {
     const size_t smem = (size_t)chunk_for(rw) * rw * sizeof(T);
     int occ = 0;
     cudaError_t e;
-    if constexpr (std::is_same<P, SqE32<2>>::value)
+    if constexpr (std::is_same<P, SqE32TC>::value) {
+      cached = 1;  // TMEM (512 columns) is allocated whole: one CTA per SM
+      cached_d = d;
+      return 1;
+    } else if constexpr (std::is_same<P, SqE32<2>>::value)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &occ, sk_main_sq2<C::THREADS, C::COLS / 2, C::RT>, C::THREADS, smem);
     else
@@ -902,6 +970,8 @@ struct Engine {
     s.rwA = P::rw(d.d);
     s.rwB = P::rw(d.d);
     s.total_n = d.n;
+    s.recA = RecLayout<P>::stride(d.n, d.d);
+    s.recB = RecLayout<P>::stride(d.m, d.d);
     const int sA = splits(d.batch, d.m, d.n, d.d);
     const int sB = splits(d.batch, d.n, d.m, d.d);
     s.S = std::max(sA, sB);
@@ -928,7 +998,7 @@ struct Engine {
     a.g.p = (T)d.p;
     if (to_target) {  // g-update: reduce over the source side, outputs = targets
       a.g.red_rec = bf.recA;
-      a.g.red_bstride = (long)d.n * a.g.rw;
+      a.g.red_bstride = RecLayout<P>::stride(d.n, d.d);
       a.g.out_pts = (const T*)d.y;
       a.g.out_pts_bstride = (long)d.m * d.d;
       a.g.cmat = (const T*)d.c;
@@ -939,7 +1009,7 @@ struct Engine {
       a.shift_in = bf.shiftB;
     } else {  // f-update: reduce over the target side, outputs = sources
       a.g.red_rec = bf.recB;
-      a.g.red_bstride = (long)d.m * a.g.rw;
+      a.g.red_bstride = RecLayout<P>::stride(d.m, d.d);
       a.g.out_pts = (const T*)d.x;
       a.g.out_pts_bstride = (long)d.n * d.d;
       a.g.cmat = (const T*)d.ct;
@@ -959,7 +1029,12 @@ struct Engine {
     a.splits_total = splits_total;
     dim3 grid(ceil_div(a.nout, OUT_PER_BLOCK), splits, d.batch);
     const size_t smem = (size_t)a.chunk * a.g.rw * sizeof(T);
-    if constexpr (std::is_same<P, SqE32<2>>::value) {
+    if constexpr (std::is_same<P, SqE32TC>::value) {
+      const size_t tsm = (size_t)TC_STAGES * TC_STAGE_BYTES;
+      UOT_CUDA_TRY(cudaFuncSetAttribute(sk_main_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tsm));
+      sk_main_tc<0><<<grid, TC_THREADS, tsm, st>>>(a, tc_kp(d.d));
+    } else if constexpr (std::is_same<P, SqE32<2>>::value) {
       static_assert(C::COLS % 2 == 0, "packed kernel needs an even column count");
       sk_main_sq2<C::THREADS, C::COLS / 2, C::RT><<<grid, C::THREADS, smem, st>>>(a);
     } else {
@@ -1014,6 +1089,7 @@ struct Engine {
     a.hat_old = hat_old;
     a.shift_out = to_target ? bf.shiftB : bf.shiftA;
     a.rec_out = to_target ? bf.recB : bf.recA;
+    a.rec_bstride = RecLayout<P>::stride(to_target ? d.m : d.n, d.d);
     a.rw = P::rw(d.d);
     a.out_pts = (const T*)(to_target ? d.y : d.x);
     a.d = d.d;
@@ -1066,6 +1142,13 @@ struct Engine {
     sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
                                                       bf.iters_done);
     UOT_CHECK_LAUNCH();
+    if constexpr (std::is_same<P, SqE32TC>::value) {
+      tc_fill_dead<<<1024, 256, 0, st>>>(bf.recA, (long)d.batch * s.recA / tc_kp(d.d), d.d,
+                                         tc_kp(d.d));
+      tc_fill_dead<<<1024, 256, 0, st>>>(bf.recB, (long)d.batch * s.recB / tc_kp(d.d), d.d,
+                                         tc_kp(d.d));
+      UOT_CHECK_LAUNCH();
+    }
     const long nm = std::max(d.n, d.m);
     sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
     sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.m, bf.shiftB);
@@ -1347,6 +1430,8 @@ int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
         if (d.d == 1) return fn(Engine<SqE32<1>>());
         if (d.d == 2) return fn(Engine<SqE32<2>>());
         if (d.d == 3) return fn(Engine<SqE32<3>>());
+        if (d.d >= 32 && tc_kp(d.d) <= 256 && d.nranks <= 1 && d.nccl_comm == nullptr)
+          return fn(Engine<SqE32TC>());
         return fn(Engine<SqE32N>());
       case UOT_COST_POWER:
         return fn(Engine<Pow1D<float>>());

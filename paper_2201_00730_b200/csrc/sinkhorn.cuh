@@ -75,7 +75,8 @@ struct TailArgs {
   T* hat_out;                  // [B][nout]
   const T* hat_old;            // [B][nout] or nullptr (delta tracking)
   T* shift_out;                // [B][nout]
-  T* rec_out;                  // [B][nout][rw]
+  T* rec_out;                  // [B] x rec_bstride records of the output side
+  long rec_bstride;
   int rw;
   const T* out_pts;            // [B][nout][d]
   int d;

@@ -1,0 +1,248 @@
+// sinkhorn_tc.cuh -- tensor-core half-step for squared-Euclidean costs on
+// d >= 32 feature vectors (BASELINE cfg4), sm_100a tcgen05.
+//
+// The exponent of every pair, t_or = z_or - m_o (log2 units), is produced by
+// ONE kind::tf32 GEMM with split-precision compensation and the row / column
+// constants folded into extra K columns:
+//   A row o (output, in TMEM):  [Yh, Yh, Yl, 1, 1, 1, ch, cm, cl, 0...]
+//   B row r (reduced, smem):    [Xh, Xl, Xh, Uh, Um, Ul, 1, 1, 1, 0...]
+// with X = 2L x_r, U_r = (pot_r - |x_r|^2) L + log2 w_r, c_o = -|y_o|^2 L -
+// m_o, every value split into TF32 hi/lo (3 parts for U and c), so
+// Yh.Xh + Yh.Xl + Yl.Xh + U + c reproduces the fp32 exponent to ~2^-21
+// (3xTF32; TF32 alone would miss the 1e-4 eps tolerance).
+// Warp roles: warp 0 streams B stages with 1-D bulk copies (the tail kernel
+// writes B directly in the canonical K-major core-matrix layout), warp 1
+// issues tcgen05.mma from one thread into a double-buffered TMEM
+// accumulator, warps 2-5 read D with tcgen05.ld and run the exp2 / sum
+// epilogue on the MUFU pipe while the next tile is multiplied.
+#pragma once
+
+#include "sinkhorn.cuh"
+#include "tcgen05.cuh"
+
+namespace uot {
+
+constexpr int TC_TILE = 128;        // M (outputs) and N (reduced) per MMA tile
+constexpr int TC_STAGE_K = 40;      // K elements per shared-memory stage
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
+constexpr int TC_STAGE_BYTES = TC_TILE * TC_STAGE_K * 4;  // 20 KiB
+
+__host__ __device__ __forceinline__ int tc_kp(int d) { return (3 * d + 6 + 39) / 40 * 40; }
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
+
+// Index of element (row rl, column k) inside one canonical 128-row tile.
+__device__ __forceinline__ long tc_tile_index(int rl, int k) {
+  return (long)(k >> 2) * (16 * 32) + (rl >> 3) * 32 + (rl & 7) * 4 + (k & 3);
+}
+
+template <int CHECK_UNUSED = 0>
+__global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, int KP) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], dfull[2], dempty[2];
+  __shared__ uint32_t tbase_s;
+  const int b = blockIdx.z;
+  if (A.done != nullptr && A.done[b]) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int split = blockIdx.y, S = gridDim.y;
+  const int ntiles = (A.nred + TC_TILE - 1) / TC_TILE;
+  const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
+  const int nst = KP / TC_STAGE_K;
+  const int d = A.g.d;
+
+  if (warp == 1) tc::tmem_alloc(&tbase_s, 512);
+  if (tid == 0) {
+    for (int i = 0; i < TC_STAGES; ++i) {
+      tc::mbar_init(&full_b[i], 1);
+      tc::mbar_init(&empty_b[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&dfull[i], 1);
+      tc::mbar_init(&dempty[i], 128);
+    }
+    tc::mbar_fence_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = tbase_s;
+
+  // Epilogue threads own one output row each (TMEM lane restriction: warp w
+  // reaches lanes 32*(w%4) .. +31).
+  const int lane_base = 32 * (warp & 3);
+  const int row = lane_base + lane;
+  const int o = blockIdx.x * TC_TILE + row;
+  float m_o = 0.f;
+  if (warp >= 2) {
+    const float* y = A.g.out_pts + b * A.g.out_pts_bstride + (long)(o < A.nout ? o : 0) * d;
+    double s2 = 0.0;
+    for (int k = 0; k < d; ++k) s2 += (double)y[k] * (double)y[k];
+    m_o = o < A.nout ? A.shift_in[(long)b * A.nout + o] : 0.f;
+    const double c = -s2 * (double)A.g.L - (double)m_o;
+    const float ch = tf32_hi((float)c);
+    const double c1 = c - (double)ch;
+    const float cm = tf32_hi((float)c1);
+    const float cl = (float)(c1 - (double)cm);
+    const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
+    for (int k0 = 0; k0 < KP; k0 += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = k0 + e;
+        float val = 0.f;
+        if (k < 3 * d) {
+          const float yk = y[k % d];
+          const float yh = tf32_hi(yk);
+          val = (k < 2 * d) ? yh : (yk - yh);
+        } else if (k < 3 * d + 3) {
+          val = 1.f;
+        } else if (k == 3 * d + 3) {
+          val = ch;
+        } else if (k == 3 * d + 4) {
+          val = cm;
+        } else if (k == 3 * d + 5) {
+          val = cl;
+        }
+        v[e] = __float_as_uint(val);
+      }
+      tc::tmem_st8(ta + k0, v);
+    }
+    tc::wait_st();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+
+  const float* recb = A.g.red_rec + b * A.g.red_bstride;
+  if (warp == 0) {
+    if (tc::elect_one()) {  // producer: B stages
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int tile = t0; tile < t1; ++tile) {
+        for (int st = 0; st < nst; ++st) {
+          tc::mbar_wait(&empty_b[slot], phase ^ 1);
+          tc::mbar_expect_tx(&full_b[slot], TC_STAGE_BYTES);
+          tc::bulk_g2s(smem + slot * TC_STAGE_BYTES,
+                       recb + (long)tile * TC_TILE * KP + (long)st * TC_TILE * TC_STAGE_K,
+                       TC_STAGE_BYTES, &full_b[slot]);
+          if (++slot == TC_STAGES) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {  // MMA issuer
+      const uint32_t idesc = tc::idesc_tf32(TC_TILE, TC_TILE);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < t1 - t0; ++i) {
+        const int buf = i & 1;
+        const uint32_t dph = (i >> 1) & 1;
+        tc::mbar_wait(&dempty[buf], dph ^ 1);
+        tc::fence_after();
+        const uint32_t dcol = tbase + 256 + buf * TC_TILE;
+        for (int st = 0; st < nst; ++st) {
+          tc::mbar_wait(&full_b[slot], phase);
+          tc::fence_after();
+          const unsigned char* sb = smem + slot * TC_STAGE_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
+            const uint64_t bd = tc::sdesc(sb + ks * 2 * 2048, 2048, 128);
+            tc::mma_tf32_ts(dcol, tbase + st * TC_STAGE_K + ks * 8, bd, idesc,
+                            (st | ks) != 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&empty_b[slot]);
+          if (++slot == TC_STAGES) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+        tc::mma_commit(&dfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // Epilogue: exp2 + sum of each accumulator row, range-checked per tile.
+    float acc = 0.f, corr = 0.f;
+    const uint32_t tl = tbase + ((uint32_t)lane_base << 16);
+    for (int i = 0; i < t1 - t0; ++i) {
+      const int buf = i & 1;
+      const uint32_t dph = (i >> 1) & 1;
+      tc::mbar_wait(&dfull[buf], dph);
+      tc::fence_after();
+      const uint32_t dcol = tl + 256 + buf * TC_TILE;
+      float s = 0.f;
+#pragma unroll
+      for (int c = 0; c < TC_TILE / 32; ++c) {
+        uint32_t v[32];
+        tc::tmem_ld32(dcol + c * 32, v);
+        tc::wait_ld();
+        float sa = 0.f, sb = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          sa += Dom<float>::ex(__uint_as_float(v[e]) + corr);
+          sb += Dom<float>::ex(__uint_as_float(v[e + 1]) + corr);
+        }
+        s += sa + sb;
+      }
+      float na = acc + s;
+      if (!(na < 1.2676506e30f && na > 7.8886091e-31f)) {
+        // Rare: the stale shift is off by > 2^100 -- rescale from this tile's max.
+        float mx = -INFINITY;
+        for (int c = 0; c < TC_TILE / 32; ++c) {
+          uint32_t v[32];
+          tc::tmem_ld32(dcol + c * 32, v);
+          tc::wait_ld();
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) + corr);
+        }
+        float mn = mx;
+        if (acc > 0.f) mn = fmaxf(mn, Dom<float>::lg(acc));
+        if (mn > -INFINITY && mn < INFINITY) {
+          if (acc > 0.f) acc *= Dom<float>::ex(-mn);
+          corr -= mn;
+        }
+        s = 0.f;
+        for (int c = 0; c < TC_TILE / 32; ++c) {
+          uint32_t v[32];
+          tc::tmem_ld32(dcol + c * 32, v);
+          tc::wait_ld();
+          for (int e = 0; e < 32; ++e) s += Dom<float>::ex(__uint_as_float(v[e]) + corr);
+        }
+        na = acc + s;
+      }
+      acc = na;
+      tc::fence_before();
+      tc::mbar_arrive(&dempty[buf]);
+    }
+    if (o < A.nout) {
+      const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
+      A.part_m[idx] = m_o - corr;
+      A.part_a[idx] = acc;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_free(tbase, 512);
+}
+
+// Dead-row fill of a canonical record buffer: every row gets U = -1e30
+// (exp2 -> 0) and the unit columns, so padded rows of the last tile never
+// contribute; live rows are overwritten by the tails.
+__global__ void tc_fill_dead(float* buf, long nrows_padded, int d, int KP) {
+  const long total = nrows_padded * KP;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const long tile = idx / ((long)TC_TILE * KP);
+    const long rem = idx % ((long)TC_TILE * KP);
+    const int k = (int)(rem / (16 * 32)) * 4 + (int)(rem % 4);
+    float v = 0.f;
+    if (k == 3 * d) v = -1e30f;
+    else if (k >= 3 * d + 3 && k < 3 * d + 6) v = 1.f;
+    buf[tile * TC_TILE * KP + rem] = v;
+  }
+}
+
+}  // namespace uot

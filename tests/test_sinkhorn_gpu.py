@@ -157,3 +157,19 @@ def test_row_sharded_protocol_emulated(precision, nshards):
         fr, gr = translated(c.alpha, c.beta, f1[0], g1[0], c.rho, c.rho)
         assert np.abs(ft - fr).max() <= 1e-4 * c.eps
         assert np.abs(gt - gr).max() <= 1e-4 * c.eps
+
+
+@pytest.mark.parametrize("d,n,m", [(64, 300, 257), (32, 128, 640), (48, 513, 129)])
+def test_tcgen05_point_clouds_vs_oracle(d, n, m):
+    """d >= 32 runs the tcgen05 3xTF32 kernel; ragged sizes exercise the
+    padded tiles.  fp32 tolerance on the translated pair (1e-4 eps)."""
+    x, y, a, b = S.cfg4_batch(batch=2, n=n, m=m, d=d, seed=d)
+    eps, rho = 0.05, 0.5
+    f, g, _, _ = run_dev(x, y, a, b, eps, rho, 40, precision="fp32")
+    for k in range(2):
+        cost = O.PointCost(x[k], y[k])
+        fo, go, _ = O.sinkhorn_fixed(cost, a[k], b[k], eps, rho, rho, "h", 40)
+        ft, gt = translated(a[k], b[k], f[k], g[k], rho, rho)
+        fr, gr = translated(a[k], b[k], fo, go, rho, rho)
+        assert np.abs(ft - fr).max() <= 1e-4 * eps, (k, np.abs(ft - fr).max())
+        assert np.abs(gt - gr).max() <= 1e-4 * eps
