@@ -234,20 +234,19 @@ struct SqE32TC {
       const float xh = tf32_hi(x);
       tile[tc_tile_index(rl, k)] = xh;
       tile[tc_tile_index(rl, d + k)] = x - xh;
-      tile[tc_tile_index(rl, 2 * d + k)] = xh;
       s2 += (double)pt[k] * (double)pt[k];
     }
     const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
     const float uh = tf32_hi((float)u);
     const double u1 = u - (double)uh;
     const float um = tf32_hi((float)u1);
-    tile[tc_tile_index(rl, 3 * d)] = uh;
-    tile[tc_tile_index(rl, 3 * d + 1)] = um;
-    tile[tc_tile_index(rl, 3 * d + 2)] = (float)(u1 - (double)um);
-    tile[tc_tile_index(rl, 3 * d + 3)] = 1.f;
-    tile[tc_tile_index(rl, 3 * d + 4)] = 1.f;
-    tile[tc_tile_index(rl, 3 * d + 5)] = 1.f;
-    for (int k = 3 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k)] = 0.f;
+    tile[tc_tile_index(rl, 2 * d)] = uh;
+    tile[tc_tile_index(rl, 2 * d + 1)] = um;
+    tile[tc_tile_index(rl, 2 * d + 2)] = (float)(u1 - (double)um);
+    tile[tc_tile_index(rl, 2 * d + 3)] = 1.f;
+    tile[tc_tile_index(rl, 2 * d + 4)] = 1.f;
+    tile[tc_tile_index(rl, 2 * d + 5)] = 1.f;
+    for (int k = 2 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k)] = 0.f;
   }
 };
 
@@ -1430,7 +1429,8 @@ int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
         if (d.d == 1) return fn(Engine<SqE32<1>>());
         if (d.d == 2) return fn(Engine<SqE32<2>>());
         if (d.d == 3) return fn(Engine<SqE32<3>>());
-        if (d.d >= 32 && tc_kp(d.d) <= 256 && d.nranks <= 1 && d.nccl_comm == nullptr)
+        if (d.d >= 32 && d.d % 8 == 0 && tc_ka(d.d) <= 256 && d.nranks <= 1 &&
+            d.nccl_comm == nullptr)
           return fn(Engine<SqE32TC>());
         return fn(Engine<SqE32N>());
       case UOT_COST_POWER:

@@ -2,14 +2,16 @@
 // d >= 32 feature vectors (BASELINE cfg4), sm_100a tcgen05.
 //
 // The exponent of every pair, t_or = z_or - m_o (log2 units), is produced by
-// ONE kind::tf32 GEMM with split-precision compensation and the row / column
+// kind::tf32 MMAs with split-precision compensation and the row / column
 // constants folded into extra K columns:
-//   A row o (output, in TMEM):  [Yh, Yh, Yl, 1, 1, 1, ch, cm, cl, 0...]
-//   B row r (reduced, smem):    [Xh, Xl, Xh, Uh, Um, Ul, 1, 1, 1, 0...]
+//   A row o (output, in TMEM):  [Yh(d), Yl(d), 1, 1, 1, ch, cm, cl, 0..]
+//   B row r (reduced, smem):    [Xh(d), Xl(d), Uh, Um, Ul, 1, 1, 1, 0..]
 // with X = 2L x_r, U_r = (pot_r - |x_r|^2) L + log2 w_r, c_o = -|y_o|^2 L -
-// m_o, every value split into TF32 hi/lo (3 parts for U and c), so
-// Yh.Xh + Yh.Xl + Yl.Xh + U + c reproduces the fp32 exponent to ~2^-21
-// (3xTF32; TF32 alone would miss the 1e-4 eps tolerance).
+// m_o, every value split into TF32 hi/lo (3 parts for U and c).  Per 8-wide
+// K slice the issuer runs Yh.Xh, Yl.Xh (same B data, two A offsets) and
+// Yh.Xl, so the 3xTF32 product Yh.Xh + Yl.Xh + Yh.Xl + U + c reproduces the
+// fp32 exponent to ~2^-21 while B carries each X value only twice
+// (TF32 alone would miss the 1e-4 eps tolerance).
 // Warp roles: warp 0 streams B stages with 1-D bulk copies (the tail kernel
 // writes B directly in the canonical K-major core-matrix layout), warp 1
 // issues tcgen05.mma from one thread into a double-buffered TMEM
@@ -23,12 +25,14 @@
 namespace uot {
 
 constexpr int TC_TILE = 128;        // M (outputs) and N (reduced) per MMA tile
-constexpr int TC_STAGE_K = 40;      // K elements per shared-memory stage
-constexpr int TC_STAGES = 4;
+constexpr int TC_STAGE_K = 16;      // K elements per shared-memory stage
+constexpr int TC_STAGES = 12;
 constexpr int TC_THREADS = 192;
-constexpr int TC_STAGE_BYTES = TC_TILE * TC_STAGE_K * 4;  // 20 KiB
+constexpr int TC_STAGE_BYTES = TC_TILE * TC_STAGE_K * 4;  // 8 KiB
 
-__host__ __device__ __forceinline__ int tc_kp(int d) { return (3 * d + 6 + 39) / 40 * 40; }
+// K extent of a reduced-side record (B) and of an output-side row (A).
+__host__ __device__ __forceinline__ int tc_kp(int d) { return (2 * d + 6 + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int tc_ka(int d) { return 2 * d + 8; }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
 
@@ -85,23 +89,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const float cm = tf32_hi((float)c1);
     const float cl = (float)(c1 - (double)cm);
     const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
-    for (int k0 = 0; k0 < KP; k0 += 8) {
+    const int KA = tc_ka(d);
+    for (int k0 = 0; k0 < KA; k0 += 8) {
       uint32_t v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int k = k0 + e;
         float val = 0.f;
-        if (k < 3 * d) {
+        if (k < 2 * d) {
           const float yk = y[k % d];
           const float yh = tf32_hi(yk);
-          val = (k < 2 * d) ? yh : (yk - yh);
-        } else if (k < 3 * d + 3) {
+          val = (k < d) ? yh : (yk - yh);
+        } else if (k < 2 * d + 3) {
           val = 1.f;
-        } else if (k == 3 * d + 3) {
+        } else if (k == 2 * d + 3) {
           val = ch;
-        } else if (k == 3 * d + 4) {
+        } else if (k == 2 * d + 4) {
           val = cm;
-        } else if (k == 3 * d + 5) {
+        } else if (k == 2 * d + 5) {
           val = cl;
         }
         v[e] = __float_as_uint(val);
@@ -144,15 +149,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
         tc::mbar_wait(&dempty[buf], dph ^ 1);
         tc::fence_after();
         const uint32_t dcol = tbase + 256 + buf * TC_TILE;
+        bool first = true;
         for (int st = 0; st < nst; ++st) {
           tc::mbar_wait(&full_b[slot], phase);
           tc::fence_after();
           const unsigned char* sb = smem + slot * TC_STAGE_BYTES;
 #pragma unroll
           for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
+            const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
             const uint64_t bd = tc::sdesc(sb + ks * 2 * 2048, 2048, 128);
-            tc::mma_tf32_ts(dcol, tbase + st * TC_STAGE_K + ks * 8, bd, idesc,
-                            (st | ks) != 0 ? 1u : 0u);
+            if (kb < d) {  // Xh: pair with Yh and Yl
+              tc::mma_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
+              tc::mma_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
+              first = false;
+            } else if (kb < 2 * d) {  // Xl: pair with Yh
+              tc::mma_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
+              first = false;
+            } else if (kb < 2 * d + 8) {  // U parts / ones against ones / c parts
+              tc::mma_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
+              first = false;
+            }
           }
           tc::mma_commit(&empty_b[slot]);
           if (++slot == TC_STAGES) {
@@ -175,18 +191,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       tc::fence_after();
       const uint32_t dcol = tl + 256 + buf * TC_TILE;
       float s = 0.f;
-#pragma unroll
-      for (int c = 0; c < TC_TILE / 32; ++c) {
-        uint32_t v[32];
-        tc::tmem_ld32(dcol + c * 32, v);
+      {
+        uint32_t v0[32], v1[32], v2[32], v3[32];
+        tc::tmem_ld32(dcol, v0);
+        tc::tmem_ld32(dcol + 32, v1);
+        tc::tmem_ld32(dcol + 64, v2);
+        tc::tmem_ld32(dcol + 96, v3);
         tc::wait_ld();
-        float sa = 0.f, sb = 0.f;
+        float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
+        if (__all_sync(0xffffffffu, corr == 0.f)) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          sa += Dom<float>::ex(__uint_as_float(v[e]) + corr);
-          sb += Dom<float>::ex(__uint_as_float(v[e + 1]) + corr);
+          for (int e = 0; e < 32; ++e) {
+            sa += Dom<float>::ex(__uint_as_float(v0[e]));
+            sb += Dom<float>::ex(__uint_as_float(v1[e]));
+            sc += Dom<float>::ex(__uint_as_float(v2[e]));
+            sd += Dom<float>::ex(__uint_as_float(v3[e]));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            sa += Dom<float>::ex(__uint_as_float(v0[e]) + corr);
+            sb += Dom<float>::ex(__uint_as_float(v1[e]) + corr);
+            sc += Dom<float>::ex(__uint_as_float(v2[e]) + corr);
+            sd += Dom<float>::ex(__uint_as_float(v3[e]) + corr);
+          }
         }
-        s += sa + sb;
+        s = (sa + sb) + (sc + sd);
       }
       float na = acc + s;
       if (!(na < 1.2676506e30f && na > 7.8886091e-31f)) {
@@ -239,8 +269,8 @@ __global__ void tc_fill_dead(float* buf, long nrows_padded, int d, int KP) {
     const long rem = idx % ((long)TC_TILE * KP);
     const int k = (int)(rem / (16 * 32)) * 4 + (int)(rem % 4);
     float v = 0.f;
-    if (k == 3 * d) v = -1e30f;
-    else if (k >= 3 * d + 3 && k < 3 * d + 6) v = 1.f;
+    if (k == 2 * d) v = -1e30f;
+    else if (k >= 2 * d + 3 && k < 2 * d + 6) v = 1.f;
     buf[tile * TC_TILE * KP + rem] = v;
   }
 }
