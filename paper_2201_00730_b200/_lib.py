@@ -13,7 +13,7 @@ import os
 from . import exceptions as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_uot_b200.so")
+SO_PATH = os.environ.get("UOT_B200_LIB") or os.path.join(_HERE, "_uot_b200.so")
 
 UOT_OK = 0
 F32, F64 = 0, 1

@@ -17,6 +17,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "_uot_b200.so")
+# Experiment hooks: UOT_NVCC_EXTRA adds nvcc flags (e.g. -DFW_MINB=3) and
+# UOT_B200_VARIANT builds _uot_b200_<variant>.so from build_<variant>/ so a
+# variant can be loaded side by side (UOT_B200_LIB=... at import time).
+VARIANT = os.environ.get("UOT_B200_VARIANT", "")
+if VARIANT:
+    OUT = os.path.join(HERE, f"_uot_b200_{VARIANT}.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -47,11 +53,12 @@ def build(verbose=False, force=False):
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
     inc, lib = _nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + (f"_{VARIANT}" if VARIANT else ""))
     os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-DUOT_WITH_NCCL",
                     "-I" + inc, "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
+    flags += os.environ.get("UOT_NVCC_EXTRA", "").split()
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

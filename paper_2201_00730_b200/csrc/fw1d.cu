@@ -19,8 +19,10 @@
 // fw.py:106-148) by safeguarded Newton on three moments per pass instead of
 // the reference's 123 ternary evaluations (FW parity).
 #include <algorithm>
+#include <type_traits>
 
 #include "../../include/uot_b200.h"
+#include "blockops.cuh"
 #include "common.cuh"
 
 namespace uot {
@@ -61,122 +63,24 @@ struct FwArgs {
   int* scratch_i;
 };
 
-// exp(x) for x <= 0 (arguments are shifted by their maximum): Cody-Waite
-// reduction by ln 2 and a degree-13 Taylor polynomial on |r| <= ln2/2
-// (truncation < 0.05 ulp); results below 2^-1022 flush to 0 (they are
-// negligible next to the unit maximum term).  ~20 instructions versus the
-// libdevice routine's special-case handling.
-__device__ __forceinline__ double exp_nonpos(double x) {
-  if (x < -708.0) return 0.0;
-  const double n = rint(x * 1.4426950408889634074);
-  double r = fma(n, -6.93147180369123816490e-01, x);
-  r = fma(n, -1.90821492927058770002e-10, r);
-  double q = 1.6059043836821614599e-10;  // 1/13!
-  q = fma(q, r, 2.0876756987868098979e-09);
-  q = fma(q, r, 2.5052108385441718775e-08);
-  q = fma(q, r, 2.7557319223985890653e-07);
-  q = fma(q, r, 2.7557319223985890653e-06);
-  q = fma(q, r, 2.4801587301587301587e-05);
-  q = fma(q, r, 1.9841269841269841270e-04);
-  q = fma(q, r, 1.3888888888888888889e-03);
-  q = fma(q, r, 8.3333333333333333333e-03);
-  q = fma(q, r, 4.1666666666666666667e-02);
-  q = fma(q, r, 1.6666666666666666667e-01);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  const long long e = (long long)((int)n + 1023) << 52;
-  return q * __longlong_as_double(e);
-}
+__device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
 
 __device__ __forceinline__ double pcost(double xi, double yj, double p) {
   const double d = xi - yj;
   if (p == 2.0) return d * d;
   const double ad = fabs(d);
   if (p == 1.0) return ad;
-  return pow(ad, p);
+  return pow_abs(d, p);
 }
 
-// Block reduction of K doubles (sum).  scratch: K * 32 doubles.
-template <int K>
-__device__ __forceinline__ void bsum(double (&v)[K], double* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = v[k];
-  }
-  __syncthreads();
-  constexpr int NW = FW_THREADS / 32;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s += scratch[k * 32 + w];
-    v[k] = s;
-  }
-  __syncthreads();
-}
-
-template <int K>
-__device__ __forceinline__ void bmax(double (&v)[K], double* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_max(v[k]);
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = v[k];
-  }
-  __syncthreads();
-  constexpr int NW = FW_THREADS / 32;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double s = -CUDART_INF;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s = fmax(s, scratch[k * 32 + w]);
-    v[k] = s;
-  }
-  __syncthreads();
-}
-
-// Exclusive block scan of K per-thread totals (sum); returns prefix offsets.
-template <int K>
-__device__ __forceinline__ void bscan_excl(double (&v)[K], double (&total)[K], double* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double incl[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double s = v[k];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double t = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += t;
-    }
-    incl[k] = s;
-  }
-  __syncthreads();
-  if (lane == 31) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) scratch[k * 32 + warp] = incl[k];
-  }
-  __syncthreads();
-  constexpr int NW = FW_THREADS / 32;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double off = 0.0, tot = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const double s = scratch[k * 32 + w];
-      if (w < warp) off += s;
-      tot += s;
-    }
-    total[k] = tot;
-    v[k] = off + incl[k] - v[k];
-  }
-  __syncthreads();
+// Cost kinds resolved at compile time for the FW kernels: PK = 0 -> p = 2,
+// 1 -> p = 1, 2 -> general p (one out-of-line pow keeps the kernel small).
+template <int PK>
+__device__ __forceinline__ double pcost_k(double xi, double yj, double p) {
+  const double d = xi - yj;
+  if constexpr (PK == 0) return d * d;
+  else if constexpr (PK == 1) return fabs(d);
+  else return pow_abs(d, p);
 }
 
 __device__ __forceinline__ int ibsum(int v, int* scratch) {
@@ -210,96 +114,13 @@ __device__ __forceinline__ int excl_max_scan(int v, int* scratch) {
   return excl;
 }
 
-// #{ l in [0, len) : arr[l] < v }  (strict) or <= v (non-strict)
-template <bool STRICT>
-__device__ __forceinline__ int count_below(const double* arr, int len, double v) {
-  int lo = 0, hi = len;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const bool below = STRICT ? (arr[mid] < v) : (arr[mid] <= v);
-    if (below)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// Block reduction of KS sums and KM maxima in one pass.  scratch: (KS+KM)*32.
-template <int KS, int KM>
-__device__ __forceinline__ void bred(double (&sv)[KS], double (&mv)[KM], double* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < KS; ++k) sv[k] = warp_sum(sv[k]);
-#pragma unroll
-  for (int k = 0; k < KM; ++k) mv[k] = warp_max(mv[k]);
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < KS; ++k) scratch[k * 32 + warp] = sv[k];
-#pragma unroll
-    for (int k = 0; k < KM; ++k) scratch[(KS + k) * 32 + warp] = mv[k];
-  }
-  __syncthreads();
-  constexpr int NW = FW_THREADS / 32;
-#pragma unroll
-  for (int k = 0; k < KS; ++k) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) t += scratch[k * 32 + w];
-    sv[k] = t;
-  }
-#pragma unroll
-  for (int k = 0; k < KM; ++k) {
-    double t = -CUDART_INF;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) t = fmax(t, scratch[(KS + k) * 32 + w]);
-    mv[k] = t;
-  }
-  __syncthreads();
-}
-
-// Two (max, sum) log-sum-exp pairs reduced over the block in one pass.
-__device__ __forceinline__ void block_lse2(LsePair& a, LsePair& b, double* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  a = warp_lse(a);
-  b = warp_lse(b);
-  __syncthreads();
-  if (lane == 0) {
-    scratch[warp] = a.m;
-    scratch[32 + warp] = a.s;
-    scratch[64 + warp] = b.m;
-    scratch[96 + warp] = b.s;
-  }
-  __syncthreads();
-  LsePair ra{-CUDART_INF, 0.0}, rb{-CUDART_INF, 0.0};
-  for (int w = 0; w < FW_THREADS / 32; ++w) {
-    ra = lse_merge(ra, LsePair{scratch[w], scratch[32 + w]});
-    rb = lse_merge(rb, LsePair{scratch[64 + w], scratch[96 + w]});
-  }
-  a = ra;
-  b = rb;
-  __syncthreads();
-}
-
-// Galloping search: first index in [j, len) with !(arr[idx] < v) (STRICT) or
-// !(arr[idx] <= v), starting from a known lower bound j.
-template <bool STRICT>
-__device__ __forceinline__ int advance_below(const double* arr, int len, int j, double v) {
-#pragma unroll 1
-  for (int step = 0; step < 6; ++step) {
-    if (j >= len) return len;
-    const bool below = STRICT ? (arr[j] < v) : (arr[j] <= v);
-    if (!below) return j;
-    ++j;
-  }
-  return j + count_below<STRICT>(arr + j, len - j, v);
-}
-
 // Per-problem CTA.  Thread t owns source/target elements t*EPT .. t*EPT+EPT-1
 // of each side.  Shared memory holds the supports, the constant weights, the
-// breakpoints and the tilted weights; registers hold the potentials.
-template <int EPT>
+// breakpoints and the merge ranks; registers hold the potentials.
+constexpr int FW_NW = FW_THREADS / 32;
+constexpr int FW_BUF = 16 * FW_NW;  // one reduction buffer (doubles)
+
+template <int EPT, int PK>
 struct Cta {
   int n, m;
   double p;
@@ -307,15 +128,49 @@ struct Cta {
   const double* sy;
   double* sA;
   double* sB;
-  double* red;
+  unsigned short* rkA;  // rkA[k] = #target events before source event k in the merge
+  unsigned short* rkB;  // rkB[l] = #source events before target event l
+  double* zred;  // scratch of the zero-weight fix (own syncs)
   bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
 
   __device__ int src(int e) const { return threadIdx.x * EPT + e; }
 
-  // Balanced 1-D OT oracle on (ta, tb): cumulative masses -> partner searches
-  // -> dual potentials (r, s).  Leaves sA/sB holding the breakpoints.
+  // Merge path over the breakpoints: thread t emits merged positions
+  // [2 EPT t, 2 EPT (t+1)) of the sweep order (source first on ties,
+  // ot1d.py:158) after one diagonal binary search, recording for every event
+  // its partner index -- the number of events of the other side before it.
+  __device__ void merge_ranks() {
+    const int na = n - 1, nb = m - 1, E = na + nb;
+    constexpr int IPT = 2 * EPT;
+    const int d0 = min((int)threadIdx.x * IPT, E);
+    int lo = max(0, d0 - nb), hi = min(d0, na);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sA[mid] <= sB[d0 - 1 - mid])
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int i = lo, j = d0 - lo;
+#pragma unroll
+    for (int s = 0; s < IPT; ++s) {
+      if (d0 + s < E) {
+        const double av = i < na ? sA[i] : CUDART_INF;
+        const double bv = j < nb ? sB[j] : CUDART_INF;
+        const bool takeA = av <= bv;
+        unsigned short* dst = takeA ? rkA + i : rkB + j;
+        *dst = (unsigned short)(takeA ? j : i);
+        i += takeA;
+        j += !takeA;
+      }
+    }
+  }
+
+  // Balanced 1-D OT oracle on (ta, tb): cumulative masses -> merge ranks ->
+  // dual potentials (r, s).  Leaves sA/sB/rkA/rkB describing the plan.
+  template <typename PING>
   __device__ void oracle(const double (&ta)[EPT], const double (&tb)[EPT], double (&r)[EPT],
-                         double (&s)[EPT], double& mass_a, double& mass_b) {
+                         double (&s)[EPT], double& mass_a, double& mass_b, PING& ping) {
     double pa[EPT], pb[EPT];
     double ca = 0.0, cb = 0.0;
 #pragma unroll
@@ -326,7 +181,7 @@ struct Cta {
       pb[e] = cb;
     }
     double tot[2] = {ca, cb}, totals[2];
-    bscan_excl<2>(tot, totals, red);
+    bops::block_scan_excl<FW_NW, 2>(tot, totals, ping.next());
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
@@ -346,8 +201,8 @@ struct Cta {
         if (i < n && ta[e] > 0.0) lza = i;
         if (i < m && tb[e] > 0.0) lzb = i;
       }
-      int pra = excl_max_scan(lza, reinterpret_cast<int*>(red));
-      int prb = excl_max_scan(lzb, reinterpret_cast<int*>(red));
+      int pra = excl_max_scan(lza, reinterpret_cast<int*>(zred));
+      int prb = excl_max_scan(lzb, reinterpret_cast<int*>(zred));
       __syncthreads();
       double fa[EPT], fb[EPT];
 #pragma unroll
@@ -367,39 +222,30 @@ struct Cta {
       }
     }
     __syncthreads();
-    // cost increments along the staircase; partners of this thread's
-    // consecutive events are monotone, so search once and gallop.
+    merge_ranks();
+    __syncthreads();
+    // cost increments along the staircase
     double da[EPT], db[EPT];
     double la = 0.0, lb = 0.0;
-    int j = 0, k = 0;
-    bool fj = true, fk = true;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
       da[e] = 0.0;
       db[e] = 0.0;
       if (i >= 1 && i < n) {
-        // source event i-1: partner j = #{l < m-1 : B_l < A_{i-1}}
-        const double v = sA[i - 1];
-        j = fj ? count_below<true>(sB, m - 1, v) : advance_below<true>(sB, m - 1, j, v);
-        fj = false;
-        const double yj = sy[j];
-        da[e] = pcost(sx[i], yj, p) - pcost(sx[i - 1], yj, p);
+        const double yj = sy[rkA[i - 1]];  // partner of source event i-1
+        da[e] = pcost_k<PK>(sx[i], yj, p) - pcost_k<PK>(sx[i - 1], yj, p);
       }
       if (i >= 1 && i < m) {
-        // target event i-1: partner = #{k < n-1 : A_k <= B_{i-1}}
-        const double v = sB[i - 1];
-        k = fk ? count_below<false>(sA, n - 1, v) : advance_below<false>(sA, n - 1, k, v);
-        fk = false;
-        const double xk = sx[k];
-        db[e] = pcost(xk, sy[i], p) - pcost(xk, sy[i - 1], p);
+        const double xk = sx[rkB[i - 1]];  // partner of target event i-1
+        db[e] = pcost_k<PK>(xk, sy[i], p) - pcost_k<PK>(xk, sy[i - 1], p);
       }
       la += da[e];
       lb += db[e];
     }
     double off[2] = {la, lb}, unused[2];
-    bscan_excl<2>(off, unused, red);
-    const double s0 = pcost(sx[0], sy[0], p);
+    bops::block_scan_excl<FW_NW, 2>(off, unused, ping.next());
+    const double s0 = pcost_k<PK>(sx[0], sy[0], p);
     double ra = off[0], rb = off[1];
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
@@ -410,30 +256,28 @@ struct Cta {
     }
   }
 
-  // Plan of the breakpoints in sA/sB, compacted to positive-mass entries in
-  // sweep order (ot1d.py:149-153).  vals: n+m doubles, codes: 2(n+m) ints.
+  // Plan of the current merge, compacted to positive-mass entries in sweep
+  // order (ot1d.py:149-153).  vals: n+m doubles, codes: 2(n+m) ints.
   __device__ void extract_plan(double* vals, int* codes, int* ei, int* ej, double* em,
                                int* count, double total) {
     const int nev = (n - 1) + (m - 1);
     for (int i = threadIdx.x; i < n - 1; i += FW_THREADS) {
-      const double v = sA[i];
-      const int j = count_below<true>(sB, m - 1, v);
+      const int j = rkA[i];
       const int rank = i + j;
-      vals[rank] = v;
+      vals[rank] = sA[i];
       codes[2 * rank] = i + 1;
       codes[2 * rank + 1] = j;
     }
     for (int l = threadIdx.x; l < m - 1; l += FW_THREADS) {
-      const double v = sB[l];
-      const int k = count_below<false>(sA, n - 1, v);
+      const int k = rkB[l];
       const int rank = l + k;
-      vals[rank] = v;
+      vals[rank] = sB[l];
       codes[2 * rank] = k;
       codes[2 * rank + 1] = l + 1;
     }
     __syncthreads();
     int base = 0;
-    int* iscr = reinterpret_cast<int*>(red);
+    int* iscr = reinterpret_cast<int*>(zred);
     for (int s0 = 0; s0 <= nev; s0 += FW_THREADS) {
       const int s = s0 + threadIdx.x;
       double mass = 0.0;
@@ -459,7 +303,7 @@ struct Cta {
       if (lane == 31) iscr[warp] = incl;
       __syncthreads();
       int off = 0, tot = 0;
-      for (int w = 0; w < FW_THREADS / 32; ++w) {
+      for (int w = 0; w < FW_NW; ++w) {
         if (w < warp) off += iscr[w];
         tot += iscr[w];
       }
@@ -477,10 +321,11 @@ struct Cta {
   }
 };
 
-template <int EPT>
+template <int EPT, int PK>
 __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double red[16 * 32];
+  __shared__ __align__(16) double red[3 * FW_BUF];
+  __shared__ double tab[32];
   const int b = blockIdx.x;
   const int n = A.n, m = A.m;
   double* sx = smem;
@@ -489,7 +334,11 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   double* sB = sA + n;
   double* sal = sB + m;  // constant weights
   double* sbe = sal + n;
-  Cta<EPT> c{n, m, A.p, sx, sy, sA, sB, red, false};
+  unsigned short* rkA = reinterpret_cast<unsigned short*>(sbe + m);
+  unsigned short* rkB = rkA + n;
+  Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false};
+  bops::Ping<FW_BUF> ping{red, 0};
+  bops::load_exp_table(tab);
 
   int nz = 0;
   for (int i = threadIdx.x; i < n; i += FW_THREADS) {
@@ -504,7 +353,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     sbe[j] = w;
     nz += (w == 0.0);
   }
-  c.zeros = ibsum(nz, reinterpret_cast<int*>(red)) > 0;  // (syncs: smem now visible)
+  c.zeros = ibsum(nz, reinterpret_cast<int*>(c.zred)) > 0;  // (syncs: smem now visible)
 
   double f[EPT], g[EPT];
 #pragma unroll
@@ -528,7 +377,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       ta[e] = i < n ? sal[i] : 0.0;
       tb[e] = i < m ? sbe[i] : 0.0;
     }
-    c.oracle(ta, tb, r, s, ma, mb);
+    c.oracle(ta, tb, r, s, ma, mb, ping);
     const int bad = fabs(ma - mb) > 1e-9 * fmax(ma, mb);  // ot1d.py:133-136
     if (threadIdx.x == 0) A.status[b] = bad ? UOT_MASS_BALANCE : 0;
     if (bad) return;
@@ -542,21 +391,32 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     return;
   }
 
+  const int lane = threadIdx.x & 31;
   const double r1 = A.r1, r2 = A.r2;
   const double i1 = 1.0 / r1, i2 = 1.0 / r2;
   const double t1 = r1 / (r1 + r2), t2 = r2 / (r1 + r2);
   double malpha, mbeta;
+  // Shifts of the two log-sum-exps: exact maxima of u = -f/r1, u' = -g/r2
+  // over the positive-weight atoms at t = 0, then the upper bound
+  // (1-gamma) shift + gamma max(-r/r1) carried through each update, so no
+  // per-iteration max reduction is needed (an underflowing sum falls back
+  // to the exact maxima).
+  double sha, shb;
   {
-    double ms[2] = {0.0, 0.0}, mm0[1] = {0.0};
+    double ms[2] = {0.0, 0.0}, mx[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       if (i < n) ms[0] += sal[i];
       if (i < m) ms[1] += sbe[i];
+      if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+      if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
     }
-    bred<2, 1>(ms, mm0, red);
+    bops::block_red<FW_NW, 2, 2>(ms, mx, ping.next());
     malpha = ms[0];
     mbeta = ms[1];
+    sha = mx[0];
+    shb = mx[1];
   }
 
   int status = 0;
@@ -564,44 +424,49 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   double last_primal = 0.0, last_dual = 0.0;
   for (int t = 0; t < A.max_iters; ++t) {
     // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303).
-    // Thread-local (max, sum) pairs merged over the block in one pass; the
-    // exponentials are shared between the log-sum-exps and the tilt.
+    // The exponentials are shared between the log-sum-exps and the tilt.
     double ta[EPT], tb[EPT];
-    double mxa = -CUDART_INF, mxb = -CUDART_INF;
+    double sums[2];
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      sums[0] = 0.0;
+      sums[1] = 0.0;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = c.src(e);
-      if (i < n && sal[i] > 0.0) mxa = fmax(mxa, -f[e] * i1);
-      if (i < m && sbe[i] > 0.0) mxb = fmax(mxb, -g[e] * i2);
-    }
-    {
-      double mxs[2] = {mxa, mxb};
-      bmax<2>(mxs, red);
-      mxa = mxs[0];
-      mxb = mxs[1];
-    }
-    LsePair pa{mxa, 0.0}, pb{mxb, 0.0};
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
+        // weights are >= 0 and exp_fast is finite, so zero weights give 0
+        ta[e] = wa * bops::exp_fast(-f[e] * i1 - sha, tab);
+        tb[e] = wb * bops::exp_fast(-g[e] * i2 - shb, tab);
+        sums[0] += ta[e];
+        sums[1] += tb[e];
+      }
+      bops::block_sum<FW_NW, 2>(sums, ping.next());
+      // block-uniform: a stale shift far above the maximum underflowed
+      if (!((sums[0] < 1e-280 && sha > -CUDART_INF) || (sums[1] < 1e-280 && shb > -CUDART_INF)))
+        break;
+      double mx[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = c.src(e);
-      const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
-      ta[e] = wa > 0.0 ? wa * exp_nonpos(-f[e] * i1 - mxa) : 0.0;
-      tb[e] = wb > 0.0 ? wb * exp_nonpos(-g[e] * i2 - mxb) : 0.0;
-      pa.s += ta[e];
-      pb.s += tb[e];
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+        if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
+      }
+      bops::block_max<FW_NW, 2>(mx, ping.next());
+      sha = mx[0];
+      shb = mx[1];
     }
-    {
-      double sums[2] = {pa.s, pb.s};
-      bsum<2>(sums, red);
-      pa.s = sums[0];
-      pb.s = sums[1];
-    }
-    const double la = pa.m + log(pa.s);
-    const double lb = pb.m + log(pb.s);
+    // Scalars, one transcendental per lane: lanes 0/1 take the logs, lanes
+    // 0/1/2 the exponentials of H_0 and of the two tilt factors.
+    const double lg = log((lane & 1) ? sums[1] : sums[0]);
+    const double la = sha + __shfl_sync(bops::FULL, lg, 0);
+    const double lb = shb + __shfl_sync(bops::FULL, lg, 1);
     const double lam = (r1 * r2 / (r1 + r2)) * (la - lb);
-    const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * exp(t1 * la + t2 * lb);
-    const double sca = mxa > -CUDART_INF ? exp(mxa - lam / r1) : 0.0;
-    const double scb = mxb > -CUDART_INF ? exp(mxb + lam / r2) : 0.0;
+    const double earg = lane == 0 ? t1 * la + t2 * lb : lane == 1 ? sha - lam / r1 : shb + lam / r2;
+    const double ev = exp(earg);  // (libdevice: arguments are not shifted here)
+    const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * __shfl_sync(bops::FULL, ev, 0);
+    const double sca = sha > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 1) : 0.0;
+    const double scb = shb > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 2) : 0.0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       ta[e] *= sca;
@@ -609,7 +474,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     }
     // --- linear oracle (ot1d.py:112-172 on the tilted marginals, fw.py:159-173)
     double r[EPT], s[EPT], mta, mtb;
-    c.oracle(ta, tb, r, s, mta, mtb);
+    c.oracle(ta, tb, r, s, mta, mtb, ping);
     if (fabs(mta - mtb) > 1e-9 * fmax(mta, mtb)) {  // fw.py:161-166
       status = UOT_MASS_BALANCE;
       break;
@@ -617,29 +482,27 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     // --- gaps, primal and line-search moments at gamma = 0.  log(ta/alpha)
     // = -(f + lam)/r1 exactly, so the KL terms of the oracle plan (whose
     // marginals are ta, tb) need no logarithm (entropies.py:123-131).
+    // mr: max of -r/r1, -s/r2 over the positive-weight atoms (shift bounds).
     double acc[9], mr[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
       const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
       acc[0] += ta[e] * (r[e] - f[e]);
       acc[1] += tb[e] * (s[e] - g[e]);
       acc[2] += ta[e] * r[e] + tb[e] * s[e];
-      if (ta[e] > 0.0) {
-        acc[3] += ta[e] * ((-f[e] - lam) * i1);
-        mr[0] = fmax(mr[0], -r[e] * i1);
-      }
-      if (tb[e] > 0.0) {
-        acc[4] += tb[e] * ((-g[e] + lam) * i2);
-        mr[1] = fmax(mr[1], -s[e] * i2);
-      }
+      if (ta[e] > 0.0) acc[3] += ta[e] * ((-f[e] - lam) * i1);
+      if (tb[e] > 0.0) acc[4] += tb[e] * ((-g[e] + lam) * i2);
+      if (i < n && sal[i] > 0.0) mr[0] = bops::dmax(mr[0], -r[e] * i1);
+      if (i < m && sbe[i] > 0.0) mr[1] = bops::dmax(mr[1], -s[e] * i2);
       acc[5] += ta[e] * va;
       acc[6] += ta[e] * va * va;
       acc[7] += tb[e] * vb;
       acc[8] += tb[e] * vb * vb;
     }
-    bred<9, 2>(acc, mr, red);
+    bops::block_red<FW_NW, 9, 2>(acc, mr, ping.next());
     const double fw_gap = acc[0] + acc[1];
     const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
     const double primal = acc[2] + r1 * kl1 + r2 * kl2;
@@ -678,17 +541,17 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
         gam = (d2 > 0.0) ? fmin(1.0, -k0 / d2) : 1.0;
         for (int it = 0; it < 24; ++it) {
           // one pass: centred moments of va / vb under p_gamma, q_gamma; the
-          // shift (1-gamma) max(u) + gamma max(-r/r1) bounds every exponent.
-          const double sha = (1.0 - gam) * pa.m + gam * mr[0];
-          const double shb = (1.0 - gam) * pb.m + gam * mr[1];
+          // shift (1-gamma) sh + gamma max(-r/r1) bounds every exponent.
+          const double pha = (1.0 - gam) * sha + gam * mr[0];
+          const double phb = (1.0 - gam) * shb + gam * mr[1];
           double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int e = 0; e < EPT; ++e) {
             const int i = c.src(e);
             const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
             const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
-            const double wa = wa0 > 0.0 ? wa0 * exp_nonpos(-f[e] * i1 - gam * va - sha) : 0.0;
-            const double wb = wb0 > 0.0 ? wb0 * exp_nonpos(-g[e] * i2 - gam * vb - shb) : 0.0;
+            const double wa = wa0 * bops::exp_fast(-f[e] * i1 - gam * va - pha, tab);
+            const double wb = wb0 * bops::exp_fast(-g[e] * i2 - gam * vb - phb, tab);
             const double xa = va - ca, xb = vb - cb;
             mom[0] += wa;
             mom[1] += wa * xa;
@@ -697,7 +560,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
             mom[4] += wb * xb;
             mom[5] += wb * xb * xb;
           }
-          bsum<6>(mom, red);
+          bops::block_sum<FW_NW, 6>(mom, ping.next());
           const double a1 = mom[1] / mom[0], a2 = mom[2] / mom[0];
           const double b1 = mom[4] / mom[3], b2 = mom[5] / mom[3];
           const double g1 = k0 - t1 * a1 - t2 * b1;
@@ -724,30 +587,33 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       }
     }
     if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
-    // --- update (fw.py:227-230)
+    // --- update (fw.py:227-230) and the next shift bounds
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       f[e] = (1.0 - gam) * f[e] + gam * r[e];
       g[e] = (1.0 - gam) * g[e] + gam * s[e];
     }
+    if (sha > -CUDART_INF) sha = (1.0 - gam) * sha + gam * mr[0];
+    if (shb > -CUDART_INF) shb = (1.0 - gam) * shb + gam * mr[1];
   }
-  // --- finalize: translate by lambda* (fw.py:235-252)
-  double mxa = -CUDART_INF, mxb = -CUDART_INF;
+  // --- finalize: translate by lambda* (fw.py:235-252), exact maxima
+  double mx[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
-    if (i < n && sal[i] > 0.0) mxa = fmax(mxa, -f[e] / r1);
-    if (i < m && sbe[i] > 0.0) mxb = fmax(mxb, -g[e] / r2);
+    if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+    if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
   }
-  LsePair pa{mxa, 0.0}, pb{mxb, 0.0};
+  bops::block_max<FW_NW, 2>(mx, ping.next());
+  double ls[2] = {0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
-    if (i < n && sal[i] > 0.0) pa.s += sal[i] * exp(-f[e] / r1 - mxa);
-    if (i < m && sbe[i] > 0.0) pb.s += sbe[i] * exp(-g[e] / r2 - mxb);
+    if (i < n) ls[0] += sal[i] * bops::exp_fast(-f[e] * i1 - mx[0], tab);
+    if (i < m) ls[1] += sbe[i] * bops::exp_fast(-g[e] * i2 - mx[1], tab);
   }
-  block_lse2(pa, pb, red);
-  const double lam = (r1 * r2 / (r1 + r2)) * ((pa.m + log(pa.s)) - (pb.m + log(pb.s)));
+  bops::block_sum<FW_NW, 2>(ls, ping.next());
+  const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(ls[0])) - (mx[1] + log(ls[1])));
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
@@ -794,7 +660,9 @@ int ept_for(int nm) {
   return -1;
 }
 
-size_t fw_smem(int n, int m) { return sizeof(double) * 3 * (size_t)(n + m); }
+size_t fw_smem(int n, int m) {
+  return sizeof(double) * 3 * (size_t)(n + m) + sizeof(unsigned short) * (size_t)(n + m);
+}
 
 int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
   const int ept = ept_for(std::max(a.n, a.m));
@@ -810,13 +678,19 @@ int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
     UOT_CHECK_LAUNCH();
     return UOT_OK;
   };
-  switch (ept) {
-    case 1: return go(fw1d_kernel<1>);
-    case 2: return go(fw1d_kernel<2>);
-    case 4: return go(fw1d_kernel<4>);
-    case 8: return go(fw1d_kernel<8>);
-    default: return go(fw1d_kernel<16>);
-  }
+  auto by_ept = [&](auto pk) -> int {
+    constexpr int PK = decltype(pk)::value;
+    switch (ept) {
+      case 1: return go(fw1d_kernel<1, PK>);
+      case 2: return go(fw1d_kernel<2, PK>);
+      case 4: return go(fw1d_kernel<4, PK>);
+      case 8: return go(fw1d_kernel<8, PK>);
+      default: return go(fw1d_kernel<16, PK>);
+    }
+  };
+  if (a.p == 2.0) return by_ept(std::integral_constant<int, 0>());
+  if (a.p == 1.0) return by_ept(std::integral_constant<int, 1>());
+  return by_ept(std::integral_constant<int, 2>());
 }
 
 size_t fw_scratch_bytes(int batch, int n, int m) {
