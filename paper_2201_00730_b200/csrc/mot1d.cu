@@ -34,6 +34,7 @@
 #include <algorithm>
 
 #include "../../include/uot_b200.h"
+#include "blockops.cuh"
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -43,7 +44,7 @@ namespace {
 
 constexpr int MT = 512;           // threads of the per-list CTAs
 constexpr int BT = 512;           // threads of the bucket CTAs
-constexpr int CAP = 8192;         // events per bucket (shared-memory capacity)
+constexpr int CAP = 4096;         // events per bucket (two shared-memory buffers)
 constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
 
 struct MotArgs {
@@ -86,26 +87,38 @@ __device__ __forceinline__ int list_len(const MotArgs& A, int q) {
   return A.lens != nullptr ? A.lens[q] : A.n;
 }
 
-__device__ __forceinline__ double exp_nonpos(double x) {
-  if (x < -708.0) return 0.0;
-  const double nn = rint(x * 1.4426950408889634074);
-  double r = fma(nn, -6.93147180369123816490e-01, x);
-  r = fma(nn, -1.90821492927058770002e-10, r);
-  double q = 1.6059043836821614599e-10;
-  q = fma(q, r, 2.0876756987868098979e-09);
-  q = fma(q, r, 2.5052108385441718775e-08);
-  q = fma(q, r, 2.7557319223985890653e-07);
-  q = fma(q, r, 2.7557319223985890653e-06);
-  q = fma(q, r, 2.4801587301587301587e-05);
-  q = fma(q, r, 1.9841269841269841270e-04);
-  q = fma(q, r, 1.3888888888888888889e-03);
-  q = fma(q, r, 8.3333333333333333333e-03);
-  q = fma(q, r, 4.1666666666666666667e-02);
-  q = fma(q, r, 1.6666666666666666667e-01);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  return q * __longlong_as_double((long long)((int)nn + 1023) << 52);
+constexpr int MNW = MT / 32;
+constexpr int MBUF = 16 * MNW;  // one-sync reduction buffer (doubles)
+
+// EPT consecutive doubles of a row starting at i0 (zero past nq); 16-byte
+// vector loads when the run is complete and aligned.
+template <int EPT>
+__device__ __forceinline__ void load_run(const double* row, int i0, int nq, double (&v)[EPT]) {
+  if (EPT % 2 == 0 && i0 + EPT <= nq && ((reinterpret_cast<uintptr_t>(row + i0) & 15) == 0)) {
+    const double2* p = reinterpret_cast<const double2*>(row + i0);
+#pragma unroll
+    for (int e = 0; e < EPT / 2; ++e) {
+      const double2 u = p[e];
+      v[2 * e] = u.x;
+      v[2 * e + 1] = u.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) v[e] = i0 + e < nq ? row[i0 + e] : 0.0;
+  }
+}
+
+template <int EPT>
+__device__ __forceinline__ void store_run(double* row, int i0, int nq, const double (&v)[EPT]) {
+  if (EPT % 2 == 0 && i0 + EPT <= nq && ((reinterpret_cast<uintptr_t>(row + i0) & 15) == 0)) {
+    double2* p = reinterpret_cast<double2*>(row + i0);
+#pragma unroll
+    for (int e = 0; e < EPT / 2; ++e) p[e] = make_double2(v[2 * e], v[2 * e + 1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (i0 + e < nq) row[i0 + e] = v[e];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -241,30 +254,6 @@ __device__ __forceinline__ int count_keys_below(const double* arr, int len, int 
   return lo;
 }
 
-// In-place bitonic sort of (key, code) pairs in shared memory; count is a
-// power of two; codes order ties ((list, index) packed).
-__device__ void bitonic_sort(double* key, int* code, int count) {
-  for (int size = 2; size <= count; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < count / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = ((lo & size) == 0);
-        const double ka = key[lo], kb = key[hi];
-        const int ca = code[lo], cb = code[hi];
-        const bool gt = (ka > kb) || (ka == kb && ca > cb);
-        if (gt == up) {
-          key[lo] = kb;
-          key[hi] = ka;
-          code[lo] = cb;
-          code[hi] = ca;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // mot_prep: one CTA per list, cluster of K CTAs per problem.
 
@@ -273,6 +262,8 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem[];
   __shared__ double scr[32 * 8];
+  __shared__ __align__(16) double red[2 * MBUF];
+  __shared__ double tab[32];
   __shared__ double slots[32];
   __shared__ int done_s;
   const int q = (int)cl.block_rank();
@@ -280,38 +271,39 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   int parity = 0;
+  bops::Ping<MBUF> ping{red, 0};
+  bops::load_exp_table(tab);
   if (threadIdx.x == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
   __syncthreads();
   if (done_s) return;  // uniform over the cluster
   double* sA = smem;                                  // [n] breakpoints
   double* samp = smem + n;                            // [SS] sample values
   int* sampt = reinterpret_cast<int*>(samp + A.SS);   // [SS] sample indices
-  double* sortk = reinterpret_cast<double*>(sampt + A.SS + (A.SS & 1));  // CTA 0: [KSS2]
+  int* srank = sampt + A.SS;                          // [SS] global sample ranks
+  double* splk = reinterpret_cast<double*>(srank + A.SS);  // CTA 0: [S+1] (16 SS bytes in)
+  int* splc = reinterpret_cast<int*>(splk + A.S + 1);                       // CTA 0: [S+1]
   const long base = ((long)b * K + q) * n;
   const double rq = A.omega[q] * A.rho;
 
+  const double irq = 1.0 / rq;
   double w[EPT], fv[EPT], ta[EPT];
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    w[e] = i < nq ? A.a[base + i] : 0.0;
-    fv[e] = i < nq ? A.f[base + i] : 0.0;
-  }
+  load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, w);
+  load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
   if (A.mode == 0) {
     // q_k = LSE_{a_k}(-f_k / rho_k)  (barycenter.py:307-313)
     double mx[1] = {-CUDART_INF};
 #pragma unroll
     for (int e = 0; e < EPT; ++e)
-      if (w[e] > 0.0) mx[0] = fmax(mx[0], -fv[e] / rq);
-    bmax_k<1>(mx, scr);
+      if (w[e] > 0.0) mx[0] = bops::dmax(mx[0], -fv[e] * irq);
+    bops::block_max<MNW, 1>(mx, ping.next());
     double sums[2] = {0.0, 0.0};
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      ta[e] = w[e] > 0.0 ? w[e] * exp_nonpos(-fv[e] / rq - mx[0]) : 0.0;
+      ta[e] = w[e] * bops::exp_fast(-fv[e] * irq - mx[0], tab);  // w >= 0, exp_fast finite
       sums[0] += ta[e];
       sums[1] += w[e];
     }
-    bsum_k<2>(sums, scr);
+    bops::block_sum<MNW, 2>(sums, ping.next());
     const double qk = mx[0] + log(sums[0]);
     // exchange (rho_k q_k, rho_k m_k, rho_k) over the cluster
     double ex[3] = {rq * qk, rq * sums[1], rq};
@@ -331,10 +323,9 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
   }
   // tilted weights -> global, breakpoints via block scan
   double loc = 0.0, pre[EPT];
+  store_run<EPT>(A.ta + base, threadIdx.x * EPT, nq, ta);
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    if (i < nq) A.ta[base + i] = ta[e];
     loc += ta[e];
     pre[e] = loc;
   }
@@ -411,46 +402,58 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
   cl.sync();
   const int S = A.S;
   if (S > 1) {
-    // CTA 0 gathers all samples, sorts them and publishes S-1 splitters in
-    // its own shared memory (as (value, code) pairs in sortk / sortc).
-    int KSS2 = 1;
-    while (KSS2 < K * SS) KSS2 <<= 1;
-    int* sortc = reinterpret_cast<int*>(sortk + KSS2);
-    if (q == 0) {
-      for (int idx = threadIdx.x; idx < KSS2; idx += MT) {
-        if (idx < K * SS) {
-          const int r = idx / SS, j = idx % SS;
-          const double* ov = cl.map_shared_rank(samp, r);
-          const int* ot = cl.map_shared_rank(sampt, r);
-          sortk[idx] = ov[j];
-          sortc[idx] = r * n + ot[j];
-        } else {
-          sortk[idx] = CUDART_INF;
-          sortc[idx] = 0x7fffffff;
+    // Global rank of each own sample among the K*SS samples (keys (value,
+    // list, index)): binary searches in the other CTAs' sorted sample arrays
+    // over DSMEM.  Exactly one sample holds each rank; the sample of rank
+    // floor(s K SS / S) is splitter s, published into CTA 0's table.
+    const int KSS = K * SS;
+    for (int j = threadIdx.x; j < SS; j += MT) srank[j] = j;
+    __syncthreads();
+    for (int pr = threadIdx.x; pr < SS * K; pr += MT) {
+      const int j = pr / K, r = pr % K;
+      if (r == q) continue;
+      const double* ov = cl.map_shared_rank(samp, r);
+      const int* ot = cl.map_shared_rank(sampt, r);
+      const double v = samp[j];
+      const int tt = sampt[j];
+      int lo = 0, hi = SS;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(ov[mid], r, ot[mid], v, q, tt))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      if (lo > 0) atomicAdd(&srank[j], lo);
+    }
+    __syncthreads();
+    double* k0 = cl.map_shared_rank(splk, 0);
+    int* c0 = cl.map_shared_rank(splc, 0);
+    for (int j = threadIdx.x; j < SS; j += MT) {
+      const int R = srank[j];
+      for (int sidx = (int)(((long)R * S + KSS - 1) / KSS); sidx < S; ++sidx) {
+        if ((int)(((long)sidx * KSS) / S) != R) break;
+        if (sidx >= 1) {
+          k0[sidx] = samp[j];
+          c0[sidx] = q * n + sampt[j];
         }
       }
-      __syncthreads();
-      bitonic_sort(sortk, sortc, KSS2);
-      // splitter s (1..S-1) is the sorted sample at rank s * (K*SS) / S
     }
     cl.sync();
     // every list locates each splitter in its own breakpoints
-    const double* k0 = cl.map_shared_rank(sortk, 0);
-    const int* c0 = cl.map_shared_rank(sortc, 0);
     int* sp = A.split + (long)b * (S + 1) * K;
-    for (int s = threadIdx.x; s <= S; s += MT) {
+    for (int sidx = threadIdx.x; sidx <= S; sidx += MT) {
       int pos;
-      if (s == 0) {
+      if (sidx == 0) {
         pos = 0;
-      } else if (s == S) {
+      } else if (sidx == S) {
         pos = max(ne, 0);
       } else {
-        const int rk = (int)(((long)s * K * SS) / S);
-        const double v = k0[rk];
-        const int code = c0[rk];
+        const double v = k0[sidx];
+        const int code = c0[sidx];
         pos = count_keys_below(sA, max(ne, 0), q, v, code / n, code % n);
       }
-      sp[(long)s * K + q] = pos;
+      sp[(long)sidx * K + q] = pos;
     }
   } else {
     int* sp = A.split + (long)b * 2 * K;
@@ -465,8 +468,70 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
 // ---------------------------------------------------------------------------
 // mot_bucket: events of one key range, sorted; cost increments.
 
-__device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, double* key, int* code,
-                                             int* lo_s, int* cnt_s) {
+// Stable merge of the bucket's K sorted runs (run q = the events of list q,
+// at [rb[q], rb[q+1])) in ceil(log2 K) pairwise rounds.  In a round every
+// element finds its output slot by one binary search in the partner run
+// group: groups are contiguous list ranges, so on equal values the left
+// (lower-list) group goes first, which is exactly the (value, list, index)
+// key order (barycenter.py:218).  Ping-pongs between the two buffers;
+// returns 0 or 1, the buffer holding the merged events.
+__device__ int merge_runs(double* key0, int* code0, double* key1, int* code1, const int* rb, int K,
+                          int total) {
+  int cur = 0;
+  for (int w = 1; w < K; w <<= 1) {
+    const double* ks = cur ? key1 : key0;
+    const int* cs = cur ? code1 : code0;
+    double* kd = cur ? key0 : key1;
+    int* cd = cur ? code0 : code1;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      int lo = 0, hi = K - 1;  // last run starting at or before e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rb[mid] <= e)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      const int g = lo / (2 * w);
+      const int l0 = rb[min(2 * g * w, K)];
+      const int m0 = rb[min((2 * g + 1) * w, K)];
+      const int r1 = rb[min((2 * g + 2) * w, K)];
+      const double v = ks[e];
+      int out;
+      if (e < m0) {  // left group: #right keys strictly below
+        int a = m0, b = r1;
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (ks[mid] < v)
+            a = mid + 1;
+          else
+            b = mid;
+        }
+        out = e + (a - m0);
+      } else {  // right group: #left keys at or below
+        int a = l0, b = m0;
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (ks[mid] <= v)
+            a = mid + 1;
+          else
+            b = mid;
+        }
+        out = (e - m0) + a;
+      }
+      kd[out] = v;
+      cd[out] = cs[e];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// Gathers the events of range s from all K lists into shared memory and
+// merges them; key/code point at the merged buffer on return.
+__device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, double* buf,
+                                             double*& key, int*& code, int* lo_s, int* cnt_s) {
   const int K = A.k, n = A.n;
   const int* sp = A.split + (long)b * (A.S + 1) * K;
   if (threadIdx.x == 0) {
@@ -482,22 +547,22 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
   __syncthreads();
   const int total = cnt_s[K];
   if (total > CAP) return -1;
-  int pw = 1;
-  while (pw < total) pw <<= 1;
+  double* key0 = buf;
+  double* key1 = buf + CAP;
+  int* code0 = reinterpret_cast<int*>(buf + 2 * CAP);
+  int* code1 = code0 + CAP;
   for (int q = 0; q < K; ++q) {
     const int lo = lo_s[q], c0 = cnt_s[q], len = cnt_s[q + 1] - c0;
     const double* Aq = A.A + ((long)b * K + q) * n;
     for (int j = threadIdx.x; j < len; j += blockDim.x) {
-      key[c0 + j] = Aq[lo + j];
-      code[c0 + j] = q * n + lo + j;
+      key0[c0 + j] = Aq[lo + j];
+      code0[c0 + j] = q * n + lo + j;
     }
   }
-  for (int j = total + threadIdx.x; j < pw; j += blockDim.x) {
-    key[j] = CUDART_INF;
-    code[j] = 0x7fffffff;
-  }
   __syncthreads();
-  bitonic_sort(key, code, pw);
+  const int which = merge_runs(key0, code0, key1, code1, cnt_s, K, total);
+  key = which ? key1 : key0;
+  code = which ? code1 : code0;
   return total;
 }
 
@@ -509,9 +574,9 @@ __global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
   const int s = blockIdx.x, b = blockIdx.y;
   if (A.done != nullptr && A.done[b]) return;
   const int K = A.k, n = A.n;
-  double* key = bsm;
-  int* code = reinterpret_cast<int*>(key + CAP);
-  const int total = bucket_gather(A, b, s, key, code, lo_s, cnt_s);
+  double* key;
+  int* code;
+  const int total = bucket_gather(A, b, s, bsm, key, code, lo_s, cnt_s);
   if (total < 0) {
     if (threadIdx.x == 0) A.status[b] = UOT_INVALID;  // bucket overflow
     return;
@@ -554,6 +619,8 @@ template <int EPT>
 __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double scr[32 * 8];
+  __shared__ __align__(16) double red[2 * MBUF];
+  __shared__ double tab[32];
   __shared__ double slots[32];
   __shared__ int done_s;
   __shared__ double cc0_s;
@@ -562,6 +629,8 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   int parity = 0;
+  bops::Ping<MBUF> ping{red, 0};
+  bops::load_exp_table(tab);
   if (threadIdx.x == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
   __syncthreads();
   if (done_s) return;
@@ -580,11 +649,11 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   __syncthreads();
   double rv[EPT];
   double loc = 0.0;
+  load_run<EPT>(A.dcc + base, threadIdx.x * EPT, nq, rv);
+  if (threadIdx.x == 0) rv[0] = 0.0;  // dcc[0] is not an event
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    const double d = (i >= 1 && i < nq) ? A.dcc[base + i] : 0.0;
-    loc += d;
+    loc += rv[e];
     rv[e] = loc;
   }
   double tot;
@@ -602,15 +671,15 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   }
   const double rq = A.omega[q] * A.rho;
   const double lamq = A.lam[(long)b * K + q];
+  const double irq = 1.0 / rq;
   double fv[EPT], tv[EPT], wv[EPT];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   double mxs[2] = {-CUDART_INF, -CUDART_INF};
+  load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+  load_run<EPT>(A.ta + base, threadIdx.x * EPT, nq, tv);
+  load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, wv);
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    fv[e] = i < nq ? A.f[base + i] : 0.0;
-    tv[e] = i < nq ? A.ta[base + i] : 0.0;
-    wv[e] = i < nq ? A.a[base + i] : 0.0;
     const double d = rv[e] - fv[e];
     acc[0] += tv[e] * d;                 // fw_gap part (barycenter.py:376-381)
     acc[1] += tv[e] * rv[e];             // plan cost via complementary slackness
@@ -620,12 +689,11 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     acc[5] += tv[e] * d;                 // first moment of d under p_0
     acc[6] += tv[e] * d * d;             // second moment
     if (wv[e] > 0.0) {
-      mxs[0] = fmax(mxs[0], -fv[e] / rq);
-      mxs[1] = fmax(mxs[1], -rv[e] / rq);
+      mxs[0] = bops::dmax(mxs[0], -fv[e] * irq);
+      mxs[1] = bops::dmax(mxs[1], -rv[e] * irq);
     }
   }
-  bsum_k<7>(acc, scr);
-  bmax_k<2>(mxs, scr);
+  bops::block_red<MNW, 7, 2>(acc, mxs, ping.next());
   // cluster sums: fw_gap, plan cost + rho KL terms, sum of centres
   const double cq = acc[5] / acc[3];
   double cs[3] = {acc[0], acc[1] + rq * (acc[2] - acc[3] + acc[4]), cq};
@@ -670,16 +738,14 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
         double mom[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
-          if (wv[e] > 0.0) {
-            const double d = rv[e] - fv[e];
-            const double ww = wv[e] * exp_nonpos(-(fv[e] + gam * d) / rq - sh);
-            const double xc = d - cq;
-            mom[0] += ww;
-            mom[1] += ww * xc;
-            mom[2] += ww * xc * xc;
-          }
+          const double d = rv[e] - fv[e];
+          const double ww = wv[e] * bops::exp_fast(-(fv[e] + gam * d) * irq - sh, tab);
+          const double xc = d - cq;
+          mom[0] += ww;
+          mom[1] += ww * xc;
+          mom[2] += ww * xc * xc;
         }
-        bsum_k<3>(mom, scr);
+        bops::block_sum<MNW, 3>(mom, ping.next());
         const double e1 = mom[1] / mom[0];
         double gv[2] = {e1, (mom[2] / mom[0] - e1 * e1) / rq};
         cluster_sum<2>(gv, slots, parity);
@@ -703,10 +769,8 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     }
   }
 #pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    if (i < nq) A.f[base + i] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
-  }
+  for (int e = 0; e < EPT; ++e) fv[e] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
+  store_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
   cl.sync();  // slots stay valid until every CTA read them
 }
 
@@ -715,12 +779,14 @@ template <int EPT>
 __global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double scr[32 * 8];
+  __shared__ double tab[32];
   __shared__ double slots[32];
   const int q = (int)cl.block_rank();
   const int b = blockIdx.y;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   int parity = 0;
+  bops::load_exp_table(tab);
   const long base = ((long)b * K + q) * n;
   const double rq = A.omega[q] * A.rho;
   double w[EPT], fv[EPT];
@@ -736,7 +802,7 @@ __global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
   double sm[1] = {0.0};
 #pragma unroll
   for (int e = 0; e < EPT; ++e)
-    if (w[e] > 0.0) sm[0] += w[e] * exp_nonpos(-fv[e] / rq - mx[0]);
+    sm[0] += w[e] * bops::exp_fast(-fv[e] / rq - mx[0], tab);
   bsum_k<1>(sm, scr);
   const double qk = mx[0] + log(sm[0]);
   double ex[2] = {rq * qk, rq};
@@ -775,9 +841,9 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
   __shared__ int kept_s;
   const int s = blockIdx.x, b = blockIdx.y;
   const int K = A.k, n = A.n;
-  double* key = bsm;
-  int* code = reinterpret_cast<int*>(key + CAP);
-  const int total = bucket_gather(A, b, s, key, code, lo_s, cnt_s);
+  double* key;
+  int* code;
+  const int total = bucket_gather(A, b, s, bsm, key, code, lo_s, cnt_s);
   if (total < 0) return;
   const double tot_mass = A.scal[b * 4 + 1];
   const double nxt = (s + 1 < A.S) ? next_event_value(A, b, s + 1) : CUDART_INF;
@@ -882,11 +948,9 @@ MotPlan plan_for(int k, int n) {
   p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
   while ((long)k * p.SS > 8192) p.SS = std::max(1, p.SS / 2);
   p.ept = ept_for(n);
-  int kss2 = 1;
-  while (kss2 < k * p.SS) kss2 <<= 1;
-  p.prep_smem = sizeof(double) * (size_t)n + (sizeof(double) + sizeof(int)) * (size_t)p.SS + 16 +
-                (sizeof(double) + sizeof(int)) * (size_t)kss2 + 16;
-  p.bucket_smem = (sizeof(double) + sizeof(int)) * (size_t)CAP;
+  p.prep_smem = sizeof(double) * (size_t)n + (sizeof(double) + 2 * sizeof(int)) * (size_t)p.SS +
+                16 + (sizeof(double) + sizeof(int)) * (size_t)(p.S + 1) + 16;
+  p.bucket_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)CAP;
   return p;
 }
 
