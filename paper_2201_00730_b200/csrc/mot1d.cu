@@ -210,9 +210,10 @@ __device__ __forceinline__ int bscan_maxi(int v, int* scr) {
 }
 
 // Cluster all-reduce (sum) of NV doubles: each CTA publishes its vector in
-// its own shared slot, then every CTA sums all slots in rank order (identical
-// results everywhere).  `slot` alternates between two buffers so one cluster
-// barrier per reduction suffices.
+// its own shared slot; after the cluster barrier every warp reads the K
+// slots in parallel (lane r <- CTA r) and butterfly-reduces them, so every
+// thread of every CTA holds bit-identical sums.  `slot` alternates between
+// two buffers so one cluster barrier per reduction suffices.
 template <int NV>
 __device__ __forceinline__ void cluster_sum(double (&v)[NV], double* slots, int& parity) {
   cg::cluster_group cl = cg::this_cluster();
@@ -223,15 +224,19 @@ __device__ __forceinline__ void cluster_sum(double (&v)[NV], double* slots, int&
   }
   cl.sync();
   const int nr = (int)cl.num_blocks();
+  const int lane = threadIdx.x & 31;
+  const double* other = cl.map_shared_rank(mine, lane < nr ? lane : 0);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = 0.0;
-  for (int r = 0; r < nr; ++r) {
-    const double* other = cl.map_shared_rank(mine, r);
+  for (int k = 0; k < NV; ++k) v[k] = lane < nr ? other[k] : 0.0;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] += other[k];
-  }
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
   parity ^= 1;
 }
+
+// Event codes: (list << 24) | index, ordered like (list, index).
+__device__ __forceinline__ int ev_code(int q, int t) { return (q << 24) | t; }
+__device__ __forceinline__ int ev_list(int c) { return c >> 24; }
+__device__ __forceinline__ int ev_index(int c) { return c & 0xFFFFFF; }
 
 // Composite event key order: (value, list, index) lexicographic.
 __device__ __forceinline__ bool key_less(double va, int qa, int ta_, double vb, int qb, int tb) {
@@ -282,6 +287,8 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
   int* srank = sampt + A.SS;                          // [SS] global sample ranks
   double* splk = reinterpret_cast<double*>(srank + A.SS);  // CTA 0: [S+1] (16 SS bytes in)
   int* splc = reinterpret_cast<int*>(splk + A.S + 1);                       // CTA 0: [S+1]
+  double* allv = splk + 2 * (A.S + 1);                     // [K SS] all samples (S > 1)
+  int* allt = reinterpret_cast<int*>(allv + (long)A.k * A.SS);
   const long base = ((long)b * K + q) * n;
   const double rq = A.omega[q] * A.rho;
 
@@ -377,12 +384,10 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
       mine[1] = mm[1];
     }
     c2.sync();
-    double mxm = -CUDART_INF, mnm = CUDART_INF;
-    for (int r = 0; r < K; ++r) {
-      const double* o = c2.map_shared_rank(mine, r);
-      mxm = fmax(mxm, o[0]);
-      mnm = fmin(mnm, o[0]);
-    }
+    const int lane = threadIdx.x & 31;
+    const double om = c2.map_shared_rank(mine, lane < K ? lane : 0)[0];
+    const double mxm = warp_max(lane < K ? om : -CUDART_INF);
+    const double mnm = warp_min(lane < K ? om : CUDART_INF);
     parity ^= 1;
     if (q == 0 && threadIdx.x == 0) {
       const bool bad = (mxm - mnm) > 1e-9 * mxm;
@@ -408,12 +413,17 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
     // floor(s K SS / S) is splitter s, published into CTA 0's table.
     const int KSS = K * SS;
     for (int j = threadIdx.x; j < SS; j += MT) srank[j] = j;
+    for (int idx = threadIdx.x; idx < KSS; idx += MT) {  // every list's samples, local copy
+      const int r = idx / SS, j = idx - r * SS;
+      allv[idx] = cl.map_shared_rank(samp, r)[j];
+      allt[idx] = cl.map_shared_rank(sampt, r)[j];
+    }
     __syncthreads();
     for (int pr = threadIdx.x; pr < SS * K; pr += MT) {
-      const int j = pr / K, r = pr % K;
+      const int j = pr / K, r = pr - j * K;
       if (r == q) continue;
-      const double* ov = cl.map_shared_rank(samp, r);
-      const int* ot = cl.map_shared_rank(sampt, r);
+      const double* ov = allv + r * SS;
+      const int* ot = allt + r * SS;
       const double v = samp[j];
       const int tt = sampt[j];
       int lo = 0, hi = SS;
@@ -435,7 +445,7 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
         if ((int)(((long)sidx * KSS) / S) != R) break;
         if (sidx >= 1) {
           k0[sidx] = samp[j];
-          c0[sidx] = q * n + sampt[j];
+          c0[sidx] = ev_code(q, sampt[j]);
         }
       }
     }
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
       } else {
         const double v = k0[sidx];
         const int code = c0[sidx];
-        pos = count_keys_below(sA, max(ne, 0), q, v, code / n, code % n);
+        pos = count_keys_below(sA, max(ne, 0), q, v, ev_list(code), ev_index(code));
       }
       sp[(long)sidx * K + q] = pos;
     }
@@ -469,58 +479,57 @@ __global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
 // mot_bucket: events of one key range, sorted; cost increments.
 
 // Stable merge of the bucket's K sorted runs (run q = the events of list q,
-// at [rb[q], rb[q+1])) in ceil(log2 K) pairwise rounds.  In a round every
-// element finds its output slot by one binary search in the partner run
-// group: groups are contiguous list ranges, so on equal values the left
-// (lower-list) group goes first, which is exactly the (value, list, index)
-// key order (barycenter.py:218).  Ping-pongs between the two buffers;
-// returns 0 or 1, the buffer holding the merged events.
+// at [rb[q], rb[q+1])) in ceil(log2 K) pairwise rounds.  Groups of runs are
+// contiguous list ranges, so on equal values the left (lower-list) group goes
+// first -- exactly the (value, list, index) key order (barycenter.py:218).
+// Each round is a merge path: thread t emits output positions
+// [t P, (t+1) P) after one diagonal binary search per group it touches.
+// Ping-pongs between the two buffers; returns the buffer holding the result.
 __device__ int merge_runs(double* key0, int* code0, double* key1, int* code1, const int* rb, int K,
                           int total) {
   int cur = 0;
+  const int P = (total + blockDim.x - 1) / blockDim.x;
   for (int w = 1; w < K; w <<= 1) {
     const double* ks = cur ? key1 : key0;
     const int* cs = cur ? code1 : code0;
     double* kd = cur ? key0 : key1;
     int* cd = cur ? code0 : code1;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      int lo = 0, hi = K - 1;  // last run starting at or before e
+    int o = threadIdx.x * P;
+    const int oend = min(total, o + P);
+    int g = 0;
+    while (o < oend) {
+      int r1 = rb[min(2 * w, K)];
+      while (o >= r1) {
+        ++g;
+        r1 = rb[min((2 * g + 2) * w, K)];
+      }
+      const int l0 = rb[min(2 * g * w, K)], m0 = rb[min((2 * g + 1) * w, K)];
+      const int nL = m0 - l0, nR = r1 - m0;
+      const int d = o - l0;
+      int lo = max(0, d - nR), hi = min(d, nL);
       while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (rb[mid] <= e)
-          lo = mid;
+        const int mid = (lo + hi) >> 1;
+        if (ks[l0 + mid] <= ks[m0 + d - 1 - mid])
+          lo = mid + 1;
         else
-          hi = mid - 1;
+          hi = mid;
       }
-      const int g = lo / (2 * w);
-      const int l0 = rb[min(2 * g * w, K)];
-      const int m0 = rb[min((2 * g + 1) * w, K)];
-      const int r1 = rb[min((2 * g + 2) * w, K)];
-      const double v = ks[e];
-      int out;
-      if (e < m0) {  // left group: #right keys strictly below
-        int a = m0, b = r1;
-        while (a < b) {
-          const int mid = (a + b) >> 1;
-          if (ks[mid] < v)
-            a = mid + 1;
-          else
-            b = mid;
+      int i = lo, j = d - lo;
+      double lv = i < nL ? ks[l0 + i] : CUDART_INF;
+      double rv = j < nR ? ks[m0 + j] : CUDART_INF;
+      const int stop = min(oend, r1);
+      for (; o < stop; ++o) {
+        const bool takeL = lv <= rv;
+        kd[o] = takeL ? lv : rv;
+        cd[o] = cs[takeL ? l0 + i : m0 + j];
+        if (takeL) {
+          ++i;
+          lv = i < nL ? ks[l0 + i] : CUDART_INF;
+        } else {
+          ++j;
+          rv = j < nR ? ks[m0 + j] : CUDART_INF;
         }
-        out = e + (a - m0);
-      } else {  // right group: #left keys at or below
-        int a = l0, b = m0;
-        while (a < b) {
-          const int mid = (a + b) >> 1;
-          if (ks[mid] <= v)
-            a = mid + 1;
-          else
-            b = mid;
-        }
-        out = (e - m0) + a;
       }
-      kd[out] = v;
-      cd[out] = cs[e];
     }
     __syncthreads();
     cur ^= 1;
@@ -551,13 +560,18 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
   double* key1 = buf + CAP;
   int* code0 = reinterpret_cast<int*>(buf + 2 * CAP);
   int* code1 = code0 + CAP;
-  for (int q = 0; q < K; ++q) {
-    const int lo = lo_s[q], c0 = cnt_s[q], len = cnt_s[q + 1] - c0;
-    const double* Aq = A.A + ((long)b * K + q) * n;
-    for (int j = threadIdx.x; j < len; j += blockDim.x) {
-      key0[c0 + j] = Aq[lo + j];
-      code0[c0 + j] = q * n + lo + j;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    int q = 0, hi = K - 1;  // last run starting at or before e
+    while (q < hi) {
+      const int mid = (q + hi + 1) >> 1;
+      if (cnt_s[mid] <= e)
+        q = mid;
+      else
+        hi = mid - 1;
     }
+    const int t = lo_s[q] + (e - cnt_s[q]);
+    key0[e] = A.A[((long)b * K + q) * n + t];
+    code0[e] = ev_code(q, t);
   }
   __syncthreads();
   const int which = merge_runs(key0, code0, key1, code1, cnt_s, K, total);
@@ -594,14 +608,14 @@ __global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
   const int e0 = threadIdx.x * per, e1 = min(total, e0 + per);
   double loc = 0.0;
   for (int e = e0; e < e1; ++e) {
-    const int q = code[e] / n, t = code[e] % n;
+    const int q = ev_list(code[e]), t = ev_index(code[e]);
     const double* xq = A.x + ((long)b * K + q) * n;
     loc += A.omega[q] * (xq[t + 1] - xq[t]);
   }
   double tot;
   double run = bscan1(loc, tot, scr);
   for (int e = e0; e < e1; ++e) {
-    const int q = code[e] / n, t = code[e] % n;
+    const int q = ev_list(code[e]), t = ev_index(code[e]);
     const double* xq = A.x + ((long)b * K + q) * n;
     const double xo = xq[t], xn = xq[t + 1];
     const double inc = A.omega[q] * (xn - xo);
@@ -898,8 +912,8 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
           const int c_lo = cnt_s[q], c_len = cnt_s[q + 1] - c_lo;
           if (e >= 0 && c_len > 0) {
             const double* Aq = A.A + ((long)b * K + q) * n + lo_s[q];
-            const int eq = code[e] / n;
-            const int et = code[e] % n;
+            const int eq = ev_list(code[e]);
+            const int et = ev_index(code[e]);
             int lo2 = 0, hi2 = c_len;
             while (lo2 < hi2) {  // #{j : (Aq[j], q, lo+j) <= (key[e], eq, et)}
               const int mid = (lo2 + hi2) >> 1;
@@ -946,10 +960,11 @@ MotPlan plan_for(int k, int n) {
   const long events = (long)k * (n - 1);
   p.S = (int)std::max(1L, (events + 2047) / 2048);
   p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
-  while ((long)k * p.SS > 8192) p.SS = std::max(1, p.SS / 2);
+  while ((long)k * p.SS > 4096) p.SS = std::max(1, p.SS / 2);
   p.ept = ept_for(n);
   p.prep_smem = sizeof(double) * (size_t)n + (sizeof(double) + 2 * sizeof(int)) * (size_t)p.SS +
-                16 + (sizeof(double) + sizeof(int)) * (size_t)(p.S + 1) + 16;
+                16 + 2 * sizeof(double) * (size_t)(p.S + 1) +
+                (sizeof(double) + sizeof(int)) * (size_t)k * p.SS + 16;
   p.bucket_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)CAP;
   return p;
 }
