@@ -46,8 +46,8 @@ __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : 
 // polynomial (truncation 3.5e-18), 2^(k mod 32 / 32) from the table, 2^(k/32)
 // by exponent construction.  Error ~1 ulp.  x < -708 returns 0 (such terms
 // are negligible next to the unit-scaled maximum), as exp_nonpos did.
-__device__ __forceinline__ double exp_fast(double x, const double* tab) {
-  const double xc = dmin(dmax(x, -708.0), 708.0);
+__device__ __forceinline__ double exp_core(double x, const double* tab) {
+  const double xc = dmax(x, -708.0);
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
   const double t = fma(xc, 46.16624130844683, magic);
   const int k = __double2loint(t);
@@ -62,8 +62,20 @@ __device__ __forceinline__ double exp_fast(double x, const double* tab) {
   const double q = fma(r2, q25, q01);  // (e^r - 1) / r
   const double tj = tab[k & 31];
   const double y = fma(tj, r * q, tj);
-  const double scale = __hiloint2double(((k >> 5) + 1023) << 20, 0);
-  return x < -708.0 ? 0.0 : y * scale;
+  return y * __hiloint2double(((k >> 5) + 1023) << 20, 0);
+}
+
+// exp(x), clamped to [-708, 708] (finite for any input); 0 below -708.
+__device__ __forceinline__ double exp_fast(double x, const double* tab) {
+  return x < -708.0 ? 0.0 : exp_core(dmin(x, 708.0), tab);
+}
+
+// w * exp(x) for a weight w >= 0 whose exponent is shifted by an upper
+// bound (x <= 0 up to rounding when w > 0); 0 for w == 0 whatever x is
+// (zero-weight atoms carry unbounded potentials) and for x < -708.
+__device__ __forceinline__ double wexp(double w, double x, const double* tab) {
+  const double e = exp_core(x, tab);
+  return (w > 0.0 && x >= -708.0) ? w * e : 0.0;
 }
 
 

@@ -435,9 +435,8 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
-        // weights are >= 0 and exp_fast is finite, so zero weights give 0
-        ta[e] = wa * bops::exp_fast(-f[e] * i1 - sha, tab);
-        tb[e] = wb * bops::exp_fast(-g[e] * i2 - shb, tab);
+        ta[e] = bops::wexp(wa, -f[e] * i1 - sha, tab);
+        tb[e] = bops::wexp(wb, -g[e] * i2 - shb, tab);
         sums[0] += ta[e];
         sums[1] += tb[e];
       }
@@ -550,8 +549,8 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
             const int i = c.src(e);
             const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
             const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
-            const double wa = wa0 * bops::exp_fast(-f[e] * i1 - gam * va - pha, tab);
-            const double wb = wb0 * bops::exp_fast(-g[e] * i2 - gam * vb - phb, tab);
+            const double wa = bops::wexp(wa0, -f[e] * i1 - gam * va - pha, tab);
+            const double wb = bops::wexp(wb0, -g[e] * i2 - gam * vb - phb, tab);
             const double xa = va - ca, xb = vb - cb;
             mom[0] += wa;
             mom[1] += wa * xa;
@@ -609,8 +608,8 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
-    if (i < n) ls[0] += sal[i] * bops::exp_fast(-f[e] * i1 - mx[0], tab);
-    if (i < m) ls[1] += sbe[i] * bops::exp_fast(-g[e] * i2 - mx[1], tab);
+    if (i < n) ls[0] += bops::wexp(sal[i], -f[e] * i1 - mx[0], tab);
+    if (i < m) ls[1] += bops::wexp(sbe[i], -g[e] * i2 - mx[1], tab);
   }
   bops::block_sum<FW_NW, 2>(ls, ping.next());
   const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(ls[0])) - (mx[1] + log(ls[1])));

@@ -46,6 +46,8 @@ constexpr int MT = 512;           // threads of the per-list CTAs
 constexpr int BT = 512;           // threads of the bucket CTAs
 constexpr int CAP = 4096;         // events per bucket (two shared-memory buffers)
 constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
+constexpr int ST = 1024;          // threads of the per-problem splitter CTA
+constexpr int SMAX = 128;         // buckets per problem
 
 struct MotArgs {
   int batch, k, n;        // n = row stride (max list length)
@@ -81,6 +83,11 @@ struct MotArgs {
   int* pcount;            // [B]
   int* bcount;            // [B][S]
   int cap_e;
+  double* lse;            // [B][K][2] (max, q_k) of the current iterate
+  double* mass;           // [B][K] input masses
+  double* tmass;          // [B][K] tilted masses
+  double* samp;           // [B][K][SS] regular samples (values)
+  int* sampt;             // [B][K][SS] (indices)
 };
 
 __device__ __forceinline__ int list_len(const MotArgs& A, int q) {
@@ -260,219 +267,327 @@ __device__ __forceinline__ int count_keys_below(const double* arr, int len, int 
 }
 
 // ---------------------------------------------------------------------------
-// mot_prep: one CTA per list, cluster of K CTAs per problem.
+// mot_lse: per-list log-sum-exp of the potentials, q_k = LSE_{a_k}(-f_k/rho_k)
+// (barycenter.py:307-313), stored as (max, q) with the input mass m_k.  Runs
+// once before the loop; mot_update refreshes it for every new iterate.
 
 template <int EPT>
-__global__ void __launch_bounds__(MT) mot_prep(MotArgs A) {
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(16) double smem[];
-  __shared__ double scr[32 * 8];
+__device__ __forceinline__ void list_lse(const double (&w)[EPT], const double (&fv)[EPT], double irq,
+                                         const double* tab, double* red0, double* red1, double& mx,
+                                         double& qk, double (&ew)[EPT]) {
+  double m1[1] = {-CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e)
+    if (w[e] > 0.0) m1[0] = bops::dmax(m1[0], -fv[e] * irq);
+  bops::block_max<MNW, 1>(m1, red0);
+  double s1[1] = {0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    ew[e] = bops::wexp(w[e], -fv[e] * irq - m1[0], tab);
+    s1[0] += ew[e];
+  }
+  bops::block_sum<MNW, 1>(s1, red1);
+  mx = m1[0];
+  qk = m1[0] + log(s1[0]);
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_lse(MotArgs A) {
   __shared__ __align__(16) double red[2 * MBUF];
   __shared__ double tab[32];
-  __shared__ double slots[32];
-  __shared__ int done_s;
-  const int q = (int)cl.block_rank();
-  const int b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
-  int parity = 0;
-  bops::Ping<MBUF> ping{red, 0};
   bops::load_exp_table(tab);
-  if (threadIdx.x == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
   __syncthreads();
-  if (done_s) return;  // uniform over the cluster
-  double* sA = smem;                                  // [n] breakpoints
-  double* samp = smem + n;                            // [SS] sample values
-  int* sampt = reinterpret_cast<int*>(samp + A.SS);   // [SS] sample indices
-  int* srank = sampt + A.SS;                          // [SS] global sample ranks
-  double* splk = reinterpret_cast<double*>(srank + A.SS);  // CTA 0: [S+1] (16 SS bytes in)
-  int* splc = reinterpret_cast<int*>(splk + A.S + 1);                       // CTA 0: [S+1]
-  double* allv = splk + 2 * (A.S + 1);                     // [K SS] all samples (S > 1)
-  int* allt = reinterpret_cast<int*>(allv + (long)A.k * A.SS);
   const long base = ((long)b * K + q) * n;
-  const double rq = A.omega[q] * A.rho;
-
-  const double irq = 1.0 / rq;
-  double w[EPT], fv[EPT], ta[EPT];
+  const double irq = 1.0 / (A.omega[q] * A.rho);
+  double w[EPT], fv[EPT];
   load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, w);
   load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
-  if (A.mode == 0) {
-    // q_k = LSE_{a_k}(-f_k / rho_k)  (barycenter.py:307-313)
-    double mx[1] = {-CUDART_INF};
+  double ms[1] = {0.0};
 #pragma unroll
-    for (int e = 0; e < EPT; ++e)
-      if (w[e] > 0.0) mx[0] = bops::dmax(mx[0], -fv[e] * irq);
-    bops::block_max<MNW, 1>(mx, ping.next());
-    double sums[2] = {0.0, 0.0};
+  for (int e = 0; e < EPT; ++e) ms[0] += w[e];
+  double mx, qk;
+  list_lse<EPT>(w, fv, irq, tab, red, red + MBUF, mx, qk, fv);
+  bops::block_sum<MNW, 1>(ms, red);
+  if (threadIdx.x == 0) {
+    A.lse[((long)b * K + q) * 2 + 0] = mx;
+    A.lse[((long)b * K + q) * 2 + 1] = qk;
+    A.mass[(long)b * K + q] = ms[0];
+  }
+}
+
+// Optimal zero-sum translation from the K per-list log-sum-exps
+// (barycenter.py:316-317): lambda_q = rho_q q_q - (rho_q / rho_tot) sum_r rho_r q_r.
+// Every warp computes the three problem sums with the same butterfly, so all
+// lists of a problem see bit-identical values.  Returns lambda_q; ex0 / ex1
+// / rtot = sum rho q, sum rho m, sum rho.
+__device__ __forceinline__ double problem_lambda(const MotArgs& A, int b, int q, double& ex0,
+                                                 double& ex1, double& rtot) {
+  const int K = A.k, lane = threadIdx.x & 31;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (lane < K) {
+    const double rr = A.omega[lane] * A.rho;
+    a0 = rr * A.lse[((long)b * K + lane) * 2 + 1];
+    a1 = rr * A.mass[(long)b * K + lane];
+    a2 = rr;
+  }
+  ex0 = warp_sum(a0);
+  ex1 = warp_sum(a1);
+  rtot = warp_sum(a2);
+  const double rq = A.omega[q] * A.rho;
+  return rq * A.lse[((long)b * K + q) * 2 + 1] - (rq / rtot) * ex0;
+}
+
+// Exclusive block scan "last positive atom": (index, breakpoint) of the last
+// atom with positive tilted weight owned by a lower thread (index -1: none).
+__device__ __forceinline__ void excl_last_pos(int& idx, double& val, int* iscr, double* vscr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int si = idx;
+  double sv = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ti = __shfl_up_sync(0xffffffffu, si, o);
+    const double tv = __shfl_up_sync(0xffffffffu, sv, o);
+    if (lane >= o && ti > si) {
+      si = ti;
+      sv = tv;
+    }
+  }
+  int ei = __shfl_up_sync(0xffffffffu, si, 1);
+  double ev = __shfl_up_sync(0xffffffffu, sv, 1);
+  if (lane == 0) {
+    ei = -1;
+    ev = 0.0;
+  }
+  __syncthreads();
+  if (lane == 31) {
+    iscr[warp] = si;
+    vscr[warp] = sv;
+  }
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) {
+    if (iscr[w] > ei) {
+      ei = iscr[w];
+      ev = vscr[w];
+    }
+  }
+  __syncthreads();
+  idx = ei;
+  val = ev;
+}
+
+// Tilted weights ta of list q -> global; breakpoints A_q = cumsum(ta) by a
+// one-sync block scan, zero-weight atoms repeating their predecessor's
+// breakpoint bit for bit (barycenter.py:209-222); the tilted mass; and the
+// list's SS regular samples (keys (A_q[t], q, t)), taken from registers by
+// the owning threads.
+template <int EPT>
+__device__ void tilt_tail(const MotArgs& A, int b, int q, int nq, const double (&ta)[EPT],
+                          double* buf, int* iscr, double* vscr) {
+  const int K = A.k, n = A.n;
+  const long base = ((long)b * K + q) * n;
+  const int i0 = threadIdx.x * EPT;
+  store_run<EPT>(A.ta + base, i0, nq, ta);
+  double av[EPT];
+  double loc = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    loc += ta[e];
+    av[e] = loc;
+  }
+  double v[1] = {loc}, tot[1];
+  bops::block_scan_excl<MNW, 1>(v, tot, buf);
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) av[e] = v[0] + av[e];
+  int any0 = 0, lz = -1;
+  double lzv = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = i0 + e;
+    if (i < nq && ta[e] == 0.0) any0 = 1;
+    if (i < nq && ta[e] > 0.0) {
+      lz = i;
+      lzv = av[e];
+    }
+  }
+  if (__syncthreads_or(any0)) {
+    int pi = lz;
+    double pv = lzv;
+    excl_last_pos(pi, pv, iscr, vscr);
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      ta[e] = w[e] * bops::exp_fast(-fv[e] * irq - mx[0], tab);  // w >= 0, exp_fast finite
-      sums[0] += ta[e];
-      sums[1] += w[e];
+      const int i = i0 + e;
+      if (i < nq && ta[e] == 0.0) av[e] = pi >= 0 ? pv : 0.0;
+      if (i < nq && ta[e] > 0.0) {
+        pi = i;
+        pv = av[e];
+      }
     }
-    bops::block_sum<MNW, 2>(sums, ping.next());
-    const double qk = mx[0] + log(sums[0]);
-    // exchange (rho_k q_k, rho_k m_k, rho_k) over the cluster
-    double ex[3] = {rq * qk, rq * sums[1], rq};
-    cluster_sum<3>(ex, slots, parity);
-    const double rho_tot = ex[2];
-    const double lamq = rq * qk - (rq / rho_tot) * ex[0];  // barycenter.py:316-317
+  }
+  store_run<EPT>(A.A + base, i0, nq, av);
+  if (threadIdx.x == 0) A.tmass[(long)b * K + q] = tot[0];
+  const int ne = nq - 1, SS = A.SS;
+  double* sv = A.samp + ((long)b * K + q) * SS;
+  int* st = A.sampt + ((long)b * K + q) * SS;
+  if (ne <= 0) {
+    for (int j = threadIdx.x; j < SS; j += MT) {
+      sv[j] = CUDART_INF;
+      st[j] = 0;
+    }
+    return;
+  }
+  // samples t_j = floor((j+1) ne / (SS+1)) falling in [i0, i0 + EPT)
+  for (int j = max(0, (int)(((long)i0 * (SS + 1)) / ne) - 1); j < SS; ++j) {
+    const int t = (int)(((long)(j + 1) * ne) / (SS + 1));
+    if (t >= i0 + EPT) break;
+    if (t >= i0) {
+      double val = 0.0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        if (i0 + e == t) val = av[e];
+      sv[j] = val;
+      st[j] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mot_tilt: one CTA per list (no cluster).  Tilted weights, breakpoints by
+// block scan, the list's tilted mass and its regular samples.
+
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_tilt(MotArgs A) {
+  __shared__ __align__(16) double red[MBUF];
+  __shared__ double tab[32];
+  __shared__ int iscr[MNW];
+  __shared__ double vscr[MNW];
+  const int q = blockIdx.x, b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  if (A.done != nullptr && A.done[b]) return;
+  bops::load_exp_table(tab);
+  const long base = ((long)b * K + q) * n;
+  double w[EPT], ta[EPT];
+  load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, w);
+  __syncthreads();
+  if (A.mode == 0) {
+    const double rq = A.omega[q] * A.rho, irq = 1.0 / rq;
+    double fv[EPT];
+    load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+    double ex0, ex1, rtot;
+    const double lamq = problem_lambda(A, b, q, ex0, ex1, rtot);
+    const double mx = A.lse[((long)b * K + q) * 2 + 0];
     if (threadIdx.x == 0) {
       A.lam[(long)b * K + q] = lamq;
-      if (q == 0) A.scal[b * 4 + 0] = ex[1] - rho_tot * exp(ex[0] / rho_tot);  // :320-327
+      if (q == 0) A.scal[b * 4 + 0] = ex1 - rtot * exp(ex0 / rtot);  // H_0, :320-327
     }
-    const double sc = exp(mx[0] - lamq / rq);
+    const double sc = exp(mx - lamq * irq);
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) ta[e] *= sc;
+    for (int e = 0; e < EPT; ++e) ta[e] = bops::wexp(w[e], -fv[e] * irq - mx, tab) * sc;
   } else {
 #pragma unroll
     for (int e = 0; e < EPT; ++e) ta[e] = w[e];
   }
-  // tilted weights -> global, breakpoints via block scan
-  double loc = 0.0, pre[EPT];
-  store_run<EPT>(A.ta + base, threadIdx.x * EPT, nq, ta);
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    loc += ta[e];
-    pre[e] = loc;
-  }
-  double total;
-  const double off = bscan1(loc, total, scr);
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    if (i < nq) sA[i] = off + pre[e];
-  }
-  // zero-weight atoms repeat their predecessor's breakpoint bit for bit
-  {
-    int lz = -1;
-    int any0 = 0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = threadIdx.x * EPT + e;
-      if (i < nq && ta[e] > 0.0) lz = i;
-      if (i < nq && ta[e] == 0.0) any0 = 1;
-    }
-    const int anyz = __syncthreads_or(any0);
-    if (anyz) {
-      int pr = bscan_maxi(lz, reinterpret_cast<int*>(scr));
-      __syncthreads();
-      double fix[EPT];
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const int i = threadIdx.x * EPT + e;
-        fix[e] = (i < nq && ta[e] == 0.0) ? (pr >= 0 ? sA[pr] : 0.0) : -1.0;
-        if (i < nq && ta[e] > 0.0) pr = i;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const int i = threadIdx.x * EPT + e;
-        if (fix[e] >= 0.0) sA[i] = fix[e];
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nq; i += MT) A.A[base + i] = sA[i];
-  // mass balance across the K inputs (barycenter.py:187-191, :368-370)
-  {
-    double mm[2] = {total, -total};
-    cg::cluster_group c2 = cg::this_cluster();
-    double* mine = slots + parity * 16;
-    if (threadIdx.x == 0) {
-      mine[0] = mm[0];
-      mine[1] = mm[1];
-    }
-    c2.sync();
-    const int lane = threadIdx.x & 31;
-    const double om = c2.map_shared_rank(mine, lane < K ? lane : 0)[0];
-    const double mxm = warp_max(lane < K ? om : -CUDART_INF);
-    const double mnm = warp_min(lane < K ? om : CUDART_INF);
-    parity ^= 1;
-    if (q == 0 && threadIdx.x == 0) {
+  tilt_tail<EPT>(A, b, q, nq, ta, red, iscr, vscr);
+}
+
+// ---------------------------------------------------------------------------
+// mot_split: one CTA per problem.  Mass balance across the K inputs
+// (barycenter.py:187-191, :368-370), global ranks of the K*SS regular samples
+// (binary searches between the sorted per-list sample arrays), the S-1
+// splitters (the samples of rank floor(s K SS / S)) and every list's split
+// positions (binary searches in its breakpoints).
+
+__global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
+  extern __shared__ __align__(16) double ssm[];
+  __shared__ double splk[SMAX + 1];
+  __shared__ int splc[SMAX + 1];
+  __shared__ int bad_s;
+  const int b = blockIdx.x;
+  const int K = A.k, n = A.n, S = A.S, SS = A.SS, KSS = K * SS;
+  if (A.done != nullptr && A.done[b]) return;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const double tm = lane < K ? A.tmass[(long)b * K + lane] : 0.0;
+    const double mxm = warp_max(lane < K ? tm : -CUDART_INF);
+    const double mnm = warp_min(lane < K ? tm : CUDART_INF);
+    if (lane == 0) {
       const bool bad = (mxm - mnm) > 1e-9 * mxm;
       A.status[b] = bad ? UOT_MASS_BALANCE : 0;
       if (bad && A.done != nullptr) A.done[b] = 1;
       A.scal[b * 4 + 1] = mnm;  // common total (min)
+      bad_s = bad && A.done != nullptr;
     }
   }
-  // regular samples of this list's events (keys (B_q[t], q, t), t < nq-1)
-  const int ne = nq - 1;
-  const int SS = A.SS;
-  for (int j = threadIdx.x; j < SS; j += MT) {
-    const int t = (ne > 0) ? (int)(((long)(j + 1) * ne) / (SS + 1)) : 0;
-    samp[j] = (ne > 0) ? sA[min(t, ne - 1)] : CUDART_INF;
-    sampt[j] = (ne > 0) ? min(t, ne - 1) : 0;
-  }
-  cl.sync();
-  const int S = A.S;
-  if (S > 1) {
-    // Global rank of each own sample among the K*SS samples (keys (value,
-    // list, index)): binary searches in the other CTAs' sorted sample arrays
-    // over DSMEM.  Exactly one sample holds each rank; the sample of rank
-    // floor(s K SS / S) is splitter s, published into CTA 0's table.
-    const int KSS = K * SS;
-    for (int j = threadIdx.x; j < SS; j += MT) srank[j] = j;
-    for (int idx = threadIdx.x; idx < KSS; idx += MT) {  // every list's samples, local copy
-      const int r = idx / SS, j = idx - r * SS;
-      allv[idx] = cl.map_shared_rank(samp, r)[j];
-      allt[idx] = cl.map_shared_rank(sampt, r)[j];
+  int* sp = A.split + (long)b * (S + 1) * K;
+  if (S == 1) {
+    for (int q = threadIdx.x; q < K; q += ST) {
+      sp[q] = 0;
+      sp[K + q] = max(list_len(A, q) - 1, 0);
     }
-    __syncthreads();
-    for (int pr = threadIdx.x; pr < SS * K; pr += MT) {
-      const int j = pr / K, r = pr - j * K;
+    return;
+  }
+  double* allv = ssm;                                  // [K SS]
+  int* allt = reinterpret_cast<int*>(allv + KSS);      // [K SS]
+  int* rank = allt + KSS;                              // [K SS]
+  for (int idx = threadIdx.x; idx < KSS; idx += ST) {
+    allv[idx] = A.samp[(long)b * KSS + idx];
+    allt[idx] = A.sampt[(long)b * KSS + idx];
+  }
+  __syncthreads();
+  if (bad_s) return;
+  // rank of sample (v, q, t): its index in its own list plus, for every
+  // other list r, #{samples u of r : u < v, or u == v and r < q}
+  int top = 1;
+  while (top * 2 <= SS) top *= 2;
+  for (int idx = threadIdx.x; idx < KSS; idx += ST) {
+    const int q = idx / SS;
+    const double v = allv[idx];
+    int R = idx - q * SS;
+    for (int r = 0; r < K; ++r) {
       if (r == q) continue;
       const double* ov = allv + r * SS;
-      const int* ot = allt + r * SS;
-      const double v = samp[j];
-      const int tt = sampt[j];
-      int lo = 0, hi = SS;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (key_less(ov[mid], r, ot[mid], v, q, tt))
-          lo = mid + 1;
-        else
-          hi = mid;
-      }
-      if (lo > 0) atomicAdd(&srank[j], lo);
-    }
-    __syncthreads();
-    double* k0 = cl.map_shared_rank(splk, 0);
-    int* c0 = cl.map_shared_rank(splc, 0);
-    for (int j = threadIdx.x; j < SS; j += MT) {
-      const int R = srank[j];
-      for (int sidx = (int)(((long)R * S + KSS - 1) / KSS); sidx < S; ++sidx) {
-        if ((int)(((long)sidx * KSS) / S) != R) break;
-        if (sidx >= 1) {
-          k0[sidx] = samp[j];
-          c0[sidx] = ev_code(q, sampt[j]);
+      const bool le = r < q;
+      int pos = 0;
+      for (int step = top; step > 0; step >>= 1) {
+        const int np = pos + step;
+        if (np <= SS) {
+          const double u = ov[np - 1];
+          if (le ? (u <= v) : (u < v)) pos = np;
         }
       }
+      R += pos;
     }
-    cl.sync();
-    // every list locates each splitter in its own breakpoints
-    int* sp = A.split + (long)b * (S + 1) * K;
-    for (int sidx = threadIdx.x; sidx <= S; sidx += MT) {
-      int pos;
-      if (sidx == 0) {
-        pos = 0;
-      } else if (sidx == S) {
-        pos = max(ne, 0);
-      } else {
-        const double v = k0[sidx];
-        const int code = c0[sidx];
-        pos = count_keys_below(sA, max(ne, 0), q, v, ev_list(code), ev_index(code));
+    rank[idx] = R;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < KSS; idx += ST) {
+    const int R = rank[idx];
+    for (int s = (int)(((long)R * S + KSS - 1) / KSS); s < S; ++s) {
+      if ((int)(((long)s * KSS) / S) != R) break;
+      if (s >= 1) {
+        splk[s] = allv[idx];
+        splc[s] = ev_code(idx / SS, allt[idx]);
       }
-      sp[(long)sidx * K + q] = pos;
-    }
-  } else {
-    int* sp = A.split + (long)b * 2 * K;
-    if (threadIdx.x == 0) {
-      sp[q] = 0;
-      sp[K + q] = max(ne, 0);
     }
   }
-  cl.sync();  // keep shared memory alive until every CTA finished reading it
+  __syncthreads();
+  for (int pr = threadIdx.x; pr < (S + 1) * K; pr += ST) {
+    const int s = pr / K, q = pr - s * K;
+    const int ne = max(list_len(A, q) - 1, 0);
+    int pos;
+    if (s == 0) {
+      pos = 0;
+    } else if (s == S) {
+      pos = ne;
+    } else {
+      pos = count_keys_below(A.A + ((long)b * K + q) * n, ne, q, splk[s], ev_list(splc[s]),
+                             ev_index(splc[s]));
+    }
+    sp[(long)s * K + q] = pos;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -543,15 +658,21 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
                                              double*& key, int*& code, int* lo_s, int* cnt_s) {
   const int K = A.k, n = A.n;
   const int* sp = A.split + (long)b * (A.S + 1) * K;
-  if (threadIdx.x == 0) {
-    int c = 0;
-    for (int q = 0; q < K; ++q) {
-      const int lo = sp[(long)s * K + q], hi = sp[(long)(s + 1) * K + q];
-      lo_s[q] = lo;
-      cnt_s[q] = c;
-      c += hi - lo;
+  if (threadIdx.x < 32) {  // lane q: list q's range, offsets by a warp scan
+    const int lane = threadIdx.x;
+    const int lo = lane < K ? sp[(long)s * K + lane] : 0;
+    const int len = lane < K ? sp[(long)(s + 1) * K + lane] - lo : 0;
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    cnt_s[K] = c;
+    if (lane < K) {
+      lo_s[lane] = lo;
+      cnt_s[lane] = incl - len;
+    }
+    if (lane == K - 1) cnt_s[K] = incl;
   }
   __syncthreads();
   const int total = cnt_s[K];
@@ -596,10 +717,11 @@ __global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
     return;
   }
   // barycentre of the tuple before the range: idx_q = lo_q
-  if (threadIdx.x == 0) {
-    double bs = 0.0;
-    for (int q = 0; q < K; ++q) bs += A.omega[q] * A.x[((long)b * K + q) * n + lo_s[q]];
-    bstart_s = bs;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const double v = lane < K ? A.omega[lane] * A.x[((long)b * K + lane) * n + lo_s[lane]] : 0.0;
+    const double bs = warp_sum(v);
+    if (lane == 0) bstart_s = bs;
   }
   __syncthreads();
   const double bstart = bstart_s;
@@ -638,6 +760,8 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   __shared__ double slots[32];
   __shared__ int done_s;
   __shared__ double cc0_s;
+  __shared__ int iscr[MNW];
+  __shared__ double vscr[MNW];
   const int q = (int)cl.block_rank();
   const int b = blockIdx.y;
   const int K = A.k, n = A.n;
@@ -650,15 +774,16 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   if (done_s) return;
   const long base = ((long)b * K + q) * n;
   // initial potential: f_1[0] = Cc(first tuple), f_k[0] = 0 (barycenter.py:206-207)
-  if (threadIdx.x == 0) {
-    double bb = 0.0;
-    for (int r = 0; r < K; ++r) bb += A.omega[r] * A.x[((long)b * K + r) * n];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     double c = 0.0;
-    for (int r = 0; r < K; ++r) {
-      const double d = A.x[((long)b * K + r) * n] - bb;
-      c += A.omega[r] * (d * d);
+    if (q == 0) {
+      const double x0 = lane < K ? A.x[((long)b * K + lane) * n] : 0.0;
+      const double om = lane < K ? A.omega[lane] : 0.0;
+      const double bb = warp_sum(om * x0);
+      c = warp_sum(om * ((x0 - bb) * (x0 - bb)));
     }
-    cc0_s = (q == 0) ? c : 0.0;
+    if (lane == 0) cc0_s = c;
   }
   __syncthreads();
   double rv[EPT];
@@ -697,7 +822,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     const double d = rv[e] - fv[e];
     acc[0] += tv[e] * d;                 // fw_gap part (barycenter.py:376-381)
     acc[1] += tv[e] * rv[e];             // plan cost via complementary slackness
-    if (tv[e] > 0.0) acc[2] += tv[e] * (-(fv[e] + lamq) / rq);  // sum ta log(ta/a)
+    if (tv[e] > 0.0) acc[2] += tv[e] * (-(fv[e] + lamq) * irq);  // sum ta log(ta/a)
     acc[3] += tv[e];                     // tilted mass
     acc[4] += wv[e];                     // input mass
     acc[5] += tv[e] * d;                 // first moment of d under p_0
@@ -753,7 +878,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           const double d = rv[e] - fv[e];
-          const double ww = wv[e] * bops::exp_fast(-(fv[e] + gam * d) * irq - sh, tab);
+          const double ww = bops::wexp(wv[e], -(fv[e] + gam * d) * irq - sh, tab);
           const double xc = d - cq;
           mom[0] += ww;
           mom[1] += ww * xc;
@@ -785,49 +910,49 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
 #pragma unroll
   for (int e = 0; e < EPT; ++e) fv[e] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
   store_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+  {  // log-sum-exp of the new iterate for the next tilt / the final translation
+    double mx, qk;
+    double* r0 = ping.next();
+    double* r1 = ping.next();
+    list_lse<EPT>(wv, fv, irq, tab, r0, r1, mx, qk, tv);  // tv <- w exp(-f/rho - mx)
+    if (threadIdx.x == 0) {
+      A.lse[((long)b * K + q) * 2 + 0] = mx;
+      A.lse[((long)b * K + q) * 2 + 1] = qk;
+    }
+    if (t + 1 < A.max_iters) {
+      // the next iteration's tilt, fused: lambda from the cluster's
+      // log-sum-exps (barycenter.py:316-317), H_0 (:320-327), breakpoints.
+      double ex[3] = {rq * qk, rq * acc[4], rq};
+      cluster_sum<3>(ex, slots, parity);
+      const double lam1 = rq * qk - (rq / ex[2]) * ex[0];
+      if (threadIdx.x == 0) {
+        A.lam[(long)b * K + q] = lam1;
+        if (q == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
+      }
+      const double sc = exp(mx - lam1 * irq);
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) tv[e] *= sc;
+      tilt_tail<EPT>(A, b, q, nq, tv, ping.next(), iscr, vscr);
+    }
+  }
   cl.sync();  // slots stay valid until every CTA read them
 }
 
-// Final translation by the optimal zero-sum lambda (barycenter.py:413-414).
+// Final translation by the optimal zero-sum lambda (barycenter.py:413-414),
+// from the log-sum-exps the last update stored for the final iterate.
 template <int EPT>
 __global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ double scr[32 * 8];
-  __shared__ double tab[32];
-  __shared__ double slots[32];
-  const int q = (int)cl.block_rank();
-  const int b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
-  int parity = 0;
-  bops::load_exp_table(tab);
   const long base = ((long)b * K + q) * n;
-  const double rq = A.omega[q] * A.rho;
-  double w[EPT], fv[EPT];
-  double mx[1] = {-CUDART_INF};
+  double ex0, ex1, rtot;
+  const double lamq = problem_lambda(A, b, q, ex0, ex1, rtot);
+  double fv[EPT];
+  load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
 #pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    w[e] = i < nq ? A.a[base + i] : 0.0;
-    fv[e] = i < nq ? A.f[base + i] : 0.0;
-    if (w[e] > 0.0) mx[0] = fmax(mx[0], -fv[e] / rq);
-  }
-  bmax_k<1>(mx, scr);
-  double sm[1] = {0.0};
-#pragma unroll
-  for (int e = 0; e < EPT; ++e)
-    sm[0] += w[e] * bops::exp_fast(-fv[e] / rq - mx[0], tab);
-  bsum_k<1>(sm, scr);
-  const double qk = mx[0] + log(sm[0]);
-  double ex[2] = {rq * qk, rq};
-  cluster_sum<2>(ex, slots, parity);
-  const double lamq = rq * qk - (rq / ex[1]) * ex[0];
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = threadIdx.x * EPT + e;
-    if (i < nq) A.out_f[base + i] = fv[e] + lamq;
-  }
-  cl.sync();
+  for (int e = 0; e < EPT; ++e) fv[e] += lamq;
+  store_run<EPT>(A.out_f + base, threadIdx.x * EPT, nq, fv);
 }
 
 // ---------------------------------------------------------------------------
@@ -941,7 +1066,7 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
 
 struct MotPlan {
   int S, SS, ept;
-  size_t prep_smem, bucket_smem;
+  size_t tilt_smem, split_smem, bucket_smem;
 };
 
 int ept_for(int n) {
@@ -962,9 +1087,8 @@ MotPlan plan_for(int k, int n) {
   p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
   while ((long)k * p.SS > 4096) p.SS = std::max(1, p.SS / 2);
   p.ept = ept_for(n);
-  p.prep_smem = sizeof(double) * (size_t)n + (sizeof(double) + 2 * sizeof(int)) * (size_t)p.SS +
-                16 + 2 * sizeof(double) * (size_t)(p.S + 1) +
-                (sizeof(double) + sizeof(int)) * (size_t)k * p.SS + 16;
+  p.tilt_smem = sizeof(double) * (size_t)n;
+  p.split_smem = (sizeof(double) + 2 * sizeof(int)) * (size_t)k * p.SS;
   p.bucket_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)CAP;
   return p;
 }
@@ -989,9 +1113,17 @@ int launch_cluster(Kern kern, int k, int batch, size_t smem, cudaStream_t st, co
   return UOT_OK;
 }
 
+// tilt -> splitters -> buckets (the K-marginal sweep); then the update.
 template <int EPT>
-int run_iteration(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
-  UOT_TRY(launch_cluster(mot_prep<EPT>, a.k, a.batch, p.prep_smem, st, a));
+int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
+  if (tilt) {  // otherwise the previous mot_update already tilted (fused)
+    mot_tilt<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
+    UOT_CHECK_LAUNCH();
+  }
+  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_split, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p.split_smem));
+  mot_split<<<a.batch, ST, p.split_smem, st>>>(a);
+  UOT_CHECK_LAUNCH();
   UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)p.bucket_smem));
   mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
@@ -1015,9 +1147,11 @@ int run_plan(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
 template <int EPT>
 int run_all(MotArgs a, const MotPlan& p, cudaStream_t st, bool fw) {
   if (fw) {
+    mot_lse<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
+    UOT_CHECK_LAUNCH();
     for (int t = 0; t < a.max_iters; ++t) {
       a.t = t;
-      UOT_TRY(run_iteration<EPT>(a, p, st));
+      UOT_TRY(run_sweep<EPT>(a, p, st, t == 0));
     }
     // plan of the last recorded iteration: its breakpoints are still in A.
     // (Converged problems stopped before updating; the others updated f
@@ -1025,15 +1159,11 @@ int run_all(MotArgs a, const MotPlan& p, cudaStream_t st, bool fw) {
     MotArgs ap = a;
     ap.done = nullptr;
     UOT_TRY(run_plan(ap, p, st));
-    UOT_TRY(launch_cluster(mot_finalize<EPT>, a.k, a.batch, 0, st, a));
+    mot_finalize<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
+    UOT_CHECK_LAUNCH();
   } else {
     a.mode = 1;
-    UOT_TRY(launch_cluster(mot_prep<EPT>, a.k, a.batch, p.prep_smem, st, a));
-    UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)p.bucket_smem));
-    mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
-    UOT_CHECK_LAUNCH();
-    UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch, 0, st, a));
+    UOT_TRY(run_sweep<EPT>(a, p, st, true));
     UOT_TRY(run_plan(a, p, st));
   }
   return UOT_OK;
@@ -1056,13 +1186,13 @@ int dispatch(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool fw) {
 // [B][4]; lam [B][K]; bcount [B][S]; done [B]; omega [K]; lens [K];
 // h0/fw/pd [B][T] + iterations (for the plain sweep).
 struct MotWs {
-  size_t off[12];
+  size_t off[17];
   size_t total;
 };
 
-MotWs ws_layout(int batch, int k, int n, int S) {
+MotWs ws_layout(int batch, int k, int n, int S, int SS) {
   MotWs w;
-  size_t sz[12];
+  size_t sz[17];
   const size_t bkn = (size_t)batch * k * n;
   sz[0] = sizeof(double) * bkn;
   sz[1] = sizeof(double) * bkn;
@@ -1076,8 +1206,13 @@ MotWs ws_layout(int batch, int k, int n, int S) {
   sz[9] = sizeof(int) * (size_t)k;
   sz[10] = sizeof(double) * 3 * (size_t)batch + sizeof(int) * (size_t)batch;
   sz[11] = sizeof(double) * bkn;  // working copy of the potentials
+  sz[12] = sizeof(double) * 2 * (size_t)batch * k;   // lse
+  sz[13] = sizeof(double) * (size_t)batch * k;       // mass
+  sz[14] = sizeof(double) * (size_t)batch * k;       // tmass
+  sz[15] = sizeof(double) * (size_t)batch * k * SS;  // samples
+  sz[16] = sizeof(int) * (size_t)batch * k * SS;     // sample indices
   size_t o = 0;
-  for (int i = 0; i < 12; ++i) {
+  for (int i = 0; i < 17; ++i) {
     w.off[i] = o;
     o += (sz[i] + 255) / 256 * 256;
   }
@@ -1088,7 +1223,7 @@ MotWs ws_layout(int batch, int k, int n, int S) {
 MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const double* omega_host,
                   const int32_t* lens_host, double rho, cudaStream_t st, int* rc) {
   MotArgs a{};
-  MotWs L = ws_layout(batch, k, n, p.S);
+  MotWs L = ws_layout(batch, k, n, p.S, p.SS);
   a.batch = batch;
   a.k = k;
   a.n = n;
@@ -1103,6 +1238,11 @@ MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const dou
   a.lam = (double*)(ws + L.off[5]);
   a.bcount = (int*)(ws + L.off[6]);
   a.done = (int*)(ws + L.off[7]);
+  a.lse = (double*)(ws + L.off[12]);
+  a.mass = (double*)(ws + L.off[13]);
+  a.tmass = (double*)(ws + L.off[14]);
+  a.samp = (double*)(ws + L.off[15]);
+  a.sampt = (int*)(ws + L.off[16]);
   double* om = (double*)(ws + L.off[8]);
   a.omega = om;
   a.lens = nullptr;
@@ -1149,7 +1289,7 @@ using namespace uot;
 extern "C" int uot_mot1d_workspace_size(int32_t batch, int32_t k, int32_t n, size_t* bytes) {
   UOT_TRY(check_sizes(batch, k, n));
   MotPlan p = plan_for(k, n);
-  *bytes = ws_layout(batch, k, n, p.S).total;
+  *bytes = ws_layout(batch, k, n, p.S, p.SS).total;
   return UOT_OK;
 }
 
@@ -1160,7 +1300,7 @@ extern "C" int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const int3
                                  void* stream) {
   UOT_TRY(check_sizes(batch, k, n));
   MotPlan p = plan_for(k, n);
-  if (workspace_bytes < ws_layout(batch, k, n, p.S).total) {
+  if (workspace_bytes < ws_layout(batch, k, n, p.S, p.SS).total) {
     set_error("uot_mot1d_batched: workspace too small");
     return UOT_INVALID;
   }
@@ -1202,7 +1342,7 @@ extern "C" int uot_bary_run(const uot_bary_desc* d, void* workspace, size_t work
     return UOT_INVALID;
   }
   MotPlan p = plan_for(d->k, d->n);
-  MotWs L = ws_layout(d->batch, d->k, d->n, p.S);
+  MotWs L = ws_layout(d->batch, d->k, d->n, p.S, p.SS);
   if (workspace_bytes < L.total) {
     set_error("uot_bary_run: workspace too small");
     return UOT_INVALID;
