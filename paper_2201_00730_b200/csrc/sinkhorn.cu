@@ -411,6 +411,41 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// 2^x for a packed pair on the FMA pipe (exp2 offload: the MUFU pipe, 16
+// ex2/clk/SM, is the kernel's bound while issue slots are left over).
+// x = n + f with n = rint(x) by the 1.5*2^23 trick, 2^f by a degree-4
+// minimax polynomial on [-1/2, 1/2] (max rel. error 2.7e-6, vs ~2^-22 for
+// ex2.approx), 2^n added into the exponent field with one IMAD.  Inputs are
+// clamped below at -127 (the result is then ~2^-127, where MUFU flushes to
+// 0: negligible next to the tile's unit-scale terms); the caller checks the
+// running maximum `pmax` (FMNMX3) against 126 and falls back to MUFU.
+__device__ __forceinline__ u64 ex2_poly2(u64 x, float& pmax) {
+  float lo, hi;
+  u2(x, lo, hi);
+  asm("max.f32 %0, %0, %1, %2;" : "+f"(pmax) : "f"(lo), "f"(hi));
+  const u64 xc = p2(fmaxf(lo, -127.f), fmaxf(hi, -127.f));
+  const u64 MAG = p2(12582912.f, 12582912.f);
+  const u64 tm = add2(xc, MAG);
+  const u64 nf = add2(tm, p2(-12582912.f, -12582912.f));
+  const u64 f = fma2(nf, p2(-1.f, -1.f), xc);
+  u64 q = fma2(f, p2(0.009570101276040077f, 0.009570101276040077f),
+               p2(0.05591786280274391f, 0.05591786280274391f));
+  q = fma2(f, q, p2(0.240247443318367f, 0.240247443318367f));
+  q = fma2(f, q, p2(0.6931217908859253f, 0.6931217908859253f));
+  q = fma2(f, q, p2(0.9999992847442627f, 0.9999992847442627f));
+  unsigned qlo, qhi, tlo, thi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(qlo), "=r"(qhi) : "l"(q));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(tm));
+  const unsigned rlo = tlo * 0x800000u + qlo, rhi = thi * 0x800000u + qhi;
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(rlo), "r"(rhi));
+  return r;
+}
+
+#ifndef SQ2_NPOLY
+#define SQ2_NPOLY 0  // rows per RT-row tile on the FMA-pipe exp2 (measured: no gain)
+#endif
+
 // Slow path of a packed tile (stale shift outside the safe window): redo
 // the tile column by column with an explicit maximum and rescale.
 template <int CP, int RT, bool CHECK>
@@ -479,22 +514,27 @@ __device__ __forceinline__ void tile_sq2(const float* srec, int rr, int clen, co
   }
   u64 na[CP];
   bool bad = false;
+  constexpr int NPOLY = CHECK ? 0 : (SQ2_NPOLY < RT ? SQ2_NPOLY : RT - 1);
+  float pmax = -INFINITY;
 #pragma unroll
   for (int j = 0; j < CP; ++j) {
     float lo, hi;
     u2(t[0][j], lo, hi);
     u64 s = p2(ex2f(lo), ex2f(hi));
 #pragma unroll
-    for (int i = 1; i < RT; ++i) {
+    for (int i = 1; i < RT - NPOLY; ++i) {
       u2(t[i][j], lo, hi);
       s = add2(s, p2(ex2f(lo), ex2f(hi)));
     }
+#pragma unroll
+    for (int i = RT - NPOLY; i < RT; ++i) s = add2(s, ex2_poly2(t[i][j], pmax));
     na[j] = add2(acc[j], s);
     float alo, ahi;
     u2(na[j], alo, ahi);
     bad |= !(alo < 1.2676506e30f && ahi < 1.2676506e30f && alo > 7.8886091e-31f &&
              ahi > 7.8886091e-31f);  // (2^-100, 2^100)
   }
+  bad |= pmax > 126.f;
   if (bad) {
     tile_sq2_slow<CP, RT, CHECK>(srec, rr, clen, y0, y1, cc, mm, acc);
   } else {
