@@ -25,6 +25,12 @@ int uot_probe_mufu_ex2(void* stream, double* ex2_per_s);
  * A from TMEM, B from shared memory); device pointers, row-major. */
 int uot_tc_selftest(const float* A, const float* B, int K, float* D, void* stream);
 
+/* tcgen05 issue-rate probe: each of `ctas` CTAs issues `reps` back-to-back
+ * 128 x n x 8 kind::tf32 MMAs (A from TMEM if ss == 0, else shared memory)
+ * and adds its clock64 cycle count to *out_dev (device pointer). */
+int uot_probe_tc_rate(int ctas, int reps, int n, int ss, unsigned long long* out_dev,
+                      void* stream);
+
 /* FP64 DFMA throughput probe (DFMA per second). */
 int uot_probe_dfma(void* stream, double* dfma_per_s);
 

@@ -1069,10 +1069,22 @@ struct Engine {
     dim3 grid(ceil_div(a.nout, OUT_PER_BLOCK), splits, d.batch);
     const size_t smem = (size_t)a.chunk * a.g.rw * sizeof(T);
     if constexpr (std::is_same<P, SqE32TC>::value) {
-      const size_t tsm = (size_t)TC_STAGES * TC_STAGE_BYTES;
-      UOT_CUDA_TRY(cudaFuncSetAttribute(sk_main_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tsm));
-      sk_main_tc<0><<<grid, TC_THREADS, tsm, st>>>(a, tc_kp(d.d));
+      const size_t tsm = tc_smem_bytes(d.d);
+      auto go = [&](auto kern) -> int {
+        UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tsm));
+        kern<<<grid, TC_THREADS, tsm, st>>>(a, tc_kp(d.d));
+        return UOT_OK;
+      };
+      int rc;
+      switch (d.d) {
+        case 32: rc = go(sk_main_tc<32>); break;
+        case 48: rc = go(sk_main_tc<48>); break;
+        case 64: rc = go(sk_main_tc<64>); break;
+        case 96: rc = go(sk_main_tc<96>); break;
+        default: rc = go(sk_main_tc<0>); break;
+      }
+      if (rc != UOT_OK) return rc;
     } else if constexpr (std::is_same<P, SqE32<2>>::value) {
       static_assert(C::COLS % 2 == 0, "packed kernel needs an even column count");
       sk_main_sq2<C::THREADS, C::COLS / 2, C::RT><<<grid, C::THREADS, smem, st>>>(a);
@@ -1557,3 +1569,15 @@ extern "C" int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* works
                                     reps, ms_out);
   });
 }
+
+#ifdef UOT_TC_PROF
+extern "C" int uot_tc_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, uot::g_tc_prof, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return 4;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(uot::g_tc_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

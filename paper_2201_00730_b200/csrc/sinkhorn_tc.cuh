@@ -25,14 +25,29 @@
 namespace uot {
 
 constexpr int TC_TILE = 128;        // M (outputs) and N (reduced) per MMA tile
-constexpr int TC_STAGE_K = 16;      // K elements per shared-memory stage
-constexpr int TC_STAGES = 12;
+#ifndef UOT_TC_STAGE_K
+#define UOT_TC_STAGE_K 16
+#endif
+constexpr int TC_STAGE_K = UOT_TC_STAGE_K;  // K elements per shared-memory stage
+#ifndef UOT_TC_STAGES
+#define UOT_TC_STAGES 12
+#endif
+constexpr int TC_STAGES = UOT_TC_STAGES;  // B-operand ring depth (bytes in flight hide L2 latency)
 constexpr int TC_THREADS = 192;
 constexpr int TC_STAGE_BYTES = TC_TILE * TC_STAGE_K * 4;  // 8 KiB
 
+// Output-side point tile staged in shared memory for the A prologue: 128
+// rows of d floats, row stride d + 4 (conflict-free float4 row reads).
+__host__ __device__ __forceinline__ int tc_ystride(int d) { return d + 4; }
+__host__ __device__ __forceinline__ size_t tc_smem_bytes(int d) {
+  return (size_t)TC_STAGES * TC_STAGE_BYTES + sizeof(float) * 128 * (size_t)tc_ystride(d);
+}
+
 // K extent of a reduced-side record (B) and of an output-side row (A).
-__host__ __device__ __forceinline__ int tc_kp(int d) { return (2 * d + 6 + 15) / 16 * 16; }
-__host__ __device__ __forceinline__ int tc_ka(int d) { return 2 * d + 8; }
+__host__ __device__ constexpr int tc_kp(int d) {
+  return (2 * d + 6 + TC_STAGE_K - 1) / TC_STAGE_K * TC_STAGE_K;
+}
+__host__ __device__ constexpr int tc_ka(int d) { return 2 * d + 8; }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
 
@@ -41,7 +56,43 @@ __device__ __forceinline__ long tc_tile_index(int rl, int k) {
   return (long)(k >> 2) * (16 * 32) + (rl >> 3) * 32 + (rl & 7) * 4 + (k & 3);
 }
 
-template <int CHECK_UNUSED = 0>
+#ifdef UOT_TC_PROF
+// Debug instrumentation (-DUOT_TC_PROF): cycles spent in each wait, summed
+// over CTAs: [0] producer empty, [1] MMA full, [2] MMA dempty, [3] epilogue
+// dfull, [4] prologue, [5] total, [6] epilogue math, [7] MMA issue loop.
+__device__ unsigned long long g_tc_prof[8];
+#define TCP_T0() const long long _tcp0 = clock64()
+#define TCP_ADD(i) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - _tcp0))
+#else
+#define TCP_T0()
+#define TCP_ADD(i)
+#endif
+
+// One K-slice (8 columns of B) of a column tile: the MMAs it feeds.  B
+// row = [Xh(d), Xl(d), Uh, Um, Ul, 1, 1, 1, 0..]; A row = [Yh(d), Yl(d), 1,
+// 1, 1, ch, cm, cl]: Xh slices meet Yh and Yl, Xl slices meet Yh, the last
+// slice meets the constants (3xTF32 split of 2L x.y + U + c).
+__device__ __forceinline__ void tc_slice_mmas(int kb, int d, uint32_t dcol, uint32_t tbase,
+                                              uint64_t bd, uint32_t idesc, bool& first) {
+  if (kb < d) {
+    tc::mma_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
+    tc::mma_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
+    first = false;
+  } else if (kb < 2 * d) {
+    tc::mma_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
+    first = false;
+  } else if (kb < 2 * d + 8) {
+    tc::mma_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
+    first = false;
+  }
+}
+
+// DT > 0: the feature dimension is a compile-time constant, so the MMA
+// issue sequence of a column tile is fully unrolled and branch-free (the
+// single issuing thread is otherwise the bottleneck: a tight tcgen05.mma
+// stream runs at the 64-cycle floor of a 128x128x8 tf32 MMA, the generic
+// loop at ~96+).  DT = 0: runtime d.
+template <int DT>
 __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, int KP) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], dfull[2], dempty[2];
@@ -52,9 +103,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int split = blockIdx.y, S = gridDim.y;
   const int ntiles = (A.nred + TC_TILE - 1) / TC_TILE;
   const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
-  const int nst = KP / TC_STAGE_K;
-  const int d = A.g.d;
+  const int nst = DT > 0 ? tc_kp(DT) / TC_STAGE_K : KP / TC_STAGE_K;
+  const int d = DT > 0 ? DT : A.g.d;
 
+#ifdef UOT_TC_PROF
+  const long long _tstart = clock64();
+#endif
   if (warp == 1) tc::tmem_alloc(&tbase_s, 512);
   if (tid == 0) {
     for (int i = 0; i < TC_STAGES; ++i) {
@@ -78,10 +132,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int row = lane_base + lane;
   const int o = blockIdx.x * TC_TILE + row;
   float m_o = 0.f;
+  // Prologue: the CTA's 128 output points -> shared memory (all threads,
+  // coalesced float4 loads), then each epilogue thread builds its A row
+  // [Yh, Yl, 1, 1, 1, ch, cm, cl] (tf32 splits) and stores it into TMEM.
+  float* ys = reinterpret_cast<float*>(smem + (size_t)TC_STAGES * TC_STAGE_BYTES);
+  const int YS = tc_ystride(d);
+  {
+    const int row0 = blockIdx.x * TC_TILE;
+    const int nrows = min(TC_TILE, A.nout - row0);
+    const float4* src =
+        reinterpret_cast<const float4*>(A.g.out_pts + b * A.g.out_pts_bstride + (long)row0 * d);
+    const int q4 = d / 4;
+    for (int idx = tid; idx < nrows * q4; idx += TC_THREADS) {
+      const int r = idx / q4, c = idx - r * q4;
+      *reinterpret_cast<float4*>(ys + r * YS + 4 * c) = src[idx];
+    }
+  }
+  __syncthreads();
   if (warp >= 2) {
-    const float* y = A.g.out_pts + b * A.g.out_pts_bstride + (long)(o < A.nout ? o : 0) * d;
+    const float* y = ys + row * YS;
     double s2 = 0.0;
-    for (int k = 0; k < d; ++k) s2 += (double)y[k] * (double)y[k];
+    if (o < A.nout) {
+      for (int k = 0; k < d; k += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(y + k);
+        s2 = fma((double)v.x, (double)v.x, s2);
+        s2 = fma((double)v.y, (double)v.y, s2);
+        s2 = fma((double)v.z, (double)v.z, s2);
+        s2 = fma((double)v.w, (double)v.w, s2);
+      }
+    }
     m_o = o < A.nout ? A.shift_in[(long)b * A.nout + o] : 0.f;
     const double c = -s2 * (double)A.g.L - (double)m_o;
     const float ch = tf32_hi((float)c);
@@ -89,35 +168,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const float cm = tf32_hi((float)c1);
     const float cl = (float)(c1 - (double)cm);
     const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
-    const int KA = tc_ka(d);
-    for (int k0 = 0; k0 < KA; k0 += 8) {
-      uint32_t v[8];
+    // Yh at columns [0, d), Yl at [d, 2d): 8 columns per store
+    for (int k0 = 0; k0 < d; k0 += 8) {
+      const float4 u0 = *reinterpret_cast<const float4*>(y + k0);
+      const float4 u1 = *reinterpret_cast<const float4*>(y + k0 + 4);
+      const float yv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      uint32_t vh[8], vl[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int k = k0 + e;
-        float val = 0.f;
-        if (k < 2 * d) {
-          const float yk = y[k % d];
-          const float yh = tf32_hi(yk);
-          val = (k < d) ? yh : (yk - yh);
-        } else if (k < 2 * d + 3) {
-          val = 1.f;
-        } else if (k == 2 * d + 3) {
-          val = ch;
-        } else if (k == 2 * d + 4) {
-          val = cm;
-        } else if (k == 2 * d + 5) {
-          val = cl;
-        }
-        v[e] = __float_as_uint(val);
+        const float yk = o < A.nout ? yv[e] : 0.f;
+        const float yh = tf32_hi(yk);
+        vh[e] = __float_as_uint(yh);
+        vl[e] = __float_as_uint(yk - yh);
       }
-      tc::tmem_st8(ta + k0, v);
+      tc::tmem_st8(ta + k0, vh);
+      tc::tmem_st8(ta + d + k0, vl);
+    }
+    {
+      const uint32_t vt[8] = {__float_as_uint(1.f), __float_as_uint(1.f), __float_as_uint(1.f),
+                              __float_as_uint(ch),  __float_as_uint(cm),  __float_as_uint(cl),
+                              0u,                   0u};
+      tc::tmem_st8(ta + 2 * d, vt);
     }
     tc::wait_st();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+#ifdef UOT_TC_PROF
+  if (tid == 0) atomicAdd(&g_tc_prof[4], (unsigned long long)(clock64() - _tstart));
+#endif
 
   const float* recb = A.g.red_rec + b * A.g.red_bstride;
   if (warp == 0) {
@@ -126,7 +206,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       uint32_t phase = 0;
       for (int tile = t0; tile < t1; ++tile) {
         for (int st = 0; st < nst; ++st) {
-          tc::mbar_wait(&empty_b[slot], phase ^ 1);
+          {
+            TCP_T0();
+            tc::mbar_wait(&empty_b[slot], phase ^ 1);
+            TCP_ADD(0);
+          }
           tc::mbar_expect_tx(&full_b[slot], TC_STAGE_BYTES);
           tc::bulk_g2s(smem + slot * TC_STAGE_BYTES,
                        recb + (long)tile * TC_TILE * KP + (long)st * TC_TILE * TC_STAGE_K,
@@ -146,37 +230,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       for (int i = 0; i < t1 - t0; ++i) {
         const int buf = i & 1;
         const uint32_t dph = (i >> 1) & 1;
-        tc::mbar_wait(&dempty[buf], dph ^ 1);
+        {
+          TCP_T0();
+          tc::mbar_wait(&dempty[buf], dph ^ 1);
+          TCP_ADD(2);
+        }
         tc::fence_after();
         const uint32_t dcol = tbase + 256 + buf * TC_TILE;
         bool first = true;
-        for (int st = 0; st < nst; ++st) {
-          tc::mbar_wait(&full_b[slot], phase);
-          tc::fence_after();
-          const unsigned char* sb = smem + slot * TC_STAGE_BYTES;
+        // shared-memory descriptor of slot 0; other slots / slices add their
+        // byte offset >> 4 to the start-address field (addresses < 256 KiB)
+        const uint64_t bd0 = tc::sdesc(smem, 2048, 128);
+        constexpr int NST = DT > 0 ? tc_kp(DT) / TC_STAGE_K : 1;
 #pragma unroll
-          for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
-            const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
-            const uint64_t bd = tc::sdesc(sb + ks * 2 * 2048, 2048, 128);
-            if (kb < d) {  // Xh: pair with Yh and Yl
-              tc::mma_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
-              tc::mma_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
-              first = false;
-            } else if (kb < 2 * d) {  // Xl: pair with Yh
-              tc::mma_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
-              first = false;
-            } else if (kb < 2 * d + 8) {  // U parts / ones against ones / c parts
-              tc::mma_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
-              first = false;
+        for (int stu = 0; stu < (DT > 0 ? NST : 1); ++stu) {
+          for (int str = 0; str < (DT > 0 ? 1 : nst); ++str) {
+            const int st = DT > 0 ? stu : str;
+            {
+              TCP_T0();
+              tc::mbar_wait(&full_b[slot], phase);
+              TCP_ADD(1);
+            }
+            tc::fence_after();
+            const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
+#ifdef UOT_TC_NOMMA  // experiment: B feed alone
+            tc::mbar_arrive(&empty_b[slot]);
+            (void)bds;
+#else
+#pragma unroll
+            for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
+              const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
+              tc_slice_mmas(kb, d, dcol, tbase, bds + (uint64_t)((ks * 2 * 2048) >> 4), idesc,
+                            first);
+            }
+            tc::mma_commit(&empty_b[slot]);
+#endif
+            if (++slot == TC_STAGES) {
+              slot = 0;
+              phase ^= 1;
             }
           }
-          tc::mma_commit(&empty_b[slot]);
-          if (++slot == TC_STAGES) {
-            slot = 0;
-            phase ^= 1;
-          }
         }
+#ifdef UOT_TC_NOMMA
+        tc::mbar_arrive(&dfull[buf]);
+#else
         tc::mma_commit(&dfull[buf]);
+#endif
       }
     }
     __syncwarp();
@@ -187,7 +286,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     for (int i = 0; i < t1 - t0; ++i) {
       const int buf = i & 1;
       const uint32_t dph = (i >> 1) & 1;
-      tc::mbar_wait(&dfull[buf], dph);
+      {
+        TCP_T0();
+        tc::mbar_wait(&dfull[buf], dph);
+        if (lane == 0) TCP_ADD(3);
+      }
       tc::fence_after();
       const uint32_t dcol = tl + 256 + buf * TC_TILE;
       float s = 0.f;
@@ -255,6 +358,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   }
   tc::fence_before();
   __syncthreads();
+#ifdef UOT_TC_PROF
+  if (tid == 0) atomicAdd(&g_tc_prof[5], (unsigned long long)(clock64() - _tstart));
+#endif
   if (warp == 1) tc::tmem_free(tbase, 512);
 }
 

@@ -71,7 +71,81 @@ __global__ void __launch_bounds__(128) tc_selftest_kernel(const float* A, const 
   if (warp == 0) tc::tmem_free(tbase, 512);
 }
 
+// Issue-rate probe: `reps` back-to-back 128 x N x 8 tf32 MMAs, timed with
+// clock64 by the issuing thread; cycles summed over CTAs.  MODE 0: one
+// accumulator, A from TMEM; 1: A from shared memory; 2: two interleaved
+// accumulators; 3: four interleaved accumulators (N <= 64).
+template <int MODE>
+__global__ void __launch_bounds__(128) tc_rate_kernel(int reps, int N, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  const int t = threadIdx.x, warp = t >> 5;
+  float* s = reinterpret_cast<float*>(smem);
+  for (int i = t; i < 2 * 256 * 8; i += blockDim.x) s[i] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) tc::tmem_alloc(&tbase_s, 512);
+  if (t == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = tbase_s;
+  if (t == 0) {
+    const uint32_t idesc = tc::idesc_tf32(128, N);
+    const uint64_t bd = tc::sdesc(s, (N / 8) * 128, 128);
+    const uint64_t ad = tc::sdesc(s + 256 * 8, 16 * 128, 128);
+    const long long c0 = clock64();
+    if (MODE == 0) {
+      tc::mma_tf32_ts(tbase + 256, tbase, bd, idesc, 0u);
+      for (int r = 1; r < reps; ++r) tc::mma_tf32_ts(tbase + 256, tbase, bd, idesc, 1u);
+    } else if (MODE == 1) {
+      tc::mma_tf32_ss(tbase + 256, ad, bd, idesc, 0u);
+      for (int r = 1; r < reps; ++r) tc::mma_tf32_ss(tbase + 256, ad, bd, idesc, 1u);
+    } else if (MODE == 2) {
+      for (int r = 0; r < reps; r += 2) {
+        tc::mma_tf32_ts(tbase + 256, tbase, bd, idesc, 1u);
+        tc::mma_tf32_ts(tbase + 384, tbase, bd, idesc, 1u);
+      }
+    } else {
+      for (int r = 0; r < reps; r += 4) {
+        tc::mma_tf32_ts(tbase + 256, tbase, bd, idesc, 1u);
+        tc::mma_tf32_ts(tbase + 320, tbase, bd, idesc, 1u);
+        tc::mma_tf32_ts(tbase + 384, tbase, bd, idesc, 1u);
+        tc::mma_tf32_ts(tbase + 448, tbase, bd, idesc, 1u);
+      }
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    atomicAdd(out, (unsigned long long)(clock64() - c0));
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tbase, 512);
+}
+
 }  // namespace uot
+
+extern "C" int uot_probe_tc_rate(int ctas, int reps, int n, int ss, unsigned long long* out_dev,
+                                 void* stream) {
+  using namespace uot;
+  if (n < 8 || n > 256 || n % 8 != 0) {
+    set_error("uot_probe_tc_rate: N in [8, 256], multiple of 8");
+    return UOT_INVALID;
+  }
+  const size_t smem = 2 * 256 * 8 * 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (ss) {
+    case 0: tc_rate_kernel<0><<<ctas, 128, smem, st>>>(reps, n, out_dev); break;
+    case 1: tc_rate_kernel<1><<<ctas, 128, smem, st>>>(reps, n, out_dev); break;
+    case 2: tc_rate_kernel<2><<<ctas, 128, smem, st>>>(reps, n, out_dev); break;
+    default: tc_rate_kernel<3><<<ctas, 128, smem, st>>>(reps, n, out_dev); break;
+  }
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
 
 extern "C" int uot_tc_selftest(const float* A, const float* B, int K, float* D, void* stream) {
   using namespace uot;
