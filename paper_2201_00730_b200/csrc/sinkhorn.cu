@@ -224,8 +224,11 @@ struct SqE32TC {
     float bias;
   };
   static int rw(int d) { return tc_kp(d); }
-  static __device__ __forceinline__ void pack_tile(float* base, long r, int KP, double hat,
-                                                   const float* pt, double w, double L, int d) {
+  // Static part of a record, written once per solve (tc_init_static):
+  // Xh, Xl = tf32 split of 2L x, the unit columns, zero padding, and |x|^2
+  // (fp64) parked in the unused columns 2d+8, 2d+9 (no MMA reads them).
+  static __device__ __forceinline__ void init_tile(float* base, long r, int KP, const float* pt,
+                                                   double L, int d) {
     float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
     const int rl = (int)(r % TC_TILE);
     double s2 = 0.0;
@@ -236,19 +239,38 @@ struct SqE32TC {
       tile[tc_tile_index(rl, d + k)] = x - xh;
       s2 += (double)pt[k] * (double)pt[k];
     }
-    const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
-    const float uh = tf32_hi((float)u);
-    const double u1 = u - (double)uh;
-    const float um = tf32_hi((float)u1);
-    tile[tc_tile_index(rl, 2 * d)] = uh;
-    tile[tc_tile_index(rl, 2 * d + 1)] = um;
-    tile[tc_tile_index(rl, 2 * d + 2)] = (float)(u1 - (double)um);
     tile[tc_tile_index(rl, 2 * d + 3)] = 1.f;
     tile[tc_tile_index(rl, 2 * d + 4)] = 1.f;
     tile[tc_tile_index(rl, 2 * d + 5)] = 1.f;
     for (int k = 2 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k)] = 0.f;
+    *reinterpret_cast<double*>(tile + tc_tile_index(rl, 2 * d + 8)) = s2;
+  }
+  // Per half-step: only U = (hat - |x|^2) L + log2 w changes -- one 16-byte
+  // store [Uh, Um, Ul, 1] per record (columns 2d .. 2d+3).
+  static __device__ __forceinline__ void pack_tile(float* base, long r, int KP, double hat,
+                                                   const float*, double w, double L, int d) {
+    float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
+    const int rl = (int)(r % TC_TILE);
+    const double s2 = *reinterpret_cast<const double*>(tile + tc_tile_index(rl, 2 * d + 8));
+    const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
+    const float uh = tf32_hi((float)u);
+    const double u1 = u - (double)uh;
+    const float um = tf32_hi((float)u1);
+    *reinterpret_cast<float4*>(tile + tc_tile_index(rl, 2 * d)) =
+        make_float4(uh, um, (float)(u1 - (double)um), 1.f);
   }
 };
+
+__global__ void tc_init_static(float* rec, long rec_bstride, const float* pts, int batch, int n,
+                               int d, int KP, double L) {
+  const long total = (long)batch * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / n);
+    const long r = i - (long)b * n;
+    SqE32TC::init_tile(rec + (long)b * rec_bstride, r, KP, pts + i * d, L, d);
+  }
+}
 
 // Record layout of a side: `rw` elements per index, or the tiled layout.
 template <class P>
@@ -1198,6 +1220,12 @@ struct Engine {
                                          tc_kp(d.d));
       tc_fill_dead<<<1024, 256, 0, st>>>(bf.recB, (long)d.batch * s.recB / tc_kp(d.d), d.d,
                                          tc_kp(d.d));
+      // same fp32-rounded L as the tails' record packing
+      const double Lr = (double)(float)(1.0 / (d.eps * Dom<float>::unit));
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x, d.batch, d.n, d.d,
+                                           tc_kp(d.d), Lr);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y, d.batch, d.m, d.d,
+                                           tc_kp(d.d), Lr);
       UOT_CHECK_LAUNCH();
     }
     const long nm = std::max(d.n, d.m);

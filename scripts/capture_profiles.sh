@@ -1,0 +1,21 @@
+#!/bin/bash
+# Round-end ncu evidence for the secondary configs (run on the GPU box under
+# gpurun; each command first runs once without ncu).  Outputs go to
+# gpurun_out/prof_*; scripts/summarize_ncu.py turns them into profiles/*.md.
+set -x
+O=gpurun_out
+# cfg2 FW: 296 problems (2 waves of 148 SMs x 2 CTAs... one per resident slot) x 20 iterations
+timeout 300 python scripts/prof_fw.py 296 20 linesearch && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_fw_launches.csv python scripts/prof_fw.py 296 20 linesearch > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fw1d_kernel -c 1 -o $O/prof_fw_full python scripts/prof_fw.py 296 20 linesearch > /dev/null 2>&1
+# cfg5 barycenter: all 64 problems, 3 iterations
+timeout 300 python scripts/prof_bary.py 64 3 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_bary_launches.csv python scripts/prof_bary.py 64 3 > /dev/null 2>&1
+for k in mot_update mot_bucket mot_split; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $O/prof_bary_$k python scripts/prof_bary.py 64 3 > /dev/null 2>&1
+done
+# cfg4: 64 of the 256 problems
+timeout 300 python scripts/perf_cfg4.py 64 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_c4_launches.csv python scripts/perf_cfg4.py 64 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sk_main_tc -s 2 -c 1 -o $O/prof_c4_full python scripts/perf_cfg4.py 64 > /dev/null 2>&1
+ls -la $O
