@@ -25,6 +25,11 @@ int uot_probe_mufu_ex2(void* stream, double* ex2_per_s);
  * A from TMEM, B from shared memory); device pointers, row-major. */
 int uot_tc_selftest(const float* A, const float* B, int K, float* D, void* stream);
 
+/* CTA-pair check: D[256x128] = A[256xK] * B[128xK]^T with
+ * tcgen05.mma.cta_group::2 on a cluster of two CTAs (A rows and B rows split
+ * between the pair's TMEM / shared memory). */
+int uot_tc_selftest2(const float* A, const float* B, int K, float* D, void* stream);
+
 /* tcgen05 issue-rate probe: each of `ctas` CTAs issues `reps` back-to-back
  * 128 x n x 8 kind::tf32 MMAs (A from TMEM if ss == 0, else shared memory)
  * and adds its clock64 cycle count to *out_dev (device pointer). */

@@ -235,15 +235,15 @@ struct SqE32TC {
     for (int k = 0; k < d; ++k) {
       const float x = (float)(2.0 * L * (double)pt[k]);
       const float xh = tf32_hi(x);
-      tile[tc_tile_index(rl, k)] = xh;
-      tile[tc_tile_index(rl, d + k)] = x - xh;
+      tile[tc_tile_index(rl, k, KP)] = xh;
+      tile[tc_tile_index(rl, d + k, KP)] = x - xh;
       s2 += (double)pt[k] * (double)pt[k];
     }
-    tile[tc_tile_index(rl, 2 * d + 3)] = 1.f;
-    tile[tc_tile_index(rl, 2 * d + 4)] = 1.f;
-    tile[tc_tile_index(rl, 2 * d + 5)] = 1.f;
-    for (int k = 2 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k)] = 0.f;
-    *reinterpret_cast<double*>(tile + tc_tile_index(rl, 2 * d + 8)) = s2;
+    tile[tc_tile_index(rl, 2 * d + 3, KP)] = 1.f;
+    tile[tc_tile_index(rl, 2 * d + 4, KP)] = 1.f;
+    tile[tc_tile_index(rl, 2 * d + 5, KP)] = 1.f;
+    for (int k = 2 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k, KP)] = 0.f;
+    *reinterpret_cast<double*>(tile + tc_tile_index(rl, 2 * d + 8, KP)) = s2;
   }
   // Per half-step: only U = (hat - |x|^2) L + log2 w changes -- one 16-byte
   // store [Uh, Um, Ul, 1] per record (columns 2d .. 2d+3).
@@ -251,12 +251,12 @@ struct SqE32TC {
                                                    const float*, double w, double L, int d) {
     float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
     const int rl = (int)(r % TC_TILE);
-    const double s2 = *reinterpret_cast<const double*>(tile + tc_tile_index(rl, 2 * d + 8));
+    const double s2 = *reinterpret_cast<const double*>(tile + tc_tile_index(rl, 2 * d + 8, KP));
     const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
     const float uh = tf32_hi((float)u);
     const double u1 = u - (double)uh;
     const float um = tf32_hi((float)u1);
-    *reinterpret_cast<float4*>(tile + tc_tile_index(rl, 2 * d)) =
+    *reinterpret_cast<float4*>(tile + tc_tile_index(rl, 2 * d, KP)) =
         make_float4(uh, um, (float)(u1 - (double)um), 1.f);
   }
 };
@@ -1095,7 +1095,19 @@ struct Engine {
       auto go = [&](auto kern) -> int {
         UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)tsm));
-        kern<<<grid, TC_THREADS, tsm, st>>>(a, tc_kp(d.d));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((grid.x + 1) / 2 * 2, grid.y, grid.z);  // whole CTA pairs
+        cfg.blockDim = dim3(TC_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = tsm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        UOT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, tc_kp(d.d)));
         return UOT_OK;
       };
       int rc;
@@ -1598,14 +1610,3 @@ extern "C" int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* works
   });
 }
 
-#ifdef UOT_TC_PROF
-extern "C" int uot_tc_prof(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, uot::g_tc_prof, sizeof(unsigned long long) * 8) != cudaSuccess)
-    return 4;
-  if (reset) {
-    unsigned long long z[8] = {0};
-    cudaMemcpyToSymbol(uot::g_tc_prof, z, sizeof(z));
-  }
-  return 0;
-}
-#endif

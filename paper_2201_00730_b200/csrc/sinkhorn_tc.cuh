@@ -1,5 +1,5 @@
 // sinkhorn_tc.cuh -- tensor-core half-step for squared-Euclidean costs on
-// d >= 32 feature vectors (BASELINE cfg4), sm_100a tcgen05.
+// d >= 32 feature vectors (BASELINE cfg4), sm_100a tcgen05, CTA pairs.
 //
 // The exponent of every pair, t_or = z_or - m_o (log2 units), is produced by
 // kind::tf32 MMAs with split-precision compensation and the row / column
@@ -12,11 +12,18 @@
 // Yh.Xl, so the 3xTF32 product Yh.Xh + Yl.Xh + Yh.Xl + U + c reproduces the
 // fp32 exponent to ~2^-21 while B carries each X value only twice
 // (TF32 alone would miss the 1e-4 eps tolerance).
-// Warp roles: warp 0 streams B stages with 1-D bulk copies (the tail kernel
-// writes B directly in the canonical K-major core-matrix layout), warp 1
-// issues tcgen05.mma from one thread into a double-buffered TMEM
-// accumulator, warps 2-5 read D with tcgen05.ld and run the exp2 / sum
-// epilogue on the MUFU pipe while the next tile is multiplied.
+//
+// CTA pairs (cta_group::2, M = 256): a cluster of two CTAs covers 256 output
+// rows; each CTA keeps its 128 A rows in its own TMEM and streams only HALF
+// of every B tile (64 of the 128 reduced rows) into its shared memory -- the
+// leader's MMA reads both halves, so each SM ingests half the B bytes (the
+// single-CTA version was bound by ~28 B/clk/SM of bulk-copy ingestion).
+// Warp roles: warp 0 streams this CTA's B halves with 1-D bulk copies; in the
+// leader, warp 1 issues tcgen05.mma.cta_group::2 from one thread into a
+// double-buffered TMEM accumulator (commits multicast to both CTAs); in the
+// peer, warp 1 relays "my half landed" to the leader's barrier; warps 2-5 of
+// both CTAs read their 128 accumulator rows with tcgen05.ld and run the
+// exp2 / sum epilogue on the MUFU pipe while the next tile is multiplied.
 #pragma once
 
 #include "sinkhorn.cuh"
@@ -24,17 +31,18 @@
 
 namespace uot {
 
-constexpr int TC_TILE = 128;        // M (outputs) and N (reduced) per MMA tile
+constexpr int TC_TILE = 128;        // outputs per CTA and reduced rows per B tile
+constexpr int TC_HALF = 64;         // reduced rows per CTA per B tile
 #ifndef UOT_TC_STAGE_K
 #define UOT_TC_STAGE_K 16
 #endif
 constexpr int TC_STAGE_K = UOT_TC_STAGE_K;  // K elements per shared-memory stage
 #ifndef UOT_TC_STAGES
-#define UOT_TC_STAGES 12
+#define UOT_TC_STAGES 24
 #endif
-constexpr int TC_STAGES = UOT_TC_STAGES;  // B-operand ring depth (bytes in flight hide L2 latency)
+constexpr int TC_STAGES = UOT_TC_STAGES;  // B-operand ring depth
 constexpr int TC_THREADS = 192;
-constexpr int TC_STAGE_BYTES = TC_TILE * TC_STAGE_K * 4;  // 8 KiB
+constexpr int TC_STAGE_BYTES = TC_HALF * TC_STAGE_K * 4;  // 4 KiB: one CTA's half stage
 
 // Output-side point tile staged in shared memory for the A prologue: 128
 // rows of d floats, row stride d + 4 (conflict-free float4 row reads).
@@ -51,73 +59,63 @@ __host__ __device__ constexpr int tc_ka(int d) { return 2 * d + 8; }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
 
-// Index of element (row rl, column k) inside one canonical 128-row tile.
-__device__ __forceinline__ long tc_tile_index(int rl, int k) {
-  return (long)(k >> 2) * (16 * 32) + (rl >> 3) * 32 + (rl & 7) * 4 + (k & 3);
+// Index of element (row rl, column k) inside one 128-row record tile: two
+// 64-row halves, each in the canonical K-major no-swizzle core-matrix layout
+// ([k/4][row/8][row%8][k%4]; LBO = 1024 B between K groups, SBO = 128 B
+// between 8-row groups), so a CTA's half of a stage is one contiguous copy.
+__device__ __forceinline__ long tc_tile_index(int rl, int k, int KP) {
+  return (long)(rl >> 6) * (TC_HALF * KP) + (long)(k >> 2) * (8 * 32) + ((rl >> 3) & 7) * 32 +
+         (rl & 7) * 4 + (k & 3);
 }
 
-#ifdef UOT_TC_PROF
-// Debug instrumentation (-DUOT_TC_PROF): cycles spent in each wait, summed
-// over CTAs: [0] producer empty, [1] MMA full, [2] MMA dempty, [3] epilogue
-// dfull, [4] prologue, [5] total, [6] epilogue math, [7] MMA issue loop.
-__device__ unsigned long long g_tc_prof[8];
-#define TCP_T0() const long long _tcp0 = clock64()
-#define TCP_ADD(i) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - _tcp0))
-#else
-#define TCP_T0()
-#define TCP_ADD(i)
-#endif
-
-// One K-slice (8 columns of B) of a column tile: the MMAs it feeds.  B
-// row = [Xh(d), Xl(d), Uh, Um, Ul, 1, 1, 1, 0..]; A row = [Yh(d), Yl(d), 1,
-// 1, 1, ch, cm, cl]: Xh slices meet Yh and Yl, Xl slices meet Yh, the last
-// slice meets the constants (3xTF32 split of 2L x.y + U + c).
+// One K-slice (8 columns of B) of a column tile: the MMAs it feeds.  Xh
+// slices meet Yh and Yl, Xl slices meet Yh, the last slice meets the
+// constants (3xTF32 split of 2L x.y + U + c).
 __device__ __forceinline__ void tc_slice_mmas(int kb, int d, uint32_t dcol, uint32_t tbase,
                                               uint64_t bd, uint32_t idesc, bool& first) {
   if (kb < d) {
-    tc::mma_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
-    tc::mma_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
+    tc::mma2_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
+    tc::mma2_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
     first = false;
   } else if (kb < 2 * d) {
-    tc::mma_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
+    tc::mma2_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
     first = false;
   } else if (kb < 2 * d + 8) {
-    tc::mma_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
+    tc::mma2_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
     first = false;
   }
 }
 
-// DT > 0: the feature dimension is a compile-time constant, so the MMA
-// issue sequence of a column tile is fully unrolled and branch-free (the
-// single issuing thread is otherwise the bottleneck: a tight tcgen05.mma
-// stream runs at the 64-cycle floor of a 128x128x8 tf32 MMA, the generic
-// loop at ~96+).  DT = 0: runtime d.
+// DT > 0: the feature dimension is a compile-time constant, so the MMA issue
+// sequence of a column tile is fully unrolled and branch-free (a tight
+// tcgen05.mma stream runs at its floor; a generic loop issue-bound).
+// DT = 0: runtime d.  Launched with cluster dims (2, 1, 1) over row tiles.
 template <int DT>
 __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, int KP) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], dfull[2], dempty[2];
+  __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], peer_b[TC_STAGES], dfull[2], dempty[2];
   __shared__ uint32_t tbase_s;
   const int b = blockIdx.z;
-  if (A.done != nullptr && A.done[b]) return;
+  if (A.done != nullptr && A.done[b]) return;  // uniform over the pair (same b)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
   const int split = blockIdx.y, S = gridDim.y;
   const int ntiles = (A.nred + TC_TILE - 1) / TC_TILE;
   const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
   const int nst = DT > 0 ? tc_kp(DT) / TC_STAGE_K : KP / TC_STAGE_K;
   const int d = DT > 0 ? DT : A.g.d;
 
-#ifdef UOT_TC_PROF
-  const long long _tstart = clock64();
-#endif
-  if (warp == 1) tc::tmem_alloc(&tbase_s, 512);
+  if (warp == 1) tc::tmem_alloc2(&tbase_s, 512);
   if (tid == 0) {
     for (int i = 0; i < TC_STAGES; ++i) {
       tc::mbar_init(&full_b[i], 1);
-      tc::mbar_init(&empty_b[i], 1);
+      tc::mbar_init(&empty_b[i], 1);  // one multicast commit per use
+      tc::mbar_init(&peer_b[i], 1);   // leader: the peer's half landed
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&dfull[i], 1);
-      tc::mbar_init(&dempty[i], 128);
+      tc::mbar_init(&dempty[i], 8);  // leader: one arrive per epilogue warp of the pair
     }
     tc::mbar_fence_init();
   }
@@ -170,16 +168,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
     // Yh at columns [0, d), Yl at [d, 2d): 8 columns per store
     for (int k0 = 0; k0 < d; k0 += 8) {
-      const float4 u0 = *reinterpret_cast<const float4*>(y + k0);
-      const float4 u1 = *reinterpret_cast<const float4*>(y + k0 + 4);
-      const float yv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      float yv[8];
+      if (o < A.nout) {
+        const float4 u0 = *reinterpret_cast<const float4*>(y + k0);
+        const float4 u1 = *reinterpret_cast<const float4*>(y + k0 + 4);
+        yv[0] = u0.x, yv[1] = u0.y, yv[2] = u0.z, yv[3] = u0.w;
+        yv[4] = u1.x, yv[5] = u1.y, yv[6] = u1.z, yv[7] = u1.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) yv[e] = 0.f;
+      }
       uint32_t vh[8], vl[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float yk = o < A.nout ? yv[e] : 0.f;
-        const float yh = tf32_hi(yk);
+        const float yh = tf32_hi(yv[e]);
         vh[e] = __float_as_uint(yh);
-        vl[e] = __float_as_uint(yk - yh);
+        vl[e] = __float_as_uint(yv[e] - yh);
       }
       tc::tmem_st8(ta + k0, vh);
       tc::tmem_st8(ta + d + k0, vl);
@@ -192,28 +196,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     }
     tc::wait_st();
   }
+  // both CTAs' A rows and barriers ready before any MMA / remote arrive
   tc::fence_before();
-  __syncthreads();
+  tc::cluster_sync_all();
   tc::fence_after();
-#ifdef UOT_TC_PROF
-  if (tid == 0) atomicAdd(&g_tc_prof[4], (unsigned long long)(clock64() - _tstart));
-#endif
 
   const float* recb = A.g.red_rec + b * A.g.red_bstride;
   if (warp == 0) {
-    if (tc::elect_one()) {  // producer: B stages
+    if (tc::elect_one()) {  // producer: this CTA's halves of the B stages
       int slot = 0;
       uint32_t phase = 0;
       for (int tile = t0; tile < t1; ++tile) {
+        const float* src = recb + (long)tile * TC_TILE * KP + (long)rank * TC_HALF * KP;
         for (int st = 0; st < nst; ++st) {
-          {
-            TCP_T0();
-            tc::mbar_wait(&empty_b[slot], phase ^ 1);
-            TCP_ADD(0);
-          }
+          tc::mbar_wait(&empty_b[slot], phase ^ 1);
           tc::mbar_expect_tx(&full_b[slot], TC_STAGE_BYTES);
-          tc::bulk_g2s(smem + slot * TC_STAGE_BYTES,
-                       recb + (long)tile * TC_TILE * KP + (long)st * TC_TILE * TC_STAGE_K,
+          tc::bulk_g2s(smem + slot * TC_STAGE_BYTES, src + (long)st * TC_HALF * TC_STAGE_K,
                        TC_STAGE_BYTES, &full_b[slot]);
           if (++slot == TC_STAGES) {
             slot = 0;
@@ -223,59 +221,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       }
     }
   } else if (warp == 1) {
-    if (tc::elect_one()) {  // MMA issuer
-      const uint32_t idesc = tc::idesc_tf32(TC_TILE, TC_TILE);
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int i = 0; i < t1 - t0; ++i) {
-        const int buf = i & 1;
-        const uint32_t dph = (i >> 1) & 1;
-        {
-          TCP_T0();
-          tc::mbar_wait(&dempty[buf], dph ^ 1);
-          TCP_ADD(2);
-        }
-        tc::fence_after();
-        const uint32_t dcol = tbase + 256 + buf * TC_TILE;
-        bool first = true;
-        // shared-memory descriptor of slot 0; other slots / slices add their
-        // byte offset >> 4 to the start-address field (addresses < 256 KiB)
-        const uint64_t bd0 = tc::sdesc(smem, 2048, 128);
-        constexpr int NST = DT > 0 ? tc_kp(DT) / TC_STAGE_K : 1;
-#pragma unroll
-        for (int stu = 0; stu < (DT > 0 ? NST : 1); ++stu) {
-          for (int str = 0; str < (DT > 0 ? 1 : nst); ++str) {
-            const int st = DT > 0 ? stu : str;
-            {
-              TCP_T0();
-              tc::mbar_wait(&full_b[slot], phase);
-              TCP_ADD(1);
-            }
-            tc::fence_after();
-            const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
-#ifdef UOT_TC_NOMMA  // experiment: B feed alone
-            tc::mbar_arrive(&empty_b[slot]);
-            (void)bds;
-#else
-#pragma unroll
-            for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
-              const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
-              tc_slice_mmas(kb, d, dcol, tbase, bds + (uint64_t)((ks * 2 * 2048) >> 4), idesc,
-                            first);
-            }
-            tc::mma_commit(&empty_b[slot]);
-#endif
-            if (++slot == TC_STAGES) {
-              slot = 0;
-              phase ^= 1;
-            }
+    if (tc::elect_one()) {
+      const int nstage = (t1 - t0) * nst;
+      if (!leader) {
+        // relay: my half of stage s landed -> the leader's peer barrier
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int s = 0; s < nstage; ++s) {
+          tc::mbar_wait(&full_b[slot], phase);
+          tc::mbar_arrive_remote_relaxed(tc::mapa(&peer_b[slot], 0));
+          if (++slot == TC_STAGES) {
+            slot = 0;
+            phase ^= 1;
           }
         }
-#ifdef UOT_TC_NOMMA
-        tc::mbar_arrive(&dfull[buf]);
-#else
-        tc::mma_commit(&dfull[buf]);
-#endif
+      } else {  // MMA issuer for the pair
+        const uint32_t idesc = tc::idesc_tf32(2 * TC_TILE, TC_TILE);
+        int slot = 0;
+        uint32_t phase = 0;
+        // descriptor of slot 0; other slots / slices add byte offset >> 4
+        const uint64_t bd0 = tc::sdesc(smem, (TC_HALF / 8) * 128, 128);
+        for (int i = 0; i < t1 - t0; ++i) {
+          const int buf = i & 1;
+          const uint32_t dph = (i >> 1) & 1;
+          tc::mbar_wait(&dempty[buf], dph ^ 1);
+          tc::fence_after();
+          const uint32_t dcol = tbase + 256 + buf * TC_TILE;
+          bool first = true;
+          constexpr int NST = DT > 0 ? tc_kp(DT) / TC_STAGE_K : 1;
+#pragma unroll
+          for (int stu = 0; stu < (DT > 0 ? NST : 1); ++stu) {
+            for (int str = 0; str < (DT > 0 ? 1 : nst); ++str) {
+              const int st = DT > 0 ? stu : str;
+              tc::mbar_wait(&full_b[slot], phase);
+              tc::mbar_wait(&peer_b[slot], phase);
+              tc::fence_after();
+              const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
+#pragma unroll
+              for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
+                const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
+                tc_slice_mmas(kb, d, dcol, tbase,
+                              bds + (uint64_t)((ks * 2 * (TC_HALF / 8) * 128) >> 4), idesc, first);
+              }
+              tc::mma2_commit_mc(&empty_b[slot], 3);
+              if (++slot == TC_STAGES) {
+                slot = 0;
+                phase ^= 1;
+              }
+            }
+          }
+          tc::mma2_commit_mc(&dfull[buf], 3);
+        }
       }
     }
     __syncwarp();
@@ -283,24 +279,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     // Epilogue: exp2 + sum of each accumulator row, range-checked per tile.
     float acc = 0.f, corr = 0.f;
     const uint32_t tl = tbase + ((uint32_t)lane_base << 16);
+    const uint32_t dempty_leader0 = tc::mapa(&dempty[0], 0);
+    const uint32_t dempty_leader1 = tc::mapa(&dempty[1], 0);
     for (int i = 0; i < t1 - t0; ++i) {
       const int buf = i & 1;
       const uint32_t dph = (i >> 1) & 1;
-      {
-        TCP_T0();
-        tc::mbar_wait(&dfull[buf], dph);
-        if (lane == 0) TCP_ADD(3);
-      }
+      tc::mbar_wait(&dfull[buf], dph);
       tc::fence_after();
       const uint32_t dcol = tl + 256 + buf * TC_TILE;
-      float s = 0.f;
+      uint32_t v0[32], v1[32], v2[32], v3[32];
+      tc::tmem_ld32(dcol, v0);
+      tc::tmem_ld32(dcol + 32, v1);
+      tc::tmem_ld32(dcol + 64, v2);
+      tc::tmem_ld32(dcol + 96, v3);
+      tc::wait_ld();
+      // The accumulator is in registers (wait::ld completed): hand the buffer
+      // back to the MMA issuer.  No TMEM read is outstanding, so a relaxed
+      // arrive suffices (a release.cluster arrive per warp and tile costs
+      // ~1.5x the kernel time).
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_remote_relaxed(buf ? dempty_leader1 : dempty_leader0);
+      float s;
       {
-        uint32_t v0[32], v1[32], v2[32], v3[32];
-        tc::tmem_ld32(dcol, v0);
-        tc::tmem_ld32(dcol + 32, v1);
-        tc::tmem_ld32(dcol + 64, v2);
-        tc::tmem_ld32(dcol + 96, v3);
-        tc::wait_ld();
         float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
         if (__all_sync(0xffffffffu, corr == 0.f)) {
 #pragma unroll
@@ -325,11 +326,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       if (!(na < 1.2676506e30f && na > 7.8886091e-31f)) {
         // Rare: the stale shift is off by > 2^100 -- rescale from this tile's max.
         float mx = -INFINITY;
-        for (int c = 0; c < TC_TILE / 32; ++c) {
-          uint32_t v[32];
-          tc::tmem_ld32(dcol + c * 32, v);
-          tc::wait_ld();
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) + corr);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          mx = fmaxf(mx, __uint_as_float(v0[e]) + corr);
+          mx = fmaxf(mx, __uint_as_float(v1[e]) + corr);
+          mx = fmaxf(mx, __uint_as_float(v2[e]) + corr);
+          mx = fmaxf(mx, __uint_as_float(v3[e]) + corr);
         }
         float mn = mx;
         if (acc > 0.f) mn = fmaxf(mn, Dom<float>::lg(acc));
@@ -338,17 +340,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
           corr -= mn;
         }
         s = 0.f;
-        for (int c = 0; c < TC_TILE / 32; ++c) {
-          uint32_t v[32];
-          tc::tmem_ld32(dcol + c * 32, v);
-          tc::wait_ld();
-          for (int e = 0; e < 32; ++e) s += Dom<float>::ex(__uint_as_float(v[e]) + corr);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          s += Dom<float>::ex(__uint_as_float(v0[e]) + corr);
+          s += Dom<float>::ex(__uint_as_float(v1[e]) + corr);
+          s += Dom<float>::ex(__uint_as_float(v2[e]) + corr);
+          s += Dom<float>::ex(__uint_as_float(v3[e]) + corr);
         }
         na = acc + s;
       }
       acc = na;
-      tc::fence_before();
-      tc::mbar_arrive(&dempty[buf]);
     }
     if (o < A.nout) {
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
@@ -357,11 +358,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     }
   }
   tc::fence_before();
-  __syncthreads();
-#ifdef UOT_TC_PROF
-  if (tid == 0) atomicAdd(&g_tc_prof[5], (unsigned long long)(clock64() - _tstart));
-#endif
-  if (warp == 1) tc::tmem_free(tbase, 512);
+  tc::cluster_sync_all();  // both CTAs done with TMEM and remote barriers
+  if (warp == 1) tc::tmem_free2(tbase, 512);
 }
 
 // Dead-row fill of a canonical record buffer: every row gets U = -1e30
@@ -373,7 +371,8 @@ __global__ void tc_fill_dead(float* buf, long nrows_padded, int d, int KP) {
        idx += (long)gridDim.x * blockDim.x) {
     const long tile = idx / ((long)TC_TILE * KP);
     const long rem = idx % ((long)TC_TILE * KP);
-    const int k = (int)(rem / (16 * 32)) * 4 + (int)(rem % 4);
+    const long r2 = rem % ((long)TC_HALF * KP);  // within a 64-row half
+    const int k = (int)(r2 / (8 * 32)) * 4 + (int)(r2 % 4);
     float v = 0.f;
     if (k == 2 * d) v = -1e30f;
     else if (k >= 2 * d + 3 && k < 2 * d + 6) v = 1.f;

@@ -32,3 +32,22 @@ def test_tc_selftest_tile(K):
     got = D.to_np(d)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
     np.testing.assert_allclose(got, ref, rtol=0, atol=2e-5 * np.sqrt(K))
+
+
+@pytest.mark.parametrize("K", [8, 64, 144])
+def test_tc_selftest_pair(K):
+    """cta_group::2: A rows split across the pair's TMEM, B rows across its smem."""
+    import torch
+
+    lib = _lib.load()
+    rng = np.random.default_rng(100 + K)
+    A = _tf32(rng.standard_normal((256, K)))
+    B = _tf32(rng.standard_normal((128, K)))
+    a = torch.as_tensor(A, device="cuda")
+    b = torch.as_tensor(B, device="cuda")
+    d = torch.zeros((256, 128), dtype=torch.float32, device="cuda")
+    _lib.check(lib.uot_tc_selftest2(_lib.ptr(a), _lib.ptr(b), K, _lib.ptr(d),
+                                    _lib.stream_handle()))
+    got = D.to_np(d)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    np.testing.assert_allclose(got, ref, rtol=0, atol=2e-5 * np.sqrt(K))
