@@ -47,7 +47,7 @@ enum { UOT_SINKHORN_F = 0, UOT_SINKHORN_H = 1 };
  * points (src/measures.py:93-105 PowerDistance); dense explicit matrix
  * (src/measures.py:108-122 ExplicitMatrix). */
 enum { UOT_COST_SQEUCLID = 0, UOT_COST_POWER = 1, UOT_COST_EXPLICIT = 2 };
-enum { UOT_STEP_HARMONIC = 0, UOT_STEP_LINESEARCH = 1 };
+enum { UOT_STEP_HARMONIC = 0, UOT_STEP_LINESEARCH = 1, UOT_STEP_PAIRWISE = 2 };
 
 /* Library identity / diagnostics. */
 const char* uot_version(void);
@@ -144,6 +144,10 @@ int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const
  * dual / lambda* in summary [batch][3]; status [batch] (1 = reweighted
  * masses disagree, fw.py:161-166).  With early_exit != 0 a problem stops at
  * the first pd_gap < gap_tol (fw.py:220-222).
+ * step = UOT_STEP_PAIRWISE runs pairwise FW (src/fw.py:255-357): an atom
+ * store of up to max_iters + 1 dual-pair atoms per problem lives in the
+ * workspace; natoms (optional [batch][max_iters]) receives the active atom
+ * count after each iteration and step_size the weight transferred.
  * n, m <= 4096 per problem (one CTA per problem, state resident on chip).
  * ------------------------------------------------------------------------ */
 typedef struct uot_fw_desc {
@@ -171,6 +175,7 @@ typedef struct uot_fw_desc {
   double* summary;
   int32_t* status;
   double* step_size; /* optional [batch][max_iters]: gamma of each iteration */
+  int32_t* natoms;   /* optional [batch][max_iters]: active atoms (pairwise) */
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);

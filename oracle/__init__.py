@@ -380,6 +380,81 @@ def fw_fixed(x, y, aw, bw, r1, r2, iters, step="linesearch", p=2.0, f0=None, g0=
     }
 
 
+ATOM_DEDUP_TOL = 1e-12
+
+
+def pfw_fixed(x, y, aw, bw, r1, r2, iters, p=2.0, gap_tol=None):
+    """Pairwise FW, fw.py:255-357 (_active_scores :255-257, _merge_atom
+    :260-272, _pfw_iteration :275-310, _pfw_solve :326-357) on the same LMO.
+
+    The atom store holds dual-pair atoms with convex weights; the iterate is
+    the weighted atom.  Each iteration: LMO at the iterate, away atom =
+    argmin over active atoms of <r_a, ta> + <s_a, tb> (lowest index on
+    ties), ternary line search of H0 along (new - away) on [0, w_away],
+    weight transfer, merge of the new atom into an existing one closer than
+    1e-12 (sup norm), drop of zero-weight atoms.  ``gap_tol=None`` removes
+    the early exit (:351-353).  Returns the dict of ``fw_fixed`` plus the
+    step sizes and atom counts."""
+    x, y, aw, bw = _c64(x), _c64(y), _c64(aw), _c64(bw)
+    R = np.zeros((1, aw.size))
+    Sg = np.zeros((1, bw.size))
+    W = np.array([1.0])
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap", "gamma", "natoms")}
+    plan = None
+    converged = False
+    for t in range(iters):
+        f, g = W @ R, W @ Sg
+        lam = lambda_star_kl(aw, bw, f, g, r1, r2)
+        with np.errstate(over="ignore"):
+            ta = aw * np.exp((-f - lam) / r1)
+            tb = bw * np.exp((-g + lam) / r2)
+        ma, mb = float(ta.sum()), float(tb.sum())
+        if abs(ma - mb) > LMO_MASS_TOL * max(ma, mb):
+            raise ValueError("reweighted marginal masses disagree")
+        ii, jj, mm, r, s = solve_ot_1d(x, y, ta, tb, p)
+        plan = (ii, jj, mm)
+        fw_gap = float(np.dot(ta, r - f) + np.dot(tb, s - g))
+        dual = h0_kl(aw, bw, f, g, r1, r2)
+        primal = eval_primal_1d(x, y, aw, bw, ii, jj, mm, p, r1, r2)
+        tr["h0"].append(dual)
+        tr["fw_gap"].append(fw_gap)
+        tr["pd_gap"].append(primal - dual)
+        scores = np.where(W > 0, R @ ta + Sg @ tb, np.inf)
+        away = int(np.argmin(scores))
+        max_step = float(W[away])
+        dr, ds = r - R[away], s - Sg[away]
+        gam = 0.0
+        if not (max_step <= 0.0 or (np.abs(dr).max() < ATOM_DEDUP_TOL
+                                     and np.abs(ds).max() < ATOM_DEDUP_TOL)):
+            def value(gg):
+                return h0_kl(aw, bw, f + gg * dr, g + gg * ds, r1, r2)
+
+            gam = ternary_max(value, 0.0, max_step, iters=60)
+            gam = max(((value(c), c) for c in (gam, 0.0, max_step)), key=lambda q: q[0])[1]
+            if gam > 0.0:
+                W = W.copy()
+                W[away] = max(W[away] - gam, 0.0)
+                dist = np.maximum(np.abs(R - r).max(axis=1), np.abs(Sg - s).max(axis=1))
+                hit = np.nonzero(dist < ATOM_DEDUP_TOL)[0]
+                if hit.size:
+                    W[hit[0]] += gam
+                else:
+                    R, Sg, W = np.vstack([R, r]), np.vstack([Sg, s]), np.concatenate([W, [gam]])
+                keep = W > 0
+                R, Sg, W = R[keep], Sg[keep], W[keep]
+        tr["gamma"].append(gam)
+        tr["natoms"].append(W.size)
+        if gap_tol is not None and primal - dual < gap_tol:
+            converged = True
+            break
+    f, g = W @ R, W @ Sg
+    lam = lambda_star_kl(aw, bw, f, g, r1, r2)
+    return {
+        "f": f + lam, "g": g - lam, "f_raw": f, "g_raw": g, "plan": plan,
+        "converged": converged, **{k: np.asarray(v) for k, v in tr.items()},
+    }
+
+
 # ---------------------------------------------------------------------------
 # barycenter.py
 

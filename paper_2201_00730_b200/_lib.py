@@ -19,7 +19,7 @@ UOT_OK = 0
 F32, F64 = 0, 1
 SINKHORN_F, SINKHORN_H = 0, 1
 COST_SQEUCLID, COST_POWER, COST_EXPLICIT = 0, 1, 2
-STEP_HARMONIC, STEP_LINESEARCH = 0, 1
+STEP_HARMONIC, STEP_LINESEARCH, STEP_PAIRWISE = 0, 1, 2
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -47,7 +47,7 @@ class FwDesc(ctypes.Structure):
         ("x", _vp), ("y", _vp), ("a", _vp), ("b", _vp), ("f", _vp), ("g", _vp),
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),
         ("ei", _vp), ("ej", _vp), ("em", _vp), ("count", _vp), ("summary", _vp),
-        ("status", _vp), ("step_size", _vp),
+        ("status", _vp), ("step_size", _vp), ("natoms", _vp),
     ]
 
 

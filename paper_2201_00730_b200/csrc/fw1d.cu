@@ -61,6 +61,14 @@ struct FwArgs {
   double* step_size;
   double* scratch;  // [batch][n+m] doubles + [batch][n+m][2] ints (plan extraction)
   int* scratch_i;
+  // pairwise FW atom store (fw.py:70-95), cap = max_iters + 1 slots per problem
+  int cap;
+  double* atoms;  // [batch][cap][n+m] (r | s) rows
+  double* wts;    // [batch][cap] weight of each slot
+  int* act;       // [batch][cap] active slots in insertion order
+  double* scs;    // [batch][cap] scores of the active atoms (per position)
+  double* dis;    // [batch][cap] sup-norm distance to the new atom
+  int* natoms;    // optional [batch][max_iters] trace
 };
 
 __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
@@ -132,6 +140,7 @@ struct Cta {
   unsigned short* rkB;  // rkB[l] = #source events before target event l
   double* zred;  // scratch of the zero-weight fix (own syncs)
   bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
+  double* pfw;   // pairwise FW staging (n + m doubles) or nullptr
 
   __device__ int src(int e) const { return threadIdx.x * EPT + e; }
 
@@ -321,6 +330,220 @@ struct Cta {
   }
 };
 
+// Pairwise FW state shared by all threads of the CTA: active atoms and
+// slots used so far (identical in every thread).
+struct PfwState {
+  int na, ntot;
+};
+
+// One pairwise step (fw.py:275-310) after the LMO of iteration t: scores of
+// the active atoms against the tilted marginals (one warp per atom, coalesced
+// rows from the workspace store) and their sup-norm distance to the new
+// atom (r, s); the away atom = argmin score (lowest position on ties);
+// safeguarded Newton on phi along (r, s) - away over [0, w_away] (fw.py:
+// 295-297 runs a ternary search + endpoint check on the same concave H0);
+// weight transfer, merge into an atom closer than 1e-12 (:260-272), drop of
+// zero weights, and the iterate update d += gamma ((r, s) - away).  Returns
+// gamma.  The shared breakpoint arrays sA / sB are free after the oracle and
+// hold ta / tb here; the new atom is staged after them.
+template <int EPT, int PK, typename PING>
+__device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, double (&f)[EPT],
+                           double (&g)[EPT], const double (&r)[EPT], const double (&s)[EPT],
+                           const double (&ta)[EPT], const double (&tb)[EPT], double mta,
+                           double mtb, double& sha, double& shb, double i1, double i2, double t1,
+                           double t2, const double* sal, const double* sbe, const double* tab,
+                           PING& ping, PfwState& pst) {
+  const int n = c.n, m = c.m, nm = n + m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ta_s = c.sA;  // [n]
+  double* tb_s = c.sB;  // [m]
+  double* nr_s = c.pfw;  // [n] new atom staging (pairwise only)
+  double* ns_s = nr_s + n;  // [m]
+  (void)sal;
+  __shared__ int away_s, hit_s, na_s;
+  __syncthreads();  // sA / sB readers (oracle, plan extraction) are done
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n) {
+      ta_s[i] = ta[e];
+      nr_s[i] = r[e];
+    }
+    if (i < m) {
+      tb_s[i] = tb[e];
+      ns_s[i] = s[e];
+    }
+  }
+  __syncthreads();
+  const long sb0 = (long)b * A.cap;
+  const double* AT = A.atoms + sb0 * nm;
+  for (int pos = warp; pos < pst.na; pos += FW_NW) {
+    const double* row = AT + (long)__ldcg(A.act + sb0 + pos) * nm;
+    double sc = 0.0, dd = 0.0;
+    for (int i = lane; i < nm; i += 32) {
+      const double v = row[i];
+      const bool src = i < n;
+      const double tw = src ? ta_s[i] : tb_s[i - n];
+      const double nv = src ? nr_s[i] : ns_s[i - n];
+      sc = fma(v, tw, sc);
+      dd = bops::dmax(dd, fabs(v - nv));
+    }
+    sc = warp_sum(sc);
+    dd = bops::warp_dmax(dd);
+    if (lane == 0) {
+      A.scs[sb0 + pos] = sc;
+      A.dis[sb0 + pos] = dd;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double best = CUDART_INF;
+    int bp = 0x7fffffff, hp = 0x7fffffff;
+    for (int pos = lane; pos < pst.na; pos += 32) {
+      const double sc = __ldcg(A.scs + sb0 + pos);
+      if (sc < best) {  // positions ascend per lane: first minimum kept
+        best = sc;
+        bp = pos;
+      }
+      if (hp == 0x7fffffff && __ldcg(A.dis + sb0 + pos) < 1e-12) hp = pos;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ob < best || (ob == best && op < bp)) {
+        best = ob;
+        bp = op;
+      }
+      hp = min(hp, __shfl_xor_sync(0xffffffffu, hp, o));
+    }
+    if (lane == 0) {
+      away_s = bp;
+      hit_s = hp == 0x7fffffff ? -1 : hp;
+    }
+  }
+  __syncthreads();
+  const int away = away_s, hit = hit_s;
+  const int aslot = __ldcg(A.act + sb0 + away);
+  const double* ra = AT + (long)aslot * nm;
+  double dA[EPT], dB[EPT];
+  double mom[4] = {0.0, 0.0, 0.0, 0.0};
+  double mxs[4] = {0.0, 0.0, -CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    dA[e] = i < n ? r[e] - ra[i] : 0.0;
+    dB[e] = i < m ? s[e] - ra[n + i] : 0.0;
+    const double va = dA[e] * i1, vb = dB[e] * i2;
+    mom[0] += ta[e] * va;
+    mom[1] += ta[e] * va * va;
+    mom[2] += tb[e] * vb;
+    mom[3] += tb[e] * vb * vb;
+    mxs[0] = bops::dmax(mxs[0], fabs(dA[e]));
+    mxs[1] = bops::dmax(mxs[1], fabs(dB[e]));
+    if (i < n && sal[i] > 0.0) mxs[2] = bops::dmax(mxs[2], -va);
+    if (i < m && sbe[i] > 0.0) mxs[3] = bops::dmax(mxs[3], -vb);
+  }
+  bops::block_red<FW_NW, 4, 4>(mom, mxs, ping.next());
+  const double gmax = __ldcg(A.wts + sb0 + aslot);
+  double gam = 0.0;
+  if (!(gmax <= 0.0 || (mxs[0] < 1e-12 && mxs[1] < 1e-12))) {  // fw.py:291-293
+    // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
+    // on [0, gmax]; centred moments as in the FW line search
+    const double ca = mom[0] / mta, cb = mom[2] / mtb;
+    const double k0 = -(t1 * ca + t2 * cb);
+    const double d2 = t1 * fmax(mom[1] / mta - ca * ca, 0.0) +
+                      t2 * fmax(mom[3] / mtb - cb * cb, 0.0);
+    if (k0 < 0.0) {
+      double lo = 0.0, hi = gmax;
+      gam = (d2 > 0.0) ? fmin(gmax, -k0 / d2) : gmax;
+      for (int it = 0; it < 32; ++it) {
+        const double pha = sha + gam * mxs[2];
+        const double phb = shb + gam * mxs[3];
+        double mm[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const int i = c.src(e);
+          const double va = dA[e] * i1, vb = dB[e] * i2;
+          const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
+          const double wa = bops::wexp(wa0, -f[e] * i1 - gam * va - pha, tab);
+          const double wb = bops::wexp(wb0, -g[e] * i2 - gam * vb - phb, tab);
+          const double xa = va - ca, xb = vb - cb;
+          mm[0] += wa;
+          mm[1] += wa * xa;
+          mm[2] += wa * xa * xa;
+          mm[3] += wb;
+          mm[4] += wb * xb;
+          mm[5] += wb * xb * xb;
+        }
+        bops::block_sum<FW_NW, 6>(mm, ping.next());
+        const double a1 = mm[1] / mm[0], a2 = mm[2] / mm[0];
+        const double b1 = mm[4] / mm[3], b2 = mm[5] / mm[3];
+        const double g1 = k0 - t1 * a1 - t2 * b1;
+        const double g2 = t1 * (a2 - a1 * a1) + t2 * (b2 - b1 * b1);
+        if (g1 < 0.0)
+          lo = gam;
+        else
+          hi = gam;
+        if (gam >= gmax && g1 <= 0.0) {
+          gam = gmax;
+          break;
+        }
+        double nxt = (g2 > 0.0) ? gam - g1 / g2 : 0.5 * (lo + hi);
+        const bool newton = nxt > lo && nxt < hi;
+        if (!newton) nxt = 0.5 * (lo + hi);
+        const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(gmax, gam)) || g1 == 0.0 ||
+                          hi - lo <= 1e-15 * fmax(1.0, gmax);
+        gam = nxt;
+        if (conv) break;
+      }
+    }
+  }
+  if (gam > 0.0) {
+    // the new atom gets a slot unless it merges into an existing one
+    const int nslot = pst.ntot;
+    if (hit < 0) {
+      double* row = A.atoms + (sb0 + nslot) * nm;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        if (i < n) row[i] = r[e];
+        if (i < m) row[n + i] = s[e];
+      }
+    }
+    if (threadIdx.x == 0) {
+      double* w = A.wts + sb0;
+      int* ac = A.act + sb0;
+      w[aslot] = fmax(w[aslot] - gam, 0.0);
+      int na = pst.na;
+      if (hit >= 0) {
+        w[ac[hit]] += gam;
+      } else {
+        w[nslot] = gam;
+        ac[na++] = nslot;
+      }
+      int k = 0;
+      for (int q = 0; q < na; ++q) {
+        const int sl = ac[q];
+        if (w[sl] > 0.0) ac[k++] = sl;
+      }
+      na_s = k;
+    }
+    if (hit < 0) ++pst.ntot;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      f[e] += gam * dA[e];
+      g[e] += gam * dB[e];
+    }
+    if (sha > -CUDART_INF) sha += gam * mxs[2];
+    if (shb > -CUDART_INF) shb += gam * mxs[3];
+    __syncthreads();
+    pst.na = na_s;
+  }
+  if (A.natoms != nullptr && threadIdx.x == 0) A.natoms[(long)b * A.max_iters + t] = pst.na;
+  return gam;
+}
+
 template <int EPT, int PK>
 __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   extern __shared__ __align__(16) double smem[];
@@ -336,7 +559,10 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   double* sbe = sal + n;
   unsigned short* rkA = reinterpret_cast<unsigned short*>(sbe + m);
   unsigned short* rkB = rkA + n;
-  Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false};
+  double* pfwbuf = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(rkB + m) + 15) & ~static_cast<uintptr_t>(15));
+  Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false,
+                 A.step == UOT_STEP_PAIRWISE ? pfwbuf : nullptr};
   bops::Ping<FW_BUF> ping{red, 0};
   bops::load_exp_table(tab);
 
@@ -422,6 +648,21 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
   int status = 0;
   int iters = 0;
   double last_primal = 0.0, last_dual = 0.0;
+  PfwState pst{1, 1};
+  if (A.step == UOT_STEP_PAIRWISE) {  // store = {(f0, g0)} with weight 1 (fw.py:332)
+    double* row = A.atoms + (long)b * A.cap * (n + m);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) row[i] = f[e];
+      if (i < m) row[n + i] = g[e];
+    }
+    if (threadIdx.x == 0) {
+      A.act[(long)b * A.cap] = 0;
+      A.wts[(long)b * A.cap] = 1.0;
+    }
+    __syncthreads();
+  }
   for (int t = 0; t < A.max_iters; ++t) {
     // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303).
     // The exponentials are shared between the log-sum-exps and the tilt.
@@ -517,6 +758,15 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     const bool stop = A.early_exit && pd_gap < A.gap_tol;  // fw.py:220-222
     if (stop || t == A.max_iters - 1) {
       c.extract_plan(vals, codes, ei, ej, em, A.count + b, fmin(mta, mtb));
+    }
+    if (A.step == UOT_STEP_PAIRWISE) {
+      // pairwise: the step of this iteration is taken before the exit test
+      // (fw.py:341-353)
+      const double gam = pfw_step(c, A, b, t, f, g, r, s, ta, tb, mta, mtb, sha, shb, i1, i2, t1,
+                                  t2, sal, sbe, tab, ping, pst);
+      if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
+      if (stop) break;
+      continue;
     }
     if (stop) break;
     // --- step size
@@ -659,8 +909,9 @@ int ept_for(int nm) {
   return -1;
 }
 
-size_t fw_smem(int n, int m) {
-  return sizeof(double) * 3 * (size_t)(n + m) + sizeof(unsigned short) * (size_t)(n + m);
+size_t fw_smem(int n, int m, bool pairwise) {
+  return sizeof(double) * 3 * (size_t)(n + m) + sizeof(unsigned short) * (size_t)(n + m) +
+         (pairwise ? 16 + sizeof(double) * (size_t)(n + m) : 0);
 }
 
 int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
@@ -669,7 +920,11 @@ int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
     set_error("1-D FW / OT kernel supports n, m <= %d per problem", 16 * FW_THREADS);
     return UOT_INVALID;
   }
-  const size_t smem = fw_smem(a.n, a.m);
+  const size_t smem = fw_smem(a.n, a.m, a.mode == 0 && a.step == UOT_STEP_PAIRWISE);
+  if (smem > 227 * 1024) {
+    set_error("pairwise FW keeps n + m <= ~6600 atoms per problem in shared memory");
+    return UOT_INVALID;
+  }
   auto go = [&](auto kern) -> int {
     UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -696,6 +951,20 @@ size_t fw_scratch_bytes(int batch, int n, int m) {
   return (sizeof(double) + 2 * sizeof(int)) * (size_t)batch * (n + m) + 256;
 }
 
+// pairwise atom store: atoms [batch][cap][n+m], wts / scs / dis [batch][cap]
+// doubles, act [batch][cap] ints; cap = max_iters + 1
+size_t pfw_store_bytes(int batch, int n, int m, int max_iters) {
+  const size_t cap = (size_t)max_iters + 1;
+  return sizeof(double) * (size_t)batch * cap * (n + m) +
+         (3 * sizeof(double) + sizeof(int)) * (size_t)batch * cap + 1024;
+}
+
+size_t fw_ws_bytes(const uot_fw_desc* d) {
+  size_t b = fw_scratch_bytes(d->batch, d->n, d->m);
+  if (d->step == UOT_STEP_PAIRWISE) b += pfw_store_bytes(d->batch, d->n, d->m, d->max_iters);
+  return b;
+}
+
 }  // namespace
 }  // namespace uot
 
@@ -706,7 +975,7 @@ extern "C" int uot_fw1d_workspace_size(const uot_fw_desc* d, size_t* bytes) {
     set_error("uot_fw1d_workspace_size: invalid descriptor");
     return UOT_INVALID;
   }
-  *bytes = fw_scratch_bytes(d->batch, d->n, d->m);
+  *bytes = fw_ws_bytes(d);
   return UOT_OK;
 }
 
@@ -719,11 +988,12 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
     set_error("uot_fw1d_run: need rho > 0 and p >= 1");
     return UOT_INVALID;
   }
-  if (d->step != UOT_STEP_HARMONIC && d->step != UOT_STEP_LINESEARCH) {
-    set_error("uot_fw1d_run: step must be harmonic or linesearch");
+  if (d->step != UOT_STEP_HARMONIC && d->step != UOT_STEP_LINESEARCH &&
+      d->step != UOT_STEP_PAIRWISE) {
+    set_error("uot_fw1d_run: step must be harmonic, linesearch or pairwise");
     return UOT_INVALID;
   }
-  if (ws_bytes < fw_scratch_bytes(d->batch, d->n, d->m)) {
+  if (ws_bytes < fw_ws_bytes(d)) {
     set_error("uot_fw1d_run: workspace too small");
     return UOT_INVALID;
   }
@@ -757,6 +1027,19 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.step_size = d->step_size;
   a.scratch = (double*)ws;
   a.scratch_i = (int*)((char*)ws + sizeof(double) * (size_t)d->batch * (d->n + d->m));
+  a.natoms = d->natoms;
+  if (d->step == UOT_STEP_PAIRWISE) {
+    const size_t cap = (size_t)d->max_iters + 1;
+    const size_t bc = (size_t)d->batch * cap;
+    char* p = (char*)ws + (fw_scratch_bytes(d->batch, d->n, d->m) + 255) / 256 * 256;
+    a.cap = (int)cap;
+    a.atoms = (double*)p;
+    p += sizeof(double) * bc * (d->n + d->m);
+    a.wts = (double*)p;
+    a.scs = a.wts + bc;
+    a.dis = a.scs + bc;
+    a.act = (int*)(a.dis + bc);
+  }
   return launch_fw(a, d->batch, (cudaStream_t)stream);
 }
 

@@ -4,6 +4,8 @@
 ``SolverReport``; ``fw_solve_batched`` runs a batch of independent problems
 (BASELINE config 2) in one launch of ``csrc/fw1d.cu``: one CTA per problem,
 every iteration (tilt, oracle, gaps, Newton line search, update) on chip.
+``step="pairwise"`` runs pairwise FW (src/fw.py:255-357) with the atom store
+in the device workspace.
 """
 
 from __future__ import annotations
@@ -61,6 +63,7 @@ class FwBatchResult:
     summary: object
     status: object
     step_size: object
+    natoms: object = None  # pairwise: active atoms after each iteration
 
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
@@ -87,16 +90,23 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         ei=D.empty((B, n + m - 1), t.int32), ej=D.empty((B, n + m - 1), t.int32),
         em=D.empty((B, n + m - 1), t.float64), count=D.empty((B,), t.int32),
         summary=D.empty((B, 3), t.float64), status=D.empty((B,), t.int32),
-        step_size=t.zeros((B, max_iters), dtype=t.float64, device=x.device))
+        step_size=t.zeros((B, max_iters), dtype=t.float64, device=x.device),
+        natoms=t.zeros((B, max_iters), dtype=t.int32, device=x.device) if step == "pairwise"
+        else None)
+    if step not in ("linesearch", "harmonic", "pairwise"):
+        raise ValueError("step must be 'harmonic', 'linesearch', or 'pairwise'")
+    code = {"linesearch": _lib.STEP_LINESEARCH, "harmonic": _lib.STEP_HARMONIC,
+            "pairwise": _lib.STEP_PAIRWISE}[step]
     desc = _lib.FwDesc(
         batch=B, n=n, m=m, p=float(p), rho1=float(rho1), rho2=float(rho2),
-        step=_lib.STEP_LINESEARCH if step == "linesearch" else _lib.STEP_HARMONIC,
+        step=code,
         max_iters=int(max_iters), gap_tol=float(gap_tol), early_exit=1 if early_exit else 0,
         x=_lib.ptr(x), y=_lib.ptr(y), a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(f), g=_lib.ptr(g),
         h0=_lib.ptr(r.h0), fw_gap=_lib.ptr(r.fw_gap), pd_gap=_lib.ptr(r.pd_gap),
         iterations=_lib.ptr(r.iterations), ei=_lib.ptr(r.ei), ej=_lib.ptr(r.ej),
         em=_lib.ptr(r.em), count=_lib.ptr(r.count), summary=_lib.ptr(r.summary),
-        status=_lib.ptr(r.status), step_size=_lib.ptr(r.step_size))
+        status=_lib.ptr(r.status), step_size=_lib.ptr(r.step_size),
+        natoms=_lib.ptr(r.natoms) if r.natoms is not None else None)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)
@@ -134,8 +144,6 @@ def _check_problem(prob):
 def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     """Maximise the invariant dual at eps = 0 (src/fw.py:176-232)."""
     _check_problem(prob)
-    if config.step == "pairwise":
-        raise UnsupportedEntropyError("pairwise FW is not on the B200 path yet")
     n, m = len(prob.alpha), len(prob.beta)
     d = init if init is not None else DualPair.zeros(n, m)
     prob.check_pair(d)

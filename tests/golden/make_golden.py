@@ -216,6 +216,62 @@ def gen_fw():
     save("fw.npz", **out)
 
 
+def ref_pfw(prob, iters):
+    """fw.py:326-357 (_pfw_solve) loop body with the early exit removed; the
+    step size is read back from the weight transfer."""
+    d0 = UF._default_init(prob)
+    store = UF.AtomStore(d0.f[None, :], d0.g[None, :], np.array([1.0]))
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap", "natoms")}
+    plan = None
+    for _ in range(iters):
+        store, diag = UF._pfw_iteration(prob, store)
+        plan = diag["plan"]
+        tr["h0"].append(diag["dual"])
+        tr["fw_gap"].append(diag["fw_gap"])
+        tr["pd_gap"].append(diag["primal"] - diag["dual"])
+        tr["natoms"].append(store.weights.size)
+    d = store.current()
+    lam = U.lambda_star(prob, d)
+    return d, lam, plan, {k: np.asarray(v) for k, v in tr.items()}
+
+
+def gen_pfw():
+    out = {}
+    cases = []
+    rng = np.random.default_rng(29)
+    specs = []
+    for k in range(5):  # small random problems
+        n, m = int(rng.integers(20, 70)), int(rng.integers(20, 70))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.exponential(1.0, n)
+        wa *= rng.uniform(0.5, 2.0) / wa.sum()
+        wb = rng.exponential(1.0, m)
+        wb *= rng.uniform(0.5, 2.0) / wb.sum()
+        r1, r2 = float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.3, 2.0))
+        p = [2.0, 1.0][k % 2]
+        specs.append((x, y, wa, wb, r1, r2, p, 80))
+    x2, y2, a2, b2 = S.cfg2_batch(count=1)
+    specs.append((x2[0], y2[0], a2[0], b2[0], 1.0, 1.0, 2.0, 150))  # cfg2 shape
+    for k, (x, y, wa, wb, r1, r2, p, iters) in enumerate(specs):
+        t0 = time.time()
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=0.0)
+        d, lam, plan, tr = ref_pfw(prob, iters)
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([r1, r2, p, iters])
+        out[f"c{k}_f_raw"], out[f"c{k}_g_raw"] = d.f, d.g
+        out[f"c{k}_f"], out[f"c{k}_g"] = d.f + lam, d.g - lam
+        out[f"c{k}_i"], out[f"c{k}_j"], out[f"c{k}_m"] = plan.source_idx, plan.target_idx, plan.mass
+        for kk, v in tr.items():
+            out[f"c{k}_{kk}"] = v
+        cases.append(k)
+        print(f"  pfw case {k}: {len(x)}x{len(y)} x{iters} atoms {tr['natoms'][-1]} "
+              f"in {time.time() - t0:.1f}s")
+    out["cases"] = np.array(cases)
+    save("pfw.npz", **out)
+
+
 def gen_mot():
     rng = np.random.default_rng(17)
     out = {}
@@ -362,7 +418,7 @@ def gen_duality():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
-                             "mot", "barycenter", "duality"]
+                             "mot", "barycenter", "duality", "pfw"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -93,6 +93,23 @@ def test_fw_small_and_cfg2_shape():
             np.testing.assert_allclose(mm, z[f"c{k}_m"], rtol=1e-9, atol=1e-15)
 
 
+def test_pfw_oracle_pinned():
+    """Pairwise FW restatement (oracle.pfw_fixed) vs the reference's own
+    _pfw_iteration loop: traces, atom counts, final pair, plan."""
+    z = golden("pfw.npz")
+    for k in cases(z):
+        r1, r2, p, iters = z[f"c{k}_par"]
+        iters_run = int(iters) if k < 5 else 40
+        out = O.pfw_fixed(z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"], z[f"c{k}_b"], r1, r2,
+                          iters_run, p=p)
+        np.testing.assert_allclose(out["h0"], z[f"c{k}_h0"][:iters_run], rtol=1e-12, atol=1e-14)
+        np.testing.assert_array_equal(out["natoms"], z[f"c{k}_natoms"][:iters_run])
+        if iters_run == int(iters):
+            assert rel_err(out["f"], out["g"], z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-12
+            np.testing.assert_array_equal(out["plan"][0], z[f"c{k}_i"])
+            np.testing.assert_array_equal(out["plan"][1], z[f"c{k}_j"])
+
+
 @pytest.mark.slow
 def test_fw_cfg2_full_500():
     z = golden("fw.npz")
