@@ -1,0 +1,938 @@
+// fw1d_kernel.cuh -- batched 1-D OT oracle (Algorithm 1) and batched Frank-Wolfe UOT
+// at eps = 0 (K4/K5/K6 of SURVEY.md §2.2).
+//
+// Reference: src/ot1d.py:112-172 (solve_ot_1d), src/fw.py:106-232 (_h0,
+// ternary line search, _lmo, fw_solve), src/duality.py:175-178, :279-303,
+// :320-344 (lambda_star, _eval_h_kl, updated_marginals, eval_primal).
+//
+// Design: one CTA per problem, THREADS x EPT elements per side held in
+// registers for the whole run (x, y and the cumulative masses live in shared
+// memory for the random accesses of the oracle), so an FW iteration touches
+// HBM only for its three trace scalars.  The monotone sweep is restated as a
+// merge of cumulative masses: with A_k = sum_{i<=k} ta_i and B_l likewise,
+// source event k happens after the target events with B_l < A_k (ties go to
+// the source, ot1d.py:158), so its partner index is a binary search, and the
+// dual potentials are prefix sums of cost differences along the staircase:
+//   r_{k+1} = r_k + C(k+1, j_k) - C(k, j_k),  s_{l+1} = s_l + C(i_l, l+1) - C(i_l, l)
+// starting from r_0 = 0, s_0 = C(0,0) (ot1d.py:138-166).  The line search
+// minimises the convex log-partition phi(gamma) (H_0 = const - (r1+r2) e^phi,
+// fw.py:106-148) by safeguarded Newton on three moments per pass instead of
+// the reference's 123 ternary evaluations (FW parity).
+#include <algorithm>
+#include <type_traits>
+
+#pragma once
+
+#include "../../include/uot_b200.h"
+#include "blockops.cuh"
+#include "common.cuh"
+
+namespace uot {
+namespace fwk {
+
+constexpr int FW_THREADS = 256;
+#ifndef FW_MINB
+#define FW_MINB 2
+#endif
+
+struct FwArgs {
+  int n, m;
+  double p;
+  double r1, r2;
+  int step;
+  int max_iters;
+  double gap_tol;
+  int early_exit;
+  int mode;  // 0 = Frank-Wolfe, 1 = plain OT oracle on (a, b)
+  const double* x;
+  const double* y;
+  const double* a;
+  const double* b;
+  double* f;
+  double* g;
+  double* h0;
+  double* fw_gap;
+  double* pd_gap;
+  int* iterations;
+  int* ei;
+  int* ej;
+  double* em;
+  int* count;
+  double* summary;
+  int* status;
+  double* step_size;
+  double* scratch;  // [batch][n+m] doubles + [batch][n+m][2] ints (plan extraction)
+  int* scratch_i;
+  // pairwise FW atom store (fw.py:70-95), cap = max_iters + 1 slots per problem
+  int cap;
+  double* atoms;  // [batch][cap][n+m] (r | s) rows
+  double* wts;    // [batch][cap] weight of each slot
+  int* act;       // [batch][cap] active slots in insertion order
+  double* scs;    // [batch][cap] scores of the active atoms (per position)
+  double* dis;    // [batch][cap] sup-norm distance to the new atom
+  int* natoms;    // optional [batch][max_iters] trace
+};
+
+static __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
+
+__device__ __forceinline__ double pcost(double xi, double yj, double p) {
+  const double d = xi - yj;
+  if (p == 2.0) return d * d;
+  const double ad = fabs(d);
+  if (p == 1.0) return ad;
+  return pow_abs(d, p);
+}
+
+// Cost kinds resolved at compile time for the FW kernels: PK = 0 -> p = 2,
+// 1 -> p = 1, 2 -> general p (one out-of-line pow keeps the kernel small).
+template <int PK>
+__device__ __forceinline__ double pcost_k(double xi, double yj, double p) {
+  const double d = xi - yj;
+  if constexpr (PK == 0) return d * d;
+  else if constexpr (PK == 1) return fabs(d);
+  else return pow_abs(d, p);
+}
+
+__device__ __forceinline__ int ibsum(int v, int* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  int s = 0;
+  for (int w = 0; w < FW_THREADS / 32; ++w) s += scratch[w];
+  __syncthreads();
+  return s;
+}
+
+// Exclusive block max-scan of one int per thread (identity -1).
+__device__ __forceinline__ int excl_max_scan(int v, int* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, t);
+  }
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = -1;
+  __syncthreads();
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) excl = max(excl, scratch[w]);
+  __syncthreads();
+  return excl;
+}
+
+// Per-problem CTA.  Thread t owns source/target elements t*EPT .. t*EPT+EPT-1
+// of each side.  Shared memory holds the supports, the constant weights, the
+// breakpoints and the merge ranks; registers hold the potentials.
+constexpr int FW_NW = FW_THREADS / 32;
+constexpr int FW_BUF = 16 * FW_NW;  // one reduction buffer (doubles)
+
+template <int EPT, int PK>
+struct Cta {
+  int n, m;
+  double p;
+  const double* sx;
+  const double* sy;
+  double* sA;
+  double* sB;
+  unsigned short* rkA;  // rkA[k] = #target events before source event k in the merge
+  unsigned short* rkB;  // rkB[l] = #source events before target event l
+  double* zred;  // scratch of the zero-weight fix (own syncs)
+  bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
+  double* pfw;   // pairwise FW staging (n + m doubles) or nullptr
+
+  __device__ int src(int e) const { return threadIdx.x * EPT + e; }
+
+  // Merge path over the breakpoints: thread t emits merged positions
+  // [2 EPT t, 2 EPT (t+1)) of the sweep order (source first on ties,
+  // ot1d.py:158) after one diagonal binary search, recording for every event
+  // its partner index -- the number of events of the other side before it.
+  __device__ void merge_ranks() {
+    const int na = n - 1, nb = m - 1, E = na + nb;
+    constexpr int IPT = 2 * EPT;
+    const int d0 = min((int)threadIdx.x * IPT, E);
+    int lo = max(0, d0 - nb), hi = min(d0, na);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sA[mid] <= sB[d0 - 1 - mid])
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int i = lo, j = d0 - lo;
+#pragma unroll
+    for (int s = 0; s < IPT; ++s) {
+      if (d0 + s < E) {
+        const double av = i < na ? sA[i] : CUDART_INF;
+        const double bv = j < nb ? sB[j] : CUDART_INF;
+        const bool takeA = av <= bv;
+        unsigned short* dst = takeA ? rkA + i : rkB + j;
+        *dst = (unsigned short)(takeA ? j : i);
+        i += takeA;
+        j += !takeA;
+      }
+    }
+  }
+
+  // Balanced 1-D OT oracle on (ta, tb): cumulative masses -> merge ranks ->
+  // dual potentials (r, s).  Leaves sA/sB/rkA/rkB describing the plan.
+  template <typename PING>
+  __device__ void oracle(const double (&ta)[EPT], const double (&tb)[EPT], double (&r)[EPT],
+                         double (&s)[EPT], double& mass_a, double& mass_b, PING& ping) {
+    double pa[EPT], pb[EPT];
+    double ca = 0.0, cb = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ca += ta[e];
+      pa[e] = ca;
+      cb += tb[e];
+      pb[e] = cb;
+    }
+    double tot[2] = {ca, cb}, totals[2];
+    bops::block_scan_excl<FW_NW, 2>(tot, totals, ping.next());
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      if (i < n) sA[i] = tot[0] + pa[e];
+      if (i < m) sB[i] = tot[1] + pb[e];
+    }
+    mass_a = totals[0];
+    mass_b = totals[1];
+    if (zeros) {
+      // A zero-weight atom must repeat its predecessor's breakpoint bit for
+      // bit (the reference emits no entry for it, ot1d.py:149-153), but the
+      // block scan associates differently across thread boundaries.
+      int lza = -1, lzb = -1;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        if (i < n && ta[e] > 0.0) lza = i;
+        if (i < m && tb[e] > 0.0) lzb = i;
+      }
+      int pra = excl_max_scan(lza, reinterpret_cast<int*>(zred));
+      int prb = excl_max_scan(lzb, reinterpret_cast<int*>(zred));
+      __syncthreads();
+      double fa[EPT], fb[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        fa[e] = (i < n && ta[e] == 0.0) ? (pra >= 0 ? sA[pra] : 0.0) : -1.0;
+        fb[e] = (i < m && tb[e] == 0.0) ? (prb >= 0 ? sB[prb] : 0.0) : -1.0;
+        if (i < n && ta[e] > 0.0) pra = i;
+        if (i < m && tb[e] > 0.0) prb = i;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = src(e);
+        if (fa[e] >= 0.0) sA[i] = fa[e];
+        if (fb[e] >= 0.0) sB[i] = fb[e];
+      }
+    }
+    __syncthreads();
+    merge_ranks();
+    __syncthreads();
+    // cost increments along the staircase
+    double da[EPT], db[EPT];
+    double la = 0.0, lb = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      da[e] = 0.0;
+      db[e] = 0.0;
+      if (i >= 1 && i < n) {
+        const double yj = sy[rkA[i - 1]];  // partner of source event i-1
+        da[e] = pcost_k<PK>(sx[i], yj, p) - pcost_k<PK>(sx[i - 1], yj, p);
+      }
+      if (i >= 1 && i < m) {
+        const double xk = sx[rkB[i - 1]];  // partner of target event i-1
+        db[e] = pcost_k<PK>(xk, sy[i], p) - pcost_k<PK>(xk, sy[i - 1], p);
+      }
+      la += da[e];
+      lb += db[e];
+    }
+    double off[2] = {la, lb}, unused[2];
+    bops::block_scan_excl<FW_NW, 2>(off, unused, ping.next());
+    const double s0 = pcost_k<PK>(sx[0], sy[0], p);
+    double ra = off[0], rb = off[1];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ra += da[e];
+      rb += db[e];
+      r[e] = ra;
+      s[e] = s0 + rb;
+    }
+  }
+
+  // Plan of the current merge, compacted to positive-mass entries in sweep
+  // order (ot1d.py:149-153).  vals: n+m doubles, codes: 2(n+m) ints.
+  __device__ void extract_plan(double* vals, int* codes, int* ei, int* ej, double* em,
+                               int* count, double total) {
+    const int nev = (n - 1) + (m - 1);
+    for (int i = threadIdx.x; i < n - 1; i += FW_THREADS) {
+      const int j = rkA[i];
+      const int rank = i + j;
+      vals[rank] = sA[i];
+      codes[2 * rank] = i + 1;
+      codes[2 * rank + 1] = j;
+    }
+    for (int l = threadIdx.x; l < m - 1; l += FW_THREADS) {
+      const int k = rkB[l];
+      const int rank = l + k;
+      vals[rank] = sB[l];
+      codes[2 * rank] = k;
+      codes[2 * rank + 1] = l + 1;
+    }
+    __syncthreads();
+    int base = 0;
+    int* iscr = reinterpret_cast<int*>(zred);
+    for (int s0 = 0; s0 <= nev; s0 += FW_THREADS) {
+      const int s = s0 + threadIdx.x;
+      double mass = 0.0;
+      int ii = 0, jj = 0;
+      if (s <= nev) {
+        const double lo = s == 0 ? 0.0 : fmin(vals[s - 1], total);
+        const double hi = s == nev ? total : fmin(vals[s], total);
+        mass = hi - lo;
+        if (s > 0) {
+          ii = codes[2 * (s - 1)];
+          jj = codes[2 * (s - 1) + 1];
+        }
+      }
+      const int keep = (s <= nev && mass > 0.0) ? 1 : 0;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      int incl = keep;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      __syncthreads();
+      if (lane == 31) iscr[warp] = incl;
+      __syncthreads();
+      int off = 0, tot = 0;
+      for (int w = 0; w < FW_NW; ++w) {
+        if (w < warp) off += iscr[w];
+        tot += iscr[w];
+      }
+      __syncthreads();
+      if (keep) {
+        const int pos = base + off + incl - 1;
+        ei[pos] = ii;
+        ej[pos] = jj;
+        em[pos] = mass;
+      }
+      base += tot;
+    }
+    if (threadIdx.x == 0) *count = base;
+    __syncthreads();
+  }
+};
+
+// Pairwise FW state shared by all threads of the CTA: active atoms and
+// slots used so far (identical in every thread).
+struct PfwState {
+  int na, ntot;
+};
+
+// One pairwise step (fw.py:275-310) after the LMO of iteration t: scores of
+// the active atoms against the tilted marginals (one warp per atom, coalesced
+// rows from the workspace store) and their sup-norm distance to the new
+// atom (r, s); the away atom = argmin score (lowest position on ties);
+// safeguarded Newton on phi along (r, s) - away over [0, w_away] (fw.py:
+// 295-297 runs a ternary search + endpoint check on the same concave H0);
+// weight transfer, merge into an atom closer than 1e-12 (:260-272), drop of
+// zero weights, and the iterate update d += gamma ((r, s) - away).  Returns
+// gamma.  The shared breakpoint arrays sA / sB are free after the oracle and
+// hold ta / tb here; the new atom is staged after them.
+template <int EPT, int PK, typename PING>
+__device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, double (&f)[EPT],
+                           double (&g)[EPT], const double (&r)[EPT], const double (&s)[EPT],
+                           const double (&ta)[EPT], const double (&tb)[EPT], double mta,
+                           double mtb, double& sha, double& shb, double i1, double i2, double t1,
+                           double t2, const double* sal, const double* sbe, const double* tab,
+                           PING& ping, PfwState& pst) {
+  const int n = c.n, m = c.m, nm = n + m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ta_s = c.sA;  // [n]
+  double* tb_s = c.sB;  // [m]
+  double* nr_s = c.pfw;  // [n] new atom staging (pairwise only)
+  double* ns_s = nr_s + n;  // [m]
+  (void)sal;
+  __shared__ int away_s, hit_s, na_s;
+  __syncthreads();  // sA / sB readers (oracle, plan extraction) are done
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n) {
+      ta_s[i] = ta[e];
+      nr_s[i] = r[e];
+    }
+    if (i < m) {
+      tb_s[i] = tb[e];
+      ns_s[i] = s[e];
+    }
+  }
+  __syncthreads();
+  const long sb0 = (long)b * A.cap;
+  const double* AT = A.atoms + sb0 * nm;
+  for (int pos = warp; pos < pst.na; pos += FW_NW) {
+    const double* row = AT + (long)__ldcg(A.act + sb0 + pos) * nm;
+    double sc = 0.0, dd = 0.0;
+    for (int i = lane; i < nm; i += 32) {
+      const double v = row[i];
+      const bool src = i < n;
+      const double tw = src ? ta_s[i] : tb_s[i - n];
+      const double nv = src ? nr_s[i] : ns_s[i - n];
+      sc = fma(v, tw, sc);
+      dd = bops::dmax(dd, fabs(v - nv));
+    }
+    sc = warp_sum(sc);
+    dd = bops::warp_dmax(dd);
+    if (lane == 0) {
+      A.scs[sb0 + pos] = sc;
+      A.dis[sb0 + pos] = dd;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double best = CUDART_INF;
+    int bp = 0x7fffffff, hp = 0x7fffffff;
+    for (int pos = lane; pos < pst.na; pos += 32) {
+      const double sc = __ldcg(A.scs + sb0 + pos);
+      if (sc < best) {  // positions ascend per lane: first minimum kept
+        best = sc;
+        bp = pos;
+      }
+      if (hp == 0x7fffffff && __ldcg(A.dis + sb0 + pos) < 1e-12) hp = pos;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ob < best || (ob == best && op < bp)) {
+        best = ob;
+        bp = op;
+      }
+      hp = min(hp, __shfl_xor_sync(0xffffffffu, hp, o));
+    }
+    if (lane == 0) {
+      away_s = bp;
+      hit_s = hp == 0x7fffffff ? -1 : hp;
+    }
+  }
+  __syncthreads();
+  const int away = away_s, hit = hit_s;
+  const int aslot = __ldcg(A.act + sb0 + away);
+  const double* ra = AT + (long)aslot * nm;
+  double dA[EPT], dB[EPT];
+  double mom[4] = {0.0, 0.0, 0.0, 0.0};
+  double mxs[4] = {0.0, 0.0, -CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    dA[e] = i < n ? r[e] - ra[i] : 0.0;
+    dB[e] = i < m ? s[e] - ra[n + i] : 0.0;
+    const double va = dA[e] * i1, vb = dB[e] * i2;
+    mom[0] += ta[e] * va;
+    mom[1] += ta[e] * va * va;
+    mom[2] += tb[e] * vb;
+    mom[3] += tb[e] * vb * vb;
+    mxs[0] = bops::dmax(mxs[0], fabs(dA[e]));
+    mxs[1] = bops::dmax(mxs[1], fabs(dB[e]));
+    if (i < n && sal[i] > 0.0) mxs[2] = bops::dmax(mxs[2], -va);
+    if (i < m && sbe[i] > 0.0) mxs[3] = bops::dmax(mxs[3], -vb);
+  }
+  bops::block_red<FW_NW, 4, 4>(mom, mxs, ping.next());
+  const double gmax = __ldcg(A.wts + sb0 + aslot);
+  double gam = 0.0;
+  if (!(gmax <= 0.0 || (mxs[0] < 1e-12 && mxs[1] < 1e-12))) {  // fw.py:291-293
+    // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
+    // on [0, gmax]; centred moments as in the FW line search
+    const double ca = mom[0] / mta, cb = mom[2] / mtb;
+    const double k0 = -(t1 * ca + t2 * cb);
+    const double d2 = t1 * fmax(mom[1] / mta - ca * ca, 0.0) +
+                      t2 * fmax(mom[3] / mtb - cb * cb, 0.0);
+    if (k0 < 0.0) {
+      double lo = 0.0, hi = gmax;
+      gam = (d2 > 0.0) ? fmin(gmax, -k0 / d2) : gmax;
+      for (int it = 0; it < 32; ++it) {
+        const double pha = sha + gam * mxs[2];
+        const double phb = shb + gam * mxs[3];
+        double mm[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const int i = c.src(e);
+          const double va = dA[e] * i1, vb = dB[e] * i2;
+          const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
+          const double wa = bops::wexp(wa0, -f[e] * i1 - gam * va - pha, tab);
+          const double wb = bops::wexp(wb0, -g[e] * i2 - gam * vb - phb, tab);
+          const double xa = va - ca, xb = vb - cb;
+          mm[0] += wa;
+          mm[1] += wa * xa;
+          mm[2] += wa * xa * xa;
+          mm[3] += wb;
+          mm[4] += wb * xb;
+          mm[5] += wb * xb * xb;
+        }
+        bops::block_sum<FW_NW, 6>(mm, ping.next());
+        const double a1 = mm[1] / mm[0], a2 = mm[2] / mm[0];
+        const double b1 = mm[4] / mm[3], b2 = mm[5] / mm[3];
+        const double g1 = k0 - t1 * a1 - t2 * b1;
+        const double g2 = t1 * (a2 - a1 * a1) + t2 * (b2 - b1 * b1);
+        if (g1 < 0.0)
+          lo = gam;
+        else
+          hi = gam;
+        if (gam >= gmax && g1 <= 0.0) {
+          gam = gmax;
+          break;
+        }
+        double nxt = (g2 > 0.0) ? gam - g1 / g2 : 0.5 * (lo + hi);
+        const bool newton = nxt > lo && nxt < hi;
+        if (!newton) nxt = 0.5 * (lo + hi);
+        const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(gmax, gam)) || g1 == 0.0 ||
+                          hi - lo <= 1e-15 * fmax(1.0, gmax);
+        gam = nxt;
+        if (conv) break;
+      }
+    }
+  }
+  if (gam > 0.0) {
+    // the new atom gets a slot unless it merges into an existing one
+    const int nslot = pst.ntot;
+    if (hit < 0) {
+      double* row = A.atoms + (sb0 + nslot) * nm;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        if (i < n) row[i] = r[e];
+        if (i < m) row[n + i] = s[e];
+      }
+    }
+    if (threadIdx.x == 0) {
+      double* w = A.wts + sb0;
+      int* ac = A.act + sb0;
+      w[aslot] = fmax(w[aslot] - gam, 0.0);
+      int na = pst.na;
+      if (hit >= 0) {
+        w[ac[hit]] += gam;
+      } else {
+        w[nslot] = gam;
+        ac[na++] = nslot;
+      }
+      int k = 0;
+      for (int q = 0; q < na; ++q) {
+        const int sl = ac[q];
+        if (w[sl] > 0.0) ac[k++] = sl;
+      }
+      na_s = k;
+    }
+    if (hit < 0) ++pst.ntot;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      f[e] += gam * dA[e];
+      g[e] += gam * dB[e];
+    }
+    if (sha > -CUDART_INF) sha += gam * mxs[2];
+    if (shb > -CUDART_INF) shb += gam * mxs[3];
+    __syncthreads();
+    pst.na = na_s;
+  }
+  if (A.natoms != nullptr && threadIdx.x == 0) A.natoms[(long)b * A.max_iters + t] = pst.na;
+  return gam;
+}
+
+template <int EPT, int PK, bool PW>
+__global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(16) double red[3 * FW_BUF];
+  __shared__ double tab[32];
+  const int b = blockIdx.x;
+  const int n = A.n, m = A.m;
+  double* sx = smem;
+  double* sy = sx + n;
+  double* sA = sy + m;
+  double* sB = sA + n;
+  double* sal = sB + m;  // constant weights
+  double* sbe = sal + n;
+  unsigned short* rkA = reinterpret_cast<unsigned short*>(sbe + m);
+  unsigned short* rkB = rkA + n;
+  double* pfwbuf = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(rkB + m) + 15) & ~static_cast<uintptr_t>(15));
+  Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false,
+                 PW ? pfwbuf : nullptr};
+  bops::Ping<FW_BUF> ping{red, 0};
+  bops::load_exp_table(tab);
+
+  int nz = 0;
+  for (int i = threadIdx.x; i < n; i += FW_THREADS) {
+    sx[i] = A.x[(long)b * n + i];
+    const double w = A.a[(long)b * n + i];
+    sal[i] = w;
+    nz += (w == 0.0);
+  }
+  for (int j = threadIdx.x; j < m; j += FW_THREADS) {
+    sy[j] = A.y[(long)b * m + j];
+    const double w = A.b[(long)b * m + j];
+    sbe[j] = w;
+    nz += (w == 0.0);
+  }
+  c.zeros = ibsum(nz, reinterpret_cast<int*>(c.zred)) > 0;  // (syncs: smem now visible)
+
+  double f[EPT], g[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    f[e] = i < n ? A.f[(long)b * n + i] : 0.0;
+    g[e] = i < m ? A.g[(long)b * m + i] : 0.0;
+  }
+  double* vals = A.scratch + (long)b * (n + m);
+  int* codes = A.scratch_i + (long)b * 2 * (n + m);
+  int* ei = A.ei + (long)b * (n + m - 1);
+  int* ej = A.ej + (long)b * (n + m - 1);
+  double* em = A.em + (long)b * (n + m - 1);
+
+  if (A.mode == 1) {
+    // Plain balanced OT on (a, b): src/ot1d.py:112-172.
+    double ta[EPT], tb[EPT], r[EPT], s[EPT], ma, mb;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      ta[e] = i < n ? sal[i] : 0.0;
+      tb[e] = i < m ? sbe[i] : 0.0;
+    }
+    c.oracle(ta, tb, r, s, ma, mb, ping);
+    const int bad = fabs(ma - mb) > 1e-9 * fmax(ma, mb);  // ot1d.py:133-136
+    if (threadIdx.x == 0) A.status[b] = bad ? UOT_MASS_BALANCE : 0;
+    if (bad) return;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) A.f[(long)b * n + i] = r[e];
+      if (i < m) A.g[(long)b * m + i] = s[e];
+    }
+    c.extract_plan(vals, codes, ei, ej, em, A.count + b, fmin(ma, mb));
+    return;
+  }
+
+  const int lane = threadIdx.x & 31;
+  const double r1 = A.r1, r2 = A.r2;
+  const double i1 = 1.0 / r1, i2 = 1.0 / r2;
+  const double t1 = r1 / (r1 + r2), t2 = r2 / (r1 + r2);
+  double malpha, mbeta;
+  // Shifts of the two log-sum-exps: exact maxima of u = -f/r1, u' = -g/r2
+  // over the positive-weight atoms at t = 0, then the upper bound
+  // (1-gamma) shift + gamma max(-r/r1) carried through each update, so no
+  // per-iteration max reduction is needed (an underflowing sum falls back
+  // to the exact maxima).
+  double sha, shb;
+  {
+    double ms[2] = {0.0, 0.0}, mx[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) ms[0] += sal[i];
+      if (i < m) ms[1] += sbe[i];
+      if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+      if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
+    }
+    bops::block_red<FW_NW, 2, 2>(ms, mx, ping.next());
+    malpha = ms[0];
+    mbeta = ms[1];
+    sha = mx[0];
+    shb = mx[1];
+  }
+
+  int status = 0;
+  int iters = 0;
+  double last_primal = 0.0, last_dual = 0.0;
+  PfwState pst{1, 1};
+  if constexpr (PW) {  // store = {(f0, g0)} with weight 1 (fw.py:332)
+    double* row = A.atoms + (long)b * A.cap * (n + m);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      if (i < n) row[i] = f[e];
+      if (i < m) row[n + i] = g[e];
+    }
+    if (threadIdx.x == 0) {
+      A.act[(long)b * A.cap] = 0;
+      A.wts[(long)b * A.cap] = 1.0;
+    }
+    __syncthreads();
+  }
+  for (int t = 0; t < A.max_iters; ++t) {
+    // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303).
+    // The exponentials are shared between the log-sum-exps and the tilt.
+    double ta[EPT], tb[EPT];
+    double sums[2];
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      sums[0] = 0.0;
+      sums[1] = 0.0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
+        ta[e] = bops::wexp(wa, -f[e] * i1 - sha, tab);
+        tb[e] = bops::wexp(wb, -g[e] * i2 - shb, tab);
+        sums[0] += ta[e];
+        sums[1] += tb[e];
+      }
+      bops::block_sum<FW_NW, 2>(sums, ping.next());
+      // block-uniform: a stale shift far above the maximum underflowed
+      if (!((sums[0] < 1e-280 && sha > -CUDART_INF) || (sums[1] < 1e-280 && shb > -CUDART_INF)))
+        break;
+      double mx[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+        if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
+      }
+      bops::block_max<FW_NW, 2>(mx, ping.next());
+      sha = mx[0];
+      shb = mx[1];
+    }
+    // Scalars, one transcendental per lane: lanes 0/1 take the logs, lanes
+    // 0/1/2 the exponentials of H_0 and of the two tilt factors.
+    const double lg = log((lane & 1) ? sums[1] : sums[0]);
+    const double la = sha + __shfl_sync(bops::FULL, lg, 0);
+    const double lb = shb + __shfl_sync(bops::FULL, lg, 1);
+    const double lam = (r1 * r2 / (r1 + r2)) * (la - lb);
+    const double earg = lane == 0 ? t1 * la + t2 * lb : lane == 1 ? sha - lam / r1 : shb + lam / r2;
+    const double ev = exp(earg);  // (libdevice: arguments are not shifted here)
+    const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * __shfl_sync(bops::FULL, ev, 0);
+    const double sca = sha > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 1) : 0.0;
+    const double scb = shb > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 2) : 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      ta[e] *= sca;
+      tb[e] *= scb;
+    }
+    // --- linear oracle (ot1d.py:112-172 on the tilted marginals, fw.py:159-173)
+    double r[EPT], s[EPT], mta, mtb;
+    c.oracle(ta, tb, r, s, mta, mtb, ping);
+    if (fabs(mta - mtb) > 1e-9 * fmax(mta, mtb)) {  // fw.py:161-166
+      status = UOT_MASS_BALANCE;
+      break;
+    }
+    // --- gaps, primal and line-search moments at gamma = 0.  log(ta/alpha)
+    // = -(f + lam)/r1 exactly, so the KL terms of the oracle plan (whose
+    // marginals are ta, tb) need no logarithm (entropies.py:123-131).
+    // mr: max of -r/r1, -s/r2 over the positive-weight atoms (shift bounds).
+    double acc[9], mr[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = c.src(e);
+      const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
+      acc[0] += ta[e] * (r[e] - f[e]);
+      acc[1] += tb[e] * (s[e] - g[e]);
+      acc[2] += ta[e] * r[e] + tb[e] * s[e];
+      if (ta[e] > 0.0) acc[3] += ta[e] * ((-f[e] - lam) * i1);
+      if (tb[e] > 0.0) acc[4] += tb[e] * ((-g[e] + lam) * i2);
+      if (i < n && sal[i] > 0.0) mr[0] = bops::dmax(mr[0], -r[e] * i1);
+      if (i < m && sbe[i] > 0.0) mr[1] = bops::dmax(mr[1], -s[e] * i2);
+      acc[5] += ta[e] * va;
+      acc[6] += ta[e] * va * va;
+      acc[7] += tb[e] * vb;
+      acc[8] += tb[e] * vb * vb;
+    }
+    bops::block_red<FW_NW, 9, 2>(acc, mr, ping.next());
+    const double fw_gap = acc[0] + acc[1];
+    const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
+    const double primal = acc[2] + r1 * kl1 + r2 * kl2;
+    const double pd_gap = primal - dual;
+    if (threadIdx.x == 0) {
+      A.h0[(long)b * A.max_iters + t] = dual;
+      A.fw_gap[(long)b * A.max_iters + t] = fw_gap;
+      A.pd_gap[(long)b * A.max_iters + t] = pd_gap;
+    }
+    iters = t + 1;
+    last_primal = primal;
+    last_dual = dual;
+    const bool stop = A.early_exit && pd_gap < A.gap_tol;  // fw.py:220-222
+    if (stop || t == A.max_iters - 1) {
+      c.extract_plan(vals, codes, ei, ej, em, A.count + b, fmin(mta, mtb));
+    }
+    if constexpr (PW) {
+      // pairwise: the step of this iteration is taken before the exit test
+      // (fw.py:341-353)
+      const double gam = pfw_step(c, A, b, t, f, g, r, s, ta, tb, mta, mtb, sha, shb, i1, i2, t1,
+                                  t2, sal, sbe, tab, ping, pst);
+      if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
+      if (stop) break;
+      continue;
+    }
+    if (stop) break;
+    // --- step size
+    double gam;
+    if (A.step == UOT_STEP_HARMONIC) {
+      gam = 2.0 / (2.0 + t);  // fw.py:223-224
+    } else {
+      // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb).
+      // The FW direction carries a translation component (f + c, g - c) that
+      // phi ignores exactly (H is translation invariant), so raw moments of
+      // va and vb nearly cancel; moments are taken about the gamma = 0 means
+      // (ca, cb) and the constant part of phi' is kept separately.
+      const double ca = acc[5] / mta, cb = acc[7] / mtb;
+      const double k0 = -(t1 * ca + t2 * cb);  // phi'(0)
+      const double d2 = t1 * fmax(acc[6] / mta - ca * ca, 0.0) +
+                        t2 * fmax(acc[8] / mtb - cb * cb, 0.0);  // starting curvature
+      if (!(k0 < 0.0)) {
+        gam = 0.0;
+      } else {
+        double lo = 0.0, hi = 1.0;
+        gam = (d2 > 0.0) ? fmin(1.0, -k0 / d2) : 1.0;
+        for (int it = 0; it < 24; ++it) {
+          // one pass: centred moments of va / vb under p_gamma, q_gamma; the
+          // shift (1-gamma) sh + gamma max(-r/r1) bounds every exponent.
+          const double pha = (1.0 - gam) * sha + gam * mr[0];
+          const double phb = (1.0 - gam) * shb + gam * mr[1];
+          double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int e = 0; e < EPT; ++e) {
+            const int i = c.src(e);
+            const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
+            const double wa0 = i < n ? sal[i] : 0.0, wb0 = i < m ? sbe[i] : 0.0;
+            const double wa = bops::wexp(wa0, -f[e] * i1 - gam * va - pha, tab);
+            const double wb = bops::wexp(wb0, -g[e] * i2 - gam * vb - phb, tab);
+            const double xa = va - ca, xb = vb - cb;
+            mom[0] += wa;
+            mom[1] += wa * xa;
+            mom[2] += wa * xa * xa;
+            mom[3] += wb;
+            mom[4] += wb * xb;
+            mom[5] += wb * xb * xb;
+          }
+          bops::block_sum<FW_NW, 6>(mom, ping.next());
+          const double a1 = mom[1] / mom[0], a2 = mom[2] / mom[0];
+          const double b1 = mom[4] / mom[3], b2 = mom[5] / mom[3];
+          const double g1 = k0 - t1 * a1 - t2 * b1;
+          const double g2 = t1 * (a2 - a1 * a1) + t2 * (b2 - b1 * b1);
+          if (g1 < 0.0)
+            lo = gam;
+          else
+            hi = gam;
+          if (gam >= 1.0 && g1 <= 0.0) {
+            gam = 1.0;
+            break;
+          }
+          double nxt = (g2 > 0.0) ? gam - g1 / g2 : 0.5 * (lo + hi);
+          const bool newton = nxt > lo && nxt < hi;
+          if (!newton) nxt = 0.5 * (lo + hi);
+          // Newton converges quadratically: once a Newton step is below
+          // 1e-9 the next iterate is exact to rounding (the reference's
+          // ternary search resolves gamma to ~1e-5 on flat problems).
+          const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(1.0, gam)) ||
+                            g1 == 0.0 || hi - lo <= 1e-15;
+          gam = nxt;
+          if (conv) break;
+        }
+      }
+    }
+    if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
+    // --- update (fw.py:227-230) and the next shift bounds
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      f[e] = (1.0 - gam) * f[e] + gam * r[e];
+      g[e] = (1.0 - gam) * g[e] + gam * s[e];
+    }
+    if (sha > -CUDART_INF) sha = (1.0 - gam) * sha + gam * mr[0];
+    if (shb > -CUDART_INF) shb = (1.0 - gam) * shb + gam * mr[1];
+  }
+  // --- finalize: translate by lambda* (fw.py:235-252), exact maxima
+  double mx[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
+    if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
+  }
+  bops::block_max<FW_NW, 2>(mx, ping.next());
+  double ls[2] = {0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n) ls[0] += bops::wexp(sal[i], -f[e] * i1 - mx[0], tab);
+    if (i < m) ls[1] += bops::wexp(sbe[i], -g[e] * i2 - mx[1], tab);
+  }
+  bops::block_sum<FW_NW, 2>(ls, ping.next());
+  const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(ls[0])) - (mx[1] + log(ls[1])));
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = c.src(e);
+    if (i < n) A.f[(long)b * n + i] = f[e] + lam;
+    if (i < m) A.g[(long)b * m + i] = g[e] - lam;
+  }
+  if (threadIdx.x == 0) {
+    A.iterations[b] = iters;
+    A.status[b] = status;
+    A.summary[b * 3 + 0] = last_primal;
+    A.summary[b * 3 + 1] = last_dual;
+    A.summary[b * 3 + 2] = lam;
+  }
+}
+
+inline int ept_for(int nm) {
+  const int per = (nm + FW_THREADS - 1) / FW_THREADS;
+  if (per <= 1) return 1;
+  if (per <= 2) return 2;
+  if (per <= 4) return 4;
+  if (per <= 8) return 8;
+  if (per <= 16) return 16;
+  return -1;
+}
+
+inline size_t fw_smem(int n, int m, bool pairwise) {
+  return sizeof(double) * 3 * (size_t)(n + m) + sizeof(unsigned short) * (size_t)(n + m) +
+         (pairwise ? 16 + sizeof(double) * (size_t)(n + m) : 0);
+}
+
+template <bool PW>
+int launch_fw_impl(const FwArgs& a, int batch, cudaStream_t st) {
+  const int ept = ept_for(std::max(a.n, a.m));
+  if (ept < 0) {
+    set_error("1-D FW / OT kernel supports n, m <= %d per problem", 16 * FW_THREADS);
+    return UOT_INVALID;
+  }
+  const size_t smem = fw_smem(a.n, a.m, PW);
+  if (smem > 227 * 1024) {
+    set_error("pairwise FW keeps n + m <= ~6600 atoms per problem in shared memory");
+    return UOT_INVALID;
+  }
+  auto go = [&](auto kern) -> int {
+    UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    kern<<<batch, FW_THREADS, smem, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  };
+  auto by_ept = [&](auto pk) -> int {
+    constexpr int PK = decltype(pk)::value;
+    switch (ept) {
+      case 1: return go(fw1d_kernel<1, PK, PW>);
+      case 2: return go(fw1d_kernel<2, PK, PW>);
+      case 4: return go(fw1d_kernel<4, PK, PW>);
+      case 8: return go(fw1d_kernel<8, PK, PW>);
+      default: return go(fw1d_kernel<16, PK, PW>);
+    }
+  };
+  if (a.p == 2.0) return by_ept(std::integral_constant<int, 0>());
+  if (a.p == 1.0) return by_ept(std::integral_constant<int, 1>());
+  return by_ept(std::integral_constant<int, 2>());
+}
+
+// pairwise instantiation lives in fw1d_pfw.cu (separate translation unit:
+// the pairwise branch otherwise raises register pressure / spills of the
+// FW and OT kernels)
+int launch_fw_pairwise(const FwArgs& a, int batch, cudaStream_t st);
+
+}  // namespace fwk
+}  // namespace uot
