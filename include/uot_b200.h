@@ -42,7 +42,7 @@ enum {
 };
 
 enum { UOT_F32 = 0, UOT_F64 = 1 };
-enum { UOT_SINKHORN_F = 0, UOT_SINKHORN_H = 1 };
+enum { UOT_SINKHORN_F = 0, UOT_SINKHORN_H = 1, UOT_SINKHORN_G = 2 };
 /* Ground costs: squared Euclidean between d-dim point clouds; |x-y|^p on 1-D
  * points (src/measures.py:93-105 PowerDistance); dense explicit matrix
  * (src/measures.py:108-122 ExplicitMatrix). */
@@ -56,16 +56,18 @@ int uot_device_arch(int device, int* sm_major, int* sm_minor);
 
 /* ------------------------------------------------------------------------
  * Sinkhorn: replaces src/sinkhorn.py:246-315 `run(prob, config, init)` for
- * variants "f" (f_sinkhorn_step, :103-114) and "h" (h_sinkhorn_step,
- * :137-163) with KL marginals (KL(rho1), KL(rho2)), for a batch of
+ * variants "f" (f_sinkhorn_step, :103-114), "h" (h_sinkhorn_step,
+ * :137-163) and "g" (g_sinkhorn_step, :117-134: translated steps at the
+ * incoming lambda, then lambda* of the new pair; unsharded) with KL marginals (KL(rho1), KL(rho2)), for a batch of
  * independent problems, with a fixed iteration budget and the reference's
  * optional `delta_f < tol` stop (:304-306) evaluated per problem.
  *
  * Inputs (dtype elements): x [batch][n][d], y [batch][m][d] (d = 1 for
  * UOT_COST_POWER); explicit costs c [batch][n][m] and its transpose
  * ct [batch][m][n]; weights a [batch][n], b [batch][m].  f [batch][n] holds
- * the initial f when init_given (the g input is unused by both variants,
- * exactly as in the reference) and receives the final pair with g.
+ * the initial f when init_given (the g input is unused by "f" and "h", as in
+ * the reference; "g" starts from lambda*(f, g) of the given pair, :263-265)
+ * and receives the final pair with g.
  * trace_delta [batch][iters] (fp64) receives ||f_t - f_{t-1}||_inf,
  * iterations [batch] the number of steps taken.
  *

@@ -224,13 +224,32 @@ def h_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2):
     return f_new, g_new
 
 
+def g_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2, lam):
+    """sinkhorn.py:117-134 with KL aprox: both half-updates at the incoming
+    translation lam, then lambda* of the new pair (duality.py:175-178).
+    Returns (f', g', lambda')."""
+    smin_a = cost.smin_cols(f + lam, eps, aw)
+    g_new = lam + (r2 / (eps + r2)) * smin_a
+    smin_b = cost.smin_rows(g_new - lam, eps, bw)
+    f_new = -lam + (r1 / (eps + r1)) * smin_b
+    return f_new, g_new, lambda_star_kl(aw, bw, f_new, g_new, r1, r2)
+
+
 def sinkhorn_fixed(cost, aw, bw, eps, r1, r2, variant, iters, f0=None, g0=None):
     """sinkhorn.py:246-315 (run) with the early exit removed (:304-306):
-    exactly ``iters`` steps; returns (f, g, delta_f trace)."""
+    exactly ``iters`` steps; returns (f, g, delta_f trace).  Variant "g"
+    starts from lambda*(f0, g0) (:263-265) and carries lambda (:270-271)."""
     f = np.zeros(cost.n) if f0 is None else _c64(f0).copy()
     g = np.zeros(cost.m) if g0 is None else _c64(g0).copy()
-    step = h_sinkhorn_step if variant == "h" else f_sinkhorn_step
     deltas = np.empty(iters)
+    if variant == "g":
+        lam = lambda_star_kl(aw, bw, f, g, r1, r2)
+        for t in range(iters):
+            fn, gn, lam = g_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2, lam)
+            deltas[t] = float(np.abs(fn - f).max())
+            f, g = fn, gn
+        return f, g, deltas
+    step = h_sinkhorn_step if variant == "h" else f_sinkhorn_step
     for t in range(iters):
         fn, gn = step(cost, aw, bw, f, g, eps, r1, r2)
         deltas[t] = float(np.abs(fn - f).max())

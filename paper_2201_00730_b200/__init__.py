@@ -37,6 +37,7 @@ from .sinkhorn import (
     SinkhornConfig,
     SolverReport,
     f_sinkhorn_step,
+    g_sinkhorn_step,
     h_sinkhorn_step,
     run,
     sinkhorn_batched,

@@ -17,7 +17,7 @@ SO_PATH = os.environ.get("UOT_B200_LIB") or os.path.join(_HERE, "_uot_b200.so")
 
 UOT_OK = 0
 F32, F64 = 0, 1
-SINKHORN_F, SINKHORN_H = 0, 1
+SINKHORN_F, SINKHORN_H, SINKHORN_G = 0, 1, 2
 COST_SQEUCLID, COST_POWER, COST_EXPLICIT = 0, 1, 2
 STEP_HARMONIC, STEP_LINESEARCH, STEP_PAIRWISE = 0, 1, 2
 

@@ -740,9 +740,20 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
   }
   if (threadIdx.x == 0) {
     const double shat = -A.rho_out * (q.m + log(q.s));
-    const double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
+    double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
+    if (A.gmode && A.mode != 1) {
+      // G (src/sinkhorn.py:128-132): g' = lam + a2 smin_cols(f + lam) = a2 smin_cols(f) +
+      // (1 - a2) lam, f' = -lam + a1 smin_rows(g' - lam) = a1 smin_rows(g') - (1 - a1) lam
+      tau = (A.out_side == 1 ? 1.0 : -1.0) * (1.0 - A.a_coef) * A.sc[b].lam;
+    }
     A.sc[b].shat[A.out_side] = shat;
     A.sc[b].tau[A.out_side] = tau;
+    if (A.gmode && A.out_side == 0) {
+      // lambda* of the new pair (duality.py:175-178) from the softmins
+      // S = Smin(hat) + tau of both sides: (rho1 S_g - rho2 S_f) / (rho1 + rho2)
+      const double Sf = shat + tau, Sg = A.sc[b].shat[1] + A.sc[b].tau[1];
+      A.sc[b].lam = (A.rho1 * Sg - A.rho2 * Sf) / (A.rho1 + A.rho2);
+    }
     if (A.hat_old != nullptr && A.trace != nullptr) {
       const double delta = fmax(qmax + tau, -(qmin + tau));
       A.trace[(long)b * A.trace_len + A.t] = delta;
@@ -814,7 +825,7 @@ __global__ void sk_reset(int batch, SkScalars* sc, unsigned int* counters, int* 
                          int* iters_done) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < batch) {
-    sc[b] = SkScalars{{0.0, 0.0}, {0.0, 0.0}};
+    sc[b] = SkScalars{{0.0, 0.0}, {0.0, 0.0}, 0.0};
     counters[b] = 0u;
     done[b] = 0;
     iters_done[b] = 0;
@@ -1169,6 +1180,9 @@ struct Engine {
     a.k_coef = H ? (eps / (eps + ro)) * (ro / (r1 + r2)) : 0.0;
     const double kk = (eps / (eps + ro)) * (rother / (r1 + r2));
     a.tau_fac = H ? kk / (1.0 - kk) : 0.0;
+    a.gmode = d.variant == UOT_SINKHORN_G ? 1 : 0;
+    a.rho1 = r1;
+    a.rho2 = r2;
     a.rho_out = ro;
     a.hat_out = hat_out;
     a.hat_old = hat_old;
@@ -1252,6 +1266,20 @@ struct Engine {
     }
     double* trace = d.trace_delta != nullptr ? d.trace_delta : bf.trace;
     const int trace_len = std::max(d.iters, 1);
+    if (d.variant == UOT_SINKHORN_G) {
+      // G starts from lambda*(f0, g0) (src/sinkhorn.py:263-265): Smin_b(g0)
+      // first, the f0 init tail then forms lambda.
+      const T* g0 = d.init_given ? (const T*)d.g : bf.zeros;
+      if (d.init_given) {
+        UOT_CUDA_TRY(cudaMemcpyAsync(bf.hatB, g0, sizeof(T) * (size_t)d.batch * d.m,
+                                     cudaMemcpyDeviceToDevice, st));
+        g0 = bf.hatB;
+      } else {
+        sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * nm, bf.zeros);
+        UOT_CHECK_LAUNCH();
+      }
+      UOT_TRY(launch_tail(d, bf, st, true, 1, 0, nullptr, bf.hatB, g0, 0, nullptr, trace_len));
+    }
     // init: hat_f = f0, Smin_a(f0), pack source records.
     UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, f0, 0, nullptr, trace_len));
     const int sB = splits(d.batch, d.m, d.n, d.d);  // g-update splits
@@ -1562,8 +1590,13 @@ int validate(const uot_sinkhorn_desc* d) {
     set_error("rho must be positive and finite");  // src/entropies.py:46-48
     return UOT_INVALID;
   }
-  if (d->variant != UOT_SINKHORN_F && d->variant != UOT_SINKHORN_H) {
-    set_error("variant must be F (0) or H (1)");
+  if (d->variant != UOT_SINKHORN_F && d->variant != UOT_SINKHORN_H &&
+      d->variant != UOT_SINKHORN_G) {
+    set_error("variant must be F (0), H (1) or G (2)");
+    return UOT_INVALID;
+  }
+  if (d->variant == UOT_SINKHORN_G && (d->nranks > 1 || d->nccl_comm != nullptr)) {
+    set_error("the G variant runs unsharded");
     return UOT_INVALID;
   }
   if (d->cost == UOT_COST_POWER && (d->d != 1 || !(d->p >= 1.0))) {

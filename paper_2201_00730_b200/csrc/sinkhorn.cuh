@@ -28,6 +28,7 @@ namespace uot {
 struct SkScalars {
   double shat[2];  // Smin^{rho_s}_{w_s}(hat_s) of side s (0 = source/f, 1 = target/g)
   double tau[2];   // lazy translation of side s: potential_s = hat_s + tau[s]
+  double lam;      // G variant: translation of the current pair (lambda*)
 };
 
 template <typename T>
@@ -71,6 +72,8 @@ struct TailArgs {
   double eps, unit, inv_eu;    // unit = ln2 (log2 domain) or 1; inv_eu = 1/(eps*unit)
   double a_coef, k_coef;       // hat = a*smin - k*(shat_red + tau_red)
   double tau_fac;              // tau_out = tau_fac * shat_out
+  int gmode;                   // G variant: tau_out = +-(1 - a) lam, then lam = lambda*
+  double rho1, rho2;
   double rho_out;
   T* hat_out;                  // [B][nout]
   const T* hat_old;            // [B][nout] or nullptr (delta tracking)

@@ -91,7 +91,7 @@ def _geometry(prob):
 
 def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
                      c=None, f0=None, tol=None, precision="fp32", stream=None, comm=None,
-                     nranks=1, rank=0, shard_rows=None):
+                     nranks=1, rank=0, shard_rows=None, g0=None):
     """Batched Sinkhorn on device.
 
     x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
@@ -103,6 +103,8 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     ``distributed.NcclComm``) the x / a / f0 given are this rank's rows and
     the returned f is this rank's slice; with ``comm=None, nranks > 1`` and
     ``shard_rows`` the same protocol runs for all shards in this process.
+    Variant "g" (src/sinkhorn.py:117-134) starts from lambda*(f0, g0) and
+    returns the overparameterised pair (plain potentials (f + lam, g - lam)).
     """
     t = D.torch()
     lib = _lib.load()
@@ -126,10 +128,17 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     g = D.empty((B, m), dt)
     if f0 is not None:
         f.copy_(D.to_dev(f0, dt).reshape(B, n))
+        if variant == "g":
+            if g0 is None:
+                g.zero_()
+            else:
+                g.copy_(D.to_dev(g0, dt).reshape(B, m))
+    if variant not in ("f", "g", "h"):
+        raise ValueError("variant must be one of 'f', 'g', 'h'")
     trace = D.empty((B, iters), t.float64)
     its = D.empty((B,), t.int32)
     desc = _lib.SinkhornDesc(
-        variant=_lib.SINKHORN_H if variant == "h" else _lib.SINKHORN_F,
+        variant={"h": _lib.SINKHORN_H, "f": _lib.SINKHORN_F, "g": _lib.SINKHORN_G}[variant],
         dtype=_lib.F32 if dt == t.float32 else _lib.F64, cost=kind, batch=B, n=n, m=m,
         d=1 if kind != _lib.COST_SQEUCLID else d, p=float(p), eps=float(eps),
         rho1=float(rho1), rho2=float(rho2), x=_lib.ptr(x), y=_lib.ptr(y), c=_lib.ptr(cm),
@@ -182,6 +191,29 @@ def f_sinkhorn_step(prob, d):
     return _one_step(prob, d, "f")
 
 
+def g_sinkhorn_step(prob, d, lam):
+    """One translated step at the incoming translation lam
+    (src/sinkhorn.py:117-134); returns (pair, new_lam).  KL marginals.
+
+    The kernel starts a G run from lambda*(f, g); the step depends on g only
+    through that scalar, so g is shifted to make lambda*(f, g') = lam
+    (lambda* moves by c rho1 / (rho1 + rho2) when g moves by c)."""
+    _require_positive_eps(prob)
+    prob.check_pair(d)
+    require_kl(prob.ent1, prob.ent2, what="g-sinkhorn")
+    r1, r2 = prob.ent1.rho, prob.ent2.rho
+    lam0 = float(kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, r1, r2)[0, 0].item())
+    g_in = np.asarray(d.g, dtype=np.float64) + (float(lam) - lam0) * (r1 + r2) / r1
+    costname, p, x, y, C = _step_inputs(prob)
+    f, g, _, _ = sinkhorn_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.eps, r1, r2,
+                                  1, variant="g", cost=costname, p=p, c=C, f0=d.f, g0=g_in,
+                                  precision="fp64")
+    pair = DualPair(D.to_np(f[0]), D.to_np(g[0]))
+    new_lam = float(kl_scalars(prob.alpha.weights, prob.beta.weights, pair.f, pair.g, r1,
+                               r2)[0, 0].item())
+    return pair, new_lam
+
+
 def h_sinkhorn_step(prob, d):
     """One translation-invariant step, g then f (src/sinkhorn.py:137-163)."""
     _require_positive_eps(prob)
@@ -203,8 +235,6 @@ def run(prob, config, init=None, reference=None):
     if config.variant == "h" and not (isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)):
         raise UnsupportedEntropyError("h-sinkhorn requires kl penalties on both marginals")
     require_kl(prob.ent1, prob.ent2, what="sinkhorn")
-    if config.variant == "g":
-        raise UnsupportedEntropyError("the g variant is not on the B200 path (use 'h')")
     if config.anderson is not None:
         raise UnsupportedEntropyError("Anderson extrapolation is not on the B200 path")
     t = D.torch()
@@ -221,7 +251,7 @@ def run(prob, config, init=None, reference=None):
         f, g, tr, its = sinkhorn_batched(
             x, y, prob.alpha.weights, prob.beta.weights, prob.eps, prob.ent1.rho, prob.ent2.rho,
             k, variant=config.variant, cost=costname, p=p, c=C, f0=f_cur, tol=config.tol,
-            precision=config.precision)
+            precision=config.precision, g0=g_cur if config.variant == "g" else None)
         t.cuda.synchronize()
         el = time.perf_counter_ns() - t0
         got = int(its[0].item())

@@ -41,15 +41,65 @@ def save(name, **arrays):
     print(f"wrote {name} ({os.path.getsize(path) / 1024:.1f} KiB)")
 
 
-def ref_sinkhorn(prob, variant, iters):
-    d = U.DualPair.zeros(len(prob.alpha), len(prob.beta))
+def ref_sinkhorn(prob, variant, iters, d0=None):
+    d = U.DualPair.zeros(len(prob.alpha), len(prob.beta)) if d0 is None else d0
     deltas = []
+    if variant == "g":  # run(): lam = lambda_star(d0), then g_sinkhorn_step (:263-271)
+        lam = U.lambda_star(prob, d)
+        for _ in range(iters):
+            new, lam = US.g_sinkhorn_step(prob, d, lam)
+            deltas.append(float(np.abs(new.f - d.f).max()))
+            d = new
+        return d.f, d.g, np.asarray(deltas)
     step = US.h_sinkhorn_step if variant == "h" else US.f_sinkhorn_step
     for _ in range(iters):
         new = step(prob, d)
         deltas.append(float(np.abs(new.f - d.f).max()))
         d = new
     return d.f, d.g, np.asarray(deltas)
+
+
+def gen_sinkhorn_g():
+    """G-Sinkhorn (sinkhorn.py:117-134) on small 1-D problems, from zeros and
+    from a nonzero initial pair, plus the cfg1 setting."""
+    rng = np.random.default_rng(41)
+    out = {}
+    cases = []
+    for k in range(8):
+        n, m = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+        p = [1.0, 2.0, 1.5][k % 3]
+        eps = [0.05, 0.5, 0.2][k % 3]
+        r1, r2 = float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.3, 2.0))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m) * 1.7
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=eps)
+        f0 = g0 = None
+        if k % 2 == 1:  # feasible nonzero start: half the row / column minima
+            C = np.abs(x[:, None] - y[None, :]) ** p
+            f0, g0 = 0.5 * C.min(axis=1) + 0.1, 0.5 * C.min(axis=0) - 0.1
+        d0 = None if f0 is None else U.DualPair(f0, g0)
+        f, g, dl = ref_sinkhorn(prob, "g", 40, d0)
+        out[f"c{k}_f"], out[f"c{k}_g"], out[f"c{k}_delta"] = f, g, dl
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_f0"] = np.zeros(n) if f0 is None else f0
+        out[f"c{k}_g0"] = np.zeros(m) if g0 is None else g0
+        out[f"c{k}_par"] = np.array([p, eps, r1, r2, 40, 0.0 if f0 is None else 1.0])
+        cases.append(k)
+    c = S.cfg1_inputs()
+    prob = U.UotProblem(U.DiscreteMeasure(c.x, c.alpha), U.DiscreteMeasure(c.y, c.beta),
+                        U.PowerDistance(2.0), U.KL(c.rho), U.KL(c.rho), eps=c.eps)
+    f, g, dl = ref_sinkhorn(prob, "g", c.iters)
+    k = 8
+    out[f"c{k}_f"], out[f"c{k}_g"], out[f"c{k}_delta"] = f, g, dl
+    out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = c.x, c.y, c.alpha, c.beta
+    out[f"c{k}_f0"], out[f"c{k}_g0"] = np.zeros(len(c.x)), np.zeros(len(c.y))
+    out[f"c{k}_par"] = np.array([2.0, c.eps, c.rho, c.rho, c.iters, 0.0])
+    cases.append(k)
+    out["cases"] = np.array(cases)
+    save("sinkhorn_g.npz", **out)
 
 
 def gen_cfg1():
@@ -418,7 +468,7 @@ def gen_duality():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
-                             "mot", "barycenter", "duality", "pfw"]
+                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -19,6 +19,20 @@ def test_cfg1_h_and_f_1000_iterations():
                                    atol=1e-13 * np.abs(z[f"{v}_f"]).max())
 
 
+def test_sinkhorn_g_cases():
+    """G-Sinkhorn restatement vs the reference's own g_sinkhorn_step loop."""
+    z = golden("sinkhorn_g.npz")
+    for k in cases(z):
+        p, eps, r1, r2, iters, hasinit = z[f"c{k}_par"]
+        cost = O.PointCost(z[f"c{k}_x"], z[f"c{k}_y"], p=p, power1d=True)
+        f0 = z[f"c{k}_f0"] if hasinit else None
+        g0 = z[f"c{k}_g0"] if hasinit else None
+        f, g, dl = O.sinkhorn_fixed(cost, z[f"c{k}_a"], z[f"c{k}_b"], eps, r1, r2, "g",
+                                    int(iters), f0, g0)
+        assert rel_err(f, g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-11
+        np.testing.assert_allclose(dl, z[f"c{k}_delta"], rtol=1e-8, atol=1e-13)
+
+
 def test_sinkhorn_small_cases():
     z = golden("sinkhorn_small.npz")
     for k in cases(z):

@@ -173,3 +173,38 @@ def test_tcgen05_point_clouds_vs_oracle(d, n, m):
         fr, gr = translated(a[k], b[k], fo, go, rho, rho)
         assert np.abs(ft - fr).max() <= 1e-4 * eps, (k, np.abs(ft - fr).max())
         assert np.abs(gt - gr).max() <= 1e-4 * eps
+
+
+# ---------------------------------------------------------------------------
+# G-Sinkhorn (src/sinkhorn.py:117-134), §8f row 2
+
+
+@pytest.mark.parametrize("k", range(9))
+def test_g_sinkhorn_matches_reference(k):
+    z = golden("sinkhorn_g.npz")
+    p, eps, r1, r2, iters, hasinit = z[f"c{k}_par"]
+    f0 = z[f"c{k}_f0"] if hasinit else None
+    g0 = z[f"c{k}_g0"] if hasinit else None
+    f, g, dl, its = P.sinkhorn_batched(z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"], z[f"c{k}_b"],
+                                       eps, r1, r2, int(iters), variant="g", cost="power", p=p,
+                                       f0=f0, g0=g0, precision="fp64")
+    fg, gg = D.to_np(f[0]), D.to_np(g[0])
+    assert rel_err(fg, gg, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-9
+    np.testing.assert_allclose(D.to_np(dl[0]), z[f"c{k}_delta"], rtol=1e-6, atol=1e-12)
+
+
+def test_g_sinkhorn_step_api():
+    """g_sinkhorn_step(prob, d, lam) mirrors the reference's signature."""
+    z = golden("sinkhorn_g.npz")
+    k = 1
+    p, eps, r1, r2, _, _ = z[f"c{k}_par"]
+    prob = P.UotProblem(P.DiscreteMeasure(z[f"c{k}_x"], z[f"c{k}_a"]),
+                        P.DiscreteMeasure(z[f"c{k}_y"], z[f"c{k}_b"]), P.PowerDistance(p),
+                        P.KL(r1), P.KL(r2), eps=eps)
+    d = P.DualPair(z[f"c{k}_f0"], z[f"c{k}_g0"])
+    cost = O.PointCost(z[f"c{k}_x"], z[f"c{k}_y"], p=p, power1d=True)
+    lam = 0.123
+    fr, gr, lr = O.g_sinkhorn_step(cost, z[f"c{k}_a"], z[f"c{k}_b"], d.f, d.g, eps, r1, r2, lam)
+    pair, lam_new = P.g_sinkhorn_step(prob, d, lam)
+    assert rel_err(pair.f, pair.g, fr, gr) < 1e-9
+    assert abs(lam_new - lr) < 1e-9 * max(1.0, abs(lr))
