@@ -103,6 +103,19 @@ typedef struct uot_sinkhorn_desc {
 } uot_sinkhorn_desc;
 
 int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);
+
+/* Verification of a given pair at scale: f, g of the
+ * descriptor are INPUTS (not modified; iters / init_given ignored).  Two
+ * on-the-fly cost passes, no N x M matrix.  out [batch][8] (fp64):
+ *   [0] res_g = max_j |g - a2 smin_cols(f) - eps/(eps+rho2) lam|  (src/sinkhorn.py:166-189)
+ *   [1] log <alpha x beta, exp((f + g - C)/eps)>                 (src/duality.py:124-132)
+ *   [2] res_f = max_i |f - a1 smin_rows(g) + eps/(eps+rho1) lam|
+ *   [4] lam = lambda*(f, g) (KL, duality.py:175-178)
+ *   [5] Smin_alpha^rho1(f), [6] Smin_beta^rho2(g)  (entropies.py:187-200)
+ * from which eval_F / eval_G / eval_H follow in closed form (KL).
+ * Workspace: uot_sinkhorn_workspace_size of the same descriptor. */
+int uot_sinkhorn_verify(const uot_sinkhorn_desc* desc, void* workspace, size_t workspace_bytes,
+                        void* stream, double* out);
 int uot_sinkhorn_run(const uot_sinkhorn_desc* desc, void* workspace, size_t workspace_bytes,
                      void* stream);
 

@@ -7,7 +7,17 @@ CUDA kernels of ``csrc/`` through the C-ABI declared in ``include/uot_b200.h``;
 there is no CPU fallback.
 """
 
-from .duality import DualPair, UotProblem, kl_scalars, lambda_star, translate
+from .duality import (
+    DualPair,
+    UotProblem,
+    dual_feasibility_violation,
+    eval_F,
+    eval_G,
+    eval_H,
+    kl_scalars,
+    lambda_star,
+    translate,
+)
 from .entropies import KL, Balanced, Berg
 from .exceptions import (
     InfeasibleDualError,
@@ -38,9 +48,11 @@ from .sinkhorn import (
     SolverReport,
     f_sinkhorn_step,
     g_sinkhorn_step,
+    h_optimality_residual,
     h_sinkhorn_step,
     run,
     sinkhorn_batched,
+    verify_batched,
 )
 
 __version__ = "0.1.0"

@@ -764,6 +764,71 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Verification at scale (§8f row 3): one side of a given pair (f, g).  After
+// a main pass that reduced the OTHER side's records over every output o,
+// folds the split partials into smin_o (src/sinkhorn.py:93-100) and per
+// problem reduces (one CTA per problem):
+//   res = max_o |pot_o - a smin_o + sgn (eps/(eps+rho)) lam|   (:166-189)
+//   L   = LSE_o(-smin_o/eps + pot_o/eps; w)  -- the log of <a x b, e^((f+g-C)/eps)>
+//         (duality.py:124-132) when this is the target side.
+// out[b*8 + base + 0..1] = (res, L).
+template <typename T>
+__global__ void __launch_bounds__(256) sk_verify_side(int nout, int nparts, const T* part_m,
+                                                     const T* part_a, const T* pot, const T* w,
+                                                     double eps, double unit, double a_coef,
+                                                     double lam_coef, const double* lam,
+                                                     double* out, int base) {
+  using D = Dom<T>;
+  __shared__ double s_m[32], s_s[32], s_x[32];
+  const int b = blockIdx.x;
+  const long pb = (long)b * nparts * nout;
+  const double lm = lam[b];
+  double res = 0.0;
+  LsePair L{-CUDART_INF, 0.0};
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    double M = -CUDART_INF;
+    for (int s = 0; s < nparts; ++s) {
+      const double a = (double)part_a[pb + (long)s * nout + o];
+      if (a > 0.0) M = fmax(M, (double)part_m[pb + (long)s * nout + o]);
+    }
+    double acc = 0.0;
+    for (int s = 0; s < nparts; ++s) {
+      const double a = (double)part_a[pb + (long)s * nout + o];
+      if (a > 0.0) acc += a * D::exd((double)part_m[pb + (long)s * nout + o] - M);
+    }
+    const double lse = M + D::lgd(acc);  // domain units
+    const double smin = -eps * unit * lse;
+    const double pv = (double)pot[(long)b * nout + o];
+    res = fmax(res, fabs(pv - a_coef * smin + lam_coef * lm));
+    const double wv = (double)w[(long)b * nout + o];
+    if (wv > 0.0) L = lse_merge(L, LsePair{unit * lse + pv / eps, wv});
+  }
+  res = block_reduce(res, s_x, MaxOp(), 0.0);
+  L = block_lse(L, s_m, s_s);
+  if (threadIdx.x == 0) {
+    out[(long)b * 8 + base + 0] = res;
+    out[(long)b * 8 + base + 1] = L.m + log(L.s);
+  }
+}
+
+// KL parts of the objectives and lambda* from the init tails' softmins.
+__global__ void sk_verify_kl(int batch, int n, int m, const SkScalars* sc, double rho1,
+                             double rho2, double* lam) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  // Smin(f) = shat[0], Smin(g) = shat[1] (tau = 0 after init tails)
+  lam[b] = (rho1 * sc[b].shat[1] - rho2 * sc[b].shat[0]) / (rho1 + rho2);
+}
+
+__global__ void sk_verify_pack(int batch, const SkScalars* sc, const double* lam, double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  out[(long)b * 8 + 4] = lam[b];
+  out[(long)b * 8 + 5] = sc[b].shat[0];
+  out[(long)b * 8 + 6] = sc[b].shat[1];
+}
+
 // Final pair: f = hat_f + tau_f, g = hat_g + tau_g (src/sinkhorn.py returns
 // the plain potentials, :163).
 template <typename T>
@@ -1304,6 +1369,66 @@ struct Engine {
     return UOT_OK;
   }
 
+  // ---- Verification of a given pair (d.f, d.g as inputs; not modified).
+  // out [batch][8]: res_g, log<a x b, e^((f+g-C)/eps)>, res_f, (unused),
+  // lambda*, Smin_a(f), Smin_b(g), (unused).
+  static int verify(const uot_sinkhorn_desc& d, void* ws, size_t ws_bytes, cudaStream_t st,
+                    double* out) {
+    Shape s = shape(d);
+    WsLayout L;
+    Buffers<T> bf;
+    const size_t need = layout<T>(s, std::max(d.iters, 1), L, &bf, (char*)ws);
+    if (ws_bytes < need) {
+      set_error("sinkhorn workspace too small: %zu < %zu", ws_bytes, need);
+      return UOT_INVALID;
+    }
+    sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
+                                                      bf.iters_done);
+    UOT_CHECK_LAUNCH();
+    if constexpr (std::is_same<P, SqE32TC>::value) {
+      tc_fill_dead<<<1024, 256, 0, st>>>(bf.recA, (long)d.batch * s.recA / tc_kp(d.d), d.d,
+                                         tc_kp(d.d));
+      tc_fill_dead<<<1024, 256, 0, st>>>(bf.recB, (long)d.batch * s.recB / tc_kp(d.d), d.d,
+                                         tc_kp(d.d));
+      const double Lr = (double)(float)(1.0 / (d.eps * Dom<float>::unit));
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x, d.batch, d.n, d.d,
+                                           tc_kp(d.d), Lr);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y, d.batch, d.m, d.d,
+                                           tc_kp(d.d), Lr);
+      UOT_CHECK_LAUNCH();
+    }
+    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
+    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.m, bf.shiftB);
+    UOT_CHECK_LAUNCH();
+    const int tl = std::max(d.iters, 1);
+    // records of both sides from the given pair (init tails: tau = 0)
+    UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, (const T*)d.f, 0, nullptr,
+                        tl));
+    UOT_TRY(launch_tail(d, bf, st, true, 1, 0, nullptr, bf.hatB, (const T*)d.g, 0, nullptr, tl));
+    double* lam = bf.trace;  // [batch] scratch (>= batch doubles)
+    sk_verify_kl<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, d.n, d.m, bf.sc, d.rho1,
+                                                         d.rho2, lam);
+    UOT_CHECK_LAUNCH();
+    const double a2 = d.rho2 / (d.rho2 + d.eps), a1 = d.rho1 / (d.rho1 + d.eps);
+    // g side: smin_cols(f) over all rows (:98) -> res_g, L
+    const int sB = splits(d.batch, d.m, d.n, d.d);
+    UOT_TRY(launch_main(d, bf, st, true, sB, 0, d.n, 0, sB));
+    sk_verify_side<T><<<d.batch, 256, 0, st>>>(d.m, sB, bf.part_m, bf.part_a, (const T*)d.g,
+                                               (const T*)d.b, d.eps, Dom<T>::unit, a2,
+                                               -(d.eps / (d.eps + d.rho2)), lam, out, 0);
+    UOT_CHECK_LAUNCH();
+    // f side: smin_rows(g) over all columns (:100) -> res_f
+    const int sA = splits(d.batch, d.n, d.m, d.d);
+    UOT_TRY(launch_main(d, bf, st, false, sA, 0, d.m, 0, sA));
+    sk_verify_side<T><<<d.batch, 256, 0, st>>>(d.n, sA, bf.part_m, bf.part_a, (const T*)d.f,
+                                               (const T*)d.a, d.eps, Dom<T>::unit, a1,
+                                               d.eps / (d.eps + d.rho1), lam, out, 2);
+    UOT_CHECK_LAUNCH();
+    sk_verify_pack<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, lam, out);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  }
+
   // ---- Row-sharded run (BASELINE cfg3 on P GPUs).  Every
   // rank owns a slice of the source rows and the whole target side.  Per
   // iteration: g-update partial LSEs over the local rows -> one (shift, sum)
@@ -1629,6 +1754,19 @@ extern "C" int uot_sinkhorn_run(const uot_sinkhorn_desc* desc, void* workspace,
   UOT_TRY(validate(desc));
   return dispatch(*desc, [&](auto eng) {
     return decltype(eng)::run(*desc, workspace, workspace_bytes, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int uot_sinkhorn_verify(const uot_sinkhorn_desc* desc, void* workspace,
+                                   size_t workspace_bytes, void* stream, double* out) {
+  using namespace uot;
+  UOT_TRY(validate(desc));
+  if (desc->nranks > 1 || desc->nccl_comm != nullptr) {
+    set_error("uot_sinkhorn_verify runs unsharded");
+    return UOT_INVALID;
+  }
+  return dispatch(*desc, [&](auto eng) {
+    return decltype(eng)::verify(*desc, workspace, workspace_bytes, (cudaStream_t)stream, out);
   });
 }
 

@@ -1,6 +1,7 @@
-"""Dual-pair / problem value types and the closed-form KL translation
-(src/duality.py:42-91, :160-178, :250-253, :279-303).  The reductions run in
-the ``uot_kl_scalars`` kernel."""
+"""Dual-pair / problem value types, the closed-form KL translation and the
+dual objectives (src/duality.py:42-91, :117-178, :250-303).  The reductions
+run in the ``uot_kl_scalars`` / ``uot_sinkhorn_verify`` kernels (no N x M
+cost matrix is formed)."""
 
 from __future__ import annotations
 
@@ -99,3 +100,88 @@ def translate(prob, d):
     """(f + t*, g - t*) (src/duality.py:250-253)."""
     lam = lambda_star(prob, d)
     return DualPair(d.f + lam, d.g - lam)
+
+
+DUAL_FEAS_TOL = 1e-9  # src/duality.py:39
+
+
+def _kl_parts(prob, sf, sg):
+    """From the softmins S = Smin^rho_w(pot): <w, rho(1 - e^(-pot/rho))> per side
+    and the coupled closed form of _eval_h_kl (duality.py:279-290)."""
+    r1, r2 = prob.ent1.rho, prob.ent2.rho
+    ma, mb = float(np.sum(prob.alpha.weights)), float(np.sum(prob.beta.weights))
+    la, lb = -sf / r1, -sg / r2  # LSE_a(-f/r1), LSE_b(-g/r2)
+    f_part = r1 * (ma - math.exp(la)) + r2 * (mb - math.exp(lb))
+    h_part = r1 * ma + r2 * mb - (r1 + r2) * math.exp((r1 * la + r2 * lb) / (r1 + r2))
+    return f_part, h_part, ma, mb
+
+
+def dual_feasibility_violation(prob, d):
+    """max(0, max_ij f_i + g_j - C_ij) (duality.py:117-121) on the device
+    (1-D |x - y|^p costs)."""
+    from .fw import feasibility_violation
+    from .measures import PowerDistance
+
+    prob.check_pair(d)
+    if not isinstance(prob.cost, PowerDistance):
+        raise UnsupportedEntropyError("the device feasibility check runs 1-D |x - y|^p costs")
+    return float(feasibility_violation(prob.alpha.points, prob.beta.points, d.f, d.g,
+                                       prob.cost.p)[0].item())
+
+
+def _eps_term(prob, d):
+    """eps (<a x b, e^((f+g-C)/eps)> - m_a m_b) (duality.py:124-132)."""
+    from .sinkhorn import _verify_prob
+
+    v = _verify_prob(prob, d)
+    ma, mb = float(np.sum(prob.alpha.weights)), float(np.sum(prob.beta.weights))
+    return prob.eps * (math.exp(v[1]) - ma * mb), v
+
+
+def eval_F(prob, d):
+    """Plain dual objective (duality.py:135-152), KL marginals."""
+    prob.check_pair(d)
+    require_kl(prob.ent1, prob.ent2, what="eval_F")
+    if prob.eps == 0:
+        from .exceptions import InfeasibleDualError
+
+        viol = dual_feasibility_violation(prob, d)
+        if viol > DUAL_FEAS_TOL:
+            raise InfeasibleDualError(f"dual constraint violated by {viol:.3e} at eps = 0")
+        out = kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.ent1.rho,
+                         prob.ent2.rho)
+        sf = float(out[0, 2].item())
+        sg = _smin(prob.beta.weights, prob.ent2.rho, d.g)
+        return _kl_parts(prob, sf, sg)[0]
+    et, v = _eps_term(prob, d)
+    return _kl_parts(prob, float(v[5]), float(v[6]))[0] - et
+
+
+def eval_G(prob, d, lam):
+    """Overparameterised dual: eval_F at (f + lam, g - lam) (duality.py:155-157)."""
+    return eval_F(prob, DualPair(d.f + lam, d.g - lam))
+
+
+def eval_H(prob, d):
+    """Translation-invariant dual (duality.py:256-276), KL closed form."""
+    prob.check_pair(d)
+    require_kl(prob.ent1, prob.ent2, what="eval_H")
+    if prob.eps == 0:
+        from .exceptions import InfeasibleDualError
+
+        viol = dual_feasibility_violation(prob, d)
+        if viol > DUAL_FEAS_TOL:
+            raise InfeasibleDualError(f"dual constraint violated by {viol:.3e} at eps = 0")
+        out = kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.ent1.rho,
+                         prob.ent2.rho)
+        return float(out[0, 1].item())
+    et, v = _eps_term(prob, d)
+    return _kl_parts(prob, float(v[5]), float(v[6]))[1] - et
+
+
+def _smin(w, rho, pot):
+    """Smin^rho_w(pot) = -rho LSE_w(-pot/rho) via the kl_scalars kernel."""
+    w = np.asarray(w, dtype=np.float64)
+    pot = np.asarray(pot, dtype=np.float64)
+    out = kl_scalars(w, w, pot, pot, rho, rho)
+    return float(out[0, 2].item())

@@ -163,6 +163,71 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     return f, g, trace, its
 
 
+def verify_batched(x, y, a, b, f, g, eps, rho1, rho2, cost="sqeuclid", p=2.0, c=None,
+                   precision="fp64", stream=None):
+    """uot_sinkhorn_verify on a batch of given pairs: returns the device
+    tensor out [B, 8] (res_g, log <a x b, e^((f+g-C)/eps)>, res_f, -, lambda*,
+    Smin_a(f), Smin_b(g), -) -- two on-the-fly cost passes, no N x M matrix."""
+    t = D.torch()
+    lib = _lib.load()
+    dt = t.float32 if precision == "fp32" else t.float64
+    kind = {"sqeuclid": _lib.COST_SQEUCLID, "power": _lib.COST_POWER,
+            "explicit": _lib.COST_EXPLICIT}[cost]
+    a = D.to_dev(a, dt)
+    b = D.to_dev(b, dt)
+    if a.ndim == 1:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    B, n = a.shape
+    m = b.shape[1]
+    x = D.to_dev(x, dt).reshape(B, n, -1)
+    y = D.to_dev(y, dt).reshape(B, m, -1)
+    d = x.shape[2]
+    cm = ct = None
+    if kind == _lib.COST_EXPLICIT:
+        cm = D.to_dev(c, dt).reshape(B, n, m)
+        ct = cm.transpose(1, 2).contiguous()
+    fd = D.to_dev(f, dt).reshape(B, n).contiguous()
+    gd = D.to_dev(g, dt).reshape(B, m).contiguous()
+    out = t.zeros((B, 8), dtype=t.float64, device=fd.device)
+    desc = _lib.SinkhornDesc(
+        variant=_lib.SINKHORN_F, dtype=_lib.F32 if dt == t.float32 else _lib.F64, cost=kind,
+        batch=B, n=n, m=m, d=1 if kind != _lib.COST_SQEUCLID else d, p=float(p), eps=float(eps),
+        rho1=float(rho1), rho2=float(rho2), x=_lib.ptr(x), y=_lib.ptr(y), c=_lib.ptr(cm),
+        ct=_lib.ptr(ct), a=_lib.ptr(a), b=_lib.ptr(b), f=_lib.ptr(fd), g=_lib.ptr(gd),
+        init_given=1, iters=1, tol=0.0, use_tol=0, trace_delta=None, iterations=None,
+        nccl_comm=None, nranks=1, rank=0, shard_rows=None)
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)),
+               "sinkhorn workspace")
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_sinkhorn_verify(ctypes.byref(desc), _lib.ptr(ws),
+                                       ctypes.c_size_t(size.value), _lib.stream_handle(stream),
+                                       _lib.ptr(out)), "uot_sinkhorn_verify")
+    return out
+
+
+def _verify_prob(prob, d):
+    if prob.eps <= 0:
+        raise ValueError("the entropic terms need eps > 0")
+    require_kl(prob.ent1, prob.ent2, what="dual objective")
+    costname, p, x, y, C = _step_inputs(prob)
+    out = verify_batched(x, y, prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.eps,
+                         prob.ent1.rho, prob.ent2.rho, cost=costname, p=p, c=C)
+    return D.to_np(out[0], readonly=False)
+
+
+def h_optimality_residual(prob, d, side="f"):
+    """Sup-norm stationarity residual of the invariant dual at the pair
+    (src/sinkhorn.py:166-189), computed on the device without C."""
+    prob.check_pair(d)
+    if not (isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)):
+        raise UnsupportedEntropyError("residual defined for kl penalties only")
+    if side not in ("f", "g"):
+        raise ValueError("side must be 'f' or 'g'")
+    v = _verify_prob(prob, d)
+    return float(v[2] if side == "f" else v[0])
+
+
 def _require_positive_eps(prob):
     if prob.eps <= 0:
         raise ValueError("sinkhorn iterations need eps > 0")

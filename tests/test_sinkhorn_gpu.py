@@ -208,3 +208,56 @@ def test_g_sinkhorn_step_api():
     pair, lam_new = P.g_sinkhorn_step(prob, d, lam)
     assert rel_err(pair.f, pair.g, fr, gr) < 1e-9
     assert abs(lam_new - lr) < 1e-9 * max(1.0, abs(lr))
+
+
+# ---------------------------------------------------------------------------
+# Verification at scale (§8f row 3): dual objectives and stationarity
+# residuals without the N x M matrix (uot_sinkhorn_verify)
+
+
+@pytest.mark.parametrize("variant", ["h", "f"])
+def test_dual_objective_matches_reference(variant):
+    z = golden("sinkhorn_small.npz")
+    for k in cases(z):
+        p, eps, r1, r2, _ = z[f"c{k}_par"]
+        prob = P.UotProblem(P.DiscreteMeasure(z[f"c{k}_x"], z[f"c{k}_a"]),
+                            P.DiscreteMeasure(z[f"c{k}_y"], z[f"c{k}_b"]), P.PowerDistance(p),
+                            P.KL(r1), P.KL(r2), eps=eps)
+        d = P.DualPair(z[f"c{k}_{variant}_f"], z[f"c{k}_{variant}_g"])
+        ref = float(z[f"c{k}_{variant}_dual"])
+        got = P.eval_H(prob, d)
+        assert abs(got - ref) <= 1e-9 * max(1.0, abs(ref)), (k, got, ref)
+
+
+def test_dual_objective_cfg1_and_residual():
+    z = golden("cfg1.npz")
+    prob = P.UotProblem(P.DiscreteMeasure(z["x"], z["alpha"]), P.DiscreteMeasure(z["y"], z["beta"]),
+                        P.PowerDistance(2.0), P.KL(float(z["rho"])), P.KL(float(z["rho"])),
+                        eps=float(z["eps"]))
+    for v in ("h", "f"):
+        d = P.DualPair(z[f"{v}_f"], z[f"{v}_g"])
+        ref = float(z[f"{v}_dual"])
+        assert abs(P.eval_H(prob, d) - ref) <= 1e-9 * max(1.0, abs(ref))
+    # stationarity right after an H step (tests/test_sinkhorn.py:145-150 of the reference)
+    d = P.DualPair(z["h_f"], z["h_g"])
+    assert P.h_optimality_residual(prob, d, "f") < 1e-9
+    # eval_F and eval_G agree at the optimal translation: G(d, lam*) = H(d)
+    lam = P.lambda_star(prob, d)
+    assert abs(P.eval_G(prob, d, lam) - P.eval_H(prob, d)) < 1e-9
+
+
+def test_verify_matches_oracle_points():
+    """Point-cloud (fp32 on-the-fly) verification vs the oracle's dense terms."""
+    z = golden("cfg3_small.npz")
+    x, y, wa, wb = z["x"], z["y"], z["alpha"], z["beta"]
+    eps, rho = float(z["eps"]), float(z["rho"])
+    f, g = z["f"], z["g"]
+    out = D.to_np(P.verify_batched(x, y, wa, wb, f, g, eps, rho, rho, precision="fp64")[0])
+    cost = O.PointCost(x, y)
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    expo = (f[:, None] + g[None, :] - C) / eps
+    L = float(np.log(np.sum(wa[:, None] * wb[None, :] * np.exp(expo))))
+    assert abs(out[1] - L) < 1e-9 * max(1.0, abs(L))
+    res_f = np.abs(f - (rho / (rho + eps)) * cost.smin_rows(g, eps, wb)
+                   + (eps / (eps + rho)) * out[4]).max()
+    assert abs(out[2] - res_f) < 1e-9
