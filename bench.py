@@ -471,7 +471,7 @@ def run_cfg1(dev):
 
     c = S.cfg1_inputs()
     out = {}
-    for v in ("h", "f"):
+    for v in ("h", "f", "g"):
         P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, 1.0, 1.0, 10,
                            variant=v, cost="power", precision="fp64")
         torch.cuda.synchronize()
@@ -479,8 +479,34 @@ def run_cfg1(dev):
             P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, 1.0, 1.0,
                                1000, variant=v, cost="power", precision="fp64")
         out[v] = 1000 / (t.ms * 1e-3)
-    return {"workload": "cfg1: H and F Sinkhorn N=M=256 fp64, 1000 iterations (latency bound)",
-            "value": out["h"], "unit": "iter/s (H)", "f_variant_iter_s": out["f"], "dtype": "f64"}
+    return {"workload": "cfg1: H, F and G Sinkhorn N=M=256 fp64, 1000 iterations (latency bound)",
+            "value": out["h"], "unit": "iter/s (H)", "f_variant_iter_s": out["f"],
+            "g_variant_iter_s": out["g"], "dtype": "f64"}
+
+
+def run_cfg3_verify(dev):
+    """§8f row 3: dual objective (eps-term) and stationarity residuals of a
+    cfg3 pair at full size, two on-the-fly passes (the reference would need
+    a 32 GiB cost matrix)."""
+    import torch
+
+    import paper_2201_00730_b200 as P
+    from paper_2201_00730_b200 import synthetic as S
+
+    c = S.cfg3_inputs()
+    f, g, _, _ = P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps,
+                                    c.rho, c.rho, 20, variant="h", precision="fp32")
+    P.verify_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], f, g, c.eps, c.rho, c.rho,
+                     precision="fp32")
+    torch.cuda.synchronize()
+    with cuda_timer() as t:
+        out = P.verify_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None], f, g, c.eps,
+                               c.rho, c.rho, precision="fp32")
+    o = out[0].cpu().numpy()
+    return {"workload": "cfg3 pair after 20 H iterations: eps-term log-sum and both "
+                        "stationarity residuals, N=M=65536 d=2 fp32",
+            "value": t.ms, "unit": "ms per verification (2 on-the-fly passes)",
+            "res_f": float(o[2]), "res_g": float(o[0]), "log_eps_sum": float(o[1])}
 
 
 def run_cfg4(rank, world, dev):
@@ -581,6 +607,7 @@ def main():
             secondary["cfg4_sinkhorn_d64"] = run_cfg4(rank, world, dev)
             if rank == 0:
                 secondary["cfg1_sinkhorn_1d"] = run_cfg1(dev)
+                secondary["cfg3_verify"] = run_cfg3_verify(dev)
         if rank == 0:
             cpu_v, cpu_cores, cpu_sample = cpu_cfg3(S_inputs_cfg3())
             line["cpu_baseline"] = {"value": cpu_v, "unit": "iter/s", "cores": cpu_cores,
