@@ -243,6 +243,19 @@ int uot_mot1d_batched(int32_t batch, int32_t k, int32_t n, const int32_t* lens, 
                       const double* a, const double* omega_host, double* f, int32_t* idx,
                       double* mass, int32_t* count, int32_t* status, void* workspace,
                       size_t workspace_bytes, void* stream);
+
+/* Certificate of a balanced multi-marginal solution (replaces
+ * src/barycenter.py:261-295 `mot_certificate` + :236-240 `plan_cost` +
+ * :243-258 `dual_feasibility_exhaustive` for the barycentric cost).  Inputs
+ * as uot_mot1d_batched's outputs: f [batch][k][n], idx [batch][k*(n-1)+1][k],
+ * mass, count.  out [batch][6]: primal (plan cost), dual sum_k <a_k, f_k>,
+ * support violation max_e |sum_k f_k - Cc|, marginal violation, exhaustive
+ * feasibility violation (only when the grid has <= 1e5 tuples), and 1.0 if
+ * that sweep ran.  workspace >= 32 k + 256 bytes (device). */
+int uot_mot_certify(int32_t batch, int32_t k, int32_t n, const int32_t* lens, const double* x,
+                    const double* a, const double* omega_host, const double* f,
+                    const int32_t* idx, const double* mass, const int32_t* count, double* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
 int uot_bary_workspace_size(const uot_bary_desc* desc, size_t* bytes);
 int uot_bary_run(const uot_bary_desc* desc, void* workspace, size_t workspace_bytes,
                  void* stream);

@@ -32,10 +32,16 @@ from .barycenter import (
     BarycenterProblem,
     MultiDual,
     MultiPlan,
+    barycentric_cost_fn,
+    dual_feasibility_exhaustive,
     extract_barycenter,
     fw_barycenter,
     fw_barycenter_batched,
+    mot_certificate,
+    mot_certify_batched,
     multimarginal_cost,
+    multimarginal_lambda,
+    plan_cost,
     solve_mot_1d,
     solve_mot_1d_batched,
 )

@@ -67,7 +67,7 @@ EXPORTS = (
     "uot_version", "uot_last_error", "uot_device_arch",
     "uot_sinkhorn_workspace_size", "uot_sinkhorn_run", "uot_sinkhorn_verify", "uot_kl_scalars",
     "uot_ot1d_workspace_size", "uot_ot1d_batched", "uot_fw1d_workspace_size", "uot_fw1d_run", "uot_feasibility_1d",
-    "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_bary_workspace_size", "uot_bary_run",
+    "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_mot_certify", "uot_bary_workspace_size", "uot_bary_run",
     "uot_nccl_unique_id", "uot_nccl_comm_init", "uot_nccl_comm_destroy",
 )
 

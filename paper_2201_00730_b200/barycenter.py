@@ -23,6 +23,7 @@ from .fw import FwConfig
 from .measures import DiscreteMeasure
 from .sinkhorn import SolverReport
 
+EXHAUSTIVE_LIMIT = 10**5  # src/barycenter.py:44
 MASS_TOL = 1e-9  # src/barycenter.py:43
 
 
@@ -205,6 +206,121 @@ def solve_mot_1d(inputs, w=None, costfn=None):
     fd = D.to_np(f[0])
     plan = _plan_from(idx[0], mass[0], count[0].item())
     return plan, MultiDual(tuple(fd[q, :lens[q]] for q in range(len(inputs))))
+
+
+def barycentric_cost_fn(w):
+    """Tuple cost Cc(x) = sum_k w_k (x_k - B)^2 (src/barycenter.py:159-166)."""
+    w = np.asarray(w, dtype=np.float64)
+
+    def costfn(points):
+        return multimarginal_cost(points, w)[0]
+
+    costfn.weights = w
+    return costfn
+
+
+def mot_certify_batched(x, a, omega, f, idx, mass, count, lens=None, stream=None):
+    """uot_mot_certify on device tensors (layout of solve_mot_1d_batched):
+    returns out [B, 6] = (primal, dual, support violation, marginal
+    violation, exhaustive feasibility violation, exhaustive-sweep flag)."""
+    t = D.torch()
+    lib = _lib.load()
+    x, a, f = (D.to_dev(v, t.float64) for v in (x, a, f))
+    B, K, n = x.shape
+    idx = D.to_dev(idx, t.int32)
+    mass = D.to_dev(mass, t.float64)
+    count = D.to_dev(count, t.int32)
+    out = t.zeros((B, 6), dtype=t.float64, device=x.device)
+    om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+    ln = None if lens is None else np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
+    ws = D.workspace(64 * K + 512)
+    _lib.check(lib.uot_mot_certify(
+        B, K, n, ln.ctypes.data_as(ctypes.c_void_p) if ln is not None else None, _lib.ptr(x),
+        _lib.ptr(a), om.ctypes.data_as(ctypes.c_void_p), _lib.ptr(f), _lib.ptr(idx),
+        _lib.ptr(mass), _lib.ptr(count), _lib.ptr(out), _lib.ptr(ws), ctypes.c_size_t(64 * K + 512),
+        _lib.stream_handle(stream)), "uot_mot_certify")
+    D.torch().cuda.current_stream().synchronize()
+    return out
+
+
+def _certify_inputs(inputs, w, plan, duals):
+    inputs = tuple(inputs)
+    x, a, f, lens = _pack(inputs, extra=tuple(duals))
+    K, n = x.shape[1], x.shape[2]
+    cap = K * (n - 1) + 1
+    idx = np.zeros((1, cap, K), dtype=np.int32)
+    mass = np.zeros((1, cap))
+    e = len(plan)
+    if e > cap:
+        raise ValueError("plan has more entries than a monotone sweep can produce")
+    idx[0, :e] = plan.indices
+    mass[0, :e] = plan.mass
+    out = mot_certify_batched(x, a, w, f, idx, mass, np.array([e], dtype=np.int32), lens)
+    return D.to_np(out[0], readonly=False)
+
+
+def _weights_of(costfn, w):
+    if costfn is None:
+        if w is None:
+            raise ValueError("need barycentric weights when costfn is omitted")
+        return np.asarray(w, dtype=np.float64)
+    wf = getattr(costfn, "weights", None)
+    if wf is None:
+        from .exceptions import UnsupportedEntropyError
+
+        raise UnsupportedEntropyError("custom tuple costs are not on the B200 path")
+    return wf
+
+
+def plan_cost(plan, inputs, costfn):
+    """sum_e mass_e Cc(tuple_e) (src/barycenter.py:236-240), on the device."""
+    inputs = tuple(inputs)
+    w = _weights_of(costfn, None)
+    duals = MultiDual(tuple(np.zeros(len(m)) for m in inputs))
+    return float(_certify_inputs(inputs, w, plan, duals)[0])
+
+
+def dual_feasibility_exhaustive(inputs, duals, costfn):
+    """max over the whole index grid of sum_k f_k - Cc (positive = violation)
+    (src/barycenter.py:243-258); grids up to 1e5 tuples, on the device."""
+    inputs = tuple(inputs)
+    if int(np.prod([len(m) for m in inputs], dtype=np.float64)) > EXHAUSTIVE_LIMIT:
+        raise ValueError("grid too large for the exhaustive check")
+    w = _weights_of(costfn, None)
+    plan = MultiPlan(np.zeros((1, len(inputs)), dtype=np.int64), np.array([1.0]))
+    v = _certify_inputs(inputs, w, plan, duals)
+    return float(v[4])
+
+
+def mot_certificate(inputs, w, plan, duals, costfn=None, rel_tol=1e-9):
+    """Optimality certificate of a balanced multi-marginal solution
+    (src/barycenter.py:261-295): primal = plan cost, dual = sum_k <a_k, f_k>,
+    violation = max(support, marginal, exhaustive feasibility when the grid
+    has at most 1e5 tuples), tolerance rel_tol (1 + |primal|)."""
+    inputs = tuple(inputs)
+    wv = _weights_of(costfn, w)
+    v = _certify_inputs(inputs, wv, plan, duals)
+    primal, dual = float(v[0]), float(v[1])
+    violation = max(float(v[2]), float(v[3]), float(v[4]))
+    return assemble_certificate(primal, dual, violation, rel_tol * (1.0 + abs(primal)))
+
+
+def multimarginal_lambda(duals, inputs, w, rho):
+    """Optimal zero-sum translation (src/barycenter.py:298-317):
+    rho_k q_k - (rho_k / sum rho) sum_j rho_j q_j, q_k = log <a_k, e^(-f_k/rho_k)>."""
+    from .duality import kl_scalars
+
+    w = np.asarray(w, dtype=np.float64)
+    rhos = w * float(rho)
+    q = []
+    for fk, m, rk in zip(duals.potentials, inputs, rhos):
+        out = kl_scalars(m.weights, m.weights, fk, fk, rk, rk)
+        q.append(-float(out[0, 2].item()) / rk)  # Smin = -rho LSE
+    q = np.array(q)
+    if not np.all(np.isfinite(q)):
+        raise ValueError("zero-mass input or diverging reduction")
+    rho_tot = float(rhos.sum())
+    return rhos * q - (rhos / rho_tot) * float(np.dot(rhos, q))
 
 
 @dataclass

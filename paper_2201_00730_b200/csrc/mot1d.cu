@@ -1062,6 +1062,113 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// Certificate of a balanced multi-marginal solution (barycenter.py:236-295):
+// one CTA per problem.  primal = sum_e mass_e Cc(tuple_e) (plan_cost), dual =
+// sum_k <a_k, f_k>, support = max_e |sum_k f_k[i_ek] - Cc(tuple_e)|, marginal
+// = max_{k,i} |sum_{e: i_ek = i} mass_e - a_k[i]| (the plan is monotone, so
+// the entries of atom i of list k are one contiguous run: two binary
+// searches), and, when the grid has at most 1e5 tuples, the exhaustive dual
+// feasibility sweep (:243-258).  Fixed reduction order: deterministic.
+constexpr int CT = 1024;
+
+__device__ __forceinline__ int run_bound(const int* idx, int K, int q, int cnt, int v, bool upper) {
+  int lo = 0, hi = cnt;  // first e with idx[e][q] > v (upper) or >= v (lower)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int x = idx[(long)mid * K + q];
+    if (upper ? (x <= v) : (x < v))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(CT) mot_certify_kernel(int K, int n, const int* lens,
+                                                         const double* omega, const double* x,
+                                                         const double* a, const double* f,
+                                                         const int* idx, const double* mass,
+                                                         const int* count, int cap_e,
+                                                         int exhaustive, double* out) {
+  __shared__ double scr[32];
+  const int b = blockIdx.x;
+  const int cnt = count[b];
+  const int* ib = idx + (long)b * cap_e * K;
+  const double* mb = mass + (long)b * cap_e;
+  const double* xb = x + (long)b * K * n;
+  const double* ab = a + (long)b * K * n;
+  const double* fb = f + (long)b * K * n;
+  double primal = 0.0, sup = 0.0;
+  for (int e = threadIdx.x; e < cnt; e += CT) {
+    double bc = 0.0, fs = 0.0;
+    for (int q = 0; q < K; ++q) {
+      const int i = ib[(long)e * K + q];
+      bc += omega[q] * xb[(long)q * n + i];
+      fs += fb[(long)q * n + i];
+    }
+    double cc = 0.0;
+    for (int q = 0; q < K; ++q) {
+      const double dx = xb[(long)q * n + ib[(long)e * K + q]] - bc;
+      cc += omega[q] * (dx * dx);
+    }
+    primal += mb[e] * cc;
+    sup = fmax(sup, fabs(fs - cc));
+  }
+  double dual = 0.0, marg = 0.0;
+  for (int q = 0; q < K; ++q) {
+    const int nq = lens != nullptr ? lens[q] : n;
+    for (int i = threadIdx.x; i < nq; i += CT) {
+      dual += ab[(long)q * n + i] * fb[(long)q * n + i];
+      const int lo = run_bound(ib, K, q, cnt, i, false), hi = run_bound(ib, K, q, cnt, i, true);
+      double m = 0.0;
+      for (int e = lo; e < hi; ++e) m += mb[e];
+      marg = fmax(marg, fabs(m - ab[(long)q * n + i]));
+    }
+  }
+  double feas = 0.0;
+  if (exhaustive) {
+    long total = 1;
+    for (int q = 0; q < K; ++q) total *= (lens != nullptr ? lens[q] : n);
+    double worst = -CUDART_INF;
+    for (long t = threadIdx.x; t < total; t += CT) {
+      long r = t;
+      double bc = 0.0, fs = 0.0;
+      for (int q = K - 1; q >= 0; --q) {  // C order: the last list varies fastest
+        const int nq = lens != nullptr ? lens[q] : n;
+        const int i = (int)(r % nq);
+        r /= nq;
+        bc += omega[q] * xb[(long)q * n + i];
+        fs += fb[(long)q * n + i];
+      }
+      r = t;
+      double cc = 0.0;
+      for (int q = K - 1; q >= 0; --q) {
+        const int nq = lens != nullptr ? lens[q] : n;
+        const int i = (int)(r % nq);
+        r /= nq;
+        const double dx = xb[(long)q * n + i] - bc;
+        cc += omega[q] * (dx * dx);
+      }
+      worst = fmax(worst, fs - cc);
+    }
+    worst = block_reduce(worst, scr, MaxOp(), -CUDART_INF);
+    feas = fmax(0.0, worst);
+  }
+  primal = block_reduce(primal, scr, SumOp(), 0.0);
+  dual = block_reduce(dual, scr, SumOp(), 0.0);
+  sup = block_reduce(sup, scr, MaxOp(), 0.0);
+  marg = block_reduce(marg, scr, MaxOp(), 0.0);
+  if (threadIdx.x == 0) {
+    out[b * 6 + 0] = primal;
+    out[b * 6 + 1] = dual;
+    out[b * 6 + 2] = sup;
+    out[b * 6 + 3] = marg;
+    out[b * 6 + 4] = feas;
+    out[b * 6 + 5] = exhaustive ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host driver.
 
 struct MotPlan {
@@ -1376,4 +1483,32 @@ extern "C" int uot_bary_run(const uot_bary_desc* d, void* workspace, size_t work
   A.pcount = d->count;
   A.cap_e = d->k * (d->n - 1) + 1;
   return dispatch(A, p, st, true);
+}
+
+extern "C" int uot_mot_certify(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                               const double* x, const double* a, const double* omega_host,
+                               const double* f, const int32_t* idx, const double* mass,
+                               const int32_t* count, double* out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  UOT_TRY(check_sizes(batch, k, n));
+  if (workspace_bytes < sizeof(double) * (size_t)k + sizeof(int) * (size_t)k + 256) {
+    set_error("uot_mot_certify: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* om = (double*)workspace;
+  int* ld = (int*)((char*)workspace + (sizeof(double) * (size_t)k + 15) / 16 * 16);
+  long grid = 1;
+  for (int q = 0; q < k; ++q) {
+    grid *= (lens != nullptr ? lens[q] : n);
+    if (grid > 100000) break;
+  }
+  UOT_CUDA_TRY(cudaMemcpyAsync(om, omega_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+  if (lens != nullptr)
+    UOT_CUDA_TRY(cudaMemcpyAsync(ld, lens, sizeof(int) * k, cudaMemcpyHostToDevice, st));
+  const int cap_e = k * (n - 1) + 1;
+  mot_certify_kernel<<<batch, CT, 0, st>>>(k, n, lens != nullptr ? ld : nullptr, om, x, a, f, idx,
+                                           mass, count, cap_e, grid <= 100000 ? 1 : 0, out);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
 }

@@ -364,6 +364,32 @@ def gen_mot():
     save("mot.npz", **out)
 
 
+def gen_mot_cert():
+    """mot_certificate (barycenter.py:261-295) of every mot.npz solution, and
+    of a perturbed dual (failing certificate) for each case."""
+    z = np.load(os.path.join(HERE, "mot.npz"))
+    out = {}
+    done = []
+    for k in z["cases"]:
+        kk = int(z[f"c{k}_k"])
+        if kk > 8:  # np.prod of the grid overflows int64 to 0 and the reference
+            continue  # then attempts the exhaustive sweep (TiB allocation)
+        inputs = [U.DiscreteMeasure(z[f"c{k}_x{q}"], z[f"c{k}_a{q}"]) for q in range(kk)]
+        w = z[f"c{k}_w"]
+        plan = UB.MultiPlan(z[f"c{k}_idx"], z[f"c{k}_m"])
+        duals = UB.MultiDual(tuple(z[f"c{k}_f{q}"] for q in range(kk)))
+        cert = UB.mot_certificate(inputs, w, plan, duals)
+        out[f"c{k}_cert"] = np.array([cert.primal, cert.dual, cert.gap, cert.feasibility_violation,
+                                      1.0 if cert.passed else 0.0])
+        bad = UB.MultiDual(tuple(z[f"c{k}_f{q}"] + (0.01 if q == 0 else 0.0) for q in range(kk)))
+        cb = UB.mot_certificate(inputs, w, plan, bad)
+        out[f"c{k}_bad"] = np.array([cb.primal, cb.dual, cb.gap, cb.feasibility_violation,
+                                     1.0 if cb.passed else 0.0])
+        done.append(k)
+    out["cases"] = np.array(done)
+    save("mot_cert.npz", **out)
+
+
 def ref_barycenter(problem, iters, step):
     """barycenter.py:361-414 with the early exit removed and no _finalize."""
     inputs, w = problem.inputs, problem.omega
@@ -468,7 +494,7 @@ def gen_duality():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
-                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g"]
+                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()
