@@ -43,6 +43,8 @@ enum {
 
 enum { UOT_F32 = 0, UOT_F64 = 1 };
 enum { UOT_SINKHORN_F = 0, UOT_SINKHORN_H = 1, UOT_SINKHORN_G = 2 };
+/* marginal penalties (src/entropies.py): KL(rho), Berg(rho), Balanced */
+enum { UOT_ENT_KL = 0, UOT_ENT_BERG = 1, UOT_ENT_BALANCED = 2 };
 /* Ground costs: squared Euclidean between d-dim point clouds; |x-y|^p on 1-D
  * points (src/measures.py:93-105 PowerDistance); dense explicit matrix
  * (src/measures.py:108-122 ExplicitMatrix). */
@@ -100,6 +102,7 @@ typedef struct uot_sinkhorn_desc {
   void* nccl_comm;
   int32_t nranks, rank;
   const int32_t* shard_rows; /* host array [nranks] (emulation only) */
+  int32_t ent1, ent2;        /* UOT_ENT_*: "h" needs KL/KL, "g" KL or Berg, "f" any */
 } uot_sinkhorn_desc;
 
 int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);

@@ -224,6 +224,137 @@ def h_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2):
     return f_new, g_new
 
 
+def berg_aprox(rho, eps, x, tol=1e-12, max_iters=100):
+    """entropies.py:224-263: root of y + eps log(rho/(rho - y)) = x, bracketed
+    safeguarded Newton (vectorised)."""
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+
+    def h(y):
+        return y + eps * np.log(rho / (rho - y)) - x
+
+    lo = np.minimum(x, rho - 1.0)
+    step = np.maximum(1.0, eps)
+    for _ in range(200):
+        bad = h(lo) > 0
+        if not bad.any():
+            break
+        lo = np.where(bad, lo - step, lo)
+        step = step * 2
+    top = np.nextafter(rho, -np.inf)
+    gap = rho - np.minimum(x, rho - 1.0)
+    hi = np.minimum(rho - gap, top)
+    for _ in range(200):
+        bad = h(hi) < 0
+        if not (bad & (hi < top)).any():
+            break
+        gap = np.where(bad, gap / 4, gap)
+        hi = np.minimum(rho - gap, top)
+    y = np.clip(np.minimum(x, rho - gap), lo, hi)
+    em = np.finfo(np.float64).eps
+    for _ in range(max_iters):
+        res = h(y)
+        resolved = (hi - lo) <= 4 * em * (1.0 + np.abs(y))
+        if np.all((np.abs(res) < tol) | resolved):
+            return y
+        lo = np.where(res < 0, y, lo)
+        hi = np.where(res > 0, y, hi)
+        newton = y - res / (1.0 + eps / (rho - y))
+        inside = (newton > lo) & (newton < hi)
+        y = np.where(inside, newton, 0.5 * (lo + hi))
+    raise ValueError("Berg aprox Newton did not converge")
+
+
+def aprox(ent, rho, eps, x):
+    """entropies.py:203-221 for ent in {"kl", "berg", "balanced"}."""
+    if ent == "kl":
+        return (rho / (eps + rho)) * np.asarray(x, dtype=np.float64)
+    if ent == "balanced":
+        return np.asarray(x, dtype=np.float64) + 0.0
+    return berg_aprox(rho, eps, x)
+
+
+def _cgrad(ent, rho, x):
+    return np.exp(x / rho) if ent == "kl" else rho / (rho - x)
+
+
+def _chess(ent, rho, x):
+    return np.exp(x / rho) / rho if ent == "kl" else rho / (rho - x) ** 2
+
+
+def lambda_star_any(aw, bw, f, g, ents, r1, r2, initial=0.0, tol=1e-11, max_iters=100):
+    """duality.py:170-247: closed form for KL/KL, else the bracketed Newton."""
+    e1, e2 = ents
+    if e1 == "kl" and e2 == "kl":
+        return lambda_star_kl(aw, bw, f, g, r1, r2)
+    lo_dom = -np.inf if e1 != "berg" else -r1 - float(f.min())
+    hi_dom = np.inf if e2 != "berg" else r2 + float(g.min())
+
+    def residual(lam):
+        with np.errstate(over="ignore"):
+            return float(np.dot(aw, _cgrad(e1, r1, -f - lam))) - float(
+                np.dot(bw, _cgrad(e2, r2, -g + lam)))
+
+    def slope(lam):
+        with np.errstate(over="ignore"):
+            return -float(np.dot(aw, _chess(e1, r1, -f - lam))) - float(
+                np.dot(bw, _chess(e2, r2, -g + lam)))
+
+    def clamp(x):
+        if np.isfinite(lo_dom):
+            x = max(x, lo_dom + 1e-12 * max(1.0, abs(lo_dom)))
+        if np.isfinite(hi_dom):
+            x = min(x, hi_dom - 1e-12 * max(1.0, abs(hi_dom)))
+        return x
+
+    lam = clamp(initial)
+    r0 = residual(lam)
+    if abs(r0) < tol:
+        return lam
+    step = 1.0
+    lo, hi = lam, lam
+    if r0 > 0:
+        for _ in range(200):
+            hi = clamp(lam + step)
+            if residual(hi) <= 0:
+                break
+            step *= 2
+    else:
+        for _ in range(200):
+            lo = clamp(lam - step)
+            if residual(lo) >= 0:
+                break
+            step *= 2
+    x = 0.5 * (lo + hi)
+    for _ in range(max_iters):
+        r = residual(x)
+        if abs(r) < tol:
+            return x
+        if r > 0:
+            lo = x
+        else:
+            hi = x
+        ds = slope(x)
+        newton = x - r / ds if ds < 0 and np.isfinite(ds) else None
+        x = newton if newton is not None and lo < newton < hi else 0.5 * (lo + hi)
+    raise ValueError("translation Newton did not converge")
+
+
+def f_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, ents):
+    """sinkhorn.py:103-114 with any aprox."""
+    g_new = -aprox(ents[1], r2, eps, -cost.smin_cols(f, eps, aw))
+    f_new = -aprox(ents[0], r1, eps, -cost.smin_rows(g_new, eps, bw))
+    return f_new, g_new
+
+
+def g_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, lam, ents):
+    """sinkhorn.py:117-134 with any aprox and lambda_star(initial=lam)."""
+    smin_a = cost.smin_cols(f + lam, eps, aw)
+    g_new = lam - aprox(ents[1], r2, eps, -smin_a)
+    smin_b = cost.smin_rows(g_new - lam, eps, bw)
+    f_new = -lam - aprox(ents[0], r1, eps, -smin_b)
+    return f_new, g_new, lambda_star_any(aw, bw, f_new, g_new, ents, r1, r2, initial=lam)
+
+
 def g_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2, lam):
     """sinkhorn.py:117-134 with KL aprox: both half-updates at the incoming
     translation lam, then lambda* of the new pair (duality.py:175-178).
@@ -235,7 +366,8 @@ def g_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2, lam):
     return f_new, g_new, lambda_star_kl(aw, bw, f_new, g_new, r1, r2)
 
 
-def sinkhorn_fixed(cost, aw, bw, eps, r1, r2, variant, iters, f0=None, g0=None):
+def sinkhorn_fixed(cost, aw, bw, eps, r1, r2, variant, iters, f0=None, g0=None,
+                   ents=("kl", "kl")):
     """sinkhorn.py:246-315 (run) with the early exit removed (:304-306):
     exactly ``iters`` steps; returns (f, g, delta_f trace).  Variant "g"
     starts from lambda*(f0, g0) (:263-265) and carries lambda (:270-271)."""
@@ -243,9 +375,15 @@ def sinkhorn_fixed(cost, aw, bw, eps, r1, r2, variant, iters, f0=None, g0=None):
     g = np.zeros(cost.m) if g0 is None else _c64(g0).copy()
     deltas = np.empty(iters)
     if variant == "g":
-        lam = lambda_star_kl(aw, bw, f, g, r1, r2)
+        lam = lambda_star_any(aw, bw, f, g, ents, r1, r2)
         for t in range(iters):
-            fn, gn, lam = g_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2, lam)
+            fn, gn, lam = g_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, lam, ents)
+            deltas[t] = float(np.abs(fn - f).max())
+            f, g = fn, gn
+        return f, g, deltas
+    if tuple(ents) != ("kl", "kl"):
+        for t in range(iters):
+            fn, gn = f_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, ents)
             deltas[t] = float(np.abs(fn - f).max())
             f, g = fn, gn
         return f, g, deltas

@@ -18,6 +18,7 @@ SO_PATH = os.environ.get("UOT_B200_LIB") or os.path.join(_HERE, "_uot_b200.so")
 UOT_OK = 0
 F32, F64 = 0, 1
 SINKHORN_F, SINKHORN_H, SINKHORN_G = 0, 1, 2
+ENT_KL, ENT_BERG, ENT_BALANCED = 0, 1, 2
 COST_SQEUCLID, COST_POWER, COST_EXPLICIT = 0, 1, 2
 STEP_HARMONIC, STEP_LINESEARCH, STEP_PAIRWISE = 0, 1, 2
 
@@ -36,6 +37,7 @@ class SinkhornDesc(ctypes.Structure):
         ("init_given", _i32), ("iters", _i32), ("tol", _f64), ("use_tol", _i32),
         ("trace_delta", _vp), ("iterations", _vp),
         ("nccl_comm", _vp), ("nranks", _i32), ("rank", _i32), ("shard_rows", _vp),
+        ("ent1", _i32), ("ent2", _i32),
     ]
 
 

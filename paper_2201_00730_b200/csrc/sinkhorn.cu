@@ -629,6 +629,150 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
 }
 
 // ---------------------------------------------------------------------------
+// Entropy helpers (src/entropies.py:141-263) for the F / G steps.
+
+// Berg aprox: the root of h(y) = y + eps log(rho / (rho - y)) - x on
+// (-inf, rho), strictly increasing with range R (entropies.py:224-263):
+// bracket (lo by doubling steps, hi towards rho by quartering gaps), then
+// bisection-safeguarded Newton to |h| < 1e-12 or a bracket of 4 ulps.
+__device__ double berg_aprox(double rho, double eps, double x) {
+  auto h = [&](double y) { return y + eps * log(rho / (rho - y)) - x; };
+  double lo = fmin(x, rho - 1.0);
+  double step = fmax(1.0, eps);
+  for (int it = 0; it < 200 && h(lo) > 0.0; ++it) {
+    lo -= step;
+    step *= 2.0;
+  }
+  const double top = nextafter(rho, -CUDART_INF);
+  double gap = rho - fmin(x, rho - 1.0);
+  double hi = fmin(rho - gap, top);
+  for (int it = 0; it < 200 && h(hi) < 0.0 && hi < top; ++it) {
+    gap *= 0.25;
+    hi = fmin(rho - gap, top);
+  }
+  double y = fmin(fmax(fmin(x, rho - gap), lo), hi);
+  const double em = 2.220446049250313e-16;
+  for (int it = 0; it < 100; ++it) {
+    const double res = h(y);
+    if (fabs(res) < 1e-12 || (hi - lo) <= 4.0 * em * (1.0 + fabs(y))) break;
+    if (res < 0.0) lo = y;
+    if (res > 0.0) hi = y;
+    const double nt = y - res / (1.0 + eps / (rho - y));
+    y = (nt > lo && nt < hi) ? nt : 0.5 * (lo + hi);
+  }
+  return y;
+}
+
+// aprox(spec, eps, x) (entropies.py:203-221)
+__device__ __forceinline__ double aprox_any(int ent, double rho, double eps, double x) {
+  if (ent == UOT_ENT_KL) return (rho / (eps + rho)) * x;
+  if (ent == UOT_ENT_BALANCED) return x;
+  return berg_aprox(rho, eps, x);
+}
+
+// conj_grad / conj_hess (entropies.py:157-184) for KL and Berg
+__device__ __forceinline__ double conj_grad_d(int ent, double rho, double x) {
+  return ent == UOT_ENT_KL ? exp(x / rho) : rho / (rho - x);
+}
+__device__ __forceinline__ double conj_hess_d(int ent, double rho, double x) {
+  return ent == UOT_ENT_KL ? exp(x / rho) / rho : rho / ((rho - x) * (rho - x));
+}
+
+// G variant with a Berg marginal: lambda* of the current pair by the
+// reference's bracketed Newton (duality.py:182-247), one CTA per problem,
+// starting from the incoming lam; the residual / slope are block reductions
+// over both potentials (pot = hat + tau).
+template <typename T>
+__global__ void __launch_bounds__(256) sk_lambda_newton(int n, int m, const T* hatA,
+                                                       const T* hatB, const T* wa, const T* wb,
+                                                       int e1, int e2, double r1, double r2,
+                                                       SkScalars* sc) {
+  __shared__ double s_x[32];
+  __shared__ double s_r[2];
+  const int b = blockIdx.x;
+  const double tf = sc[b].tau[0], tg = sc[b].tau[1];
+  const T* f = hatA + (long)b * n;
+  const T* g = hatB + (long)b * m;
+  const T* a = wa + (long)b * n;
+  const T* bw = wb + (long)b * m;
+  double fmn = CUDART_INF, gmn = CUDART_INF;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) fmn = fmin(fmn, (double)f[i] + tf);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) gmn = fmin(gmn, (double)g[j] + tg);
+  fmn = block_reduce(fmn, s_x, MinOp(), CUDART_INF);
+  gmn = block_reduce(gmn, s_x, MinOp(), CUDART_INF);
+  const double lo_dom = e1 == UOT_ENT_BERG ? -r1 - fmn : -CUDART_INF;
+  const double hi_dom = e2 == UOT_ENT_BERG ? r2 + gmn : CUDART_INF;
+  auto clamp = [&](double x) {
+    if (lo_dom > -CUDART_INF) x = fmax(x, lo_dom + 1e-12 * fmax(1.0, fabs(lo_dom)));
+    if (hi_dom < CUDART_INF) x = fmin(x, hi_dom - 1e-12 * fmax(1.0, fabs(hi_dom)));
+    return x;
+  };
+  // residual and slope at lam (block-uniform results)
+  auto eval = [&](double lam, double& res, double& slope) {
+    double s1 = 0.0, s2 = 0.0, h1 = 0.0, h2 = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double w = (double)a[i];
+      if (w > 0.0) {
+        const double xv = -((double)f[i] + tf) - lam;
+        s1 += w * conj_grad_d(e1, r1, xv);
+        h1 += w * conj_hess_d(e1, r1, xv);
+      }
+    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      const double w = (double)bw[j];
+      if (w > 0.0) {
+        const double xv = -((double)g[j] + tg) + lam;
+        s2 += w * conj_grad_d(e2, r2, xv);
+        h2 += w * conj_hess_d(e2, r2, xv);
+      }
+    }
+    s1 = block_reduce(s1, s_x, SumOp(), 0.0);
+    s2 = block_reduce(s2, s_x, SumOp(), 0.0);
+    h1 = block_reduce(h1, s_x, SumOp(), 0.0);
+    h2 = block_reduce(h2, s_x, SumOp(), 0.0);
+    res = s1 - s2;
+    slope = -h1 - h2;
+  };
+  const double tol = 1e-11;
+  double lam = clamp(sc[b].lam), r, ds;
+  eval(lam, r, ds);
+  if (fabs(r) >= tol) {
+    double lo = lam, hi = lam, step = 1.0;
+    if (r > 0.0) {
+      for (int it = 0; it < 200; ++it) {
+        hi = clamp(lam + step);
+        double rh, dh;
+        eval(hi, rh, dh);
+        if (rh <= 0.0) break;
+        step *= 2.0;
+      }
+    } else {
+      for (int it = 0; it < 200; ++it) {
+        lo = clamp(lam - step);
+        double rl, dl;
+        eval(lo, rl, dl);
+        if (rl >= 0.0) break;
+        step *= 2.0;
+      }
+    }
+    double x = 0.5 * (lo + hi);
+    for (int it = 0; it < 100; ++it) {
+      eval(x, r, ds);
+      if (fabs(r) < tol) break;
+      if (r > 0.0)
+        lo = x;
+      else
+        hi = x;
+      const double nt = (ds < 0.0 && isfinite(ds)) ? x - r / ds : CUDART_NAN;
+      x = (nt > lo && nt < hi) ? nt : 0.5 * (lo + hi);
+    }
+    lam = x;
+  }
+  if (threadIdx.x == 0) sc[b].lam = lam;
+  (void)s_r;
+}
+
+// ---------------------------------------------------------------------------
 // Tail kernel.
 
 constexpr int TAIL_THREADS = 256;
@@ -685,7 +829,17 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
       const double lse = M + D::lgd(acc);  // domain units, excluding tau_red
       A.shift_out[(long)b * A.nout + o] = (T)lse;
       const double smin = -A.eps * A.unit * (lse + tau_red * A.inv_eu);
-      hat = A.a_coef * smin - A.k_coef * smin_red;
+      if (A.gmode) {
+        // G (src/sinkhorn.py:128-132) at the incoming lam, any aprox:
+        // g' = lam - aprox(eps, lam - smin_cols(f)), f' = -lam - aprox(eps, -smin_rows(g) - lam)
+        const double lm = sc.lam;
+        hat = A.out_side == 1 ? lm - aprox_any(A.ent_out, A.rho_out, A.eps, lm - smin)
+                              : -lm - aprox_any(A.ent_out, A.rho_out, A.eps, -smin - lm);
+      } else if (A.ent_out == UOT_ENT_KL) {
+        hat = A.a_coef * smin - A.k_coef * smin_red;
+      } else {
+        hat = -aprox_any(A.ent_out, A.rho_out, A.eps, -smin);  // F step, :111-113
+      }
     }
     const T hat_t = (T)hat;
     hat = (double)hat_t;
@@ -740,15 +894,10 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
   }
   if (threadIdx.x == 0) {
     const double shat = -A.rho_out * (q.m + log(q.s));
-    double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
-    if (A.gmode && A.mode != 1) {
-      // G (src/sinkhorn.py:128-132): g' = lam + a2 smin_cols(f + lam) = a2 smin_cols(f) +
-      // (1 - a2) lam, f' = -lam + a1 smin_rows(g' - lam) = a1 smin_rows(g') - (1 - a1) lam
-      tau = (A.out_side == 1 ? 1.0 : -1.0) * (1.0 - A.a_coef) * A.sc[b].lam;
-    }
+    const double tau = (A.mode == 1) ? 0.0 : A.tau_fac * shat;
     A.sc[b].shat[A.out_side] = shat;
     A.sc[b].tau[A.out_side] = tau;
-    if (A.gmode && A.out_side == 0) {
+    if (A.gmode && A.lam_closed && A.out_side == 0) {
       // lambda* of the new pair (duality.py:175-178) from the softmins
       // S = Smin(hat) + tau of both sides: (rho1 S_g - rho2 S_f) / (rho1 + rho2)
       const double Sf = shat + tau, Sg = A.sc[b].shat[1] + A.sc[b].tau[1];
@@ -1248,6 +1397,9 @@ struct Engine {
     a.gmode = d.variant == UOT_SINKHORN_G ? 1 : 0;
     a.rho1 = r1;
     a.rho2 = r2;
+    a.ent_out = to_target ? d.ent2 : d.ent1;
+    a.lam_closed = (d.ent1 == UOT_ENT_KL && d.ent2 == UOT_ENT_KL) ? 1 : 0;
+    if (a.ent_out == UOT_ENT_BALANCED) a.a_coef = 1.0;
     a.rho_out = ro;
     a.hat_out = hat_out;
     a.hat_old = hat_old;
@@ -1347,6 +1499,16 @@ struct Engine {
     }
     // init: hat_f = f0, Smin_a(f0), pack source records.
     UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, f0, 0, nullptr, trace_len));
+    const bool g_newton =
+        d.variant == UOT_SINKHORN_G && !(d.ent1 == UOT_ENT_KL && d.ent2 == UOT_ENT_KL);
+    auto lam_newton = [&](const T* hatA) -> int {
+      sk_lambda_newton<T><<<d.batch, 256, 0, st>>>(d.n, d.m, hatA, bf.hatB, (const T*)d.a,
+                                                   (const T*)d.b, d.ent1, d.ent2, d.rho1, d.rho2,
+                                                   bf.sc);
+      UOT_CHECK_LAUNCH();
+      return UOT_OK;
+    };
+    if (g_newton) UOT_TRY(lam_newton(bf.hatA0));  // lambda*(f0, g0) (:263-265)
     const int sB = splits(d.batch, d.m, d.n, d.d);  // g-update splits
     const int sA = splits(d.batch, d.n, d.m, d.d);  // f-update splits
     for (int t = 0; t < d.iters; ++t) {
@@ -1358,6 +1520,7 @@ struct Engine {
       UOT_TRY(launch_main(d, bf, st, false, sA, 0, d.m, 0, sA));
       UOT_TRY(launch_tail(d, bf, st, false, 0, sA, hat_old, hat_new, nullptr, t, trace,
                           trace_len));
+      if (g_newton) UOT_TRY(lam_newton(hat_new));  // lambda_star(pair, initial=lam) (:134)
     }
     sk_finalize<T><<<dim3(ceil_div(nm, 256), d.batch), 256, 0, st>>>(
         d.n, d.m, bf.hatA0, bf.hatA1, bf.hatB, bf.sc, bf.iters_done, (T*)d.f, (T*)d.g);
@@ -1720,6 +1883,25 @@ int validate(const uot_sinkhorn_desc* d) {
     set_error("variant must be F (0), H (1) or G (2)");
     return UOT_INVALID;
   }
+  if (d->ent1 < UOT_ENT_KL || d->ent1 > UOT_ENT_BALANCED || d->ent2 < UOT_ENT_KL ||
+      d->ent2 > UOT_ENT_BALANCED) {
+    set_error("ent1 / ent2 must be UOT_ENT_KL, UOT_ENT_BERG or UOT_ENT_BALANCED");
+    return UOT_INVALID;
+  }
+  const bool klkl = d->ent1 == UOT_ENT_KL && d->ent2 == UOT_ENT_KL;
+  if (d->variant == UOT_SINKHORN_H && !klkl) {
+    set_error("h-sinkhorn requires kl penalties on both marginals");  // sinkhorn.py:151-152
+    return UOT_UNSUPPORTED_ENTROPY;
+  }
+  if (d->variant == UOT_SINKHORN_G &&
+      (d->ent1 == UOT_ENT_BALANCED || d->ent2 == UOT_ENT_BALANCED)) {
+    set_error("optimal translation needs strictly convex conjugates (KL or Berg)");
+    return UOT_UNSUPPORTED_ENTROPY;
+  }
+  if (!klkl && (d->nranks > 1 || d->nccl_comm != nullptr)) {
+    set_error("row sharding runs KL marginals");
+    return UOT_INVALID;
+  }
   if (d->variant == UOT_SINKHORN_G && (d->nranks > 1 || d->nccl_comm != nullptr)) {
     set_error("the G variant runs unsharded");
     return UOT_INVALID;
@@ -1764,6 +1946,10 @@ extern "C" int uot_sinkhorn_verify(const uot_sinkhorn_desc* desc, void* workspac
   if (desc->nranks > 1 || desc->nccl_comm != nullptr) {
     set_error("uot_sinkhorn_verify runs unsharded");
     return UOT_INVALID;
+  }
+  if (desc->ent1 != UOT_ENT_KL || desc->ent2 != UOT_ENT_KL) {
+    set_error("uot_sinkhorn_verify evaluates KL objectives");
+    return UOT_UNSUPPORTED_ENTROPY;
   }
   return dispatch(*desc, [&](auto eng) {
     return decltype(eng)::verify(*desc, workspace, workspace_bytes, (cudaStream_t)stream, out);

@@ -72,8 +72,10 @@ struct TailArgs {
   double eps, unit, inv_eu;    // unit = ln2 (log2 domain) or 1; inv_eu = 1/(eps*unit)
   double a_coef, k_coef;       // hat = a*smin - k*(shat_red + tau_red)
   double tau_fac;              // tau_out = tau_fac * shat_out
-  int gmode;                   // G variant: tau_out = +-(1 - a) lam, then lam = lambda*
+  int gmode;                   // G variant: hat includes lam, then lam = lambda* (KL/KL)
   double rho1, rho2;
+  int ent_out;                 // UOT_ENT_* of the output side's marginal
+  int lam_closed;              // G: lambda* in closed form (KL/KL) in the f-tail
   double rho_out;
   T* hat_out;                  // [B][nout]
   const T* hat_old;            // [B][nout] or nullptr (delta tracking)

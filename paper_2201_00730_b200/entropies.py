@@ -29,7 +29,8 @@ class KL:
 
 @dataclass(frozen=True)
 class Berg:
-    """Berg marginal penalty (accepted for validation; not on the GPU path)."""
+    """Berg marginal penalty rho * (sum log(nu/mu) ...): F and G Sinkhorn steps
+    run it on the device (aprox by per-element Newton, lambda* by Newton)."""
 
     rho: float = 1.0
 
@@ -39,7 +40,24 @@ class Berg:
 
 @dataclass(frozen=True)
 class Balanced:
-    """Hard marginal constraint (accepted for validation; not on the GPU path)."""
+    """Hard marginal constraint (aprox = identity): F Sinkhorn steps only."""
+
+
+def ent_code(spec):
+    """UOT_ENT_* code of an entropy spec (include/uot_b200.h)."""
+    from .exceptions import UnsupportedEntropyError
+
+    if isinstance(spec, KL):
+        return 0
+    if isinstance(spec, Berg):
+        return 1
+    if isinstance(spec, Balanced):
+        return 2
+    raise UnsupportedEntropyError(f"unknown entropy {spec!r}")
+
+
+def ent_rho(spec):
+    return float(getattr(spec, "rho", 1.0))
 
 
 def require_kl(*specs, what="this solver"):

@@ -17,7 +17,13 @@ import numpy as np
 from . import _device as D
 from . import _lib
 from .duality import DualPair, UotProblem, kl_scalars
-from .entropies import KL, require_kl
+from .entropies import KL, Berg, ent_code, ent_rho, require_kl
+
+_ENT_NAME = {0: "kl", 1: "berg", 2: "balanced"}
+
+
+def _ents(prob):
+    return _ENT_NAME[ent_code(prob.ent1)], _ENT_NAME[ent_code(prob.ent2)]
 from .exceptions import UnsupportedEntropyError
 from .measures import ExplicitMatrix, PowerDistance, SqEuclideanPoints, check_submodular  # noqa: F401
 
@@ -91,7 +97,7 @@ def _geometry(prob):
 
 def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
                      c=None, f0=None, tol=None, precision="fp32", stream=None, comm=None,
-                     nranks=1, rank=0, shard_rows=None, g0=None):
+                     nranks=1, rank=0, shard_rows=None, g0=None, ent1="kl", ent2="kl"):
     """Batched Sinkhorn on device.
 
     x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
@@ -105,6 +111,8 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     ``shard_rows`` the same protocol runs for all shards in this process.
     Variant "g" (src/sinkhorn.py:117-134) starts from lambda*(f0, g0) and
     returns the overparameterised pair (plain potentials (f + lam, g - lam)).
+    ``ent1`` / ``ent2`` in {"kl", "berg", "balanced"} select the marginal
+    penalties (rho1 / rho2 are their strengths; "h" needs KL/KL).
     """
     t = D.torch()
     lib = _lib.load()
@@ -146,7 +154,9 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
         init_given=1 if f0 is not None else 0, iters=int(iters),
         tol=float(tol) if tol is not None else 0.0, use_tol=1 if tol is not None else 0,
         trace_delta=_lib.ptr(trace), iterations=_lib.ptr(its), nccl_comm=comm,
-        nranks=int(nranks), rank=int(rank), shard_rows=None)
+        nranks=int(nranks), rank=int(rank), shard_rows=None,
+        ent1={"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG, "balanced": _lib.ENT_BALANCED}[ent1],
+        ent2={"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG, "balanced": _lib.ENT_BALANCED}[ent2])
     rows_arr = None
     if shard_rows is not None:
         import numpy as _np
@@ -243,16 +253,20 @@ def _step_inputs(prob):
 def _one_step(prob, d, variant):
     _require_positive_eps(prob)
     prob.check_pair(d)
-    require_kl(prob.ent1, prob.ent2, what=f"{variant}-sinkhorn")
+    if variant == "h":
+        require_kl(prob.ent1, prob.ent2, what="h-sinkhorn")
+    e1, e2 = _ents(prob)
     costname, p, x, y, C = _step_inputs(prob)
     f, g, _, _ = sinkhorn_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.eps,
-                                  prob.ent1.rho, prob.ent2.rho, 1, variant=variant, cost=costname,
-                                  p=p, c=C, f0=d.f, precision="fp64")
+                                  ent_rho(prob.ent1), ent_rho(prob.ent2), 1, variant=variant,
+                                  cost=costname, p=p, c=C, f0=d.f, precision="fp64", ent1=e1,
+                                  ent2=e2)
     return DualPair(D.to_np(f[0]), D.to_np(g[0]))
 
 
 def f_sinkhorn_step(prob, d):
-    """One plain step, g then f (src/sinkhorn.py:103-114), KL marginals."""
+    """One plain step, g then f (src/sinkhorn.py:103-114); KL, Berg or
+    Balanced marginals (aprox per entropy, entropies.py:203-263)."""
     return _one_step(prob, d, "f")
 
 
@@ -299,7 +313,12 @@ def run(prob, config, init=None, reference=None):
     prob.check_pair(d)
     if config.variant == "h" and not (isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)):
         raise UnsupportedEntropyError("h-sinkhorn requires kl penalties on both marginals")
-    require_kl(prob.ent1, prob.ent2, what="sinkhorn")
+    if config.variant == "g" and not all(isinstance(e, (KL, Berg)) for e in (prob.ent1, prob.ent2)):
+        raise UnsupportedEntropyError(
+            "optimal translation needs strictly convex conjugates (KL or Berg)")
+    e1, e2 = _ents(prob)
+    if reference is not None:
+        require_kl(prob.ent1, prob.ent2, what="err_f tracing")
     if config.anderson is not None:
         raise UnsupportedEntropyError("Anderson extrapolation is not on the B200 path")
     t = D.torch()
@@ -314,9 +333,10 @@ def run(prob, config, init=None, reference=None):
         k = min(chunk, config.max_iters - done)
         t0 = time.perf_counter_ns()
         f, g, tr, its = sinkhorn_batched(
-            x, y, prob.alpha.weights, prob.beta.weights, prob.eps, prob.ent1.rho, prob.ent2.rho,
-            k, variant=config.variant, cost=costname, p=p, c=C, f0=f_cur, tol=config.tol,
-            precision=config.precision, g0=g_cur if config.variant == "g" else None)
+            x, y, prob.alpha.weights, prob.beta.weights, prob.eps, ent_rho(prob.ent1),
+            ent_rho(prob.ent2), k, variant=config.variant, cost=costname, p=p, c=C, f0=f_cur,
+            tol=config.tol, precision=config.precision,
+            g0=g_cur if config.variant == "g" else None, ent1=e1, ent2=e2)
         t.cuda.synchronize()
         el = time.perf_counter_ns() - t0
         got = int(its[0].item())

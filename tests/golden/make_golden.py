@@ -59,6 +59,38 @@ def ref_sinkhorn(prob, variant, iters, d0=None):
     return d.f, d.g, np.asarray(deltas)
 
 
+def gen_sinkhorn_ent():
+    """F and G steps with Berg / Balanced penalties (entropies.py:203-263,
+    duality.py:182-247), small 1-D problems."""
+    rng = np.random.default_rng(53)
+    out = {}
+    combos = [("f", "berg", "berg"), ("f", "kl", "berg"), ("f", "berg", "balanced"),
+              ("f", "balanced", "kl"), ("g", "berg", "kl"), ("g", "berg", "berg"),
+              ("g", "kl", "berg"), ("f", "berg", "berg")]
+    names = {"kl": U.KL, "berg": U.Berg}
+    for k, (var, e1, e2) in enumerate(combos):
+        n, m = int(rng.integers(3, 30)), int(rng.integers(3, 30))
+        p = [1.0, 2.0][k % 2]
+        eps = [0.1, 0.5][k % 2]
+        r1, r2 = float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m)
+        if "balanced" in (e1, e2):
+            wb *= wa.sum() / wb.sum()
+        ent = [names[e](r) if e != "balanced" else U.Balanced() for e, r in ((e1, r1), (e2, r2))]
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), ent[0], ent[1], eps=eps)
+        f, g, dl = ref_sinkhorn(prob, var, 25)
+        out[f"c{k}_f"], out[f"c{k}_g"], out[f"c{k}_delta"] = f, g, dl
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([p, eps, r1, r2, 25])
+        out[f"c{k}_spec"] = np.array([var, e1, e2])
+    out["cases"] = np.arange(len(combos))
+    save("sinkhorn_ent.npz", **out)
+
+
 def gen_sinkhorn_g():
     """G-Sinkhorn (sinkhorn.py:117-134) on small 1-D problems, from zeros and
     from a nonzero initial pair, plus the cfg1 setting."""
@@ -494,7 +526,7 @@ def gen_duality():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
-                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert"]
+                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert", "sinkhorn_ent"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

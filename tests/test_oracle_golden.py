@@ -33,6 +33,18 @@ def test_sinkhorn_g_cases():
         np.testing.assert_allclose(dl, z[f"c{k}_delta"], rtol=1e-8, atol=1e-13)
 
 
+def test_sinkhorn_entropies():
+    """F / G steps with Berg and Balanced penalties vs the reference."""
+    z = golden("sinkhorn_ent.npz")
+    for k in cases(z):
+        p, eps, r1, r2, iters = z[f"c{k}_par"]
+        var, e1, e2 = (str(v) for v in z[f"c{k}_spec"])
+        cost = O.PointCost(z[f"c{k}_x"], z[f"c{k}_y"], p=p, power1d=True)
+        f, g, dl = O.sinkhorn_fixed(cost, z[f"c{k}_a"], z[f"c{k}_b"], eps, r1, r2, var,
+                                    int(iters), ents=(e1, e2))
+        assert rel_err(f, g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-11, (k, var, e1, e2)
+
+
 def test_sinkhorn_small_cases():
     z = golden("sinkhorn_small.npz")
     for k in cases(z):

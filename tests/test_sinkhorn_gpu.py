@@ -261,3 +261,24 @@ def test_verify_matches_oracle_points():
     res_f = np.abs(f - (rho / (rho + eps)) * cost.smin_rows(g, eps, wb)
                    + (eps / (eps + rho)) * out[4]).max()
     assert abs(out[2] - res_f) < 1e-9
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_sinkhorn_berg_balanced(k):
+    """F / G Sinkhorn with Berg (per-element Newton aprox, Newton lambda*)
+    and Balanced penalties (§8f row 2) vs the reference."""
+    z = golden("sinkhorn_ent.npz")
+    p, eps, r1, r2, iters = z[f"c{k}_par"]
+    var, e1, e2 = (str(v) for v in z[f"c{k}_spec"])
+    f, g, dl, its = P.sinkhorn_batched(z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"], z[f"c{k}_b"],
+                                       eps, r1, r2, int(iters), variant=var, cost="power", p=p,
+                                       precision="fp64", ent1=e1, ent2=e2)
+    assert rel_err(D.to_np(f[0]), D.to_np(g[0]), z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-9, (var, e1, e2)
+    np.testing.assert_allclose(D.to_np(dl[0]), z[f"c{k}_delta"], rtol=1e-6, atol=1e-12)
+
+
+def test_h_rejects_berg():
+    z = golden("sinkhorn_ent.npz")
+    with pytest.raises(P.UnsupportedEntropyError):
+        P.sinkhorn_batched(z["c0_x"], z["c0_y"], z["c0_a"], z["c0_b"], 0.1, 1.0, 1.0, 2,
+                           variant="h", cost="power", precision="fp64", ent1="berg", ent2="kl")
