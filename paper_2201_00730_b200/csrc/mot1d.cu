@@ -43,7 +43,10 @@ namespace uot {
 namespace {
 
 constexpr int MT = 512;           // threads of the per-list CTAs
-constexpr int BT = 512;           // threads of the bucket CTAs
+#ifndef UOT_BT
+#define UOT_BT 512
+#endif
+constexpr int BT = UOT_BT;  // threads of the bucket CTAs
 constexpr int CAP = 4096;         // events per bucket (two shared-memory buffers)
 constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
 constexpr int ST = 1024;          // threads of the per-problem splitter CTA
