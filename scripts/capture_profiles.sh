@@ -1,10 +1,14 @@
 #!/bin/bash
-# Round-end ncu evidence for the secondary configs (run on the GPU box under
-# gpurun; each command first runs once without ncu).  Outputs go to
-# gpurun_out/prof_*; scripts/summarize_ncu.py turns them into profiles/*.md.
+# Round-end ncu evidence (run on the GPU box under gpurun; each command first
+# runs once without ncu).  Outputs go to gpurun_out/prof_*; then run
+# scripts/make_profile_md.sh here to refresh profiles/*.md.
 set -x
 O=gpurun_out
-# cfg2 FW: 296 problems (2 waves of 148 SMs x 2 CTAs... one per resident slot) x 20 iterations
+# cfg3 headline: launch list of a short bench run + full capture of the main kernel
+timeout 300 python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_cfg3_launches.csv python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sk_main -s 4 -c 2 -o $O/prof_cfg3_full python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null 2>&1
+# cfg2 FW: 296 problems x 20 iterations
 timeout 300 python scripts/prof_fw.py 296 20 linesearch && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_fw_launches.csv python scripts/prof_fw.py 296 20 linesearch > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fw1d_kernel -c 1 -o $O/prof_fw_full python scripts/prof_fw.py 296 20 linesearch > /dev/null 2>&1
