@@ -132,6 +132,31 @@ int uot_kl_scalars(int32_t batch, int32_t n, int32_t m, const double* a, const d
                    void* stream);
 
 /* ------------------------------------------------------------------------
+ * Anderson extrapolation of the Sinkhorn map: replaces the window state of
+ * src/sinkhorn.py:215-243 (`_AndersonState.push` / `extrapolate`) and
+ * src/sinkhorn.py:197-212 `anderson_weights`, as used by run() with
+ * `config.anderson` (:281-292).  fp64, device pointers, `batch` independent
+ * windows over vectors of length len = n + m (the concatenated (f, g)).
+ * uot_anderson_step pushes (tz, tz - z) -- restarting the window when the new
+ * residual's sup norm exceeds the previous one's, keeping the last `depth`
+ * entries -- then writes the extrapolation to znew (may alias z) and
+ * delta_f[b] = max_{i < nf} |znew - z|.  status[b] = 1 when the window
+ * system is singular / degenerate (the reference raises LinAlgError).
+ * Device limit: depth <= 32.  The workspace is persistent state: call
+ * uot_anderson_reset once before the first step.
+ * ------------------------------------------------------------------------ */
+int uot_anderson_workspace_size(int32_t batch, int64_t len, int32_t depth, size_t* bytes);
+int uot_anderson_reset(int32_t batch, int64_t len, int32_t depth, void* workspace,
+                       size_t workspace_bytes, void* stream);
+int uot_anderson_step(int32_t batch, int64_t len, int64_t nf, int32_t depth, double reg,
+                      const double* z, const double* tz, double* znew, double* delta_f,
+                      int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+/* anderson_weights(U, r) for one window U [rows][k] (row-major): c [k],
+ * status (device int32) 1 on a singular system.  k <= 32. */
+int uot_anderson_weights(int32_t rows, int32_t k, const double* U, double reg, double* c,
+                         int32_t* status, void* stream);
+
+/* ------------------------------------------------------------------------
  * Balanced 1-D OT (Algorithm 1): replaces src/ot1d.py:112-172
  * `solve_ot_1d(a, b, cost)` for a batch of problems with sorted supports.
  * fp64.  Costs: UOT_COST_POWER with exponent p, or UOT_COST_EXPLICIT with

@@ -395,6 +395,103 @@ def sinkhorn_fixed(cost, aw, bw, eps, r1, r2, variant, iters, f0=None, g0=None,
     return f, g, deltas
 
 
+def anderson_weights(U, r):
+    """sinkhorn.py:197-212: the window weights c with (U'U + r I) c
+    proportional to the ones vector and sum(c) = 1.  The k x k system is
+    solved by Gaussian elimination with partial pivoting (the device's
+    algorithm; LAPACK dgesv in the reference); an exactly zero pivot or a
+    zero / non-finite normaliser raises LinAlgError like the reference."""
+    U = np.asarray(U, dtype=np.float64)
+    if U.ndim != 2 or U.shape[1] < 1:
+        raise ValueError("U must be a matrix with at least one column")
+    k = U.shape[1]
+    A = np.empty((k, k))
+    for i in range(k):
+        for j in range(k):
+            A[i, j] = float(np.dot(U[:, i], U[:, j]))
+        A[i, i] += r
+    sol = _solve_pivoted(A, np.ones(k))
+    den = float(sol.sum())
+    if not np.isfinite(den) or den == 0.0:
+        raise np.linalg.LinAlgError("degenerate weight normalization")
+    return sol / den
+
+
+def _solve_pivoted(A, rhs):
+    A = A.copy()
+    x = rhs.astype(np.float64).copy()
+    k = A.shape[0]
+    for col in range(k):
+        piv = col + int(np.argmax(np.abs(A[col:, col])))
+        if A[piv, col] == 0.0:
+            raise np.linalg.LinAlgError("Singular matrix")
+        if piv != col:
+            A[[col, piv]] = A[[piv, col]]
+            x[[col, piv]] = x[[piv, col]]
+        for row in range(col + 1, k):
+            fac = A[row, col] / A[col, col]
+            A[row, col:] -= fac * A[col, col:]
+            x[row] -= fac * x[col]
+    for row in range(k - 1, -1, -1):
+        x[row] = (x[row] - float(np.dot(A[row, row + 1:], x[row + 1:]))) / A[row, row]
+    return x
+
+
+class AndersonState:
+    """sinkhorn.py:215-243: window of (T z, T z - z); restart when the new
+    residual's sup norm exceeds the previous one's, keep the last ``depth``."""
+
+    def __init__(self, depth, reg):
+        self.depth, self.reg = depth, reg
+        self.maps, self.res, self.sizes = [], [], []
+
+    def push_extrapolate(self, z, tz):
+        r = tz - z
+        size = float(np.abs(r).max())
+        if self.sizes and size > self.sizes[-1]:
+            self.maps, self.res, self.sizes = [], [], []
+        self.maps.append(tz)
+        self.res.append(r)
+        self.sizes.append(size)
+        if len(self.maps) > self.depth:
+            self.maps, self.res, self.sizes = self.maps[1:], self.res[1:], self.sizes[1:]
+        if len(self.maps) == 1:
+            return self.maps[0]
+        c = anderson_weights(np.stack(self.res, axis=1), self.reg)
+        zn = np.zeros(len(z))
+        for ck, mk in zip(c, self.maps):
+            zn = zn + ck * mk
+        return zn
+
+
+def sinkhorn_anderson(cost, aw, bw, eps, r1, r2, variant, iters, depth, reg, f0=None,
+                      g0=None, ents=("kl", "kl")):
+    """sinkhorn.py:246-315 with ``config.anderson`` set (window state
+    :215-243): every iteration maps z = (f, g) through one step, pushes
+    (T z, T z - z) -- the window restarts when the new residual's sup norm
+    exceeds the previous one's, and keeps the last ``depth`` entries -- and
+    moves to the extrapolation sum_k c_k (T z)_k.  Variant "g" carries the
+    step's lambda (:270-271).  Exactly ``iters`` iterations (no early
+    exit); returns (f, g, delta_f trace)."""
+    n, m = cost.n, cost.m
+    f = np.zeros(n) if f0 is None else _c64(f0).copy()
+    g = np.zeros(m) if g0 is None else _c64(g0).copy()
+    lam = lambda_star_any(aw, bw, f, g, ents, r1, r2) if variant == "g" else 0.0
+    win = AndersonState(depth, reg)
+    deltas = np.empty(iters)
+    for t in range(iters):
+        if variant == "g":
+            fn, gn, lam = g_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, lam, ents)
+        elif variant == "h":
+            fn, gn = h_sinkhorn_step(cost, aw, bw, f, g, eps, r1, r2)
+        else:
+            fn, gn = f_sinkhorn_step_any(cost, aw, bw, f, g, eps, r1, r2, ents)
+        zn = win.push_extrapolate(np.concatenate([f, g]), np.concatenate([fn, gn]))
+        deltas[t] = float(np.abs(zn[:n] - f).max())
+        f, g = zn[:n].copy(), zn[n:].copy()
+    return f, g, deltas
+
+
 def h_optimality_residual(cost, aw, bw, f, g, eps, r1, r2, side="f"):
     """sinkhorn.py:166-189."""
     lam = lambda_star_kl(aw, bw, f, g, r1, r2)

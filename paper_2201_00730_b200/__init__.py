@@ -50,8 +50,10 @@ from .fw import FwConfig, feasibility_violation, fw_solve, fw_solve_batched
 from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched
 from .sinkhorn import (
     AndersonConfig,
+    AndersonWindow,
     SinkhornConfig,
     SolverReport,
+    anderson_weights,
     f_sinkhorn_step,
     g_sinkhorn_step,
     h_optimality_residual,

@@ -30,7 +30,8 @@ from .measures import ExplicitMatrix, PowerDistance, SqEuclideanPoints, check_su
 
 @dataclass(frozen=True)
 class AndersonConfig:
-    """Anderson window (src/sinkhorn.py:45-56); accepted, not on the B200 path."""
+    """Anderson window depth and ridge (src/sinkhorn.py:45-56); the window
+    lives on the device (csrc/anderson.cu), depth <= 32 there."""
 
     depth: int = 4
     reg: float = 1e-7
@@ -320,7 +321,7 @@ def run(prob, config, init=None, reference=None):
     if reference is not None:
         require_kl(prob.ent1, prob.ent2, what="err_f tracing")
     if config.anderson is not None:
-        raise UnsupportedEntropyError("Anderson extrapolation is not on the B200 path")
+        return _run_anderson(prob, config, d, reference, e1, e2)
     t = D.torch()
     costname, p, x, y, C = _step_inputs(prob)
     deltas, walls, err_f, err_g = [], [], [], []
@@ -362,3 +363,115 @@ def run(prob, config, init=None, reference=None):
         trace["err_g"] = np.asarray(err_g)
     return SolverReport(final=DualPair(f_cur, g_cur), iterations=len(deltas), converged=converged,
                         trace=trace)
+
+
+def anderson_weights(U, r):
+    """Window weights c with (U'U + r I) c proportional to 1 and sum c = 1
+    (src/sinkhorn.py:197-212), computed on the device (uot_anderson_weights:
+    block-reduced Gram, pivoted elimination).  Raises LinAlgError on a
+    singular window like the reference."""
+    U = np.asarray(U, dtype=np.float64)
+    if U.ndim != 2 or U.shape[1] < 1:
+        raise ValueError("U must be a matrix with at least one column")
+    t = D.torch()
+    lib = _lib.load()
+    rows, k = U.shape
+    Ud = D.to_dev(U, t.float64)
+    c = D.empty((k,), t.float64)
+    st = t.zeros((1,), dtype=t.int32, device=Ud.device)
+    _lib.check(lib.uot_anderson_weights(rows, k, _lib.ptr(Ud), float(r), _lib.ptr(c), _lib.ptr(st),
+                                        _lib.stream_handle()), "uot_anderson_weights")
+    if int(st.item()) != 0:
+        raise np.linalg.LinAlgError("singular or degenerate Anderson window")
+    return D.to_np(c, readonly=False)
+
+
+class AndersonWindow:
+    """Device-resident Anderson state for ``batch`` windows over vectors of
+    length ``length`` (mirror of src/sinkhorn.py:215-243 _AndersonState)."""
+
+    def __init__(self, batch, length, depth, reg, stream=None):
+        self.lib = _lib.load()
+        self.batch, self.length, self.depth, self.reg = int(batch), int(length), int(depth), float(reg)
+        size = ctypes.c_size_t(0)
+        _lib.check(self.lib.uot_anderson_workspace_size(self.batch, self.length, self.depth,
+                                                        ctypes.byref(size)), "anderson workspace")
+        self.nbytes = size.value
+        self.ws = D.workspace(self.nbytes)
+        t = D.torch()
+        self.delta = D.empty((self.batch,), t.float64)
+        self.status = t.zeros((self.batch,), dtype=t.int32, device=self.ws.device)
+        self.stream = stream
+        _lib.check(self.lib.uot_anderson_reset(self.batch, self.length, self.depth,
+                                               _lib.ptr(self.ws), self.nbytes,
+                                               _lib.stream_handle(stream)), "uot_anderson_reset")
+
+    def step(self, z, tz, znew, nf):
+        """push(z, tz) + extrapolate into znew (device fp64 [batch, length]);
+        returns the device tensors (delta_f [batch], status [batch])."""
+        _lib.check(self.lib.uot_anderson_step(
+            self.batch, self.length, int(nf), self.depth, self.reg, _lib.ptr(z), _lib.ptr(tz),
+            _lib.ptr(znew), _lib.ptr(self.delta), _lib.ptr(self.status), _lib.ptr(self.ws),
+            self.nbytes, _lib.stream_handle(self.stream)), "uot_anderson_step")
+        return self.delta, self.status
+
+
+def _run_anderson(prob, config, d, reference, e1, e2):
+    """run() with ``config.anderson`` (src/sinkhorn.py:281-292): each
+    iteration is one device step of the variant from the current f (and, for
+    "g", the carried lambda), then the device window's push + extrapolation
+    of the concatenated (f, g).  The reference's step maps read g only
+    through lambda, so the extrapolated g is carried for "g" and returned."""
+    t = D.torch()
+    n, m = len(prob.alpha), len(prob.beta)
+    variant = config.variant
+    if variant == "g" or reference is not None:
+        if variant != "f":
+            require_kl(prob.ent1, prob.ent2, what="translated Anderson iterates")
+    r1, r2 = ent_rho(prob.ent1), ent_rho(prob.ent2)
+    aw, bw = prob.alpha.weights, prob.beta.weights
+    costname, p, x, y, C = _step_inputs(prob)
+    f64 = t.float64
+    z = D.to_dev(np.concatenate([np.asarray(d.f, np.float64), np.asarray(d.g, np.float64)]),
+                 f64).reshape(1, n + m)
+    tz = t.empty_like(z)
+    win = AndersonWindow(1, n + m, config.anderson.depth, config.anderson.reg)
+    lam = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item()) if variant == "g" else 0.0
+    deltas, walls, err_f, err_g = [], [], [], []
+    converged = False
+    for _ in range(config.max_iters):
+        t0 = time.perf_counter_ns()
+        g_in = None
+        if variant == "g":  # start the device G step at the carried lambda (g_sinkhorn_step)
+            lam0 = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item())
+            g_in = z[0, n:] + (lam - lam0) * (r1 + r2) / r1
+        f1, g1, _, _ = sinkhorn_batched(x, y, aw, bw, prob.eps, r1, r2, 1, variant=variant,
+                                        cost=costname, p=p, c=C, f0=z[0, :n], g0=g_in,
+                                        precision=config.precision, ent1=e1, ent2=e2)
+        tz[0, :n].copy_(f1[0])
+        tz[0, n:].copy_(g1[0])
+        if variant == "g":
+            lam = float(kl_scalars(aw, bw, tz[0, :n], tz[0, n:], r1, r2)[0, 0].item())
+        delta, status = win.step(z, tz, z, n)
+        dl = float(delta[0].item())
+        if int(status[0].item()) != 0:
+            raise np.linalg.LinAlgError("singular Anderson window (anderson_weights)")
+        walls.append(time.perf_counter_ns() - t0)
+        deltas.append(dl)
+        if reference is not None:
+            shift = 0.0
+            if variant != "f":
+                shift = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item())
+            fz = D.to_np(z[0, :n])
+            gz = D.to_np(z[0, n:])
+            err_f.append(float(np.abs(fz + shift - reference.f).max()))
+            err_g.append(float(np.abs(gz - shift - reference.g).max()))
+        if dl < config.tol:
+            converged = True
+            break
+    trace = {"delta_f": np.asarray(deltas), "wall_ns": np.asarray(walls, dtype=np.int64)}
+    if reference is not None:
+        trace["err_f"] = np.asarray(err_f)
+        trace["err_g"] = np.asarray(err_g)
+    final = DualPair(D.to_np(z[0, :n]).copy(), D.to_np(z[0, n:]).copy())
+    return SolverReport(final=final, iterations=len(deltas), converged=converged, trace=trace)

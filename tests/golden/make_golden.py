@@ -524,9 +524,73 @@ def gen_duality():
     save("duality.npz", **out)
 
 
+def gen_anderson():
+    """Anderson-extrapolated runs (sinkhorn.py:197-243, :281-292) through the
+    reference's own ``run`` (tol 1e-300 so the budget is spent unless delta_f
+    hits exactly 0), plus ``anderson_weights`` known answers."""
+    from uotkit.synthetic import mixture_measure
+
+    out = {}
+    cases = []
+    # the reference's own acceleration test problem (tests/test_sinkhorn.py:260-271)
+    a, _ = mixture_measure(20, 55)
+    b, _ = mixture_measure(20, 56)
+    specs = [(a.points, a.weights, b.points, b.weights, 2.0, 0.1, 5.0, 5.0, "f", 200, 4, 1e-7,
+              "kl", None)]
+    rng = np.random.default_rng(97)
+    combos = [("f", 4, 1e-7, "kl"), ("h", 4, 1e-7, "kl"), ("g", 4, 1e-7, "kl"),
+              ("f", 1, 1e-7, "kl"), ("f", 2, 1e-3, "kl"), ("h", 7, 1e-7, "kl"),
+              ("f", 5, 0.0, "kl"), ("f", 4, 1e-7, "berg"), ("g", 3, 1e-6, "kl"),
+              ("h", 3, 1e-5, "kl")]
+    for k, (var, depth, reg, ent) in enumerate(combos):
+        n, m = int(rng.integers(4, 48)), int(rng.integers(4, 48))
+        p = [2.0, 1.0, 1.5][k % 3]
+        eps = [0.1, 0.3, 0.05][k % 3]
+        r1, r2 = float(rng.uniform(0.5, 3.0)), float(rng.uniform(0.5, 3.0))
+        x = np.sort(rng.uniform(0, 1, n))
+        y = np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m) * 1.4
+        start = None
+        if k % 2 == 1:
+            C = np.abs(x[:, None] - y[None, :]) ** p
+            start = (0.5 * C.min(axis=1) + 0.05, 0.5 * C.min(axis=0) - 0.05)
+        specs.append((x, wa, y, wb, p, eps, r1, r2, var, 60, depth, reg, ent, start))
+    c = S.cfg1_inputs()
+    specs.append((c.x, c.alpha, c.y, c.beta, 2.0, c.eps, c.rho, c.rho, "f", 300, 4, 1e-7, "kl",
+                  None))
+    for k, (x, wa, y, wb, p, eps, r1, r2, var, iters, depth, reg, ent, start) in enumerate(specs):
+        E = U.KL if ent == "kl" else U.Berg
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(p), E(r1), E(r2), eps=eps)
+        init = None if start is None else U.DualPair(*start)
+        cfg = US.SinkhornConfig(var, iters, 1e-300, US.AndersonConfig(depth, reg))
+        rep = US.run(prob, cfg, init=init)
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_f0"] = np.zeros(len(x)) if start is None else start[0]
+        out[f"c{k}_g0"] = np.zeros(len(y)) if start is None else start[1]
+        out[f"c{k}_f"], out[f"c{k}_g"] = rep.final.f, rep.final.g
+        out[f"c{k}_delta"] = rep.trace["delta_f"]
+        out[f"c{k}_par"] = np.array([p, eps, r1, r2, iters, depth, reg,
+                                     {"f": 0, "h": 1, "g": 2}[var], 0 if ent == "kl" else 1])
+        cases.append(k)
+    out["cases"] = np.array(cases)
+    # anderson_weights known answers (tests/test_sinkhorn.py:243-258) + random windows
+    wins = [(np.array([[1.0], [2.0]]), 1e-7), (np.tile(np.array([[1.0], [2.0]]), (1, 3)), 1e-7),
+            (np.array([[np.sqrt(2.0), 0.0], [0.0, 1.0]]), 0.0)]
+    for k in range(6):
+        wins.append((rng.normal(size=(int(rng.integers(3, 200)), k % 5 + 2)), [0.0, 1e-7, 1e-2][k % 3]))
+    for k, (Um, r) in enumerate(wins):
+        out[f"w{k}_U"], out[f"w{k}_r"] = Um, np.array(r)
+        out[f"w{k}_c"] = US.anderson_weights(Um, r)
+    out["nwin"] = np.array(len(wins))
+    save("anderson.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
-                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert", "sinkhorn_ent"]
+                             "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
+                             "sinkhorn_ent", "anderson"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

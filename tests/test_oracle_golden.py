@@ -198,3 +198,28 @@ def test_duality_scalars():
         cost = O.PointCost(z[f"c{k}_x"], z[f"c{k}_y"], p=2.0, power1d=True)
         H = O.eval_h_kl(a, b, f, g, r1, r2, eps, smin_fn=lambda ff, e: cost.smin_cols(ff, e, a))
         assert abs(H - float(z[f"c{k}_H"])) <= 1e-10 * (1 + abs(H))
+
+
+def test_anderson_weights_known_answers():
+    """anderson_weights restatement vs the reference (tests/test_sinkhorn.py:243-258)."""
+    z = golden("anderson.npz")
+    for k in range(int(z["nwin"])):
+        c = O.anderson_weights(z[f"w{k}_U"], float(z[f"w{k}_r"]))
+        np.testing.assert_allclose(c, z[f"w{k}_c"], rtol=1e-7, atol=1e-12)
+    with pytest.raises(np.linalg.LinAlgError):
+        O.anderson_weights(np.zeros((3, 2)), 0.0)
+
+
+def test_anderson_runs():
+    """Anderson-extrapolated F / H / G runs vs the reference's own run()."""
+    z = golden("anderson.npz")
+    for k in cases(z):
+        p, eps, r1, r2, iters, depth, reg, var, ent = z[f"c{k}_par"]
+        var = "fhg"[int(var)]
+        ents = ("kl", "kl") if ent == 0 else ("berg", "berg")
+        cost = O.PointCost(z[f"c{k}_x"], z[f"c{k}_y"], p=p, power1d=True)
+        steps = len(z[f"c{k}_delta"])
+        f, g, dl = O.sinkhorn_anderson(cost, z[f"c{k}_a"], z[f"c{k}_b"], eps, r1, r2, var, steps,
+                                       int(depth), reg, z[f"c{k}_f0"], z[f"c{k}_g0"], ents=ents)
+        assert rel_err(f, g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-9, (k, var)
+        np.testing.assert_allclose(dl, z[f"c{k}_delta"], rtol=1e-5, atol=1e-11)
