@@ -54,6 +54,7 @@ from .sinkhorn import (
     SinkhornConfig,
     SolverReport,
     anderson_weights,
+    estimate_rate,
     f_sinkhorn_step,
     g_sinkhorn_step,
     h_optimality_residual,
@@ -61,6 +62,19 @@ from .sinkhorn import (
     run,
     sinkhorn_batched,
     verify_batched,
+    write_trace_csv,
 )
+from .formats import (
+    read_measure_csv,
+    read_measure_json,
+    read_multiplan_csv,
+    read_plan_csv,
+    write_gap_csv,
+    write_measure_csv,
+    write_measure_json,
+    write_multiplan_csv,
+    write_plan_csv,
+)
+from .synthetic import mixture_measure, uniform_measure
 
 __version__ = "0.1.0"

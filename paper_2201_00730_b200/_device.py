@@ -26,7 +26,10 @@ def to_dev(a, dtype):
     t = torch()
     if isinstance(a, t.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
-    return t.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=device()).contiguous()
+    arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:  # read-only API arrays: torch wants a writable buffer
+        arr = arr.copy()
+    return t.as_tensor(arr, dtype=dtype, device=device()).contiguous()
 
 
 def to_np(t, readonly=True):

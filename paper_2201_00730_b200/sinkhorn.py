@@ -475,3 +475,28 @@ def _run_anderson(prob, config, d, reference, e1, e2):
         trace["err_g"] = np.asarray(err_g)
     final = DualPair(D.to_np(z[0, :n]).copy(), D.to_np(z[0, n:]).copy())
     return SolverReport(final=final, iterations=len(deltas), converged=converged, trace=trace)
+
+
+def estimate_rate(errors):
+    """Empirical contraction factor exp(median_t log(e_{t+1}/e_t))
+    (src/sinkhorn.py:318-335): trailing entries below 1e-13 (noise floor) are
+    dropped first; fewer than two usable ratios raise ValueError.  Host
+    statistic over a trace the device produced."""
+    e = np.asarray(errors, dtype=np.float64)
+    if e.ndim != 1 or e.size < 3:
+        raise ValueError("need at least three error values")
+    if (e <= 0).any():
+        raise ValueError("errors must be strictly positive")
+    keep = e.size
+    while keep > 0 and e[keep - 1] < 1e-13:
+        keep -= 1
+    if keep < 3:
+        raise ValueError("fewer than 2 usable ratios after truncation")
+    return float(np.exp(np.median(np.diff(np.log(e[:keep])))))
+
+
+def write_trace_csv(report, path_or_buf):
+    """``iter,delta_f,err_f,err_g,wall_ns`` rows (src/sinkhorn.py:349-373)."""
+    from .formats import write_trace_csv as _w
+
+    _w(report, path_or_buf)

@@ -31,6 +31,8 @@ __all__ = [
     "cfg5_batch",
     "max_sq_distance",
     "gaussian_pdf",
+    "mixture_measure",
+    "uniform_measure",
 ]
 
 
@@ -178,3 +180,35 @@ def cfg5_batch(batch=64, k=16, n=8192, seed=2025, start=0, count=None, floor=1e-
             x[p, q] = pts
             w[p, q] = dens * (rng.uniform(0.5, 2.0) / dens.sum())
     return x, w
+
+
+# -- CLI generators (src/synthetic.py:12-49), same draws per seed ------------
+
+
+def mixture_measure(n, seed, sigma=0.03, mu1_range=(0.1, 0.4), mu2_range=(0.6, 0.9),
+                    amp_range=(0.1, 0.8)):
+    """Two-bump empirical mixture with equal atom weights 1/n: centres from
+    the two ranges, amplitudes from ``amp_range``, each sample assigned to
+    the first bump with probability a/(a+b).  Returns (measure, params)."""
+    from .measures import DiscreteMeasure
+
+    if n < 1:
+        raise ValueError("need at least one sample")
+    rng = np.random.default_rng(seed)
+    centre1, centre2 = float(rng.uniform(*mu1_range)), float(rng.uniform(*mu2_range))
+    amp1, amp2 = float(rng.uniform(*amp_range)), float(rng.uniform(*amp_range))
+    first = rng.random(n) < amp1 / (amp1 + amp2)
+    z = rng.normal(0.0, 1.0, n)
+    pts = np.where(first, centre1 + sigma * z, centre2 + sigma * z)
+    return (DiscreteMeasure(pts, np.full(n, 1.0 / n)),
+            {"sigma": sigma, "mu1": centre1, "mu2": centre2, "a": amp1, "b": amp2})
+
+
+def uniform_measure(n, seed, lo=0.0, hi=1.0):
+    """n atoms drawn uniformly on [lo, hi], weights 1/n."""
+    from .measures import DiscreteMeasure
+
+    if n < 1:
+        raise ValueError("need at least one sample")
+    pts = np.random.default_rng(seed).uniform(lo, hi, n)
+    return DiscreteMeasure(pts, np.full(n, 1.0 / n)), {"lo": lo, "hi": hi}

@@ -587,10 +587,65 @@ def gen_anderson():
     save("anderson.npz", **out)
 
 
+def gen_formats():
+    """Reference writer outputs (measures / plans / traces, src/measures.py:185-254,
+    src/ot1d.py:188-215, src/barycenter.py:446-475, src/sinkhorn.py:349-373,
+    src/fw.py:360-381) and `uotkit gen` stdout, as text fixtures."""
+    import contextlib
+    import io
+
+    from uotkit import cli as UC
+    from uotkit import measures as UM
+    from uotkit import ot1d as UO
+
+    out = {}
+
+    def text(fn, *args):
+        buf = io.StringIO()
+        fn(*args, buf)
+        return buf.getvalue()
+
+    for k, (kind, n, seed) in enumerate([("mixture", 40, 9), ("uniform", 3, 5), ("mixture", 5, 1),
+                                         ("uniform", 17, 123)]):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert UC.main(["gen", "--kind", kind, "--n", str(n), "--seed", str(seed)]) == 0
+        out[f"gen{k}_args"] = np.array([kind, str(n), str(seed)])
+        out[f"gen{k}_text"] = np.array(buf.getvalue())
+    rng = np.random.default_rng(5)
+    a = U.DiscreteMeasure(rng.uniform(0, 1, 7), rng.uniform(0.1, 1, 7))
+    b = U.DiscreteMeasure(rng.uniform(0, 1, 5), rng.uniform(0.1, 1, 5) * 0.0 + a.mass / 5)
+    out["ma_x"], out["ma_w"] = a.points, a.weights
+    out["mb_x"], out["mb_w"] = b.points, b.weights
+    out["ma_csv"] = np.array(UM.measure_to_csv_text(a, ["one", "two three"]))
+    out["ma_json"] = np.array(text(UM.write_measure_json, a))
+    plan, _ = U.solve_ot_1d(a, b, U.PowerDistance(2.0))
+    out["plan_i"], out["plan_j"], out["plan_m"] = plan.source_idx, plan.target_idx, plan.mass
+    out["plan_csv"] = np.array(text(UO.write_plan_csv, plan))
+    mp = UB.MultiPlan(np.array([[0, 0, 0], [0, 1, 0], [1, 1, 2]]), np.array([0.25, 0.5, 1e-17]))
+    out["mp_idx"], out["mp_mass"] = mp.indices, mp.mass
+    out["mp_csv"] = np.array(text(UB.write_multiplan_csv, mp))
+    tr = {"delta_f": np.array([0.5, 1e-3, 2.5e-17]), "wall_ns": np.array([10, 20, 30])}
+    rep = US.SolverReport(final=U.DualPair.zeros(1, 1), iterations=3, converged=True, trace=tr)
+    out["tr_delta"], out["tr_wall"] = tr["delta_f"], tr["wall_ns"]
+    out["trace_csv"] = np.array(text(US.write_trace_csv, rep))
+    tr2 = dict(tr, err_f=np.array([1.0, 0.1, 0.01]), err_g=np.array([2.0, 0.2, 1e-300]))
+    rep2 = US.SolverReport(final=U.DualPair.zeros(1, 1), iterations=3, converged=True, trace=tr2)
+    out["tr_errf"], out["tr_errg"] = tr2["err_f"], tr2["err_g"]
+    out["trace_ref_csv"] = np.array(text(US.write_trace_csv, rep2))
+    tg = {"h0": np.array([0.1, 0.2]), "fw_gap": np.array([1.0, 1e-9]),
+          "pd_gap": np.array([2.0, -1e-18]), "wall_ns": np.array([5, 7])}
+    rep3 = US.SolverReport(final=U.DualPair.zeros(1, 1), iterations=2, converged=True, trace=tg)
+    out["gap_h0"], out["gap_fw"], out["gap_pd"], out["gap_wall"] = (tg["h0"], tg["fw_gap"],
+                                                                    tg["pd_gap"], tg["wall_ns"])
+    out["gap_csv"] = np.array(text(UF.write_gap_csv, rep3))
+    save("formats.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson"]
+                             "sinkhorn_ent", "anderson", "formats"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()
