@@ -376,7 +376,9 @@ def run_cfg2(rank, world, dev, peaks):
     x, y, a, b = S.cfg2_batch(batch=4096, start=lo, count=hi - lo)
     x, y, a, b = (torch.as_tensor(v, device=dev) for v in (x, y, a, b))
     iters = 500
-    P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 5, "linesearch")
+    # warm-up with the timed shapes, so the caching allocator already holds the
+    # trace / workspace blocks (their cudaMalloc is not part of an iteration)
+    P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, iters, "linesearch")
     torch.cuda.synchronize()
     with cuda_timer() as t:
         r = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, iters, "linesearch")
@@ -409,7 +411,7 @@ def run_cfg2_pfw(rank, world, dev, peaks):
     x, y, a, b = S.cfg2_batch(batch=4096, start=lo, count=hi - lo)
     x, y, a, b = (torch.as_tensor(v, device=dev) for v in (x, y, a, b))
     iters = 200
-    P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 5, "pairwise")
+    P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, iters, "pairwise")  # warm-up, same shapes
     torch.cuda.synchronize()
     with cuda_timer() as t:
         r = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, iters, "pairwise")
@@ -446,7 +448,7 @@ def run_cfg5(rank, world, dev, peaks):
     x, a = torch.as_tensor(xs, device=dev), torch.as_tensor(ws, device=dev)
     w = np.full(16, 1 / 16)
     iters = 1000
-    P.fw_barycenter_batched(x, a, w, 1.0, 3, "linesearch")
+    P.fw_barycenter_batched(x, a, w, 1.0, iters, "linesearch")  # warm-up, same shapes
     torch.cuda.synchronize()
     with cuda_timer() as t:
         r = P.fw_barycenter_batched(x, a, w, 1.0, iters, "linesearch")
@@ -520,7 +522,8 @@ def run_cfg4(rank, world, dev):
     x, y, a, b = S.cfg4_batch(start=lo, count=hi - lo)
     xt, yt, at, bt = (torch.as_tensor(v, dtype=torch.float32, device=dev) for v in (x, y, a, b))
     iters = 30
-    P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, 2, precision="fp32")
+    P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
+                       precision="fp32")  # warm-up, same shapes
     torch.cuda.synchronize()
     with cuda_timer() as t:
         P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
