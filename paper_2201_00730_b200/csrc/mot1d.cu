@@ -47,10 +47,10 @@ constexpr int MT = 512;           // threads of the per-list CTAs
 #define UOT_BT 512
 #endif
 constexpr int BT = UOT_BT;  // threads of the bucket CTAs
-constexpr int CAP = 4096;         // events per bucket (two shared-memory buffers)
+constexpr int CAP = 3072;         // events per bucket (two shared-memory buffers)
 constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
 constexpr int ST = 1024;          // threads of the per-problem splitter CTA
-constexpr int SMAX = 128;         // buckets per problem
+constexpr int SMAX = 192;         // buckets per problem
 
 struct MotArgs {
   int batch, k, n;        // n = row stride (max list length)
@@ -1193,7 +1193,7 @@ int ept_for(int n) {
 MotPlan plan_for(int k, int n) {
   MotPlan p;
   const long events = (long)k * (n - 1);
-  p.S = (int)std::max(1L, (events + 2047) / 2048);
+  p.S = (int)std::min((long)SMAX, std::max(1L, (events + 1535) / 1536));
   p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
   while ((long)k * p.SS > 4096) p.SS = std::max(1, p.SS / 2);
   p.ept = ept_for(n);
