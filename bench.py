@@ -217,6 +217,42 @@ def cpu_cfg5(iters=2):
     return rate, cores, sample
 
 
+def cpu_cfg4(cols=1024):
+    """cfg4: one g half-step of problem 0 restricted to `cols` columns (fp64
+    oracle, d = 64 squared Euclidean computed directly), all host threads;
+    scaled to 2 x 256 x 4096 x 4096 pair evaluations per batched iteration."""
+    import oracle as O
+    from paper_2201_00730_b200 import synthetic as S
+
+    threads = host_cores()
+    os.environ["ORACLE_THREADS"] = str(threads)
+    x, y, a, b = S.cfg4_batch(count=1)
+    cost = O.PointCost(x[0], y[0][:cols])
+    t0 = time.perf_counter()
+    cost.smin_cols(np.zeros(x.shape[1]), S.CFG4_EPS, a[0])
+    el = time.perf_counter() - t0
+    pairs = x.shape[1] * cols
+    rate = 1.0 / (el / pairs * 2.0 * 256 * x.shape[1] * y.shape[1])
+    sample = (f"one g half-step of problem 0 restricted to {cols} of {y.shape[1]} columns "
+              f"({pairs:.3g} pairs, d=64, fp64 C oracle, {threads} threads), extrapolated to "
+              f"2*B*N*M pairs per batched iteration")
+    return rate, threads, sample
+
+
+def cpu_cfg1(iters=1000):
+    """cfg1: the oracle port's H-Sinkhorn on one core, `iters` iterations."""
+    import oracle as O
+    from paper_2201_00730_b200 import synthetic as S
+
+    os.environ["ORACLE_THREADS"] = "1"
+    c = S.cfg1_inputs()
+    cost = O.PointCost(c.x, c.y, p=2.0, power1d=True)
+    t0 = time.perf_counter()
+    O.sinkhorn_fixed(cost, c.alpha, c.beta, c.eps, c.rho, c.rho, "h", iters)
+    el = time.perf_counter() - t0
+    return iters / el, 1, f"{iters} H iterations of cfg1 (oracle port, one thread)"
+
+
 # ---------------------------------------------------------------------------
 # Headline: cfg3 TI-Sinkhorn (row-sharded for N > 1).
 
@@ -622,6 +658,13 @@ def main():
                 v5, c5, s5 = cpu_cfg5()
                 secondary["cfg5_barycenter"]["cpu_baseline"] = {
                     "value": v5, "unit": "iter/s", "cores": c5, "kind": "port", "sample": s5}
+                v4, c4, s4 = cpu_cfg4()
+                secondary["cfg4_sinkhorn_d64"]["cpu_baseline"] = {
+                    "value": v4, "unit": "iter/s", "cores": c4, "kind": "port", "sample": s4}
+                v1, c1, s1 = cpu_cfg1()
+                secondary["cfg1_sinkhorn_1d"]["cpu_baseline"] = {
+                    "value": v1, "unit": "iter/s (H)", "cores": c1, "kind": "port", "sample": s1}
+                os.environ["ORACLE_THREADS"] = str(host_cores())
             line["secondary"] = secondary
             line["peaks"] = {"hbm_gbs": peaks.get("hbm_gbs"), "source": peak_src}
             line["clocks"] = clk.summary()
