@@ -194,3 +194,18 @@ extern "C" int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const dou
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }
+
+#ifdef UOT_NEWTON_STATS
+// scripts/newton_stats.py (stats build only): Newton passes / line searches
+extern "C" int uot_debug_fw_stats(unsigned long long* out, int reset) {
+  unsigned long long h[2];
+  cudaMemcpyFromSymbol(h, uot::fwk::g_newton_stats, sizeof(h));
+  out[0] = h[0];
+  out[1] = h[1];
+  if (reset) {
+    h[0] = h[1] = 0;
+    cudaMemcpyToSymbol(uot::fwk::g_newton_stats, h, sizeof(h));
+  }
+  return 0;
+}
+#endif

@@ -29,6 +29,9 @@
 
 namespace uot {
 namespace fwk {
+#ifdef UOT_NEWTON_STATS
+static __device__ unsigned long long g_newton_stats[2];  // passes, line searches
+#endif
 
 constexpr int FW_THREADS = 256;
 #ifndef FW_MINB
@@ -790,6 +793,9 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       } else {
         double lo = 0.0, hi = 1.0;
         gam = (d2 > 0.0) ? fmin(1.0, -k0 / d2) : 1.0;
+#ifdef UOT_NEWTON_STATS
+        if (threadIdx.x == 0) atomicAdd(&g_newton_stats[1], 1ull);
+#endif
         for (int it = 0; it < 24; ++it) {
           // one pass: centred moments of va / vb under p_gamma, q_gamma; the
           // shift (1-gamma) sh + gamma max(-r/r1) bounds every exponent.
@@ -812,6 +818,9 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
             mom[5] += wb * xb * xb;
           }
           bops::block_sum<FW_NW, 6>(mom, ping.next());
+#ifdef UOT_NEWTON_STATS
+          if (threadIdx.x == 0) atomicAdd(&g_newton_stats[0], 1ull);
+#endif
           const double a1 = mom[1] / mom[0], a2 = mom[2] / mom[0];
           const double b1 = mom[4] / mom[3], b2 = mom[5] / mom[3];
           const double g1 = k0 - t1 * a1 - t2 * b1;

@@ -98,6 +98,9 @@ __device__ __forceinline__ int list_len(const MotArgs& A, int q) {
 }
 
 constexpr int MNW = MT / 32;
+#ifdef UOT_NEWTON_STATS
+__device__ unsigned long long g_mot_stats[2];  // Newton passes, line searches
+#endif
 constexpr int MBUF = 16 * MNW;  // one-sync reduction buffer (doubles)
 
 // EPT consecutive doubles of a row starting at i0 (zero past nq); 16-byte
@@ -875,6 +878,9 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     } else {
       double lo = 0.0, hi = 1.0;
       gam = vs[0] > 0.0 ? fmin(1.0, -k0 / vs[0]) : 1.0;
+#ifdef UOT_NEWTON_STATS
+      if (threadIdx.x == 0 && q == 0) atomicAdd(&g_mot_stats[1], 1ull);
+#endif
       for (int it = 0; it < 24; ++it) {
         const double sh = (1.0 - gam) * mxs[0] + gam * mxs[1];
         double mom[3] = {0.0, 0.0, 0.0};
@@ -888,6 +894,9 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
           mom[2] += ww * xc * xc;
         }
         bops::block_sum<MNW, 3>(mom, ping.next());
+#ifdef UOT_NEWTON_STATS
+        if (threadIdx.x == 0 && q == 0) atomicAdd(&g_mot_stats[0], 1ull);
+#endif
         const double e1 = mom[1] / mom[0];
         double gv[2] = {e1, (mom[2] / mom[0] - e1 * e1) / rq};
         cluster_sum<2>(gv, slots, parity);
@@ -1515,3 +1524,18 @@ extern "C" int uot_mot_certify(int32_t batch, int32_t k, int32_t n, const int32_
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }
+
+#ifdef UOT_NEWTON_STATS
+// scripts/newton_stats.py (stats build only): Newton passes / line searches
+extern "C" int uot_debug_mot_stats(unsigned long long* out, int reset) {
+  unsigned long long h[2];
+  cudaMemcpyFromSymbol(h, uot::g_mot_stats, sizeof(h));
+  out[0] = h[0];
+  out[1] = h[1];
+  if (reset) {
+    h[0] = h[1] = 0;
+    cudaMemcpyToSymbol(uot::g_mot_stats, h, sizeof(h));
+  }
+  return 0;
+}
+#endif
