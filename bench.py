@@ -566,19 +566,33 @@ def run_cfg4(rank, world, dev):
                            precision="fp32")
     ms = max_over_ranks(t.ms, world, dev)
     value = iters / (ms * 1e-3)  # batched iterations over all 256 problems (all ranks)
-    # tensor work per iteration: 2 half-steps x B x N x M pairs x 25 MMA-slices
-    # of 128x128x8 per 128x128 tile (3xTF32 split) = 2*256*4096^2*(25*8) MAC
-    macs = 2.0 * 256 * 4096 * 4096 * 25 * 8
-    return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32, tcgen05 kind::tf32 "
-                        "3xTF32 cost tiles (A in TMEM, B ring in smem) + MUFU LSE epilogue; "
+    # Per 256 x 128 pair tile: 12 kind::f16 MMAs (fp16 hi/lo splits, K = 16)
+    # and one kind::tf32 MMA (the row / column constants, K = 8); one ex2 per
+    # pair on the MUFU pipe, which now bounds the kernel.
+    tiles = 2.0 * 256 * (4096 / 256) * (4096 / 128)  # per iteration (two half-steps)
+    tflops = tiles * (12 * 2 * 256 * 128 * 16 + 2 * 256 * 128 * 8) * value / 1e12
+    exps = 2.0 * 256 * 4096 * 4096 * value / 1e9
+    import ctypes
+
+    from paper_2201_00730_b200 import _lib
+
+    lib = _lib.load()
+    peak = ctypes.c_double(0.0)
+    lib.uot_probe_mufu_ex2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
+    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(peak)))
+    peak_g = peak.value / 1e9
+    return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32, tcgen05 cost tiles "
+                        "(kind::f16 hi/lo splits + one kind::tf32 constants MMA, A in TMEM, B "
+                        "ring in smem, CTA pairs) + MUFU LSE epilogue; "
                         f"timed over {iters} of the 300 iterations",
-            "value": value, "unit": "iter/s", "dtype": "f32 (3xTF32 tensor)",
-            "roofline": {"bound": "tensor", "achieved": macs * 2 * value / 1e12,
-                         "peak": 1100.0, "unit": "TFLOP/s",
-                         "frac": macs * 2 * value / 1e12 / 1100.0,
-                         "peak_source": "B200_PROFILING.md dense tf32 1.1 PFLOP/s (MEASURED_PEAKS "
-                                        "has no tf32 figure); issue-rate probe: 64.1 cycles per "
-                                        "128x128x8 MMA = the floor"}}
+            "value": value, "unit": "iter/s", "dtype": "f32 (fp16-split tensor, fp32 accumulate)",
+            "roofline": {"bound": "mufu", "achieved": exps, "peak": peak_g, "unit": "Gex2/s",
+                         "frac": exps / peak_g,
+                         "work_per_iteration": "2*B*N*M = 8.59e9 ex2",
+                         "peak_source": "measured live: uot_probe_mufu_ex2"},
+            "tensor": {"achieved_tflops": tflops, "peak_tflops": 2250.0,
+                       "frac": tflops / 2250.0,
+                       "peak_source": "B200_PROFILING.md dense fp16 2.25 PFLOP/s"}}
 
 
 # ---------------------------------------------------------------------------

@@ -216,47 +216,58 @@ struct Explicit {
 };
 
 // fp32 squared Euclidean on d >= 32 features via tcgen05 (sinkhorn_tc.cuh).
-// Records are written straight into the canonical K-major tile layout that
-// the main kernel bulk-copies into shared memory.
+// Records are written straight into the tile layout that the main kernel
+// bulk-copies into shared memory.
 struct SqE32TC {
   using T = float;
   struct Out {
     float bias;
   };
   static int rw(int d) { return tc_kp(d); }
-  // Static part of a record, written once per solve (tc_init_static):
-  // Xh, Xl = tf32 split of 2L x, the unit columns, zero padding, and |x|^2
-  // (fp64) parked in the unused columns 2d+8, 2d+9 (no MMA reads them).
+  // Static part of a record, written once per solve (tc_init_static): the
+  // fp16 split Xh, Xl of (2L / 8) x, zero padding, the unit columns and
+  // |x|^2 (fp64) parked in float columns 8-9 (no MMA reads them).
   static __device__ __forceinline__ void init_tile(float* base, long r, int KP, const float* pt,
                                                    double L, int d) {
     float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
+    __half* th = reinterpret_cast<__half*>(tile);
     const int rl = (int)(r % TC_TILE);
+    const int dp = tc_dp(d), kh = tc_kh(d);
+    const double sc = 2.0 * L / (double)TC_YSCALE;
     double s2 = 0.0;
-    for (int k = 0; k < d; ++k) {
-      const float x = (float)(2.0 * L * (double)pt[k]);
-      const float xh = tf32_hi(x);
-      tile[tc_tile_index(rl, k, KP)] = xh;
-      tile[tc_tile_index(rl, d + k, KP)] = x - xh;
-      s2 += (double)pt[k] * (double)pt[k];
+    for (int k = 0; k < dp; ++k) {
+      float xh = 0.f, xl = 0.f;
+      if (k < d) {
+        const float x = (float)(sc * (double)pt[k]);
+        xh = __half2float(__float2half_rn(x));
+        xl = x - xh;
+        s2 += (double)pt[k] * (double)pt[k];
+      }
+      th[tc_xidx(rl, k, d)] = __float2half_rn(xh);
+      th[tc_xidx(rl, dp + k, d)] = __float2half_rn(xl);
     }
-    tile[tc_tile_index(rl, 2 * d + 3, KP)] = 1.f;
-    tile[tc_tile_index(rl, 2 * d + 4, KP)] = 1.f;
-    tile[tc_tile_index(rl, 2 * d + 5, KP)] = 1.f;
-    for (int k = 2 * d + 6; k < KP; ++k) tile[tc_tile_index(rl, k, KP)] = 0.f;
-    *reinterpret_cast<double*>(tile + tc_tile_index(rl, 2 * d + 8, KP)) = s2;
+    for (int k = 2 * dp; k < kh; ++k) th[tc_xidx(rl, k, d)] = __float2half_rn(0.f);
+    tile[tc_cidx(rl, 3, d)] = 1.f;
+    tile[tc_cidx(rl, 4, d)] = 1.f;
+    tile[tc_cidx(rl, 5, d)] = 1.f;
+    tile[tc_cidx(rl, 6, d)] = 0.f;
+    tile[tc_cidx(rl, 7, d)] = 0.f;
+    tile[tc_cidx(rl, 10, d)] = 0.f;
+    tile[tc_cidx(rl, 11, d)] = 0.f;
+    *reinterpret_cast<double*>(tile + tc_cidx(rl, 8, d)) = s2;
   }
   // Per half-step: only U = (hat - |x|^2) L + log2 w changes -- one 16-byte
-  // store [Uh, Um, Ul, 1] per record (columns 2d .. 2d+3).
+  // store [Uh, Um, Ul, 1] (tf32 splits) per record.
   static __device__ __forceinline__ void pack_tile(float* base, long r, int KP, double hat,
                                                    const float*, double w, double L, int d) {
     float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
     const int rl = (int)(r % TC_TILE);
-    const double s2 = *reinterpret_cast<const double*>(tile + tc_tile_index(rl, 2 * d + 8, KP));
+    const double s2 = *reinterpret_cast<const double*>(tile + tc_cidx(rl, 8, d));
     const double u = w > 0.0 ? (hat - s2) * L + log2(w) : -1e30;
     const float uh = tf32_hi((float)u);
     const double u1 = u - (double)uh;
     const float um = tf32_hi((float)u1);
-    *reinterpret_cast<float4*>(tile + tc_tile_index(rl, 2 * d, KP)) =
+    *reinterpret_cast<float4*>(tile + tc_cidx(rl, 0, d)) =
         make_float4(uh, um, (float)(u1 - (double)um), 1.f);
   }
 };
@@ -1837,7 +1848,7 @@ int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
         if (d.d == 1) return fn(Engine<SqE32<1>>());
         if (d.d == 2) return fn(Engine<SqE32<2>>());
         if (d.d == 3) return fn(Engine<SqE32<3>>());
-        if (d.d >= 32 && d.d % 8 == 0 && tc_ka(d.d) <= 256 && d.nranks <= 1 &&
+        if (d.d >= 32 && d.d % 4 == 0 && tc_ka(d.d) <= 256 && d.nranks <= 1 &&
             d.nccl_comm == nullptr)
           return fn(Engine<SqE32TC>());
         return fn(Engine<SqE32N>());

@@ -1,23 +1,26 @@
 // sinkhorn_tc.cuh -- tensor-core half-step for squared-Euclidean costs on
 // d >= 32 feature vectors (BASELINE cfg4), sm_100a tcgen05, CTA pairs.
 //
-// The exponent of every pair, t_or = z_or - m_o (log2 units), is produced by
-// kind::tf32 MMAs with split-precision compensation and the row / column
-// constants folded into extra K columns:
-//   A row o (output, in TMEM):  [Yh(d), Yl(d), 1, 1, 1, ch, cm, cl, 0..]
-//   B row r (reduced, smem):    [Xh(d), Xl(d), Uh, Um, Ul, 1, 1, 1, 0..]
-// with X = 2L x_r, U_r = (pot_r - |x_r|^2) L + log2 w_r, c_o = -|y_o|^2 L -
-// m_o, every value split into TF32 hi/lo (3 parts for U and c).  Per 8-wide
-// K slice the issuer runs Yh.Xh, Yl.Xh (same B data, two A offsets) and
-// Yh.Xl, so the 3xTF32 product Yh.Xh + Yl.Xh + Yh.Xl + U + c reproduces the
-// fp32 exponent to ~2^-21 while B carries each X value only twice
-// (TF32 alone would miss the 1e-4 eps tolerance).
+// The exponent of every pair, t_or = z_or - m_o (log2 units), comes out of
+// the tensor pipe complete:
+//   2L x.y     by kind::f16 MMAs on fp16 hi/lo splits (3 products, fp32
+//              accumulate): A row o = [Yh, Yl] of 8 y_o, B row r = [Xh, Xl]
+//              of (2L / 8) x_r; per 16-wide K slice of Xh the issuer runs
+//              Yh.Xh and Yl.Xh (same B data), per slice of Xl it runs Yh.Xl.
+//              The power-of-two scale 8 balances the operands so the lo parts
+//              stay clear of the fp16 subnormal range; the dropped Yl.Xl term
+//              is ~2^-22 relative (|error| <~ 2^-22 2L in log2 units).
+//   U_r + c_o  by one kind::tf32 MMA into the same accumulator:
+//              A = [1, 1, 1, ch, cm, cl, 0, 0], B = [Uh, Um, Ul, 1, 1, 1, 0, 0]
+//              (3-way tf32 splits: fp32 range and precision for
+//              U_r = (pot_r - |x_r|^2) L + log2 w_r and c_o = -|y_o|^2 L - m_o).
+// fp16 operands halve the MMA count of the former 3xTF32 split (12 + 1 per
+// 256x128 tile at d = 64 instead of 25) and the B bytes per tile.
 //
 // CTA pairs (cta_group::2, M = 256): a cluster of two CTAs covers 256 output
 // rows; each CTA keeps its 128 A rows in its own TMEM and streams only HALF
 // of every B tile (64 of the 128 reduced rows) into its shared memory -- the
-// leader's MMA reads both halves, so each SM ingests half the B bytes (the
-// single-CTA version was bound by ~28 B/clk/SM of bulk-copy ingestion).
+// leader's MMA reads both halves, so each SM ingests half the B bytes.
 // Warp roles: warp 0 streams this CTA's B halves with 1-D bulk copies; in the
 // leader, warp 1 issues tcgen05.mma.cta_group::2 from one thread into a
 // double-buffered TMEM accumulator (commits multicast to both CTAs); in the
@@ -26,6 +29,8 @@
 // exp2 / sum epilogue on the MUFU pipe while the next tile is multiplied.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "sinkhorn.cuh"
 #include "tcgen05.cuh"
 
@@ -33,16 +38,17 @@ namespace uot {
 
 constexpr int TC_TILE = 128;        // outputs per CTA and reduced rows per B tile
 constexpr int TC_HALF = 64;         // reduced rows per CTA per B tile
-#ifndef UOT_TC_STAGE_K
-#define UOT_TC_STAGE_K 16
-#endif
-constexpr int TC_STAGE_K = UOT_TC_STAGE_K;  // K elements per shared-memory stage
 #ifndef UOT_TC_STAGES
 #define UOT_TC_STAGES 24
 #endif
 constexpr int TC_STAGES = UOT_TC_STAGES;  // B-operand ring depth
-constexpr int TC_THREADS = 192;
-constexpr int TC_STAGE_BYTES = TC_HALF * TC_STAGE_K * 4;  // 4 KiB: one CTA's half stage
+// warps 0 (B producer), 1 (MMA issuer / relay), 2-9 (epilogue: two warps per
+// TMEM lane quarter, each reducing 64 of a tile's 128 columns, so two warps
+// per SM sub-partition keep the MUFU pipe fed)
+constexpr int TC_THREADS = 320;
+constexpr int TC_STAGE_BYTES = 4096;  // one CTA's half of a stage: 32 fp16 K columns
+constexpr int TC_CBYTES = 2048;       // the constants' stage: 8 tf32 K columns
+constexpr float TC_YSCALE = 8.f;      // A = 8 y, B = (2L / 8) x (exact power-of-two scales)
 
 // Output-side point tile staged in shared memory for the A prologue: 128
 // rows of d floats, row stride d + 4 (conflict-free float4 row reads).
@@ -51,37 +57,49 @@ __host__ __device__ __forceinline__ size_t tc_smem_bytes(int d) {
   return (size_t)TC_STAGES * TC_STAGE_BYTES + sizeof(float) * 128 * (size_t)tc_ystride(d);
 }
 
-// K extent of a reduced-side record (B) and of an output-side row (A).
-__host__ __device__ constexpr int tc_kp(int d) {
-  return (2 * d + 6 + TC_STAGE_K - 1) / TC_STAGE_K * TC_STAGE_K;
+// Record of a reduced row: an fp16 section [Xh(dp), Xl(dp), 0..] of KH
+// halves (dp = d rounded up to 16, KH = 2 dp rounded up to 32) and a float
+// section of 12 columns [Uh, Um, Ul, 1, 1, 1, 0, 0, |x|^2 (fp64), 0, 0].
+__host__ __device__ constexpr int tc_dp(int d) { return (d + 15) / 16 * 16; }
+__host__ __device__ constexpr int tc_kh(int d) { return (2 * tc_dp(d) + 31) / 32 * 32; }
+// floats per record (size bookkeeping: KH halves + 12 floats)
+__host__ __device__ constexpr int tc_kp(int d) { return tc_kh(d) / 2 + 12; }
+// TMEM columns of an A row: dp packed fp16 pairs' worth (Yh, Yl) + 8 tf32
+__host__ __device__ constexpr int tc_ka(int d) { return tc_dp(d) + 8; }
+
+// A 128-row tile is two 64-row halves [X section | float section], each in
+// the canonical K-major no-swizzle core-matrix layout (8 rows x 16 bytes per
+// core matrix; LBO = 1024 B between K groups, SBO = 128 B between 8-row
+// groups), so a CTA's half of a tile is one contiguous run of stages.
+__host__ __device__ __forceinline__ long tc_half_floats(int d) { return (long)TC_HALF * tc_kp(d); }
+// fp16 element (rl, k) of a tile, as an index in halves from the tile base
+__device__ __forceinline__ long tc_xidx(int rl, int k, int d) {
+  return (long)(rl >> 6) * 2 * tc_half_floats(d) + (long)(k >> 3) * 512 + ((rl >> 3) & 7) * 64 +
+         (rl & 7) * 8 + (k & 7);
 }
-__host__ __device__ constexpr int tc_ka(int d) { return 2 * d + 8; }
+// float-section element (rl, c), c < 12, as an index in floats from the tile base
+__device__ __forceinline__ long tc_cidx(int rl, int c, int d) {
+  return (long)(rl >> 6) * tc_half_floats(d) + 32L * tc_kh(d) + (c >> 2) * 256 +
+         ((rl >> 3) & 7) * 32 + (rl & 7) * 4 + (c & 3);
+}
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
 
-// Index of element (row rl, column k) inside one 128-row record tile: two
-// 64-row halves, each in the canonical K-major no-swizzle core-matrix layout
-// ([k/4][row/8][row%8][k%4]; LBO = 1024 B between K groups, SBO = 128 B
-// between 8-row groups), so a CTA's half of a stage is one contiguous copy.
-__device__ __forceinline__ long tc_tile_index(int rl, int k, int KP) {
-  return (long)(rl >> 6) * (TC_HALF * KP) + (long)(k >> 2) * (8 * 32) + ((rl >> 3) & 7) * 32 +
-         (rl & 7) * 4 + (k & 3);
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);  // .x (low 16 bits) = a
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// One K-slice (8 columns of B) of a column tile: the MMAs it feeds.  Xh
-// slices meet Yh and Yl, Xl slices meet Yh, the last slice meets the
-// constants (3xTF32 split of 2L x.y + U + c).
-__device__ __forceinline__ void tc_slice_mmas(int kb, int d, uint32_t dcol, uint32_t tbase,
+// The MMAs one 16-wide fp16 K slice of B feeds (kh = its K offset in halves):
+// Xh slices meet Yh and Yl, Xl slices meet Yh.
+__device__ __forceinline__ void tc_slice_mmas(int kh, int dp, uint32_t dcol, uint32_t tbase,
                                               uint64_t bd, uint32_t idesc, bool& first) {
-  if (kb < d) {
-    tc::mma2_tf32_ts(dcol, tbase + kb, bd, idesc, first ? 0u : 1u);
-    tc::mma2_tf32_ts(dcol, tbase + d + kb, bd, idesc, 1u);
+  if (kh < dp) {
+    tc::mma2_f16_ts(dcol, tbase + (kh >> 1), bd, idesc, first ? 0u : 1u);
+    tc::mma2_f16_ts(dcol, tbase + ((dp + kh) >> 1), bd, idesc, 1u);
     first = false;
-  } else if (kb < 2 * d) {
-    tc::mma2_tf32_ts(dcol, tbase + (kb - d), bd, idesc, first ? 0u : 1u);
-    first = false;
-  } else if (kb < 2 * d + 8) {
-    tc::mma2_tf32_ts(dcol, tbase + 2 * d, bd, idesc, first ? 0u : 1u);
+  } else if (kh < 2 * dp) {
+    tc::mma2_f16_ts(dcol, tbase + ((kh - dp) >> 1), bd, idesc, first ? 0u : 1u);
     first = false;
   }
 }
@@ -103,8 +121,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int split = blockIdx.y, S = gridDim.y;
   const int ntiles = (A.nred + TC_TILE - 1) / TC_TILE;
   const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
-  const int nst = DT > 0 ? tc_kp(DT) / TC_STAGE_K : KP / TC_STAGE_K;
   const int d = DT > 0 ? DT : A.g.d;
+  const int dp = tc_dp(d);
+  const int nxs = tc_kh(d) / 32;  // fp16 stages per tile half; then one constants stage
+  const int nst = nxs + 1;
+  (void)KP;
 
   if (warp == 1) tc::tmem_alloc2(&tbase_s, 512);
   if (tid == 0) {
@@ -115,7 +136,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&dfull[i], 1);
-      tc::mbar_init(&dempty[i], 8);  // leader: one arrive per epilogue warp of the pair
+      tc::mbar_init(&dempty[i], 16);  // leader: one arrive per epilogue warp of the pair
     }
     tc::mbar_fence_init();
   }
@@ -129,6 +150,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int lane_base = 32 * (warp & 3);
   const int row = lane_base + lane;
   const int o = blockIdx.x * TC_TILE + row;
+  const int chalf = warp >= 6 ? 1 : 0;  // epilogue: columns [64 chalf, 64 chalf + 64)
+  __shared__ float half_m[TC_TILE], half_a[TC_TILE];
   float m_o = 0.f;
   // Prologue: the CTA's 128 output points -> shared memory (all threads,
   // coalesced float4 loads), then each epilogue thread builds its A row
@@ -147,7 +170,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     }
   }
   __syncthreads();
-  if (warp >= 2) {
+  if (warp >= 6) m_o = o < A.nout ? A.shift_in[(long)b * A.nout + o] : 0.f;
+  if (warp >= 2 && warp < 6) {
     const float* y = ys + row * YS;
     double s2 = 0.0;
     if (o < A.nout) {
@@ -166,33 +190,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const float cm = tf32_hi((float)c1);
     const float cl = (float)(c1 - (double)cm);
     const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
-    // Yh at columns [0, d), Yl at [d, 2d): 8 columns per store
-    for (int k0 = 0; k0 < d; k0 += 8) {
-      float yv[8];
-      if (o < A.nout) {
-        const float4 u0 = *reinterpret_cast<const float4*>(y + k0);
-        const float4 u1 = *reinterpret_cast<const float4*>(y + k0 + 4);
-        yv[0] = u0.x, yv[1] = u0.y, yv[2] = u0.z, yv[3] = u0.w;
-        yv[4] = u1.x, yv[5] = u1.y, yv[6] = u1.z, yv[7] = u1.w;
-      } else {
+    // fp16 splits of 8 y: Yh at columns [0, dp/2), Yl at [dp/2, dp) (two
+    // halves per column, the even K index in the low half); 16 K per store
+    for (int k0 = 0; k0 < dp; k0 += 16) {
+      float yv[16];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) yv[e] = 0.f;
+      for (int e = 0; e < 16; e += 4) {
+        if (o < A.nout && k0 + e < d) {
+          const float4 u = *reinterpret_cast<const float4*>(y + k0 + e);
+          yv[e] = u.x, yv[e + 1] = u.y, yv[e + 2] = u.z, yv[e + 3] = u.w;
+        } else {
+          yv[e] = yv[e + 1] = yv[e + 2] = yv[e + 3] = 0.f;
+        }
       }
       uint32_t vh[8], vl[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float yh = tf32_hi(yv[e]);
-        vh[e] = __float_as_uint(yh);
-        vl[e] = __float_as_uint(yv[e] - yh);
+      for (int c = 0; c < 8; ++c) {
+        const float a0 = TC_YSCALE * yv[2 * c], a1 = TC_YSCALE * yv[2 * c + 1];
+        const float h0 = __half2float(__float2half_rn(a0)), h1 = __half2float(__float2half_rn(a1));
+        vh[c] = pack_h2(h0, h1);
+        vl[c] = pack_h2(a0 - h0, a1 - h1);
       }
-      tc::tmem_st8(ta + k0, vh);
-      tc::tmem_st8(ta + d + k0, vl);
+      tc::tmem_st8(ta + (k0 >> 1), vh);
+      tc::tmem_st8(ta + ((dp + k0) >> 1), vl);
     }
     {
       const uint32_t vt[8] = {__float_as_uint(1.f), __float_as_uint(1.f), __float_as_uint(1.f),
                               __float_as_uint(ch),  __float_as_uint(cm),  __float_as_uint(cl),
                               0u,                   0u};
-      tc::tmem_st8(ta + 2 * d, vt);
+      tc::tmem_st8(ta + dp, vt);
     }
     tc::wait_st();
   }
@@ -206,13 +232,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     if (tc::elect_one()) {  // producer: this CTA's halves of the B stages
       int slot = 0;
       uint32_t phase = 0;
+      const long hf = tc_half_floats(d);
       for (int tile = t0; tile < t1; ++tile) {
-        const float* src = recb + (long)tile * TC_TILE * KP + (long)rank * TC_HALF * KP;
+        const float* src = recb + (long)tile * 2 * hf + (long)rank * hf;
         for (int st = 0; st < nst; ++st) {
+          const uint32_t bytes = st < nxs ? TC_STAGE_BYTES : TC_CBYTES;
           tc::mbar_wait(&empty_b[slot], phase ^ 1);
-          tc::mbar_expect_tx(&full_b[slot], TC_STAGE_BYTES);
-          tc::bulk_g2s(smem + slot * TC_STAGE_BYTES, src + (long)st * TC_HALF * TC_STAGE_K,
-                       TC_STAGE_BYTES, &full_b[slot]);
+          tc::mbar_expect_tx(&full_b[slot], bytes);
+          tc::bulk_g2s(smem + slot * TC_STAGE_BYTES, src + (long)st * (TC_STAGE_BYTES / 4), bytes,
+                       &full_b[slot]);
           if (++slot == TC_STAGES) {
             slot = 0;
             phase ^= 1;
@@ -236,11 +264,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
           }
         }
       } else {  // MMA issuer for the pair
-        const uint32_t idesc = tc::idesc_tf32(2 * TC_TILE, TC_TILE);
+        const uint32_t idesc = tc::idesc_f16(2 * TC_TILE, TC_TILE);
+        const uint32_t idesc32 = tc::idesc_tf32(2 * TC_TILE, TC_TILE);
         int slot = 0;
         uint32_t phase = 0;
         // descriptor of slot 0; other slots / slices add byte offset >> 4
         const uint64_t bd0 = tc::sdesc(smem, (TC_HALF / 8) * 128, 128);
+        constexpr int NXS = DT > 0 ? tc_kh(DT) / 32 : 1;
         for (int i = 0; i < t1 - t0; ++i) {
           const int buf = i & 1;
           const uint32_t dph = (i >> 1) & 1;
@@ -248,26 +278,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
           tc::fence_after();
           const uint32_t dcol = tbase + 256 + buf * TC_TILE;
           bool first = true;
-          constexpr int NST = DT > 0 ? tc_kp(DT) / TC_STAGE_K : 1;
 #pragma unroll
-          for (int stu = 0; stu < (DT > 0 ? NST : 1); ++stu) {
-            for (int str = 0; str < (DT > 0 ? 1 : nst); ++str) {
+          for (int stu = 0; stu < (DT > 0 ? NXS : 1); ++stu) {
+            for (int str = 0; str < (DT > 0 ? 1 : nxs); ++str) {
               const int st = DT > 0 ? stu : str;
               tc::mbar_wait(&full_b[slot], phase);
               tc::mbar_wait(&peer_b[slot], phase);
               tc::fence_after();
               const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
 #pragma unroll
-              for (int ks = 0; ks < TC_STAGE_K / 8; ++ks) {
-                const int kb = st * TC_STAGE_K + ks * 8;  // K offset of this slice in B
-                tc_slice_mmas(kb, d, dcol, tbase,
-                              bds + (uint64_t)((ks * 2 * (TC_HALF / 8) * 128) >> 4), idesc, first);
-              }
+              for (int ks = 0; ks < 2; ++ks)  // two 16-wide K slices (2 KB each) per stage
+                tc_slice_mmas(st * 32 + ks * 16, dp, dcol, tbase,
+                              bds + (uint64_t)((ks * 2048) >> 4), idesc, first);
               tc::mma2_commit_mc(&empty_b[slot], 3);
               if (++slot == TC_STAGES) {
                 slot = 0;
                 phase ^= 1;
               }
+            }
+          }
+          {  // the constants: U_r + c_o by one tf32 MMA into the same accumulator
+            tc::mbar_wait(&full_b[slot], phase);
+            tc::mbar_wait(&peer_b[slot], phase);
+            tc::fence_after();
+            const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
+            tc::mma2_tf32_ts(dcol, tbase + dp, bds, idesc32, first ? 0u : 1u);
+            tc::mma2_commit_mc(&empty_b[slot], 3);
+            if (++slot == TC_STAGES) {
+              slot = 0;
+              phase ^= 1;
             }
           }
           tc::mma2_commit_mc(&dfull[buf], 3);
@@ -286,12 +325,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       const uint32_t dph = (i >> 1) & 1;
       tc::mbar_wait(&dfull[buf], dph);
       tc::fence_after();
-      const uint32_t dcol = tl + 256 + buf * TC_TILE;
-      uint32_t v0[32], v1[32], v2[32], v3[32];
+      const uint32_t dcol = tl + 256 + buf * TC_TILE + 64 * chalf;
+      uint32_t v0[32], v1[32];
       tc::tmem_ld32(dcol, v0);
       tc::tmem_ld32(dcol + 32, v1);
-      tc::tmem_ld32(dcol + 64, v2);
-      tc::tmem_ld32(dcol + 96, v3);
       tc::wait_ld();
       // The accumulator is in registers (wait::ld completed): hand the buffer
       // back to the MMA issuer.  No TMEM read is outstanding, so a relaxed
@@ -305,19 +342,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
         float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
         if (__all_sync(0xffffffffu, corr == 0.f)) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
+          for (int e = 0; e < 16; ++e) {
             sa += Dom<float>::ex(__uint_as_float(v0[e]));
-            sb += Dom<float>::ex(__uint_as_float(v1[e]));
-            sc += Dom<float>::ex(__uint_as_float(v2[e]));
-            sd += Dom<float>::ex(__uint_as_float(v3[e]));
+            sb += Dom<float>::ex(__uint_as_float(v0[e + 16]));
+            sc += Dom<float>::ex(__uint_as_float(v1[e]));
+            sd += Dom<float>::ex(__uint_as_float(v1[e + 16]));
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
+          for (int e = 0; e < 16; ++e) {
             sa += Dom<float>::ex(__uint_as_float(v0[e]) + corr);
-            sb += Dom<float>::ex(__uint_as_float(v1[e]) + corr);
-            sc += Dom<float>::ex(__uint_as_float(v2[e]) + corr);
-            sd += Dom<float>::ex(__uint_as_float(v3[e]) + corr);
+            sb += Dom<float>::ex(__uint_as_float(v0[e + 16]) + corr);
+            sc += Dom<float>::ex(__uint_as_float(v1[e]) + corr);
+            sd += Dom<float>::ex(__uint_as_float(v1[e + 16]) + corr);
           }
         }
         s = (sa + sb) + (sc + sd);
@@ -330,8 +367,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
         for (int e = 0; e < 32; ++e) {
           mx = fmaxf(mx, __uint_as_float(v0[e]) + corr);
           mx = fmaxf(mx, __uint_as_float(v1[e]) + corr);
-          mx = fmaxf(mx, __uint_as_float(v2[e]) + corr);
-          mx = fmaxf(mx, __uint_as_float(v3[e]) + corr);
         }
         float mn = mx;
         if (acc > 0.f) mn = fmaxf(mn, Dom<float>::lg(acc));
@@ -344,17 +379,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
         for (int e = 0; e < 32; ++e) {
           s += Dom<float>::ex(__uint_as_float(v0[e]) + corr);
           s += Dom<float>::ex(__uint_as_float(v1[e]) + corr);
-          s += Dom<float>::ex(__uint_as_float(v2[e]) + corr);
-          s += Dom<float>::ex(__uint_as_float(v3[e]) + corr);
         }
         na = acc + s;
       }
       acc = na;
     }
-    if (o < A.nout) {
+    // merge the two column halves of each row: (shift, sum) pairs in log2 units
+    if (chalf) {
+      half_m[row] = m_o - corr;
+      half_a[row] = acc;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight epilogue warps
+    if (!chalf && o < A.nout) {
+      float pm = m_o - corr, pa = acc;
+      const float qm = half_m[row], qa = half_a[row];
+      if (qa > 0.f) {
+        if (!(pa > 0.f)) {
+          pm = qm;
+          pa = qa;
+        } else if (qm > pm) {
+          pa = pa * Dom<float>::ex(pm - qm) + qa;
+          pm = qm;
+        } else {
+          pa += qa * Dom<float>::ex(qm - pm);
+        }
+      }
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
-      A.part_m[idx] = m_o - corr;
-      A.part_a[idx] = acc;
+      A.part_m[idx] = pm;
+      A.part_a[idx] = pa;
     }
   }
   tc::fence_before();
@@ -362,21 +414,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   if (warp == 1) tc::tmem_free2(tbase, 512);
 }
 
-// Dead-row fill of a canonical record buffer: every row gets U = -1e30
-// (exp2 -> 0) and the unit columns, so padded rows of the last tile never
-// contribute; live rows are overwritten by the tails.
-__global__ void tc_fill_dead(float* buf, long nrows_padded, int d, int KP) {
-  const long total = nrows_padded * KP;
+// Dead-row fill of a record buffer: X = 0 and U = -1e30 (exp2 -> 0) with
+// the unit columns, so padded rows of the last tile never contribute; live
+// rows are overwritten by tc_init_static and the tails.
+__global__ void tc_fill_dead(float* buf, long nrows_padded, int d, int) {
+  const long hf = tc_half_floats(d);
+  const long total = nrows_padded / TC_TILE * 2 * hf;  // floats
+  const long xf = 32L * tc_kh(d);                       // floats of a half's X section
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
-    const long tile = idx / ((long)TC_TILE * KP);
-    const long rem = idx % ((long)TC_TILE * KP);
-    const long r2 = rem % ((long)TC_HALF * KP);  // within a 64-row half
-    const int k = (int)(r2 / (8 * 32)) * 4 + (int)(r2 % 4);
+    const long r = idx % hf;  // within a 64-row half
     float v = 0.f;
-    if (k == 2 * d) v = -1e30f;
-    else if (k >= 2 * d + 3 && k < 2 * d + 6) v = 1.f;
-    buf[tile * TC_TILE * KP + rem] = v;
+    if (r >= xf) {
+      const long cc = r - xf;
+      const int c = (int)(cc / 256) * 4 + (int)(cc % 4);
+      if (c == 0) v = -1e30f;
+      else if (c >= 3 && c < 6) v = 1.f;
+    }
+    buf[idx] = v;
   }
 }
 

@@ -138,6 +138,17 @@ __device__ __forceinline__ void mma2_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem, both CTAs] (+)= A[tmem, both CTAs] * B[smem]^T, kind::f16 (fp16
+// inputs, fp32 accumulate); A in TMEM holds two fp16 per 32-bit column.
+__device__ __forceinline__ void mma2_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive on `bar` (same offset) in every CTA of `mask` when the pair's MMAs finish
 __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -182,6 +193,14 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4)                      // D = F32
          | (2u << 7)                    // A = TF32
          | (2u << 10)                   // B = TF32
+         | ((uint32_t)(N >> 3) << 17)   // N
+         | ((uint32_t)(M >> 4) << 24);  // M
+}
+
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4)                      // D = F32
+         | (0u << 7)                    // A = F16
+         | (0u << 10)                   // B = F16
          | ((uint32_t)(N >> 3) << 17)   // N
          | ((uint32_t)(M >> 4) << 24);  // M
 }
