@@ -1170,7 +1170,7 @@ struct Cfg<SqE64> {
 };
 template <>
 struct Cfg<SqE32TC> {
-  static constexpr int THREADS = 128, COLS = 1, RT = 1;  // 128 outputs per CTA (one MMA tile)
+  static constexpr int THREADS = 128, COLS = 2, RT = 1;  // 256 outputs per CTA (two MMA blocks)
 };
 template <typename TT>
 struct Cfg<Explicit<TT>> {
@@ -1848,7 +1848,7 @@ int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
         if (d.d == 1) return fn(Engine<SqE32<1>>());
         if (d.d == 2) return fn(Engine<SqE32<2>>());
         if (d.d == 3) return fn(Engine<SqE32<3>>());
-        if (d.d >= 32 && d.d % 4 == 0 && tc_ka(d.d) <= 256 && d.nranks <= 1 &&
+        if (d.d >= 32 && d.d % 4 == 0 && 2 * tc_ka(d.d) <= 256 && d.nranks <= 1 &&
             d.nccl_comm == nullptr)
           return fn(Engine<SqE32TC>());
         return fn(Engine<SqE32N>());

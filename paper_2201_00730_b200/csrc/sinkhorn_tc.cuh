@@ -42,19 +42,20 @@ constexpr int TC_HALF = 64;         // reduced rows per CTA per B tile
 #define UOT_TC_STAGES 24
 #endif
 constexpr int TC_STAGES = UOT_TC_STAGES;  // B-operand ring depth
-// warps 0 (B producer), 1 (MMA issuer / relay), 2-9 (epilogue: two warps per
-// TMEM lane quarter, each reducing 64 of a tile's 128 columns, so two warps
-// per SM sub-partition keep the MUFU pipe fed)
+// warps 0 (B producer), 1 (MMA issuer / relay), 2-5 and 6-9 (epilogue of
+// output blocks 0 and 1: two warps per SM sub-partition keep the MUFU fed)
 constexpr int TC_THREADS = 320;
+constexpr int TC_NB = 2;  // output blocks of 128 rows per CTA
 constexpr int TC_STAGE_BYTES = 4096;  // one CTA's half of a stage: 32 fp16 K columns
 constexpr int TC_CBYTES = 2048;       // the constants' stage: 8 tf32 K columns
 constexpr float TC_YSCALE = 8.f;      // A = 8 y, B = (2L / 8) x (exact power-of-two scales)
 
-// Output-side point tile staged in shared memory for the A prologue: 128
-// rows of d floats, row stride d + 4 (conflict-free float4 row reads).
+// Output-side points staged in shared memory for the A prologue: 256 rows
+// of d floats, row stride d + 4 (conflict-free float4 row reads).
 __host__ __device__ __forceinline__ int tc_ystride(int d) { return d + 4; }
 __host__ __device__ __forceinline__ size_t tc_smem_bytes(int d) {
-  return (size_t)TC_STAGES * TC_STAGE_BYTES + sizeof(float) * 128 * (size_t)tc_ystride(d);
+  return (size_t)TC_STAGES * TC_STAGE_BYTES +
+         sizeof(float) * TC_NB * 128 * (size_t)tc_ystride(d);
 }
 
 // Record of a reduced row: an fp16 section [Xh(dp), Xl(dp), 0..] of KH
@@ -107,11 +108,15 @@ __device__ __forceinline__ void tc_slice_mmas(int kh, int dp, uint32_t dcol, uin
 // DT > 0: the feature dimension is a compile-time constant, so the MMA issue
 // sequence of a column tile is fully unrolled and branch-free (a tight
 // tcgen05.mma stream runs at its floor; a generic loop issue-bound).
-// DT = 0: runtime d.  Launched with cluster dims (2, 1, 1) over row tiles.
+// DT = 0: runtime d.  Launched with cluster dims (2, 1, 1); CTA c owns the
+// output blocks 2c and 2c + 1 (128 rows each, A_0 / A_1 in its TMEM), so
+// every B tile that lands feeds both blocks' MMAs (the pair's M = 256 rows
+// of block j are CTA 2p's and CTA 2p+1's block j).
 template <int DT>
 __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, int KP) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], peer_b[TC_STAGES], dfull[2], dempty[2];
+  __shared__ uint64_t full_b[TC_STAGES], empty_b[TC_STAGES], peer_b[TC_STAGES], dfull[TC_NB],
+      dempty[TC_NB];
   __shared__ uint32_t tbase_s;
   const int b = blockIdx.z;
   if (A.done != nullptr && A.done[b]) return;  // uniform over the pair (same b)
@@ -123,6 +128,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
   const int d = DT > 0 ? DT : A.g.d;
   const int dp = tc_dp(d);
+  const int ka = tc_ka(d);        // TMEM columns of one A block
   const int nxs = tc_kh(d) / 32;  // fp16 stages per tile half; then one constants stage
   const int nst = nxs + 1;
   (void)KP;
@@ -134,9 +140,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       tc::mbar_init(&empty_b[i], 1);  // one multicast commit per use
       tc::mbar_init(&peer_b[i], 1);   // leader: the peer's half landed
     }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&dfull[i], 1);
-      tc::mbar_init(&dempty[i], 16);  // leader: one arrive per epilogue warp of the pair
+    for (int j = 0; j < TC_NB; ++j) {
+      tc::mbar_init(&dfull[j], 1);
+      tc::mbar_init(&dempty[j], 8);  // leader: one arrive per epilogue warp of the block, both CTAs
     }
     tc::mbar_fence_init();
   }
@@ -145,22 +151,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   tc::fence_after();
   const uint32_t tbase = tbase_s;
 
-  // Epilogue threads own one output row each (TMEM lane restriction: warp w
-  // reaches lanes 32*(w%4) .. +31).
+  // Epilogue threads own one output row of one block each (TMEM lane
+  // restriction: warp w reaches lanes 32*(w%4) .. +31).
+  const int blk = warp >= 2 ? (warp - 2) >> 2 : 0;
   const int lane_base = 32 * (warp & 3);
   const int row = lane_base + lane;
-  const int o = blockIdx.x * TC_TILE + row;
-  const int chalf = warp >= 6 ? 1 : 0;  // epilogue: columns [64 chalf, 64 chalf + 64)
-  __shared__ float half_m[TC_TILE], half_a[TC_TILE];
+  const int row0 = blockIdx.x * (TC_NB * TC_TILE);
+  const int o = row0 + blk * TC_TILE + row;
   float m_o = 0.f;
-  // Prologue: the CTA's 128 output points -> shared memory (all threads,
+  // Prologue: the CTA's 256 output points -> shared memory (all threads,
   // coalesced float4 loads), then each epilogue thread builds its A row
-  // [Yh, Yl, 1, 1, 1, ch, cm, cl] (tf32 splits) and stores it into TMEM.
+  // (fp16 splits of 8 y + the tf32 constants) in its block's TMEM columns.
   float* ys = reinterpret_cast<float*>(smem + (size_t)TC_STAGES * TC_STAGE_BYTES);
   const int YS = tc_ystride(d);
   {
-    const int row0 = blockIdx.x * TC_TILE;
-    const int nrows = min(TC_TILE, A.nout - row0);
+    const int nrows = max(0, min(TC_NB * TC_TILE, A.nout - row0));
     const float4* src =
         reinterpret_cast<const float4*>(A.g.out_pts + b * A.g.out_pts_bstride + (long)row0 * d);
     const int q4 = d / 4;
@@ -170,9 +175,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     }
   }
   __syncthreads();
-  if (warp >= 6) m_o = o < A.nout ? A.shift_in[(long)b * A.nout + o] : 0.f;
-  if (warp >= 2 && warp < 6) {
-    const float* y = ys + row * YS;
+  if (warp >= 2) {
+    const float* y = ys + (blk * TC_TILE + row) * YS;
     double s2 = 0.0;
     if (o < A.nout) {
       for (int k = 0; k < d; k += 4) {
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const double c1 = c - (double)ch;
     const float cm = tf32_hi((float)c1);
     const float cl = (float)(c1 - (double)cm);
-    const uint32_t ta = tbase + ((uint32_t)lane_base << 16);
+    const uint32_t ta = tbase + ((uint32_t)lane_base << 16) + blk * ka;
     // fp16 splits of 8 y: Yh at columns [0, dp/2), Yl at [dp/2, dp) (two
     // halves per column, the even K index in the low half); 16 K per store
     for (int k0 = 0; k0 < dp; k0 += 16) {
@@ -205,11 +209,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       }
       uint32_t vh[8], vl[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float a0 = TC_YSCALE * yv[2 * c], a1 = TC_YSCALE * yv[2 * c + 1];
+      for (int cc = 0; cc < 8; ++cc) {
+        const float a0 = TC_YSCALE * yv[2 * cc], a1 = TC_YSCALE * yv[2 * cc + 1];
         const float h0 = __half2float(__float2half_rn(a0)), h1 = __half2float(__float2half_rn(a1));
-        vh[c] = pack_h2(h0, h1);
-        vl[c] = pack_h2(a0 - h0, a1 - h1);
+        vh[cc] = pack_h2(h0, h1);
+        vl[cc] = pack_h2(a0 - h0, a1 - h1);
       }
       tc::tmem_st8(ta + (k0 >> 1), vh);
       tc::tmem_st8(ta + ((dp + k0) >> 1), vl);
@@ -266,77 +270,75 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       } else {  // MMA issuer for the pair
         const uint32_t idesc = tc::idesc_f16(2 * TC_TILE, TC_TILE);
         const uint32_t idesc32 = tc::idesc_tf32(2 * TC_TILE, TC_TILE);
-        int slot = 0;
-        uint32_t phase = 0;
         // descriptor of slot 0; other slots / slices add byte offset >> 4
         const uint64_t bd0 = tc::sdesc(smem, (TC_HALF / 8) * 128, 128);
         constexpr int NXS = DT > 0 ? tc_kh(DT) / 32 : 1;
+        int slot0 = 0;
+        uint32_t phase0 = 0;
         for (int i = 0; i < t1 - t0; ++i) {
-          const int buf = i & 1;
-          const uint32_t dph = (i >> 1) & 1;
-          tc::mbar_wait(&dempty[buf], dph ^ 1);
-          tc::fence_after();
-          const uint32_t dcol = tbase + 256 + buf * TC_TILE;
-          bool first = true;
+          const uint32_t ph = i & 1;
+#pragma unroll 1
+          for (int j = 0; j < TC_NB; ++j) {  // block 0, then block 1 on the same stages
+            tc::mbar_wait(&dempty[j], ph ^ 1);
+            tc::fence_after();
+            const uint32_t dcol = tbase + 256 + j * TC_TILE;
+            const uint32_t abase = tbase + j * ka;
+            bool first = true;
+            int slot = slot0;
+            uint32_t phase = phase0;
 #pragma unroll
-          for (int stu = 0; stu < (DT > 0 ? NXS : 1); ++stu) {
-            for (int str = 0; str < (DT > 0 ? 1 : nxs); ++str) {
-              const int st = DT > 0 ? stu : str;
-              tc::mbar_wait(&full_b[slot], phase);
-              tc::mbar_wait(&peer_b[slot], phase);
-              tc::fence_after();
+            for (int stu = 0; stu < (DT > 0 ? NXS : 1); ++stu) {
+              for (int str = 0; str < (DT > 0 ? 1 : nxs); ++str) {
+                const int st = DT > 0 ? stu : str;
+                if (j == 0) {
+                  tc::mbar_wait(&full_b[slot], phase);
+                  tc::mbar_wait(&peer_b[slot], phase);
+                  tc::fence_after();
+                }
+                const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks)  // two 16-wide K slices (2 KB each) per stage
+                  tc_slice_mmas(st * 32 + ks * 16, dp, dcol, abase,
+                                bds + (uint64_t)((ks * 2048) >> 4), idesc, first);
+                if (j == TC_NB - 1) tc::mma2_commit_mc(&empty_b[slot], 3);
+                if (++slot == TC_STAGES) {
+                  slot = 0;
+                  phase ^= 1;
+                }
+              }
+            }
+            {  // the constants: U_r + c_o by one tf32 MMA into the same accumulator
+              if (j == 0) {
+                tc::mbar_wait(&full_b[slot], phase);
+                tc::mbar_wait(&peer_b[slot], phase);
+                tc::fence_after();
+              }
               const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
-#pragma unroll
-              for (int ks = 0; ks < 2; ++ks)  // two 16-wide K slices (2 KB each) per stage
-                tc_slice_mmas(st * 32 + ks * 16, dp, dcol, tbase,
-                              bds + (uint64_t)((ks * 2048) >> 4), idesc, first);
-              tc::mma2_commit_mc(&empty_b[slot], 3);
+              tc::mma2_tf32_ts(dcol, abase + dp, bds, idesc32, first ? 0u : 1u);
+              if (j == TC_NB - 1) tc::mma2_commit_mc(&empty_b[slot], 3);
               if (++slot == TC_STAGES) {
                 slot = 0;
                 phase ^= 1;
               }
             }
-          }
-          {  // the constants: U_r + c_o by one tf32 MMA into the same accumulator
-            tc::mbar_wait(&full_b[slot], phase);
-            tc::mbar_wait(&peer_b[slot], phase);
-            tc::fence_after();
-            const uint64_t bds = bd0 + (uint64_t)((slot * TC_STAGE_BYTES) >> 4);
-            tc::mma2_tf32_ts(dcol, tbase + dp, bds, idesc32, first ? 0u : 1u);
-            tc::mma2_commit_mc(&empty_b[slot], 3);
-            if (++slot == TC_STAGES) {
-              slot = 0;
-              phase ^= 1;
+            tc::mma2_commit_mc(&dfull[j], 3);
+            if (j == TC_NB - 1) {
+              slot0 = slot;
+              phase0 = phase;
             }
           }
-          tc::mma2_commit_mc(&dfull[buf], 3);
         }
       }
     }
     __syncwarp();
   } else {
-    // Epilogue: exp2 + sum of each accumulator row, range-checked per tile.
+    // Epilogue: exp2 + sum of each accumulator row in two 64-column chunks,
+    // range-checked per chunk; the block's accumulator is handed back as soon
+    // as its second chunk is in registers.
     float acc = 0.f, corr = 0.f;
-    const uint32_t tl = tbase + ((uint32_t)lane_base << 16);
-    const uint32_t dempty_leader0 = tc::mapa(&dempty[0], 0);
-    const uint32_t dempty_leader1 = tc::mapa(&dempty[1], 0);
-    for (int i = 0; i < t1 - t0; ++i) {
-      const int buf = i & 1;
-      const uint32_t dph = (i >> 1) & 1;
-      tc::mbar_wait(&dfull[buf], dph);
-      tc::fence_after();
-      const uint32_t dcol = tl + 256 + buf * TC_TILE + 64 * chalf;
-      uint32_t v0[32], v1[32];
-      tc::tmem_ld32(dcol, v0);
-      tc::tmem_ld32(dcol + 32, v1);
-      tc::wait_ld();
-      // The accumulator is in registers (wait::ld completed): hand the buffer
-      // back to the MMA issuer.  No TMEM read is outstanding, so a relaxed
-      // arrive suffices (a release.cluster arrive per warp and tile costs
-      // ~1.5x the kernel time).
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive_remote_relaxed(buf ? dempty_leader1 : dempty_leader0);
+    const uint32_t tl = tbase + ((uint32_t)lane_base << 16) + 256 + blk * TC_TILE;
+    const uint32_t dempty_leader = tc::mapa(&dempty[blk], 0);
+    auto chunk = [&](const uint32_t (&v0)[32], const uint32_t (&v1)[32]) {
       float s;
       {
         float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       }
       float na = acc + s;
       if (!(na < 1.2676506e30f && na > 7.8886091e-31f)) {
-        // Rare: the stale shift is off by > 2^100 -- rescale from this tile's max.
+        // Rare: the stale shift is off by > 2^100 -- rescale from this chunk's max.
         float mx = -INFINITY;
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -383,30 +385,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
         na = acc + s;
       }
       acc = na;
+    };
+    for (int i = 0; i < t1 - t0; ++i) {
+      tc::mbar_wait(&dfull[blk], i & 1);
+      tc::fence_after();
+      uint32_t v0[32], v1[32];
+      tc::tmem_ld32(tl, v0);
+      tc::tmem_ld32(tl + 32, v1);
+      tc::wait_ld();
+      chunk(v0, v1);
+      tc::tmem_ld32(tl + 64, v0);
+      tc::tmem_ld32(tl + 96, v1);
+      tc::wait_ld();
+      // No TMEM read is outstanding, so a relaxed arrive suffices (a
+      // release.cluster arrive per warp and tile costs ~1.5x the kernel time).
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_remote_relaxed(dempty_leader);
+      chunk(v0, v1);
     }
-    // merge the two column halves of each row: (shift, sum) pairs in log2 units
-    if (chalf) {
-      half_m[row] = m_o - corr;
-      half_a[row] = acc;
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight epilogue warps
-    if (!chalf && o < A.nout) {
-      float pm = m_o - corr, pa = acc;
-      const float qm = half_m[row], qa = half_a[row];
-      if (qa > 0.f) {
-        if (!(pa > 0.f)) {
-          pm = qm;
-          pa = qa;
-        } else if (qm > pm) {
-          pa = pa * Dom<float>::ex(pm - qm) + qa;
-          pm = qm;
-        } else {
-          pa += qa * Dom<float>::ex(qm - pm);
-        }
-      }
+    if (o < A.nout) {
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
-      A.part_m[idx] = pm;
-      A.part_a[idx] = pa;
+      A.part_m[idx] = m_o - corr;
+      A.part_a[idx] = acc;
     }
   }
   tc::fence_before();
