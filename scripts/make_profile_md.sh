@@ -19,7 +19,9 @@ cp gpurun_out/prof_cfg3_launches.csv profiles/${R}_cfg3_launches.csv
 { echo "# Round 1 — cfg5 barycenter FW (64 problems x K=16 x N=8192, fp64, 3 iterations): \`python scripts/prof_bary.py 64 3\`"; echo;
   echo "## Launch list (cold-cache, serialised — compare shares)"; echo; python $S launches gpurun_out/prof_bary_launches.csv;
   for k in mot_update mot_bucket mot_split; do echo; echo "## Full capture: $k"; echo; python $S full gpurun_out/prof_bary_$k.ncu-rep; done; } > profiles/${R}_cfg5_barycenter.md
-{ echo "# Round 1 — cfg4 batched Sinkhorn d=64 on tcgen05 CTA pairs (64 of 256 problems, N=M=4096, fp32 3xTF32): \`python scripts/perf_cfg4.py 64\`"; echo;
+{ echo "# Round 1 — cfg4 batched Sinkhorn d=64 on tcgen05 CTA pairs: fp16 hi/lo split MMAs + one tf32 constants MMA, two output blocks per CTA (64 of 256 problems, N=M=4096): \`python scripts/perf_cfg4.py 64\`"; echo;
   echo "## Launch list (cold-cache, serialised — compare shares)"; echo; python $S launches gpurun_out/prof_c4_launches.csv; echo;
-  echo "## Full capture of sk_main_tc<64>"; echo; python $S full gpurun_out/prof_c4_full.ncu-rep; } > profiles/${R}_cfg4_tcgen05.md
+  echo "## Full capture of sk_main_tc<64>"; echo; python $S full gpurun_out/prof_c4_full.ncu-rep; echo;
+  echo "Reading: MUFU (XU) and tensor pipe shares above; steady state is MUFU-bound, the rest is the per-CTA prologue (256 output points, A rows into TMEM) and pipeline fill/drain. Round-1 start (3xTF32, one block per CTA, 4 epilogue warps): 557 us per launch, tensor 80%, MUFU 52%."; } > profiles/${R}_cfg4_tcgen05.md
+cp gpurun_out/prof_c4_launches.csv profiles/${R}_cfg4_launches.csv
 echo done
