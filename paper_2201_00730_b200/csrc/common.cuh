@@ -162,6 +162,17 @@ struct SumOp {
   __device__ T operator()(T a, T b) const { return a + b; }
 };
 
+// Block log-sum-exp of (m, s) pairs as max then rescaled sum: one exp per
+// thread and two plain reductions (block_lse merges pairwise, one exp per
+// butterfly step).  Pairs with s <= 0 are empty; an empty block gives
+// (-inf, 0).  `sx` needs 32 doubles.
+__device__ __forceinline__ LsePair block_lse_ms(LsePair p, double* sx) {
+  const bool live = p.s > 0.0;
+  const double m = block_reduce(live ? p.m : -CUDART_INF, sx, MaxOp(), -CUDART_INF);
+  const double s = block_reduce(live ? p.s * exp(p.m - m) : 0.0, sx, SumOp(), 0.0);
+  return LsePair{m, s};
+}
+
 // "Last block done" pattern: every block publishes its partial then calls
 // this; exactly one block (the last to arrive) gets true and must reset the
 // counter.  Requires a __threadfence() by the publishing thread first.

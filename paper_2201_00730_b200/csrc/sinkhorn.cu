@@ -826,18 +826,25 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     if (A.mode == 1) {
       hat = (double)A.pot_in[(long)b * A.nout + o];
     } else {
-      double M = -CUDART_INF;
+      // fold the split partials (shift, sum): max, then the rescaled sum
+      // (loads unrolled for memory-level parallelism; fp32 partials combine
+      // with the fast exp2 -- they carry fp32 precision anyway)
+      T M = (T)(-CUDART_INF);
       const long pbase = (long)b * A.pstride_b + o;
+#pragma unroll 4
       for (int s = 0; s < A.nparts; ++s) {
-        const double a = (double)A.part_a[pbase + (long)s * A.pstride_s];
-        if (a > 0.0) M = fmax(M, (double)A.part_m[pbase + (long)s * A.pstride_s]);
+        const T a = A.part_a[pbase + (long)s * A.pstride_s];
+        const T mm = A.part_m[pbase + (long)s * A.pstride_s];
+        if (a > (T)0) M = mm > M ? mm : M;
       }
-      double acc = 0.0;
+      T acc = 0;
+#pragma unroll 4
       for (int s = 0; s < A.nparts; ++s) {
-        const double a = (double)A.part_a[pbase + (long)s * A.pstride_s];
-        if (a > 0.0) acc += a * D::exd((double)A.part_m[pbase + (long)s * A.pstride_s] - M);
+        const T a = A.part_a[pbase + (long)s * A.pstride_s];
+        const T mm = A.part_m[pbase + (long)s * A.pstride_s];
+        if (a > (T)0) acc += a * D::ex(mm - M);
       }
-      const double lse = M + D::lgd(acc);  // domain units, excluding tau_red
+      const double lse = (double)M + D::lgd((double)acc);  // domain units, excluding tau_red
       A.shift_out[(long)b * A.nout + o] = (T)lse;
       const double smin = -A.eps * A.unit * (lse + tau_red * A.inv_eu);
       if (A.gmode) {
@@ -867,7 +874,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     }
   }
   // Block partials: log-sum-exp of -hat/rho weighted by w, and delta bounds.
-  pr = block_lse(pr, s_m, s_s);
+  pr = block_lse_ms(pr, s_x);
   dmax = block_reduce(dmax, s_x, MaxOp(), -CUDART_INF);
   dmin = block_reduce(dmin, s_x, MinOp(), CUDART_INF);
   double* blk = A.blk + (long)b * gridDim.x * 4;
@@ -886,7 +893,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     qmax = fmax(qmax, blk[k * 4 + 2]);
     qmin = fmin(qmin, blk[k * 4 + 3]);
   }
-  q = block_lse(q, s_m, s_s);
+  q = block_lse_ms(q, s_x);
   qmax = block_reduce(qmax, s_x, MaxOp(), -CUDART_INF);
   qmin = block_reduce(qmin, s_x, MinOp(), CUDART_INF);
   if (threadIdx.x == 0 && A.shard == 1) {
