@@ -1985,3 +1985,11 @@ extern "C" int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* works
   });
 }
 
+
+#ifdef UOT_TC_TIMING
+// scripts/tc_timeline.py (timing build only)
+extern "C" int uot_debug_tc_stamps(unsigned long long* out, int n) {
+  cudaMemcpyFromSymbol(out, uot::g_tc_stamps, sizeof(unsigned long long) * 5 * (size_t)n);
+  return 0;
+}
+#endif

@@ -112,6 +112,21 @@ __device__ __forceinline__ void tc_slice_mmas(int kh, int dp, uint32_t dcol, uin
 // output blocks 2c and 2c + 1 (128 rows each, A_0 / A_1 in its TMEM), so
 // every B tile that lands feeds both blocks' MMAs (the pair's M = 256 rows
 // of block j are CTA 2p's and CTA 2p+1's block j).
+#ifdef UOT_TC_TIMING
+// timing build only (scripts/tc_timeline.py): per-CTA %globaltimer stamps
+// (start, A ready, first tile, last tile, end)
+__device__ unsigned long long g_tc_stamps[1 << 16][5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_STAMP(k) \
+  if (threadIdx.x == 64) g_tc_stamps[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x][k] = gtimer()
+#else
+#define TC_STAMP(k)
+#endif
+
 template <int DT>
 __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, int KP) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -126,6 +141,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int split = blockIdx.y, S = gridDim.y;
   const int ntiles = (A.nred + TC_TILE - 1) / TC_TILE;
   const int t0 = (int)((long)ntiles * split / S), t1 = (int)((long)ntiles * (split + 1) / S);
+  TC_STAMP(0);
   const int d = DT > 0 ? DT : A.g.d;
   const int dp = tc_dp(d);
   const int ka = tc_ka(d);        // TMEM columns of one A block
@@ -230,6 +246,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   tc::fence_before();
   tc::cluster_sync_all();
   tc::fence_after();
+  TC_STAMP(1);
 
   const float* recb = A.g.red_rec + b * A.g.red_bstride;
   if (warp == 0) {
@@ -388,6 +405,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     };
     for (int i = 0; i < t1 - t0; ++i) {
       tc::mbar_wait(&dfull[blk], i & 1);
+      if (i == 0) TC_STAMP(2);
       tc::fence_after();
       uint32_t v0[32], v1[32];
       tc::tmem_ld32(tl, v0);
@@ -404,6 +422,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       if (lane == 0) tc::mbar_arrive_remote_relaxed(dempty_leader);
       chunk(v0, v1);
     }
+    TC_STAMP(3);
     if (o < A.nout) {
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
       A.part_m[idx] = m_o - corr;
@@ -412,6 +431,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   }
   tc::fence_before();
   tc::cluster_sync_all();  // both CTAs done with TMEM and remote barriers
+  TC_STAMP(4);
   if (warp == 1) tc::tmem_free2(tbase, 512);
 }
 
