@@ -175,33 +175,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int row0 = blockIdx.x * (TC_NB * TC_TILE);
   const int o = row0 + blk * TC_TILE + row;
   float m_o = 0.f;
-  // Prologue: the CTA's 256 output points -> shared memory (all threads,
-  // coalesced float4 loads), then each epilogue thread builds its A row
-  // (fp16 splits of 8 y + the tf32 constants) in its block's TMEM columns.
+  // Prologue: the producer warp arrives at the cluster barrier and starts
+  // streaming B stages at once (they depend on nothing else); the other
+  // warps stage the CTA's 256 output points in shared memory (coalesced
+  // float4 loads), then each epilogue thread builds its A row (fp16 splits of
+  // 8 y + the tf32 constants) in its block's TMEM columns.
   float* ys = reinterpret_cast<float*>(smem + (size_t)TC_STAGES * TC_STAGE_BYTES);
   const int YS = tc_ystride(d);
-  {
+  if (warp == 0) {
+    tc::cluster_arrive();
+  } else {
     const int nrows = max(0, min(TC_NB * TC_TILE, A.nout - row0));
     const float4* src =
         reinterpret_cast<const float4*>(A.g.out_pts + b * A.g.out_pts_bstride + (long)row0 * d);
     const int q4 = d / 4;
-    for (int idx = tid; idx < nrows * q4; idx += TC_THREADS) {
+    for (int idx = tid - 32; idx < nrows * q4; idx += TC_THREADS - 32) {
       const int r = idx / q4, c = idx - r * q4;
       *reinterpret_cast<float4*>(ys + r * YS + 4 * c) = src[idx];
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(TC_THREADS - 32) : "memory");
   }
-  __syncthreads();
   if (warp >= 2) {
     const float* y = ys + (blk * TC_TILE + row) * YS;
     double s2 = 0.0;
     if (o < A.nout) {
+      double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;  // four independent fp64 chains
       for (int k = 0; k < d; k += 4) {
         const float4 v = *reinterpret_cast<const float4*>(y + k);
-        s2 = fma((double)v.x, (double)v.x, s2);
-        s2 = fma((double)v.y, (double)v.y, s2);
-        s2 = fma((double)v.z, (double)v.z, s2);
-        s2 = fma((double)v.w, (double)v.w, s2);
+        q0 = fma((double)v.x, (double)v.x, q0);
+        q1 = fma((double)v.y, (double)v.y, q1);
+        q2 = fma((double)v.z, (double)v.z, q2);
+        q3 = fma((double)v.w, (double)v.w, q3);
       }
+      s2 = (q0 + q1) + (q2 + q3);
     }
     m_o = o < A.nout ? A.shift_in[(long)b * A.nout + o] : 0.f;
     const double c = -s2 * (double)A.g.L - (double)m_o;
@@ -243,9 +249,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     tc::wait_st();
   }
   // both CTAs' A rows and barriers ready before any MMA / remote arrive
-  tc::fence_before();
-  tc::cluster_sync_all();
-  tc::fence_after();
+  if (warp != 0) {
+    tc::fence_before();
+    tc::cluster_arrive();
+    tc::cluster_wait();
+    tc::fence_after();
+  }
   TC_STAMP(1);
 
   const float* recb = A.g.red_rec + b * A.g.red_bstride;
@@ -428,6 +437,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       A.part_m[idx] = m_o - corr;
       A.part_a[idx] = acc;
     }
+  }
+  if (warp == 0) {
+    __syncwarp();
+    tc::cluster_wait();  // the producer warp's early arrive (phase 0)
   }
   tc::fence_before();
   tc::cluster_sync_all();  // both CTAs done with TMEM and remote barriers
