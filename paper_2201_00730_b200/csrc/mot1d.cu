@@ -757,9 +757,77 @@ __global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
 // ---------------------------------------------------------------------------
 // mot_update: dual atoms, gaps, line search, update (cluster of K CTAs).
 
+// Coalesced staging of per-list rows for the run-per-thread kernels: a warp
+// reads 512 consecutive bytes per instruction (instead of 32 lines, one per
+// thread's 128-byte run) into shared memory laid out as runs of EPT + 2
+// doubles (16-byte aligned, conflict-free per-thread 16-byte reads).
+template <int EPT>
+struct StageRun {
+  static constexpr int RUN = EPT + 2;
+  static constexpr size_t BYTES = (size_t)MT * RUN * sizeof(double);
+  static constexpr bool ON = EPT >= 4 && EPT % 2 == 0 && 2 * BYTES <= 220000;
+};
+
+template <int EPT>
+__device__ __forceinline__ void stage_store(double* buf, const double* row, int nq) {
+  constexpr int RUN = StageRun<EPT>::RUN;
+  const int nch = nq >> 1;
+  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+    for (int j = threadIdx.x; j < nch; j += MT) {
+      const int i = 2 * j, r = i / EPT, c = i - r * EPT;
+      *reinterpret_cast<double2*>(buf + r * RUN + c) = __ldg(r2 + j);
+    }
+    if ((nq & 1) && threadIdx.x == 0) {
+      const int i = nq - 1, r = i / EPT;
+      buf[r * RUN + (i - r * EPT)] = row[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nq; i += MT) {
+      const int r = i / EPT;
+      buf[r * RUN + (i - r * EPT)] = row[i];
+    }
+  }
+}
+
+template <int EPT>
+__device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v)[EPT]) {
+  constexpr int RUN = StageRun<EPT>::RUN;
+  const double2* p = reinterpret_cast<const double2*>(buf + threadIdx.x * RUN);
+#pragma unroll
+  for (int e = 0; e < EPT / 2; ++e) {
+    const double2 u = p[e];
+    v[2 * e] = u.x;
+    v[2 * e + 1] = u.y;
+  }
+  const int i0 = threadIdx.x * EPT;
+  if (i0 + EPT > nq) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (i0 + e >= nq) v[e] = 0.0;
+  }
+}
+
+#ifdef UOT_MOT_TIMING
+// timing build only (scripts/mot_timeline.py): %globaltimer stamps of one
+// thread per CTA at the phase boundaries of mot_update
+__device__ unsigned long long g_mot_stamps[1 << 14][8];
+__device__ __forceinline__ unsigned long long mtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MOT_STAMP(k) \
+  if (threadIdx.x == 0) g_mot_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
+#else
+#define MOT_STAMP(k)
+#endif
+
 template <int EPT>
 __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
+  MOT_STAMP(0);
   cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double stg[];  // 2 staging buffers (StageRun)
   __shared__ double scr[32 * 8];
   __shared__ __align__(16) double red[2 * MBUF];
   __shared__ double tab[32];
@@ -779,6 +847,36 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   __syncthreads();
   if (done_s) return;
   const long base = ((long)b * K + q) * n;
+  // Issue every per-list load up front (cost increments, potentials, tilted
+  // and input weights) so their latencies overlap each other and the scan.
+  double rv[EPT], fv[EPT], tv[EPT], wv[EPT];
+  double loc = 0.0;
+  if constexpr (StageRun<EPT>::ON) {
+    // two rounds of two coalesced rows through the staging buffers
+    double* b0 = stg;
+    double* b1 = stg + MT * StageRun<EPT>::RUN;
+    stage_store<EPT>(b0, A.dcc + base, nq);
+    if (A.mode != 1) stage_store<EPT>(b1, A.f + base, nq);
+    __syncthreads();
+    stage_load<EPT>(b0, nq, rv);
+    if (A.mode != 1) stage_load<EPT>(b1, nq, fv);
+    __syncthreads();
+    if (A.mode != 1) {
+      stage_store<EPT>(b0, A.ta + base, nq);
+      stage_store<EPT>(b1, A.a + base, nq);
+      __syncthreads();
+      stage_load<EPT>(b0, nq, tv);
+      stage_load<EPT>(b1, nq, wv);
+    }
+  } else {
+    load_run<EPT>(A.dcc + base, threadIdx.x * EPT, nq, rv);
+    if (A.mode != 1) {
+      load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+      load_run<EPT>(A.ta + base, threadIdx.x * EPT, nq, tv);
+      load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, wv);
+    }
+  }
+  MOT_STAMP(1);
   // initial potential: f_1[0] = Cc(first tuple), f_k[0] = 0 (barycenter.py:206-207)
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -792,9 +890,6 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     if (lane == 0) cc0_s = c;
   }
   __syncthreads();
-  double rv[EPT];
-  double loc = 0.0;
-  load_run<EPT>(A.dcc + base, threadIdx.x * EPT, nq, rv);
   if (threadIdx.x == 0) rv[0] = 0.0;  // dcc[0] is not an event
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
@@ -817,12 +912,8 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   const double rq = A.omega[q] * A.rho;
   const double lamq = A.lam[(long)b * K + q];
   const double irq = 1.0 / rq;
-  double fv[EPT], tv[EPT], wv[EPT];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   double mxs[2] = {-CUDART_INF, -CUDART_INF};
-  load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
-  load_run<EPT>(A.ta + base, threadIdx.x * EPT, nq, tv);
-  load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, wv);
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const double d = rv[e] - fv[e];
@@ -839,10 +930,14 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     }
   }
   bops::block_red<MNW, 7, 2>(acc, mxs, ping.next());
+  MOT_STAMP(2);
   // cluster sums: fw_gap, plan cost + rho KL terms, sum of centres
   const double cq = acc[5] / acc[3];
-  double cs[3] = {acc[0], acc[1] + rq * (acc[2] - acc[3] + acc[4]), cq};
-  cluster_sum<3>(cs, slots, parity);
+  // (the line search's starting curvature rides along: one cluster barrier
+  // instead of two)
+  double cs[4] = {acc[0], acc[1] + rq * (acc[2] - acc[3] + acc[4]), cq,
+                  fmax(acc[6] / acc[3] - cq * cq, 0.0) / rq};
+  cluster_sum<4>(cs, slots, parity);
   const double fw_gap = cs[0];
   const double primal = cs[1];
   const double dual = A.scal[b * 4 + 0];
@@ -856,6 +951,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     A.summary[b * 2 + 0] = primal;
     A.summary[b * 2 + 1] = dual;
   }
+  MOT_STAMP(3);
   const bool stop = A.early_exit && pd_gap < A.gap_tol;  // barycenter.py:394-396
   if (stop) {
     if (q == 0 && threadIdx.x == 0) A.done[b] = 2;  // converged (plan of this iteration kept)
@@ -870,9 +966,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     // Phi' = -sum_k E_k[d_k], Phi'' = sum_k Var_k[d_k] / rho_k; moments are
     // centred at the gamma = 0 means (translation invariance, see fw1d.cu).
     const double k0 = -cs[2];
-    const double v0 = fmax(acc[6] / acc[3] - cq * cq, 0.0) / rq;
-    double vs[1] = {v0};
-    cluster_sum<1>(vs, slots, parity);
+    const double vs[1] = {cs[3]};
     if (!(k0 < 0.0)) {
       gam = 0.0;
     } else {
@@ -921,12 +1015,14 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   }
 #pragma unroll
   for (int e = 0; e < EPT; ++e) fv[e] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
+  MOT_STAMP(4);
   store_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
   {  // log-sum-exp of the new iterate for the next tilt / the final translation
     double mx, qk;
     double* r0 = ping.next();
     double* r1 = ping.next();
     list_lse<EPT>(wv, fv, irq, tab, r0, r1, mx, qk, tv);  // tv <- w exp(-f/rho - mx)
+    MOT_STAMP(5);
     if (threadIdx.x == 0) {
       A.lse[((long)b * K + q) * 2 + 0] = mx;
       A.lse[((long)b * K + q) * 2 + 1] = qk;
@@ -946,8 +1042,10 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
       for (int e = 0; e < EPT; ++e) tv[e] *= sc;
       tilt_tail<EPT>(A, b, q, nq, tv, ping.next(), iscr, vscr);
     }
+    MOT_STAMP(6);
   }
   cl.sync();  // slots stay valid until every CTA read them
+  MOT_STAMP(7);
 }
 
 // Final translation by the optimal zero-sum lambda (barycenter.py:413-414),
@@ -1247,7 +1345,8 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
                                     (int)p.bucket_smem));
   mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
   UOT_CHECK_LAUNCH();
-  UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch, 0, st, a));
+  UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch,
+                         StageRun<EPT>::ON ? 2 * StageRun<EPT>::BYTES : 0, st, a));
   return UOT_OK;
 }
 
@@ -1536,6 +1635,14 @@ extern "C" int uot_debug_mot_stats(unsigned long long* out, int reset) {
     h[0] = h[1] = 0;
     cudaMemcpyToSymbol(uot::g_mot_stats, h, sizeof(h));
   }
+  return 0;
+}
+#endif
+
+#ifdef UOT_MOT_TIMING
+// scripts/mot_timeline.py (timing build only)
+extern "C" int uot_debug_mot_stamps(unsigned long long* out, int n) {
+  cudaMemcpyFromSymbol(out, uot::g_mot_stamps, sizeof(unsigned long long) * 8 * (size_t)n);
   return 0;
 }
 #endif
