@@ -384,6 +384,88 @@ __device__ __forceinline__ void excl_last_pos(int& idx, double& val, int* iscr, 
   val = ev;
 }
 
+// Coalesced staging of per-list rows for the run-per-thread kernels: a warp
+// reads 512 consecutive bytes per instruction (instead of 32 lines, one per
+// thread's 128-byte run) into shared memory laid out as runs of EPT + 2
+// doubles (16-byte aligned, conflict-free per-thread 16-byte reads).
+template <int EPT>
+struct StageRun {
+  static constexpr int RUN = EPT + 2;
+  static constexpr size_t BYTES = (size_t)MT * RUN * sizeof(double);
+  static constexpr bool ON = EPT >= 4 && EPT % 2 == 0 && 2 * BYTES <= 220000;
+};
+
+template <int EPT>
+__device__ __forceinline__ void stage_store(double* buf, const double* row, int nq) {
+  constexpr int RUN = StageRun<EPT>::RUN;
+  const int nch = nq >> 1;
+  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+    for (int j = threadIdx.x; j < nch; j += MT) {
+      const int i = 2 * j, r = i / EPT, c = i - r * EPT;
+      *reinterpret_cast<double2*>(buf + r * RUN + c) = __ldg(r2 + j);
+    }
+    if ((nq & 1) && threadIdx.x == 0) {
+      const int i = nq - 1, r = i / EPT;
+      buf[r * RUN + (i - r * EPT)] = row[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nq; i += MT) {
+      const int r = i / EPT;
+      buf[r * RUN + (i - r * EPT)] = row[i];
+    }
+  }
+}
+
+template <int EPT>
+__device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v)[EPT]) {
+  constexpr int RUN = StageRun<EPT>::RUN;
+  const double2* p = reinterpret_cast<const double2*>(buf + threadIdx.x * RUN);
+#pragma unroll
+  for (int e = 0; e < EPT / 2; ++e) {
+    const double2 u = p[e];
+    v[2 * e] = u.x;
+    v[2 * e + 1] = u.y;
+  }
+  const int i0 = threadIdx.x * EPT;
+  if (i0 + EPT > nq) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (i0 + e >= nq) v[e] = 0.0;
+  }
+}
+
+// The reverse: each thread puts its run into the staging buffer; after a
+// __syncthreads the row leaves with coalesced 16-byte stores.
+template <int EPT>
+__device__ __forceinline__ void stage_put(double* buf, const double (&v)[EPT]) {
+  double2* p = reinterpret_cast<double2*>(buf + threadIdx.x * StageRun<EPT>::RUN);
+#pragma unroll
+  for (int e = 0; e < EPT / 2; ++e) p[e] = make_double2(v[2 * e], v[2 * e + 1]);
+}
+
+template <int EPT>
+__device__ __forceinline__ void stage_out(const double* buf, double* row, int nq) {
+  constexpr int RUN = StageRun<EPT>::RUN;
+  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    double2* r2 = reinterpret_cast<double2*>(row);
+    const int nch = nq >> 1;
+    for (int j = threadIdx.x; j < nch; j += MT) {
+      const int i = 2 * j, r = i / EPT, c = i - r * EPT;
+      r2[j] = *reinterpret_cast<const double2*>(buf + r * RUN + c);
+    }
+    if ((nq & 1) && threadIdx.x == 0) {
+      const int i = nq - 1, r = i / EPT;
+      row[i] = buf[r * RUN + (i - r * EPT)];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nq; i += MT) {
+      const int r = i / EPT;
+      row[i] = buf[r * RUN + (i - r * EPT)];
+    }
+  }
+}
+
 // Tilted weights ta of list q -> global; breakpoints A_q = cumsum(ta) by a
 // one-sync block scan, zero-weight atoms repeating their predecessor's
 // breakpoint bit for bit (barycenter.py:209-222); the tilted mass; and the
@@ -391,11 +473,15 @@ __device__ __forceinline__ void excl_last_pos(int& idx, double& val, int* iscr, 
 // the owning threads.
 template <int EPT>
 __device__ void tilt_tail(const MotArgs& A, int b, int q, int nq, const double (&ta)[EPT],
-                          double* buf, int* iscr, double* vscr) {
+                          double* buf, int* iscr, double* vscr, double* sbuf = nullptr) {
   const int K = A.k, n = A.n;
   const long base = ((long)b * K + q) * n;
   const int i0 = threadIdx.x * EPT;
-  store_run<EPT>(A.ta + base, i0, nq, ta);
+  const bool staged = StageRun<EPT>::ON && sbuf != nullptr;
+  if (staged)
+    stage_put<EPT>(sbuf, ta);
+  else
+    store_run<EPT>(A.ta + base, i0, nq, ta);
   double av[EPT];
   double loc = 0.0;
 #pragma unroll
@@ -432,7 +518,15 @@ __device__ void tilt_tail(const MotArgs& A, int b, int q, int nq, const double (
       }
     }
   }
-  store_run<EPT>(A.A + base, i0, nq, av);
+  if (staged) {  // both rows leave coalesced
+    double* sb1 = sbuf + MT * StageRun<EPT>::RUN;
+    stage_put<EPT>(sb1, av);
+    __syncthreads();
+    stage_out<EPT>(sbuf, A.ta + base, nq);
+    stage_out<EPT>(sb1, A.A + base, nq);
+  } else {
+    store_run<EPT>(A.A + base, i0, nq, av);
+  }
   if (threadIdx.x == 0) A.tmass[(long)b * K + q] = tot[0];
   const int ne = nq - 1, SS = A.SS;
   double* sv = A.samp + ((long)b * K + q) * SS;
@@ -757,57 +851,6 @@ __global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
 // ---------------------------------------------------------------------------
 // mot_update: dual atoms, gaps, line search, update (cluster of K CTAs).
 
-// Coalesced staging of per-list rows for the run-per-thread kernels: a warp
-// reads 512 consecutive bytes per instruction (instead of 32 lines, one per
-// thread's 128-byte run) into shared memory laid out as runs of EPT + 2
-// doubles (16-byte aligned, conflict-free per-thread 16-byte reads).
-template <int EPT>
-struct StageRun {
-  static constexpr int RUN = EPT + 2;
-  static constexpr size_t BYTES = (size_t)MT * RUN * sizeof(double);
-  static constexpr bool ON = EPT >= 4 && EPT % 2 == 0 && 2 * BYTES <= 220000;
-};
-
-template <int EPT>
-__device__ __forceinline__ void stage_store(double* buf, const double* row, int nq) {
-  constexpr int RUN = StageRun<EPT>::RUN;
-  const int nch = nq >> 1;
-  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-    const double2* r2 = reinterpret_cast<const double2*>(row);
-    for (int j = threadIdx.x; j < nch; j += MT) {
-      const int i = 2 * j, r = i / EPT, c = i - r * EPT;
-      *reinterpret_cast<double2*>(buf + r * RUN + c) = __ldg(r2 + j);
-    }
-    if ((nq & 1) && threadIdx.x == 0) {
-      const int i = nq - 1, r = i / EPT;
-      buf[r * RUN + (i - r * EPT)] = row[i];
-    }
-  } else {
-    for (int i = threadIdx.x; i < nq; i += MT) {
-      const int r = i / EPT;
-      buf[r * RUN + (i - r * EPT)] = row[i];
-    }
-  }
-}
-
-template <int EPT>
-__device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v)[EPT]) {
-  constexpr int RUN = StageRun<EPT>::RUN;
-  const double2* p = reinterpret_cast<const double2*>(buf + threadIdx.x * RUN);
-#pragma unroll
-  for (int e = 0; e < EPT / 2; ++e) {
-    const double2 u = p[e];
-    v[2 * e] = u.x;
-    v[2 * e + 1] = u.y;
-  }
-  const int i0 = threadIdx.x * EPT;
-  if (i0 + EPT > nq) {
-#pragma unroll
-    for (int e = 0; e < EPT; ++e)
-      if (i0 + e >= nq) v[e] = 0.0;
-  }
-}
-
 #ifdef UOT_MOT_TIMING
 // timing build only (scripts/mot_timeline.py): %globaltimer stamps of one
 // thread per CTA at the phase boundaries of mot_update
@@ -1016,7 +1059,13 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
 #pragma unroll
   for (int e = 0; e < EPT; ++e) fv[e] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
   MOT_STAMP(4);
-  store_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+  if constexpr (StageRun<EPT>::ON) {  // coalesced: the stage buffer is free here
+    stage_put<EPT>(stg, fv);
+    __syncthreads();
+    stage_out<EPT>(stg, A.f + base, nq);  // list_lse's barriers order the reuse below
+  } else {
+    store_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
+  }
   {  // log-sum-exp of the new iterate for the next tilt / the final translation
     double mx, qk;
     double* r0 = ping.next();
@@ -1040,7 +1089,8 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
       const double sc = exp(mx - lam1 * irq);
 #pragma unroll
       for (int e = 0; e < EPT; ++e) tv[e] *= sc;
-      tilt_tail<EPT>(A, b, q, nq, tv, ping.next(), iscr, vscr);
+      tilt_tail<EPT>(A, b, q, nq, tv, ping.next(), iscr, vscr,
+                     StageRun<EPT>::ON ? stg : nullptr);
     }
     MOT_STAMP(6);
   }
