@@ -157,6 +157,31 @@ int uot_anderson_weights(int32_t rows, int32_t k, const double* U, double reg, d
                          int32_t* status, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Dense and plan-level helpers of the reference API (fp64, device pointers):
+ *  uot_cost_matrix: C[i*m + j] = |x_i - y_j|^p -- src/measures.py:125-145
+ *    `build_cost_matrix` (p = 1: |d|, p = 2: d*d as the reference).
+ *  uot_cost_quadruple_diameter: out[0] = max_{k,l} range_j (C[j,k] - C[j,l])
+ *    -- src/measures.py:168-184 (used by birkhoff_rate_bound,
+ *    src/sinkhorn.py:338-346).
+ *  uot_updated_marginals: ta = a exp((-f - lam)/rho1), tb = b exp((-g + lam)/rho2)
+ *    -- src/duality.py:293-303 for KL/KL (lam = lambda*(f, g)).
+ *  uot_eval_primal: out[0] = <plan, C> + eps KL(plan | a x b) + D1 + D2 over
+ *    the plan entries (ii, jj, mass)[E] -- src/duality.py:306-344; cost from
+ *    x, y, p (1-D power) or the dense C when non-NULL; KL / Balanced
+ *    divergences (UOT_ENT_*), +inf where the reference returns +inf.
+ * ------------------------------------------------------------------------ */
+int uot_cost_matrix(int32_t n, int32_t m, const double* x, const double* y, double p, double* C,
+                    void* stream);
+int uot_cost_quadruple_diameter(int32_t n, int32_t m, const double* C, double* out, void* stream);
+int uot_updated_marginals(int32_t n, int32_t m, const double* a, const double* b, const double* f,
+                          const double* g, double rho1, double rho2, double lam, double* ta,
+                          double* tb, void* stream);
+int uot_eval_primal(int32_t n, int32_t m, const double* x, const double* y, double p,
+                    const double* C, const double* a, const double* b, int32_t E,
+                    const int64_t* ii, const int64_t* jj, const double* mass, int32_t ent1,
+                    int32_t ent2, double rho1, double rho2, double eps, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
  * Balanced 1-D OT (Algorithm 1): replaces src/ot1d.py:112-172
  * `solve_ot_1d(a, b, cost)` for a batch of problems with sorted supports.
  * fp64.  Costs: UOT_COST_POWER with exponent p, or UOT_COST_EXPLICIT with

@@ -12,6 +12,8 @@ from .duality import (
     UotProblem,
     dual_feasibility_violation,
     eval_F,
+    eval_primal,
+    updated_marginals,
     eval_G,
     eval_H,
     kl_scalars,
@@ -27,7 +29,14 @@ from .exceptions import (
     UnsupportedEntropyError,
     UotError,
 )
-from .measures import DiscreteMeasure, ExplicitMatrix, PowerDistance, SqEuclideanPoints
+from .measures import (
+    DiscreteMeasure,
+    ExplicitMatrix,
+    PowerDistance,
+    SqEuclideanPoints,
+    build_cost_matrix,
+    cost_quadruple_diameter,
+)
 from .barycenter import (
     BarycenterProblem,
     MultiDual,
@@ -45,7 +54,13 @@ from .barycenter import (
     solve_mot_1d,
     solve_mot_1d_batched,
 )
-from .certify import Certificate, assemble_certificate
+from .certify import (
+    Certificate,
+    assemble_certificate,
+    double_star_norm,
+    hilbert_norm,
+    scalar_max_oracle,
+)
 from .fw import FwConfig, feasibility_violation, fw_solve, fw_solve_batched
 from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched
 from .sinkhorn import (
@@ -54,6 +69,7 @@ from .sinkhorn import (
     SinkhornConfig,
     SolverReport,
     anderson_weights,
+    birkhoff_rate_bound,
     estimate_rate,
     f_sinkhorn_step,
     g_sinkhorn_step,

@@ -185,3 +185,79 @@ def _smin(w, rho, pot):
     pot = np.asarray(pot, dtype=np.float64)
     out = kl_scalars(w, w, pot, pot, rho, rho)
     return float(out[0, 2].item())
+
+
+def updated_marginals(prob, d):
+    """Reweighted marginals at the optimal translation (src/duality.py:293-303):
+    (a exp((-f - t*)/rho1), b exp((-g + t*)/rho2)) for KL/KL, on the device."""
+    prob.check_pair(d)
+    require_kl(prob.ent1, prob.ent2, what="updated_marginals")
+    t = D.torch()
+    lib = _lib.load()
+    n, m = len(prob.alpha), len(prob.beta)
+    a, b, f, g = (D.to_dev(v, t.float64) for v in (prob.alpha.weights, prob.beta.weights, d.f, d.g))
+    lam = float(kl_scalars(a, b, f, g, prob.ent1.rho, prob.ent2.rho)[0, 0].item())
+    ta, tb = D.empty((n,), t.float64), D.empty((m,), t.float64)
+    _lib.check(lib.uot_updated_marginals(n, m, _lib.ptr(a), _lib.ptr(b), _lib.ptr(f), _lib.ptr(g),
+                                         float(prob.ent1.rho), float(prob.ent2.rho), lam,
+                                         _lib.ptr(ta), _lib.ptr(tb), _lib.stream_handle()),
+               "uot_updated_marginals")
+    return D.to_np(ta, readonly=False), D.to_np(tb, readonly=False)
+
+
+def eval_primal(prob, plan):
+    """Primal objective of a transport plan (src/duality.py:320-344):
+    <plan, C> + eps KL(plan | alpha x beta) + D1(plan_1 | alpha) +
+    D2(plan_2 | beta), +inf where the reference gives +inf.  ``plan`` is a
+    SparsePlan-like object or a dense (N, M) array; evaluated on the device
+    (KL and Balanced divergences)."""
+    from .entropies import Balanced
+    from .measures import ExplicitMatrix, PowerDistance
+
+    n, m = len(prob.alpha), len(prob.beta)
+    if hasattr(plan, "source_idx"):
+        ii, jj, mass = plan.source_idx, plan.target_idx, plan.mass
+    else:
+        dense = np.asarray(plan, dtype=np.float64)
+        if dense.shape != (n, m):
+            raise ValueError(f"dense plan must have shape ({n}, {m})")
+        if np.any(dense < 0):
+            raise ValueError("plan mass must be nonnegative")
+        ii, jj = np.nonzero(dense)
+        mass = dense[ii, jj]
+    mass = np.asarray(mass, dtype=np.float64)
+    if np.any(mass < 0):
+        raise ValueError("plan mass must be nonnegative")
+    codes = []
+    for spec in (prob.ent1, prob.ent2):
+        if isinstance(spec, KL):
+            codes.append((_lib.ENT_KL, float(spec.rho)))
+        elif isinstance(spec, Balanced):
+            codes.append((_lib.ENT_BALANCED, 0.0))
+        else:
+            raise UnsupportedEntropyError("eval_primal runs KL / Balanced divergences on the B200 path")
+    t = D.torch()
+    lib = _lib.load()
+    x = y = C = None
+    p = 2.0
+    if isinstance(prob.cost, PowerDistance):
+        x = D.to_dev(prob.alpha.points, t.float64)
+        y = D.to_dev(prob.beta.points, t.float64)
+        p = float(prob.cost.p)
+    elif isinstance(prob.cost, ExplicitMatrix):
+        C = D.to_dev(prob.cost.matrix, t.float64)
+    else:
+        raise TypeError(f"unknown cost specification {prob.cost!r}")
+    a = D.to_dev(prob.alpha.weights, t.float64)
+    b = D.to_dev(prob.beta.weights, t.float64)
+    E = int(mass.size)
+    di = D.to_dev(np.asarray(ii, dtype=np.int64), t.int64) if E else None
+    dj = D.to_dev(np.asarray(jj, dtype=np.int64), t.int64) if E else None
+    dm = D.to_dev(mass, t.float64) if E else None
+    out = D.empty((1,), t.float64)
+    _lib.check(lib.uot_eval_primal(n, m, _lib.ptr(x), _lib.ptr(y), p, _lib.ptr(C), _lib.ptr(a),
+                                   _lib.ptr(b), E, _lib.ptr(di), _lib.ptr(dj), _lib.ptr(dm),
+                                   codes[0][0], codes[1][0], codes[0][1], codes[1][1],
+                                   float(prob.eps), _lib.ptr(out), _lib.stream_handle()),
+               "uot_eval_primal")
+    return float(out.item())

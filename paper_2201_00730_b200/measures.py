@@ -134,3 +134,53 @@ def check_submodular(C, tol=None):
     worst = float((C[:-1, 1:] + C[1:, :-1] - C[:-1, :-1] - C[1:, 1:]).min())
     if worst < -tol:
         raise SubmodularityError(f"cost matrix is not submodular (worst adjacent minor {worst:.3e})")
+
+
+def build_cost_matrix(a, b, cost):
+    """Dense C[i, j] = c(x_i, y_j) (src/measures.py:125-145): computed on the
+    device for PowerDistance (uot_cost_matrix); ExplicitMatrix returns the
+    stored matrix after the shape check.  Returns a read-only numpy array."""
+    if isinstance(cost, PowerDistance):
+        from . import _device as D
+        from . import _lib
+
+        t = D.torch()
+        lib = _lib.load()
+        x = D.to_dev(a.points, t.float64)
+        y = D.to_dev(b.points, t.float64)
+        C = D.empty((len(a), len(b)), t.float64)
+        _lib.check(lib.uot_cost_matrix(len(a), len(b), _lib.ptr(x), _lib.ptr(y), float(cost.p),
+                                       _lib.ptr(C), _lib.stream_handle()), "uot_cost_matrix")
+        return D.to_np(C)
+    if isinstance(cost, ExplicitMatrix):
+        if cost.matrix.shape != (len(a), len(b)):
+            raise ValueError(f"explicit cost shape {cost.matrix.shape} does not match supports "
+                             f"({len(a)}, {len(b)})")
+        return cost.matrix
+    raise TypeError(f"unknown cost specification {cost!r}")
+
+
+def cost_quadruple_diameter(C):
+    """max over index quadruples of C[j,k] + C[i,l] - C[j,l] - C[i,k]
+    (src/measures.py:168-184): per column pair the range of the
+    column-difference vector, O(N M^2) on the device."""
+    from . import _device as D
+    from . import _lib
+
+    t = D.torch()
+    if isinstance(C, t.Tensor):
+        Cd = C.to(device=D.device(), dtype=t.float64).contiguous()
+    else:
+        Cn = np.asarray(C, dtype=np.float64)
+        if Cn.ndim != 2:
+            raise ValueError("cost must be a 2-D matrix")
+        if not np.all(np.isfinite(Cn)):
+            raise ValueError("cost entries must be finite")
+        Cd = D.to_dev(Cn, t.float64)
+    if Cd.ndim != 2:
+        raise ValueError("cost must be a 2-D matrix")
+    lib = _lib.load()
+    out = D.empty((1,), t.float64)
+    _lib.check(lib.uot_cost_quadruple_diameter(Cd.shape[0], Cd.shape[1], _lib.ptr(Cd), _lib.ptr(out),
+                                               _lib.stream_handle()), "uot_cost_quadruple_diameter")
+    return float(out.item())

@@ -500,3 +500,19 @@ def write_trace_csv(report, path_or_buf):
     from .formats import write_trace_csv as _w
 
     _w(report, path_or_buf)
+
+
+def birkhoff_rate_bound(prob):
+    """tanh(D / (4 eps)) with D the cost's quadruple diameter
+    (src/sinkhorn.py:338-346): the contraction bound of the softmin in the
+    Hilbert seminorm; D computed on the device."""
+    from .measures import build_cost_matrix, cost_quadruple_diameter
+
+    _require_positive_eps(prob)
+    if isinstance(prob.cost, PowerDistance):
+        C = build_cost_matrix(prob.alpha, prob.beta, prob.cost)
+    elif isinstance(prob.cost, ExplicitMatrix):
+        C = prob.cost.matrix
+    else:
+        raise UnsupportedEntropyError("birkhoff_rate_bound needs a 1-D or explicit cost")
+    return float(np.tanh(cost_quadruple_diameter(C) / (4.0 * prob.eps)))

@@ -642,10 +642,73 @@ def gen_formats():
     save("formats.npz", **out)
 
 
+def gen_dense():
+    """Dense / plan-level API helpers: build_cost_matrix, cost_quadruple_diameter,
+    birkhoff_rate_bound, updated_marginals, eval_primal (sparse and dense plans,
+    eps = 0 and eps > 0, KL and Balanced, an infinite case), and the certify
+    norms / scalar oracle (src/measures.py:125-184, src/sinkhorn.py:338-346,
+    src/duality.py:293-344, src/certify.py:73-118)."""
+    from uotkit import certify as UC
+    from uotkit import duality as UD
+    from uotkit import measures as UM
+
+    rng = np.random.default_rng(311)
+    out = {}
+    k = 0
+    for p, (n, m) in zip([1.0, 2.0, 1.5, 2.0], [(7, 9), (33, 20), (12, 12), (60, 45)]):
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        a, b = rng.uniform(0.1, 1, n), rng.uniform(0.1, 1, m)
+        b *= a.sum() / b.sum()
+        A, Bm = U.DiscreteMeasure(x, a), U.DiscreteMeasure(y, b)
+        C = UM.build_cost_matrix(A, Bm, U.PowerDistance(p))
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, a, b
+        out[f"c{k}_p"] = np.array(p)
+        out[f"c{k}_C"] = C
+        out[f"c{k}_diam"] = np.array(UM.cost_quadruple_diameter(C))
+        r1, r2 = float(rng.uniform(0.5, 2)), float(rng.uniform(0.5, 2))
+        eps = [0.05, 0.2, 0.1, 0.3][k]
+        prob = U.UotProblem(A, Bm, U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=eps)
+        out[f"c{k}_par"] = np.array([r1, r2, eps])
+        out[f"c{k}_birkhoff"] = np.array(US.birkhoff_rate_bound(prob))
+        f, g = rng.normal(size=n) * 0.3, rng.normal(size=m) * 0.3
+        out[f"c{k}_f"], out[f"c{k}_g"] = f, g
+        ta, tb = UD.updated_marginals(prob, U.DualPair(f, g))
+        out[f"c{k}_ta"], out[f"c{k}_tb"] = ta, tb
+        # sparse plan (the balanced 1-D OT plan) at eps = 0 and eps > 0
+        plan, _ = U.solve_ot_1d(A, Bm, U.PowerDistance(p))
+        out[f"c{k}_pi"], out[f"c{k}_pj"], out[f"c{k}_pm"] = (plan.source_idx, plan.target_idx,
+                                                              plan.mass)
+        prob0 = U.UotProblem(A, Bm, U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=0.0)
+        out[f"c{k}_primal0"] = np.array(UD.eval_primal(prob0, plan))
+        out[f"c{k}_primal_eps"] = np.array(UD.eval_primal(prob, plan))
+        dense = rng.uniform(0, 1, (n, m)) * (rng.uniform(0, 1, (n, m)) < 0.3) / (n * m)
+        out[f"c{k}_dense"] = dense
+        out[f"c{k}_primal_dense"] = np.array(UD.eval_primal(prob, dense))
+        probB = U.UotProblem(A, Bm, U.PowerDistance(p), U.Balanced(), U.KL(r2), eps=0.0)
+        out[f"c{k}_primal_bal"] = np.array(UD.eval_primal(probB, plan))
+        k += 1
+    out["ncases"] = np.array(k)
+    # infinite: mass on a zero-weight atom
+    x = np.linspace(0, 1, 5)
+    a = np.array([0.2, 0.0, 0.3, 0.2, 0.3])
+    A = U.DiscreteMeasure(x, a)
+    prob = U.UotProblem(A, A, U.PowerDistance(2.0), U.KL(1.0), U.KL(1.0), eps=0.0)
+    dense = np.diag([0.2, 0.1, 0.3, 0.2, 0.2])
+    out["inf_primal"] = np.array(UD.eval_primal(prob, dense))
+    v = rng.normal(size=17)
+    w = rng.normal(size=9)
+    out["norm_f"], out["norm_g"] = v, w
+    out["hilbert"] = np.array(UC.hilbert_norm(v))
+    out["dstar"] = np.array(UC.double_star_norm(v, w))
+    xm, vm = UC.scalar_max_oracle(lambda t: -(t - 0.37) ** 2 + 0.5 * np.sin(3 * t), (0.0, 1.0))
+    out["oracle_x"], out["oracle_v"] = np.array(xm), np.array(vm)
+    save("dense.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats"]
+                             "sinkhorn_ent", "anderson", "formats", "dense"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -97,3 +97,17 @@ def test_estimate_rate():
     assert P.estimate_rate(np.ones(6)) == 1.0
     with pytest.raises(ValueError):
         P.estimate_rate(np.array([1.0, 1e-14, 1e-15]))
+
+
+def test_certify_norms_and_scalar_oracle():
+    """Certificate helpers vs the reference (tests/golden/dense.npz)."""
+    z = golden("dense.npz")
+    assert P.hilbert_norm(z["norm_f"]) == float(z["hilbert"])
+    assert P.double_star_norm(z["norm_f"], z["norm_g"]) == float(z["dstar"])
+    xm, vm = P.scalar_max_oracle(lambda t: -(t - 0.37) ** 2 + 0.5 * np.sin(3 * t), (0.0, 1.0))
+    assert xm == pytest.approx(float(z["oracle_x"]), abs=1e-9)
+    assert vm == pytest.approx(float(z["oracle_v"]), abs=1e-12)
+    with pytest.raises(ValueError):
+        P.scalar_max_oracle(lambda t: t * t, (-1.0, 1.0))
+    with pytest.raises(ValueError):
+        P.hilbert_norm([])
