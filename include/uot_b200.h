@@ -157,6 +157,24 @@ int uot_anderson_weights(int32_t rows, int32_t k, const double* U, double reg, d
                          int32_t* status, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Entropy family (src/entropies.py), fp64, device pointers:
+ *  uot_logdotexp: out[o*inner + i] = log sum_k w[k] exp(scale v[o][k][i]) with
+ *    zero-weight entries masked before the max shift -- :67-92 `logdotexp`
+ *    (flat: outer = inner = 1; `softmin` :187-200 is scale = -1/eps).
+ *  uot_entropy_map: op 0 conj, 1 conj_grad, 2 conj_hess, 3 aprox of entropy
+ *    `ent` (UOT_ENT_*) elementwise -- :142-221; *bad (device int32) = 1 when a
+ *    Berg argument leaves x < rho (the reference raises ValueError).
+ *  uot_divergence: out[0] = D(mu | nu) -- :104-140 (+inf where the reference
+ *    returns +inf).
+ * ------------------------------------------------------------------------ */
+int uot_logdotexp(int64_t outer, int64_t k, int64_t inner, const double* v, const double* w,
+                  double scale, double* out, void* stream);
+int uot_entropy_map(int32_t op, int32_t ent, double rho, double eps, int64_t n, const double* x,
+                    double* out, int32_t* bad, void* stream);
+int uot_divergence(int32_t ent, double rho, int64_t n, const double* mu, const double* nu,
+                   double* out, void* stream);
+
+/* ------------------------------------------------------------------------
  * Dense and plan-level helpers of the reference API (fp64, device pointers):
  *  uot_cost_matrix: C[i*m + j] = |x_i - y_j|^p -- src/measures.py:125-145
  *    `build_cost_matrix` (p = 1: |d|, p = 2: d*d as the reference).

@@ -70,6 +70,7 @@ EXPORTS = (
     "uot_sinkhorn_workspace_size", "uot_sinkhorn_run", "uot_sinkhorn_verify", "uot_kl_scalars",
     "uot_anderson_workspace_size", "uot_anderson_reset", "uot_anderson_step", "uot_anderson_weights",
     "uot_cost_matrix", "uot_cost_quadruple_diameter", "uot_updated_marginals", "uot_eval_primal",
+    "uot_logdotexp", "uot_entropy_map", "uot_divergence",
     "uot_ot1d_workspace_size", "uot_ot1d_batched", "uot_fw1d_workspace_size", "uot_fw1d_run", "uot_feasibility_1d",
     "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_mot_certify", "uot_bary_workspace_size", "uot_bary_run",
     "uot_nccl_unique_id", "uot_nccl_comm_init", "uot_nccl_comm_destroy",
@@ -99,6 +100,9 @@ def load(require_gpu=True):
         lib.uot_cost_quadruple_diameter.argtypes = [_i32, _i32, _vp, _vp, _vp]
         lib.uot_updated_marginals.argtypes = [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _f64, _f64,
                                               _vp, _vp, _vp]
+        lib.uot_logdotexp.argtypes = [_i64, _i64, _i64, _vp, _vp, _f64, _vp, _vp]
+        lib.uot_entropy_map.argtypes = [_i32, _i32, _f64, _f64, _i64, _vp, _vp, _vp, _vp]
+        lib.uot_divergence.argtypes = [_i32, _f64, _i64, _vp, _vp, _vp, _vp]
         lib.uot_eval_primal.argtypes = [_i32, _i32, _vp, _vp, _f64, _vp, _vp, _vp, _i32, _vp, _vp,
                                         _vp, _i32, _i32, _f64, _f64, _f64, _vp, _vp]
         _LIB = lib

@@ -427,3 +427,20 @@ def extract_barycenter(plan, inputs, w):
     w = np.asarray(w, dtype=np.float64)
     pts = np.stack([inputs[k].points[plan.indices[:, k]] for k in range(plan.k)], axis=1)
     return DiscreteMeasure(pts @ w, plan.mass)
+
+
+# File formats (paper_2201_00730_b200/formats.py), re-exported where the reference defines them.
+
+
+def write_multiplan_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.write_multiplan_csv`."""
+    from . import formats as _F
+
+    return _F.write_multiplan_csv(*args, **kwargs)
+
+
+def read_multiplan_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.read_multiplan_csv`."""
+    from . import formats as _F
+
+    return _F.read_multiplan_csv(*args, **kwargs)

@@ -1993,3 +1993,156 @@ extern "C" int uot_debug_tc_stamps(unsigned long long* out, int n) {
   return 0;
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// The entropy-family functions of the reference API on the device
+// (src/entropies.py:67-263): weighted log-sum-exp (flat and along an axis),
+// conjugates and their derivatives, aprox, and the divergences.
+
+namespace uot {
+namespace {
+
+// op 0 conj, 1 conj_grad, 2 conj_hess, 3 aprox (entropies.py:142-221)
+__global__ void entropy_map_kernel(int op, int ent, double rho, double eps, long n,
+                                   const double* __restrict__ x, double* __restrict__ out,
+                                   int* __restrict__ bad) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    double r = 0.0;
+    if (op == 3) {
+      r = aprox_any(ent, rho, eps, v);
+    } else if (ent == UOT_ENT_KL) {
+      r = op == 0 ? rho * expm1(v / rho) : op == 1 ? exp(v / rho) : exp(v / rho) / rho;
+    } else if (ent == UOT_ENT_BERG) {
+      if (op != 2 && !(v < rho)) *bad = 1;  // the conjugate lives on x < rho
+      r = op == 0 ? -rho * log1p(-v / rho) : op == 1 ? rho / (rho - v) : rho / ((rho - v) * (rho - v));
+    } else {
+      r = op == 0 ? v + 0.0 : op == 1 ? 1.0 : 0.0;
+    }
+    out[i] = r;
+  }
+}
+
+// log sum_k w_k exp(scale v[o][k][i]) with zero-weight entries masked before
+// the max shift (entropies.py:67-92); one thread per (o, i) output.
+__global__ void lse_axis_kernel(long outer, long K, long inner, const double* __restrict__ v,
+                                const double* __restrict__ w, double scale,
+                                double* __restrict__ out) {
+  const long total = outer * inner;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const long o = t / inner, i = t - o * inner;
+    const double* vo = v + o * K * inner + i;
+    double mx = -CUDART_INF;
+    for (long k = 0; k < K; ++k)
+      if (w[k] > 0.0) mx = fmax(mx, scale * vo[k * inner]);
+    const double sh = isfinite(mx) ? mx : 0.0;
+    double s = 0.0;
+    for (long k = 0; k < K; ++k)
+      if (w[k] > 0.0) s += w[k] * exp(scale * vo[k * inner] - sh);
+    out[t] = log(s) + sh;
+  }
+}
+
+// inner == 1: one block per output (masked block max, then the sum).
+__global__ void __launch_bounds__(256) lse_flat_kernel(long K, const double* __restrict__ v,
+                                                       const double* __restrict__ w, double scale,
+                                                       double* __restrict__ out) {
+  __shared__ double scratch[32];
+  const double* vo = v + blockIdx.x * K;
+  double mx = -CUDART_INF;
+  for (long k = threadIdx.x; k < K; k += blockDim.x)
+    if (w[k] > 0.0) mx = fmax(mx, scale * vo[k]);
+  mx = block_reduce(mx, scratch, MaxOp(), -CUDART_INF);
+  const double sh = isfinite(mx) ? mx : 0.0;
+  double s = 0.0;
+  for (long k = threadIdx.x; k < K; k += blockDim.x)
+    if (w[k] > 0.0) s += w[k] * exp(scale * vo[k] - sh);
+  s = block_reduce(s, scratch, SumOp(), 0.0);
+  if (threadIdx.x == 0) out[blockIdx.x] = log(s) + sh;
+}
+
+// Csiszar divergence (entropies.py:104-140), one block.
+__global__ void __launch_bounds__(1024) divergence_kernel(int ent, double rho, long n,
+                                                          const double* __restrict__ mu,
+                                                          const double* __restrict__ nu,
+                                                          double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double terms = 0.0, sing = 0.0, zero_mu = 0.0, md = 0.0, mw = 0.0;
+  for (long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double m = mu[i], w = nu[i];
+    if (ent == UOT_ENT_BALANCED) {
+      md = fmax(md, fabs(m - w));
+      mw = fmax(mw, fabs(w));
+    } else if (w > 0.0) {
+      if (ent == UOT_ENT_KL) {
+        terms += (m > 0.0 ? m * log(m / w) : 0.0) - m + w;
+      } else {
+        if (m == 0.0) zero_mu = 1.0;
+        else terms += m - w - w * log(m / w);
+      }
+    } else {
+      sing += m;
+    }
+  }
+  terms = block_reduce(terms, scratch, SumOp(), 0.0);
+  sing = block_reduce(sing, scratch, SumOp(), 0.0);
+  zero_mu = block_reduce(zero_mu, scratch, MaxOp(), 0.0);
+  md = block_reduce(md, scratch, MaxOp(), 0.0);
+  mw = block_reduce(mw, scratch, MaxOp(), 0.0);
+  if (threadIdx.x != 0) return;
+  double r;
+  if (ent == UOT_ENT_BALANCED) r = md <= 1e-9 * (1.0 + mw) ? 0.0 : CUDART_INF;
+  else if (ent == UOT_ENT_KL) r = sing > 0.0 ? CUDART_INF : rho * terms;
+  else r = zero_mu > 0.0 ? CUDART_INF : rho * (terms + sing);
+  out[0] = r;
+}
+
+}  // namespace
+}  // namespace uot
+
+extern "C" int uot_entropy_map(int32_t op, int32_t ent, double rho, double eps, int64_t n,
+                               const double* x, double* out, int32_t* bad, void* stream) {
+  using namespace uot;
+  if (op < 0 || op > 3 || ent < 0 || ent > 2 || n < 0 || (op == 3 && !(eps > 0.0))) {
+    set_error("entropy_map: invalid arguments");
+    return UOT_INVALID;
+  }
+  if (n == 0) return UOT_OK;
+  const long blocks = std::min<long>(4096, (n + 255) / 256);
+  entropy_map_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(op, ent, rho, eps, n, x,
+                                                                         out, bad);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
+extern "C" int uot_logdotexp(int64_t outer, int64_t k, int64_t inner, const double* v,
+                             const double* w, double scale, double* out, void* stream) {
+  using namespace uot;
+  if (outer < 1 || k < 0 || inner < 1 || out == nullptr) {
+    set_error("logdotexp: invalid arguments");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (inner == 1 && outer <= 65535) {
+    lse_flat_kernel<<<(unsigned)outer, 256, 0, st>>>(k, v, w, scale, out);
+  } else {
+    const long blocks = std::min<long>(4096, (outer * inner + 255) / 256);
+    lse_axis_kernel<<<(unsigned)blocks, 256, 0, st>>>(outer, k, inner, v, w, scale, out);
+  }
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
+extern "C" int uot_divergence(int32_t ent, double rho, int64_t n, const double* mu,
+                              const double* nu, double* out, void* stream) {
+  using namespace uot;
+  if (ent < 0 || ent > 2 || n < 0 || out == nullptr) {
+    set_error("divergence: invalid arguments");
+    return UOT_INVALID;
+  }
+  divergence_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ent, rho, n, mu, nu, out);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}

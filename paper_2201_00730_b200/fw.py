@@ -20,7 +20,7 @@ from . import _device as D
 from . import _lib
 from .certify import assemble_certificate
 from .duality import DualPair
-from .entropies import KL, Berg
+from .entropies import KL, Berg, require_kl
 from .exceptions import InfeasibleDualError, MassBalanceError, UnsupportedEntropyError
 from .measures import PowerDistance
 from .ot1d import SparsePlan
@@ -179,3 +179,117 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
              "wall_ns": np.full(its, wall, dtype=np.int64)}
     return SolverReport(final=DualPair(fin_f, fin_g), iterations=its, converged=converged,
                         trace=trace, certificate=cert, plan=plan)
+
+
+# File formats (paper_2201_00730_b200/formats.py), re-exported where the reference defines them.
+
+
+def write_gap_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.write_gap_csv`."""
+    from . import formats as _F
+
+    return _F.write_gap_csv(*args, **kwargs)
+
+
+# ---------------------------------------------------------------------------
+# Single-step building blocks of src/fw.py (ternary search, the H0 line
+# search, the pairwise atom store and one pairwise step), for callers that
+# drive FW themselves; the solvers above run whole iterations on the device.
+
+ATOM_DEDUP_TOL = 1e-12  # src/fw.py:47
+
+
+def ternary_max(fn, lo=0.0, hi=1.0, iters=60):
+    """Ternary search for the maximiser of a concave scalar function (:118-128)."""
+    a, b = float(lo), float(hi)
+    for _ in range(iters):
+        m1, m2 = a + (b - a) / 3.0, b - (b - a) / 3.0
+        if fn(m1) < fn(m2):
+            a = m1
+        else:
+            b = m2
+    return 0.5 * (a + b)
+
+
+def _h0_value(prob, f, g):
+    from .duality import kl_scalars
+
+    return float(kl_scalars(prob.alpha.weights, prob.beta.weights, f, g, prob.ent1.rho,
+                            prob.ent2.rho)[0, 1].item())
+
+
+def line_search_h0(prob, current, target):
+    """Step in [0, 1] maximising H0 on the segment: 60 ternary steps and an
+    endpoint comparison (:131-148); every H0 value on the device."""
+    require_kl(prob.ent1, prob.ent2, what="line_search_h0")
+
+    def value(gamma):
+        return _h0_value(prob, (1.0 - gamma) * current.f + gamma * target.f,
+                         (1.0 - gamma) * current.g + gamma * target.g)
+
+    gamma = ternary_max(value, 0.0, 1.0, iters=60)
+    return max(((value(c), c) for c in (gamma, 0.0, 1.0)), key=lambda z: z[0])[1]
+
+
+class AtomStore:
+    """Active dual-pair atoms of pairwise FW with convex weights (:70-95)."""
+
+    def __init__(self, r_atoms, s_atoms, weights):
+        r = np.atleast_2d(np.asarray(r_atoms, dtype=np.float64))
+        s = np.atleast_2d(np.asarray(s_atoms, dtype=np.float64))
+        w = np.atleast_1d(np.asarray(weights, dtype=np.float64))
+        if r.shape[0] != s.shape[0] or r.shape[0] != w.size or w.size == 0:
+            raise ValueError("store arrays must agree on the number of atoms")
+        if np.any(w < -1e-14):
+            raise ValueError("weights must stay nonnegative")
+        if abs(w.sum() - 1.0) > 1e-12:
+            raise ValueError("weights must sum to one")
+        self.r_atoms, self.s_atoms, self.weights = r, s, w
+
+    def current(self):
+        return DualPair(self.weights @ self.r_atoms, self.weights @ self.s_atoms)
+
+
+def pfw_step(prob, store):
+    """One pairwise weight transfer (:255-323): device LMO (updated marginals,
+    1-D oracle), the least aligned active atom as donor, a ternary H0 line
+    search on [0, w_away] with endpoint comparison, dedup merge of the new
+    atom and removal of emptied atoms."""
+    from .duality import updated_marginals
+    from .measures import DiscreteMeasure
+    from .ot1d import solve_ot_1d
+
+    if store.weights.size == 0:
+        raise ValueError("atom store is empty")
+    _check_problem(prob)
+    d = store.current()
+    ta, tb = updated_marginals(prob, d)
+    _, atom = solve_ot_1d(DiscreteMeasure(prob.alpha.points, ta),
+                          DiscreteMeasure(prob.beta.points, tb), prob.cost)
+    scores = np.where(store.weights > 0, store.r_atoms @ ta + store.s_atoms @ tb, np.inf)
+    away = int(np.argmin(scores))
+    max_step = float(store.weights[away])
+    dr, ds = atom.f - store.r_atoms[away], atom.g - store.s_atoms[away]
+    if max_step <= 0.0 or (np.abs(dr).max() < ATOM_DEDUP_TOL and np.abs(ds).max() < ATOM_DEDUP_TOL):
+        return store
+
+    def value(gamma):
+        return _h0_value(prob, d.f + gamma * dr, d.g + gamma * ds)
+
+    gamma = ternary_max(value, 0.0, max_step, iters=60)
+    gamma = max(((value(c), c) for c in (gamma, 0.0, max_step)), key=lambda z: z[0])[1]
+    if gamma <= 0.0:
+        return store
+    w = store.weights.copy()
+    w[away] = max(w[away] - gamma, 0.0)
+    r_atoms, s_atoms = store.r_atoms, store.s_atoms
+    dist = np.maximum(np.abs(r_atoms - atom.f).max(axis=1), np.abs(s_atoms - atom.g).max(axis=1))
+    hit = np.nonzero(dist < ATOM_DEDUP_TOL)[0]
+    if hit.size:
+        w[hit[0]] += gamma
+    else:
+        r_atoms = np.vstack([r_atoms, atom.f])
+        s_atoms = np.vstack([s_atoms, atom.g])
+        w = np.concatenate([w, [gamma]])
+    keep = w > 0
+    return AtomStore(r_atoms[keep], s_atoms[keep], w[keep])

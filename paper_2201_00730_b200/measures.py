@@ -184,3 +184,41 @@ def cost_quadruple_diameter(C):
     _lib.check(lib.uot_cost_quadruple_diameter(Cd.shape[0], Cd.shape[1], _lib.ptr(Cd), _lib.ptr(out),
                                                _lib.stream_handle()), "uot_cost_quadruple_diameter")
     return float(out.item())
+
+
+# File formats (paper_2201_00730_b200/formats.py), re-exported where the reference defines them.
+
+
+def read_measure_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.read_measure_csv`."""
+    from . import formats as _F
+
+    return _F.read_measure_csv(*args, **kwargs)
+
+
+def write_measure_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.write_measure_csv`."""
+    from . import formats as _F
+
+    return _F.write_measure_csv(*args, **kwargs)
+
+
+def read_measure_json(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.read_measure_json`."""
+    from . import formats as _F
+
+    return _F.read_measure_json(*args, **kwargs)
+
+
+def write_measure_json(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.write_measure_json`."""
+    from . import formats as _F
+
+    return _F.write_measure_json(*args, **kwargs)
+
+
+def measure_to_csv_text(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.measure_to_csv_text`."""
+    from . import formats as _F
+
+    return _F.measure_to_csv_text(*args, **kwargs)

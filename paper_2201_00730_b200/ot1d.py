@@ -137,3 +137,20 @@ def check_complementary_slackness(plan, d, C, tol=1e-9):
         return False
     on = spread[plan.source_idx, plan.target_idx]
     return bool(np.abs(on).max(initial=0.0) <= tol)
+
+
+# File formats (paper_2201_00730_b200/formats.py), re-exported where the reference defines them.
+
+
+def write_plan_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.write_plan_csv`."""
+    from . import formats as _F
+
+    return _F.write_plan_csv(*args, **kwargs)
+
+
+def read_plan_csv(*args, **kwargs):
+    """See :func:`paper_2201_00730_b200.formats.read_plan_csv`."""
+    from . import formats as _F
+
+    return _F.read_plan_csv(*args, **kwargs)

@@ -705,10 +705,81 @@ def gen_dense():
     save("dense.npz", **out)
 
 
+def gen_entropy_api():
+    """Entropy-family functions (src/entropies.py:67-263), the FW single-step
+    API (line_search_h0, pfw_step on an AtomStore, src/fw.py:118-323) and the
+    certify grid oracles (src/certify.py:121-177), from the reference."""
+    from uotkit import certify as UC
+    from uotkit import entropies as UE
+
+    rng = np.random.default_rng(2718)
+    out = {}
+    v = rng.normal(size=40) * 3
+    w = rng.uniform(0, 1, 40)
+    w[::7] = 0.0
+    out["v"], out["w"] = v, w
+    out["lde_flat"] = np.array(UE.logdotexp(v, w))
+    M = rng.normal(size=(6, 40))
+    out["M"] = M
+    out["lde_ax1"] = UE.logdotexp(M, w, axis=1)
+    M0 = rng.normal(size=(40, 5))
+    out["M0"] = M0
+    out["lde_ax0"] = UE.logdotexp(M0, w, axis=0)
+    out["lde_zero"] = np.array(UE.logdotexp(v, np.zeros(40)))
+    A = U.DiscreteMeasure(np.arange(40.0), np.where(w > 0, w, 0.5))
+    out["aw"] = A.weights
+    out["softmin"] = np.array(UE.softmin(A, 0.3, v))
+    x = rng.normal(size=25)
+    out["x"] = x
+    specs = {"kl": U.KL(1.7), "berg": U.Berg(2.5), "bal": U.Balanced()}
+    for name, sp in specs.items():
+        xs = np.minimum(x, 2.4) if name == "berg" else x
+        out[f"{name}_x"] = xs
+        out[f"{name}_conj"] = UE.conj(sp, xs)
+        out[f"{name}_grad"] = UE.conj_grad(sp, xs)
+        out[f"{name}_hess"] = UE.conj_hess(sp, xs)
+        out[f"{name}_aprox"] = UE.aprox(sp, 0.2, xs)
+        mu = rng.uniform(0, 1, 30)
+        nu = rng.uniform(0, 1, 30)
+        nu[3] = 0.0
+        if name == "berg":
+            mu[5] = 0.7
+        out[f"{name}_mu"], out[f"{name}_nu"] = mu, nu
+        out[f"{name}_div"] = np.array(UE.divergence(sp, mu, nu))
+        mu2 = mu.copy()
+        mu2[3] = 0.0
+        out[f"{name}_mu2"] = mu2
+        out[f"{name}_div2"] = np.array(UE.divergence(sp, mu2, nu))
+        out[f"{name}_div_same"] = np.array(UE.divergence(sp, nu, nu))
+    # FW single steps on a small problem
+    n, m = 30, 24
+    xx, yy = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+    a, b = rng.uniform(0.1, 1, n), rng.uniform(0.1, 1, m) * 1.3
+    prob = U.UotProblem(U.DiscreteMeasure(xx, a), U.DiscreteMeasure(yy, b), U.PowerDistance(2.0),
+                        U.KL(1.2), U.KL(0.8), eps=0.0)
+    out["fw_x"], out["fw_y"], out["fw_a"], out["fw_b"] = xx, yy, a, b
+    cur = U.DualPair(np.zeros(n), np.zeros(m))
+    _, _, _, atom, _ = UF._lmo(prob, cur)
+    out["ls_gamma"] = np.array(UF.line_search_h0(prob, cur, atom))
+    store = UF.AtomStore(np.zeros((1, n)), np.zeros((1, m)), np.array([1.0]))
+    for it in range(4):
+        store = UF.pfw_step(prob, store)
+        out[f"pfw{it}_r"], out[f"pfw{it}_s"], out[f"pfw{it}_w"] = (store.r_atoms, store.s_atoms,
+                                                                    store.weights)
+    f = rng.normal(size=11)
+    g = rng.normal(size=7)
+    out["gf"], out["gg"] = f, g
+    out["hgrid"] = np.array(UC.hilbert_norm_grid(f))
+    out["dgrid"] = np.array(UC.double_star_norm_grid(f, g))
+    gx, gv = UC.grid_max_scalar(lambda t: -(t - 0.123) ** 2, 0.0, 1.0)
+    out["gmax"] = np.array([gx, gv])
+    save("entropy_api.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

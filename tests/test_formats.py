@@ -111,3 +111,13 @@ def test_certify_norms_and_scalar_oracle():
         P.scalar_max_oracle(lambda t: t * t, (-1.0, 1.0))
     with pytest.raises(ValueError):
         P.hilbert_norm([])
+
+
+def test_certify_grid_oracles():
+    z = golden("entropy_api.npz")
+    assert P.certify.hilbert_norm_grid(z["gf"]) == pytest.approx(float(z["hgrid"]), abs=1e-12)
+    assert P.certify.double_star_norm_grid(z["gf"], z["gg"]) == pytest.approx(float(z["dgrid"]),
+                                                                              abs=1e-12)
+    gx, gv = P.certify.grid_max_scalar(lambda t: -(t - 0.123) ** 2, 0.0, 1.0)
+    np.testing.assert_allclose([gx, gv], z["gmax"], atol=1e-12)
+    assert P.fw.ternary_max(lambda t: -(t - 0.25) ** 2) == pytest.approx(0.25, abs=1e-9)
