@@ -161,7 +161,7 @@ def test_row_sharded_protocol_emulated(precision, nshards):
 
 @pytest.mark.parametrize("d,n,m", [(64, 300, 257), (32, 128, 640), (48, 513, 129)])
 def test_tcgen05_point_clouds_vs_oracle(d, n, m):
-    """d >= 32 runs the tcgen05 3xTF32 kernel; ragged sizes exercise the
+    """d >= 32 runs the tcgen05 fp16-split kernel; ragged sizes exercise the
     padded tiles.  fp32 tolerance on the translated pair (1e-4 eps)."""
     x, y, a, b = S.cfg4_batch(batch=2, n=n, m=m, d=d, seed=d)
     eps, rho = 0.05, 0.5
@@ -282,3 +282,37 @@ def test_h_rejects_berg():
     with pytest.raises(P.UnsupportedEntropyError):
         P.sinkhorn_batched(z["c0_x"], z["c0_y"], z["c0_a"], z["c0_b"], 0.1, 1.0, 1.0, 2,
                            variant="h", cost="power", precision="fp64", ent1="berg", ent2="kl")
+
+
+def test_row_sharded_real_nccl_single_rank():
+    """The real NCCL branch of the row-sharded path (communicator built in the
+    extension from a unique id broadcast by torch.distributed, ncclAllGather
+    per iteration, the scalar all-gather at the end) with one rank: equals
+    the unsharded solve.  Multi-rank runs need more than one GPU."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2201_00730_b200.distributed import NcclComm
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        c = S.cfg3_inputs(n=1024, m=768, seed=13)
+        f1, g1, t1, _ = run_dev(c.x[None], c.y[None], c.alpha[None], c.beta[None], c.eps, c.rho,
+                                20, precision="fp64")
+        with NcclComm(1, 0) as comm:
+            f, g, tr, its = P.sinkhorn_batched(c.x[None], c.y[None], c.alpha[None], c.beta[None],
+                                               c.eps, c.rho, c.rho, 20, precision="fp64",
+                                               comm=comm.handle, nranks=1, rank=0)
+            f, g = D.to_np(f).astype(float), D.to_np(g).astype(float)
+        assert int(its[0].item()) == 20
+        assert rel_err(f[0], g[0], f1[0], g1[0]) < 1e-12
+        np.testing.assert_allclose(D.to_np(tr)[0], t1[0], rtol=1e-9, atol=1e-14)
+    finally:
+        if created:
+            dist.destroy_process_group()
