@@ -60,9 +60,12 @@ int uot_device_arch(int device, int* sm_major, int* sm_minor);
  * Sinkhorn: replaces src/sinkhorn.py:246-315 `run(prob, config, init)` for
  * variants "f" (f_sinkhorn_step, :103-114), "h" (h_sinkhorn_step,
  * :137-163) and "g" (g_sinkhorn_step, :117-134: translated steps at the
- * incoming lambda, then lambda* of the new pair; unsharded) with KL marginals (KL(rho1), KL(rho2)), for a batch of
- * independent problems, with a fixed iteration budget and the reference's
- * optional `delta_f < tol` stop (:304-306) evaluated per problem.
+ * incoming lambda, then lambda* of the new pair; unsharded), with the
+ * marginal penalties ent1 / ent2 (KL, Berg, Balanced; "h" is KL/KL), for a
+ * batch of independent problems, with a fixed iteration budget and the
+ * reference's optional `delta_f < tol` stop (:304-306) evaluated per problem.
+ * fp32 squared-Euclidean costs with d >= 32 run on the tensor cores
+ * (tcgen05: fp16 hi/lo split cost tiles + a tf32 constants MMA).
  *
  * Inputs (dtype elements): x [batch][n][d], y [batch][m][d] (d = 1 for
  * UOT_COST_POWER); explicit costs c [batch][n][m] and its transpose
