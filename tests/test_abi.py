@@ -47,3 +47,21 @@ def test_no_cpu_fallback_without_gpu():
     prob = P.UotProblem(a, a, P.PowerDistance(2.0), P.KL(1.0), P.KL(1.0), eps=0.1)
     with pytest.raises(P.UotError):
         P.h_sinkhorn_step(prob, P.DualPair.zeros(2, 2))
+
+
+def test_product_never_imports_the_oracle():
+    """oracle/ is the checker: nothing in the product package may import,
+    link or execute it (there is no CPU fallback)."""
+    import re
+
+    pkg = os.path.join(ROOT, "paper_2201_00730_b200")
+    offenders = []
+    for dirpath, _, files in os.walk(pkg):
+        for name in files:
+            if not name.endswith((".py", ".cu", ".cuh")):
+                continue
+            text = open(os.path.join(dirpath, name), encoding="utf-8").read()
+            if re.search(r"^\s*(import oracle|from oracle|import\s+oracle\b)|_oracle\.so|oracle_smin",
+                         text, re.M):
+                offenders.append(name)
+    assert offenders == []
