@@ -2,6 +2,7 @@
 // structure).  Reference: src/sinkhorn.py:93-163, src/entropies.py:67-92,
 // :187-214, src/duality.py:175-178.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -923,8 +924,9 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     }
     if (A.hat_old != nullptr && A.trace != nullptr) {
       const double delta = fmax(qmax + tau, -(qmin + tau));
-      A.trace[(long)b * A.trace_len + A.t] = delta;
-      A.iters_done[b] = A.t + 1;
+      const int tt = A.t_dev ? A.iters_done[b] : A.t;  // replayed graphs carry no t
+      A.trace[(long)b * A.trace_len + tt] = delta;
+      A.iters_done[b] = tt + 1;
       if (A.use_tol && delta < A.tol) A.done[b] = 1;
     }
     A.counter[b] = 0u;
@@ -1387,8 +1389,9 @@ struct Engine {
   static int launch_tail(const uot_sinkhorn_desc& d, const Buffers<T>& bf, cudaStream_t st,
                          bool to_target, int mode, int nparts, const T* hat_old, T* hat_out,
                          const T* pot_in, int t, double* trace, int trace_len,
-                         const ShardOpt* so = nullptr) {
+                         const ShardOpt* so = nullptr, int t_dev = 0) {
     TailArgs<T> a{};
+    a.t_dev = t_dev;
     const bool H = d.variant == UOT_SINKHORN_H;
     const double eps = d.eps, r1 = d.rho1, r2 = d.rho2;
     const double ro = to_target ? r2 : r1;        // own marginal strength
@@ -1529,17 +1532,61 @@ struct Engine {
     if (g_newton) UOT_TRY(lam_newton(bf.hatA0));  // lambda*(f0, g0) (:263-265)
     const int sB = splits(d.batch, d.m, d.n, d.d);  // g-update splits
     const int sA = splits(d.batch, d.n, d.m, d.d);  // f-update splits
-    for (int t = 0; t < d.iters; ++t) {
+    // one iteration: two half-steps (main + tail each), hat buffers by parity
+    auto body = [&](int t, cudaStream_t s, int t_dev) -> int {
       T* hat_old = (t & 1) ? bf.hatA1 : bf.hatA0;
       T* hat_new = (t & 1) ? bf.hatA0 : bf.hatA1;
-      UOT_TRY(launch_main(d, bf, st, true, sB, 0, d.n, 0, sB));
-      UOT_TRY(launch_tail(d, bf, st, true, 0, sB, nullptr, bf.hatB, nullptr, t, nullptr,
-                          trace_len));
-      UOT_TRY(launch_main(d, bf, st, false, sA, 0, d.m, 0, sA));
-      UOT_TRY(launch_tail(d, bf, st, false, 0, sA, hat_old, hat_new, nullptr, t, trace,
-                          trace_len));
-      if (g_newton) UOT_TRY(lam_newton(hat_new));  // lambda_star(pair, initial=lam) (:134)
+      UOT_TRY(launch_main(d, bf, s, true, sB, 0, d.n, 0, sB));
+      UOT_TRY(launch_tail(d, bf, s, true, 0, sB, nullptr, bf.hatB, nullptr, t, nullptr,
+                          trace_len, nullptr, t_dev));
+      UOT_TRY(launch_main(d, bf, s, false, sA, 0, d.m, 0, sA));
+      UOT_TRY(launch_tail(d, bf, s, false, 0, sA, hat_old, hat_new, nullptr, t, trace,
+                          trace_len, nullptr, t_dev));
+      if (g_newton) {  // lambda_star(pair, initial=lam) (:134)
+        sk_lambda_newton<T><<<d.batch, 256, 0, s>>>(d.n, d.m, hat_new, bf.hatB, (const T*)d.a,
+                                                    (const T*)d.b, d.ent1, d.ent2, d.rho1, d.rho2,
+                                                    bf.sc);
+        UOT_CHECK_LAUNCH();
+      }
+      return UOT_OK;
+    };
+    // Long runs replay a captured two-iteration CUDA graph: the per-kernel
+    // CPU launch cost otherwise bounds small problems (the kernels read the
+    // iteration index from iters_done, so the graph carries no t).
+    const int pairs = (d.iters >= 8 && !std::getenv("UOT_NO_GRAPH")) ? d.iters / 2 : 0;
+    if (pairs > 0) {
+      static thread_local cudaStream_t cap = nullptr;  // capture stream (per thread, per device)
+      static thread_local int cap_dev = -1;
+      int dev = 0;
+      UOT_CUDA_TRY(cudaGetDevice(&dev));
+      if (cap == nullptr || cap_dev != dev) {
+        UOT_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cap_dev = dev;
+      }
+      cudaGraph_t graph = nullptr;
+      UOT_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      int rc = body(0, cap, 1);
+      if (rc == UOT_OK) rc = body(1, cap, 1);
+      const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+      if (rc != UOT_OK) {
+        if (graph != nullptr) cudaGraphDestroy(graph);
+        return rc;
+      }
+      UOT_CUDA_TRY(ce);
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      UOT_CUDA_TRY(ie);
+      for (int k = 0; k < pairs; ++k) {
+        const cudaError_t le = cudaGraphLaunch(exec, st);
+        if (le != cudaSuccess) {
+          cudaGraphExecDestroy(exec);
+          UOT_CUDA_TRY(le);
+        }
+      }
+      UOT_CUDA_TRY(cudaGraphExecDestroy(exec));  // the launches stay enqueued
     }
+    for (int t = 2 * pairs; t < d.iters; ++t) UOT_TRY(body(t, st, pairs > 0 ? 1 : 0));
     sk_finalize<T><<<dim3(ceil_div(nm, 256), d.batch), 256, 0, st>>>(
         d.n, d.m, bf.hatA0, bf.hatA1, bf.hatB, bf.sc, bf.iters_done, (T*)d.f, (T*)d.g);
     UOT_CHECK_LAUNCH();

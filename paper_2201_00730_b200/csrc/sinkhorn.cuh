@@ -91,6 +91,7 @@ struct TailArgs {
   unsigned int* counter;       // [B]
   double* trace;               // [B][trace_len] or nullptr
   int trace_len, t;
+  int t_dev;                   // 1: t = iters_done[b] (graph-replayed iterations)
   int* iters_done;             // [B]
   int* done;                   // [B]
   double tol;
