@@ -265,6 +265,8 @@ typedef struct uot_fw_desc {
   int32_t* status;
   double* step_size; /* optional [batch][max_iters]: gamma of each iteration */
   int32_t* natoms;   /* optional [batch][max_iters]: active atoms (pairwise) */
+  const double* ref_f; /* optional [batch][n]: reference potential (src/fw.py:217-219) */
+  double* err_f;       /* optional [batch][max_iters]: ||f_t + lambda*_t - ref_f||_inf */
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);

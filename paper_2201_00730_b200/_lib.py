@@ -49,7 +49,7 @@ class FwDesc(ctypes.Structure):
         ("x", _vp), ("y", _vp), ("a", _vp), ("b", _vp), ("f", _vp), ("g", _vp),
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),
         ("ei", _vp), ("ej", _vp), ("em", _vp), ("count", _vp), ("summary", _vp),
-        ("status", _vp), ("step_size", _vp), ("natoms", _vp),
+        ("status", _vp), ("step_size", _vp), ("natoms", _vp), ("ref_f", _vp), ("err_f", _vp),
     ]
 
 

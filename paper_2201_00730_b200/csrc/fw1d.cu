@@ -116,6 +116,8 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.scratch = (double*)ws;
   a.scratch_i = (int*)((char*)ws + sizeof(double) * (size_t)d->batch * (d->n + d->m));
   a.natoms = d->natoms;
+  a.ref_f = d->ref_f;
+  a.err_f = d->err_f;
   if (d->step == UOT_STEP_PAIRWISE) {
     const size_t cap = (size_t)d->max_iters + 1;
     const size_t bc = (size_t)d->batch * cap;

@@ -74,6 +74,8 @@ struct FwArgs {
   double* scs;    // [batch][cap] scores of the active atoms (per position)
   double* dis;    // [batch][cap] sup-norm distance to the new atom
   int* natoms;    // optional [batch][max_iters] trace
+  const double* ref_f;  // optional [batch][n]: reference potential
+  double* err_f;        // optional [batch][max_iters]: sup error of the translated iterate
 };
 
 static __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
@@ -710,6 +712,16 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     const double earg = lane == 0 ? t1 * la + t2 * lb : lane == 1 ? sha - lam / r1 : shb + lam / r2;
     const double ev = exp(earg);  // (libdevice: arguments are not shifted here)
     const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * __shfl_sync(bops::FULL, ev, 0);
+    if (A.err_f != nullptr) {  // fw.py:217-219: translated iterate vs the reference
+      double em1[1] = {0.0};
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = c.src(e);
+        if (i < n) em1[0] = bops::dmax(em1[0], fabs(f[e] + lam - A.ref_f[(long)b * n + i]));
+      }
+      bops::block_max<FW_NW, 1>(em1, ping.next());
+      if (threadIdx.x == 0) A.err_f[(long)b * A.max_iters + t] = em1[0];
+    }
     const double sca = sha > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 1) : 0.0;
     const double scb = shb > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 2) : 0.0;
 #pragma unroll

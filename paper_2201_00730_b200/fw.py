@@ -64,10 +64,11 @@ class FwBatchResult:
     status: object
     step_size: object
     natoms: object = None  # pairwise: active atoms after each iteration
+    err_f: object = None   # with ref_f: translated-iterate error per iteration
 
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
-                     gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None):
+                     gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None, ref_f=None):
     """Batched FW on device: x, a [B, N]; y, b [B, M] sorted supports.
 
     ``early_exit=False`` runs exactly ``max_iters`` iterations per problem
@@ -107,6 +108,12 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         em=_lib.ptr(r.em), count=_lib.ptr(r.count), summary=_lib.ptr(r.summary),
         status=_lib.ptr(r.status), step_size=_lib.ptr(r.step_size),
         natoms=_lib.ptr(r.natoms) if r.natoms is not None else None)
+    ref_d = None
+    if ref_f is not None:  # err_f trace against a reference potential (fw.py:217-219)
+        ref_d = D.to_dev(ref_f, t.float64).reshape(B, n).contiguous()
+        r.err_f = t.zeros((B, max_iters), dtype=t.float64, device=x.device)
+        desc.ref_f = _lib.ptr(ref_d)
+        desc.err_f = _lib.ptr(r.err_f)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)
@@ -152,12 +159,13 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     viol = float(feasibility_violation(x, y, d.f, d.g, p)[0].item())
     if viol > FEAS_TOL:
         raise InfeasibleDualError("initial pair violates f + g <= C")
-    if reference is not None:
-        raise UnsupportedEntropyError("err_f tracing is not on the B200 FW path")
+    if reference is not None and len(reference.f) != n:
+        raise ValueError("reference potential does not match the problem")
     tic = time.perf_counter_ns()
     r = fw_solve_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.ent1.rho,
                          prob.ent2.rho, p, config.max_iters, config.step, config.gap_tol,
-                         early_exit=True, f0=d.f, g0=d.g)
+                         early_exit=True, f0=d.f, g0=d.g,
+                         ref_f=None if reference is None else reference.f)
     st = int(r.status[0].item())
     if st == 1:
         raise MassBalanceError("reweighted marginal masses disagree; optimal translation looks broken")
@@ -177,6 +185,8 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     cert = assemble_certificate(primal, dual, feas, config.gap_tol)
     trace = {"h0": h0, "fw_gap": fg, "pd_gap": pd,
              "wall_ns": np.full(its, wall, dtype=np.int64)}
+    if reference is not None:
+        trace["err_f"] = D.to_np(r.err_f[0, :its], readonly=False)
     return SolverReport(final=DualPair(fin_f, fin_g), iterations=its, converged=converged,
                         trace=trace, certificate=cert, plan=plan)
 

@@ -766,6 +766,11 @@ def gen_entropy_api():
         store = UF.pfw_step(prob, store)
         out[f"pfw{it}_r"], out[f"pfw{it}_s"], out[f"pfw{it}_w"] = (store.r_atoms, store.s_atoms,
                                                                     store.weights)
+    # fw_solve with a reference pair: the err_f trace (src/fw.py:217-219)
+    ref = UF.fw_solve(prob, UF.FwConfig("harmonic", 400, 1e-12)).final
+    rep = UF.fw_solve(prob, UF.FwConfig("harmonic", 30, 1e-300), reference=ref)
+    out["fw_ref_f"], out["fw_ref_g"] = ref.f, ref.g
+    out["fw_err_f"] = rep.trace["err_f"]
     f = rng.normal(size=11)
     g = rng.normal(size=7)
     out["gf"], out["gg"] = f, g

@@ -89,3 +89,14 @@ def test_fw_single_steps():
         assert np.abs(cur.g - ref_s).max() <= 1e-6 * scale, it
         np.testing.assert_allclose(np.sort(store.weights[store.weights > 1e-9]),
                                    np.sort(ref_w[ref_w > 1e-9]), atol=1e-6)
+
+
+def test_fw_solve_reference_err_f_trace():
+    """fw_solve(..., reference=pair) traces ||f_t + lambda*_t - ref.f||_inf
+    (src/fw.py:217-219); harmonic steps so the trajectory is the reference's."""
+    z = golden("entropy_api.npz")
+    prob = P.UotProblem(P.DiscreteMeasure(z["fw_x"], z["fw_a"]), P.DiscreteMeasure(z["fw_y"], z["fw_b"]),
+                        P.PowerDistance(2.0), P.KL(1.2), P.KL(0.8), eps=0.0)
+    ref = P.DualPair(z["fw_ref_f"], z["fw_ref_g"])
+    rep = P.fw_solve(prob, P.FwConfig("harmonic", 30, 1e-300), reference=ref)
+    np.testing.assert_allclose(rep.trace["err_f"], z["fw_err_f"], rtol=1e-9, atol=1e-13)
