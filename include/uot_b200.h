@@ -209,9 +209,10 @@ int uot_eval_primal(int32_t n, int32_t m, const double* x, const double* y, doub
  * c [batch][n][m].  Outputs: f [batch][n], g [batch][m]; plan entries
  * (ei, ej int32, em fp64) [batch][n+m-1] with count [batch]; entries are in
  * sweep order.  status [batch] gets 1 for a mass mismatch above 1e-9
- * relative (src/ot1d.py:133-136).  The ExplicitMatrix cost is validated on
- * the host (Monge check, src/measures.py:148-165) and is not on the B200
- * path yet (returns 3).  n, m <= 4096 per problem.
+ * relative (src/ot1d.py:133-136).  An ExplicitMatrix cost (device c,
+ * row-major per problem) is looked up at C(i, j) along the staircase
+ * exactly as src/ot1d.py:100-107 does; the caller validates it (Monge check,
+ * src/measures.py:148-165); p is ignored then.  n, m <= 4096 per problem.
  * ------------------------------------------------------------------------ */
 int uot_ot1d_workspace_size(int32_t batch, int32_t n, int32_t m, size_t* bytes);
 int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
@@ -224,7 +225,8 @@ int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const
  * `fw_solve(prob, FwConfig(step, max_iters, gap_tol))` (+ `_lmo` :159-173,
  * `_h0` :106-115, `eval_primal` src/duality.py:320-344, line search
  * :131-148, `_finalize` :235-252) for KL(rho1)/KL(rho2) marginals and
- * |x-y|^p costs on sorted supports.  fp64.
+ * |x-y|^p costs on sorted supports, or an explicit (Monge) cost matrix c
+ * [batch][n][m] when c != NULL (ExplicitMatrix, src/fw.py:168-172).  fp64.
  *
  * f, g [batch][n|m]: in = initial pair (must be dual feasible), out = the
  * final iterate TRANSLATED by lambda* (report.final).  Traces
@@ -267,6 +269,7 @@ typedef struct uot_fw_desc {
   int32_t* natoms;   /* optional [batch][max_iters]: active atoms (pairwise) */
   const double* ref_f; /* optional [batch][n]: reference potential (src/fw.py:217-219) */
   double* err_f;       /* optional [batch][max_iters]: ||f_t + lambda*_t - ref_f||_inf */
+  const double* c;     /* optional [batch][n][m]: explicit cost (else |x - y|^p) */
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);
@@ -277,6 +280,9 @@ int uot_fw1d_run(const uot_fw_desc* desc, void* workspace, size_t workspace_byte
  * out [batch] fp64. */
 int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
                        double p, const double* f, const double* g, double* out, void* stream);
+/* The same for explicit costs C [batch][n][m] (ExplicitMatrix). */
+int uot_feasibility_explicit(int32_t batch, int32_t n, int32_t m, const double* C,
+                             const double* f, const double* g, double* out, void* stream);
 
 /* ------------------------------------------------------------------------
  * Balanced K-marginal sweep (Algorithm 3) and the KL barycenter FW:

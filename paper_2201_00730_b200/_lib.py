@@ -49,7 +49,7 @@ class FwDesc(ctypes.Structure):
         ("x", _vp), ("y", _vp), ("a", _vp), ("b", _vp), ("f", _vp), ("g", _vp),
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),
         ("ei", _vp), ("ej", _vp), ("em", _vp), ("count", _vp), ("summary", _vp),
-        ("status", _vp), ("step_size", _vp), ("natoms", _vp), ("ref_f", _vp), ("err_f", _vp),
+        ("status", _vp), ("step_size", _vp), ("natoms", _vp), ("ref_f", _vp), ("err_f", _vp), ("c", _vp),
     ]
 
 
@@ -72,6 +72,7 @@ EXPORTS = (
     "uot_cost_matrix", "uot_cost_quadruple_diameter", "uot_updated_marginals", "uot_eval_primal",
     "uot_logdotexp", "uot_entropy_map", "uot_divergence",
     "uot_ot1d_workspace_size", "uot_ot1d_batched", "uot_fw1d_workspace_size", "uot_fw1d_run", "uot_feasibility_1d",
+    "uot_feasibility_explicit",
     "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_mot_certify", "uot_bary_workspace_size", "uot_bary_run",
     "uot_nccl_unique_id", "uot_nccl_comm_init", "uot_nccl_comm_destroy",
 )

@@ -379,15 +379,15 @@ def fw_barycenter(problem, config=FwConfig(), init=None):
     """Frank-Wolfe on the invariant dual of the KL multimarginal problem
     (src/barycenter.py:330-430).  Returns ``(report, plan)``.
 
-    The certificate's feasibility term is 0 here: the reference evaluates it
-    only when the full index grid holds <= 1e5 tuples (:416-418) by an
-    exhaustive host sweep; the B200 path does not enumerate the grid."""
+    The certificate's feasibility term is the exhaustive grid check when the
+    index grid holds <= 1e5 tuples, else 0 (:416-418), evaluated on the
+    device on the translated potentials (the translation sums to zero,
+    :298-317, so the grid maximum is the same).  ``step="pairwise"`` takes
+    the line-search branch, as the reference's step dispatch does (:397-407:
+    anything but "harmonic" runs the ternary line search)."""
     if problem.rho is None:
         raise ValueError("balanced barycenters route directly through solve_mot_1d")
-    if config.step == "pairwise":
-        from .exceptions import UnsupportedEntropyError
-
-        raise UnsupportedEntropyError("pairwise FW is not on the B200 barycenter path")
+    step = "linesearch" if config.step == "pairwise" else config.step
     inputs = problem.inputs
     pots0 = None
     if init is not None:
@@ -396,7 +396,7 @@ def fw_barycenter(problem, config=FwConfig(), init=None):
             raise ValueError("initial potentials do not match the inputs")
     x, a, f0, lens = _pack(inputs, pots0)
     tic = time.perf_counter_ns()
-    r = fw_barycenter_batched(x, a, problem.omega, problem.rho, config.max_iters, config.step,
+    r = fw_barycenter_batched(x, a, problem.omega, problem.rho, config.max_iters, step,
                               config.gap_tol, early_exit=True, f0=f0, lens=lens)
     st = int(r.status[0].item())
     if st == 1:
@@ -414,7 +414,10 @@ def fw_barycenter(problem, config=FwConfig(), init=None):
     final = MultiDual(tuple(fd[q, :lens[q]] for q in range(len(inputs))))
     plan = _plan_from(r.idx[0], r.mass[0], r.count[0].item())
     primal, dual = (float(v) for v in D.to_np(r.summary[0]))
-    cert = assemble_certificate(primal, dual, 0.0, config.gap_tol)
+    feas = 0.0
+    if int(np.prod([len(m) for m in inputs], dtype=np.float64)) <= EXHAUSTIVE_LIMIT:
+        feas = dual_feasibility_exhaustive(inputs, final, barycentric_cost_fn(problem.omega))
+    cert = assemble_certificate(primal, dual, feas, config.gap_tol)
     report = SolverReport(final=final, iterations=its, converged=converged, trace=trace,
                           certificate=cert, plan=plan)
     return report, plan

@@ -11,15 +11,17 @@ using namespace fwk;
 
 // Dense feasibility max(0, max_ij f_i + g_j - C_ij): duality.py:117-121.
 __global__ void feasibility_kernel(int n, int m, const double* x, const double* y, double p,
-                                   const double* f, const double* g, double* out) {
+                                   const double* C, const double* f, const double* g,
+                                   double* out) {
   __shared__ double scr[32];
   const int b = blockIdx.y;
   double worst = -CUDART_INF;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)n * m;
        t += (long)gridDim.x * blockDim.x) {
     const int i = (int)(t / m), j = (int)(t % m);
-    const double v = f[(long)b * n + i] + g[(long)b * m + j] -
-                     pcost(x[(long)b * n + i], y[(long)b * m + j], p);
+    const double c = C != nullptr ? C[(long)b * n * m + t]
+                                  : pcost(x[(long)b * n + i], y[(long)b * m + j], p);
+    const double v = f[(long)b * n + i] + g[(long)b * m + j] - c;
     worst = fmax(worst, v);
   }
   worst = block_reduce(worst, scr, MaxOp(), -CUDART_INF);
@@ -72,8 +74,8 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
     set_error("uot_fw1d_run: invalid descriptor");
     return UOT_INVALID;
   }
-  if (!(d->rho1 > 0) || !(d->rho2 > 0) || !(d->p >= 1.0)) {
-    set_error("uot_fw1d_run: need rho > 0 and p >= 1");
+  if (!(d->rho1 > 0) || !(d->rho2 > 0) || (d->c == nullptr && !(d->p >= 1.0))) {
+    set_error("uot_fw1d_run: need rho > 0 and p >= 1 (or an explicit cost c)");
     return UOT_INVALID;
   }
   if (d->step != UOT_STEP_HARMONIC && d->step != UOT_STEP_LINESEARCH &&
@@ -118,6 +120,7 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.natoms = d->natoms;
   a.ref_f = d->ref_f;
   a.err_f = d->err_f;
+  a.C = d->c;
   if (d->step == UOT_STEP_PAIRWISE) {
     const size_t cap = (size_t)d->max_iters + 1;
     const size_t bc = (size_t)d->batch * cap;
@@ -147,13 +150,12 @@ extern "C" int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const doubl
                                 double p, const double* c, double* f, double* g, int32_t* ei,
                                 int32_t* ej, double* em, int32_t* count, int32_t* status,
                                 void* workspace, size_t workspace_bytes, void* stream) {
-  (void)c;
-  if (batch < 1 || n < 1 || m < 1 || !(p >= 1.0)) {
+  if (batch < 1 || n < 1 || m < 1 || (cost == UOT_COST_POWER && !(p >= 1.0))) {
     set_error("uot_ot1d_batched: invalid arguments");
     return UOT_INVALID;
   }
-  if (cost != UOT_COST_POWER) {
-    set_error("uot_ot1d_batched: only |x-y|^p costs run on the B200 path");
+  if (cost != UOT_COST_POWER && !(cost == UOT_COST_EXPLICIT && c != nullptr)) {
+    set_error("uot_ot1d_batched: cost must be UOT_COST_POWER or UOT_COST_EXPLICIT with c");
     return UOT_INVALID;
   }
   if (workspace_bytes < fw_scratch_bytes(batch, n, m)) {
@@ -176,6 +178,7 @@ extern "C" int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const doubl
   A.em = em;
   A.count = count;
   A.status = status;
+  A.C = cost == UOT_COST_EXPLICIT ? c : nullptr;
   A.scratch = (double*)workspace;
   A.scratch_i = (int*)((char*)workspace + sizeof(double) * (size_t)batch * (n + m));
   return launch_fw(A, batch, (cudaStream_t)stream);
@@ -192,7 +195,24 @@ extern "C" int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const dou
   UOT_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * batch, st));
   const long nm = (long)n * m;
   const int blocks = (int)std::min<long>(1024, (nm + 255) / 256);
-  feasibility_kernel<<<dim3(blocks, batch), 256, 0, st>>>(n, m, x, y, p, f, g, out);
+  feasibility_kernel<<<dim3(blocks, batch), 256, 0, st>>>(n, m, x, y, p, nullptr, f, g, out);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
+extern "C" int uot_feasibility_explicit(int32_t batch, int32_t n, int32_t m, const double* C,
+                                        const double* f, const double* g, double* out,
+                                        void* stream) {
+  if (batch < 1 || n < 1 || m < 1 || C == nullptr) {
+    set_error("uot_feasibility_explicit: invalid arguments");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  UOT_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * batch, st));
+  const long nm = (long)n * m;
+  const int blocks = (int)std::min<long>(1024, (nm + 255) / 256);
+  feasibility_kernel<<<dim3(blocks, batch), 256, 0, st>>>(n, m, nullptr, nullptr, 0.0, C, f, g,
+                                                          out);
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }

@@ -76,6 +76,7 @@ struct FwArgs {
   int* natoms;    // optional [batch][max_iters] trace
   const double* ref_f;  // optional [batch][n]: reference potential
   double* err_f;        // optional [batch][max_iters]: sup error of the translated iterate
+  const double* C;      // optional [batch][n][m]: explicit cost (PK = 3), else |x - y|^p
 };
 
 static __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
@@ -89,7 +90,8 @@ __device__ __forceinline__ double pcost(double xi, double yj, double p) {
 }
 
 // Cost kinds resolved at compile time for the FW kernels: PK = 0 -> p = 2,
-// 1 -> p = 1, 2 -> general p (one out-of-line pow keeps the kernel small).
+// 1 -> p = 1, 2 -> general p (one out-of-line pow keeps the kernel small),
+// 3 -> explicit matrix (ExplicitMatrix, src/ot1d.py:100-107; Cta::cost).
 template <int PK>
 __device__ __forceinline__ double pcost_k(double xi, double yj, double p) {
   const double d = xi - yj;
@@ -148,6 +150,13 @@ struct Cta {
   double* zred;  // scratch of the zero-weight fix (own syncs)
   bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
   double* pfw;   // pairwise FW staging (n + m doubles) or nullptr
+  const double* cm = nullptr;  // PK == 3: this problem's [n][m] cost matrix
+
+  // C(i, j): the cost at source i, target j (src/ot1d.py:92-109)
+  __device__ __forceinline__ double cost(int i, int j) const {
+    if constexpr (PK == 3) return __ldg(cm + (long)i * m + j);
+    else return pcost_k<PK>(sx[i], sy[j], p);
+  }
 
   __device__ int src(int e) const { return threadIdx.x * EPT + e; }
 
@@ -249,19 +258,19 @@ struct Cta {
       da[e] = 0.0;
       db[e] = 0.0;
       if (i >= 1 && i < n) {
-        const double yj = sy[rkA[i - 1]];  // partner of source event i-1
-        da[e] = pcost_k<PK>(sx[i], yj, p) - pcost_k<PK>(sx[i - 1], yj, p);
+        const int j = rkA[i - 1];  // partner of source event i-1
+        da[e] = cost(i, j) - cost(i - 1, j);
       }
       if (i >= 1 && i < m) {
-        const double xk = sx[rkB[i - 1]];  // partner of target event i-1
-        db[e] = pcost_k<PK>(xk, sy[i], p) - pcost_k<PK>(xk, sy[i - 1], p);
+        const int k = rkB[i - 1];  // partner of target event i-1
+        db[e] = cost(k, i) - cost(k, i - 1);
       }
       la += da[e];
       lb += db[e];
     }
     double off[2] = {la, lb}, unused[2];
     bops::block_scan_excl<FW_NW, 2>(off, unused, ping.next());
-    const double s0 = pcost_k<PK>(sx[0], sy[0], p);
+    const double s0 = cost(0, 0);
     double ra = off[0], rb = off[1];
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
@@ -570,6 +579,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       (reinterpret_cast<uintptr_t>(rkB + m) + 15) & ~static_cast<uintptr_t>(15));
   Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false,
                  PW ? pfwbuf : nullptr};
+  if constexpr (PK == 3) c.cm = A.C + (long)b * n * m;
   bops::Ping<FW_BUF> ping{red, 0};
   bops::load_exp_table(tab);
 
@@ -945,6 +955,7 @@ int launch_fw_impl(const FwArgs& a, int batch, cudaStream_t st) {
       default: return go(fw1d_kernel<16, PK, PW>);
     }
   };
+  if (a.C != nullptr) return by_ept(std::integral_constant<int, 3>());
   if (a.p == 2.0) return by_ept(std::integral_constant<int, 0>());
   if (a.p == 1.0) return by_ept(std::integral_constant<int, 1>());
   return by_ept(std::integral_constant<int, 2>());

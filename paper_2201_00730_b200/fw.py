@@ -22,7 +22,7 @@ from .certify import assemble_certificate
 from .duality import DualPair
 from .entropies import KL, Berg, require_kl
 from .exceptions import InfeasibleDualError, MassBalanceError, UnsupportedEntropyError
-from .measures import PowerDistance
+from .measures import ExplicitMatrix, PowerDistance, check_submodular
 from .ot1d import SparsePlan
 from .sinkhorn import SolverReport
 
@@ -65,11 +65,14 @@ class FwBatchResult:
     step_size: object
     natoms: object = None  # pairwise: active atoms after each iteration
     err_f: object = None   # with ref_f: translated-iterate error per iteration
+    cost: object = None    # explicit cost matrix kept alive for the launch
 
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
-                     gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None, ref_f=None):
-    """Batched FW on device: x, a [B, N]; y, b [B, M] sorted supports.
+                     gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None, ref_f=None,
+                     C=None):
+    """Batched FW on device: x, a [B, N]; y, b [B, M] sorted supports;
+    ``C`` [B, N, M] (optional) an explicit Monge cost instead of |x - y|^p.
 
     ``early_exit=False`` runs exactly ``max_iters`` iterations per problem
     (BASELINE fixed-iteration configs); True applies fw.py:220-222 per
@@ -114,6 +117,9 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         r.err_f = t.zeros((B, max_iters), dtype=t.float64, device=x.device)
         desc.ref_f = _lib.ptr(ref_d)
         desc.err_f = _lib.ptr(r.err_f)
+    if C is not None:
+        r.cost = D.to_dev(C, t.float64).reshape(B, n, m).contiguous()
+        desc.c = _lib.ptr(r.cost)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)
@@ -122,14 +128,21 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
     return r
 
 
-def feasibility_violation(x, y, f, g, p=2.0, stream=None):
-    """max(0, max_ij f_i + g_j - |x_i - y_j|^p) per problem (device, fp64)."""
+def feasibility_violation(x, y, f, g, p=2.0, stream=None, C=None):
+    """max(0, max_ij f_i + g_j - C_ij) per problem (device, fp64), C_ij =
+    |x_i - y_j|^p or the explicit ``C`` [B, N, M]."""
     t = D.torch()
     lib = _lib.load()
     x, y, f, g = (D.to_dev(v, t.float64) for v in (x, y, f, g))
     if x.ndim == 1:
         x, y, f, g = (v.unsqueeze(0) for v in (x, y, f, g))
     out = D.empty((x.shape[0],), t.float64)
+    if C is not None:
+        B, n, m = x.shape[0], x.shape[1], y.shape[1]
+        C = D.to_dev(C, t.float64).reshape(B, n, m).contiguous()
+        _lib.check(lib.uot_feasibility_explicit(B, n, m, _lib.ptr(C), _lib.ptr(f), _lib.ptr(g),
+                                                _lib.ptr(out), _lib.stream_handle(stream)))
+        return out
     _lib.check(lib.uot_feasibility_1d(x.shape[0], x.shape[1], y.shape[1], _lib.ptr(x),
                                       _lib.ptr(y), ctypes.c_double(p), _lib.ptr(f), _lib.ptr(g),
                                       _lib.ptr(out), _lib.stream_handle(stream)))
@@ -144,28 +157,49 @@ def _check_problem(prob):
             raise UnsupportedEntropyError("frank-wolfe needs strictly convex conjugates (KL or Berg)")
         if not isinstance(spec, KL):
             raise UnsupportedEntropyError("the B200 FW path runs KL penalties")
-    if not isinstance(prob.cost, PowerDistance):
-        raise UnsupportedEntropyError("the B200 FW path runs |x - y|^p costs")
+    if not isinstance(prob.cost, (PowerDistance, ExplicitMatrix)):
+        raise TypeError(f"unknown cost specification {prob.cost!r}")
+
+
+def _default_init(prob, C):
+    """Zero pair, or half row / column minima for a cost with negative
+    entries so that f + g <= C (src/fw.py:151-156); minima on the device."""
+    n, m = len(prob.alpha), len(prob.beta)
+    if C is None:  # |x - y|^p >= 0
+        return DualPair.zeros(n, m)
+    if float(C.min().item()) >= 0:
+        return DualPair.zeros(n, m)
+    return DualPair(D.to_np(0.5 * C.min(dim=1).values), D.to_np(0.5 * C.min(dim=0).values))
 
 
 def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     """Maximise the invariant dual at eps = 0 (src/fw.py:176-232)."""
     _check_problem(prob)
     n, m = len(prob.alpha), len(prob.beta)
-    d = init if init is not None else DualPair.zeros(n, m)
-    prob.check_pair(d)
     x, y = prob.alpha.points, prob.beta.points
-    p = prob.cost.p
-    viol = float(feasibility_violation(x, y, d.f, d.g, p)[0].item())
+    C = None
+    p = 2.0
+    if isinstance(prob.cost, ExplicitMatrix):
+        if prob.cost.matrix.shape != (n, m):
+            raise ValueError(f"explicit cost shape {prob.cost.matrix.shape} does not match "
+                             f"supports ({n}, {m})")
+        C = D.to_dev(prob.cost.matrix, D.torch().float64)
+    else:
+        p = prob.cost.p
+    d = init if init is not None else _default_init(prob, C)
+    prob.check_pair(d)
+    viol = float(feasibility_violation(x, y, d.f, d.g, p, C=C)[0].item())
     if viol > FEAS_TOL:
         raise InfeasibleDualError("initial pair violates f + g <= C")
+    if C is not None:  # the oracle's Monge check (src/ot1d.py:106, via _lmo)
+        check_submodular(prob.cost.matrix)
     if reference is not None and len(reference.f) != n:
         raise ValueError("reference potential does not match the problem")
     tic = time.perf_counter_ns()
     r = fw_solve_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.ent1.rho,
                          prob.ent2.rho, p, config.max_iters, config.step, config.gap_tol,
                          early_exit=True, f0=d.f, g0=d.g,
-                         ref_f=None if reference is None else reference.f)
+                         ref_f=None if reference is None else reference.f, C=C)
     st = int(r.status[0].item())
     if st == 1:
         raise MassBalanceError("reweighted marginal masses disagree; optimal translation looks broken")
@@ -181,7 +215,7 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     fin_f = D.to_np(r.f[0])
     fin_g = D.to_np(r.g[0])
     # feasibility of the untranslated iterate (f - lam, g + lam) (fw.py:238-240)
-    feas = float(feasibility_violation(x, y, fin_f - lam, fin_g + lam, p)[0].item())
+    feas = float(feasibility_violation(x, y, fin_f - lam, fin_g + lam, p, C=C)[0].item())
     cert = assemble_certificate(primal, dual, feas, config.gap_tol)
     trace = {"h0": h0, "fw_gap": fg, "pd_gap": pd,
              "wall_ns": np.full(its, wall, dtype=np.int64)}

@@ -72,10 +72,11 @@ class SparsePlan:
         return float(np.dot(self.mass, np.asarray(C)[self.source_idx, self.target_idx]))
 
 
-def solve_ot_1d_batched(x, y, a, b, p=2.0, stream=None):
+def solve_ot_1d_batched(x, y, a, b, p=2.0, stream=None, C=None):
     """Device batch: x, a [B, N], y, b [B, M] (sorted supports).  Returns
     (f, g, ei, ej, em, count, status) device tensors; entries of problem k
-    are ei[k, :count[k]] etc. in sweep order."""
+    are ei[k, :count[k]] etc. in sweep order.  ``C`` [B, N, M] (optional)
+    is an explicit Monge cost used instead of |x - y|^p."""
     t = D.torch()
     lib = _lib.load()
     x, y, a, b = (D.to_dev(v, t.float64) for v in (x, y, a, b))
@@ -90,12 +91,15 @@ def solve_ot_1d_batched(x, y, a, b, p=2.0, stream=None):
     em = D.empty((B, n + m - 1), t.float64)
     count = D.empty((B,), t.int32)
     status = D.empty((B,), t.int32)
+    if C is not None:
+        C = D.to_dev(C, t.float64).reshape(B, n, m).contiguous()
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_ot1d_workspace_size(B, n, m, ctypes.byref(size)))
     ws = D.workspace(size.value)
     _lib.check(lib.uot_ot1d_batched(
-        B, n, m, _lib.ptr(x), _lib.ptr(y), _lib.ptr(a), _lib.ptr(b), _lib.COST_POWER,
-        ctypes.c_double(p), None, _lib.ptr(f), _lib.ptr(g), _lib.ptr(ei), _lib.ptr(ej),
+        B, n, m, _lib.ptr(x), _lib.ptr(y), _lib.ptr(a), _lib.ptr(b),
+        _lib.COST_POWER if C is None else _lib.COST_EXPLICIT, ctypes.c_double(p),
+        None if C is None else _lib.ptr(C), _lib.ptr(f), _lib.ptr(g), _lib.ptr(ei), _lib.ptr(ej),
         _lib.ptr(em), _lib.ptr(count), _lib.ptr(status), _lib.ptr(ws),
         ctypes.c_size_t(size.value), _lib.stream_handle(stream)), "uot_ot1d_batched")
     return f, g, ei, ej, em, count, status
@@ -114,13 +118,13 @@ def solve_ot_1d(a, b, cost=PowerDistance(2.0)):
             raise ValueError(f"explicit cost shape {cost.matrix.shape} does not match supports "
                              f"({len(a)}, {len(b)})")
         check_submodular(cost.matrix)
-        from .exceptions import UnsupportedEntropyError
-
-        raise UnsupportedEntropyError("explicit costs are not on the B200 1-D oracle path")
-    if not isinstance(cost, PowerDistance):
+        f, g, ei, ej, em, count, status = solve_ot_1d_batched(
+            a.points, b.points, a.weights, b.weights, C=cost.matrix)
+    elif isinstance(cost, PowerDistance):
+        f, g, ei, ej, em, count, status = solve_ot_1d_batched(a.points, b.points, a.weights,
+                                                              b.weights, cost.p)
+    else:
         raise TypeError(f"unknown cost specification {cost!r}")
-    f, g, ei, ej, em, count, status = solve_ot_1d_batched(a.points, b.points, a.weights,
-                                                          b.weights, cost.p)
     if int(status[0].item()) != 0:
         raise MassBalanceError("balanced solver needs equal masses")
     k = int(count[0].item())

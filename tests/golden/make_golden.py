@@ -781,10 +781,130 @@ def gen_entropy_api():
     save("entropy_api.npz", **out)
 
 
+def _monge(rng, x, y, kind):
+    """Submodular (Monge) cost families for the ExplicitMatrix path."""
+    d = x[:, None] - y[None, :]
+    u = rng.normal(size=x.size)
+    v = rng.normal(size=y.size)
+    if kind == 0:  # convex |d|^1.5 plus separable terms
+        return np.abs(d) ** 1.5 + u[:, None] + v[None, :]
+    if kind == 1:  # -x y (submodular for sorted supports), negative entries
+        return -3.0 * x[:, None] * y[None, :] + 0.1 * u[:, None]
+    if kind == 2:  # barycentric two-marginal cost, tests/test_barycenter.py:68-80
+        return 0.3 * 0.7 * d ** 2
+    return d ** 2 - 0.5  # tests/test_fw.py:86-91 (negative entries)
+
+
+def gen_explicit():
+    """ExplicitMatrix costs through solve_ot_1d (src/ot1d.py:92-109) and
+    fw_solve (src/fw.py:151-232, :326-357 incl. the half-minima default
+    init for negative costs), from the reference."""
+    rng = np.random.default_rng(4242)
+    out = {}
+    ot_cases, fw_cases = [], []
+    k = 0
+    for kind in range(4):
+        for _ in range(6):
+            n, m = (int(v) for v in rng.integers(1, 40, 2))
+            x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+            wa = rng.uniform(0.0, 1.0, n)
+            if n > 3:
+                wa[1] = 0.0  # zero-weight atoms keep their recursion values
+            wb = rng.uniform(0.0, 1.0, m)
+            wb *= wa.sum() / wb.sum()
+            C = _monge(rng, x, y, kind)
+            plan, d = U.solve_ot_1d(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                                    U.ExplicitMatrix(C))
+            out[f"o{k}_x"], out[f"o{k}_y"], out[f"o{k}_a"], out[f"o{k}_b"] = x, y, wa, wb
+            out[f"o{k}_C"] = C
+            out[f"o{k}_i"], out[f"o{k}_j"], out[f"o{k}_m"] = (plan.source_idx, plan.target_idx,
+                                                              plan.mass)
+            out[f"o{k}_f"], out[f"o{k}_g"] = d.f, d.g
+            ot_cases.append(k)
+            k += 1
+    k = 0
+    for kind, step, iters in ((0, "linesearch", 60), (1, "harmonic", 80), (1, "linesearch", 60),
+                              (3, "harmonic", 50), (0, "pairwise", 40), (1, "pairwise", 40)):
+        n, m = int(rng.integers(20, 50)), int(rng.integers(20, 50))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa = rng.exponential(1.0, n)
+        wa *= rng.uniform(0.5, 2.0) / wa.sum()
+        wb = rng.exponential(1.0, m)
+        wb *= rng.uniform(0.5, 2.0) / wb.sum()
+        r1, r2 = float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.3, 2.0))
+        C = _monge(rng, x, y, kind)
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.ExplicitMatrix(C), U.KL(r1), U.KL(r2), eps=0.0)
+        d0 = UF._default_init(prob)
+        if step == "pairwise":
+            d, lam, plan, tr = ref_pfw(prob, iters)
+        else:
+            d, lam, plan, tr = ref_fw(prob, iters, step)
+        out[f"w{k}_x"], out[f"w{k}_y"], out[f"w{k}_a"], out[f"w{k}_b"] = x, y, wa, wb
+        out[f"w{k}_C"] = C
+        out[f"w{k}_par"] = np.array([r1, r2, iters, ["harmonic", "linesearch", "pairwise"].index(step)])
+        out[f"w{k}_f0"], out[f"w{k}_g0"] = d0.f, d0.g
+        out[f"w{k}_f"], out[f"w{k}_g"] = d.f + lam, d.g - lam
+        out[f"w{k}_i"], out[f"w{k}_j"], out[f"w{k}_m"] = plan.source_idx, plan.target_idx, plan.mass
+        for kk, v in tr.items():
+            out[f"w{k}_{kk}"] = v
+        fw_cases.append(k)
+        k += 1
+    # tests/test_fw.py:86-91 end to end: the reference's own fw_solve report
+    a4 = U.DiscreteMeasure(np.sort(rng.uniform(0, 1, 4)), rng.uniform(0.2, 1, 4))
+    b4 = U.DiscreteMeasure(np.sort(rng.uniform(0, 1, 4)), rng.uniform(0.2, 1, 4))
+    C4 = (a4.points[:, None] - b4.points[None, :]) ** 2 - 0.5
+    rep = U.fw_solve(U.UotProblem(a4, b4, U.ExplicitMatrix(C4), U.KL(1.0), U.KL(1.0), eps=0.0),
+                     U.FwConfig("linesearch", 2000, 1e-8))
+    out["e_x"], out["e_y"], out["e_a"], out["e_b"], out["e_C"] = (a4.points, b4.points,
+                                                                  a4.weights, b4.weights, C4)
+    out["e_f"], out["e_g"] = rep.final.f, rep.final.g
+    out["e_iters"] = np.array(rep.iterations)
+    out["e_passed"] = np.array(bool(rep.certificate.passed))
+    out["ot_cases"], out["fw_cases"] = np.array(ot_cases), np.array(fw_cases)
+    save("explicit.npz", **out)
+
+
+def gen_bary_api():
+    """The reference's own fw_barycenter report (src/barycenter.py:330-430):
+    pairwise (= the line-search branch, :397-407) and harmonic, with the
+    exhaustive feasibility term of the certificate (:416-418)."""
+    rng = np.random.default_rng(77)
+    out = {}
+    k = 0
+    for K, step, iters in ((3, "pairwise", 25), (3, "linesearch", 25), (2, "harmonic", 40),
+                           (4, "pairwise", 15)):
+        inputs = []
+        for _q in range(K):
+            n = int(rng.integers(6, 18))
+            wq = rng.uniform(0.05, 1.0, n)
+            wq *= rng.uniform(0.5, 2.0) / wq.sum()
+            inputs.append(U.DiscreteMeasure(np.sort(rng.uniform(0, 1, n)), wq))
+        w = rng.uniform(0.2, 1.0, K)
+        w /= w.sum()
+        rho = float(rng.uniform(0.5, 2.0))
+        rep, plan = U.fw_barycenter(U.BarycenterProblem(tuple(inputs), w, rho),
+                                    U.FwConfig(step, iters, 1e-9))
+        out[f"c{k}_k"] = np.array(K)
+        out[f"c{k}_w"] = w
+        out[f"c{k}_par"] = np.array([rho, iters, ["harmonic", "linesearch", "pairwise"].index(step)])
+        for q, mq in enumerate(inputs):
+            out[f"c{k}_x{q}"], out[f"c{k}_a{q}"] = mq.points, mq.weights
+            out[f"c{k}_f{q}"] = rep.final.potentials[q]
+        out[f"c{k}_h0"] = np.asarray(rep.trace["h0"])
+        out[f"c{k}_pd_gap"] = np.asarray(rep.trace["pd_gap"])
+        c = rep.certificate
+        out[f"c{k}_cert"] = np.array([c.primal, c.dual, c.gap, c.feasibility_violation, float(c.passed)])
+        out[f"c{k}_iters"] = np.array(rep.iterations)
+        k += 1
+    out["cases"] = np.arange(k)
+    save("bary_api.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -159,3 +159,30 @@ def test_mot_certificate_cfg5_scale():
     c = P.mot_certificate(inputs, w, plan, duals)
     assert c.passed
     assert abs(P.plan_cost(plan, inputs, P.barycentric_cost_fn(w)) - c.primal) < 1e-12
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_fw_barycenter_report_vs_reference(k):
+    """The reference's own fw_barycenter report (tests/golden/bary_api.npz):
+    early exit, the final translated potentials, the certificate including
+    its exhaustive feasibility term (src/barycenter.py:416-418); step
+    "pairwise" runs the line-search branch (:397-407)."""
+    z = golden("bary_api.npz")
+    inputs, kk = _inputs(z, k)
+    rho, iters, st = z[f"c{k}_par"]
+    step = ["harmonic", "linesearch", "pairwise"][int(st)]
+    problem = P.BarycenterProblem(tuple(inputs), z[f"c{k}_w"], float(rho))
+    rep, plan = P.fw_barycenter(problem, P.FwConfig(step, int(iters), 1e-9))
+    assert rep.iterations == int(z[f"c{k}_iters"])
+    ref_h0 = z[f"c{k}_h0"]
+    np.testing.assert_allclose(rep.trace["h0"], ref_h0, rtol=1e-9, atol=1e-13)
+    scale = max(np.abs(z[f"c{k}_f{q}"]).max() for q in range(kk))
+    tol = 1e-9 if step == "harmonic" else 1e-6
+    for q in range(kk):
+        assert np.abs(rep.final.potentials[q] - z[f"c{k}_f{q}"]).max() <= tol * scale
+    primal, dual, gap, feas, passed = z[f"c{k}_cert"]
+    c = rep.certificate
+    assert c.primal == pytest.approx(primal, rel=1e-9)
+    assert c.dual == pytest.approx(dual, rel=1e-9)
+    assert abs(c.feasibility_violation - feas) <= 1e-12
+    assert c.passed == bool(passed)

@@ -85,6 +85,20 @@ def test_ot1d_sweep_bit_exact():
         np.testing.assert_array_equal(g, z[f"c{k}_g"])
 
 
+
+def test_ot1d_explicit_cost_goldens():
+    """ExplicitMatrix costs (src/ot1d.py:100-107): the oracle's sweep with
+    C(i, j) looked up reproduces the reference bit for bit."""
+    z = golden("explicit.npz")
+    for k in z["ot_cases"]:
+        ii, jj, mm, f, g = O.solve_ot_1d(None, None, z[f"o{k}_a"], z[f"o{k}_b"],
+                                         explicit=z[f"o{k}_C"])
+        np.testing.assert_array_equal(ii, z[f"o{k}_i"])
+        np.testing.assert_array_equal(jj, z[f"o{k}_j"])
+        np.testing.assert_array_equal(mm, z[f"o{k}_m"])
+        np.testing.assert_array_equal(f, z[f"o{k}_f"])
+        np.testing.assert_array_equal(g, z[f"o{k}_g"])
+
 def test_ot1d_known_answer_two_by_two():
     # tests/test_ot1d.py:47-58 of the reference
     ii, jj, mm, f, g = O.solve_ot_1d([0.0, 1.0], [0.0, 1.0], [0.7, 0.3], [0.4, 0.6], 1.0)
