@@ -188,7 +188,7 @@ int uot_divergence(int32_t ent, double rho, int64_t n, const double* mu, const d
  *    -- src/duality.py:293-303 for KL/KL (lam = lambda*(f, g)).
  *  uot_eval_primal: out[0] = <plan, C> + eps KL(plan | a x b) + D1 + D2 over
  *    the plan entries (ii, jj, mass)[E] -- src/duality.py:306-344; cost from
- *    x, y, p (1-D power) or the dense C when non-NULL; KL / Balanced
+ *    x, y, p (1-D power) or the dense C when non-NULL; KL / Berg / Balanced
  *    divergences (UOT_ENT_*), +inf where the reference returns +inf.
  * ------------------------------------------------------------------------ */
 int uot_cost_matrix(int32_t n, int32_t m, const double* x, const double* y, double p, double* C,
@@ -240,6 +240,12 @@ int uot_ot1d_batched(int32_t batch, int32_t n, int32_t m, const double* x, const
  * workspace; natoms (optional [batch][max_iters]) receives the active atom
  * count after each iteration and step_size the weight transferred.
  * n, m <= 4096 per problem (one CTA per problem, state resident on chip).
+ * A Berg penalty on either side (ent1 / ent2 = UOT_ENT_BERG, src/fw.py:98-103)
+ * runs the generic path (csrc/fw1d_generic.cu): per iteration the bracketed
+ * Newton translation (src/duality.py:182-247), the oracle and a ternary line
+ * search whose every value solves its own translation (fw.py:106-148);
+ * harmonic / line search steps; the call synchronises the stream every 16
+ * iterations to test the early exit.  status 3 = NewtonError.
  * ------------------------------------------------------------------------ */
 typedef struct uot_fw_desc {
   int32_t batch, n, m;
@@ -270,6 +276,7 @@ typedef struct uot_fw_desc {
   const double* ref_f; /* optional [batch][n]: reference potential (src/fw.py:217-219) */
   double* err_f;       /* optional [batch][max_iters]: ||f_t + lambda*_t - ref_f||_inf */
   const double* c;     /* optional [batch][n][m]: explicit cost (else |x - y|^p) */
+  int32_t ent1, ent2;  /* UOT_ENT_KL (0, default) or UOT_ENT_BERG per marginal */
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);
@@ -280,6 +287,18 @@ int uot_fw1d_run(const uot_fw_desc* desc, void* workspace, size_t workspace_byte
  * out [batch] fp64. */
 int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
                        double p, const double* f, const double* g, double* out, void* stream);
+/* Optimal translation lambda* of (f, g) for KL / Berg penalties by the
+ * bracketed Newton of src/duality.py:182-247 started at lam0 (solve != 0), or
+ * lambda = lam0 given (solve == 0, e.g. eval_G / eval_F).  Optional outputs:
+ * lam [batch]; ta, tb [batch][n|m] = weights * conj_grad(-f - lam | -g + lam)
+ * (updated_marginals, :293-303); h [batch] = <a, -phi1*(-(f + lam))> +
+ * <b, -phi2*(-(g - lam))> (_h0, src/fw.py:111-115; src/duality.py:102-114,
+ * Balanced allowed when solve == 0); status [batch]: 0, 1 = empty Berg
+ * domain, 2 = no bracket, 3 = no convergence (NewtonError). */
+int uot_translation(int32_t batch, int32_t n, int32_t m, const double* a, const double* b,
+                    const double* f, const double* g, int32_t ent1, int32_t ent2, double rho1,
+                    double rho2, int32_t solve, double lam0, double* lam, double* ta, double* tb,
+                    double* h, int32_t* status, void* stream);
 /* The same for explicit costs C [batch][n][m] (ExplicitMatrix). */
 int uot_feasibility_explicit(int32_t batch, int32_t n, int32_t m, const double* C,
                              const double* f, const double* g, double* out, void* stream);

@@ -50,6 +50,7 @@ class FwDesc(ctypes.Structure):
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),
         ("ei", _vp), ("ej", _vp), ("em", _vp), ("count", _vp), ("summary", _vp),
         ("status", _vp), ("step_size", _vp), ("natoms", _vp), ("ref_f", _vp), ("err_f", _vp), ("c", _vp),
+        ("ent1", _i32), ("ent2", _i32),
     ]
 
 
@@ -72,7 +73,7 @@ EXPORTS = (
     "uot_cost_matrix", "uot_cost_quadruple_diameter", "uot_updated_marginals", "uot_eval_primal",
     "uot_logdotexp", "uot_entropy_map", "uot_divergence",
     "uot_ot1d_workspace_size", "uot_ot1d_batched", "uot_fw1d_workspace_size", "uot_fw1d_run", "uot_feasibility_1d",
-    "uot_feasibility_explicit",
+    "uot_feasibility_explicit", "uot_translation",
     "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_mot_certify", "uot_bary_workspace_size", "uot_bary_run",
     "uot_nccl_unique_id", "uot_nccl_comm_init", "uot_nccl_comm_destroy",
 )
@@ -98,6 +99,9 @@ def load(require_gpu=True):
                                           _vp, ctypes.c_size_t, _vp]
         lib.uot_anderson_weights.argtypes = [_i32, _i32, _vp, _f64, _vp, _vp, _vp]
         lib.uot_cost_matrix.argtypes = [_i32, _i32, _vp, _vp, _f64, _vp, _vp]
+        lib.uot_translation.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f64,
+                                        _f64, _i32, _f64, _vp, _vp, _vp, _vp, _vp, _vp]
+        lib.uot_feasibility_explicit.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]
         lib.uot_cost_quadruple_diameter.argtypes = [_i32, _i32, _vp, _vp, _vp]
         lib.uot_updated_marginals.argtypes = [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _f64, _f64,
                                               _vp, _vp, _vp]

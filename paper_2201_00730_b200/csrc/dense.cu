@@ -63,14 +63,17 @@ __global__ void updated_marginals_kernel(int n, int m, const double* __restrict_
 // One side's divergence terms for index range [lo, hi) with marginals from
 // the plan entries (every entry scanned per index: deterministic, general
 // plans).  KL: sum_{w>0} [mu log(mu/w) - mu + w], singular mass -> inf;
-// Balanced: max |mu - w| (the caller applies the 1e-9 tolerance).
+// Berg: sum_{w>0} [mu - w - w log(mu/w)] + singular mass, inf at mu = 0 < w
+// (src/entropies.py:132-137); Balanced: max |mu - w| (the caller applies the
+// 1e-9 tolerance).
 struct SideAcc {
-  double terms, sing, maxdiff, maxw;
+  double terms, sing, maxdiff, maxw, inf;
 };
 
 __device__ SideAcc side_terms(int count, const double* w, int E, const int64_t* idx,
-                              const double* mass, bool balanced) {
-  SideAcc s{0.0, 0.0, 0.0, 0.0};
+                              const double* mass, int ent) {
+  const bool balanced = ent == UOT_ENT_BALANCED;
+  SideAcc s{0.0, 0.0, 0.0, 0.0, 0.0};
   for (int i = threadIdx.x; i < count; i += blockDim.x) {
     double mu = 0.0;
     for (int e = 0; e < E; ++e)
@@ -79,6 +82,11 @@ __device__ SideAcc side_terms(int count, const double* w, int E, const int64_t* 
     if (balanced) {
       s.maxdiff = fmax(s.maxdiff, fabs(mu - wi));
       s.maxw = fmax(s.maxw, fabs(wi));
+    } else if (wi > 0.0 && ent == UOT_ENT_BERG) {
+      if (mu == 0.0)
+        s.inf = 1.0;
+      else
+        s.terms += mu - wi - wi * log(mu / wi);
     } else if (wi > 0.0) {
       s.terms += (mu > 0.0 ? mu * log(mu / wi) : 0.0) - mu + wi;
     } else {
@@ -110,8 +118,8 @@ __global__ void __launch_bounds__(1024)
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) ma += a[i];
   for (int j = threadIdx.x; j < m; j += blockDim.x) mb += b[j];
-  const SideAcc s1 = side_terms(n, a, E, ii, mass, ent1 == UOT_ENT_BALANCED);
-  const SideAcc s2 = side_terms(m, b, E, jj, mass, ent2 == UOT_ENT_BALANCED);
+  const SideAcc s1 = side_terms(n, a, E, ii, mass, ent1);
+  const SideAcc s2 = side_terms(m, b, E, jj, mass, ent2);
   cost = block_reduce(cost, scratch, SumOp(), 0.0);
   klp = block_reduce(klp, scratch, SumOp(), 0.0);
   qbad = block_reduce(qbad, scratch, MaxOp(), 0.0);
@@ -125,13 +133,16 @@ __global__ void __launch_bounds__(1024)
   const double g2 = block_reduce(s2.sing, scratch, SumOp(), 0.0);
   const double d2 = block_reduce(s2.maxdiff, scratch, MaxOp(), 0.0);
   const double w2 = block_reduce(s2.maxw, scratch, MaxOp(), 0.0);
+  const double i1 = block_reduce(s1.inf, scratch, MaxOp(), 0.0);
+  const double i2 = block_reduce(s2.inf, scratch, MaxOp(), 0.0);
   if (threadIdx.x != 0) return;
-  auto div = [](int ent, double rho, double t, double sing, double md, double mw) {
+  auto div = [](int ent, double rho, double t, double sing, double md, double mw, double inf) {
     if (ent == UOT_ENT_BALANCED) return md <= 1e-9 * (1.0 + mw) ? 0.0 : CUDART_INF;  // :119-121
+    if (ent == UOT_ENT_BERG) return inf > 0.0 ? CUDART_INF : rho * (t + sing);
     if (sing > 0.0) return CUDART_INF;
     return rho * t;
   };
-  double total = cost + div(ent1, rho1, t1, g1, d1, w1) + div(ent2, rho2, t2, g2, d2, w2);
+  double total = cost + div(ent1, rho1, t1, g1, d1, w1, i1) + div(ent2, rho2, t2, g2, d2, w2, i2);
   if (eps > 0.0) total += qbad > 0.0 ? CUDART_INF : eps * (klp + ma * mb);
   out[0] = total;
 }
@@ -189,10 +200,6 @@ extern "C" int uot_eval_primal(int32_t n, int32_t m, const double* x, const doub
   if (n < 1 || m < 1 || E < 0 || out == nullptr || (C == nullptr && (x == nullptr || y == nullptr))) {
     set_error("eval_primal: invalid arguments");
     return UOT_INVALID;
-  }
-  if (ent1 == UOT_ENT_BERG || ent2 == UOT_ENT_BERG) {
-    set_error("eval_primal: the Berg divergence is not on the B200 path");
-    return UOT_UNSUPPORTED_ENTROPY;
   }
   eval_primal_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n, m, x, y, p, C, a, b, E, ii, jj, mass,
                                                            ent1, ent2, rho1, rho2, eps, out);

@@ -49,13 +49,23 @@ size_t pfw_store_bytes(int batch, int n, int m, int max_iters) {
          (3 * sizeof(double) + sizeof(int)) * (size_t)batch * cap + 1024;
 }
 
+bool generic_entropies(const uot_fw_desc* d) {
+  return d->ent1 != UOT_ENT_KL || d->ent2 != UOT_ENT_KL;
+}
+
 size_t fw_ws_bytes(const uot_fw_desc* d) {
+  if (generic_entropies(d)) return fwk::generic_ws_bytes(d->batch, d->n, d->m);
   size_t b = fw_scratch_bytes(d->batch, d->n, d->m);
   if (d->step == UOT_STEP_PAIRWISE) b += pfw_store_bytes(d->batch, d->n, d->m, d->max_iters);
   return b;
 }
 
 }  // namespace
+
+namespace fwk {
+int launch_fw_ot(const FwArgs& a, int batch, cudaStream_t st) { return launch_fw(a, batch, st); }
+size_t ot_scratch_bytes(int batch, int n, int m) { return fw_scratch_bytes(batch, n, m); }
+}  // namespace fwk
 }  // namespace uot
 
 using namespace uot;
@@ -82,6 +92,18 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
       d->step != UOT_STEP_PAIRWISE) {
     set_error("uot_fw1d_run: step must be harmonic, linesearch or pairwise");
     return UOT_INVALID;
+  }
+  const bool gen = generic_entropies(d);
+  if (gen) {  // fw.py:98-103: KL or Berg on each side
+    if ((d->ent1 != UOT_ENT_KL && d->ent1 != UOT_ENT_BERG) ||
+        (d->ent2 != UOT_ENT_KL && d->ent2 != UOT_ENT_BERG)) {
+      set_error("frank-wolfe needs strictly convex conjugates (KL or Berg)");
+      return UOT_UNSUPPORTED_ENTROPY;
+    }
+    if (d->step == UOT_STEP_PAIRWISE) {
+      set_error("uot_fw1d_run: pairwise FW runs KL/KL penalties on the B200 path");
+      return UOT_UNSUPPORTED_ENTROPY;
+    }
   }
   if (ws_bytes < fw_ws_bytes(d)) {
     set_error("uot_fw1d_run: workspace too small");
@@ -121,6 +143,8 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.ref_f = d->ref_f;
   a.err_f = d->err_f;
   a.C = d->c;
+  if (gen) return fwk::run_fw_generic(a, d->batch, d->ent1, d->ent2, ws, ws_bytes,
+                                     (cudaStream_t)stream);
   if (d->step == UOT_STEP_PAIRWISE) {
     const size_t cap = (size_t)d->max_iters + 1;
     const size_t bc = (size_t)d->batch * cap;

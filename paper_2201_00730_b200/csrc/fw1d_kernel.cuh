@@ -965,6 +965,10 @@ int launch_fw_impl(const FwArgs& a, int batch, cudaStream_t st) {
 // the pairwise branch otherwise raises register pressure / spills of the
 // FW and OT kernels)
 int launch_fw_pairwise(const FwArgs& a, int batch, cudaStream_t st);
+// non-KL penalties (fw1d_generic.cu)
+size_t generic_ws_bytes(int batch, int n, int m);
+int run_fw_generic(const FwArgs& a, int batch, int e1, int e2, void* ws, size_t ws_bytes,
+                   cudaStream_t st);
 
 }  // namespace fwk
 }  // namespace uot

@@ -13,8 +13,8 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .entropies import KL, Berg, require_kl
-from .exceptions import UnsupportedEntropyError
+from .entropies import KL, Balanced, Berg, ent_code, ent_rho, require_kl
+from .exceptions import NewtonError, UnsupportedEntropyError
 from .measures import DiscreteMeasure
 
 
@@ -81,17 +81,56 @@ def _strictly_convex(spec):
     return isinstance(spec, (KL, Berg))
 
 
+_NEWTON_MSG = {1: "empty translation domain for Berg conjugates",
+               2: "failed to bracket the optimal translation",
+               3: "translation Newton did not reach the residual target"}
+
+
+def translation(prob, f, g, solve=True, lam0=0.0, marginals=False, value=False):
+    """One ``uot_translation`` launch: the bracketed-Newton translation of
+    (f, g) (src/duality.py:182-247) from ``lam0`` (or lam0 itself with
+    ``solve=False``), optionally the updated marginals (:293-303) and the
+    value <a, -phi1*(-(f + lam))> + <b, -phi2*(-(g - lam))> (:102-114).
+    Returns (lam, ta, tb, h) with device tensors / None; raises NewtonError
+    like the reference."""
+    t = D.torch()
+    lib = _lib.load()
+    n, m = len(prob.alpha), len(prob.beta)
+    a, b, fd, gd = (D.to_dev(v, t.float64) for v in (prob.alpha.weights, prob.beta.weights, f, g))
+    lam = D.empty((1,), t.float64)
+    st = D.empty((1,), t.int32)
+    ta = D.empty((n,), t.float64) if marginals else None
+    tb = D.empty((m,), t.float64) if marginals else None
+    h = D.empty((1,), t.float64) if value else None
+    _lib.check(lib.uot_translation(1, n, m, _lib.ptr(a), _lib.ptr(b), _lib.ptr(fd), _lib.ptr(gd),
+                                   ent_code(prob.ent1), ent_code(prob.ent2), ent_rho(prob.ent1),
+                                   ent_rho(prob.ent2), 1 if solve else 0, float(lam0),
+                                   _lib.ptr(lam), _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(h),
+                                   _lib.ptr(st), _lib.stream_handle()), "uot_translation")
+    code = int(st[0].item())
+    if code:
+        raise NewtonError(_NEWTON_MSG[code])
+    return float(lam[0].item()), ta, tb, h
+
+
+def _both_kl(prob):
+    return isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)
+
+
 def lambda_star(prob, d, tol=1e-11, max_iters=100, initial=0.0):
     """Optimal translation t* maximising G(f + t, g - t) (src/duality.py:160-179).
 
     KL/KL has the closed form rho1 rho2/(rho1+rho2) (LSE_a(-f/rho1) -
-    LSE_b(-g/rho2)), evaluated on the GPU.  Balanced is rejected like the
-    reference; Berg (Newton branch, :182-247) is not on the B200 path."""
+    LSE_b(-g/rho2)), evaluated on the GPU; KL/Berg mixes and Berg/Berg run the
+    reference's bracketed Newton (:182-247) in ``uot_translation`` (tolerance
+    1e-11, 100 Newton steps: the reference defaults).  Balanced is rejected
+    like the reference."""
     prob.check_pair(d)
     if not (_strictly_convex(prob.ent1) and _strictly_convex(prob.ent2)):
         raise UnsupportedEntropyError(
             "optimal translation needs strictly convex conjugates (KL or Berg)")
-    require_kl(prob.ent1, prob.ent2, what="lambda_star")
+    if not _both_kl(prob):
+        return translation(prob, d.f, d.g, True, initial)[0]
     out = kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.ent1.rho, prob.ent2.rho)
     return float(out[0, 0].item())
 
@@ -118,11 +157,14 @@ def _kl_parts(prob, sf, sg):
 
 def dual_feasibility_violation(prob, d):
     """max(0, max_ij f_i + g_j - C_ij) (duality.py:117-121) on the device
-    (1-D |x - y|^p costs)."""
+    (1-D |x - y|^p costs and explicit matrices)."""
     from .fw import feasibility_violation
-    from .measures import PowerDistance
+    from .measures import ExplicitMatrix, PowerDistance
 
     prob.check_pair(d)
+    if isinstance(prob.cost, ExplicitMatrix):
+        return float(feasibility_violation(prob.alpha.points, prob.beta.points, d.f, d.g,
+                                           C=prob.cost.matrix)[0].item())
     if not isinstance(prob.cost, PowerDistance):
         raise UnsupportedEntropyError("the device feasibility check runs 1-D |x - y|^p costs")
     return float(feasibility_violation(prob.alpha.points, prob.beta.points, d.f, d.g,
@@ -131,17 +173,45 @@ def dual_feasibility_violation(prob, d):
 
 def _eps_term(prob, d):
     """eps (<a x b, e^((f+g-C)/eps)> - m_a m_b) (duality.py:124-132)."""
-    from .sinkhorn import _verify_prob
+    from .sinkhorn import _step_inputs, _verify_prob, verify_batched
 
-    v = _verify_prob(prob, d)
+    if _both_kl(prob):
+        v = _verify_prob(prob, d)
+    else:  # the log-partition column does not depend on the penalties
+        costname, p, x, y, C = _step_inputs(prob)
+        v = D.to_np(verify_batched(x, y, prob.alpha.weights, prob.beta.weights, d.f, d.g,
+                                   prob.eps, 1.0, 1.0, cost=costname, p=p, c=C)[0],
+                    readonly=False)
     ma, mb = float(np.sum(prob.alpha.weights)), float(np.sum(prob.beta.weights))
     return prob.eps * (math.exp(v[1]) - ma * mb), v
 
 
+def _check_feasible(prob, d):
+    if prob.eps == 0:
+        from .exceptions import InfeasibleDualError
+
+        viol = dual_feasibility_violation(prob, d)
+        if viol > DUAL_FEAS_TOL:
+            raise InfeasibleDualError(f"dual constraint violated by {viol:.3e} at eps = 0")
+
+
+def _eval_f_generic(prob, d):
+    """<a, -phi1*(-f)> + <b, -phi2*(-g)> (- the eps term) for any penalties
+    (duality.py:135-152), the sums in uot_translation at lam = 0."""
+    _check_feasible(prob, d)
+    h = translation(prob, d.f, d.g, solve=False, lam0=0.0, value=True)[3]
+    total = float(h[0].item())
+    if prob.eps > 0:
+        total -= _eps_term(prob, d)[0]
+    return total
+
+
 def eval_F(prob, d):
-    """Plain dual objective (duality.py:135-152), KL marginals."""
+    """Plain dual objective (duality.py:135-152); KL/KL through the LSE
+    kernels, other penalties through the uot_translation sums."""
     prob.check_pair(d)
-    require_kl(prob.ent1, prob.ent2, what="eval_F")
+    if not _both_kl(prob):
+        return _eval_f_generic(prob, d)
     if prob.eps == 0:
         from .exceptions import InfeasibleDualError
 
@@ -163,9 +233,13 @@ def eval_G(prob, d, lam):
 
 
 def eval_H(prob, d):
-    """Translation-invariant dual (duality.py:256-276), KL closed form."""
+    """Translation-invariant dual (duality.py:256-276): KL closed form,
+    eval_F for Balanced/Balanced, else eval_G at the Newton translation."""
     prob.check_pair(d)
-    require_kl(prob.ent1, prob.ent2, what="eval_H")
+    if isinstance(prob.ent1, Balanced) and isinstance(prob.ent2, Balanced):
+        return eval_F(prob, d)  # every translation gives the same value (:264-265)
+    if not _both_kl(prob):
+        return eval_G(prob, d, lambda_star(prob, d))  # :275-276
     if prob.eps == 0:
         from .exceptions import InfeasibleDualError
 
@@ -191,7 +265,12 @@ def updated_marginals(prob, d):
     """Reweighted marginals at the optimal translation (src/duality.py:293-303):
     (a exp((-f - t*)/rho1), b exp((-g + t*)/rho2)) for KL/KL, on the device."""
     prob.check_pair(d)
-    require_kl(prob.ent1, prob.ent2, what="updated_marginals")
+    if not _both_kl(prob):
+        if not (_strictly_convex(prob.ent1) and _strictly_convex(prob.ent2)):
+            raise UnsupportedEntropyError(
+                "optimal translation needs strictly convex conjugates (KL or Berg)")
+        _, ta, tb, _ = translation(prob, d.f, d.g, marginals=True)
+        return D.to_np(ta, readonly=False), D.to_np(tb, readonly=False)
     t = D.torch()
     lib = _lib.load()
     n, m = len(prob.alpha), len(prob.beta)
@@ -234,8 +313,10 @@ def eval_primal(prob, plan):
             codes.append((_lib.ENT_KL, float(spec.rho)))
         elif isinstance(spec, Balanced):
             codes.append((_lib.ENT_BALANCED, 0.0))
+        elif isinstance(spec, Berg):
+            codes.append((_lib.ENT_BERG, float(spec.rho)))
         else:
-            raise UnsupportedEntropyError("eval_primal runs KL / Balanced divergences on the B200 path")
+            raise UnsupportedEntropyError(f"unknown entropy {spec!r}")
     t = D.torch()
     lib = _lib.load()
     x = y = C = None

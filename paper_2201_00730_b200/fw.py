@@ -20,8 +20,9 @@ from . import _device as D
 from . import _lib
 from .certify import assemble_certificate
 from .duality import DualPair
-from .entropies import KL, Berg, require_kl
-from .exceptions import InfeasibleDualError, MassBalanceError, UnsupportedEntropyError
+from .entropies import KL, Berg
+from .exceptions import (InfeasibleDualError, MassBalanceError, NewtonError,
+                         UnsupportedEntropyError)
 from .measures import ExplicitMatrix, PowerDistance, check_submodular
 from .ot1d import SparsePlan
 from .sinkhorn import SolverReport
@@ -70,9 +71,11 @@ class FwBatchResult:
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
                      gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None, ref_f=None,
-                     C=None):
+                     C=None, ent1="kl", ent2="kl"):
     """Batched FW on device: x, a [B, N]; y, b [B, M] sorted supports;
-    ``C`` [B, N, M] (optional) an explicit Monge cost instead of |x - y|^p.
+    ``C`` [B, N, M] (optional) an explicit Monge cost instead of |x - y|^p;
+    ``ent1`` / ``ent2`` "kl" or "berg" (Berg runs the generic path,
+    csrc/fw1d_generic.cu).
 
     ``early_exit=False`` runs exactly ``max_iters`` iterations per problem
     (BASELINE fixed-iteration configs); True applies fw.py:220-222 per
@@ -120,6 +123,8 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
     if C is not None:
         r.cost = D.to_dev(C, t.float64).reshape(B, n, m).contiguous()
         desc.c = _lib.ptr(r.cost)
+    codes = {"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG}
+    desc.ent1, desc.ent2 = codes[ent1], codes[ent2]
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)
@@ -155,8 +160,6 @@ def _check_problem(prob):
     for spec in (prob.ent1, prob.ent2):
         if not isinstance(spec, (KL, Berg)):
             raise UnsupportedEntropyError("frank-wolfe needs strictly convex conjugates (KL or Berg)")
-        if not isinstance(spec, KL):
-            raise UnsupportedEntropyError("the B200 FW path runs KL penalties")
     if not isinstance(prob.cost, (PowerDistance, ExplicitMatrix)):
         raise TypeError(f"unknown cost specification {prob.cost!r}")
 
@@ -175,6 +178,9 @@ def _default_init(prob, C):
 def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     """Maximise the invariant dual at eps = 0 (src/fw.py:176-232)."""
     _check_problem(prob)
+    kl = isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)
+    if config.step == "pairwise" and not kl:
+        raise UnsupportedEntropyError("pairwise FW runs KL/KL penalties on the B200 path")
     n, m = len(prob.alpha), len(prob.beta)
     x, y = prob.alpha.points, prob.beta.points
     C = None
@@ -199,10 +205,14 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     r = fw_solve_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.ent1.rho,
                          prob.ent2.rho, p, config.max_iters, config.step, config.gap_tol,
                          early_exit=True, f0=d.f, g0=d.g,
-                         ref_f=None if reference is None else reference.f, C=C)
+                         ref_f=None if reference is None else reference.f, C=C,
+                         ent1="kl" if isinstance(prob.ent1, KL) else "berg",
+                         ent2="kl" if isinstance(prob.ent2, KL) else "berg")
     st = int(r.status[0].item())
     if st == 1:
         raise MassBalanceError("reweighted marginal masses disagree; optimal translation looks broken")
+    if st == 3:
+        raise NewtonError("translation Newton did not reach the residual target")
     its = int(r.iterations[0].item())
     wall = (time.perf_counter_ns() - tic) // max(its, 1)
     h0 = D.to_np(r.h0[0, :its], readonly=False)
@@ -256,16 +266,21 @@ def ternary_max(fn, lo=0.0, hi=1.0, iters=60):
 
 
 def _h0_value(prob, f, g):
-    from .duality import kl_scalars
+    """_h0 (src/fw.py:106-115): KL closed form, else the translated sums."""
+    from .duality import kl_scalars, translation
 
-    return float(kl_scalars(prob.alpha.weights, prob.beta.weights, f, g, prob.ent1.rho,
-                            prob.ent2.rho)[0, 1].item())
+    if isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL):
+        return float(kl_scalars(prob.alpha.weights, prob.beta.weights, f, g, prob.ent1.rho,
+                                prob.ent2.rho)[0, 1].item())
+    return float(translation(prob, f, g, value=True)[3][0].item())
 
 
 def line_search_h0(prob, current, target):
     """Step in [0, 1] maximising H0 on the segment: 60 ternary steps and an
     endpoint comparison (:131-148); every H0 value on the device."""
-    require_kl(prob.ent1, prob.ent2, what="line_search_h0")
+    for spec in (prob.ent1, prob.ent2):
+        if not isinstance(spec, (KL, Berg)):
+            raise UnsupportedEntropyError("frank-wolfe needs strictly convex conjugates (KL or Berg)")
 
     def value(gamma):
         return _h0_value(prob, (1.0 - gamma) * current.f + gamma * target.f,

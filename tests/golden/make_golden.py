@@ -901,10 +901,91 @@ def gen_bary_api():
     save("bary_api.npz", **out)
 
 
+def gen_berg():
+    """Berg / mixed penalties off the KL closed form: the bracketed-Newton
+    translation, updated marginals, F / G / H values, the primal with the
+    Berg divergence (src/duality.py:135-303, src/entropies.py:104-138) and
+    fixed-iteration FW runs (src/fw.py:106-232), from the reference."""
+    from uotkit import duality as UD
+
+    rng = np.random.default_rng(9001)
+    out = {}
+    specs = [(U.Berg(1.0), U.Berg(1.0)), (U.KL(0.8), U.Berg(1.4)), (U.Berg(0.6), U.KL(1.3)),
+             (U.Berg(2.5), U.Berg(0.4))]
+    for k, (e1, e2) in enumerate(specs):
+        n, m = int(rng.integers(4, 30)), int(rng.integers(4, 30))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa, wb = rng.uniform(0.0, 1.0, n), rng.uniform(0.0, 1.0, m)
+        wa[0] = 0.0
+        f, g = rng.uniform(-0.3, 0.3, n), rng.uniform(-0.3, 0.3, m)
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(2.0), e1, e2, eps=0.0)
+        d = U.DualPair(f, g)
+        out[f"d{k}_x"], out[f"d{k}_y"], out[f"d{k}_a"], out[f"d{k}_b"] = x, y, wa, wb
+        out[f"d{k}_f"], out[f"d{k}_g"] = f, g
+        out[f"d{k}_ent"] = np.array([0 if isinstance(e1, U.KL) else 1, e1.rho,
+                                     0 if isinstance(e2, U.KL) else 1, e2.rho])
+        lam = U.lambda_star(prob, d)
+        out[f"d{k}_lam"] = np.array(lam)
+        ta, tb = U.updated_marginals(prob, d)
+        out[f"d{k}_ta"], out[f"d{k}_tb"] = ta, tb
+        # F / G / H at eps = 0 on a feasible pair, and F at eps > 0
+        C = np.abs(x[:, None] - y[None, :]) ** 2
+        fs = np.minimum(f, (C - g[None, :]).min(axis=1))
+        dfs = U.DualPair(fs, g)
+        out[f"d{k}_fs"] = fs
+        out[f"d{k}_F"] = np.array(UD.eval_F(prob, dfs))
+        out[f"d{k}_G"] = np.array(UD.eval_G(prob, dfs, 0.07))
+        out[f"d{k}_H"] = np.array(UD.eval_H(prob, dfs))
+        pe = U.UotProblem(prob.alpha, prob.beta, prob.cost, e1, e2, eps=0.3)
+        out[f"d{k}_Feps"] = np.array(UD.eval_F(pe, d))
+        # primal of a plan with full support on the positive-weight atoms
+        plan, _ = U.solve_ot_1d(U.DiscreteMeasure(x, ta), U.DiscreteMeasure(y, tb))
+        out[f"d{k}_pi"], out[f"d{k}_pj"], out[f"d{k}_pm"] = (plan.source_idx, plan.target_idx,
+                                                             plan.mass)
+        out[f"d{k}_primal"] = np.array(U.eval_primal(prob, plan))
+        out[f"d{k}_primal_eps"] = np.array(U.eval_primal(pe, plan))
+    fw_specs = [(U.Berg(1.0), U.Berg(1.0), "linesearch", 40), (U.KL(0.8), U.Berg(1.4), "harmonic", 60),
+                (U.Berg(0.7), U.KL(1.1), "linesearch", 40), (U.Berg(1.5), U.Berg(0.5), "harmonic", 50)]
+    for k, (e1, e2, step, iters) in enumerate(fw_specs):
+        n, m = int(rng.integers(15, 45)), int(rng.integers(15, 45))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa = rng.exponential(1.0, n)
+        wa *= rng.uniform(0.5, 2.0) / wa.sum()
+        wb = rng.exponential(1.0, m)
+        wb *= rng.uniform(0.5, 2.0) / wb.sum()
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(2.0), e1, e2, eps=0.0)
+        dd, lam, plan, tr = ref_fw(prob, iters, step)
+        out[f"w{k}_x"], out[f"w{k}_y"], out[f"w{k}_a"], out[f"w{k}_b"] = x, y, wa, wb
+        out[f"w{k}_par"] = np.array([0 if isinstance(e1, U.KL) else 1, e1.rho,
+                                     0 if isinstance(e2, U.KL) else 1, e2.rho, iters,
+                                     1.0 if step == "linesearch" else 0.0])
+        out[f"w{k}_f"], out[f"w{k}_g"] = dd.f + lam, dd.g - lam
+        out[f"w{k}_i"], out[f"w{k}_j"], out[f"w{k}_m"] = plan.source_idx, plan.target_idx, plan.mass
+        for kk, v in tr.items():
+            out[f"w{k}_{kk}"] = v
+    # tests/test_fw.py:121-125: the reference's own report on a Berg instance
+    xa, xb = np.sort(rng.uniform(0, 1, 10)), np.sort(rng.uniform(0, 1, 9))
+    wa = rng.uniform(0.2, 1.0, 10)
+    wb = rng.uniform(0.2, 1.0, 9)
+    wb *= wa.sum() / wb.sum()
+    prob = U.UotProblem(U.DiscreteMeasure(xa, wa), U.DiscreteMeasure(xb, wb),
+                        U.PowerDistance(2.0), U.Berg(1.0), U.Berg(1.0), eps=0.0)
+    rep = U.fw_solve(prob, U.FwConfig("linesearch", 3000, 1e-7))
+    out["e_x"], out["e_y"], out["e_a"], out["e_b"] = xa, xb, wa, wb
+    out["e_f"], out["e_g"] = rep.final.f, rep.final.g
+    out["e_iters"] = np.array(rep.iterations)
+    out["e_h0"] = np.asarray(rep.trace["h0"])
+    out["e_passed"] = np.array(bool(rep.certificate.passed))
+    out["d_cases"], out["w_cases"] = np.arange(len(specs)), np.arange(len(fw_specs))
+    save("berg.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()
