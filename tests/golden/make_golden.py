@@ -982,10 +982,42 @@ def gen_berg():
     save("berg.npz", **out)
 
 
+def gen_sk_trace():
+    """run(prob, config, reference=...) error traces for penalties off the
+    KL closed form (src/sinkhorn.py:246-315): F with Berg / Balanced (no
+    translation) and G with a Berg marginal (Newton translation)."""
+    rng = np.random.default_rng(606)
+    out = {}
+    specs = [("f", U.Berg(1.0), U.Berg(0.7)), ("f", U.KL(0.9), U.Balanced()),
+             ("g", U.KL(0.8), U.Berg(1.2)), ("g", U.Berg(1.5), U.Berg(0.6))]
+    for k, (variant, e1, e2) in enumerate(specs):
+        n, m = int(rng.integers(8, 30)), int(rng.integers(8, 30))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m)
+        if isinstance(e2, U.Balanced):
+            wb *= wa.sum() / wb.sum()
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(2.0), e1, e2, eps=0.2)
+        ref = US.run(prob, U.SinkhornConfig("f", 20000, 1e-13)).final
+        rep = US.run(prob, U.SinkhornConfig(variant, 25, 1e-15), reference=ref)
+        code = {U.KL: 0, U.Berg: 1, U.Balanced: 2}
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([0 if variant == "f" else 1, code[type(e1)],
+                                     getattr(e1, "rho", 1.0), code[type(e2)],
+                                     getattr(e2, "rho", 1.0)])
+        out[f"c{k}_ref_f"], out[f"c{k}_ref_g"] = ref.f, ref.g
+        for key in ("delta_f", "err_f", "err_g"):
+            out[f"c{k}_{key}"] = np.asarray(rep.trace[key])
+        out[f"c{k}_f"], out[f"c{k}_g"] = rep.final.f, rep.final.g
+    out["cases"] = np.arange(len(specs))
+    save("sk_trace.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()
