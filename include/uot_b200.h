@@ -106,6 +106,8 @@ typedef struct uot_sinkhorn_desc {
   int32_t nranks, rank;
   const int32_t* shard_rows; /* host array [nranks] (emulation only) */
   int32_t ent1, ent2;        /* UOT_ENT_*: "h" needs KL/KL, "g" KL or Berg, "f" any */
+  int32_t lam_given;         /* "g", single device: start from lam0 instead of lambda*(f0, g0) */
+  double lam0;               /* (g_sinkhorn_step's incoming lam, src/sinkhorn.py:117-134) */
 } uot_sinkhorn_desc;
 
 int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);

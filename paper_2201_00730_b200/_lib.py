@@ -37,7 +37,7 @@ class SinkhornDesc(ctypes.Structure):
         ("init_given", _i32), ("iters", _i32), ("tol", _f64), ("use_tol", _i32),
         ("trace_delta", _vp), ("iterations", _vp),
         ("nccl_comm", _vp), ("nranks", _i32), ("rank", _i32), ("shard_rows", _vp),
-        ("ent1", _i32), ("ent2", _i32),
+        ("ent1", _i32), ("ent2", _i32), ("lam_given", _i32), ("lam0", _f64),
     ]
 
 

@@ -1066,6 +1066,11 @@ __global__ void sk_reset(int batch, SkScalars* sc, unsigned int* counters, int* 
   }
 }
 
+__global__ void sk_set_lam(int batch, SkScalars* sc, double lam) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) sc[b].lam = lam;
+}
+
 template <typename T>
 __global__ void sk_zero(long n, T* p) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
@@ -1529,7 +1534,12 @@ struct Engine {
       UOT_CHECK_LAUNCH();
       return UOT_OK;
     };
-    if (g_newton) UOT_TRY(lam_newton(bf.hatA0));  // lambda*(f0, g0) (:263-265)
+    if (d.variant == UOT_SINKHORN_G && d.lam_given) {  // g_sinkhorn_step(prob, d, lam)
+      sk_set_lam<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, d.lam0);
+      UOT_CHECK_LAUNCH();
+    } else if (g_newton) {
+      UOT_TRY(lam_newton(bf.hatA0));  // lambda*(f0, g0) (:263-265)
+    }
     const int sB = splits(d.batch, d.m, d.n, d.d);  // g-update splits
     const int sA = splits(d.batch, d.n, d.m, d.d);  // f-update splits
     // one iteration: two half-steps (main + tail each), hat buffers by parity

@@ -98,7 +98,8 @@ def _geometry(prob):
 
 def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
                      c=None, f0=None, tol=None, precision="fp32", stream=None, comm=None,
-                     nranks=1, rank=0, shard_rows=None, g0=None, ent1="kl", ent2="kl"):
+                     nranks=1, rank=0, shard_rows=None, g0=None, ent1="kl", ent2="kl",
+                     lam0=None):
     """Batched Sinkhorn on device.
 
     x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
@@ -157,7 +158,8 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
         trace_delta=_lib.ptr(trace), iterations=_lib.ptr(its), nccl_comm=comm,
         nranks=int(nranks), rank=int(rank), shard_rows=None,
         ent1={"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG, "balanced": _lib.ENT_BALANCED}[ent1],
-        ent2={"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG, "balanced": _lib.ENT_BALANCED}[ent2])
+        ent2={"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG, "balanced": _lib.ENT_BALANCED}[ent2],
+        lam_given=0 if lam0 is None else 1, lam0=0.0 if lam0 is None else float(lam0))
     rows_arr = None
     if shard_rows is not None:
         import numpy as _np
@@ -273,25 +275,26 @@ def f_sinkhorn_step(prob, d):
 
 def g_sinkhorn_step(prob, d, lam):
     """One translated step at the incoming translation lam
-    (src/sinkhorn.py:117-134); returns (pair, new_lam).  KL marginals.
+    (src/sinkhorn.py:117-134); returns (pair, new_lam) with new_lam =
+    lambda_star(pair, initial=lam).  KL or Berg marginals: the device G run
+    starts from the given lam (descriptor lam_given) instead of
+    lambda*(f, g); the translation after the step is the closed form (KL/KL)
+    or the bracketed Newton (uot_translation)."""
+    from .duality import lambda_star
 
-    The kernel starts a G run from lambda*(f, g); the step depends on g only
-    through that scalar, so g is shifted to make lambda*(f, g') = lam
-    (lambda* moves by c rho1 / (rho1 + rho2) when g moves by c)."""
     _require_positive_eps(prob)
     prob.check_pair(d)
-    require_kl(prob.ent1, prob.ent2, what="g-sinkhorn")
-    r1, r2 = prob.ent1.rho, prob.ent2.rho
-    lam0 = float(kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, r1, r2)[0, 0].item())
-    g_in = np.asarray(d.g, dtype=np.float64) + (float(lam) - lam0) * (r1 + r2) / r1
+    if not all(isinstance(e, (KL, Berg)) for e in (prob.ent1, prob.ent2)):
+        raise UnsupportedEntropyError(
+            "optimal translation needs strictly convex conjugates (KL or Berg)")
+    e1, e2 = _ents(prob)
     costname, p, x, y, C = _step_inputs(prob)
-    f, g, _, _ = sinkhorn_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.eps, r1, r2,
-                                  1, variant="g", cost=costname, p=p, c=C, f0=d.f, g0=g_in,
-                                  precision="fp64")
+    f, g, _, _ = sinkhorn_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.eps,
+                                  ent_rho(prob.ent1), ent_rho(prob.ent2), 1, variant="g",
+                                  cost=costname, p=p, c=C, f0=d.f, g0=d.g, precision="fp64",
+                                  ent1=e1, ent2=e2, lam0=float(lam))
     pair = DualPair(D.to_np(f[0]), D.to_np(g[0]))
-    new_lam = float(kl_scalars(prob.alpha.weights, prob.beta.weights, pair.f, pair.g, r1,
-                               r2)[0, 0].item())
-    return pair, new_lam
+    return pair, lambda_star(prob, pair, initial=float(lam))
 
 
 def h_sinkhorn_step(prob, d):
@@ -423,10 +426,13 @@ def _run_anderson(prob, config, d, reference, e1, e2):
     through lambda, so the extrapolated g is carried for "g" and returned."""
     t = D.torch()
     n, m = len(prob.alpha), len(prob.beta)
+    from .duality import lambda_star
+
     variant = config.variant
-    if variant == "g" or reference is not None:
-        if variant != "f":
-            require_kl(prob.ent1, prob.ent2, what="translated Anderson iterates")
+
+    def lam_of(zz, initial=0.0):  # translation of a device (f | g) row, closed form or Newton
+        return lambda_star(prob, DualPair(D.to_np(zz[:n]), D.to_np(zz[n:])), initial=initial)
+
     r1, r2 = ent_rho(prob.ent1), ent_rho(prob.ent2)
     aw, bw = prob.alpha.weights, prob.beta.weights
     costname, p, x, y, C = _step_inputs(prob)
@@ -435,22 +441,21 @@ def _run_anderson(prob, config, d, reference, e1, e2):
                  f64).reshape(1, n + m)
     tz = t.empty_like(z)
     win = AndersonWindow(1, n + m, config.anderson.depth, config.anderson.reg)
-    lam = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item()) if variant == "g" else 0.0
+    lam = lam_of(z[0]) if variant == "g" else 0.0
     deltas, walls, err_f, err_g = [], [], [], []
     converged = False
     for _ in range(config.max_iters):
         t0 = time.perf_counter_ns()
-        g_in = None
-        if variant == "g":  # start the device G step at the carried lambda (g_sinkhorn_step)
-            lam0 = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item())
-            g_in = z[0, n:] + (lam - lam0) * (r1 + r2) / r1
+        gv = variant == "g"  # the device G step starts at the carried lambda (g_sinkhorn_step)
         f1, g1, _, _ = sinkhorn_batched(x, y, aw, bw, prob.eps, r1, r2, 1, variant=variant,
-                                        cost=costname, p=p, c=C, f0=z[0, :n], g0=g_in,
-                                        precision=config.precision, ent1=e1, ent2=e2)
+                                        cost=costname, p=p, c=C, f0=z[0, :n],
+                                        g0=z[0, n:] if gv else None,
+                                        precision=config.precision, ent1=e1, ent2=e2,
+                                        lam0=lam if gv else None)
         tz[0, :n].copy_(f1[0])
         tz[0, n:].copy_(g1[0])
         if variant == "g":
-            lam = float(kl_scalars(aw, bw, tz[0, :n], tz[0, n:], r1, r2)[0, 0].item())
+            lam = lam_of(tz[0], lam)
         delta, status = win.step(z, tz, z, n)
         dl = float(delta[0].item())
         if int(status[0].item()) != 0:
@@ -460,7 +465,7 @@ def _run_anderson(prob, config, d, reference, e1, e2):
         if reference is not None:
             shift = 0.0
             if variant != "f":
-                shift = float(kl_scalars(aw, bw, z[0, :n], z[0, n:], r1, r2)[0, 0].item())
+                shift = lam_of(z[0], lam)
             fz = D.to_np(z[0, :n])
             gz = D.to_np(z[0, n:])
             err_f.append(float(np.abs(fz + shift - reference.f).max()))

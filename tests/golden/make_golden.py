@@ -1011,6 +1011,29 @@ def gen_sk_trace():
             out[f"c{k}_{key}"] = np.asarray(rep.trace[key])
         out[f"c{k}_f"], out[f"c{k}_g"] = rep.final.f, rep.final.g
     out["cases"] = np.arange(len(specs))
+    # g_sinkhorn_step at a given lam and Anderson-accelerated G with Berg
+    for k, (e1, e2) in enumerate([(U.Berg(1.1), U.Berg(0.8)), (U.KL(0.7), U.Berg(1.3)),
+                                  (U.Berg(0.9), U.KL(1.6))]):
+        n, m = int(rng.integers(8, 30)), int(rng.integers(8, 30))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa, wb = rng.uniform(0.1, 1.0, n), rng.uniform(0.1, 1.0, m)
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(2.0), e1, e2, eps=0.15)
+        f0, g0 = rng.uniform(-0.2, 0.2, n), rng.uniform(-0.2, 0.2, m)
+        pair, lam1 = US.g_sinkhorn_step(prob, U.DualPair(f0, g0), 0.13)
+        ref = US.run(prob, U.SinkhornConfig("f", 20000, 1e-13)).final
+        rep = US.run(prob, U.SinkhornConfig("g", 12, 1e-15, anderson=U.AndersonConfig(3, 1e-9)),
+                     reference=ref)
+        code = {U.KL: 0, U.Berg: 1}
+        out[f"s{k}_x"], out[f"s{k}_y"], out[f"s{k}_a"], out[f"s{k}_b"] = x, y, wa, wb
+        out[f"s{k}_par"] = np.array([code[type(e1)], e1.rho, code[type(e2)], e2.rho])
+        out[f"s{k}_f0"], out[f"s{k}_g0"] = f0, g0
+        out[f"s{k}_f1"], out[f"s{k}_g1"], out[f"s{k}_lam1"] = pair.f, pair.g, np.array(lam1)
+        out[f"s{k}_ref_f"], out[f"s{k}_ref_g"] = ref.f, ref.g
+        for key in ("delta_f", "err_f", "err_g"):
+            out[f"s{k}_and_{key}"] = np.asarray(rep.trace[key])
+        out[f"s{k}_and_f"], out[f"s{k}_and_g"] = rep.final.f, rep.final.g
+    out["step_cases"] = np.arange(3)
     save("sk_trace.npz", **out)
 
 

@@ -33,3 +33,37 @@ def test_error_traces_match_reference(k):
     for key in ("delta_f", "err_f", "err_g"):
         np.testing.assert_allclose(rep.trace[key][:L], z[f"c{k}_{key}"][:L], rtol=1e-8, atol=1e-11,
                                    err_msg=key)
+
+
+def _sprob(z, k):
+    c1, r1, c2, r2 = z[f"s{k}_par"]
+    return P.UotProblem(P.DiscreteMeasure(z[f"s{k}_x"], z[f"s{k}_a"]),
+                        P.DiscreteMeasure(z[f"s{k}_y"], z[f"s{k}_b"]), P.PowerDistance(2.0),
+                        _ent(c1, r1), _ent(c2, r2), eps=0.15)
+
+
+@pytest.mark.parametrize("k", range(3))
+def test_g_step_at_given_lambda_berg(k):
+    """g_sinkhorn_step(prob, d, lam) with Berg marginals (src/sinkhorn.py:117-134):
+    the device G run starts from the given lam (descriptor lam_given)."""
+    z = golden("sk_trace.npz")
+    prob = _sprob(z, k)
+    pair, lam1 = P.g_sinkhorn_step(prob, P.DualPair(z[f"s{k}_f0"], z[f"s{k}_g0"]), 0.13)
+    np.testing.assert_allclose(pair.f, z[f"s{k}_f1"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(pair.g, z[f"s{k}_g1"], rtol=0, atol=1e-12)
+    assert lam1 == pytest.approx(float(z[f"s{k}_lam1"]), abs=1e-10)
+
+
+@pytest.mark.parametrize("k", range(3))
+def test_anderson_g_berg_traces(k):
+    """Anderson-accelerated G (src/sinkhorn.py:281-292) with a Berg marginal:
+    the carried lambda is the Newton translation of the stepped pair."""
+    z = golden("sk_trace.npz")
+    prob = _sprob(z, k)
+    ref = P.DualPair(z[f"s{k}_ref_f"], z[f"s{k}_ref_g"])
+    rep = P.run(prob, P.SinkhornConfig("g", 12, 1e-15, anderson=P.AndersonConfig(3, 1e-9)),
+                reference=ref)
+    for key in ("delta_f", "err_f", "err_g"):
+        np.testing.assert_allclose(rep.trace[key], z[f"s{k}_and_{key}"], rtol=1e-7, atol=1e-11,
+                                   err_msg=key)
+    np.testing.assert_allclose(rep.final.f, z[f"s{k}_and_f"], rtol=0, atol=1e-10)
