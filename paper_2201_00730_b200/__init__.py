@@ -20,7 +20,8 @@ from .duality import (
     lambda_star,
     translate,
 )
-from .entropies import KL, Balanced, Berg
+from .entropies import (KL, Balanced, Berg, aprox, conj, conj_grad, conj_hess, divergence,
+                        logdotexp, softmin)
 from .exceptions import (
     InfeasibleDualError,
     MassBalanceError,
@@ -61,7 +62,8 @@ from .certify import (
     hilbert_norm,
     scalar_max_oracle,
 )
-from .fw import FwConfig, feasibility_violation, fw_solve, fw_solve_batched
+from .fw import (AtomStore, FwConfig, feasibility_violation, fw_solve, fw_solve_batched,
+                 line_search_h0, pfw_step, ternary_max)
 from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched
 from .sinkhorn import (
     AndersonConfig,

@@ -8,6 +8,7 @@ from __future__ import annotations
 import ctypes
 import math
 from dataclasses import dataclass
+from functools import cached_property
 
 import numpy as np
 
@@ -56,6 +57,14 @@ class UotProblem:
     def __post_init__(self):
         if not (math.isfinite(self.eps) and self.eps >= 0):
             raise ValueError("eps must be nonnegative and finite")
+
+    @cached_property
+    def cost_matrix(self):
+        """Dense C (src/duality.py:85-87), built on the device on first use and
+        cached; the solvers never need it (costs are formed on the fly)."""
+        from .measures import build_cost_matrix
+
+        return build_cost_matrix(self.alpha, self.beta, self.cost)
 
     def check_pair(self, d):
         if d.f.size != len(self.alpha) or d.g.size != len(self.beta):

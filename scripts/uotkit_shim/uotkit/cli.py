@@ -1,0 +1,1 @@
+from paper_2201_00730_b200.cli import *  # noqa
