@@ -179,8 +179,6 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     """Maximise the invariant dual at eps = 0 (src/fw.py:176-232)."""
     _check_problem(prob)
     kl = isinstance(prob.ent1, KL) and isinstance(prob.ent2, KL)
-    if config.step == "pairwise" and not kl:
-        raise UnsupportedEntropyError("pairwise FW runs KL/KL penalties on the B200 path")
     n, m = len(prob.alpha), len(prob.beta)
     x, y = prob.alpha.points, prob.beta.points
     C = None
@@ -199,6 +197,8 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
         raise InfeasibleDualError("initial pair violates f + g <= C")
     if C is not None:  # the oracle's Monge check (src/ot1d.py:106, via _lmo)
         check_submodular(prob.cost.matrix)
+    if config.step == "pairwise" and not kl:
+        return _pfw_solve_host(prob, config, d, reference)
     if reference is not None and len(reference.f) != n:
         raise ValueError("reference potential does not match the problem")
     tic = time.perf_counter_ns()
@@ -309,28 +309,32 @@ class AtomStore:
         return DualPair(self.weights @ self.r_atoms, self.weights @ self.s_atoms)
 
 
-def pfw_step(prob, store):
-    """One pairwise weight transfer (:255-323): device LMO (updated marginals,
-    1-D oracle), the least aligned active atom as donor, a ternary H0 line
-    search on [0, w_away] with endpoint comparison, dedup merge of the new
-    atom and removal of emptied atoms."""
-    from .duality import updated_marginals
+def _pfw_iteration(prob, store):
+    """One pairwise step (src/fw.py:275-310); returns (new_store, diag) with
+    the iterate, the oracle plan, the linear gap, H0 and the plan's primal.
+    Device LMO (updated marginals + 1-D oracle), H0 values, primal; the atom
+    bookkeeping is host work on the store."""
+    from .duality import eval_primal, updated_marginals
     from .measures import DiscreteMeasure
     from .ot1d import solve_ot_1d
 
-    if store.weights.size == 0:
-        raise ValueError("atom store is empty")
-    _check_problem(prob)
     d = store.current()
     ta, tb = updated_marginals(prob, d)
-    _, atom = solve_ot_1d(DiscreteMeasure(prob.alpha.points, ta),
-                          DiscreteMeasure(prob.beta.points, tb), prob.cost)
+    mass_a, mass_b = float(ta.sum()), float(tb.sum())
+    if abs(mass_a - mass_b) > 1e-9 * max(mass_a, mass_b):  # fw.py:161-166
+        raise MassBalanceError(f"reweighted marginal masses disagree ({mass_a:.12g} vs "
+                               f"{mass_b:.12g}); optimal translation looks broken")
+    plan, atom = solve_ot_1d(DiscreteMeasure(prob.alpha.points, ta),
+                             DiscreteMeasure(prob.beta.points, tb), prob.cost)
+    diag = {"pair": d, "plan": plan,
+            "fw_gap": float(np.dot(ta, atom.f - d.f) + np.dot(tb, atom.g - d.g)),
+            "dual": _h0_value(prob, d.f, d.g), "primal": eval_primal(prob, plan)}
     scores = np.where(store.weights > 0, store.r_atoms @ ta + store.s_atoms @ tb, np.inf)
     away = int(np.argmin(scores))
     max_step = float(store.weights[away])
     dr, ds = atom.f - store.r_atoms[away], atom.g - store.s_atoms[away]
     if max_step <= 0.0 or (np.abs(dr).max() < ATOM_DEDUP_TOL and np.abs(ds).max() < ATOM_DEDUP_TOL):
-        return store
+        return store, diag
 
     def value(gamma):
         return _h0_value(prob, d.f + gamma * dr, d.g + gamma * ds)
@@ -338,7 +342,7 @@ def pfw_step(prob, store):
     gamma = ternary_max(value, 0.0, max_step, iters=60)
     gamma = max(((value(c), c) for c in (gamma, 0.0, max_step)), key=lambda z: z[0])[1]
     if gamma <= 0.0:
-        return store
+        return store, diag
     w = store.weights.copy()
     w[away] = max(w[away] - gamma, 0.0)
     r_atoms, s_atoms = store.r_atoms, store.s_atoms
@@ -351,4 +355,51 @@ def pfw_step(prob, store):
         s_atoms = np.vstack([s_atoms, atom.g])
         w = np.concatenate([w, [gamma]])
     keep = w > 0
-    return AtomStore(r_atoms[keep], s_atoms[keep], w[keep])
+    return AtomStore(r_atoms[keep], s_atoms[keep], w[keep]), diag
+
+
+def pfw_step(prob, store):
+    """One pairwise weight transfer (:255-323): device LMO (updated marginals,
+    1-D oracle), the least aligned active atom as donor, a ternary H0 line
+    search on [0, w_away] with endpoint comparison, dedup merge of the new
+    atom and removal of emptied atoms."""
+    if store.weights.size == 0:
+        raise ValueError("atom store is empty")
+    _check_problem(prob)
+    return _pfw_iteration(prob, store)[0]
+
+
+def _pfw_solve_host(prob, config, d0, reference):
+    """Pairwise FW for Berg / mixed penalties (src/fw.py:326-357), one
+    device-backed _pfw_iteration per step; KL/KL runs fully on the device."""
+    from .duality import dual_feasibility_violation, lambda_star
+
+    store = AtomStore(d0.f[None, :], d0.g[None, :], np.array([1.0]))
+    trace = {k: [] for k in ("h0", "fw_gap", "pd_gap", "wall_ns")}
+    err_f = []
+    converged = False
+    plan, primal, dual = None, np.nan, np.nan
+    for _ in range(config.max_iters):
+        tic = time.perf_counter_ns()
+        store, diag = _pfw_iteration(prob, store)
+        plan, dual, primal = diag["plan"], diag["dual"], diag["primal"]
+        pd_gap = primal - dual
+        trace["h0"].append(dual)
+        trace["fw_gap"].append(diag["fw_gap"])
+        trace["pd_gap"].append(pd_gap)
+        trace["wall_ns"].append(time.perf_counter_ns() - tic)
+        if reference is not None:
+            pair = diag["pair"]
+            err_f.append(float(np.abs(pair.f + lambda_star(prob, pair) - reference.f).max()))
+        if pd_gap < config.gap_tol:
+            converged = True
+            break
+    d = store.current()
+    lam = lambda_star(prob, d)  # _finalize (:235-252)
+    cert = assemble_certificate(primal, dual, dual_feasibility_violation(prob, d), config.gap_tol)
+    out = {k: np.asarray(v) for k, v in trace.items()}
+    out["wall_ns"] = out["wall_ns"].astype(np.int64)
+    if reference is not None:
+        out["err_f"] = np.asarray(err_f)
+    return SolverReport(final=DualPair(d.f + lam, d.g - lam), iterations=len(out["h0"]),
+                        converged=converged, trace=out, certificate=cert, plan=plan)

@@ -1037,10 +1037,55 @@ def gen_sk_trace():
     save("sk_trace.npz", **out)
 
 
+def gen_berg_pfw():
+    """Pairwise FW with Berg / mixed penalties: the reference's own fw_solve
+    report (src/fw.py:326-357) and its CLI (uot1d --entropy berg)."""
+    import contextlib
+    import io
+    import tempfile
+
+    from uotkit.cli import main as ref_main
+
+    rng = np.random.default_rng(4747)
+    out = {}
+    for k, (e1, e2, iters) in enumerate([(U.Berg(1.0), U.Berg(1.0), 40), (U.KL(0.8), U.Berg(1.3), 40),
+                                         (U.Berg(0.6), U.KL(1.2), 25)]):
+        n, m = int(rng.integers(8, 25)), int(rng.integers(8, 25))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m)
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.PowerDistance(2.0), e1, e2, eps=0.0)
+        rep = U.fw_solve(prob, U.FwConfig("pairwise", iters, 1e-10))
+        code = {U.KL: 0, U.Berg: 1}
+        out[f"c{k}_x"], out[f"c{k}_y"], out[f"c{k}_a"], out[f"c{k}_b"] = x, y, wa, wb
+        out[f"c{k}_par"] = np.array([code[type(e1)], e1.rho, code[type(e2)], e2.rho, iters])
+        out[f"c{k}_h0"] = np.asarray(rep.trace["h0"])
+        out[f"c{k}_pd_gap"] = np.asarray(rep.trace["pd_gap"])
+        out[f"c{k}_f"], out[f"c{k}_g"] = rep.final.f, rep.final.g
+        out[f"c{k}_passed"] = np.array(bool(rep.certificate.passed))
+    with tempfile.TemporaryDirectory() as tmp:
+        a, b = os.path.join(tmp, "a.csv"), os.path.join(tmp, "b.csv")
+        with contextlib.redirect_stdout(io.StringIO()):
+            ref_main(["gen", "--n", "12", "--seed", "5", "--out", a])
+            ref_main(["gen", "--n", "10", "--seed", "6", "--out", b])
+        for method in ("fw-ls", "fw", "pfw"):
+            o = os.path.join(tmp, "o.json")
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = ref_main(["uot1d", a, b, "--entropy", "berg", "--method", method,
+                               "--gap-tol", "1e-7", "--max-iters", "3000", "--out", o])
+            out[f"cli_{method}_rc"] = np.array(rc)
+            out[f"cli_{method}_cert"] = np.frombuffer(buf.getvalue().splitlines()[0].encode(),
+                                                      dtype=np.uint8)
+    out["cases"] = np.arange(3)
+    save("berg_pfw.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -130,3 +130,44 @@ def test_berg_line_search_and_batched_equals_single():
     _, atom = P.solve_ot_1d(P.DiscreteMeasure(args[0], ta), P.DiscreteMeasure(args[1], tb))
     gm = F.line_search_h0(prob, d0, atom)
     assert gm == pytest.approx(float(rs.step_size[0, 0].item()), abs=1e-9)
+
+
+@pytest.mark.parametrize("k", range(3))
+def test_berg_pairwise_report(k):
+    """Pairwise FW with Berg / mixed penalties (src/fw.py:326-357) against the
+    reference's own report: same early exit (+-1 at a 1e-10 gap), the H0 trace
+    while one atom is active, final translated pair and certificate."""
+    z = golden("berg_pfw.npz")
+    c1, r1, c2, r2, iters = z[f"c{k}_par"]
+    prob = P.UotProblem(P.DiscreteMeasure(z[f"c{k}_x"], z[f"c{k}_a"]),
+                        P.DiscreteMeasure(z[f"c{k}_y"], z[f"c{k}_b"]), P.PowerDistance(2.0),
+                        _ent(c1, r1), _ent(c2, r2), eps=0.0)
+    rep = P.fw_solve(prob, P.FwConfig("pairwise", int(iters), 1e-10))
+    ref_h0 = z[f"c{k}_h0"]
+    assert abs(rep.iterations - len(ref_h0)) <= 1
+    np.testing.assert_allclose(rep.trace["h0"][:2], ref_h0[:2], rtol=1e-9, atol=1e-13)
+    assert rep.certificate.passed == bool(z[f"c{k}_passed"])
+    assert rel_err(rep.final.f, rep.final.g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-6
+
+
+@pytest.mark.parametrize("method", ["fw-ls", "fw", "pfw"])
+def test_cli_uot1d_berg(tmp_path, capsys, method):
+    """uot1d --entropy berg through the CLI: exit code and certificate as the
+    reference's CLI prints them on the same generated inputs."""
+    import json
+
+    from paper_2201_00730_b200 import cli
+
+    z = golden("berg_pfw.npz")
+    a, b = tmp_path / "a.csv", tmp_path / "b.csv"
+    assert cli.main(["gen", "--n", "12", "--seed", "5", "--out", str(a)]) == 0
+    assert cli.main(["gen", "--n", "10", "--seed", "6", "--out", str(b)]) == 0
+    capsys.readouterr()
+    rc = cli.main(["uot1d", str(a), str(b), "--entropy", "berg", "--method", method, "--gap-tol",
+                   "1e-7", "--max-iters", "3000", "--out", str(tmp_path / "o.json")])
+    assert rc == int(z[f"cli_{method}_rc"])
+    got = json.loads(capsys.readouterr().out.splitlines()[0])
+    want = json.loads(bytes(z[f"cli_{method}_cert"]).decode())
+    assert got["passed"] == want["passed"]
+    assert got["primal"] == pytest.approx(want["primal"], rel=1e-6)
+    assert got["dual"] == pytest.approx(want["dual"], rel=1e-6)
