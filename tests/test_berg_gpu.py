@@ -171,3 +171,29 @@ def test_cli_uot1d_berg(tmp_path, capsys, method):
     assert got["passed"] == want["passed"]
     assert got["primal"] == pytest.approx(want["primal"], rel=1e-6)
     assert got["dual"] == pytest.approx(want["dual"], rel=1e-6)
+
+
+def test_berg_fw_edges_and_ragged_early_exit():
+    """Single atoms, zero-weight atoms, and a batch whose problems stop at
+    different iterations (per-problem done flags, host check every 16)."""
+    rng = np.random.default_rng(77)
+    one = F.fw_solve_batched([0.2], [0.7], [1.0], [0.5], 1.0, 0.7, 2.0, 50, "linesearch",
+                             gap_tol=1e-10, early_exit=True, ent1="berg", ent2="berg")
+    assert int(one.status[0].item()) == 0 and int(one.count[0].item()) == 1
+    B, n, m = 5, 30, 24
+    x = np.sort(rng.uniform(0, 1, (B, n)), axis=1)
+    y = np.sort(rng.uniform(0, 1, (B, m)), axis=1)
+    a = rng.uniform(0.1, 1, (B, n))
+    a[:, ::6] = 0.0
+    b = rng.uniform(0.1, 1, (B, m)) * rng.uniform(0.3, 3.0, (B, 1))
+    rb = F.fw_solve_batched(x, y, a, b, 0.8, 1.3, 2.0, 200, "harmonic", gap_tol=1e-4,
+                            early_exit=True, ent1="kl", ent2="berg")
+    its = D.to_np(rb.iterations)
+    assert len(set(its.tolist())) > 1  # ragged stop
+    for q in range(B):
+        rs = F.fw_solve_batched(x[q], y[q], a[q], b[q], 0.8, 1.3, 2.0, 200, "harmonic",
+                                gap_tol=1e-4, early_exit=True, ent1="kl", ent2="berg")
+        assert int(rs.iterations[0].item()) == its[q]
+        assert np.array_equal(D.to_np(rs.f[0]), D.to_np(rb.f[q]))
+        assert D.to_np(rb.pd_gap[q, its[q] - 1]) < 1e-4
+        assert np.all(D.to_np(rb.em[q, :int(rb.count[q].item())]) > 0)
