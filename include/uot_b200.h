@@ -290,7 +290,8 @@ int uot_fw1d_run(const uot_fw_desc* desc, void* workspace, size_t workspace_byte
 int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, const double* y,
                        double p, const double* f, const double* g, double* out, void* stream);
 /* Optimal translation lambda* of (f, g) for KL / Berg penalties by the
- * bracketed Newton of src/duality.py:182-247 started at lam0 (solve != 0), or
+ * bracketed Newton of src/duality.py:182-247 started at lam0 (solve != 0; stop at
+ * |residual| < tol within max_iters Newton steps -- the reference's 1e-11 / 100), or
  * lambda = lam0 given (solve == 0, e.g. eval_G / eval_F).  Optional outputs:
  * lam [batch]; ta, tb [batch][n|m] = weights * conj_grad(-f - lam | -g + lam)
  * (updated_marginals, :293-303); h [batch] = <a, -phi1*(-(f + lam))> +
@@ -299,8 +300,8 @@ int uot_feasibility_1d(int32_t batch, int32_t n, int32_t m, const double* x, con
  * domain, 2 = no bracket, 3 = no convergence (NewtonError). */
 int uot_translation(int32_t batch, int32_t n, int32_t m, const double* a, const double* b,
                     const double* f, const double* g, int32_t ent1, int32_t ent2, double rho1,
-                    double rho2, int32_t solve, double lam0, double* lam, double* ta, double* tb,
-                    double* h, int32_t* status, void* stream);
+                    double rho2, int32_t solve, double lam0, double tol, int32_t max_iters,
+                    double* lam, double* ta, double* tb, double* h, int32_t* status, void* stream);
 /* The same for explicit costs C [batch][n][m] (ExplicitMatrix). */
 int uot_feasibility_explicit(int32_t batch, int32_t n, int32_t m, const double* C,
                              const double* f, const double* g, double* out, void* stream);

@@ -100,7 +100,8 @@ def load(require_gpu=True):
         lib.uot_anderson_weights.argtypes = [_i32, _i32, _vp, _f64, _vp, _vp, _vp]
         lib.uot_cost_matrix.argtypes = [_i32, _i32, _vp, _vp, _f64, _vp, _vp]
         lib.uot_translation.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f64,
-                                        _f64, _i32, _f64, _vp, _vp, _vp, _vp, _vp, _vp]
+                                        _f64, _i32, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp,
+                                        _vp]
         lib.uot_feasibility_explicit.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]
         lib.uot_cost_quadruple_diameter.argtypes = [_i32, _i32, _vp, _vp, _vp]
         lib.uot_updated_marginals.argtypes = [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _f64, _f64,

@@ -80,6 +80,8 @@ struct Sides {
   const double* b;
   int e1, e2;
   double r1, r2;
+  double tol = NEWTON_TOL;     // lambda_star(tol, max_iters) (duality.py:160)
+  int max_iters = NEWTON_ITERS;
 };
 
 // (1 - gamma) u + gamma v without FMA contraction (numpy's rounding, fw.py:140-144)
@@ -133,7 +135,7 @@ __device__ double newton_lambda(const Sides& S, PF pf, PG pg, double init, doubl
   };
   double lam = clamp(init), r, ds;
   eval(lam, r, ds);
-  if (fabs(r) < NEWTON_TOL) return lam;
+  if (fabs(r) < S.tol) return lam;
   double lo = lam, hi = lam, step = 1.0;
   bool ok = false;
   if (r > 0.0) {
@@ -158,9 +160,9 @@ __device__ double newton_lambda(const Sides& S, PF pf, PG pg, double init, doubl
     return CUDART_NAN;
   }
   double x = 0.5 * (lo + hi);
-  for (int it = 0; it < NEWTON_ITERS; ++it) {
+  for (int it = 0; it < S.max_iters; ++it) {
     eval(x, r, ds);
-    if (fabs(r) < NEWTON_TOL) return x;
+    if (fabs(r) < S.tol) return x;
     if (r > 0.0)
       lo = x;
     else
@@ -549,10 +551,10 @@ using namespace uot;
 extern "C" int uot_translation(int32_t batch, int32_t n, int32_t m, const double* a,
                                const double* b, const double* f, const double* g, int32_t ent1,
                                int32_t ent2, double rho1, double rho2, int32_t solve, double lam0,
-                               double* lam, double* ta, double* tb, double* h, int32_t* status,
-                               void* stream) {
+                               double tol, int32_t max_iters, double* lam, double* ta, double* tb,
+                               double* h, int32_t* status, void* stream) {
   if (batch < 1 || n < 1 || m < 1 || a == nullptr || b == nullptr || f == nullptr ||
-      g == nullptr || !(rho1 > 0.0) || !(rho2 > 0.0)) {
+      g == nullptr || !(rho1 > 0.0) || !(rho2 > 0.0) || !(tol > 0.0) || max_iters < 1) {
     set_error("uot_translation: invalid arguments");
     return UOT_INVALID;
   }
@@ -560,8 +562,11 @@ extern "C" int uot_translation(int32_t batch, int32_t n, int32_t m, const double
     set_error("optimal translation needs strictly convex conjugates (KL or Berg)");
     return UOT_UNSUPPORTED_ENTROPY;
   }
-  translation_kernel<<<batch, GT, 0, (cudaStream_t)stream>>>(
-      Sides{n, m, a, b, ent1, ent2, rho1, rho2}, f, g, solve, lam0, lam, ta, tb, h, status);
+  Sides S{n, m, a, b, ent1, ent2, rho1, rho2};
+  S.tol = tol;
+  S.max_iters = max_iters;
+  translation_kernel<<<batch, GT, 0, (cudaStream_t)stream>>>(S, f, g, solve, lam0, lam, ta, tb, h,
+                                                             status);
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }

@@ -95,7 +95,8 @@ _NEWTON_MSG = {1: "empty translation domain for Berg conjugates",
                3: "translation Newton did not reach the residual target"}
 
 
-def translation(prob, f, g, solve=True, lam0=0.0, marginals=False, value=False):
+def translation(prob, f, g, solve=True, lam0=0.0, marginals=False, value=False, tol=1e-11,
+                max_iters=100):
     """One ``uot_translation`` launch: the bracketed-Newton translation of
     (f, g) (src/duality.py:182-247) from ``lam0`` (or lam0 itself with
     ``solve=False``), optionally the updated marginals (:293-303) and the
@@ -114,7 +115,7 @@ def translation(prob, f, g, solve=True, lam0=0.0, marginals=False, value=False):
     _lib.check(lib.uot_translation(1, n, m, _lib.ptr(a), _lib.ptr(b), _lib.ptr(fd), _lib.ptr(gd),
                                    ent_code(prob.ent1), ent_code(prob.ent2), ent_rho(prob.ent1),
                                    ent_rho(prob.ent2), 1 if solve else 0, float(lam0),
-                                   _lib.ptr(lam), _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(h),
+                                   float(tol), int(max_iters), _lib.ptr(lam), _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(h),
                                    _lib.ptr(st), _lib.stream_handle()), "uot_translation")
     code = int(st[0].item())
     if code:
@@ -131,15 +132,15 @@ def lambda_star(prob, d, tol=1e-11, max_iters=100, initial=0.0):
 
     KL/KL has the closed form rho1 rho2/(rho1+rho2) (LSE_a(-f/rho1) -
     LSE_b(-g/rho2)), evaluated on the GPU; KL/Berg mixes and Berg/Berg run the
-    reference's bracketed Newton (:182-247) in ``uot_translation`` (tolerance
-    1e-11, 100 Newton steps: the reference defaults).  Balanced is rejected
-    like the reference."""
+    reference's bracketed Newton (:182-247) in ``uot_translation`` with the
+    given ``tol`` / ``max_iters`` / ``initial``.  Balanced is rejected like
+    the reference."""
     prob.check_pair(d)
     if not (_strictly_convex(prob.ent1) and _strictly_convex(prob.ent2)):
         raise UnsupportedEntropyError(
             "optimal translation needs strictly convex conjugates (KL or Berg)")
     if not _both_kl(prob):
-        return translation(prob, d.f, d.g, True, initial)[0]
+        return translation(prob, d.f, d.g, True, initial, tol=tol, max_iters=max_iters)[0]
     out = kl_scalars(prob.alpha.weights, prob.beta.weights, d.f, d.g, prob.ent1.rho, prob.ent2.rho)
     return float(out[0, 0].item())
 

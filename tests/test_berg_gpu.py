@@ -197,3 +197,17 @@ def test_berg_fw_edges_and_ragged_early_exit():
         assert np.array_equal(D.to_np(rs.f[0]), D.to_np(rb.f[q]))
         assert D.to_np(rb.pd_gap[q, its[q] - 1]) < 1e-4
         assert np.all(D.to_np(rb.em[q, :int(rb.count[q].item())]) > 0)
+
+
+def test_lambda_star_tolerance_arguments():
+    """lambda_star(prob, d, tol, max_iters, initial) (src/duality.py:160):
+    the stopping rule is the caller's; too few Newton steps raise."""
+    z = golden("berg.npz")
+    prob = _dprob(z, 0)
+    d = P.DualPair(z["d0_f"], z["d0_g"])
+    tight = P.lambda_star(prob, d)
+    loose = P.lambda_star(prob, d, tol=1e-2)
+    assert abs(loose - tight) < 0.1
+    assert P.lambda_star(prob, d, initial=tight) == pytest.approx(tight, abs=1e-10)
+    with pytest.raises(P.NewtonError):
+        P.lambda_star(prob, d, tol=1e-300, max_iters=1)
