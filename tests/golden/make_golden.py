@@ -1079,6 +1079,34 @@ def gen_berg_pfw():
             out[f"cli_{method}_cert"] = np.frombuffer(buf.getvalue().splitlines()[0].encode(),
                                                       dtype=np.uint8)
     out["cases"] = np.arange(3)
+    # explicit (negative-entry) Monge cost with Berg / mixed penalties, fixed iterations
+    for k, (e1, e2, step) in enumerate([(U.Berg(1.2), U.KL(0.9), "linesearch"),
+                                        (U.Berg(0.8), U.Berg(1.1), "harmonic")]):
+        n, m = int(rng.integers(10, 30)), int(rng.integers(10, 30))
+        x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+        wa = rng.uniform(0.1, 1.0, n)
+        wb = rng.uniform(0.1, 1.0, m)
+        C = _monge(rng, x, y, 1)
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.ExplicitMatrix(C), e1, e2, eps=0.0)
+        try:  # the half-minima init can leave the Berg translation domain empty
+            U.fw_solve(prob, U.FwConfig(step, 5, 1e-12))
+            out[f"x{k}_big_newton_error"] = np.array(False)
+        except U.NewtonError:
+            out[f"x{k}_big_newton_error"] = np.array(True)
+        out[f"x{k}_Cbig"] = C
+        C = 0.2 * C
+        prob = U.UotProblem(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                            U.ExplicitMatrix(C), e1, e2, eps=0.0)
+        d0 = UF._default_init(prob)
+        dd, lam, plan, tr = ref_fw(prob, 30, step)
+        out[f"x{k}_x"], out[f"x{k}_y"], out[f"x{k}_a"], out[f"x{k}_b"], out[f"x{k}_C"] = x, y, wa, wb, C
+        out[f"x{k}_par"] = np.array([0 if isinstance(e1, U.KL) else 1, e1.rho,
+                                     0 if isinstance(e2, U.KL) else 1, e2.rho,
+                                     1.0 if step == "linesearch" else 0.0])
+        out[f"x{k}_f0"], out[f"x{k}_g0"] = d0.f, d0.g
+        out[f"x{k}_f"], out[f"x{k}_g"] = dd.f + lam, dd.g - lam
+        out[f"x{k}_h0"] = tr["h0"]
     save("berg_pfw.npz", **out)
 
 

@@ -211,3 +211,41 @@ def test_lambda_star_tolerance_arguments():
     assert P.lambda_star(prob, d, initial=tight) == pytest.approx(tight, abs=1e-10)
     with pytest.raises(P.NewtonError):
         P.lambda_star(prob, d, tol=1e-300, max_iters=1)
+
+
+@pytest.mark.parametrize("k", range(2))
+def test_berg_fw_explicit_cost(k):
+    """Explicit (negative-entry) Monge costs with Berg / mixed penalties on the
+    generic FW path: the oracle reads C(i, j), the primal's transport cost
+    too; h0 trace and final pair vs the reference's fixed-iteration loop."""
+    z = golden("berg_pfw.npz")
+    c1, r1, c2, r2, ls = z[f"x{k}_par"]
+    ent = {0: "kl", 1: "berg"}
+    step = "linesearch" if ls else "harmonic"
+    r = F.fw_solve_batched(z[f"x{k}_x"], z[f"x{k}_y"], z[f"x{k}_a"], z[f"x{k}_b"], float(r1),
+                           float(r2), 2.0, 30, step, f0=z[f"x{k}_f0"], g0=z[f"x{k}_g0"],
+                           C=z[f"x{k}_C"], ent1=ent[int(c1)], ent2=ent[int(c2)])
+    assert int(r.status[0].item()) == 0
+    ref_h0 = z[f"x{k}_h0"]
+    np.testing.assert_allclose(D.to_np(r.h0[0]), ref_h0, rtol=1e-9,
+                               atol=1e-12 * np.abs(ref_h0).max())
+    err = rel_err(D.to_np(r.f[0]), D.to_np(r.g[0]), z[f"x{k}_f"], z[f"x{k}_g"])
+    assert err < (1e-9 if step == "harmonic" else 1e-6), err
+
+
+@pytest.mark.parametrize("k", range(2))
+def test_berg_fw_explicit_newton_error_like_reference(k):
+    """With the unscaled negative cost the half-minima init can leave the Berg
+    translation domain empty: fw_solve raises NewtonError exactly when the
+    reference does (src/duality.py:187-190)."""
+    z = golden("berg_pfw.npz")
+    c1, r1, c2, r2, ls = z[f"x{k}_par"]
+    prob = P.UotProblem(P.DiscreteMeasure(z[f"x{k}_x"], z[f"x{k}_a"]),
+                        P.DiscreteMeasure(z[f"x{k}_y"], z[f"x{k}_b"]),
+                        P.ExplicitMatrix(z[f"x{k}_Cbig"]), _ent(c1, r1), _ent(c2, r2), eps=0.0)
+    cfg = P.FwConfig("linesearch" if ls else "harmonic", 5, 1e-12)
+    if bool(z[f"x{k}_big_newton_error"]):
+        with pytest.raises(P.NewtonError):
+            P.fw_solve(prob, cfg)
+    else:
+        assert P.fw_solve(prob, cfg).iterations >= 1
