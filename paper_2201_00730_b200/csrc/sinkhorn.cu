@@ -1207,7 +1207,11 @@ int num_sms() {
 // (SMs x resident CTAs per SM), while keeping >= 16 reduced indices per split.
 int choose_splits(int B, long nout, long nred, int out_per_block, int occ = 0) {
   const long out_blocks = (nout + out_per_block - 1) / out_per_block;
-  const long s_max = std::min(4096L, std::max(1L, nred / 16));
+  static const long rows_min = [] {  // rows per split floor (UOT_SPLIT_ROWS: tuning only)
+    const char* e = std::getenv("UOT_SPLIT_ROWS");
+    return e ? std::max(1L, std::atol(e)) : 16L;
+  }();
+  const long s_max = std::min(4096L, std::max(1L, nred / rows_min));
   if (occ <= 0) {
     const long target = (long)num_sms() * 24;
     long s = (target + out_blocks * B - 1) / (out_blocks * B);
