@@ -279,6 +279,17 @@ typedef struct uot_fw_desc {
   double* err_f;       /* optional [batch][max_iters]: ||f_t + lambda*_t - ref_f||_inf */
   const double* c;     /* optional [batch][n][m]: explicit cost (else |x - y|^p) */
   int32_t ent1, ent2;  /* UOT_ENT_KL (0, default) or UOT_ENT_BERG per marginal */
+  /* Parity / trace mode (all optional, NULL = off; KL path):
+   * step_in [batch][max_iters]: replay these step sizes instead of the step
+   *   rule (the reference's gamma_t, src/fw.py:223-230 / :295-297);
+   * away_in [batch][max_iters]: pairwise only, the away position in the
+   *   active list (insertion order, fw.py:287), -1 = no step that iteration;
+   * supp_hash / supp_nnz [batch][max_iters]: hash and entry count of every
+   *   iteration's oracle plan support (plan-hash definition below). */
+  const double* step_in;
+  const int32_t* away_in;
+  uint64_t* supp_hash;
+  int32_t* supp_nnz;
 } uot_fw_desc;
 
 int uot_fw1d_workspace_size(const uot_fw_desc* desc, size_t* bytes);
@@ -339,7 +350,23 @@ typedef struct uot_bary_desc {
   int32_t* count;
   double* summary;     /* [batch][2]: primal, dual of the last iteration */
   int32_t* status;
+  /* Parity / trace mode (optional, NULL = off): step_in [batch][max_iters]
+   * replays the reference's gamma_t (barycenter.py:397-411); supp_hash /
+   * supp_nnz [batch][max_iters] receive every iteration's plan support hash
+   * and entry count. */
+  const double* step_in;
+  uint64_t* supp_hash;
+  int32_t* supp_nnz;
 } uot_bary_desc;
+
+/* Plan-support hash of the trace mode (supp_hash above):
+ *   mix64(z): z += 0x9e3779b97f4a7c15; z = (z ^ z>>30) * 0xbf58476d1ce4e5b9;
+ *             z = (z ^ z>>27) * 0x94d049bb133111eb; return z ^ z>>31
+ *   entry with index tuple (i_0 .. i_{K-1}) (K = 2 for the 1-D OT plan):
+ *             mix64(sum_q mix64(((q + 1) << 40) | i_q))   (mod 2^64)
+ *   plan:     sum of the entry hashes over the positive-mass entries (mod 2^64)
+ * Equal supports give equal hashes; the tests compare them with the hash of
+ * the reference's SparsePlan / MultiPlan indices at every iteration. */
 
 int uot_mot1d_workspace_size(int32_t batch, int32_t k, int32_t n, size_t* bytes);
 /* f receives the sweep's dual potentials (barycenter.py:206-229). */

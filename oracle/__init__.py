@@ -150,6 +150,35 @@ def eval_h_kl(aw, bw, f, g, r1, r2, eps=0.0, smin_fn=None):
 
 
 # ---------------------------------------------------------------------------
+# Plan-support hash of the device trace mode (include/uot_b200.h, "plan-support
+# hash"): entry (i_0 .. i_{K-1}) -> mix64(sum_q mix64(((q+1) << 40) | i_q)),
+# plan -> wrapping sum over its entries.  numpy uint64 arithmetic wraps mod 2^64.
+
+
+def _mix64(z):
+    z = np.asarray(z, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def plan_hash(idx):
+    """idx: (E, K) entry index tuples (a SparsePlan as columns (i, j), or a
+    MultiPlan's indices).  Returns (hash as int64 bit pattern, entry count)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    if idx.size == 0:
+        return np.int64(0), 0
+    key = np.zeros(idx.shape[0], dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for q in range(idx.shape[1]):
+            key = key + _mix64((np.uint64(q + 1) << np.uint64(40)) | idx[:, q].astype(np.uint64))
+        tot = _mix64(key).sum(dtype=np.uint64)  # integer reductions wrap mod 2^64
+    return np.array([tot], dtype=np.uint64).view(np.int64)[0], int(idx.shape[0])
+
+
+# ---------------------------------------------------------------------------
 # sinkhorn.py
 
 
@@ -584,17 +613,19 @@ def eval_primal_1d(x, y, aw, bw, ii, jj, mass, p, r1, r2):
 
 
 def fw_fixed(x, y, aw, bw, r1, r2, iters, step="linesearch", p=2.0, f0=None, g0=None,
-             gap_tol=None):
+             gap_tol=None, gammas=None):
     """fw.py:176-232 (fw_solve) + _lmo :159-173 + _finalize :235-252.
 
     With ``gap_tol=None`` the early exit (:220-222) is removed so exactly
     ``iters`` iterations run (BASELINE fixed-iteration configs); otherwise
-    the reference's exit rule applies.  Returns a dict with the final
-    translated pair, the untranslated iterate, traces and the last plan."""
+    the reference's exit rule applies.  ``gammas`` replays given step sizes.
+    Returns a dict with the final translated pair, the untranslated iterate,
+    traces (incl. gamma and each iteration's plan_hash / entry count) and the
+    last plan."""
     x, y, aw, bw = _c64(x), _c64(y), _c64(aw), _c64(bw)
     f = np.zeros(aw.size) if f0 is None else _c64(f0).copy()
     g = np.zeros(bw.size) if g0 is None else _c64(g0).copy()
-    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap")}
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap", "gamma", "supp_hash", "nnz")}
     plan = None
     converged = False
     for t in range(iters):
@@ -607,6 +638,9 @@ def fw_fixed(x, y, aw, bw, r1, r2, iters, step="linesearch", p=2.0, f0=None, g0=
             raise ValueError("reweighted marginal masses disagree")
         ii, jj, mm, r, s = solve_ot_1d(x, y, ta, tb, p)
         plan = (ii, jj, mm)
+        hh, cc = plan_hash(np.stack([ii, jj], axis=1))
+        tr["supp_hash"].append(hh)
+        tr["nnz"].append(cc)
         fw_gap = float(np.dot(ta, r - f) + np.dot(tb, s - g))
         dual = h0_kl(aw, bw, f, g, r1, r2)
         primal = eval_primal_1d(x, y, aw, bw, ii, jj, mm, p, r1, r2)
@@ -616,10 +650,13 @@ def fw_fixed(x, y, aw, bw, r1, r2, iters, step="linesearch", p=2.0, f0=None, g0=
         if gap_tol is not None and primal - dual < gap_tol:
             converged = True
             break
-        if step == "harmonic":
+        if gammas is not None:
+            gam = float(gammas[t])
+        elif step == "harmonic":
             gam = 2.0 / (2.0 + t)
         else:
             gam = line_search_h0(aw, bw, f, g, r, s, r1, r2)
+        tr["gamma"].append(gam)
         f = (1.0 - gam) * f + gam * r
         g = (1.0 - gam) * g + gam * s
     lam = lambda_star_kl(aw, bw, f, g, r1, r2)
@@ -653,7 +690,7 @@ def pfw_fixed(x, y, aw, bw, r1, r2, iters, p=2.0, gap_tol=None):
     R = np.zeros((1, aw.size))
     Sg = np.zeros((1, bw.size))
     W = np.array([1.0])
-    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap", "gamma", "natoms")}
+    tr = {k: [] for k in ("h0", "fw_gap", "pd_gap", "gamma", "natoms", "supp_hash", "nnz")}
     plan = None
     converged = False
     for t in range(iters):
@@ -667,6 +704,9 @@ def pfw_fixed(x, y, aw, bw, r1, r2, iters, p=2.0, gap_tol=None):
             raise ValueError("reweighted marginal masses disagree")
         ii, jj, mm, r, s = solve_ot_1d(x, y, ta, tb, p)
         plan = (ii, jj, mm)
+        hh, cc = plan_hash(np.stack([ii, jj], axis=1))
+        tr["supp_hash"].append(hh)
+        tr["nnz"].append(cc)
         fw_gap = float(np.dot(ta, r - f) + np.dot(tb, s - g))
         dual = h0_kl(aw, bw, f, g, r1, r2)
         primal = eval_primal_1d(x, y, aw, bw, ii, jj, mm, p, r1, r2)
@@ -767,15 +807,18 @@ def plan_cost(idx, mass, xs, w):
     return float(np.dot(mass, ((pts - b[:, None]) ** 2) @ w))
 
 
-def fw_barycenter_fixed(xs, ws, w, rho, iters, step="linesearch", pots0=None, gap_tol=None):
+def fw_barycenter_fixed(xs, ws, w, rho, iters, step="linesearch", pots0=None, gap_tol=None,
+                        gammas=None):
     """barycenter.py:330-430 loop body (:361-411) without the exhaustive
     feasibility check of _finalize (:416-418, overflows at cfg5 scale,
-    SURVEY.md §0 finding 3).  ``gap_tol=None`` removes the early exit."""
+    SURVEY.md §0 finding 3).  ``gap_tol=None`` removes the early exit;
+    ``gammas`` replays given step sizes.  Traces include gamma and each
+    iteration's plan_hash / entry count."""
     w = _c64(w)
     rhos = w * float(rho)
     k = len(xs)
     pots = [np.zeros(len(a)) for a in xs] if pots0 is None else [_c64(p).copy() for p in pots0]
-    tr = {k_: [] for k_ in ("h0", "fw_gap", "pd_gap")}
+    tr = {k_: [] for k_ in ("h0", "fw_gap", "pd_gap", "gamma", "supp_hash", "nnz")}
     plan = None
     converged = False
     for t in range(iters):
@@ -786,6 +829,9 @@ def fw_barycenter_fixed(xs, ws, w, rho, iters, step="linesearch", pots0=None, ga
             raise ValueError("translated masses disagree; translation broken")
         idx, mass, atoms = solve_mot_1d(xs, tilted, w)
         plan = (idx, mass)
+        hh, cc = plan_hash(idx)
+        tr["supp_hash"].append(hh)
+        tr["nnz"].append(cc)
         fw_gap = float(sum(np.dot(tw, r - f) for tw, r, f in zip(tilted, atoms, pots)))
         dual = h_value(ws, rhos, pots)
         marg = []
@@ -801,7 +847,9 @@ def fw_barycenter_fixed(xs, ws, w, rho, iters, step="linesearch", pots0=None, ga
         if gap_tol is not None and primal - dual < gap_tol:
             converged = True
             break
-        if step == "harmonic":
+        if gammas is not None:
+            gam = float(gammas[t])
+        elif step == "harmonic":
             gam = 2.0 / (2.0 + t)
         else:
 
@@ -810,6 +858,7 @@ def fw_barycenter_fixed(xs, ws, w, rho, iters, step="linesearch", pots0=None, ga
 
             gam = ternary_max(value, 0.0, 1.0, iters=60)
             gam = max(((value(c), c) for c in (gam, 0.0, 1.0)), key=lambda z: z[0])[1]
+        tr["gamma"].append(gam)
         pots = [(1.0 - gam) * f + gam * r for f, r in zip(pots, atoms)]
     lam = multimarginal_lambda(pots, ws, w, rho)
     return {

@@ -51,6 +51,7 @@ class FwDesc(ctypes.Structure):
         ("ei", _vp), ("ej", _vp), ("em", _vp), ("count", _vp), ("summary", _vp),
         ("status", _vp), ("step_size", _vp), ("natoms", _vp), ("ref_f", _vp), ("err_f", _vp), ("c", _vp),
         ("ent1", _i32), ("ent2", _i32),
+        ("step_in", _vp), ("away_in", _vp), ("supp_hash", _vp), ("supp_nnz", _vp),
     ]
 
 
@@ -62,6 +63,7 @@ class BaryDesc(ctypes.Structure):
         ("x", _vp), ("a", _vp), ("f", _vp),
         ("h0", _vp), ("fw_gap", _vp), ("pd_gap", _vp), ("iterations", _vp),
         ("idx", _vp), ("mass", _vp), ("count", _vp), ("summary", _vp), ("status", _vp),
+        ("step_in", _vp), ("supp_hash", _vp), ("supp_nnz", _vp),
     ]
 
 

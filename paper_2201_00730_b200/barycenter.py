@@ -335,12 +335,18 @@ class BaryBatchResult:
     count: object
     summary: object
     status: object
+    supp_hash: object = None
+    supp_nnz: object = None
+    replay: object = None
 
 
 def fw_barycenter_batched(x, a, omega, rho=1.0, max_iters=1000, step="linesearch",
-                          gap_tol=1e-6, early_exit=False, f0=None, lens=None, stream=None):
+                          gap_tol=1e-6, early_exit=False, f0=None, lens=None, stream=None,
+                          step_in=None, trace_support=False):
     """Batched KL barycenter FW on device: x, a [B, K, n] (sorted rows).
-    Returns device tensors; f is translated (report.final)."""
+    Returns device tensors; f is translated (report.final).  ``step_in``
+    [B, max_iters] replays given step sizes (the reference's gamma_t);
+    ``trace_support`` records every iteration's plan-support hash / count."""
     t = D.torch()
     lib = _lib.load()
     x = D.to_dev(x, t.float64)
@@ -366,6 +372,9 @@ def fw_barycenter_batched(x, a, omega, rho=1.0, max_iters=1000, step="linesearch
         fw_gap=_lib.ptr(r.fw_gap), pd_gap=_lib.ptr(r.pd_gap), iterations=_lib.ptr(r.iterations),
         idx=_lib.ptr(r.idx), mass=_lib.ptr(r.mass), count=_lib.ptr(r.count),
         summary=_lib.ptr(r.summary), status=_lib.ptr(r.status))
+    from .fw import _trace_args
+
+    _trace_args(desc, r, B, max_iters, step_in, None, trace_support, x.device)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_bary_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)

@@ -57,6 +57,25 @@ constexpr double LN2 = 0.69314718055994530942;
 constexpr double LOG2E = 1.44269504088896340736;
 
 // ---------------------------------------------------------------------------
+// Plan-support hash (trace mode, parity tests only).  A plan entry with index
+// tuple (i_0 .. i_{K-1}) hashes to mix64(sum_q mix64(((q+1) << 40) | i_q));
+// the plan hashes to the wrapping sum over its positive-mass entries, so the
+// value is independent of the order in which threads find the entries and
+// equal plans give equal hashes (tests/golden/make_golden.py: plan_hash).
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long coord_key(int q, int i) {
+  return mix64(((unsigned long long)(q + 1) << 40) | (unsigned long long)(unsigned)i);
+}
+__host__ __device__ __forceinline__ unsigned long long pair_hash(int i, int j) {
+  return mix64(coord_key(0, i) + coord_key(1, j));
+}
+
+// ---------------------------------------------------------------------------
 // Warp / block reductions.
 
 template <typename T>

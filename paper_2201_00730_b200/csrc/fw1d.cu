@@ -143,6 +143,22 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
   a.ref_f = d->ref_f;
   a.err_f = d->err_f;
   a.C = d->c;
+  a.step_in = d->step_in;
+  a.away_in = d->away_in;
+  a.supp_hash = reinterpret_cast<unsigned long long*>(d->supp_hash);
+  a.supp_nnz = d->supp_nnz;
+  if ((a.supp_hash == nullptr) != (a.supp_nnz == nullptr)) {
+    set_error("uot_fw1d_run: supp_hash and supp_nnz go together");
+    return UOT_INVALID;
+  }
+  if (gen && (a.step_in != nullptr || a.supp_hash != nullptr)) {
+    set_error("uot_fw1d_run: the replay / support-trace mode runs KL/KL penalties");
+    return UOT_INVALID;
+  }
+  if (a.away_in != nullptr && (d->step != UOT_STEP_PAIRWISE || a.step_in == nullptr)) {
+    set_error("uot_fw1d_run: away_in replays pairwise steps together with step_in");
+    return UOT_INVALID;
+  }
   if (gen) return fwk::run_fw_generic(a, d->batch, d->ent1, d->ent2, ws, ws_bytes,
                                      (cudaStream_t)stream);
   if (d->step == UOT_STEP_PAIRWISE) {

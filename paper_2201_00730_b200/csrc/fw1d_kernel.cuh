@@ -77,6 +77,12 @@ struct FwArgs {
   const double* ref_f;  // optional [batch][n]: reference potential
   double* err_f;        // optional [batch][max_iters]: sup error of the translated iterate
   const double* C;      // optional [batch][n][m]: explicit cost (PK = 3), else |x - y|^p
+  // parity / trace mode (optional): replayed step sizes and away positions,
+  // per-iteration plan-support hash and entry count
+  const double* step_in;
+  const int* away_in;
+  unsigned long long* supp_hash;
+  int* supp_nnz;
 };
 
 static __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
@@ -344,6 +350,53 @@ struct Cta {
     if (threadIdx.x == 0) *count = base;
     __syncthreads();
   }
+
+  // Support hash and entry count of the current merge (trace mode): entry
+  // after source event i is (i + 1, rkA[i]), after target event l is
+  // (rkB[l], l + 1), the first is (0, 0); its mass is the next merged
+  // breakpoint minus this one, both capped at the total (extract_plan's
+  // rule), and the next breakpoint is the smaller of the two sides' next
+  // unconsumed ones.
+  __device__ void plan_hash(double total, unsigned long long* out_h, int* out_n) {
+    __shared__ unsigned long long hs;
+    __shared__ int ns;
+    if (threadIdx.x == 0) {
+      hs = 0ull;
+      ns = 0;
+    }
+    __syncthreads();
+    const int na = n - 1, nb = m - 1;
+    unsigned long long h = 0ull;
+    int cnt = 0;
+    auto entry = [&](int i, int j, double lo, double nxt) {
+      if (fmin(nxt, total) - fmin(lo, total) > 0.0) {
+        h += pair_hash(i, j);
+        ++cnt;
+      }
+    };
+    auto va = [&](int i) { return i < na ? sA[i] : CUDART_INF; };
+    auto vb = [&](int j) { return j < nb ? sB[j] : CUDART_INF; };
+    if (threadIdx.x == 0) entry(0, 0, 0.0, fmin(va(0), vb(0)));
+    for (int i = threadIdx.x; i < na; i += FW_THREADS) {
+      const int j = rkA[i];
+      entry(i + 1, j, sA[i], fmin(va(i + 1), vb(j)));
+    }
+    for (int l = threadIdx.x; l < nb; l += FW_THREADS) {
+      const int k = rkB[l];
+      entry(k, l + 1, sB[l], fmin(va(k), vb(l + 1)));
+    }
+    h = warp_sum(h);
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&hs, h);
+      atomicAdd(&ns, cnt);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *out_h = hs;
+      *out_n = ns;
+    }
+  }
 };
 
 // Pairwise FW state shared by all threads of the CTA: active atoms and
@@ -439,7 +492,10 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
     }
   }
   __syncthreads();
-  const int away = away_s, hit = hit_s;
+  const long tix = (long)b * A.max_iters + t;
+  const bool replay = A.away_in != nullptr && A.step_in != nullptr;
+  const int away = replay ? max(__ldg(A.away_in + tix), 0) : away_s;
+  const int hit = hit_s;
   const int aslot = __ldcg(A.act + sb0 + away);
   const double* ra = AT + (long)aslot * nm;
   double dA[EPT], dB[EPT];
@@ -463,7 +519,9 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
   bops::block_red<FW_NW, 4, 4>(mom, mxs, ping.next());
   const double gmax = __ldcg(A.wts + sb0 + aslot);
   double gam = 0.0;
-  if (!(gmax <= 0.0 || (mxs[0] < 1e-12 && mxs[1] < 1e-12))) {  // fw.py:291-293
+  if (replay) {  // the reference's away atom and transfer (no step: away < 0)
+    gam = __ldg(A.away_in + tix) < 0 ? 0.0 : __ldg(A.step_in + tix);
+  } else if (!(gmax <= 0.0 || (mxs[0] < 1e-12 && mxs[1] < 1e-12))) {  // fw.py:291-293
     // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
     // on [0, gmax]; centred moments as in the FW line search
     const double ca = mom[0] / mta, cb = mom[2] / mtb;
@@ -746,6 +804,9 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       status = UOT_MASS_BALANCE;
       break;
     }
+    if (A.supp_hash != nullptr)
+      c.plan_hash(fmin(mta, mtb), A.supp_hash + (long)b * A.max_iters + t,
+                  A.supp_nnz + (long)b * A.max_iters + t);
     // --- gaps, primal and line-search moments at gamma = 0.  log(ta/alpha)
     // = -(f + lam)/r1 exactly, so the KL terms of the oracle plan (whose
     // marginals are ta, tb) need no logarithm (entropies.py:123-131).
@@ -798,7 +859,9 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     if (stop) break;
     // --- step size
     double gam;
-    if (A.step == UOT_STEP_HARMONIC) {
+    if (A.step_in != nullptr) {
+      gam = __ldg(A.step_in + (long)b * A.max_iters + t);  // replayed gamma_t
+    } else if (A.step == UOT_STEP_HARMONIC) {
       gam = 2.0 / (2.0 + t);  // fw.py:223-224
     } else {
       // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb).
@@ -869,11 +932,13 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       }
     }
     if (A.step_size != nullptr && threadIdx.x == 0) A.step_size[(long)b * A.max_iters + t] = gam;
-    // --- update (fw.py:227-230) and the next shift bounds
+    // --- update (fw.py:227-230) and the next shift bounds, rounded as numpy
+    // rounds (1 - gamma) f + gamma r: two products and a sum, no FMA
+    const double omg = 1.0 - gam;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      f[e] = (1.0 - gam) * f[e] + gam * r[e];
-      g[e] = (1.0 - gam) * g[e] + gam * s[e];
+      f[e] = __dadd_rn(__dmul_rn(omg, f[e]), __dmul_rn(gam, r[e]));
+      g[e] = __dadd_rn(__dmul_rn(omg, g[e]), __dmul_rn(gam, s[e]));
     }
     if (sha > -CUDART_INF) sha = (1.0 - gam) * sha + gam * mr[0];
     if (shb > -CUDART_INF) shb = (1.0 - gam) * shb + gam * mr[1];

@@ -91,6 +91,10 @@ struct MotArgs {
   double* tmass;          // [B][K] tilted masses
   double* samp;           // [B][K][SS] regular samples (values)
   int* sampt;             // [B][K][SS] (indices)
+  // parity / trace mode (optional)
+  const double* step_in;  // [B][max_iters] replayed gamma_t
+  unsigned long long* supp_hash;  // [B][max_iters] plan-support hash
+  int* supp_nnz;          // [B][max_iters] plan entry count
 };
 
 __device__ __forceinline__ int list_len(const MotArgs& A, int q) {
@@ -1002,7 +1006,9 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     return;
   }
   double gam;
-  if (A.step == UOT_STEP_HARMONIC) {
+  if (A.step_in != nullptr) {
+    gam = __ldg(A.step_in + (long)b * A.max_iters + t);  // replayed gamma_t
+  } else if (A.step == UOT_STEP_HARMONIC) {
     gam = 2.0 / (2.0 + t);
   } else {
     // minimise Phi(gamma) = sum_k rho_k LSE_{a_k}(-(f_k + gamma d_k)/rho_k):
@@ -1056,8 +1062,10 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
       }
     }
   }
+  // barycenter.py:409-411, rounded as numpy rounds it (two products, a sum)
+  const double omg = 1.0 - gam;
 #pragma unroll
-  for (int e = 0; e < EPT; ++e) fv[e] = (1.0 - gam) * fv[e] + gam * rv[e];  // barycenter.py:409-411
+  for (int e = 0; e < EPT; ++e) fv[e] = __dadd_rn(__dmul_rn(omg, fv[e]), __dmul_rn(gam, rv[e]));
   MOT_STAMP(4);
   if constexpr (StageRun<EPT>::ON) {  // coalesced: the stage buffer is free here
     stage_put<EPT>(stg, fv);
@@ -1132,7 +1140,10 @@ __device__ __forceinline__ double next_event_value(const MotArgs& A, int b, int 
   return v;
 }
 
-template <bool WRITE>
+// WRITE: materialise tuples + masses; HASH (trace mode, WRITE false): add
+// every kept entry's tuple hash and the entry count into supp_hash / supp_nnz
+// of iteration A.t (zeroed by the host before the run).
+template <bool WRITE, bool HASH = false>
 __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ int lo_s[KMAX + 1], cnt_s[KMAX + 1];
@@ -1154,6 +1165,7 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
     for (int r = 0; r < s; ++r) out_base += A.bcount[(long)b * A.S + r];
   }
   int kept_run = 0;
+  unsigned long long hacc = 0ull;
   for (int c0 = 0; c0 < nst; c0 += BT) {
     const int c = c0 + threadIdx.x;
     const int e = c + first;  // state after event e (e = -1: initial state)
@@ -1181,40 +1193,43 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
       tot += scan_s[w];
     }
     __syncthreads();
-    if (WRITE && keep) {
-      const int pos = out_base + kept_run + offw + incl - 1;
-      if (pos < A.cap_e) {
-        A.pmass[(long)b * A.cap_e + pos] = mass;
-        // tuple: lo_q + #{events of list q among sorted events [0, e]}
-        int* row = A.pidx + ((long)b * A.cap_e + pos) * K;
-        for (int q = 0; q < K; ++q) {
-          int cnt = 0;
-          // events are sorted; count list-q codes in [0, e] by binary search
-          // on the (list, index) code within the sorted range is not
-          // monotone, so count by a linear scan of the run of list q via
-          // its position: the number of q-events before e equals the number
-          // of q-events with key <= key[e] (keys of one list are ordered).
-          const int c_lo = cnt_s[q], c_len = cnt_s[q + 1] - c_lo;
-          if (e >= 0 && c_len > 0) {
-            const double* Aq = A.A + ((long)b * K + q) * n + lo_s[q];
-            const int eq = ev_list(code[e]);
-            const int et = ev_index(code[e]);
-            int lo2 = 0, hi2 = c_len;
-            while (lo2 < hi2) {  // #{j : (Aq[j], q, lo+j) <= (key[e], eq, et)}
-              const int mid = (lo2 + hi2) >> 1;
-              const bool le = !key_less(key[e], eq, et, Aq[mid], q, lo_s[q] + mid);
-              if (le)
-                lo2 = mid + 1;
-              else
-                hi2 = mid;
-            }
-            cnt = lo2;
+    const int pos = out_base + kept_run + offw + incl - 1;
+    if ((WRITE && keep && pos < A.cap_e) || (HASH && keep)) {
+      if (WRITE) A.pmass[(long)b * A.cap_e + pos] = mass;
+      // tuple: lo_q + #{events of list q among sorted events [0, e]}; the
+      // events of one list are ordered, so the count is a binary search of
+      // (key[e], list, index) among list q's keys in this range.
+      unsigned long long tkey = 0ull;
+      for (int q = 0; q < K; ++q) {
+        int cnt = 0;
+        const int c_lo = cnt_s[q], c_len = cnt_s[q + 1] - c_lo;
+        if (e >= 0 && c_len > 0) {
+          const double* Aq = A.A + ((long)b * K + q) * n + lo_s[q];
+          const int eq = ev_list(code[e]);
+          const int et = ev_index(code[e]);
+          int lo2 = 0, hi2 = c_len;
+          while (lo2 < hi2) {  // #{j : (Aq[j], q, lo+j) <= (key[e], eq, et)}
+            const int mid = (lo2 + hi2) >> 1;
+            const bool le = !key_less(key[e], eq, et, Aq[mid], q, lo_s[q] + mid);
+            if (le)
+              lo2 = mid + 1;
+            else
+              hi2 = mid;
           }
-          row[q] = lo_s[q] + cnt;
+          cnt = lo2;
         }
+        if (WRITE) A.pidx[((long)b * A.cap_e + pos) * K + q] = lo_s[q] + cnt;
+        if (HASH) tkey += coord_key(q, lo_s[q] + cnt);
       }
+      if (HASH) hacc += mix64(tkey);
     }
     kept_run += tot;
+  }
+  if (HASH) {
+    hacc = warp_sum(hacc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(A.supp_hash + (long)b * A.max_iters + A.t, hacc);
+    if (threadIdx.x == 0) atomicAdd(A.supp_nnz + (long)b * A.max_iters + A.t, kept_run);
+    return;
   }
   if (!WRITE && threadIdx.x == 0) A.bcount[(long)b * A.S + s] = kept_run;
   if (WRITE && threadIdx.x == 0 && s == A.S - 1) A.pcount[b] = min(out_base + kept_run, A.cap_e);
@@ -1395,6 +1410,13 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
                                     (int)p.bucket_smem));
   mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
   UOT_CHECK_LAUNCH();
+  if (a.supp_hash != nullptr) {  // trace mode: this iteration's plan support
+    UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<false, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)p.bucket_smem));
+    mot_plan<false, true><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+    UOT_CHECK_LAUNCH();
+  }
   UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch,
                          StageRun<EPT>::ON ? 2 * StageRun<EPT>::BYTES : 0, st, a));
   return UOT_OK;
@@ -1643,6 +1665,18 @@ extern "C" int uot_bary_run(const uot_bary_desc* d, void* workspace, size_t work
   A.pmass = d->mass;
   A.pcount = d->count;
   A.cap_e = d->k * (d->n - 1) + 1;
+  A.step_in = d->step_in;
+  A.supp_hash = reinterpret_cast<unsigned long long*>(d->supp_hash);
+  A.supp_nnz = d->supp_nnz;
+  if ((A.supp_hash == nullptr) != (A.supp_nnz == nullptr)) {
+    set_error("uot_bary_run: supp_hash and supp_nnz go together");
+    return UOT_INVALID;
+  }
+  if (A.supp_hash != nullptr) {
+    const size_t bt = (size_t)d->batch * d->max_iters;
+    UOT_CUDA_TRY(cudaMemsetAsync(A.supp_hash, 0, sizeof(unsigned long long) * bt, st));
+    UOT_CUDA_TRY(cudaMemsetAsync(A.supp_nnz, 0, sizeof(int) * bt, st));
+  }
   return dispatch(A, p, st, true);
 }
 

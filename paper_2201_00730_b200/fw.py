@@ -67,11 +67,35 @@ class FwBatchResult:
     natoms: object = None  # pairwise: active atoms after each iteration
     err_f: object = None   # with ref_f: translated-iterate error per iteration
     cost: object = None    # explicit cost matrix kept alive for the launch
+    supp_hash: object = None  # trace_support: per-iteration plan-support hash (int64 view)
+    supp_nnz: object = None   # trace_support: per-iteration plan entry count
+    replay: object = None     # replayed step sizes / away positions kept alive
+
+
+def _trace_args(desc, r, B, T, step_in, away_in, trace_support, device):
+    """Fill the replay / support-trace fields of an FW or barycenter descriptor."""
+    t = D.torch()
+    keep = []
+    if step_in is not None:
+        st = D.to_dev(step_in, t.float64).reshape(B, T).contiguous()
+        keep.append(st)
+        desc.step_in = _lib.ptr(st)
+    if away_in is not None:
+        aw = D.to_dev(away_in, t.int32).reshape(B, T).contiguous()
+        keep.append(aw)
+        desc.away_in = _lib.ptr(aw)
+    if trace_support:
+        r.supp_hash = t.zeros((B, T), dtype=t.int64, device=device)
+        r.supp_nnz = t.zeros((B, T), dtype=t.int32, device=device)
+        desc.supp_hash = _lib.ptr(r.supp_hash)
+        desc.supp_nnz = _lib.ptr(r.supp_nnz)
+    r.replay = keep
 
 
 def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step="linesearch",
                      gap_tol=1e-6, early_exit=False, f0=None, g0=None, stream=None, ref_f=None,
-                     C=None, ent1="kl", ent2="kl"):
+                     C=None, ent1="kl", ent2="kl", step_in=None, away_in=None,
+                     trace_support=False):
     """Batched FW on device: x, a [B, N]; y, b [B, M] sorted supports;
     ``C`` [B, N, M] (optional) an explicit Monge cost instead of |x - y|^p;
     ``ent1`` / ``ent2`` "kl" or "berg" (Berg runs the generic path,
@@ -79,7 +103,12 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
 
     ``early_exit=False`` runs exactly ``max_iters`` iterations per problem
     (BASELINE fixed-iteration configs); True applies fw.py:220-222 per
-    problem.  f/g come back translated by lambda* (report.final)."""
+    problem.  f/g come back translated by lambda* (report.final).
+
+    Parity mode: ``step_in`` [B, max_iters] replays given step sizes (the
+    reference's gamma_t) and, for pairwise, ``away_in`` [B, max_iters] the
+    away positions (-1 = no step); ``trace_support`` records every
+    iteration's plan-support hash and entry count (include/uot_b200.h)."""
     t = D.torch()
     lib = _lib.load()
     x, y, a, b = (D.to_dev(v, t.float64) for v in (x, y, a, b))
@@ -125,6 +154,7 @@ def fw_solve_batched(x, y, a, b, rho1=1.0, rho2=1.0, p=2.0, max_iters=500, step=
         desc.c = _lib.ptr(r.cost)
     codes = {"kl": _lib.ENT_KL, "berg": _lib.ENT_BERG}
     desc.ent1, desc.ent2 = codes[ent1], codes[ent2]
+    _trace_args(desc, r, B, max_iters, step_in, away_in, trace_support, x.device)
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_fw1d_workspace_size(ctypes.byref(desc), ctypes.byref(size)))
     ws = D.workspace(size.value)

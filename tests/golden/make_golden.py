@@ -32,6 +32,7 @@ from uotkit import barycenter as UB  # noqa: E402
 from uotkit import fw as UF  # noqa: E402
 from uotkit import sinkhorn as US  # noqa: E402
 
+import oracle as O  # noqa: E402  (plan_hash only)
 from paper_2201_00730_b200 import synthetic as S  # noqa: E402
 
 
@@ -1110,10 +1111,157 @@ def gen_berg_pfw():
     save("berg_pfw.npz", **out)
 
 
+
+# ---------------------------------------------------------------------------
+# Replay fixtures (round 2): the reference loops of fw.npz / pfw.npz /
+# barycenter.npz re-run with every iteration's step size gamma_t (and, for
+# pairwise, the away position) and the hash + entry count of every
+# iteration's oracle plan recorded, so the device can replay the reference's
+# steps and be compared at every iteration (tests/test_replay_gpu.py).
+
+
+def _hash_pairs(plan):
+    return O.plan_hash(np.stack([plan.source_idx, plan.target_idx], axis=1))
+
+
+def ref_fw_rec(prob, iters, step):
+    """fw.py:176-232 loop body (as ref_fw) recording gamma_t and the plans."""
+    d = UF._default_init(prob)
+    rec = {k: [] for k in ("h0", "gamma", "hash", "nnz")}
+    for t in range(iters):
+        ta, tb, plan, atom, fw_gap = UF._lmo(prob, d)
+        rec["h0"].append(UF._h0(prob, d.f, d.g))
+        h, c = _hash_pairs(plan)
+        rec["hash"].append(h)
+        rec["nnz"].append(c)
+        gamma = 2.0 / (2.0 + t) if step == "harmonic" else UF.line_search_h0(prob, d, atom)
+        rec["gamma"].append(gamma)
+        d = U.DualPair((1.0 - gamma) * d.f + gamma * atom.f, (1.0 - gamma) * d.g + gamma * atom.g)
+    return d, {k: np.asarray(v) for k, v in rec.items()}
+
+
+def ref_pfw_rec(prob, iters):
+    """fw.py:275-310 (_pfw_iteration), restated step by step on the
+    reference's own helpers (_lmo, _h0, _active_scores, ternary_max,
+    _merge_atom) so the away position and the transfer can be recorded;
+    away = -1 when the iteration makes no step (fw.py:291-293, :298-299)."""
+    d0 = UF._default_init(prob)
+    store = UF.AtomStore(d0.f[None, :], d0.g[None, :], np.array([1.0]))
+    rec = {k: [] for k in ("h0", "gamma", "away", "hash", "nnz", "natoms")}
+    for _ in range(iters):
+        d = store.current()
+        ta, tb, plan, atom, fw_gap = UF._lmo(prob, d)
+        rec["h0"].append(UF._h0(prob, d.f, d.g))
+        h, c = _hash_pairs(plan)
+        rec["hash"].append(h)
+        rec["nnz"].append(c)
+        scores = UF._active_scores(store, ta, tb)
+        away = int(np.argmin(scores))
+        max_step = float(store.weights[away])
+        dr = atom.f - store.r_atoms[away]
+        ds = atom.g - store.s_atoms[away]
+        gamma = 0.0
+        if not (max_step <= 0.0 or (np.abs(dr).max() < UF.ATOM_DEDUP_TOL
+                                    and np.abs(ds).max() < UF.ATOM_DEDUP_TOL)):
+            def value(gg):
+                return UF._h0(prob, d.f + gg * dr, d.g + gg * ds)
+            gamma = UF.ternary_max(value, 0.0, max_step, iters=60)
+            gamma = max(((value(c_), c_) for c_ in (gamma, 0.0, max_step)), key=lambda z: z[0])[1]
+        if gamma > 0.0:
+            w = store.weights.copy()
+            w[away] = max(w[away] - gamma, 0.0)
+            r_atoms, s_atoms, w = UF._merge_atom(store.r_atoms, store.s_atoms, w, atom.f, atom.g,
+                                                 gamma)
+            keep = w > 0
+            if not keep.all():
+                r_atoms, s_atoms, w = r_atoms[keep], s_atoms[keep], w[keep]
+            store = UF.AtomStore(r_atoms, s_atoms, w)
+            rec["away"].append(away)
+        else:
+            rec["away"].append(-1)
+        rec["gamma"].append(gamma)
+        rec["natoms"].append(store.weights.size)
+    return store.current(), {k: np.asarray(v) for k, v in rec.items()}
+
+
+def ref_barycenter_rec(problem, iters, step):
+    """barycenter.py:361-411 (as ref_barycenter) recording gamma_t and the plans."""
+    inputs, w = problem.inputs, problem.omega
+    rhos = problem.rhos()
+    costfn = UB.barycentric_cost_fn(w)
+    pots = [np.zeros(len(a)) for a in inputs]
+    rec = {k: [] for k in ("h0", "gamma", "hash", "nnz")}
+    for t in range(iters):
+        lam = UB.multimarginal_lambda(UB.MultiDual(tuple(pots)), inputs, w, problem.rho)
+        tilted = [a.weights * np.exp(-(f + lk) / rk) for a, f, lk, rk in zip(inputs, pots, lam, rhos)]
+        plan, atoms = UB.solve_mot_1d([U.DiscreteMeasure(a.points, tw) for a, tw in zip(inputs, tilted)],
+                                      w, costfn)
+        rec["h0"].append(UB._h_value(inputs, rhos, pots))
+        h, c = O.plan_hash(plan.indices)
+        rec["hash"].append(h)
+        rec["nnz"].append(c)
+        if step == "harmonic":
+            gamma = 2.0 / (2.0 + t)
+        else:
+            def value(g):
+                return UB._h_value(inputs, rhos, [(1.0 - g) * f + g * r for f, r in zip(pots, atoms.potentials)])
+            gamma = UF.ternary_max(value, 0.0, 1.0, iters=60)
+            gamma = max(((value(c_), c_) for c_ in (gamma, 0.0, 1.0)), key=lambda z: z[0])[1]
+        rec["gamma"].append(gamma)
+        pots = [(1.0 - gamma) * f + gamma * r for f, r in zip(pots, atoms.potentials)]
+    return pots, {k: np.asarray(v) for k, v in rec.items()}
+
+
+def gen_replay():
+    out = {}
+    z = np.load(os.path.join(HERE, "fw.npz"))
+    for k in z["cases"]:
+        r1, r2, p, iters, ls = z[f"c{k}_par"]
+        step = "linesearch" if ls else "harmonic"
+        prob = U.UotProblem(U.DiscreteMeasure(z[f"c{k}_x"], z[f"c{k}_a"]),
+                            U.DiscreteMeasure(z[f"c{k}_y"], z[f"c{k}_b"]),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=0.0)
+        t0 = time.time()
+        d, rec = ref_fw_rec(prob, int(iters), step)
+        out[f"fw{k}_f"], out[f"fw{k}_g"] = d.f, d.g
+        for kk, v in rec.items():
+            out[f"fw{k}_{kk}"] = v
+        print(f"  replay fw {k}: {step} x{int(iters)} in {time.time() - t0:.1f}s", flush=True)
+    z = np.load(os.path.join(HERE, "pfw.npz"))
+    for k in z["cases"]:
+        r1, r2, p, iters = z[f"c{k}_par"]
+        prob = U.UotProblem(U.DiscreteMeasure(z[f"c{k}_x"], z[f"c{k}_a"]),
+                            U.DiscreteMeasure(z[f"c{k}_y"], z[f"c{k}_b"]),
+                            U.PowerDistance(p), U.KL(r1), U.KL(r2), eps=0.0)
+        t0 = time.time()
+        d, rec = ref_pfw_rec(prob, int(iters))
+        assert np.array_equal(rec["natoms"], z[f"c{k}_natoms"])  # same loop as ref_pfw
+        out[f"pfw{k}_f"], out[f"pfw{k}_g"] = d.f, d.g
+        for kk, v in rec.items():
+            out[f"pfw{k}_{kk}"] = v
+        print(f"  replay pfw {k}: x{int(iters)} in {time.time() - t0:.1f}s", flush=True)
+    z = np.load(os.path.join(HERE, "barycenter.npz"))
+    for k in z["cases"]:
+        kk_ = int(z[f"c{k}_k"])
+        rho, iters, ls = z[f"c{k}_par"]
+        inputs = tuple(U.DiscreteMeasure(z[f"c{k}_x{q}"], z[f"c{k}_a{q}"]) for q in range(kk_))
+        problem = U.BarycenterProblem(inputs, z[f"c{k}_w"], float(rho))
+        t0 = time.time()
+        pots, rec = ref_barycenter_rec(problem, int(iters), "linesearch" if ls else "harmonic")
+        for q in range(kk_):
+            out[f"bary{k}_f{q}"] = pots[q]
+        for kk, v in rec.items():
+            out[f"bary{k}_{kk}"] = v
+        print(f"  replay barycenter {k}: K={kk_} x{int(iters)} in {time.time() - t0:.1f}s", flush=True)
+    out["fw_cases"] = np.load(os.path.join(HERE, "fw.npz"))["cases"]
+    out["pfw_cases"] = np.load(os.path.join(HERE, "pfw.npz"))["cases"]
+    out["bary_cases"] = np.load(os.path.join(HERE, "barycenter.npz"))["cases"]
+    save("replay.npz", **out)
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw", "replay"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -237,3 +237,24 @@ def test_anderson_runs():
                                        int(depth), reg, z[f"c{k}_f0"], z[f"c{k}_g0"], ents=ents)
         assert rel_err(f, g, z[f"c{k}_f"], z[f"c{k}_g"]) < 1e-9, (k, var)
         np.testing.assert_allclose(dl, z[f"c{k}_delta"], rtol=1e-5, atol=1e-11)
+
+
+def test_oracle_replay_hashes_match_reference():
+    """The oracle's plan_hash of its own plans, with the reference's step
+    sizes replayed, equals the hash the reference's plans gave (replay.npz),
+    at every iteration: pins the hash definition the device trace uses."""
+    z, zr = golden("fw.npz"), golden("replay.npz")
+    for k in (0, 1, 4):
+        r1, r2, p, iters, ls = z[f"c{k}_par"]
+        out = O.fw_fixed(z[f"c{k}_x"], z[f"c{k}_y"], z[f"c{k}_a"], z[f"c{k}_b"], r1, r2,
+                         int(iters), p=p, gammas=zr[f"fw{k}_gamma"])
+        np.testing.assert_array_equal(out["supp_hash"], zr[f"fw{k}_hash"])
+        np.testing.assert_array_equal(out["nnz"], zr[f"fw{k}_nnz"])
+    zb = golden("barycenter.npz")
+    for k in (0, 3):
+        kk = int(zb[f"c{k}_k"])
+        rho, iters, ls = zb[f"c{k}_par"]
+        out = O.fw_barycenter_fixed([zb[f"c{k}_x{q}"] for q in range(kk)],
+                                    [zb[f"c{k}_a{q}"] for q in range(kk)], zb[f"c{k}_w"],
+                                    float(rho), int(iters), gammas=zr[f"bary{k}_gamma"])
+        np.testing.assert_array_equal(out["supp_hash"], zr[f"bary{k}_hash"])
