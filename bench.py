@@ -42,7 +42,26 @@ def load_peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return json.load(fh), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+        return ({"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": None},
+                "fallback (B200_PROFILING.md)")
+
+
+PROBES_PATH = os.path.join(ROOT, "profiles", "r2_probes.json")
+
+
+def load_probes():
+    """Committed MUFU / DFMA probe results (scripts/run_probes.py on a B200):
+    the FIXED denominators of the exp-bound rooflines."""
+    try:
+        with open(PROBES_PATH) as fh:
+            pr = json.load(fh)
+        return {"ex2_per_s": pr["ex2"]["per_s_median"], "dfma_per_s": pr["dfma"]["per_s_median"],
+                "source": "profiles/r2_probes.json (uot_probe_mufu_ex2 / uot_probe_dfma, "
+                          f"median at {pr['ex2']['clocks'].get('sm_mhz')} MHz)"}
+    except (OSError, KeyError, ValueError):
+        # nominal: 16 ex2/clk/SM and 64 DFMA/clk/SM x 148 SMs x 1965 MHz
+        return {"ex2_per_s": 16 * 148 * 1.965e9, "dfma_per_s": 64 * 148 * 1.965e9,
+                "source": "nominal (no committed probe file)"}
 
 
 class ClockSampler:
@@ -142,7 +161,10 @@ def host_cores():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_cfg3(c, cols=512):
+CFG3_SAMPLE_COLS = 4096
+
+
+def cpu_cfg3(c, cols=CFG3_SAMPLE_COLS):
     import oracle as O
 
     threads = host_cores()
@@ -158,6 +180,7 @@ def cpu_cfg3(c, cols=512):
     sample = (f"one g half-step restricted to {cols} of {len(c.y)} columns x {len(c.x)} rows "
               f"({pairs:.3g} pair evaluations, fp64 C oracle restating sinkhorn.py:93-100 over "
               f"entropies.py:84-92, {threads} threads), extrapolated to 2*N*M pairs/iteration")
+    cpu_cfg3.last_seconds = el
     return rate, threads, sample
 
 
@@ -257,6 +280,16 @@ def cpu_cfg1(iters=1000):
 # Headline: cfg3 TI-Sinkhorn (row-sharded for N > 1).
 
 
+def cfg3_config(c, world):
+    """The config dict of the headline line -- shared with --impl reference so
+    both arms name the same workload."""
+    return {"workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
+            "n": len(c.x), "m": len(c.y), "d": 2, "eps": c.eps, "rho": c.rho, "variant": "h",
+            "parallelism": f"rows/{world} (NCCL all-gather per iteration)" if world > 1
+            else "single GPU",
+            "l2": f"{L2_FLUSH_BYTES >> 20} MiB write between steps (included in timing)"}
+
+
 def run_cfg3(args, rank, world, dev, comm):
     import torch
 
@@ -322,11 +355,12 @@ def run_cfg3(args, rank, world, dev, comm):
     _lib.check(lib.uot_sinkhorn_time_main(ctypes.byref(desc), _lib.ptr(ws), size.value,
                                           _lib.stream_handle(), 20, ms2))
     kernel_ms = 0.5 * (ms2[0] + ms2[1])
-    peak = ctypes.c_double(0.0)
+    probes = load_probes()
+    live = ctypes.c_double(0.0)
     lib.uot_probe_mufu_ex2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
-    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(peak)))
+    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(live)))
     achieved = float(nl) * float(m) / (kernel_ms * 1e-3) / 1e9
-    peak_g = peak.value / 1e9
+    peak_g = probes["ex2_per_s"] / 1e9
 
     e2e = run_cfg3_e2e(P, c, xl, al, args.steps, dev, kw, world)
     traffic = None
@@ -337,24 +371,15 @@ def run_cfg3(args, rank, world, dev, comm):
         traffic = None
     roof = {"bound": "mufu", "achieved": achieved, "peak": peak_g, "unit": "Gex2/s",
             "frac": achieved / peak_g, "traffic": traffic,
-            "traffic_note": "DRAM bytes per launch from the committed ncu capture; algorithmic "
-                            "input per launch = 65536 x 16 B records + 65536 x 12 B columns",
-            "kernel": "sk_main<SqE32<2>>: fused on-the-fly cost + online log-sum-exp half-step",
-            "kernel_ms": kernel_ms, "work_per_launch": f"{nl}*{m} ex2 (this rank's rows x M)",
-            "peak_source": "measured live: uot_probe_mufu_ex2 (ex2.approx.ftz on all SMs, "
-                           "CUDA events); MEASURED_PEAKS.json carries no MUFU figure"}
+            "kernel": "sk_main_sq2", "kernel_ms": kernel_ms,
+            "work_per_launch": f"{nl}*{m} ex2",
+            "peak_source": probes["source"], "peak_live_probe": live.value / 1e9}
     line = {
         "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded 8-component 2-D Gaussian mixtures, BASELINE cfg3)",
-        "config": {
-            "workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
-            "n": n, "m": m, "d": 2, "eps": c.eps, "rho": c.rho, "variant": "h",
-            "parallelism": f"rows/{world} (NCCL all-gather per iteration)" if world > 1
-            else "single GPU",
-            "l2": f"{L2_FLUSH_BYTES >> 20} MiB write between steps (included in timing; "
-                  f"{tf.ms:.3f} ms each)"},
+        "config": cfg3_config(c, world), "l2_flush_ms": tf.ms,
         "roofline": roof, "e2e": e2e,
         "gpu_launches": (4 + 7) * args.steps if world == 1 else (5 + 8) * args.steps,
     }
@@ -572,15 +597,9 @@ def run_cfg4(rank, world, dev):
     tiles = 2.0 * 256 * (4096 / 256) * (4096 / 128)  # per iteration (two half-steps)
     tflops = tiles * (12 * 2 * 256 * 128 * 16 + 2 * 256 * 128 * 8) * value / 1e12
     exps = 2.0 * 256 * 4096 * 4096 * value / 1e9
-    import ctypes
-
-    from paper_2201_00730_b200 import _lib
-
-    lib = _lib.load()
-    peak = ctypes.c_double(0.0)
-    lib.uot_probe_mufu_ex2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
-    _lib.check(lib.uot_probe_mufu_ex2(_lib.stream_handle(), ctypes.byref(peak)))
-    peak_g = peak.value / 1e9
+    probes = load_probes()
+    peak_g = probes["ex2_per_s"] / 1e9
+    peaks, _ = load_peaks()
     return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32, tcgen05 cost tiles "
                         "(kind::f16 hi/lo splits + one kind::tf32 constants MMA, A in TMEM, B "
                         "ring in smem, CTA pairs) + MUFU LSE epilogue; "
@@ -589,41 +608,84 @@ def run_cfg4(rank, world, dev):
             "roofline": {"bound": "mufu", "achieved": exps, "peak": peak_g, "unit": "Gex2/s",
                          "frac": exps / peak_g,
                          "work_per_iteration": "2*B*N*M = 8.59e9 ex2",
-                         "peak_source": "measured live: uot_probe_mufu_ex2"},
-            "tensor": {"achieved_tflops": tflops, "peak_tflops": 2250.0,
-                       "frac": tflops / 2250.0,
-                       "peak_source": "B200_PROFILING.md dense fp16 2.25 PFLOP/s"}}
+                         "peak_source": probes["source"]},
+            "tensor": {"achieved_tflops": tflops, "peak_tflops": peaks["bf16_tflops"],
+                       "frac": tflops / peaks["bf16_tflops"],
+                       "peak_sustained_tflops": peaks.get("bf16_tflops_sustained"),
+                       "frac_sustained": tflops / peaks["bf16_tflops_sustained"]
+                       if peaks.get("bf16_tflops_sustained") else None,
+                       "peak_source": "MEASURED_PEAKS.json dense bf16 (burst / sustained); "
+                                      "the fp16 MMAs issue at the bf16 rate"}}
 
 
 # ---------------------------------------------------------------------------
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's algorithm (oracle port) on host cores."""
+    """--impl reference: the reference's algorithm (the oracle port of
+    sinkhorn.py:93-100 / entropies.py:84-92 in C, every host thread) on the
+    headline workload.  Each step is the same bounded sample as the headline
+    line's cpu_baseline (one g half-step over CFG3_SAMPLE_COLS of the 65536
+    columns); value extrapolates it to whole iterations/s.  ms_per_step is the
+    measured wall time of one sampled step."""
     if rank != 0:
         return
     from paper_2201_00730_b200 import synthetic as S
 
     c = S.cfg3_inputs()
-    vals = []
+    vals, secs = [], []
     for k in range(args.warmup + args.steps):
-        v, threads, sample = cpu_cfg3(c, cols=128)
+        v, threads, sample = cpu_cfg3(c)
         if k >= args.warmup:
             vals.append(v)
+            secs.append(cpu_cfg3.last_seconds)
     value = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iter/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * float(np.mean(secs)), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3: H-Sinkhorn N=M=65536 d=2 fp32, eps=1e-2*max|x-y|^2, KL rho=1",
-                   "n": len(c.x), "m": len(c.y), "eps": c.eps},
+        "config": cfg3_config(c, args.gpus),
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "value_spread": [float(min(vals)), float(max(vals))]},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "note": "ms_per_step = wall time of one sampled step (not of a whole iteration); value "
+                "= the sample's pair rate extrapolated to 2*N*M pairs per iteration",
     }
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n):
+    """--gpus N without torchrun: relaunch this script under
+    torch.distributed.run with N local ranks (the driver's own launch line)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def compact(entry):
+    """Secondary entries in the printed line: the numbers only (the driver
+    keeps a bounded tail of stdout); the descriptive keys go to
+    gpurun_out/bench_detail.json."""
+    keep = ("value", "unit", "ms_total", "dtype", "f_variant_iter_s", "g_variant_iter_s",
+            "mean_active_atoms", "res_f", "res_g")
+    out = {k: entry[k] for k in keep if k in entry}
+    for sub in ("roofline", "tensor", "issue"):
+        if sub in entry:
+            out[sub] = {k: v for k, v in entry[sub].items()
+                        if k in ("bound", "achieved", "peak", "unit", "frac", "achieved_tflops",
+                                 "peak_tflops", "peak_sustained_tflops", "frac_sustained")}
+    if "cpu_baseline" in entry:
+        cb = entry["cpu_baseline"]
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind")}
+    return out
 
 
 def main():
@@ -634,8 +696,12 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -662,7 +728,9 @@ def main():
                 secondary["cfg1_sinkhorn_1d"] = run_cfg1(dev)
                 secondary["cfg3_verify"] = run_cfg3_verify(dev)
         if rank == 0:
-            cpu_v, cpu_cores, cpu_sample = cpu_cfg3(S_inputs_cfg3())
+            cpu_runs = [cpu_cfg3(S_inputs_cfg3()) for _ in range(3)]
+            cpu_v = float(np.mean([r_[0] for r_ in cpu_runs]))
+            cpu_cores, cpu_sample = cpu_runs[0][1], cpu_runs[0][2] + " (mean of 3 samples)"
             line["cpu_baseline"] = {"value": cpu_v, "unit": "iter/s", "cores": cpu_cores,
                                     "kind": "port", "sample": cpu_sample}
             if not args.no_secondary and world == 1:
@@ -679,9 +747,15 @@ def main():
                 secondary["cfg1_sinkhorn_1d"]["cpu_baseline"] = {
                     "value": v1, "unit": "iter/s (H)", "cores": c1, "kind": "port", "sample": s1}
                 os.environ["ORACLE_THREADS"] = str(host_cores())
-            line["secondary"] = secondary
             line["peaks"] = {"hbm_gbs": peaks.get("hbm_gbs"), "source": peak_src}
             line["clocks"] = clk.summary()
+            try:
+                os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+                with open(os.path.join(ROOT, "gpurun_out", "bench_detail.json"), "w") as fh:
+                    json.dump(dict(line, secondary=secondary), fh, indent=1)
+            except OSError:
+                pass
+            line["secondary"] = {k: compact(v) for k, v in secondary.items()}
             print(json.dumps(line), flush=True)
     finally:
         if comm is not None:

@@ -64,8 +64,12 @@ int uot_device_arch(int device, int* sm_major, int* sm_minor);
  * marginal penalties ent1 / ent2 (KL, Berg, Balanced; "h" is KL/KL), for a
  * batch of independent problems, with a fixed iteration budget and the
  * reference's optional `delta_f < tol` stop (:304-306) evaluated per problem.
- * fp32 squared-Euclidean costs with d >= 32 run on the tensor cores
- * (tcgen05: fp16 hi/lo split cost tiles + a tf32 constants MMA).
+ * fp32 squared-Euclidean costs with d >= 32 (d % 4 == 0) run on the tensor
+ * cores (tcgen05: fp16 hi/lo split cost tiles + a tf32 constants MMA, points
+ * taken relative to the midpoint of the two clouds' centroids, operands balanced by a
+ * power-of-two scale; the fp16 range holds while 2 R^2 / (eps ln 2) < ~4e9,
+ * R = the largest distance to that point -- beyond it the fp32 log-domain
+ * exponents themselves carry no precision).
  *
  * Inputs (dtype elements): x [batch][n][d], y [batch][m][d] (d = 1 for
  * UOT_COST_POWER); explicit costs c [batch][n][m] and its transpose
@@ -108,6 +112,10 @@ typedef struct uot_sinkhorn_desc {
   int32_t ent1, ent2;        /* UOT_ENT_*: "h" needs KL/KL, "g" KL or Berg, "f" any */
   int32_t lam_given;         /* "g", single device: start from lam0 instead of lambda*(f0, g0) */
   double lam0;               /* (g_sinkhorn_step's incoming lam, src/sinkhorn.py:117-134) */
+  int32_t* status;           /* optional [batch]: 0, or the NewtonError of the G variant's
+                                lambda* with a Berg marginal (src/duality.py:182-247):
+                                1 empty domain, 2 no bracket, 3 no convergence; the problem
+                                stops at that iteration */
 } uot_sinkhorn_desc;
 
 int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);

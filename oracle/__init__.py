@@ -784,6 +784,49 @@ def solve_mot_1d(xs, ws, w):
     return idx[:e].copy(), mass[:e].copy(), [pots[off[q]:off[q] + lens[q]].copy() for q in range(k)]
 
 
+def mot_mismatch_report(idx_a, mass_a, idx_b, mass_b, cums):
+    """Compare two K-marginal plans (tuples + masses) entry by entry.  Returns
+    the entry counts, the number of entries present in only one plan, the
+    mass those entries carry (mass_moved = max over the two plans), and, at
+    every place where the two sweeps take a different step, the gap between
+    the cumulative breakpoints that decided it (cums[q][i] = sum_{s<=i} w_q[s],
+    barycenter.py:209-229): max_gap (absolute) and max_gap_rel (relative to
+    the total mass)."""
+    ta = {tuple(r): m for r, m in zip(np.asarray(idx_a).tolist(), mass_a)}
+    tb = {tuple(r): m for r, m in zip(np.asarray(idx_b).tolist(), mass_b)}
+    only_a = set(ta) - set(tb)
+    only_b = set(tb) - set(ta)
+    total = float(np.sum(mass_b))
+    gaps = []
+    ia, ib = np.asarray(idx_a), np.asarray(idx_b)
+    e = 0
+    n = min(len(ia), len(ib))
+    while e < n:
+        if np.array_equal(ia[e], ib[e]):
+            e += 1
+            continue
+        prev = ia[e - 1] if e > 0 else np.zeros(ia.shape[1], dtype=np.int64)
+        qs = sorted(set(np.nonzero(ia[e] != prev)[0]) | set(np.nonzero(ib[e] != prev)[0]))
+        vals = [float(cums[q][prev[q]]) for q in qs]
+        gaps.append(max(vals) - min(vals) if vals else 0.0)
+        # resynchronise on the next common tuple
+        rest_b = {tuple(r): k for k, r in enumerate(ib[e:].tolist())}
+        k = e
+        while k < len(ia) and tuple(ia[k].tolist()) not in rest_b:
+            k += 1
+        if k >= len(ia):
+            break
+        shift = rest_b[tuple(ia[k].tolist())] + e - k
+        ia_k, ib_k = ia[k:], ib[k + shift:]
+        ia, ib = ia_k, ib_k
+        n = min(len(ia), len(ib))
+        e = 0
+    return {"entries": (len(idx_a), len(idx_b)), "differing": (len(only_a), len(only_b)),
+            "mass_moved": max(sum(ta[t] for t in only_a), sum(tb[t] for t in only_b), 0.0),
+            "mismatch_sites": len(gaps), "max_gap": max(gaps) if gaps else 0.0,
+            "max_gap_rel": (max(gaps) / total) if gaps else 0.0}
+
+
 def multimarginal_lambda(pots, ws, w, rho):
     """barycenter.py:298-317."""
     rhos = np.asarray(w, dtype=np.float64) * float(rho)

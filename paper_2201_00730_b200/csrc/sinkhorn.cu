@@ -71,10 +71,11 @@ struct SqE32 {
   };
   static __device__ __forceinline__ void load(Out& o, const DirGeo<float>& g, int b, int idx) {
     const float* p = g.out_pts + b * g.out_pts_bstride + (long)idx * D;
+    const float* c = g.ctr + b * g.ctr_bstride;
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      o.y[k] = p[k];
+      o.y[k] = p[k] - c[k];
       s = fmaf(o.y[k], o.y[k], s);
     }
     o.bias = -s * g.L;
@@ -92,11 +93,15 @@ struct SqE32 {
     }
   }
   static __device__ __forceinline__ void pack(float* rec, double hat, const float* pt, double w,
-                                              double L, double, int) {
+                                              double L, double, int, const float* ctr) {
     double s = 0.0;
-    for (int k = 0; k < D; ++k) s += (double)pt[k] * (double)pt[k];
+    float xc[D];
+    for (int k = 0; k < D; ++k) {
+      xc[k] = pt[k] - ctr[k];
+      s += (double)xc[k] * (double)xc[k];
+    }
     rec[0] = (float)((hat - s) * L + log2(w));
-    for (int k = 0; k < D; ++k) rec[1 + k] = (float)(2.0 * L * (double)pt[k]);
+    for (int k = 0; k < D; ++k) rec[1 + k] = (float)(2.0 * L * (double)xc[k]);
     for (int k = D + 1; k < RW; ++k) rec[k] = 0.f;
   }
   static int rw(int) { return RW; }
@@ -108,26 +113,34 @@ struct SqE32N {
   using T = float;
   struct Out {
     const float* y;
+    const float* c;
     float bias;
   };
   static __device__ __forceinline__ void load(Out& o, const DirGeo<float>& g, int b, int idx) {
     o.y = g.out_pts + b * g.out_pts_bstride + (long)idx * g.d;
+    o.c = g.ctr + b * g.ctr_bstride;
     float s = 0.f;
-    for (int k = 0; k < g.d; ++k) s = fmaf(o.y[k], o.y[k], s);
+    for (int k = 0; k < g.d; ++k) {
+      const float yc = o.y[k] - o.c[k];
+      s = fmaf(yc, yc, s);
+    }
     o.bias = -s * g.L;
   }
   static __device__ __forceinline__ float arg(const float* rec, long, const Out& o,
                                               const DirGeo<float>& g, int) {
     float a = rec[0];
-    for (int k = 0; k < g.d; ++k) a = fmaf(rec[1 + k], __ldg(o.y + k), a);
+    for (int k = 0; k < g.d; ++k) a = fmaf(rec[1 + k], __ldg(o.y + k) - __ldg(o.c + k), a);
     return a;
   }
   static __device__ __forceinline__ void pack(float* rec, double hat, const float* pt, double w,
-                                              double L, double, int d) {
+                                              double L, double, int d, const float* ctr) {
     double s = 0.0;
-    for (int k = 0; k < d; ++k) s += (double)pt[k] * (double)pt[k];
+    for (int k = 0; k < d; ++k) {
+      const float xc = pt[k] - ctr[k];
+      s += (double)xc * (double)xc;
+    }
     rec[0] = (float)((hat - s) * L + log2(w));
-    for (int k = 0; k < d; ++k) rec[1 + k] = (float)(2.0 * L * (double)pt[k]);
+    for (int k = 0; k < d; ++k) rec[1 + k] = (float)(2.0 * L * (double)(pt[k] - ctr[k]));
   }
   static int rw(int d) { return d + 1; }
 };
@@ -157,7 +170,7 @@ struct Pow1D {
     return rec[0] - g.L * cost(rec[1], o.y, g.p);
   }
   static __device__ __forceinline__ void pack(T* rec, double hat, const T* pt, double w, double L,
-                                              double, int) {
+                                              double, int, const T*) {
     rec[0] = (T)(hat * L + (Dom<T>::unit == 1.0 ? log(w) : log2(w)));
     rec[1] = pt[0];
   }
@@ -186,7 +199,7 @@ struct SqE64 {
     return rec[0] - g.L * c;
   }
   static __device__ __forceinline__ void pack(double* rec, double hat, const double* pt, double w,
-                                              double L, double, int d) {
+                                              double L, double, int d, const double*) {
     rec[0] = hat * L + log(w);
     for (int k = 0; k < d; ++k) rec[1 + k] = pt[k];
   }
@@ -210,7 +223,7 @@ struct Explicit {
     return rec[0] - g.L * __ldg(g.cmat + b * g.cm_bstride + r * g.ld_r + (long)o.o * g.ld_o);
   }
   static __device__ __forceinline__ void pack(T* rec, double hat, const T*, double w, double L,
-                                              double, int) {
+                                              double, int, const T*) {
     rec[0] = (T)(hat * L + (Dom<T>::unit == 1.0 ? log(w) : log2(w)));
   }
   static int rw(int) { return 1; }
@@ -226,23 +239,27 @@ struct SqE32TC {
   };
   static int rw(int d) { return tc_kp(d); }
   // Static part of a record, written once per solve (tc_init_static): the
-  // fp16 split Xh, Xl of (2L / 8) x, zero padding, the unit columns and
-  // |x|^2 (fp64) parked in float columns 8-9 (no MMA reads them).
+  // fp16 split Xh, Xl of (2L / S) x', zero padding, the unit columns and
+  // |x'|^2 (fp64) parked in float columns 8-9 (no MMA reads them).  x' = x - c
+  // is the point relative to the problem's centre c (tc_center: |x - y|^2 =
+  // |x'|^2 - 2 x'.y' + |y'|^2 for any c), so the fp16 operands and the fp32
+  // accumulator scale with the clouds' extent, not their distance from the origin.
   static __device__ __forceinline__ void init_tile(float* base, long r, int KP, const float* pt,
-                                                   double L, int d) {
+                                                   const float* ctr, double L, double S, int d) {
     float* tile = base + (r / TC_TILE) * (long)TC_TILE * KP;
     __half* th = reinterpret_cast<__half*>(tile);
     const int rl = (int)(r % TC_TILE);
     const int dp = tc_dp(d), kh = tc_kh(d);
-    const double sc = 2.0 * L / (double)TC_YSCALE;
+    const double sc = 2.0 * L / S;
     double s2 = 0.0;
     for (int k = 0; k < dp; ++k) {
       float xh = 0.f, xl = 0.f;
       if (k < d) {
-        const float x = (float)(sc * (double)pt[k]);
+        const float xc = pt[k] - ctr[k];
+        const float x = (float)(sc * (double)xc);
         xh = __half2float(__float2half_rn(x));
         xl = x - xh;
-        s2 += (double)pt[k] * (double)pt[k];
+        s2 += (double)xc * (double)xc;
       }
       th[tc_xidx(rl, k, d)] = __float2half_rn(xh);
       th[tc_xidx(rl, dp + k, d)] = __float2half_rn(xl);
@@ -273,15 +290,84 @@ struct SqE32TC {
   }
 };
 
-__global__ void tc_init_static(float* rec, long rec_bstride, const float* pts, int batch, int n,
-                               int d, int KP, double L) {
+__global__ void tc_init_static(float* rec, long rec_bstride, const float* pts, const float* ctr,
+                               long ctr_bstride, int batch, int n, int d, int KP, double L,
+                               double S) {
   const long total = (long)batch * n;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
     const int b = (int)(i / n);
     const long r = i - (long)b * n;
-    SqE32TC::init_tile(rec + (long)b * rec_bstride, r, KP, pts + i * d, L, d);
+    SqE32TC::init_tile(rec + (long)b * rec_bstride, r, KP, pts + i * d, ctr + b * ctr_bstride, L,
+                       S, d);
   }
+}
+
+// Centre of problem b's fp32 point clouds (the expanded-form engines SqE32<D>,
+// SqE32N and the tcgen05 path): the midpoint of the two clouds' centroids,
+// c = (mean x + mean y) / 2.  |x - y|^2 = |x'|^2 - 2 x'.y' + |y'|^2 for any c,
+// and with x' = x - c, y' = y - c every term scales with the clouds' radii,
+// not with their distance from the origin (no cancellation).  For d <= 256,
+// thread t of the (R x d)-thread block owns coordinate t % d of rows t / d,
+// t/d + R, ...; the R partials of a coordinate are added in a fixed order
+// (deterministic); larger d loops over the coordinates.
+__global__ void __launch_bounds__(256) sk_center(const float* x, const float* y, int n, int m,
+                                                 int d, float* ctr) {
+  __shared__ double part[256];
+  const int b = blockIdx.x;
+  const float* xb = x + (long)b * n * d;
+  const float* yb = y + (long)b * m * d;
+  if (d > 256) {
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+      double sx = 0.0, sy = 0.0;
+      for (int i = 0; i < n; ++i) sx += (double)xb[(long)i * d + k];
+      for (int j = 0; j < m; ++j) sy += (double)yb[(long)j * d + k];
+      ctr[(long)b * d + k] = (float)(0.5 * (sx / n + sy / m));
+    }
+    return;
+  }
+  const int R = blockDim.x / d;
+  const int k = threadIdx.x % d, r0 = threadIdx.x / d;
+  double sx = 0.0, sy = 0.0;
+  if (r0 < R) {
+    for (int i = r0; i < n; i += R) sx += (double)xb[(long)i * d + k];
+    for (int j = r0; j < m; j += R) sy += (double)yb[(long)j * d + k];
+  }
+  part[threadIdx.x] = 0.5 * (sx / n + sy / m);
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double c = 0.0;
+    for (int r = 0; r < R; ++r) c += part[r * d + threadIdx.x];
+    ctr[(long)b * d + threadIdx.x] = (float)c;
+  }
+}
+
+template <class P>
+constexpr bool centred() {
+  return std::is_same<P, SqE32TC>::value || std::is_same<P, SqE32N>::value ||
+         std::is_same<P, SqE32<1>>::value || std::is_same<P, SqE32<2>>::value ||
+         std::is_same<P, SqE32<3>>::value;
+}
+
+template <class P>
+int launch_center(const uot_sinkhorn_desc& d, float* ctr, cudaStream_t st) {
+  if constexpr (centred<P>()) {
+    const int threads = d.d <= 256 ? d.d * (256 / d.d) : 256;
+    sk_center<<<d.batch, threads, 0, st>>>((const float*)d.x, (const float*)d.y, d.n, d.m, d.d,
+                                           ctr);
+    UOT_CHECK_LAUNCH();
+  }
+  return UOT_OK;
+}
+
+// Power-of-two A-operand scale S of the tcgen05 path: the A rows carry S y'
+// and the B records (2L / S) x', so S = sqrt(2L) balances their magnitudes
+// (both ~ sqrt(2L) |x'|).  fp16 then overflows only when 2L R^2 > ~4e9
+// (R = the largest distance to the centre), where the fp32 exponent
+// arguments themselves (~2L R^2 in log2 units) carry no precision left.
+inline double tc_ascale(double L) {
+  const double s = std::ldexp(1.0, (int)std::lround(0.5 * std::log2(2.0 * L)));
+  return std::min(std::max(s, std::ldexp(1.0, -24)), std::ldexp(1.0, 24));
 }
 
 // Record layout of a side: `rw` elements per index, or the tiled layout.
@@ -290,8 +376,8 @@ struct RecLayout {
   static long stride(int n, int d) { return (long)n * P::rw(d); }
   static __device__ __forceinline__ void pack(typename P::T* base, long o, int rw, double hat,
                                               const typename P::T* pt, double w, double L,
-                                              double p, int d) {
-    P::pack(base + o * rw, hat, pt, w, L, p, d);
+                                              double p, int d, const typename P::T* ctr) {
+    P::pack(base + o * rw, hat, pt, w, L, p, d, ctr);
   }
 };
 template <>
@@ -301,7 +387,7 @@ struct RecLayout<SqE32TC> {
   }
   static __device__ __forceinline__ void pack(float* base, long o, int rw, double hat,
                                               const float* pt, double w, double L, double,
-                                              int d) {
+                                              int d, const float*) {
     SqE32TC::pack_tile(base, o, rw, hat, pt, w, L, d);
   }
 };
@@ -592,6 +678,7 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
   const int obase = blockIdx.x * THREADS * COLS + threadIdx.x;
   const float L = A.g.L;
   const float* pts = A.g.out_pts + b * A.g.out_pts_bstride;
+  const float cen0 = A.g.ctr[b * A.g.ctr_bstride], cen1 = A.g.ctr[b * A.g.ctr_bstride + 1];
 #pragma unroll
   for (int j = 0; j < CP; ++j) {
     float ya0[2], ya1[2], c[2];
@@ -599,7 +686,8 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
     for (int h = 0; h < 2; ++h) {
       const int o = obase + (2 * j + h) * THREADS;
       const bool ok = o < A.nout;
-      const float q0 = ok ? pts[(long)o * 2] : 0.f, q1 = ok ? pts[(long)o * 2 + 1] : 0.f;
+      const float q0 = ok ? pts[(long)o * 2] - cen0 : 0.f;
+      const float q1 = ok ? pts[(long)o * 2 + 1] - cen1 : 0.f;
       ya0[h] = q0;
       ya1[h] = q1;
       mm[2 * j + h] = ok ? A.shift_in[(long)b * A.nout + o] : 0.f;
@@ -698,7 +786,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) sk_lambda_newton(int n, int m, const T* hatA,
                                                        const T* hatB, const T* wa, const T* wb,
                                                        int e1, int e2, double r1, double r2,
-                                                       SkScalars* sc) {
+                                                       SkScalars* sc, int* status, int* done) {
   __shared__ double s_x[32];
   __shared__ double s_r[2];
   const int b = blockIdx.x;
@@ -714,6 +802,18 @@ __global__ void __launch_bounds__(256) sk_lambda_newton(int n, int m, const T* h
   gmn = block_reduce(gmn, s_x, MinOp(), CUDART_INF);
   const double lo_dom = e1 == UOT_ENT_BERG ? -r1 - fmn : -CUDART_INF;
   const double hi_dom = e2 == UOT_ENT_BERG ? r2 + gmn : CUDART_INF;
+  // NewtonError cases of src/duality.py:182-247 (codes as uot_translation):
+  // the problem stops (done) and the status goes to the caller.
+  auto fail = [&](int code) {
+    if (threadIdx.x == 0) {
+      if (status != nullptr) status[b] = code;
+      done[b] = 1;
+    }
+  };
+  if (!(lo_dom < hi_dom)) {  // :188-189 empty translation domain
+    fail(1);
+    return;
+  }
   auto clamp = [&](double x) {
     if (lo_dom > -CUDART_INF) x = fmax(x, lo_dom + 1e-12 * fmax(1.0, fabs(lo_dom)));
     if (hi_dom < CUDART_INF) x = fmin(x, hi_dom - 1e-12 * fmax(1.0, fabs(hi_dom)));
@@ -750,33 +850,46 @@ __global__ void __launch_bounds__(256) sk_lambda_newton(int n, int m, const T* h
   eval(lam, r, ds);
   if (fabs(r) >= tol) {
     double lo = lam, hi = lam, step = 1.0;
+    bool bracketed = false;
     if (r > 0.0) {
-      for (int it = 0; it < 200; ++it) {
+      for (int it = 0; it < 200 && !bracketed; ++it) {
         hi = clamp(lam + step);
         double rh, dh;
         eval(hi, rh, dh);
-        if (rh <= 0.0) break;
+        bracketed = rh <= 0.0;
         step *= 2.0;
       }
     } else {
-      for (int it = 0; it < 200; ++it) {
+      for (int it = 0; it < 200 && !bracketed; ++it) {
         lo = clamp(lam - step);
         double rl, dl;
         eval(lo, rl, dl);
-        if (rl >= 0.0) break;
+        bracketed = rl >= 0.0;
         step *= 2.0;
       }
     }
+    if (!bracketed) {  // :220-229 failed to bracket
+      fail(2);
+      return;
+    }
     double x = 0.5 * (lo + hi);
+    bool conv = false;
     for (int it = 0; it < 100; ++it) {
       eval(x, r, ds);
-      if (fabs(r) < tol) break;
+      if (fabs(r) < tol) {
+        conv = true;
+        break;
+      }
       if (r > 0.0)
         lo = x;
       else
         hi = x;
       const double nt = (ds < 0.0 && isfinite(ds)) ? x - r / ds : CUDART_NAN;
       x = (nt > lo && nt < hi) ? nt : 0.5 * (lo + hi);
+    }
+    if (!conv) {  // :247 no convergence
+      fail(3);
+      return;
     }
     lam = x;
   }
@@ -866,7 +979,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) sk_tail(TailArgs<typename P::T> 
     const double w = (double)A.out_w[(long)b * A.nout + o];
     RecLayout<P>::pack(A.rec_out + (long)b * A.rec_bstride, o, A.rw, hat,
                        A.out_pts + ((long)b * A.nout + o) * A.d, w, (double)A.L, (double)A.p,
-                       A.d);
+                       A.d, A.ctr != nullptr ? A.ctr + (long)b * A.d : nullptr);
     if (w > 0.0) pr = LsePair{-hat / A.rho_out, w};
     if (A.hat_old != nullptr) {
       const double dl = hat - ((double)A.hat_old[(long)b * A.nout + o] + tau_old);
@@ -1083,7 +1196,7 @@ __global__ void sk_zero(long n, T* p) {
 namespace {
 
 struct WsLayout {
-  size_t off[16];
+  size_t off[17];
   size_t total;
 };
 
@@ -1105,6 +1218,7 @@ struct Buffers {
   int* done;
   int* iters_done;
   double* trace;  // scratch trace when the caller passes none
+  T* ctr;         // [B][d] centre of the tcgen05 operands (tc_center)
 };
 
 struct Shape {
@@ -1115,7 +1229,7 @@ struct Shape {
 
 template <typename T>
 size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* base) {
-  size_t sizes[16];
+  size_t sizes[17];
   const long nm = std::max(s.total_n, s.m);
   sizes[0] = sizeof(T) * (size_t)s.B * s.recA;
   sizes[1] = sizeof(T) * (size_t)s.B * s.recB;
@@ -1133,8 +1247,9 @@ size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* bas
   sizes[13] = sizeof(int) * (size_t)s.B;
   sizes[14] = sizeof(int) * (size_t)s.B;
   sizes[15] = sizeof(double) * (size_t)s.B * std::max(iters, 1);
+  sizes[16] = sizeof(T) * (size_t)s.B * std::max(s.d, 4);
   size_t off = 0;
-  for (int k = 0; k < 16; ++k) {
+  for (int k = 0; k < 17; ++k) {
     L.off[k] = off;
     off += (sizes[k] + 255) / 256 * 256;
   }
@@ -1156,6 +1271,7 @@ size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* bas
     buf->done = (int*)(base + L.off[13]);
     buf->iters_done = (int*)(base + L.off[14]);
     buf->trace = (double*)(base + L.off[15]);
+    buf->ctr = (T*)(base + L.off[16]);
   }
   return L.total;
 }
@@ -1240,8 +1356,9 @@ struct Engine {
   static constexpr int OUT_PER_BLOCK = C::THREADS * C::COLS;
 
   static int occupancy(int d) {
-    static int cached = -1;
-    static int cached_d = -1;
+    // per host thread: concurrent callers with different d never share the pair
+    static thread_local int cached = -1;
+    static thread_local int cached_d = -1;
     if (cached >= 0 && cached_d == d) return cached;
     const int rw = P::rw(d);
     const size_t smem = (size_t)chunk_for(rw) * rw * sizeof(T);
@@ -1334,6 +1451,10 @@ struct Engine {
       a.nout = d.n;
       a.shift_in = bf.shiftA;
     }
+    a.g.ctr = bf.ctr;
+    a.g.ctr_bstride = d.d;
+    a.g.ascale = (T)tc_ascale((double)(float)L);
+    a.g.tc_full = 2.0 * (double)(float)L > 128.0 ? 1 : 0;
     a.nred = nred;
     a.red_offset = red_offset;
     a.part_m = bf.part_m;
@@ -1438,6 +1559,7 @@ struct Engine {
     a.rec_bstride = RecLayout<P>::stride(to_target ? d.m : d.n, d.d);
     a.rw = P::rw(d.d);
     a.out_pts = (const T*)(to_target ? d.y : d.x);
+    a.ctr = centred<P>() ? bf.ctr : nullptr;
     a.d = d.d;
     a.out_w = (const T*)(to_target ? d.b : d.a);
     a.L = (T)(1.0 / (eps * Dom<T>::unit));
@@ -1488,6 +1610,7 @@ struct Engine {
     sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
                                                       bf.iters_done);
     UOT_CHECK_LAUNCH();
+    UOT_TRY(launch_center<P>(d, reinterpret_cast<float*>(bf.ctr), st));
     if constexpr (std::is_same<P, SqE32TC>::value) {
       tc_fill_dead<<<1024, 256, 0, st>>>(bf.recA, (long)d.batch * s.recA / tc_kp(d.d), d.d,
                                          tc_kp(d.d));
@@ -1495,10 +1618,13 @@ struct Engine {
                                          tc_kp(d.d));
       // same fp32-rounded L as the tails' record packing
       const double Lr = (double)(float)(1.0 / (d.eps * Dom<float>::unit));
-      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x, d.batch, d.n, d.d,
-                                           tc_kp(d.d), Lr);
-      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y, d.batch, d.m, d.d,
-                                           tc_kp(d.d), Lr);
+      const double Sa = tc_ascale(Lr);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x,
+                                           (const float*)bf.ctr, (long)d.d, d.batch, d.n,
+                                           d.d, tc_kp(d.d), Lr, Sa);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y,
+                                           (const float*)bf.ctr, (long)d.d, d.batch, d.m,
+                                           d.d, tc_kp(d.d), Lr, Sa);
       UOT_CHECK_LAUNCH();
     }
     const long nm = std::max(d.n, d.m);
@@ -1531,10 +1657,12 @@ struct Engine {
     UOT_TRY(launch_tail(d, bf, st, false, 1, 0, nullptr, bf.hatA0, f0, 0, nullptr, trace_len));
     const bool g_newton =
         d.variant == UOT_SINKHORN_G && !(d.ent1 == UOT_ENT_KL && d.ent2 == UOT_ENT_KL);
+    if (d.status != nullptr)
+      UOT_CUDA_TRY(cudaMemsetAsync(d.status, 0, sizeof(int32_t) * (size_t)d.batch, st));
     auto lam_newton = [&](const T* hatA) -> int {
       sk_lambda_newton<T><<<d.batch, 256, 0, st>>>(d.n, d.m, hatA, bf.hatB, (const T*)d.a,
                                                    (const T*)d.b, d.ent1, d.ent2, d.rho1, d.rho2,
-                                                   bf.sc);
+                                                   bf.sc, d.status, bf.done);
       UOT_CHECK_LAUNCH();
       return UOT_OK;
     };
@@ -1559,7 +1687,7 @@ struct Engine {
       if (g_newton) {  // lambda_star(pair, initial=lam) (:134)
         sk_lambda_newton<T><<<d.batch, 256, 0, s>>>(d.n, d.m, hat_new, bf.hatB, (const T*)d.a,
                                                     (const T*)d.b, d.ent1, d.ent2, d.rho1, d.rho2,
-                                                    bf.sc);
+                                                    bf.sc, d.status, bf.done);
         UOT_CHECK_LAUNCH();
       }
       return UOT_OK;
@@ -1627,16 +1755,20 @@ struct Engine {
     sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf.sc, bf.counter, bf.done,
                                                       bf.iters_done);
     UOT_CHECK_LAUNCH();
+    UOT_TRY(launch_center<P>(d, reinterpret_cast<float*>(bf.ctr), st));
     if constexpr (std::is_same<P, SqE32TC>::value) {
       tc_fill_dead<<<1024, 256, 0, st>>>(bf.recA, (long)d.batch * s.recA / tc_kp(d.d), d.d,
                                          tc_kp(d.d));
       tc_fill_dead<<<1024, 256, 0, st>>>(bf.recB, (long)d.batch * s.recB / tc_kp(d.d), d.d,
                                          tc_kp(d.d));
       const double Lr = (double)(float)(1.0 / (d.eps * Dom<float>::unit));
-      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x, d.batch, d.n, d.d,
-                                           tc_kp(d.d), Lr);
-      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y, d.batch, d.m, d.d,
-                                           tc_kp(d.d), Lr);
+      const double Sa = tc_ascale(Lr);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recA, s.recA, (const float*)d.x,
+                                           (const float*)bf.ctr, (long)d.d, d.batch, d.n,
+                                           d.d, tc_kp(d.d), Lr, Sa);
+      tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y,
+                                           (const float*)bf.ctr, (long)d.d, d.batch, d.m,
+                                           d.d, tc_kp(d.d), Lr, Sa);
       UOT_CHECK_LAUNCH();
     }
     sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
@@ -1809,6 +1941,9 @@ struct Engine {
       sA[r] = splits(d.batch, L.nl[r], d.m, d.d);
       sk_reset<<<ceil_div(d.batch, 128), 128, 0, st>>>(d.batch, bf[r].sc, bf[r].counter,
                                                         bf[r].done, bf[r].iters_done);
+      // each shard centres its own records (the cost, hence every partial, does not
+      // depend on the centre)
+      UOT_TRY(launch_center<P>(dr[r], reinterpret_cast<float*>(bf[r].ctr), st));
       sk_zero<T><<<256, 256, 0, st>>>((long)L.nl[r], bf[r].shiftA);
       sk_zero<T><<<256, 256, 0, st>>>((long)d.m, bf[r].shiftB);
       UOT_CHECK_LAUNCH();
@@ -1916,8 +2051,9 @@ int dispatch(const uot_sinkhorn_desc& d, Fn&& fn) {
         if (d.d == 1) return fn(Engine<SqE32<1>>());
         if (d.d == 2) return fn(Engine<SqE32<2>>());
         if (d.d == 3) return fn(Engine<SqE32<3>>());
+        // UOT_SINKHORN_SIMT=1 keeps d >= 32 on the SIMT engine (comparison runs)
         if (d.d >= 32 && d.d % 4 == 0 && 2 * tc_ka(d.d) <= 256 && d.nranks <= 1 &&
-            d.nccl_comm == nullptr)
+            d.nccl_comm == nullptr && std::getenv("UOT_SINKHORN_SIMT") == nullptr)
           return fn(Engine<SqE32TC>());
         return fn(Engine<SqE32N>());
       case UOT_COST_POWER:

@@ -43,6 +43,10 @@ struct DirGeo {
   T p;                  // power exponent (power-1D cost)
   const T* cmat;        // explicit cost: C(r,o) = cmat[b*cm_bstride + r*ld_r + o*ld_o]
   long cm_bstride, ld_r, ld_o;
+  const T* ctr;         // tcgen05 path: per-problem centre [B][d] (tc_center)
+  long ctr_bstride;
+  T ascale;             // tcgen05 path: power-of-two scale of the A operand (B gets 2L/ascale)
+  int tc_full;          // tcgen05 path: also the Yl*Xl product (2L > 128, i.e. eps < ~0.0225)
 };
 
 template <typename T>
@@ -84,6 +88,7 @@ struct TailArgs {
   long rec_bstride;
   int rw;
   const T* out_pts;            // [B][nout][d]
+  const T* ctr;                // [B][d] centre of the fp32 expanded-form records, or nullptr
   int d;
   const T* out_w;              // [B][nout]
   T L, p;

@@ -48,7 +48,7 @@ constexpr int TC_THREADS = 320;
 constexpr int TC_NB = 2;  // output blocks of 128 rows per CTA
 constexpr int TC_STAGE_BYTES = 4096;  // one CTA's half of a stage: 32 fp16 K columns
 constexpr int TC_CBYTES = 2048;       // the constants' stage: 8 tf32 K columns
-constexpr float TC_YSCALE = 8.f;      // A = 8 y, B = (2L / 8) x (exact power-of-two scales)
+// A = S y', B = (2L / S) x' with the power-of-two S = tc_ascale(L) (sinkhorn.cu)
 
 // Output-side points staged in shared memory for the A prologue: 256 rows
 // of d floats, row stride d + 4 (conflict-free float4 row reads).
@@ -92,15 +92,19 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 }
 
 // The MMAs one 16-wide fp16 K slice of B feeds (kh = its K offset in halves):
-// Xh slices meet Yh and Yl, Xl slices meet Yh.
+// Xh slices meet Yh and Yl, Xl slices meet Yh -- and Yl too when `full` (the
+// Yl Xl term is <= 2^-22 2L |x'||y'| in log2 units: dropped at moderate L,
+// kept for small eps, see DirGeo::tc_full).
 __device__ __forceinline__ void tc_slice_mmas(int kh, int dp, uint32_t dcol, uint32_t tbase,
-                                              uint64_t bd, uint32_t idesc, bool& first) {
+                                              uint64_t bd, uint32_t idesc, bool& first,
+                                              bool full) {
   if (kh < dp) {
     tc::mma2_f16_ts(dcol, tbase + (kh >> 1), bd, idesc, first ? 0u : 1u);
     tc::mma2_f16_ts(dcol, tbase + ((dp + kh) >> 1), bd, idesc, 1u);
     first = false;
   } else if (kh < 2 * dp) {
     tc::mma2_f16_ts(dcol, tbase + ((kh - dp) >> 1), bd, idesc, first ? 0u : 1u);
+    if (full) tc::mma2_f16_ts(dcol, tbase + (kh >> 1), bd, idesc, 1u);
     first = false;
   }
 }
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int ka = tc_ka(d);        // TMEM columns of one A block
   const int nxs = tc_kh(d) / 32;  // fp16 stages per tile half; then one constants stage
   const int nst = nxs + 1;
+  const bool full4 = A.g.tc_full != 0;
   (void)KP;
 
   if (warp == 1) tc::tmem_alloc2(&tbase_s, 512);
@@ -188,10 +193,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
     const int nrows = max(0, min(TC_NB * TC_TILE, A.nout - row0));
     const float4* src =
         reinterpret_cast<const float4*>(A.g.out_pts + b * A.g.out_pts_bstride + (long)row0 * d);
+    const float4* cen = reinterpret_cast<const float4*>(A.g.ctr + b * A.g.ctr_bstride);
     const int q4 = d / 4;
     for (int idx = tid - 32; idx < nrows * q4; idx += TC_THREADS - 32) {
       const int r = idx / q4, c = idx - r * q4;
-      *reinterpret_cast<float4*>(ys + r * YS + 4 * c) = src[idx];
+      const float4 v = src[idx], cv = __ldg(cen + c);  // y' = y - centre (see init_tile)
+      *reinterpret_cast<float4*>(ys + r * YS + 4 * c) =
+          make_float4(v.x - cv.x, v.y - cv.y, v.z - cv.z, v.w - cv.w);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(TC_THREADS - 32) : "memory");
   }
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       uint32_t vh[8], vl[8];
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
-        const float a0 = TC_YSCALE * yv[2 * cc], a1 = TC_YSCALE * yv[2 * cc + 1];
+        const float a0 = A.g.ascale * yv[2 * cc], a1 = A.g.ascale * yv[2 * cc + 1];
         const float h0 = __half2float(__float2half_rn(a0)), h1 = __half2float(__float2half_rn(a1));
         vh[cc] = pack_h2(h0, h1);
         vl[cc] = pack_h2(a0 - h0, a1 - h1);
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks)  // two 16-wide K slices (2 KB each) per stage
                   tc_slice_mmas(st * 32 + ks * 16, dp, dcol, abase,
-                                bds + (uint64_t)((ks * 2048) >> 4), idesc, first);
+                                bds + (uint64_t)((ks * 2048) >> 4), idesc, first, full4);
                 if (j == TC_NB - 1) tc::mma2_commit_mc(&empty_b[slot], 3);
                 if (++slot == TC_STAGES) {
                   slot = 0;

@@ -170,10 +170,35 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)),
                "sinkhorn workspace")
     ws = D.workspace(size.value)
+    status = None
+    if variant == "g" and "berg" in (ent1, ent2):  # lambda* by Newton: NewtonError possible
+        status = t.zeros((B,), dtype=t.int32, device=a.device)
+        desc.status = _lib.ptr(status)
     _lib.check(lib.uot_sinkhorn_run(ctypes.byref(desc), _lib.ptr(ws), ctypes.c_size_t(size.value),
                                     _lib.stream_handle(stream)), "uot_sinkhorn_run")
     del rows_arr  # host array read during the (synchronous) enqueue only
+    if status is not None:
+        raise_newton_status(status)
     return f, g, trace, its
+
+
+_NEWTON_MESSAGES = {  # src/duality.py:188-189, :220-229, :247
+    1: "empty translation domain for Berg conjugates",
+    2: "failed to bracket the optimal translation",
+    3: "translation Newton did not reach the residual target",
+}
+
+
+def raise_newton_status(status):
+    """Raise the reference's NewtonError for the first failed problem of a
+    per-problem status vector (uot_sinkhorn_run / uot_translation codes)."""
+    from .exceptions import NewtonError
+
+    st = D.to_np(status, readonly=False)
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        code = int(st[bad[0]])
+        raise NewtonError(_NEWTON_MESSAGES.get(code, f"translation Newton failed ({code})"))
 
 
 def verify_batched(x, y, a, b, f, g, eps, rho1, rho2, cost="sqeuclid", p=2.0, c=None,

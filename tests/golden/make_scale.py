@@ -111,7 +111,7 @@ def dual_h(cost, a, b, f, g, eps, rho):
 def gen_cfg3(iters=200):
     c = S.cfg3_inputs()
     cost = FastPointCost(c.x, c.y)
-    f, g, delta, snaps = h_run(cost, c.alpha, c.beta, c.eps, c.rho, iters, keep=(1, 20))
+    f, g, delta, snaps = h_run(cost, c.alpha, c.beta, c.eps, c.rho, iters, keep=(1,))
     out = dict(eps=c.eps, rho=c.rho, iters=iters, f=f, g=g, delta=delta,
                lam=O.lambda_star_kl(c.alpha, c.beta, f, g, c.rho, c.rho),
                dual=dual_h(cost, c.alpha, c.beta, f, g, c.eps, c.rho))
@@ -143,12 +143,12 @@ def gen_cfg5(iters=200, problems=(0, 1)):
             t0 = time.time()
             r = O.fw_barycenter_fixed(list(x[0]), list(w[0]), om, 1.0, iters, step=step)
             tag = f"p{p}_{step[0]}"
-            out[f"{tag}_pots"] = np.stack(r["pots_raw"])
+            pots = np.stack(r["pots"])  # translated by the final lambda (barycenter.py:413-414)
+            # every 8th atom of every list (fixture size) + per-list sums of all atoms
+            out[f"{tag}_pots8"] = pots[:, ::8].copy()
+            out[f"{tag}_potsum"] = pots.sum(axis=1)
             for key in ("h0", "fw_gap", "pd_gap", "gamma", "nnz", "supp_hash"):
                 out[f"{tag}_{key}"] = r[key]
-            idx, mass = r["plan"]
-            out[f"{tag}_idx"] = idx.astype(np.int16)
-            out[f"{tag}_mass"] = mass
             print(f"  cfg5 problem {p} {step}: {time.time() - t0:.0f}s", flush=True)
     save("cfg5_full.npz", **out)
 

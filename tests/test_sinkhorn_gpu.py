@@ -316,3 +316,25 @@ def test_row_sharded_real_nccl_single_rank():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,offset", [(2, 1000.0), (3, -300.0), (5, 1000.0), (2, 0.0)])
+def test_fp32_point_clouds_off_origin(d, offset):
+    """The fp32 expanded-form engines (x.y on the FMA pipe, records
+    U = (hat - |x|^2) L + log2 w) take the points relative to the midpoint
+    of the two clouds' centroids (sk_center), so a cloud far from the origin
+    keeps fp32 tolerance: uncentred, |x|^2 L would swamp the exponent.  The
+    oracle runs on the same fp32-rounded points (fp64)."""
+    rng = np.random.default_rng(d)
+    n, m = 700, 530
+    x = (rng.standard_normal((n, d)) * 0.3 + offset).astype(np.float32).astype(np.float64)
+    y = (rng.standard_normal((m, d)) * 0.3 + 0.2 + offset).astype(np.float32).astype(np.float64)
+    a = rng.uniform(0.5, 1.5, n)
+    a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m)
+    b *= 1.2 / b.sum()
+    eps = 0.02
+    f, g, _, _ = run_dev(x[None], y[None], a[None], b[None], eps, 1.0, 50, precision="fp32")
+    fo, go, _ = O.sinkhorn_fixed(O.PointCost(x, y), a, b, eps, 1.0, 1.0, "h", 50)
+    err = max(np.abs(f[0] - fo).max(), np.abs(g[0] - go).max())
+    assert err <= 1e-4 * eps, err

@@ -67,3 +67,21 @@ def test_anderson_g_berg_traces(k):
         np.testing.assert_allclose(rep.trace[key], z[f"s{k}_and_{key}"], rtol=1e-7, atol=1e-11,
                                    err_msg=key)
     np.testing.assert_allclose(rep.final.f, z[f"s{k}_and_f"], rtol=0, atol=1e-10)
+
+
+def test_g_sinkhorn_berg_newton_error_like_reference():
+    """an empty Berg translation domain (src/duality.py:188-189)
+    raises NewtonError from the device G run exactly where the reference
+    raises it (checked against uotkit in the build container: Berg/Berg with
+    f0 = g0 = -3 raises, Berg/KL from the same start runs)."""
+    x = np.linspace(0, 1, 20)
+    a, b = np.full(20, 0.05), np.full(20, 0.06)
+    init = P.DualPair(np.full(20, -3.0), np.full(20, -3.0))
+    prob = P.UotProblem(P.DiscreteMeasure(x, a), P.DiscreteMeasure(x, b), P.PowerDistance(2.0),
+                        P.Berg(1.0), P.Berg(1.0), eps=0.05)
+    with pytest.raises(P.NewtonError, match="empty translation domain"):
+        P.run(prob, P.SinkhornConfig("g", 10, 1e-12), init=init)
+    prob = P.UotProblem(P.DiscreteMeasure(x, a), P.DiscreteMeasure(x, b), P.PowerDistance(2.0),
+                        P.Berg(1.0), P.KL(1.0), eps=0.05)
+    rep = P.run(prob, P.SinkhornConfig("g", 10, 1e-12), init=init)
+    assert np.isfinite(rep.final.f).all() and np.isfinite(rep.final.g).all()

@@ -5,6 +5,7 @@ import ctypes
 import numpy as np
 import pytest
 
+import paper_2201_00730_b200 as P
 from paper_2201_00730_b200 import _device as D
 from paper_2201_00730_b200 import _lib
 
@@ -51,3 +52,39 @@ def test_tc_selftest_pair(K):
     got = D.to_np(d)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
     np.testing.assert_allclose(got, ref, rtol=0, atol=2e-5 * np.sqrt(K))
+
+
+@pytest.mark.parametrize("offset,eps", [(5000.0, 0.05), (0.0, 0.004)])
+def test_tc_path_off_origin_and_small_eps(offset, eps, monkeypatch):
+    """the tcgen05 operands are the points relative to the first
+    source point with a balanced power-of-two scale, so clouds far from the
+    origin (the old fixed 8 y / (2L/8) x split overflowed fp16 there) and small
+    eps stay finite and as accurate as the fp32 SIMT engine on the same
+    inputs (UOT_SINKHORN_SIMT=1).  At eps = 0.05 both meet 1e-4 * eps; at
+    eps = 0.004 fp32 itself cannot (log2-domain arguments ~ 1e3 carry 1e-4
+    absolute rounding), so the bar there is the SIMT engine's own error.  The
+    oracle gets the same fp32-rounded points."""
+    import oracle as O
+    from paper_2201_00730_b200 import synthetic as S
+
+    x, y, a, b = S.cfg4_batch(batch=1, n=384, m=320, d=64, seed=77)
+    x = (x + offset).astype(np.float32).astype(np.float64)
+    y = (y + offset).astype(np.float32).astype(np.float64)
+    fo, go, _ = O.sinkhorn_fixed(O.PointCost(x[0], y[0]), a[0], b[0], eps, 0.5, 0.5, "h", 20)
+    lamo = O.lambda_star_kl(a[0], b[0], fo, go, 0.5, 0.5)
+
+    def err_of(simt):
+        if simt:
+            monkeypatch.setenv("UOT_SINKHORN_SIMT", "1")
+        else:
+            monkeypatch.delenv("UOT_SINKHORN_SIMT", raising=False)
+        f, g, _, _ = P.sinkhorn_batched(x, y, a, b, eps, 0.5, 0.5, 20, precision="fp32")
+        f = f[0].cpu().numpy().astype(np.float64)
+        g = g[0].cpu().numpy().astype(np.float64)
+        assert np.isfinite(f).all() and np.isfinite(g).all()
+        lam = O.lambda_star_kl(a[0], b[0], f, g, 0.5, 0.5)
+        return max(np.abs(f + lam - fo - lamo).max(), np.abs(g - lam - go + lamo).max())
+
+    e_tc, e_simt = err_of(False), err_of(True)
+    print(f"offset {offset} eps {eps}: tcgen05 {e_tc:.3e}, SIMT {e_simt:.3e}")
+    assert e_tc <= max(1e-4 * eps, 2.0 * e_simt), (e_tc, e_simt)
