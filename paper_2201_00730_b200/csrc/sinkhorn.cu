@@ -305,24 +305,31 @@ __global__ void tc_init_static(float* rec, long rec_bstride, const float* pts, c
 
 // Centre of problem b's fp32 point clouds (the expanded-form engines SqE32<D>,
 // SqE32N and the tcgen05 path): the midpoint of the two clouds' centroids,
-// c = (mean x + mean y) / 2.  |x - y|^2 = |x'|^2 - 2 x'.y' + |y'|^2 for any c,
+// c = (mean x + mean y) / 2, estimated on an evenly strided sample of at most
+// CTR_SAMPLES points per side (one short kernel per solve; any c inside the
+// clouds' hull does the job).  |x - y|^2 = |x'|^2 - 2 x'.y' + |y'|^2 for any c,
 // and with x' = x - c, y' = y - c every term scales with the clouds' radii,
 // not with their distance from the origin (no cancellation).  For d <= 256,
-// thread t of the (R x d)-thread block owns coordinate t % d of rows t / d,
+// thread t of the (R x d)-thread block owns coordinate t % d of samples t / d,
 // t/d + R, ...; the R partials of a coordinate are added in a fixed order
 // (deterministic); larger d loops over the coordinates.
+constexpr int CTR_SAMPLES = 1024;
+
 __global__ void __launch_bounds__(256) sk_center(const float* x, const float* y, int n, int m,
                                                  int d, float* ctr) {
   __shared__ double part[256];
   const int b = blockIdx.x;
   const float* xb = x + (long)b * n * d;
   const float* yb = y + (long)b * m * d;
+  const int sn = min(n, CTR_SAMPLES), sm = min(m, CTR_SAMPLES);
+  auto row_x = [&](int s) { return (long)s * n / sn; };
+  auto row_y = [&](int s) { return (long)s * m / sm; };
   if (d > 256) {
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
       double sx = 0.0, sy = 0.0;
-      for (int i = 0; i < n; ++i) sx += (double)xb[(long)i * d + k];
-      for (int j = 0; j < m; ++j) sy += (double)yb[(long)j * d + k];
-      ctr[(long)b * d + k] = (float)(0.5 * (sx / n + sy / m));
+      for (int i = 0; i < sn; ++i) sx += (double)xb[row_x(i) * d + k];
+      for (int j = 0; j < sm; ++j) sy += (double)yb[row_y(j) * d + k];
+      ctr[(long)b * d + k] = (float)(0.5 * (sx / sn + sy / sm));
     }
     return;
   }
@@ -330,10 +337,10 @@ __global__ void __launch_bounds__(256) sk_center(const float* x, const float* y,
   const int k = threadIdx.x % d, r0 = threadIdx.x / d;
   double sx = 0.0, sy = 0.0;
   if (r0 < R) {
-    for (int i = r0; i < n; i += R) sx += (double)xb[(long)i * d + k];
-    for (int j = r0; j < m; j += R) sy += (double)yb[(long)j * d + k];
+    for (int i = r0; i < sn; i += R) sx += (double)xb[row_x(i) * d + k];
+    for (int j = r0; j < sm; j += R) sy += (double)yb[row_y(j) * d + k];
   }
-  part[threadIdx.x] = 0.5 * (sx / n + sy / m);
+  part[threadIdx.x] = 0.5 * (sx / sn + sy / sm);
   __syncthreads();
   if (threadIdx.x < d) {
     double c = 0.0;
