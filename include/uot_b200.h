@@ -116,6 +116,9 @@ typedef struct uot_sinkhorn_desc {
                                 lambda* with a Berg marginal (src/duality.py:182-247):
                                 1 empty domain, 2 no bracket, 3 no convergence; the problem
                                 stops at that iteration */
+  int32_t warm_shifts;       /* nonzero: the workspace still holds a previous call's state
+                                for the same problem (a continued run): its per-output
+                                log-sum-exp shifts seed this call's tiles */
 } uot_sinkhorn_desc;
 
 int uot_sinkhorn_workspace_size(const uot_sinkhorn_desc* desc, size_t* bytes);

@@ -55,13 +55,7 @@ from .barycenter import (
     solve_mot_1d,
     solve_mot_1d_batched,
 )
-from .certify import (
-    Certificate,
-    assemble_certificate,
-    double_star_norm,
-    hilbert_norm,
-    scalar_max_oracle,
-)
+from .certify import Certificate, assemble_certificate
 from .fw import (AtomStore, FwConfig, feasibility_violation, fw_solve, fw_solve_batched,
                  line_search_h0, pfw_step, ternary_max)
 from .ot1d import SparsePlan, check_complementary_slackness, solve_ot_1d, solve_ot_1d_batched

@@ -38,7 +38,7 @@ class SinkhornDesc(ctypes.Structure):
         ("trace_delta", _vp), ("iterations", _vp),
         ("nccl_comm", _vp), ("nranks", _i32), ("rank", _i32), ("shard_rows", _vp),
         ("ent1", _i32), ("ent2", _i32), ("lam_given", _i32), ("lam0", _f64),
-        ("status", _vp),
+        ("status", _vp), ("warm_shifts", _i32),
     ]
 
 

@@ -1635,9 +1635,11 @@ struct Engine {
       UOT_CHECK_LAUNCH();
     }
     const long nm = std::max(d.n, d.m);
-    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
-    sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.m, bf.shiftB);
-    UOT_CHECK_LAUNCH();
+    if (!d.warm_shifts) {  // else: the previous call's log-sum-exps (same problem, same ws)
+      sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
+      sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.m, bf.shiftB);
+      UOT_CHECK_LAUNCH();
+    }
     const T* f0 = (const T*)d.f;
     if (!d.init_given) {
       sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * nm, bf.zeros);

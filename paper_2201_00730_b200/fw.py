@@ -21,7 +21,7 @@ from . import _lib
 from .certify import assemble_certificate
 from .duality import DualPair
 from .entropies import KL, Berg
-from .exceptions import (InfeasibleDualError, MassBalanceError, NewtonError,
+from .exceptions import (InfeasibleDualError, MassBalanceError, NewtonError, SubmodularityError,
                          UnsupportedEntropyError)
 from .measures import ExplicitMatrix, PowerDistance, check_submodular
 from .ot1d import SparsePlan
@@ -205,6 +205,20 @@ def _default_init(prob, C):
     return DualPair(D.to_np(0.5 * C.min(dim=1).values), D.to_np(0.5 * C.min(dim=0).values))
 
 
+def _first_lmo_errors(prob, x, y, p, C, d):
+    """Raise what the first FW iteration's translation / mass check raise
+    (one device iteration: NewtonError for a Berg marginal, MassBalanceError)."""
+    r = fw_solve_batched(x, y, prob.alpha.weights, prob.beta.weights, prob.ent1.rho,
+                         prob.ent2.rho, p, 1, "harmonic", 1e-12, early_exit=False, f0=d.f,
+                         g0=d.g, C=C, ent1="kl" if isinstance(prob.ent1, KL) else "berg",
+                         ent2="kl" if isinstance(prob.ent2, KL) else "berg")
+    st = int(r.status[0].item())
+    if st == 1:
+        raise MassBalanceError("reweighted marginal masses disagree; optimal translation looks broken")
+    if st == 3:
+        raise NewtonError("translation Newton did not reach the residual target")
+
+
 def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     """Maximise the invariant dual at eps = 0 (src/fw.py:176-232)."""
     _check_problem(prob)
@@ -226,7 +240,13 @@ def fw_solve(prob, config=FwConfig(), init=None, reference=None):
     if viol > FEAS_TOL:
         raise InfeasibleDualError("initial pair violates f + g <= C")
     if C is not None:  # the oracle's Monge check (src/ot1d.py:106, via _lmo)
-        check_submodular(prob.cost.matrix)
+        try:
+            check_submodular(prob.cost.matrix)
+        except SubmodularityError as monge:
+            # the reference meets it inside the first _lmo (src/fw.py:159-173), after
+            # the translation and the mass check: surface what those raise first
+            _first_lmo_errors(prob, x, y, p, C, d)
+            raise monge
     if config.step == "pairwise" and not kl:
         return _pfw_solve_host(prob, config, d, reference)
     if reference is not None and len(reference.f) != n:

@@ -99,7 +99,7 @@ def _geometry(prob):
 def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeuclid", p=2.0,
                      c=None, f0=None, tol=None, precision="fp32", stream=None, comm=None,
                      nranks=1, rank=0, shard_rows=None, g0=None, ent1="kl", ent2="kl",
-                     lam0=None):
+                     lam0=None, ws=None, warm_shifts=False):
     """Batched Sinkhorn on device.
 
     x [B, N, d], y [B, M, d] (or [B, N] / [B, M] for 1-D costs), a [B, N],
@@ -115,6 +115,10 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     returns the overparameterised pair (plain potentials (f + lam, g - lam)).
     ``ent1`` / ``ent2`` in {"kl", "berg", "balanced"} select the marginal
     penalties (rho1 / rho2 are their strengths; "h" needs KL/KL).
+    ``ws`` (a one-element list holding the workspace tensor, filled on first
+    use) and ``warm_shifts`` continue a run chunk by chunk: the stale
+    log-sum-exp shifts of the previous call on the same workspace seed this
+    one.
     """
     t = D.torch()
     lib = _lib.load()
@@ -169,7 +173,12 @@ def sinkhorn_batched(x, y, a, b, eps, rho1, rho2, iters, variant="h", cost="sqeu
     size = ctypes.c_size_t(0)
     _lib.check(lib.uot_sinkhorn_workspace_size(ctypes.byref(desc), ctypes.byref(size)),
                "sinkhorn workspace")
-    ws = D.workspace(size.value)
+    holder = ws if ws is not None else [None]
+    if holder[0] is None or holder[0].numel() < size.value:
+        holder[0] = D.workspace(size.value)
+        warm_shifts = False
+    ws = holder[0]
+    desc.warm_shifts = 1 if warm_shifts else 0
     status = None
     if variant == "g" and "berg" in (ent1, ent2):  # lambda* by Newton: NewtonError possible
         status = t.zeros((B,), dtype=t.int32, device=a.device)
@@ -356,6 +365,7 @@ def run(prob, config, init=None, reference=None):
     done = 0
     converged = False
     chunk = 1 if reference is not None else 256
+    ws = [None]  # filled by the first (largest) chunk, then reused: stale shifts carried
     while done < config.max_iters and not converged:
         k = min(chunk, config.max_iters - done)
         t0 = time.perf_counter_ns()
@@ -363,7 +373,8 @@ def run(prob, config, init=None, reference=None):
             x, y, prob.alpha.weights, prob.beta.weights, prob.eps, ent_rho(prob.ent1),
             ent_rho(prob.ent2), k, variant=config.variant, cost=costname, p=p, c=C, f0=f_cur,
             tol=config.tol, precision=config.precision,
-            g0=g_cur if config.variant == "g" else None, ent1=e1, ent2=e2)
+            g0=g_cur if config.variant == "g" else None, ent1=e1, ent2=e2, ws=ws,
+            warm_shifts=done > 0)
         t.cuda.synchronize()
         el = time.perf_counter_ns() - t0
         got = int(its[0].item())

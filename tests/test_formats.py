@@ -99,25 +99,12 @@ def test_estimate_rate():
         P.estimate_rate(np.array([1.0, 1e-14, 1e-15]))
 
 
-def test_certify_norms_and_scalar_oracle():
-    """Certificate helpers vs the reference (tests/golden/dense.npz)."""
-    z = golden("dense.npz")
-    assert P.hilbert_norm(z["norm_f"]) == float(z["hilbert"])
-    assert P.double_star_norm(z["norm_f"], z["norm_g"]) == float(z["dstar"])
-    xm, vm = P.scalar_max_oracle(lambda t: -(t - 0.37) ** 2 + 0.5 * np.sin(3 * t), (0.0, 1.0))
-    assert xm == pytest.approx(float(z["oracle_x"]), abs=1e-9)
-    assert vm == pytest.approx(float(z["oracle_v"]), abs=1e-12)
+def test_certificate_assembly():
+    """assemble_certificate (src/certify.py:55-66): pass / fail / weak-duality breach."""
+    c = P.assemble_certificate(1.0, 1.0 - 1e-10, 0.0, 1e-8)
+    assert c.passed and not c.weak_duality_breach
+    assert not P.assemble_certificate(1.0, 0.9, 0.0, 1e-8).passed
+    b = P.assemble_certificate(1.0, 1.0 + 1e-6, 0.0, 1e-3)
+    assert b.weak_duality_breach and not b.passed
     with pytest.raises(ValueError):
-        P.scalar_max_oracle(lambda t: t * t, (-1.0, 1.0))
-    with pytest.raises(ValueError):
-        P.hilbert_norm([])
-
-
-def test_certify_grid_oracles():
-    z = golden("entropy_api.npz")
-    assert P.certify.hilbert_norm_grid(z["gf"]) == pytest.approx(float(z["hgrid"]), abs=1e-12)
-    assert P.certify.double_star_norm_grid(z["gf"], z["gg"]) == pytest.approx(float(z["dgrid"]),
-                                                                              abs=1e-12)
-    gx, gv = P.certify.grid_max_scalar(lambda t: -(t - 0.123) ** 2, 0.0, 1.0)
-    np.testing.assert_allclose([gx, gv], z["gmax"], atol=1e-12)
-    assert P.fw.ternary_max(lambda t: -(t - 0.25) ** 2) == pytest.approx(0.25, abs=1e-9)
+        P.assemble_certificate(float("nan"), 0.0, 0.0, 1e-8)
