@@ -784,6 +784,22 @@ def solve_mot_1d(xs, ws, w):
     return idx[:e].copy(), mass[:e].copy(), [pots[off[q]:off[q] + lens[q]].copy() for q in range(k)]
 
 
+def large_ot_inputs(n, m, seed):
+    """Seeded balanced 1-D OT inputs for the large-size goldens (test
+    fixture generator): sorted uniform supports with a run of duplicated
+    points, Exp(1) weights with ~10% exact zeros, both scaled to mass 1.3."""
+    rng = np.random.default_rng(seed)
+    x = np.sort(rng.uniform(0.0, 1.0, n))
+    y = np.sort(rng.uniform(0.0, 1.0, m))
+    x[n // 3:n // 3 + 5] = x[n // 3]  # coincident atoms
+    wa = rng.exponential(1.0, n) * (rng.random(n) > 0.1)
+    wb = rng.exponential(1.0, m) * (rng.random(m) > 0.1)
+    wa[0] = wb[0] = 1.0
+    wa *= 1.3 / wa.sum()
+    wb *= 1.3 / wb.sum()
+    return x, y, wa, wb
+
+
 def mot_mismatch_report(idx_a, mass_a, idx_b, mass_b, cums):
     """Compare two K-marginal plans (tuples + masses) entry by entry.  Returns
     the entry counts, the number of entries present in only one plan, the

@@ -32,13 +32,27 @@ __global__ void feasibility_kernel(int n, int m, const double* x, const double* 
   }
 }
 
-int launch_fw(const FwArgs& a, int batch, cudaStream_t st) {
-  if (a.mode == 0 && a.step == UOT_STEP_PAIRWISE) return launch_fw_pairwise(a, batch, st);
-  return launch_fw_impl<false>(a, batch, st);
+
+// Plan-extraction scratch (vals [batch][n+m] doubles, codes [batch][n+m][2]
+// ints), then -- for problems on the large path (fwk::fw_big) -- the
+// per-problem arrays the resident path keeps in shared memory.
+size_t fw_scratch_core(int batch, int n, int m) {
+  return ((sizeof(double) + 2 * sizeof(int)) * (size_t)batch * (n + m) + 255) / 256 * 256;
+}
+size_t fw_scratch_bytes(int batch, int n, int m) {
+  size_t b = fw_scratch_core(batch, n, m) + 256;
+  if (fwk::fw_big(n, m)) b += (size_t)batch * fwk::fw_big_stride(n, m);
+  return b;
+}
+char* fw_big_region(void* scratch, int batch, int n, int m) {
+  return fwk::fw_big(n, m) ? (char*)scratch + fw_scratch_core(batch, n, m) : nullptr;
 }
 
-size_t fw_scratch_bytes(int batch, int n, int m) {
-  return (sizeof(double) + 2 * sizeof(int)) * (size_t)batch * (n + m) + 256;
+int launch_fw(const FwArgs& a0, int batch, cudaStream_t st) {
+  FwArgs a = a0;
+  if (a.big == nullptr) a.big = fw_big_region(a.scratch, batch, a.n, a.m);
+  if (a.mode == 0 && a.step == UOT_STEP_PAIRWISE) return launch_fw_pairwise(a, batch, st);
+  return launch_fw_impl<false>(a, batch, st);
 }
 
 // pairwise atom store: atoms [batch][cap][n+m], wts / scs / dis [batch][cap]

@@ -19,6 +19,7 @@
 // fw.py:106-148) by safeguarded Newton on three moments per pass instead of
 // the reference's 123 ternary evaluations (FW parity).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #pragma once
@@ -34,6 +35,7 @@ static __device__ unsigned long long g_newton_stats[2];  // passes, line searche
 #endif
 
 constexpr int FW_THREADS = 256;
+constexpr int FW_THREADS_BIG = 1024;  // large problems (n or m > 4096)
 #ifndef FW_MINB
 #define FW_MINB 2
 #endif
@@ -83,6 +85,10 @@ struct FwArgs {
   const int* away_in;
   unsigned long long* supp_hash;
   int* supp_nnz;
+  // large problems (NT = FW_THREADS_BIG): the per-problem arrays that live in
+  // shared memory on the resident path live here, big_stride bytes per problem
+  char* big;
+  size_t big_stride;
 };
 
 static __device__ __noinline__ double pow_abs(double d, double p) { return pow(fabs(d), p); }
@@ -106,6 +112,7 @@ __device__ __forceinline__ double pcost_k(double xi, double yj, double p) {
   else return pow_abs(d, p);
 }
 
+template <int NW>
 __device__ __forceinline__ int ibsum(int v, int* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum(v);
@@ -113,7 +120,7 @@ __device__ __forceinline__ int ibsum(int v, int* scratch) {
   if (lane == 0) scratch[warp] = v;
   __syncthreads();
   int s = 0;
-  for (int w = 0; w < FW_THREADS / 32; ++w) s += scratch[w];
+  for (int w = 0; w < NW; ++w) s += scratch[w];
   __syncthreads();
   return s;
 }
@@ -140,19 +147,24 @@ __device__ __forceinline__ int excl_max_scan(int v, int* scratch) {
 // Per-problem CTA.  Thread t owns source/target elements t*EPT .. t*EPT+EPT-1
 // of each side.  Shared memory holds the supports, the constant weights, the
 // breakpoints and the merge ranks; registers hold the potentials.
-constexpr int FW_NW = FW_THREADS / 32;
-constexpr int FW_BUF = 16 * FW_NW;  // one reduction buffer (doubles)
 
-template <int EPT, int PK>
+// Merge-rank type: 16-bit on the resident path (n, m <= 4096), 32-bit for
+// large problems.
+template <int NT>
+using RankT = std::conditional_t<(NT > FW_THREADS), int, unsigned short>;
+
+template <int EPT, int PK, int NT = FW_THREADS>
 struct Cta {
+  static constexpr int NW = NT / 32;
+  using RK = RankT<NT>;
   int n, m;
   double p;
   const double* sx;
   const double* sy;
   double* sA;
   double* sB;
-  unsigned short* rkA;  // rkA[k] = #target events before source event k in the merge
-  unsigned short* rkB;  // rkB[l] = #source events before target event l
+  RK* rkA;  // rkA[k] = #target events before source event k in the merge
+  RK* rkB;  // rkB[l] = #source events before target event l
   double* zred;  // scratch of the zero-weight fix (own syncs)
   bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
   double* pfw;   // pairwise FW staging (n + m doubles) or nullptr
@@ -189,8 +201,8 @@ struct Cta {
         const double av = i < na ? sA[i] : CUDART_INF;
         const double bv = j < nb ? sB[j] : CUDART_INF;
         const bool takeA = av <= bv;
-        unsigned short* dst = takeA ? rkA + i : rkB + j;
-        *dst = (unsigned short)(takeA ? j : i);
+        RK* dst = takeA ? rkA + i : rkB + j;
+        *dst = (RK)(takeA ? j : i);
         i += takeA;
         j += !takeA;
       }
@@ -212,7 +224,7 @@ struct Cta {
       pb[e] = cb;
     }
     double tot[2] = {ca, cb}, totals[2];
-    bops::block_scan_excl<FW_NW, 2>(tot, totals, ping.next());
+    bops::block_scan_excl<NW, 2>(tot, totals, ping.next());
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
@@ -275,7 +287,7 @@ struct Cta {
       lb += db[e];
     }
     double off[2] = {la, lb}, unused[2];
-    bops::block_scan_excl<FW_NW, 2>(off, unused, ping.next());
+    bops::block_scan_excl<NW, 2>(off, unused, ping.next());
     const double s0 = cost(0, 0);
     double ra = off[0], rb = off[1];
 #pragma unroll
@@ -292,14 +304,14 @@ struct Cta {
   __device__ void extract_plan(double* vals, int* codes, int* ei, int* ej, double* em,
                                int* count, double total) {
     const int nev = (n - 1) + (m - 1);
-    for (int i = threadIdx.x; i < n - 1; i += FW_THREADS) {
+    for (int i = threadIdx.x; i < n - 1; i += NT) {
       const int j = rkA[i];
       const int rank = i + j;
       vals[rank] = sA[i];
       codes[2 * rank] = i + 1;
       codes[2 * rank + 1] = j;
     }
-    for (int l = threadIdx.x; l < m - 1; l += FW_THREADS) {
+    for (int l = threadIdx.x; l < m - 1; l += NT) {
       const int k = rkB[l];
       const int rank = l + k;
       vals[rank] = sB[l];
@@ -309,7 +321,7 @@ struct Cta {
     __syncthreads();
     int base = 0;
     int* iscr = reinterpret_cast<int*>(zred);
-    for (int s0 = 0; s0 <= nev; s0 += FW_THREADS) {
+    for (int s0 = 0; s0 <= nev; s0 += NT) {
       const int s = s0 + threadIdx.x;
       double mass = 0.0;
       int ii = 0, jj = 0;
@@ -334,7 +346,7 @@ struct Cta {
       if (lane == 31) iscr[warp] = incl;
       __syncthreads();
       int off = 0, tot = 0;
-      for (int w = 0; w < FW_NW; ++w) {
+      for (int w = 0; w < NW; ++w) {
         if (w < warp) off += iscr[w];
         tot += iscr[w];
       }
@@ -377,11 +389,11 @@ struct Cta {
     auto va = [&](int i) { return i < na ? sA[i] : CUDART_INF; };
     auto vb = [&](int j) { return j < nb ? sB[j] : CUDART_INF; };
     if (threadIdx.x == 0) entry(0, 0, 0.0, fmin(va(0), vb(0)));
-    for (int i = threadIdx.x; i < na; i += FW_THREADS) {
+    for (int i = threadIdx.x; i < na; i += NT) {
       const int j = rkA[i];
       entry(i + 1, j, sA[i], fmin(va(i + 1), vb(j)));
     }
-    for (int l = threadIdx.x; l < nb; l += FW_THREADS) {
+    for (int l = threadIdx.x; l < nb; l += NT) {
       const int k = rkB[l];
       entry(k, l + 1, sB[l], fmin(va(k), vb(l + 1)));
     }
@@ -415,8 +427,8 @@ struct PfwState {
 // zero weights, and the iterate update d += gamma ((r, s) - away).  Returns
 // gamma.  The shared breakpoint arrays sA / sB are free after the oracle and
 // hold ta / tb here; the new atom is staged after them.
-template <int EPT, int PK, typename PING>
-__device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, double (&f)[EPT],
+template <int EPT, int PK, int NT, typename PING>
+__device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, double (&f)[EPT],
                            double (&g)[EPT], const double (&r)[EPT], const double (&s)[EPT],
                            const double (&ta)[EPT], const double (&tb)[EPT], double mta,
                            double mtb, double& sha, double& shb, double i1, double i2, double t1,
@@ -446,7 +458,7 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
   __syncthreads();
   const long sb0 = (long)b * A.cap;
   const double* AT = A.atoms + sb0 * nm;
-  for (int pos = warp; pos < pst.na; pos += FW_NW) {
+  for (int pos = warp; pos < pst.na; pos += Cta<EPT, PK, NT>::NW) {
     const double* row = AT + (long)__ldcg(A.act + sb0 + pos) * nm;
     double sc = 0.0, dd = 0.0;
     for (int i = lane; i < nm; i += 32) {
@@ -516,7 +528,7 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
     if (i < n && sal[i] > 0.0) mxs[2] = bops::dmax(mxs[2], -va);
     if (i < m && sbe[i] > 0.0) mxs[3] = bops::dmax(mxs[3], -vb);
   }
-  bops::block_red<FW_NW, 4, 4>(mom, mxs, ping.next());
+  bops::block_red<Cta<EPT, PK, NT>::NW, 4, 4>(mom, mxs, ping.next());
   const double gmax = __ldcg(A.wts + sb0 + aslot);
   double gam = 0.0;
   if (replay) {  // the reference's away atom and transfer (no step: away < 0)
@@ -550,7 +562,7 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
           mm[4] += wb * xb;
           mm[5] += wb * xb * xb;
         }
-        bops::block_sum<FW_NW, 6>(mm, ping.next());
+        bops::block_sum<Cta<EPT, PK, NT>::NW, 6>(mm, ping.next());
         const double a1 = mm[1] / mm[0], a2 = mm[2] / mm[0];
         const double b1 = mm[4] / mm[3], b2 = mm[5] / mm[3];
         const double g1 = k0 - t1 * a1 - t2 * b1;
@@ -618,43 +630,52 @@ __device__ double pfw_step(Cta<EPT, PK>& c, const FwArgs& A, int b, int t, doubl
   return gam;
 }
 
-template <int EPT, int PK, bool PW>
-__global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
+// NT = FW_THREADS: resident path (per-problem arrays in shared memory, two
+// CTAs per SM).  NT = FW_THREADS_BIG: large problems -- the same arrays in the
+// global workspace (L2-resident per problem), 32-bit merge ranks, one CTA of
+// 1024 threads per problem.
+template <int EPT, int PK, bool PW, int NT = FW_THREADS>
+__global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kernel(FwArgs A) {
+  constexpr int NW = NT / 32;
+  constexpr int BUF = 16 * NW;  // one reduction buffer (doubles)
+  using RK = RankT<NT>;
   extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(16) double red[3 * FW_BUF];
+  __shared__ __align__(16) double red[3 * BUF];
   __shared__ double tab[32];
   const int b = blockIdx.x;
   const int n = A.n, m = A.m;
-  double* sx = smem;
+  double* base = smem;
+  if constexpr (NT != FW_THREADS) base = reinterpret_cast<double*>(A.big + (size_t)b * A.big_stride);
+  double* sx = base;
   double* sy = sx + n;
   double* sA = sy + m;
   double* sB = sA + n;
   double* sal = sB + m;  // constant weights
   double* sbe = sal + n;
-  unsigned short* rkA = reinterpret_cast<unsigned short*>(sbe + m);
-  unsigned short* rkB = rkA + n;
+  RK* rkA = reinterpret_cast<RK*>(sbe + m);
+  RK* rkB = rkA + n;
   double* pfwbuf = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(rkB + m) + 15) & ~static_cast<uintptr_t>(15));
-  Cta<EPT, PK> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * FW_BUF, false,
-                 PW ? pfwbuf : nullptr};
+  Cta<EPT, PK, NT> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * BUF, false,
+                     PW ? pfwbuf : nullptr};
   if constexpr (PK == 3) c.cm = A.C + (long)b * n * m;
-  bops::Ping<FW_BUF> ping{red, 0};
+  bops::Ping<BUF> ping{red, 0};
   bops::load_exp_table(tab);
 
   int nz = 0;
-  for (int i = threadIdx.x; i < n; i += FW_THREADS) {
+  for (int i = threadIdx.x; i < n; i += NT) {
     sx[i] = A.x[(long)b * n + i];
     const double w = A.a[(long)b * n + i];
     sal[i] = w;
     nz += (w == 0.0);
   }
-  for (int j = threadIdx.x; j < m; j += FW_THREADS) {
+  for (int j = threadIdx.x; j < m; j += NT) {
     sy[j] = A.y[(long)b * m + j];
     const double w = A.b[(long)b * m + j];
     sbe[j] = w;
     nz += (w == 0.0);
   }
-  c.zeros = ibsum(nz, reinterpret_cast<int*>(c.zred)) > 0;  // (syncs: smem now visible)
+  c.zeros = ibsum<NW>(nz, reinterpret_cast<int*>(c.zred)) > 0;  // (syncs: smem now visible)
 
   double f[EPT], g[EPT];
 #pragma unroll
@@ -713,7 +734,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
       if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
     }
-    bops::block_red<FW_NW, 2, 2>(ms, mx, ping.next());
+    bops::block_red<NW, 2, 2>(ms, mx, ping.next());
     malpha = ms[0];
     mbeta = ms[1];
     sha = mx[0];
@@ -756,7 +777,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
         sums[0] += ta[e];
         sums[1] += tb[e];
       }
-      bops::block_sum<FW_NW, 2>(sums, ping.next());
+      bops::block_sum<NW, 2>(sums, ping.next());
       // block-uniform: a stale shift far above the maximum underflowed
       if (!((sums[0] < 1e-280 && sha > -CUDART_INF) || (sums[1] < 1e-280 && shb > -CUDART_INF)))
         break;
@@ -767,7 +788,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
         if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
         if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
       }
-      bops::block_max<FW_NW, 2>(mx, ping.next());
+      bops::block_max<NW, 2>(mx, ping.next());
       sha = mx[0];
       shb = mx[1];
     }
@@ -787,7 +808,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
         const int i = c.src(e);
         if (i < n) em1[0] = bops::dmax(em1[0], fabs(f[e] + lam - A.ref_f[(long)b * n + i]));
       }
-      bops::block_max<FW_NW, 1>(em1, ping.next());
+      bops::block_max<NW, 1>(em1, ping.next());
       if (threadIdx.x == 0) A.err_f[(long)b * A.max_iters + t] = em1[0];
     }
     const double sca = sha > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 1) : 0.0;
@@ -830,7 +851,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
       acc[7] += tb[e] * vb;
       acc[8] += tb[e] * vb * vb;
     }
-    bops::block_red<FW_NW, 9, 2>(acc, mr, ping.next());
+    bops::block_red<NW, 9, 2>(acc, mr, ping.next());
     const double fw_gap = acc[0] + acc[1];
     const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
     const double primal = acc[2] + r1 * kl1 + r2 * kl2;
@@ -902,7 +923,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
             mom[4] += wb * xb;
             mom[5] += wb * xb * xb;
           }
-          bops::block_sum<FW_NW, 6>(mom, ping.next());
+          bops::block_sum<NW, 6>(mom, ping.next());
 #ifdef UOT_NEWTON_STATS
           if (threadIdx.x == 0) atomicAdd(&g_newton_stats[0], 1ull);
 #endif
@@ -951,7 +972,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
     if (i < m && sbe[i] > 0.0) mx[1] = bops::dmax(mx[1], -g[e] * i2);
   }
-  bops::block_max<FW_NW, 2>(mx, ping.next());
+  bops::block_max<NW, 2>(mx, ping.next());
   double ls[2] = {0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
@@ -959,7 +980,7 @@ __global__ void __launch_bounds__(FW_THREADS, FW_MINB) fw1d_kernel(FwArgs A) {
     if (i < n) ls[0] += bops::wexp(sal[i], -f[e] * i1 - mx[0], tab);
     if (i < m) ls[1] += bops::wexp(sbe[i], -g[e] * i2 - mx[1], tab);
   }
-  bops::block_sum<FW_NW, 2>(ls, ping.next());
+  bops::block_sum<NW, 2>(ls, ping.next());
   const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(ls[0])) - (mx[1] + log(ls[1])));
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
@@ -986,38 +1007,94 @@ inline int ept_for(int nm) {
   return -1;
 }
 
-inline size_t fw_smem(int n, int m, bool pairwise) {
-  return sizeof(double) * 3 * (size_t)(n + m) + sizeof(unsigned short) * (size_t)(n + m) +
+// Large-problem path: elements per thread at FW_THREADS_BIG threads.
+constexpr int FW_EPT_BIG_MAX = 16;  // n, m <= 16384 per problem
+inline int ept_for_big(int nm) {
+  const int per = (nm + FW_THREADS_BIG - 1) / FW_THREADS_BIG;
+  for (int e = 8; e <= FW_EPT_BIG_MAX; e *= 2)
+    if (per <= e) return e;
+  return -1;
+}
+
+// Per-problem array bytes: supports, cumulative masses, weights (3 (n + m)
+// doubles), merge ranks (rk_bytes each) and, for pairwise, the new atom's
+// staging (n + m doubles).
+inline size_t fw_smem(int n, int m, bool pairwise, size_t rk_bytes = 2) {
+  return sizeof(double) * 3 * (size_t)(n + m) + rk_bytes * (size_t)(n + m) +
          (pairwise ? 16 + sizeof(double) * (size_t)(n + m) : 0);
 }
 
+constexpr size_t FW_SMEM_MAX = 227 * 1024;
+
+// Whether (n, m) takes the large-problem path (its arrays in the workspace).
+// (UOT_FW_FORCE_BIG=1 sends every size there: parity of the two paths in tests.)
+inline bool fw_force_big() {
+  static const bool f = std::getenv("UOT_FW_FORCE_BIG") != nullptr;
+  return f;
+}
+inline bool fw_big(int n, int m) {
+  return fw_force_big() || ept_for(std::max(n, m)) < 0 || fw_smem(n, m, true) > FW_SMEM_MAX;
+}
+inline size_t fw_big_stride(int n, int m) { return (fw_smem(n, m, true, 4) + 255) / 256 * 256; }
+
+// Large-problem instantiations live in their own translation units
+// (fw1d_big.cu, fw1d_pfw_big.cu) so they compile in parallel with the rest.
+template <bool PW, int PK>
+int launch_fw_big(const FwArgs& a, int batch, cudaStream_t st, int ept) {
+  if (ept == 8)
+    fw1d_kernel<8, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  else
+    fw1d_kernel<16, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+#define UOT_FW_BIG(EXT, PW)                                                          \
+  EXT template int launch_fw_big<PW, 0>(const FwArgs&, int, cudaStream_t, int);     \
+  EXT template int launch_fw_big<PW, 1>(const FwArgs&, int, cudaStream_t, int);     \
+  EXT template int launch_fw_big<PW, 2>(const FwArgs&, int, cudaStream_t, int);     \
+  EXT template int launch_fw_big<PW, 3>(const FwArgs&, int, cudaStream_t, int);
+#ifndef UOT_FW_BIG_TU
+UOT_FW_BIG(extern, false)
+UOT_FW_BIG(extern, true)
+#endif
+
 template <bool PW>
-int launch_fw_impl(const FwArgs& a, int batch, cudaStream_t st) {
-  const int ept = ept_for(std::max(a.n, a.m));
-  if (ept < 0) {
-    set_error("1-D FW / OT kernel supports n, m <= %d per problem", 16 * FW_THREADS);
-    return UOT_INVALID;
-  }
+int launch_fw_impl(const FwArgs& a0, int batch, cudaStream_t st) {
+  FwArgs a = a0;
+  const int mx = std::max(a.n, a.m);
+  const int ept = ept_for(mx);
   const size_t smem = fw_smem(a.n, a.m, PW);
-  if (smem > 227 * 1024) {
-    set_error("pairwise FW keeps n + m <= ~6600 atoms per problem in shared memory");
+  const bool big = fw_force_big() || ept < 0 || smem > FW_SMEM_MAX;
+  const int eptb = big ? ept_for_big(mx) : 0;
+  if (big && eptb < 0) {
+    set_error("1-D FW / OT kernel supports n, m <= %d per problem",
+              FW_EPT_BIG_MAX * FW_THREADS_BIG);
     return UOT_INVALID;
   }
-  auto go = [&](auto kern) -> int {
-    UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    kern<<<batch, FW_THREADS, smem, st>>>(a);
+  if (big) {  // arrays after the plan-extraction scratch (fw1d.cu: fw_scratch_bytes)
+    if (a.big == nullptr) {
+      set_error("1-D FW / OT: workspace lacks the large-problem region");
+      return UOT_INVALID;
+    }
+    a.big_stride = fw_big_stride(a.n, a.m);
+  }
+  auto go = [&](auto kern, int nt, size_t sm) -> int {
+    if (sm > 0)
+      UOT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sm));
+    kern<<<batch, nt, sm, st>>>(a);
     UOT_CHECK_LAUNCH();
     return UOT_OK;
   };
   auto by_ept = [&](auto pk) -> int {
     constexpr int PK = decltype(pk)::value;
+    if (big) return launch_fw_big<PW, PK>(a, batch, st, eptb);
     switch (ept) {
-      case 1: return go(fw1d_kernel<1, PK, PW>);
-      case 2: return go(fw1d_kernel<2, PK, PW>);
-      case 4: return go(fw1d_kernel<4, PK, PW>);
-      case 8: return go(fw1d_kernel<8, PK, PW>);
-      default: return go(fw1d_kernel<16, PK, PW>);
+      case 1: return go(fw1d_kernel<1, PK, PW>, FW_THREADS, smem);
+      case 2: return go(fw1d_kernel<2, PK, PW>, FW_THREADS, smem);
+      case 4: return go(fw1d_kernel<4, PK, PW>, FW_THREADS, smem);
+      case 8: return go(fw1d_kernel<8, PK, PW>, FW_THREADS, smem);
+      default: return go(fw1d_kernel<16, PK, PW>, FW_THREADS, smem);
     }
   };
   if (a.C != nullptr) return by_ept(std::integral_constant<int, 3>());

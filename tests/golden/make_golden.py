@@ -1258,10 +1258,78 @@ def gen_replay():
     out["bary_cases"] = np.load(os.path.join(HERE, "barycenter.npz"))["cases"]
     save("replay.npz", **out)
 
+
+# ---------------------------------------------------------------------------
+# Large 1-D problems (round 2): sizes beyond the resident
+# on-chip path (n or m > 4096) -- the paper's FW experiment (PAPER.md:589:
+# 5.000-sample measures, rho = 0.1) and n = 16384 (m = 12001: no exact ties of the uniform
+# cumulative masses; m = 12000 is kept as the structural-tie case).  Inputs come from the
+# reference's own generators (uotkit.synthetic, mirrored byte-for-byte by
+# paper_2201_00730_b200.synthetic) or oracle.large_ot_inputs, so the fixture
+# stores only outputs: potentials, per-iteration gamma / support hashes.
+
+
+def gen_large():
+    from uotkit import synthetic as USyn
+
+    out = {}
+    # solve_ot_1d with zero-weight atoms and ties, p = 2 and p = 1
+    for k, (n, m, p, seed) in enumerate(((5000, 4999, 2.0, 1), (16384, 16384, 1.0, 2),
+                                         (4097, 12000, 2.0, 3))):
+        x, y, wa, wb = O.large_ot_inputs(n, m, seed)
+        t0 = time.time()
+        plan, duals = U.solve_ot_1d(U.DiscreteMeasure(x, wa), U.DiscreteMeasure(y, wb),
+                                    U.PowerDistance(p))
+        h, c = _hash_pairs(plan)
+        out[f"ot{k}_spec"] = np.array([n, m, p, seed])
+        out[f"ot{k}_f"], out[f"ot{k}_g"] = duals.f, duals.g
+        out[f"ot{k}_hash"], out[f"ot{k}_nnz"] = np.array(h), np.array(c)
+        out[f"ot{k}_mass8"] = plan.mass[::8].copy()
+        print(f"  large ot {k}: {n}x{m} p={p} entries {c} in {time.time() - t0:.1f}s", flush=True)
+    # FW on the paper's 5000-sample mixtures (rho = 0.1) and at n = 16384
+    specs = [(5000, 5000, 11, 12, 0.1, "linesearch", 60), (5000, 5000, 11, 12, 0.1, "harmonic", 60),
+             (16384, 12001, 13, 14, 1.0, "linesearch", 25)]
+    for k, (n, m, sa, sb, rho, step, iters) in enumerate(specs):
+        a, _ = USyn.mixture_measure(n, sa)
+        b, _ = USyn.mixture_measure(m, sb)
+        prob = U.UotProblem(a, b, U.PowerDistance(2.0), U.KL(rho), U.KL(rho), eps=0.0)
+        t0 = time.time()
+        d, rec = ref_fw_rec(prob, iters, step)
+        lam = U.lambda_star(prob, d)
+        out[f"fw{k}_spec"] = np.array([n, m, sa, sb, rho, 1.0 if step == "linesearch" else 0.0,
+                                       iters])
+        out[f"fw{k}_f"], out[f"fw{k}_g"] = d.f + lam, d.g - lam
+        for kk, v in rec.items():
+            out[f"fw{k}_{kk}"] = v
+        print(f"  large fw {k}: {n}x{m} {step} x{iters} in {time.time() - t0:.1f}s", flush=True)
+    # pairwise FW on the 5000-sample mixtures
+    a, _ = USyn.mixture_measure(5000, 11)
+    b, _ = USyn.mixture_measure(5000, 12)
+    prob = U.UotProblem(a, b, U.PowerDistance(2.0), U.KL(0.1), U.KL(0.1), eps=0.0)
+    t0 = time.time()
+    d, rec = ref_pfw_rec(prob, 40)
+    lam = U.lambda_star(prob, d)
+    out["pfw_f"], out["pfw_g"] = d.f + lam, d.g - lam
+    for kk, v in rec.items():
+        out[f"pfw_{kk}"] = v
+    print(f"  large pfw: 5000x5000 x40 in {time.time() - t0:.1f}s", flush=True)
+    # uniform weights on 16384 x 12000 atoms: the cumulative masses of the two
+    # sides coincide exactly at every 4096-th / 3000-th atom (structural ties,
+    # SURVEY.md §0 finding 8); gamma_t, per-iteration plans (hash) recorded
+    a, _ = USyn.mixture_measure(16384, 13)
+    b, _ = USyn.mixture_measure(12000, 14)
+    prob = U.UotProblem(a, b, U.PowerDistance(2.0), U.KL(1.0), U.KL(1.0), eps=0.0)
+    d, rec = ref_fw_rec(prob, 6, "linesearch")
+    lam = U.lambda_star(prob, d)
+    out["tie_f"], out["tie_g"] = d.f + lam, d.g - lam
+    for kk, v in rec.items():
+        out[f"tie_{kk}"] = v
+    save("large.npz", **out)
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw", "replay"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw", "replay", "large"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()
