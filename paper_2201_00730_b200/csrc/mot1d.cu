@@ -32,6 +32,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/uot_b200.h"
 #include "blockops.cuh"
@@ -47,7 +48,10 @@ constexpr int MT = 512;           // threads of the per-list CTAs
 #define UOT_BT 512
 #endif
 constexpr int BT = UOT_BT;  // threads of the bucket CTAs
-constexpr int CAP = 3072;         // events per bucket (two shared-memory buffers)
+#ifndef UOT_BT2
+#define UOT_BT2 256
+#endif
+constexpr int BT2 = UOT_BT2;  // threads of the cost-increment bucket CTAs (mot_bucket)
 constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
 constexpr int ST = 1024;          // threads of the per-problem splitter CTA
 constexpr int SMAX = 192;         // buckets per problem
@@ -91,6 +95,7 @@ struct MotArgs {
   double* tmass;          // [B][K] tilted masses
   double* samp;           // [B][K][SS] regular samples (values)
   int* sampt;             // [B][K][SS] (indices)
+  int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
   // parity / trace mode (optional)
   const double* step_in;  // [B][max_iters] replayed gamma_t
   unsigned long long* supp_hash;  // [B][max_iters] plan-support hash
@@ -476,15 +481,16 @@ __device__ __forceinline__ void stage_out(const double* buf, double* row, int nq
 // list's SS regular samples (keys (A_q[t], q, t)), taken from registers by
 // the owning threads.
 template <int EPT>
-__device__ void tilt_tail(const MotArgs& A, int b, int q, int nq, const double (&ta)[EPT],
-                          double* buf, int* iscr, double* vscr, double* sbuf = nullptr) {
+__device__ __forceinline__ void tilt_tail(const MotArgs& A, int b, int q, int nq, const double (&ta)[EPT],
+                          double* buf, int* iscr, double* vscr, double* sbuf = nullptr,
+                          bool store_ta = true) {
   const int K = A.k, n = A.n;
   const long base = ((long)b * K + q) * n;
   const int i0 = threadIdx.x * EPT;
   const bool staged = StageRun<EPT>::ON && sbuf != nullptr;
   if (staged)
     stage_put<EPT>(sbuf, ta);
-  else
+  else if (store_ta)
     store_run<EPT>(A.ta + base, i0, nq, ta);
   double av[EPT];
   double loc = 0.0;
@@ -604,10 +610,14 @@ __global__ void __launch_bounds__(MT) mot_tilt(MotArgs A) {
 // splitters (the samples of rank floor(s K SS / S)) and every list's split
 // positions (binary searches in its breakpoints).
 
+__device__ int merge_runs(double* key0, int* code0, double* key1, int* code1, const int* rb, int K,
+                          int total);
+
 __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
   extern __shared__ __align__(16) double ssm[];
   __shared__ double splk[SMAX + 1];
-  __shared__ int splc[SMAX + 1];
+  __shared__ int splc[SMAX + 1], splr[SMAX + 1];
+  __shared__ int rb[KMAX + 1];
   __shared__ int bad_s;
   const int b = blockIdx.x;
   const int K = A.k, n = A.n, S = A.S, SS = A.SS, KSS = K * SS;
@@ -624,6 +634,7 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
       A.scal[b * 4 + 1] = mnm;  // common total (min)
       bad_s = bad && A.done != nullptr;
     }
+    if (lane <= K) rb[lane] = lane * SS;
   }
   int* sp = A.split + (long)b * (S + 1) * K;
   if (S == 1) {
@@ -633,64 +644,70 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
     }
     return;
   }
-  double* allv = ssm;                                  // [K SS]
-  int* allt = reinterpret_cast<int*>(allv + KSS);      // [K SS]
-  int* rank = allt + KSS;                              // [K SS]
+  // the K sorted sample lists, merged in (value, list, index) order: a
+  // sample's merged position is its global rank
+  double* key0 = ssm;
+  double* key1 = key0 + KSS;
+  int* code0 = reinterpret_cast<int*>(key1 + KSS);
+  int* code1 = code0 + KSS;
+  int* pos = code1 + KSS;  // merged position of sample slot q SS + j
   for (int idx = threadIdx.x; idx < KSS; idx += ST) {
-    allv[idx] = A.samp[(long)b * KSS + idx];
-    allt[idx] = A.sampt[(long)b * KSS + idx];
+    key0[idx] = A.samp[(long)b * KSS + idx];
+    code0[idx] = idx;
   }
   __syncthreads();
   if (bad_s) return;
-  // rank of sample (v, q, t): its index in its own list plus, for every
-  // other list r, #{samples u of r : u < v, or u == v and r < q}
+  const int which = merge_runs(key0, code0, key1, code1, rb, K, KSS);
+  const double* mk = which ? key1 : key0;
+  const int* mc = which ? code1 : code0;
+  for (int r = threadIdx.x; r < KSS; r += ST) pos[mc[r]] = r;
+  // splitters: the samples of rank floor(s K SS / S)
+  for (int s = 1 + threadIdx.x; s < S; s += ST) {
+    const int R = (int)(((long)s * KSS) / S);
+    const int slot = mc[R], q = slot / SS, j = slot - q * SS;
+    splk[s] = mk[R];
+    splc[s] = ev_code(q, A.sampt[(long)b * KSS + slot]);
+    splr[s] = R;
+    (void)j;
+  }
+  __syncthreads();
+  // split positions: list q's samples bracket the position (merged ranks
+  // below R: binary search in pos), then a short search in the breakpoints
   int top = 1;
   while (top * 2 <= SS) top *= 2;
-  for (int idx = threadIdx.x; idx < KSS; idx += ST) {
-    const int q = idx / SS;
-    const double v = allv[idx];
-    int R = idx - q * SS;
-    for (int r = 0; r < K; ++r) {
-      if (r == q) continue;
-      const double* ov = allv + r * SS;
-      const bool le = r < q;
-      int pos = 0;
-      for (int step = top; step > 0; step >>= 1) {
-        const int np = pos + step;
-        if (np <= SS) {
-          const double u = ov[np - 1];
-          if (le ? (u <= v) : (u < v)) pos = np;
-        }
-      }
-      R += pos;
-    }
-    rank[idx] = R;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < KSS; idx += ST) {
-    const int R = rank[idx];
-    for (int s = (int)(((long)R * S + KSS - 1) / KSS); s < S; ++s) {
-      if ((int)(((long)s * KSS) / S) != R) break;
-      if (s >= 1) {
-        splk[s] = allv[idx];
-        splc[s] = ev_code(idx / SS, allt[idx]);
-      }
-    }
-  }
-  __syncthreads();
   for (int pr = threadIdx.x; pr < (S + 1) * K; pr += ST) {
     const int s = pr / K, q = pr - s * K;
     const int ne = max(list_len(A, q) - 1, 0);
-    int pos;
+    int p;
     if (s == 0) {
-      pos = 0;
+      p = 0;
     } else if (s == S) {
-      pos = ne;
+      p = ne;
     } else {
-      pos = count_keys_below(A.A + ((long)b * K + q) * n, ne, q, splk[s], ev_list(splc[s]),
-                             ev_index(splc[s]));
+      const int R = splr[s];
+      const int* pq = pos + q * SS;
+      int c = 0;  // #{j : pos(q, j) < R}
+      for (int step = top; step > 0; step >>= 1)
+        if (c + step <= SS && pq[c + step - 1] < R) c += step;
+      const int* tq = A.sampt + (long)b * KSS + q * SS;
+      // events below sample c-1's index are below the splitter, events from
+      // sample c's index on are not (sample c is the splitter or after it)
+      const int lo = min(c > 0 ? tq[c - 1] : 0, ne);
+      const int hi = c < SS ? tq[c] : ne;
+      const double* Aq = A.A + ((long)b * K + q) * n;
+      const double v = splk[s];
+      const int qs = ev_list(splc[s]), ts = ev_index(splc[s]);
+      int l = lo, h = max(lo, min(hi, ne));
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (key_less(Aq[mid], q, mid, v, qs, ts))
+          l = mid + 1;
+        else
+          h = mid;
+      }
+      p = l;
     }
-    sp[(long)s * K + q] = pos;
+    sp[(long)s * K + q] = p;
   }
 }
 
@@ -780,11 +797,12 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
   }
   __syncthreads();
   const int total = cnt_s[K];
-  if (total > CAP) return -1;
+  const int cap = A.cap;
+  if (total > cap) return -1;
   double* key0 = buf;
-  double* key1 = buf + CAP;
-  int* code0 = reinterpret_cast<int*>(buf + 2 * CAP);
-  int* code1 = code0 + CAP;
+  double* key1 = buf + cap;
+  int* code0 = reinterpret_cast<int*>(buf + 2 * cap);
+  int* code1 = code0 + cap;
   for (int e = threadIdx.x; e < total; e += blockDim.x) {
     int q = 0, hi = K - 1;  // last run starting at or before e
     while (q < hi) {
@@ -805,50 +823,183 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
   return total;
 }
 
-__global__ void __launch_bounds__(BT) mot_bucket(MotArgs A) {
+// Stable pairwise merge rounds of the bucket's K sorted runs, moving each
+// event's key with a 16-bit code (its gather position: the run layout is the
+// lists' ranges concatenated in list order, so the position identifies list
+// and index).  Same merge path and tie rule as merge_runs.
+__device__ int merge_runs16(double* key0, uint16_t* code0, double* key1, uint16_t* code1,
+                            const int* rb, int K, int total) {
+  int cur = 0;
+  const int P = (total + blockDim.x - 1) / blockDim.x;
+  for (int w = 1; w < K; w <<= 1) {
+    const double* ks = cur ? key1 : key0;
+    const uint16_t* cs = cur ? code1 : code0;
+    double* kd = cur ? key0 : key1;
+    uint16_t* cd = cur ? code0 : code1;
+    int o = threadIdx.x * P;
+    const int oend = min(total, o + P);
+    int g = 0;
+    while (o < oend) {
+      int r1 = rb[min(2 * w, K)];
+      while (o >= r1) {
+        ++g;
+        r1 = rb[min((2 * g + 2) * w, K)];
+      }
+      const int l0 = rb[min(2 * g * w, K)], m0 = rb[min((2 * g + 1) * w, K)];
+      const int nL = m0 - l0, nR = r1 - m0;
+      const int d = o - l0;
+      int lo = max(0, d - nR), hi = min(d, nL);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ks[l0 + mid] <= ks[m0 + d - 1 - mid])
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      int i = lo, j = d - lo;
+      double lv = i < nL ? ks[l0 + i] : CUDART_INF;
+      double rv = j < nR ? ks[m0 + j] : CUDART_INF;
+      const int stop = min(oend, r1);
+      for (; o < stop; ++o) {
+        const bool takeL = lv <= rv;
+        kd[o] = takeL ? lv : rv;
+        cd[o] = cs[takeL ? l0 + i : m0 + j];
+        if (takeL) {
+          ++i;
+          lv = i < nL ? ks[l0 + i] : CUDART_INF;
+        } else {
+          ++j;
+          rv = j < nR ? ks[m0 + j] : CUDART_INF;
+        }
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// Shared memory of one mot_bucket CTA: two key buffers, the supports of the
+// ranges (one more per list), two code buffers and the position -> list table.
+__host__ __device__ __forceinline__ size_t bucket_smem_bytes(int cap, int k) {
+  return (size_t)cap * (3 * sizeof(double) + 2 * sizeof(uint16_t) + 1) + (size_t)k * sizeof(double) +
+         16;
+}
+
+// mot_bucket: the events of key range s of problem b, merged in shared
+// memory, and their cost increments.  Gather: the lists' ranges (keys, and
+// the supports x_q[lo_q .. hi_q]) concatenated in list order, every thread's
+// loads issued back to back (one latency per batch, not one per list).
+// After the merge every thread owns a contiguous run of sorted events: the
+// barycentre before each event is bstart + an exclusive scan of the
+// increments w_q (x_q[t+1] - x_q[t]), and dCc = inc (x_q[t+1] + x_q[t] - Bb -
+// Ba) (barycenter.py:223-229) lands at the event's gather position, so each
+// list's increments leave with coalesced stores.
+constexpr int GU = 8;  // gather batch (loads in flight per thread)
+
+__global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ int lo_s[KMAX + 1], cnt_s[KMAX + 1];
+  __shared__ double om_s[KMAX];
   __shared__ double scr[32];
   __shared__ double bstart_s;
   const int s = blockIdx.x, b = blockIdx.y;
   if (A.done != nullptr && A.done[b]) return;
-  const int K = A.k, n = A.n;
-  double* key;
-  int* code;
-  const int total = bucket_gather(A, b, s, bsm, key, code, lo_s, cnt_s);
-  if (total < 0) {
-    if (threadIdx.x == 0) A.status[b] = UOT_INVALID;  // bucket overflow
-    return;
-  }
-  // barycentre of the tuple before the range: idx_q = lo_q
-  if (threadIdx.x < 32) {
+  const int K = A.k, n = A.n, cap = A.cap;
+  const int* sp = A.split + (long)b * (A.S + 1) * K;
+  if (threadIdx.x < 32) {  // lane q: list q's range, offsets by a warp scan
     const int lane = threadIdx.x;
-    const double v = lane < K ? A.omega[lane] * A.x[((long)b * K + lane) * n + lo_s[lane]] : 0.0;
-    const double bs = warp_sum(v);
+    const int lo = lane < K ? sp[(long)s * K + lane] : 0;
+    const int len = lane < K ? sp[(long)(s + 1) * K + lane] - lo : 0;
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const double om = lane < K ? A.omega[lane] : 0.0;
+    // barycentre of the tuple before the range: idx_q = lo_q
+    const double bs = warp_sum(lane < K ? om * A.x[((long)b * K + lane) * n + lo] : 0.0);
+    if (lane < K) {
+      lo_s[lane] = lo;
+      cnt_s[lane] = incl - len;
+      om_s[lane] = om;
+    }
+    if (lane == K - 1) cnt_s[K] = incl;
     if (lane == 0) bstart_s = bs;
   }
   __syncthreads();
-  const double bstart = bstart_s;
-  // each thread handles a contiguous run of sorted events
-  const int per = (total + BT - 1) / BT;
+  const int total = cnt_s[K];
+  if (total > cap) {  // excluded by bucket_bound; kept as a guard
+    if (threadIdx.x == 0) A.status[b] = UOT_INVALID;
+    return;
+  }
+  if (total == 0) return;
+  double* key0 = bsm;
+  double* key1 = bsm + cap;
+  double* xs = bsm + 2 * cap;  // list q's supports at [cnt_q + q, cnt_{q+1} + q]
+  uint16_t* c0 = reinterpret_cast<uint16_t*>(xs + cap + K);
+  uint16_t* c1 = c0 + cap;
+  uint8_t* qt = reinterpret_cast<uint8_t*>(c1 + cap);
+  const long rowb = (long)b * K * n;
+  // slots [0, total): keys; [total, 2 total + K): supports
+  const int nslot = 2 * total + K;
+  for (int base = 0; base < nslot; base += BT2 * GU) {
+    double v[GU];
+    int dst[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int e = base + u * BT2 + threadIdx.x;
+      dst[u] = -1;
+      v[u] = 0.0;
+      if (e < total) {
+        int q = 0;
+#pragma unroll
+        for (int st = KMAX / 2; st > 0; st >>= 1)
+          if (q + st < K && cnt_s[q + st] <= e) q += st;
+        v[u] = __ldg(A.A + rowb + (long)q * n + lo_s[q] + (e - cnt_s[q]));
+        dst[u] = e;
+        qt[e] = (uint8_t)q;
+        c0[e] = (uint16_t)e;
+      } else if (e < nslot) {
+        const int xi = e - total;  // supports slot: list q owns [cnt_q + q, cnt_{q+1} + q]
+        int q = 0;
+#pragma unroll
+        for (int st = KMAX / 2; st > 0; st >>= 1)
+          if (q + st < K && cnt_s[q + st] + q + st <= xi) q += st;
+        v[u] = __ldg(A.x + rowb + (long)q * n + lo_s[q] + (xi - cnt_s[q] - q));
+        dst[u] = 2 * cap + xi;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u)
+      if (dst[u] >= 0) bsm[dst[u]] = v[u];
+  }
+  __syncthreads();
+  const int which = merge_runs16(key0, c0, key1, c1, cnt_s, K, total);
+  const uint16_t* code = which ? c1 : c0;
+  const int per = (total + BT2 - 1) / BT2;
   const int e0 = threadIdx.x * per, e1 = min(total, e0 + per);
   double loc = 0.0;
   for (int e = e0; e < e1; ++e) {
-    const int q = ev_list(code[e]), t = ev_index(code[e]);
-    const double* xq = A.x + ((long)b * K + q) * n;
-    loc += A.omega[q] * (xq[t + 1] - xq[t]);
+    const int g = code[e], q = qt[g];
+    loc += om_s[q] * (xs[g + q + 1] - xs[g + q]);
   }
   double tot;
-  double run = bscan1(loc, tot, scr);
+  double run = bscan1(loc, tot, scr) + bstart_s;
+  double* out = key0;  // keys are dead after the merge: dCc by gather position
   for (int e = e0; e < e1; ++e) {
-    const int q = ev_list(code[e]), t = ev_index(code[e]);
-    const double* xq = A.x + ((long)b * K + q) * n;
-    const double xo = xq[t], xn = xq[t + 1];
-    const double inc = A.omega[q] * (xn - xo);
-    const double bb = bstart + run;
-    const double ba = bb + inc;
-    A.dcc[((long)b * K + q) * n + t + 1] = inc * (xn + xo - bb - ba);
+    const int g = code[e], q = qt[g];
+    const double xo = xs[g + q], xn = xs[g + q + 1];
+    const double inc = om_s[q] * (xn - xo);
+    const double bb = run, ba = bb + inc;
+    out[g] = inc * (xn + xo - bb - ba);
     run += inc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < total; e += BT2) {
+    const int q = qt[e];
+    A.dcc[rowb + (long)q * n + lo_s[q] + (e - cnt_s[q]) + 1] = out[e];
   }
 }
 
@@ -864,8 +1015,9 @@ __device__ __forceinline__ unsigned long long mtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define MOT_STAMP(k) \
-  if (threadIdx.x == 0) g_mot_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
+#define MOT_STAMP(k)                                     \
+  if (threadIdx.x == 0 && A.t + 2 == A.max_iters) /* the last update with a tilt */ \
+  g_mot_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
 #else
 #define MOT_STAMP(k)
 #endif
@@ -1102,6 +1254,505 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
     }
     MOT_STAMP(6);
   }
+  cl.sync();  // slots stay valid until every CTA read them
+  MOT_STAMP(7);
+}
+
+// ---------------------------------------------------------------------------
+// mot_update2: the same update with TWO lists per CTA (clusters of K/2 CTAs),
+// so twice as many problems are co-resident as with one 16-CTA cluster per
+// problem (16-CTA clusters of 512-thread CTAs: at most 7 in flight).  List A
+// (2c) lives in registers exactly as in mot_update; list B (2c+1) keeps its
+// rows (dual atoms, potentials, input weights) in shared memory, staged by
+// cp.async in a swizzled run layout (thread t's 16-byte chunk c of a row at
+// t EPT + 2 (c ^ sw(t)): conflict-free per-thread vector reads, coalesced
+// fills).  Per-list reductions are formed per list as before; cluster sums
+// read list l's value in lane l, in the same order as cluster_sum.
+
+template <int EPT>
+struct Swz {
+  static constexpr int PAIRS = EPT / 2;
+  __device__ static __forceinline__ int chunk(int t, int c) {
+    if constexpr (PAIRS >= 8) return c ^ (t & 7);
+    else if constexpr (PAIRS == 4) return c ^ ((t >> 1) & 3);
+    else if constexpr (PAIRS == 2) return c ^ ((t >> 2) & 1);
+    else return c;
+  }
+  __device__ static __forceinline__ double2* at(double* row, int t, int c) {
+    return reinterpret_cast<double2*>(row + t * EPT + 2 * chunk(t, c));
+  }
+  __device__ static __forceinline__ const double2* at(const double* row, int t, int c) {
+    return reinterpret_cast<const double2*>(row + t * EPT + 2 * chunk(t, c));
+  }
+  // global row (16-byte aligned, nq valid entries) -> swizzled shared row, async
+  __device__ static __forceinline__ void fill(double* srow, const double* grow, int nq) {
+    for (int j = threadIdx.x; j < MT * PAIRS; j += MT) {
+      const int t = j / PAIRS, c = j - t * PAIRS;
+      const int rem = nq - 2 * j;
+      const int bytes = rem >= 2 ? 16 : rem == 1 ? 8 : 0;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(at(srow, t, c));
+      const double* src = bytes > 0 ? grow + 2 * j : grow;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                   "r"(bytes));
+    }
+  }
+  // swizzled shared row -> global row (coalesced)
+  __device__ static __forceinline__ void drain(const double* srow, double* grow, int nq) {
+    for (int j = threadIdx.x; j < MT * PAIRS && 2 * j < nq; j += MT) {
+      const int t = j / PAIRS, c = j - t * PAIRS;
+      const double2 v = *at(srow, t, c);
+      if (2 * j + 1 < nq)
+        *reinterpret_cast<double2*>(grow + 2 * j) = v;
+      else
+        grow[2 * j] = v.x;
+    }
+  }
+};
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Cluster all-reduce over the K lists of a two-lists-per-CTA cluster: CTA c
+// publishes (list 2c, list 2c+1); lane l reads list l; butterfly over the warp.
+template <int NV>
+__device__ __forceinline__ void cluster_sum2(double (&va)[NV], const double (&vb)[NV],
+                                             double* slots, int& parity, int K) {
+  static_assert(NV <= 8, "cluster_sum2: NV <= 8");
+  cg::cluster_group cl = cg::this_cluster();
+  double* mine = slots + parity * 16;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      mine[k] = va[k];
+      mine[8 + k] = vb[k];
+    }
+  }
+  cl.sync();
+  const int lane = threadIdx.x & 31;
+  const bool act = lane < K;
+  const double* other = cl.map_shared_rank(mine, act ? (lane >> 1) : 0);
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = act ? other[(lane & 1) * 8 + k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) va[k] = warp_sum(v[k]);
+  parity ^= 1;
+}
+
+template <int EPT>
+constexpr size_t upd2_smem() {
+  return 3 * (size_t)MT * EPT * sizeof(double);
+}
+
+// tilt_tail for a list whose row sits in shared memory (swizzled, holding
+// w exp(-f/rho - mx)): scaled in place to the tilted weights, then turned in
+// place into the breakpoints with tilt_tail's association (local prefix,
+// plus the block offset) and zero-weight fix-up; the row leaves coalesced.
+template <int EPT>
+__device__ __forceinline__ void tilt_tail_smem(const MotArgs& A, int b, int q, int nq, double* row,
+                                               double scale, double* buf, int* iscr,
+                                               double* vscr) {
+  using SW = Swz<EPT>;
+  constexpr int PAIRS = EPT / 2;
+  const int K = A.k, n = A.n, tid = threadIdx.x;
+  const int i0 = tid * EPT;
+  double loc = 0.0;
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    double2* p = SW::at(row, tid, cc);
+    double2 v = *p;
+    v.x *= scale;
+    v.y *= scale;
+    *p = v;
+    loc += v.x;
+    loc += v.y;
+  }
+  double v1[1] = {loc}, tot[1];
+  bops::block_scan_excl<MNW, 1>(v1, tot, buf);
+  const double off = v1[0];
+  int any0 = 0, lz = -1;
+  double lzv = 0.0;
+  loc = 0.0;
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    double2* p = SW::at(row, tid, cc);
+    const double2 t2 = *p;
+    double2 a2;
+    loc += t2.x;
+    a2.x = off + loc;
+    loc += t2.y;
+    a2.y = off + loc;
+    const int i = i0 + 2 * cc;
+    if (i < nq && t2.x == 0.0) any0 = 1;
+    if (i < nq && t2.x > 0.0) {
+      lz = i;
+      lzv = a2.x;
+    }
+    if (i + 1 < nq && t2.y == 0.0) any0 = 1;
+    if (i + 1 < nq && t2.y > 0.0) {
+      lz = i + 1;
+      lzv = a2.y;
+    }
+    // zero-weight atoms are marked by a negative value (breakpoints are >= 0)
+    // until the fix-up below gives them their predecessor's breakpoint
+    *p = make_double2(t2.x == 0.0 ? -a2.x - 1.0 : a2.x, t2.y == 0.0 ? -a2.y - 1.0 : a2.y);
+  }
+  if (__syncthreads_or(any0)) {
+    int pi = lz;
+    double pv = lzv;
+    excl_last_pos(pi, pv, iscr, vscr);
+#pragma unroll 1
+    for (int cc = 0; cc < PAIRS; ++cc) {
+      double2* p = SW::at(row, tid, cc);
+      double2 a2 = *p;
+      const int i = i0 + 2 * cc;
+      if (i < nq && a2.x < 0.0) a2.x = pi >= 0 ? pv : 0.0;
+      else if (i < nq) { pi = i; pv = a2.x; }
+      if (i + 1 < nq && a2.y < 0.0) a2.y = pi >= 0 ? pv : 0.0;
+      else if (i + 1 < nq) { pi = i + 1; pv = a2.y; }
+      *p = a2;
+    }
+  }
+  __syncthreads();
+  const long base = ((long)b * K + q) * n;
+  SW::drain(row, A.A + base, nq);
+  if (tid == 0) A.tmass[(long)b * K + q] = tot[0];
+  const int ne = nq - 1, SS = A.SS;
+  double* sv = A.samp + ((long)b * K + q) * SS;
+  int* st = A.sampt + ((long)b * K + q) * SS;
+  if (ne <= 0) {
+    for (int j = tid; j < SS; j += MT) {
+      sv[j] = CUDART_INF;
+      st[j] = 0;
+    }
+    return;
+  }
+  for (int j = tid; j < SS; j += MT) {  // samples t_j = floor((j+1) ne / (SS+1))
+    const int t = (int)(((long)(j + 1) * ne) / (SS + 1));
+    const int th = t / EPT, e = t - th * EPT;
+    const double2 a2 = *SW::at(row, th, e >> 1);
+    sv[j] = (e & 1) ? a2.y : a2.x;
+    st[j] = t;
+  }
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
+  MOT_STAMP(0);
+  using SW = Swz<EPT>;
+  constexpr int PAIRS = EPT / 2;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double rows[];  // list B: r (dcc first), f, w
+  constexpr int RBUF = 8 * MNW;  // the 6 + 2 gap reductions are the widest
+  __shared__ __align__(16) double red[2 * RBUF];
+  __shared__ double tab[32];
+  __shared__ double slots[32];
+  __shared__ int done_s;
+  __shared__ double cc0_s;
+  __shared__ int iscr[MNW];
+  __shared__ double vscr[MNW];
+  const int c = (int)cl.block_rank();
+  const int qa = 2 * c, qb = 2 * c + 1;
+  const int b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int na = list_len(A, qa), nb = list_len(A, qb);
+  const int tid = threadIdx.x, i0 = tid * EPT;
+  int parity = 0;
+  bops::Ping<RBUF> ping{red, 0};
+  bops::load_exp_table(tab);
+  if (tid == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
+  __syncthreads();
+  if (done_s) return;
+  const long basea = ((long)b * K + qa) * n, baseb = ((long)b * K + qb) * n;
+  double* rB = rows;
+  double* fB = rows + MT * EPT;
+  double* wB = rows + 2 * MT * EPT;
+  SW::fill(rB, A.dcc + baseb, nb);
+  SW::fill(fB, A.f + baseb, nb);
+  SW::fill(wB, A.a + baseb, nb);
+  double rv[EPT], fv[EPT], wv[EPT];
+  load_run<EPT>(A.dcc + basea, i0, na, rv);
+  load_run<EPT>(A.f + basea, i0, na, fv);
+  load_run<EPT>(A.a + basea, i0, na, wv);
+  if (tid < 32) {  // f_1[0] = Cc(first tuple) (barycenter.py:206-207); list 0 is list A of CTA 0
+    const int lane = tid;
+    double cc = 0.0;
+    if (c == 0) {
+      const double x0 = lane < K ? A.x[((long)b * K + lane) * n] : 0.0;
+      const double om = lane < K ? A.omega[lane] : 0.0;
+      const double bb = warp_sum(om * x0);
+      cc = warp_sum(om * ((x0 - bb) * (x0 - bb)));
+    }
+    if (lane == 0) cc0_s = cc;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  MOT_STAMP(1);
+  // dual atoms: prefix sums of the cost increments (dcc[0] is not an event)
+  if (tid == 0) rv[0] = 0.0;
+  double sc2[2] = {0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    sc2[0] += rv[e];
+    rv[e] = sc2[0];
+  }
+  if (tid == 0) SW::at(rB, 0, 0)->x = 0.0;
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 d = *SW::at(rB, tid, cc);
+    sc2[1] += d.x;
+    sc2[1] += d.y;
+  }
+  {
+    double tot2[2];
+    bops::block_scan_excl<MNW, 2>(sc2, tot2, ping.next());
+  }
+  const double offa = sc2[0] + cc0_s, offb = sc2[1];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) rv[e] += offa;
+  {
+    double lb = 0.0;  // list B: local inclusive prefix + offset, in place
+#pragma unroll 2
+    for (int cc = 0; cc < PAIRS; ++cc) {
+      double2* p = SW::at(rB, tid, cc);
+      const double2 d = *p;
+      lb += d.x;
+      const double x0 = lb + offb;
+      lb += d.y;
+      *p = make_double2(x0, lb + offb);
+    }
+  }
+  const double rqa = A.omega[qa] * A.rho, rqb = A.omega[qb] * A.rho;
+  const double irqa = 1.0 / rqa, irqb = 1.0 / rqb;
+  const double lama = A.lam[(long)b * K + qa], lamb = A.lam[(long)b * K + qb];
+  // gap sums (barycenter.py:376-381), plan cost by complementary slackness,
+  // KL terms, masses, second moment of d under the current tilt (its first
+  // moment is the gap term); shift bounds.  One block reduction per list
+  // keeps the accumulators of only one list live.
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  double mxs[2] = {-CUDART_INF, -CUDART_INF};
+  // The tilted weights are recomputed exactly as the tilt formed them,
+  // ta = wexp(w, -f/rho - mx) * exp(mx - lambda/rho), with the stored mx and
+  // lambda (bit-identical; no row round trip through HBM).
+  const double mxa = A.lse[((long)b * K + qa) * 2 + 0], mxb = A.lse[((long)b * K + qb) * 2 + 0];
+  const double tsa = exp(mxa - lama * irqa), tsb = exp(mxb - lamb * irqb);
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const double r = rv[e], f = fv[e], w = wv[e];
+    const double tv = bops::wexp(w, -f * irqa - mxa, tab) * tsa;
+    const double d = r - f;
+    acc[0] += tv * d;
+    acc[1] += tv * r;
+    if (tv > 0.0) acc[2] += tv * (-(f + lama) * irqa);
+    acc[3] += tv;
+    acc[4] += w;
+    acc[5] += tv * d * d;
+    if (w > 0.0) {
+      mxs[0] = bops::dmax(mxs[0], -f * irqa);
+      mxs[1] = bops::dmax(mxs[1], -r * irqa);
+    }
+  }
+  bops::block_red<MNW, 6, 2>(acc, mxs, ping.next());
+  const double cqa = acc[0] / acc[3];
+  double cs[4] = {acc[0], acc[1] + rqa * (acc[2] - acc[3] + acc[4]), cqa,
+                  fmax(acc[5] / acc[3] - cqa * cqa, 0.0) / rqa};
+  const double mass_a = acc[4];
+  const double mxa0 = mxs[0], mxa1 = mxs[1];
+  {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] = 0.0;
+    mxs[0] = mxs[1] = -CUDART_INF;
+#pragma unroll 2
+    for (int cc = 0; cc < PAIRS; ++cc) {
+      const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+      const double rr[2] = {r2.x, r2.y}, ff[2] = {f2.x, f2.y}, ww[2] = {w2.x, w2.y};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double t = bops::wexp(ww[h], -ff[h] * irqb - mxb, tab) * tsb;
+        const double d = rr[h] - ff[h];
+        acc[0] += t * d;
+        acc[1] += t * rr[h];
+        if (t > 0.0) acc[2] += t * (-(ff[h] + lamb) * irqb);
+        acc[3] += t;
+        acc[4] += ww[h];
+        acc[5] += t * d * d;
+        if (ww[h] > 0.0) {
+          mxs[0] = bops::dmax(mxs[0], -ff[h] * irqb);
+          mxs[1] = bops::dmax(mxs[1], -rr[h] * irqb);
+        }
+      }
+    }
+  }
+  bops::block_red<MNW, 6, 2>(acc, mxs, ping.next());
+  const double cqb = acc[0] / acc[3];
+  const double csb[4] = {acc[0], acc[1] + rqb * (acc[2] - acc[3] + acc[4]), cqb,
+                         fmax(acc[5] / acc[3] - cqb * cqb, 0.0) / rqb};
+  const double mass_b = acc[4];
+  const double mxb0 = mxs[0], mxb1 = mxs[1];
+  MOT_STAMP(2);
+  cluster_sum2<4>(cs, csb, slots, parity, K);
+  MOT_STAMP(3);
+  const double fw_gap = cs[0];
+  const double primal = cs[1];
+  const double dual = A.scal[b * 4 + 0];
+  const double pd_gap = primal - dual;
+  const int t = A.t;
+  if (c == 0 && tid == 0) {
+    A.h0[(long)b * A.max_iters + t] = dual;
+    A.fw_gap[(long)b * A.max_iters + t] = fw_gap;
+    A.pd_gap[(long)b * A.max_iters + t] = pd_gap;
+    A.iterations[b] = t + 1;
+    A.summary[b * 2 + 0] = primal;
+    A.summary[b * 2 + 1] = dual;
+  }
+  const bool stop = A.early_exit && pd_gap < A.gap_tol;  // barycenter.py:394-396
+  if (stop) {
+    if (c == 0 && tid == 0) A.done[b] = 2;
+    cl.sync();
+    return;
+  }
+  double gam;
+  if (A.step_in != nullptr) {
+    gam = __ldg(A.step_in + (long)b * A.max_iters + t);  // replayed gamma_t
+  } else if (A.step == UOT_STEP_HARMONIC) {
+    gam = 2.0 / (2.0 + t);
+  } else {  // safeguarded Newton on Phi(gamma) (see mot_update)
+    const double k0 = -cs[2];
+    const double vs = cs[3];
+    if (!(k0 < 0.0)) {
+      gam = 0.0;
+    } else {
+      double lo = 0.0, hi = 1.0;
+      gam = vs > 0.0 ? fmin(1.0, -k0 / vs) : 1.0;
+#ifdef UOT_NEWTON_STATS
+      if (tid == 0 && c == 0) atomicAdd(&g_mot_stats[1], 1ull);
+#endif
+      for (int it = 0; it < 24; ++it) {
+        const double sha = (1.0 - gam) * mxa0 + gam * mxa1;
+        const double shb = (1.0 - gam) * mxb0 + gam * mxb1;
+        double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const double d = rv[e] - fv[e];
+          const double ww = bops::wexp(wv[e], -(fv[e] + gam * d) * irqa - sha, tab);
+          const double xc = d - cqa;
+          mom[0] += ww;
+          mom[1] += ww * xc;
+          mom[2] += ww * xc * xc;
+        }
+#pragma unroll 2
+        for (int cc = 0; cc < PAIRS; ++cc) {
+          const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc),
+                        w2 = *SW::at(wB, tid, cc);
+          const double rr[2] = {r2.x, r2.y}, ff[2] = {f2.x, f2.y}, wq[2] = {w2.x, w2.y};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double d = rr[h] - ff[h];
+            const double ww = bops::wexp(wq[h], -(ff[h] + gam * d) * irqb - shb, tab);
+            const double xc = d - cqb;
+            mom[3] += ww;
+            mom[4] += ww * xc;
+            mom[5] += ww * xc * xc;
+          }
+        }
+        bops::block_sum<MNW, 6>(mom, ping.next());
+#ifdef UOT_NEWTON_STATS
+        if (tid == 0 && c == 0) atomicAdd(&g_mot_stats[0], 1ull);
+#endif
+        const double e1a = mom[1] / mom[0], e1b = mom[4] / mom[3];
+        double gv[2] = {e1a, (mom[2] / mom[0] - e1a * e1a) / rqa};
+        const double gvb[2] = {e1b, (mom[5] / mom[3] - e1b * e1b) / rqb};
+        cluster_sum2<2>(gv, gvb, slots, parity, K);
+        const double g1 = k0 - gv[0], g2 = gv[1];
+        if (g1 < 0.0)
+          lo = gam;
+        else
+          hi = gam;
+        if (gam >= 1.0 && g1 <= 0.0) {
+          gam = 1.0;
+          break;
+        }
+        double nxt = g2 > 0.0 ? gam - g1 / g2 : 0.5 * (lo + hi);
+        const bool newton = nxt > lo && nxt < hi;
+        if (!newton) nxt = 0.5 * (lo + hi);
+        const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(1.0, gam)) || g1 == 0.0 ||
+                          hi - lo <= 1e-15;
+        gam = nxt;
+        if (conv) break;
+      }
+    }
+  }
+  MOT_STAMP(4);
+  // barycenter.py:409-411, rounded as numpy rounds it (two products, a sum)
+  const double omg = 1.0 - gam;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) fv[e] = __dadd_rn(__dmul_rn(omg, fv[e]), __dmul_rn(gam, rv[e]));
+  store_run<EPT>(A.f + basea, i0, na, fv);
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc);
+    *SW::at(fB, tid, cc) = make_double2(__dadd_rn(__dmul_rn(omg, f2.x), __dmul_rn(gam, r2.x)),
+                                        __dadd_rn(__dmul_rn(omg, f2.y), __dmul_rn(gam, r2.y)));
+  }
+  // log-sum-exps of the new iterate (both lists; list_lse's arithmetic)
+  double m2[2] = {-CUDART_INF, -CUDART_INF};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e)
+    if (wv[e] > 0.0) m2[0] = bops::dmax(m2[0], -fv[e] * irqa);
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+    if (w2.x > 0.0) m2[1] = bops::dmax(m2[1], -f2.x * irqb);
+    if (w2.y > 0.0) m2[1] = bops::dmax(m2[1], -f2.y * irqb);
+  }
+  bops::block_max<MNW, 2>(m2, ping.next());
+  double tv[EPT];
+  double s2[2] = {0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    tv[e] = bops::wexp(wv[e], -fv[e] * irqa - m2[0], tab);
+    s2[0] += tv[e];
+  }
+#pragma unroll 2
+  for (int cc = 0; cc < PAIRS; ++cc) {  // list B's w exp(-f/rho - mx) replaces its dual atoms
+    const double2 f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+    const double ex = bops::wexp(w2.x, -f2.x * irqb - m2[1], tab);
+    const double ey = bops::wexp(w2.y, -f2.y * irqb - m2[1], tab);
+    s2[1] += ex;
+    s2[1] += ey;
+    *SW::at(rB, tid, cc) = make_double2(ex, ey);
+  }
+  bops::block_sum<MNW, 2>(s2, ping.next());
+  const double qka = m2[0] + log(s2[0]), qkb = m2[1] + log(s2[1]);
+  if (tid == 0) {
+    A.lse[((long)b * K + qa) * 2 + 0] = m2[0];
+    A.lse[((long)b * K + qa) * 2 + 1] = qka;
+    A.lse[((long)b * K + qb) * 2 + 0] = m2[1];
+    A.lse[((long)b * K + qb) * 2 + 1] = qkb;
+  }
+  Swz<EPT>::drain(fB, A.f + baseb, nb);
+  MOT_STAMP(5);
+  if (t + 1 < A.max_iters) {
+    // the next iteration's tilt, fused: lambda from the cluster's
+    // log-sum-exps (barycenter.py:316-317), H_0 (:320-327), breakpoints.
+    double ex[3] = {rqa * qka, rqa * mass_a, rqa};
+    const double exb[3] = {rqb * qkb, rqb * mass_b, rqb};
+    cluster_sum2<3>(ex, exb, slots, parity, K);
+    const double lam1a = rqa * qka - (rqa / ex[2]) * ex[0];
+    const double lam1b = rqb * qkb - (rqb / ex[2]) * ex[0];
+    if (tid == 0) {
+      A.lam[(long)b * K + qa] = lam1a;
+      A.lam[(long)b * K + qb] = lam1b;
+      if (c == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
+    }
+    const double sca = exp(m2[0] - lam1a * irqa), scb = exp(m2[1] - lam1b * irqb);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) tv[e] *= sca;
+    tilt_tail<EPT>(A, b, qa, na, tv, ping.next(), iscr, vscr, nullptr, false);
+    tilt_tail_smem<EPT>(A, b, qb, nb, rB, scb, ping.next(), iscr, vscr);
+  }
+  MOT_STAMP(6);
   cl.sync();  // slots stay valid until every CTA read them
   MOT_STAMP(7);
 }
@@ -1347,8 +1998,8 @@ __global__ void __launch_bounds__(CT) mot_certify_kernel(int K, int n, const int
 // Host driver.
 
 struct MotPlan {
-  int S, SS, ept;
-  size_t tilt_smem, split_smem, bucket_smem;
+  int S, SS, ept, cap;
+  size_t tilt_smem, split_smem, bucket_smem, plan_smem;
 };
 
 int ept_for(int n) {
@@ -1362,6 +2013,20 @@ int ept_for(int n) {
   return -1;
 }
 
+// Largest possible bucket under regular sampling: list q has
+// SS samples at t_j = floor((j+1) ne / (SS+1)), consecutive samples (and the
+// list ends) at most gmax = ceil(ne / (SS+1)) + 1 events apart; bucket s holds
+// the samples of global rank [R_s, R_{s+1}), at most ceil(K SS / S) of them,
+// and list q's events in the bucket lie strictly between the two list-q
+// samples just outside it: <= (c_q + 1) gmax - 1 events for c_q samples
+// inside.  Summed over the lists: (ceil(K SS / S) + K) gmax - K.
+long bucket_bound(int k, int ne, int S, int SS) {
+  if (S == 1) return (long)k * ne;
+  const long per = ((long)k * SS + S - 1) / S;
+  const long gmax = ((long)ne + SS) / (SS + 1) + 1;
+  return std::max(1L, (per + k) * gmax - k);
+}
+
 MotPlan plan_for(int k, int n) {
   MotPlan p;
   const long events = (long)k * (n - 1);
@@ -1369,10 +2034,22 @@ MotPlan plan_for(int k, int n) {
   p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
   while ((long)k * p.SS > 4096) p.SS = std::max(1, p.SS / 2);
   p.ept = ept_for(n);
+  p.cap = (int)std::min(bucket_bound(k, std::max(n - 1, 0), p.S, p.SS), 60000L);
   p.tilt_smem = sizeof(double) * (size_t)n;
-  p.split_smem = (sizeof(double) + 2 * sizeof(int)) * (size_t)k * p.SS;
-  p.bucket_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)CAP;
+  p.split_smem = (2 * sizeof(double) + 3 * sizeof(int)) * (size_t)k * p.SS;
+  p.bucket_smem = bucket_smem_bytes(p.cap, k);
+  p.plan_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)p.cap;
   return p;
+}
+
+// Two lists per CTA (mot_update2) when K is even, the cluster stays portable
+// and rows are 16-byte aligned; UOT_MOT_UPDATE1=1 forces the one-list kernel.
+bool use_update2(const MotArgs& a) {
+  static const bool off = [] {
+    const char* e = getenv("UOT_MOT_UPDATE1");
+    return e != nullptr && e[0] == '1';
+  }();
+  return !off && a.mode == 0 && a.k % 2 == 0 && a.k / 2 <= 8 && a.n % 2 == 0;
 }
 
 template <class Kern>
@@ -1395,6 +2072,14 @@ int launch_cluster(Kern kern, int k, int batch, size_t smem, cudaStream_t st, co
   return UOT_OK;
 }
 
+int launch_bucket(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
+  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p.bucket_smem));
+  mot_bucket<<<dim3(p.S, a.batch), BT2, p.bucket_smem, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
 // tilt -> splitters -> buckets (the K-marginal sweep); then the update.
 template <int EPT>
 int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
@@ -1406,16 +2091,19 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
                                     (int)p.split_smem));
   mot_split<<<a.batch, ST, p.split_smem, st>>>(a);
   UOT_CHECK_LAUNCH();
-  UOT_CUDA_TRY(cudaFuncSetAttribute(mot_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)p.bucket_smem));
-  mot_bucket<<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
-  UOT_CHECK_LAUNCH();
+  UOT_TRY(launch_bucket(a, p, st));
   if (a.supp_hash != nullptr) {  // trace mode: this iteration's plan support
     UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<false, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)p.bucket_smem));
-    mot_plan<false, true><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+                                      (int)p.plan_smem));
+    mot_plan<false, true><<<dim3(p.S, a.batch), BT, p.plan_smem, st>>>(a);
     UOT_CHECK_LAUNCH();
+  }
+  if constexpr (EPT == 8 || EPT == 16) {
+    if (use_update2(a)) {
+      UOT_TRY(launch_cluster(mot_update2<EPT>, a.k / 2, a.batch, upd2_smem<EPT>(), st, a));
+      return UOT_OK;
+    }
   }
   UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch,
                          StageRun<EPT>::ON ? 2 * StageRun<EPT>::BYTES : 0, st, a));
@@ -1424,12 +2112,12 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
 
 int run_plan(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
   UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)p.bucket_smem));
+                                    (int)p.plan_smem));
   UOT_CUDA_TRY(cudaFuncSetAttribute(mot_plan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)p.bucket_smem));
-  mot_plan<false><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+                                    (int)p.plan_smem));
+  mot_plan<false><<<dim3(p.S, a.batch), BT, p.plan_smem, st>>>(a);
   UOT_CHECK_LAUNCH();
-  mot_plan<true><<<dim3(p.S, a.batch), BT, p.bucket_smem, st>>>(a);
+  mot_plan<true><<<dim3(p.S, a.batch), BT, p.plan_smem, st>>>(a);
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }
@@ -1520,6 +2208,7 @@ MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const dou
   a.rho = rho;
   a.S = p.S;
   a.SS = p.SS;
+  a.cap = p.cap;
   a.ta = (double*)(ws + L.off[0]);
   a.A = (double*)(ws + L.off[1]);
   a.dcc = (double*)(ws + L.off[2]);
@@ -1566,6 +2255,11 @@ int check_sizes(int batch, int k, int n) {
   }
   if (ept_for(n) < 0) {
     set_error("lists longer than %d atoms are not supported", 32 * MT);
+    return UOT_INVALID;
+  }
+  const MotPlan p = plan_for(k, n);
+  if (p.plan_smem > 227 * 1024 || p.bucket_smem > 227 * 1024) {
+    set_error("bucket capacity %d exceeds shared memory", p.cap);
     return UOT_INVALID;
   }
   return UOT_OK;

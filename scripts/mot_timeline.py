@@ -24,7 +24,10 @@ t = t[t[:, 0] > 0]
 d = np.diff(t, axis=1) / 1e3
 names = ["load dcc/f/ta/a", "scan + gap sums", "cluster sum + scalars", "line search",
          "update + store", "log-sum-exp", "tilt + samples", "cluster sync"]
-for k in range(7):
+if os.environ.get("UOT_MOT_UPDATE1") != "1":  # mot_update2 phases
+    names = ["load rows", "scan + gap sums", "cluster sum", "line search",
+             "update + LSE + drain", "tilt x2 + samples", "cluster sync"]
+for k in range(len(names)):
     print(f"{names[k]:24s} mean {d[:, k].mean():7.2f} us  p90 {np.percentile(d[:, k], 90):7.2f}")
 life = (t[:, 7] - t[:, 0]) / 1e3
 print(f"CTA lifetime mean {life.mean():.2f} us; span {(t[:, 7].max() - t[:, 0].min()) / 1e3:.1f} us")
