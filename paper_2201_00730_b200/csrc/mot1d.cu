@@ -610,8 +610,8 @@ __global__ void __launch_bounds__(MT) mot_tilt(MotArgs A) {
 // splitters (the samples of rank floor(s K SS / S)) and every list's split
 // positions (binary searches in its breakpoints).
 
-__device__ int merge_runs(double* key0, int* code0, double* key1, int* code1, const int* rb, int K,
-                          int total);
+__device__ int merge_runs16(const double* key, uint16_t* code0, uint16_t* code1, const int* rb,
+                            int K, int total);
 
 __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
   extern __shared__ __align__(16) double ssm[];
@@ -647,28 +647,24 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
   // the K sorted sample lists, merged in (value, list, index) order: a
   // sample's merged position is its global rank
   double* key0 = ssm;
-  double* key1 = key0 + KSS;
-  int* code0 = reinterpret_cast<int*>(key1 + KSS);
-  int* code1 = code0 + KSS;
-  int* pos = code1 + KSS;  // merged position of sample slot q SS + j
+  uint16_t* code0 = reinterpret_cast<uint16_t*>(key0 + KSS);
+  uint16_t* code1 = code0 + KSS;
+  uint16_t* pos = code1 + KSS;  // merged position of sample slot q SS + j
   for (int idx = threadIdx.x; idx < KSS; idx += ST) {
     key0[idx] = A.samp[(long)b * KSS + idx];
-    code0[idx] = idx;
+    code0[idx] = (uint16_t)idx;
   }
   __syncthreads();
   if (bad_s) return;
-  const int which = merge_runs(key0, code0, key1, code1, rb, K, KSS);
-  const double* mk = which ? key1 : key0;
-  const int* mc = which ? code1 : code0;
-  for (int r = threadIdx.x; r < KSS; r += ST) pos[mc[r]] = r;
+  const uint16_t* mc = merge_runs16(key0, code0, code1, rb, K, KSS) ? code1 : code0;
+  for (int r = threadIdx.x; r < KSS; r += ST) pos[mc[r]] = (uint16_t)r;
   // splitters: the samples of rank floor(s K SS / S)
   for (int s = 1 + threadIdx.x; s < S; s += ST) {
     const int R = (int)(((long)s * KSS) / S);
-    const int slot = mc[R], q = slot / SS, j = slot - q * SS;
-    splk[s] = mk[R];
+    const int slot = mc[R], q = slot / SS;
+    splk[s] = key0[slot];
     splc[s] = ev_code(q, A.sampt[(long)b * KSS + slot]);
     splr[s] = R;
-    (void)j;
   }
   __syncthreads();
   // split positions: list q's samples bracket the position (merged ranks
@@ -685,7 +681,7 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
       p = ne;
     } else {
       const int R = splr[s];
-      const int* pq = pos + q * SS;
+      const uint16_t* pq = pos + q * SS;
       int c = 0;  // #{j : pos(q, j) < R}
       for (int step = top; step > 0; step >>= 1)
         if (c + step <= SS && pq[c + step - 1] < R) c += step;
@@ -713,6 +709,26 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
 
 // ---------------------------------------------------------------------------
 // mot_bucket: events of one key range, sorted; cost increments.
+
+#ifdef UOT_MOT_TIMING
+// timing build only (scripts/mot_timeline.py): %globaltimer stamps of one
+// thread per CTA at the phase boundaries of mot_update
+__device__ unsigned long long g_mot_stamps[1 << 14][8];
+__device__ __forceinline__ unsigned long long mtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MOT_STAMP(k)                                     \
+  if (threadIdx.x == 0 && A.t + 2 == A.max_iters) /* the last update with a tilt */ \
+  g_mot_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
+__device__ unsigned long long g_bkt_stamps[1 << 14][6];
+#define BKT_STAMP(k) \
+  if (threadIdx.x == 0) g_bkt_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
+#else
+#define MOT_STAMP(k)
+#define BKT_STAMP(k)
+#endif
 
 // Stable merge of the bucket's K sorted runs (run q = the events of list q,
 // at [rb[q], rb[q+1])) in ceil(log2 K) pairwise rounds.  Groups of runs are
@@ -827,14 +843,13 @@ __device__ __forceinline__ int bucket_gather(const MotArgs& A, int b, int s, dou
 // event's key with a 16-bit code (its gather position: the run layout is the
 // lists' ranges concatenated in list order, so the position identifies list
 // and index).  Same merge path and tie rule as merge_runs.
-__device__ int merge_runs16(double* key0, uint16_t* code0, double* key1, uint16_t* code1,
-                            const int* rb, int K, int total) {
+__device__ int merge_runs16(const double* key, uint16_t* code0, uint16_t* code1, const int* rb,
+                            int K, int total) {
+  // codes are gather positions; keys are read through them (key[code])
   int cur = 0;
   const int P = (total + blockDim.x - 1) / blockDim.x;
   for (int w = 1; w < K; w <<= 1) {
-    const double* ks = cur ? key1 : key0;
     const uint16_t* cs = cur ? code1 : code0;
-    double* kd = cur ? key0 : key1;
     uint16_t* cd = cur ? code0 : code1;
     int o = threadIdx.x * P;
     const int oend = min(total, o + P);
@@ -851,26 +866,29 @@ __device__ int merge_runs16(double* key0, uint16_t* code0, double* key1, uint16_
       int lo = max(0, d - nR), hi = min(d, nL);
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (ks[l0 + mid] <= ks[m0 + d - 1 - mid])
+        if (key[cs[l0 + mid]] <= key[cs[m0 + d - 1 - mid]])
           lo = mid + 1;
         else
           hi = mid;
       }
-      int i = lo, j = d - lo;
-      double lv = i < nL ? ks[l0 + i] : CUDART_INF;
-      double rv = j < nR ? ks[m0 + j] : CUDART_INF;
+      int il = l0 + lo, ir = m0 + (d - lo);
+      uint16_t lc = cs[min(il, total - 1)], rc = cs[min(ir, total - 1)];
+      double lv = il < m0 ? key[lc] : CUDART_INF;
+      double rv = ir < r1 ? key[rc] : CUDART_INF;
       const int stop = min(oend, r1);
       for (; o < stop; ++o) {
         const bool takeL = lv <= rv;
-        kd[o] = takeL ? lv : rv;
-        cd[o] = cs[takeL ? l0 + i : m0 + j];
-        if (takeL) {
-          ++i;
-          lv = i < nL ? ks[l0 + i] : CUDART_INF;
-        } else {
-          ++j;
-          rv = j < nR ? ks[m0 + j] : CUDART_INF;
-        }
+        cd[o] = takeL ? lc : rc;
+        il += takeL;
+        ir += !takeL;
+        const int ni = takeL ? il : ir;
+        const bool in = takeL ? (il < m0) : (ir < r1);
+        const uint16_t nc = cs[min(ni, total - 1)];
+        const double nv = in ? key[nc] : CUDART_INF;
+        lv = takeL ? nv : lv;
+        lc = takeL ? nc : lc;
+        rv = takeL ? rv : nv;
+        rc = takeL ? rc : nc;
       }
     }
     __syncthreads();
@@ -879,23 +897,125 @@ __device__ int merge_runs16(double* key0, uint16_t* code0, double* key1, uint16_
   return cur;
 }
 
+// Bucket sort of the gathered events by value (one bin per two events on
+// average, bins by linear interpolation between the smallest and largest key
+// -- monotone, so bin order is key order), then an insertion sort of every
+// bin by (value, gather position); the gather layout is (list, index) order,
+// so the result is exactly the (value, list, index) merge of merge_runs16.
+// Counting and scattering use shared-memory atomics (the order inside a bin
+// before its sort is irrelevant: the key order is total).  Returns 1 with the
+// result in key1 / code1, or 0 when a bin would hold more than BINMAX events
+// (heavily tied or clustered keys): the caller then merges instead.
+constexpr int BINMAX = 64;
+
+__device__ int bin_sort(const double* key0, uint16_t* code1, int* binc, const int* rb, int K,
+                        int total) {
+  __shared__ double kmin_s, kmax_s;
+  __shared__ int over_s;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double mn = CUDART_INF, mx = -CUDART_INF;
+    if (tid < K && rb[tid + 1] > rb[tid]) {
+      mn = key0[rb[tid]];
+      mx = key0[rb[tid + 1] - 1];
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if (tid == 0) {
+      kmin_s = mn;
+      kmax_s = mx;
+      over_s = 0;
+    }
+  }
+  const int NB = max(1, total >> 1);
+  for (int i = tid; i < NB; i += blockDim.x) binc[i] = 0;
+  __syncthreads();
+  const double kmin = kmin_s, span = kmax_s - kmin_s;
+  if (!(span > 0.0)) return 0;
+  const double scale = (double)NB / span;
+  for (int e = tid; e < total; e += blockDim.x) {
+    const int bi = min(NB - 1, (int)((key0[e] - kmin) * scale));
+    atomicAdd(&binc[bi], 1);
+  }
+  __syncthreads();
+  // exclusive scan of the bin counts (contiguous chunk per thread) + overflow check
+  const int per = (NB + blockDim.x - 1) / blockDim.x;
+  const int b0 = tid * per, b1 = min(NB, b0 + per);
+  int loc = 0, big = 0;
+  for (int i = b0; i < b1; ++i) {
+    loc += binc[i];
+    big = max(big, binc[i]);
+  }
+  if (big > BINMAX) over_s = 1;
+  __shared__ int wsum[32];
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (over_s) return 0;
+  int off = incl - loc;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  for (int i = b0; i < b1; ++i) {
+    const int c = binc[i];
+    binc[i] = off;
+    off += c;
+  }
+  __syncthreads();
+  for (int e = tid; e < total; e += blockDim.x) {
+    const int bi = min(NB - 1, (int)((key0[e] - kmin) * scale));
+    code1[atomicAdd(&binc[bi], 1)] = (uint16_t)e;
+  }
+  __syncthreads();
+  // binc[i] is now the end of bin i; insertion sort by (key, gather position)
+  for (int i = tid; i < NB; i += blockDim.x) {
+    const int st = i == 0 ? 0 : binc[i - 1], en = binc[i];
+    for (int a = st + 1; a < en; ++a) {
+      const uint16_t c = code1[a];
+      const double k = key0[c];
+      int j = a - 1;
+      while (j >= st) {
+        const uint16_t cj = code1[j];
+        const double kj = key0[cj];
+        if (!(kj > k || (kj == k && cj > c))) break;
+        code1[j + 1] = cj;
+        --j;
+      }
+      code1[j + 1] = c;
+    }
+  }
+  __syncthreads();
+  return 1;
+}
+
 // Shared memory of one mot_bucket CTA: two key buffers, the supports of the
 // ranges (one more per list), two code buffers and the position -> list table.
 __host__ __device__ __forceinline__ size_t bucket_smem_bytes(int cap, int k) {
-  return (size_t)cap * (3 * sizeof(double) + 2 * sizeof(uint16_t) + 1) + (size_t)k * sizeof(double) +
-         16;
+  return (size_t)cap * (2 * sizeof(double) + 2 * sizeof(uint16_t) + 1) + (size_t)k * sizeof(double) +
+         16 + (size_t)(cap / 2 + 2) * sizeof(int);
 }
 
 // mot_bucket: the events of key range s of problem b, merged in shared
 // memory, and their cost increments.  Gather: the lists' ranges (keys, and
-// the supports x_q[lo_q .. hi_q]) concatenated in list order, every thread's
-// loads issued back to back (one latency per batch, not one per list).
+// the supports x_q[lo_q .. hi_q]) concatenated in list order, one warp per
+// list (coalesced).
 // After the merge every thread owns a contiguous run of sorted events: the
 // barycentre before each event is bstart + an exclusive scan of the
 // increments w_q (x_q[t+1] - x_q[t]), and dCc = inc (x_q[t+1] + x_q[t] - Bb -
 // Ba) (barycenter.py:223-229) lands at the event's gather position, so each
 // list's increments leave with coalesced stores.
-constexpr int GU = 8;  // gather batch (loads in flight per thread)
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
 
 __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   extern __shared__ __align__(16) double bsm[];
@@ -903,32 +1023,33 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   __shared__ double om_s[KMAX];
   __shared__ double scr[32];
   __shared__ double bstart_s;
+  __shared__ int done_s;
+  BKT_STAMP(0);
   const int s = blockIdx.x, b = blockIdx.y;
-  if (A.done != nullptr && A.done[b]) return;
   const int K = A.k, n = A.n, cap = A.cap;
   const int* sp = A.split + (long)b * (A.S + 1) * K;
-  if (threadIdx.x < 32) {  // lane q: list q's range, offsets by a warp scan
+  if (threadIdx.x < 32) {  // lane q: list q's range, offsets by a warp scan (one latency)
     const int lane = threadIdx.x;
+    const int dn = (lane == 0 && A.done != nullptr) ? A.done[b] : 0;
     const int lo = lane < K ? sp[(long)s * K + lane] : 0;
     const int len = lane < K ? sp[(long)(s + 1) * K + lane] - lo : 0;
+    const double om = lane < K ? A.omega[lane] : 0.0;
     int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    const double om = lane < K ? A.omega[lane] : 0.0;
-    // barycentre of the tuple before the range: idx_q = lo_q
-    const double bs = warp_sum(lane < K ? om * A.x[((long)b * K + lane) * n + lo] : 0.0);
     if (lane < K) {
       lo_s[lane] = lo;
       cnt_s[lane] = incl - len;
       om_s[lane] = om;
     }
     if (lane == K - 1) cnt_s[K] = incl;
-    if (lane == 0) bstart_s = bs;
+    if (lane == 0) done_s = dn;
   }
   __syncthreads();
+  if (done_s) return;
   const int total = cnt_s[K];
   if (total > cap) {  // excluded by bucket_bound; kept as a guard
     if (threadIdx.x == 0) A.status[b] = UOT_INVALID;
@@ -936,48 +1057,43 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   }
   if (total == 0) return;
   double* key0 = bsm;
-  double* key1 = bsm + cap;
-  double* xs = bsm + 2 * cap;  // list q's supports at [cnt_q + q, cnt_{q+1} + q]
+  double* xs = bsm + cap;  // list q's supports at [cnt_q + q, cnt_{q+1} + q]
   uint16_t* c0 = reinterpret_cast<uint16_t*>(xs + cap + K);
   uint16_t* c1 = c0 + cap;
   uint8_t* qt = reinterpret_cast<uint8_t*>(c1 + cap);
   const long rowb = (long)b * K * n;
-  // slots [0, total): keys; [total, 2 total + K): supports
-  const int nslot = 2 * total + K;
-  for (int base = 0; base < nslot; base += BT2 * GU) {
-    double v[GU];
-    int dst[GU];
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int e = base + u * BT2 + threadIdx.x;
-      dst[u] = -1;
-      v[u] = 0.0;
-      if (e < total) {
-        int q = 0;
-#pragma unroll
-        for (int st = KMAX / 2; st > 0; st >>= 1)
-          if (q + st < K && cnt_s[q + st] <= e) q += st;
-        v[u] = __ldg(A.A + rowb + (long)q * n + lo_s[q] + (e - cnt_s[q]));
-        dst[u] = e;
-        qt[e] = (uint8_t)q;
-        c0[e] = (uint16_t)e;
-      } else if (e < nslot) {
-        const int xi = e - total;  // supports slot: list q owns [cnt_q + q, cnt_{q+1} + q]
-        int q = 0;
-#pragma unroll
-        for (int st = KMAX / 2; st > 0; st >>= 1)
-          if (q + st < K && cnt_s[q + st] + q + st <= xi) q += st;
-        v[u] = __ldg(A.x + rowb + (long)q * n + lo_s[q] + (xi - cnt_s[q] - q));
-        dst[u] = 2 * cap + xi;
+  {  // warp w gathers lists w, w + NW, ...: keys and supports by cp.async (all
+     // loads in flight at once), codes and list tags
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = BT2 / 32;
+    for (int q = warp; q < K; q += NW) {
+      const int c = cnt_s[q], len = cnt_s[q + 1] - c;
+      const double* Aq = A.A + rowb + (long)q * n + lo_s[q];
+      const double* xq = A.x + rowb + (long)q * n + lo_s[q];
+      double* xd = xs + c + q;
+      for (int j = lane; j < len; j += 32) {
+        cp_async8(key0 + c + j, Aq + j);
+        cp_async8(xd + j, xq + j);
+        c0[c + j] = (uint16_t)(c + j);
+        qt[c + j] = (uint8_t)q;
       }
+      if (lane == 0) cp_async8(xd + len, xq + len);
     }
-#pragma unroll
-    for (int u = 0; u < GU; ++u)
-      if (dst[u] >= 0) bsm[dst[u]] = v[u];
+    cp_async_wait_all();
   }
   __syncthreads();
-  const int which = merge_runs16(key0, c0, key1, c1, cnt_s, K, total);
-  const uint16_t* code = which ? c1 : c0;
+  if (threadIdx.x < 32) {  // barycentre of the tuple before the range: idx_q = lo_q
+    const int lane = threadIdx.x;
+    const double bs = warp_sum(lane < K ? om_s[lane] * xs[cnt_s[lane] + lane] : 0.0);
+    if (lane == 0) bstart_s = bs;
+  }
+  BKT_STAMP(1);
+  int* binc = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(qt + cap) + 15) & ~static_cast<uintptr_t>(15));
+  const uint16_t* code = c1;
+  if (!bin_sort(key0, c1, binc, cnt_s, K, total))
+    code = merge_runs16(key0, c0, c1, cnt_s, K, total) ? c1 : c0;
+  BKT_STAMP(2);
   const int per = (total + BT2 - 1) / BT2;
   const int e0 = threadIdx.x * per, e1 = min(total, e0 + per);
   double loc = 0.0;
@@ -997,30 +1113,18 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
     run += inc;
   }
   __syncthreads();
+  BKT_STAMP(3);
   for (int e = threadIdx.x; e < total; e += BT2) {
     const int q = qt[e];
     A.dcc[rowb + (long)q * n + lo_s[q] + (e - cnt_s[q]) + 1] = out[e];
   }
+  BKT_STAMP(4);
 }
 
 // ---------------------------------------------------------------------------
 // mot_update: dual atoms, gaps, line search, update (cluster of K CTAs).
 
-#ifdef UOT_MOT_TIMING
-// timing build only (scripts/mot_timeline.py): %globaltimer stamps of one
-// thread per CTA at the phase boundaries of mot_update
-__device__ unsigned long long g_mot_stamps[1 << 14][8];
-__device__ __forceinline__ unsigned long long mtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define MOT_STAMP(k)                                     \
-  if (threadIdx.x == 0 && A.t + 2 == A.max_iters) /* the last update with a tilt */ \
-  g_mot_stamps[blockIdx.y * gridDim.x + blockIdx.x][k] = mtimer()
-#else
-#define MOT_STAMP(k)
-#endif
+
 
 template <int EPT>
 __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
@@ -1309,9 +1413,6 @@ struct Swz {
   }
 };
 
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
 
 // Cluster all-reduce over the K lists of a two-lists-per-CTA cluster: CTA c
 // publishes (list 2c, list 2c+1); lane l reads list l; butterfly over the warp.
@@ -2031,12 +2132,13 @@ MotPlan plan_for(int k, int n) {
   MotPlan p;
   const long events = (long)k * (n - 1);
   p.S = (int)std::min((long)SMAX, std::max(1L, (events + 1535) / 1536));
-  p.SS = (p.S > 1) ? std::min(4 * p.S, std::max(1, n - 1)) : 1;
-  while ((long)k * p.SS > 4096) p.SS = std::max(1, p.SS / 2);
+  // samples per list: enough that the bucket bound stays ~1.25x the average
+  // (K SS <= 8192 keeps mot_split's sample merge in shared memory)
+  p.SS = (p.S > 1) ? std::max(1, std::min({16 * p.S, n - 1, 8192 / k})) : 1;
   p.ept = ept_for(n);
   p.cap = (int)std::min(bucket_bound(k, std::max(n - 1, 0), p.S, p.SS), 60000L);
   p.tilt_smem = sizeof(double) * (size_t)n;
-  p.split_smem = (2 * sizeof(double) + 3 * sizeof(int)) * (size_t)k * p.SS;
+  p.split_smem = (sizeof(double) + 3 * sizeof(uint16_t)) * (size_t)k * p.SS;
   p.bucket_smem = bucket_smem_bytes(p.cap, k);
   p.plan_smem = 2 * (sizeof(double) + sizeof(int)) * (size_t)p.cap;
   return p;
@@ -2418,6 +2520,10 @@ extern "C" int uot_debug_mot_stats(unsigned long long* out, int reset) {
 #endif
 
 #ifdef UOT_MOT_TIMING
+extern "C" int uot_debug_bkt_stamps(unsigned long long* out, int n) {
+  cudaMemcpyFromSymbol(out, uot::g_bkt_stamps, sizeof(unsigned long long) * 6 * (size_t)n);
+  return 0;
+}
 // scripts/mot_timeline.py (timing build only)
 extern "C" int uot_debug_mot_stamps(unsigned long long* out, int n) {
   cudaMemcpyFromSymbol(out, uot::g_mot_stamps, sizeof(unsigned long long) * 8 * (size_t)n);
