@@ -96,6 +96,7 @@ struct MotArgs {
   double* samp;           // [B][K][SS] regular samples (values)
   int* sampt;             // [B][K][SS] (indices)
   int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
+  int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1, parity tests)
   // parity / trace mode (optional)
   const double* step_in;  // [B][max_iters] replayed gamma_t
   unsigned long long* supp_hash;  // [B][max_iters] plan-support hash
@@ -1091,7 +1092,7 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   int* binc = reinterpret_cast<int*>(
       (reinterpret_cast<uintptr_t>(qt + cap) + 15) & ~static_cast<uintptr_t>(15));
   const uint16_t* code = c1;
-  if (!bin_sort(key0, c1, binc, cnt_s, K, total))
+  if (A.no_bin || !bin_sort(key0, c1, binc, cnt_s, K, total))
     code = merge_runs16(key0, c0, c1, cnt_s, K, total) ? c1 : c0;
   BKT_STAMP(2);
   const int per = (total + BT2 - 1) / BT2;
@@ -2146,12 +2147,14 @@ MotPlan plan_for(int k, int n) {
 
 // Two lists per CTA (mot_update2) when K is even, the cluster stays portable
 // and rows are 16-byte aligned; UOT_MOT_UPDATE1=1 forces the one-list kernel.
+bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e != nullptr && e[0] == '1';
+}
+
 bool use_update2(const MotArgs& a) {
-  static const bool off = [] {
-    const char* e = getenv("UOT_MOT_UPDATE1");
-    return e != nullptr && e[0] == '1';
-  }();
-  return !off && a.mode == 0 && a.k % 2 == 0 && a.k / 2 <= 8 && a.n % 2 == 0;
+  return !env_flag("UOT_MOT_UPDATE1") && a.mode == 0 && a.k % 2 == 0 && a.k / 2 <= 8 &&
+         a.n % 2 == 0;
 }
 
 template <class Kern>
@@ -2311,6 +2314,7 @@ MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const dou
   a.S = p.S;
   a.SS = p.SS;
   a.cap = p.cap;
+  a.no_bin = env_flag("UOT_MOT_NOBIN") ? 1 : 0;
   a.ta = (double*)(ws + L.off[0]);
   a.A = (double*)(ws + L.off[1]);
   a.dcc = (double*)(ws + L.off[2]);

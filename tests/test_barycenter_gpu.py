@@ -186,3 +186,40 @@ def test_fw_barycenter_report_vs_reference(k):
     assert c.dual == pytest.approx(dual, rel=1e-9)
     assert abs(c.feasibility_violation - feas) <= 1e-12
     assert c.passed == bool(passed)
+
+
+# ---------------------------------------------------------------------------
+# Kernel variants of the sweep (csrc/mot1d.cu): the bin sort and its merge-path
+# fallback order the events identically (the (value, list, index) order is
+# total), and the one-list / two-lists-per-CTA updates compute the same
+# iterates; clustered keys (zero-weight runs repeat breakpoints) and ties
+# across lists (identical inputs) exercise the fallback and the tie rule.
+@pytest.mark.parametrize("env", ["UOT_MOT_NOBIN", "UOT_MOT_UPDATE1"])
+def test_sweep_variants_agree(monkeypatch, env):
+    xs, ws = S.cfg5_batch(count=3, n=2048)
+    ws[1, :, 100:400] = 0.0          # zero-weight runs: repeated breakpoints
+    xs[2, 5] = xs[2, 4]              # two identical lists: cross-list ties
+    ws[2, 5] = ws[2, 4]
+    w = np.full(16, 1 / 16)
+    base = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, "linesearch", trace_support=True)
+    monkeypatch.setenv(env, "1")
+    alt = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, "linesearch", trace_support=True)
+    monkeypatch.delenv(env)
+    assert (D.to_np(base.status) == 0).all() and (D.to_np(alt.status) == 0).all()
+    np.testing.assert_array_equal(D.to_np(base.supp_hash), D.to_np(alt.supp_hash))
+    f0, f1 = D.to_np(base.f), D.to_np(alt.f)
+    assert np.abs(f0 - f1).max() <= 1e-12 * np.abs(f0).max()
+    np.testing.assert_allclose(D.to_np(alt.h0), D.to_np(base.h0), rtol=1e-13)
+    c = D.to_np(base.count)
+    for p in range(3):
+        np.testing.assert_array_equal(D.to_np(alt.idx[p, :c[p]]), D.to_np(base.idx[p, :c[p]]))
+    # balanced sweep at full size through the fallback as well
+    if env == "UOT_MOT_NOBIN":
+        xb, wb = S.cfg5_batch(count=1)
+        wb = wb / wb.sum(axis=2, keepdims=True)
+        r0 = P.solve_mot_1d_batched(xb, wb, w)
+        monkeypatch.setenv(env, "1")
+        r1 = P.solve_mot_1d_batched(xb, wb, w)
+        monkeypatch.delenv(env)
+        c0 = int(r0[3][0].item())
+        np.testing.assert_array_equal(D.to_np(r0[1][0, :c0]), D.to_np(r1[1][0, :c0]))
