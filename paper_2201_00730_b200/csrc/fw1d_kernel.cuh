@@ -233,6 +233,29 @@ struct Cta {
     }
     mass_a = totals[0];
     mass_b = totals[1];
+    oracle_tail(ta, tb, r, s, ping);
+  }
+
+  // The oracle from breakpoints scanned before the tilt factors were known:
+  // B = scale (offset + local inclusive prefix) of the unscaled weights (the
+  // scan then doubles as the log-sum-exp reduction: one block sync less).
+  template <typename PING>
+  __device__ void oracle_scaled(const double (&ta)[EPT], const double (&tb)[EPT],
+                                const double (&pa)[EPT], const double (&pb)[EPT], double offa,
+                                double offb, double sca, double scb, double (&r)[EPT],
+                                double (&s)[EPT], PING& ping) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = src(e);
+      if (i < n) sA[i] = sca * (offa + pa[e]);
+      if (i < m) sB[i] = scb * (offb + pb[e]);
+    }
+    oracle_tail(ta, tb, r, s, ping);
+  }
+
+  template <typename PING>
+  __device__ __forceinline__ void oracle_tail(const double (&ta)[EPT], const double (&tb)[EPT],
+                                              double (&r)[EPT], double (&s)[EPT], PING& ping) {
     if (zeros) {
       // A zero-weight atom must repeat its predecessor's breakpoint bit for
       // bit (the reference emits no entry for it, ot1d.py:149-153), but the
@@ -762,22 +785,27 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   for (int t = 0; t < A.max_iters; ++t) {
     // --- lambda*, H_0 and the tilted marginals (duality.py:175-178, :279-303).
     // The exponentials are shared between the log-sum-exps and the tilt.
-    double ta[EPT], tb[EPT];
-    double sums[2];
+    double ta[EPT], tb[EPT], pa[EPT], pb[EPT];
+    double sums[2], offs[2];
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
-      sums[0] = 0.0;
-      sums[1] = 0.0;
+      // exponentials, local prefixes and one block scan: the scan's totals are
+      // the log-sum-exp sums, its offsets give the breakpoints (oracle_scaled)
+      double ca = 0.0, cb = 0.0;
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
         ta[e] = bops::wexp(wa, -f[e] * i1 - sha, tab);
         tb[e] = bops::wexp(wb, -g[e] * i2 - shb, tab);
-        sums[0] += ta[e];
-        sums[1] += tb[e];
+        ca += ta[e];
+        pa[e] = ca;
+        cb += tb[e];
+        pb[e] = cb;
       }
-      bops::block_sum<NW, 2>(sums, ping.next());
+      offs[0] = ca;
+      offs[1] = cb;
+      bops::block_scan_excl<NW, 2>(offs, sums, ping.next());
       // block-uniform: a stale shift far above the maximum underflowed
       if (!((sums[0] < 1e-280 && sha > -CUDART_INF) || (sums[1] < 1e-280 && shb > -CUDART_INF)))
         break;
@@ -819,8 +847,9 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
       tb[e] *= scb;
     }
     // --- linear oracle (ot1d.py:112-172 on the tilted marginals, fw.py:159-173)
-    double r[EPT], s[EPT], mta, mtb;
-    c.oracle(ta, tb, r, s, mta, mtb, ping);
+    double r[EPT], s[EPT];
+    const double mta = sca * sums[0], mtb = scb * sums[1];
+    c.oracle_scaled(ta, tb, pa, pb, offs[0], offs[1], sca, scb, r, s, ping);
     if (fabs(mta - mtb) > 1e-9 * fmax(mta, mtb)) {  // fw.py:161-166
       status = UOT_MASS_BALANCE;
       break;
@@ -851,7 +880,27 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
       acc[7] += tb[e] * vb;
       acc[8] += tb[e] * vb * vb;
     }
-    bops::block_red<NW, 9, 2>(acc, mr, ping.next());
+    {
+      // one-sync block reduction; the trace sums (0-4) are combined only
+      // where they are needed (warp 0 writes the traces; every thread when
+      // the early exit tests the primal-dual gap)
+      double* rb = ping.next();
+      bops::put_sums<NW, 9>(acc, rb);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double mx = bops::warp_dmax(mr[k]);
+        if (lane == 0) rb[(9 + k) * NW + (threadIdx.x >> 5)] = mx;
+      }
+      __syncthreads();
+      if (A.early_exit || threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) acc[k] = bops::get_sum<NW>(rb + k * NW);
+      }
+#pragma unroll
+      for (int k = 5; k < 9; ++k) acc[k] = bops::get_sum<NW>(rb + k * NW);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) mr[k] = bops::get_max<NW>(rb + (9 + k) * NW);
+    }
     const double fw_gap = acc[0] + acc[1];
     const double kl1 = acc[3] - mta + malpha, kl2 = acc[4] - mtb + mbeta;
     const double primal = acc[2] + r1 * kl1 + r2 * kl2;
