@@ -1203,7 +1203,7 @@ __global__ void sk_zero(long n, T* p) {
 namespace {
 
 struct WsLayout {
-  size_t off[17];
+  size_t off[18];
   size_t total;
 };
 
@@ -1226,17 +1226,20 @@ struct Buffers {
   int* iters_done;
   double* trace;  // scratch trace when the caller passes none
   T* ctr;         // [B][d] centre of the tcgen05 operands (tc_center)
+  uint32_t* packA;  // tcgen05 path: precomputed A rows of the sources [B][n][W] (tc_pack_out)
+  uint32_t* packB;  // ... of the targets [B][m][W]
 };
 
 struct Shape {
   int B, n, m, d, rwA, rwB, S, nblk;
   int total_n;  // all shards (emulation)
   long recA, recB;  // record elements per problem
+  int pack_w = 0;   // tcgen05 path: words per precomputed A row (0: none)
 };
 
 template <typename T>
 size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* base) {
-  size_t sizes[17];
+  size_t sizes[18];
   const long nm = std::max(s.total_n, s.m);
   sizes[0] = sizeof(T) * (size_t)s.B * s.recA;
   sizes[1] = sizeof(T) * (size_t)s.B * s.recB;
@@ -1255,8 +1258,9 @@ size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* bas
   sizes[14] = sizeof(int) * (size_t)s.B;
   sizes[15] = sizeof(double) * (size_t)s.B * std::max(iters, 1);
   sizes[16] = sizeof(T) * (size_t)s.B * std::max(s.d, 4);
+  sizes[17] = sizeof(uint32_t) * (size_t)s.B * (s.total_n + s.m) * s.pack_w;
   size_t off = 0;
-  for (int k = 0; k < 17; ++k) {
+  for (int k = 0; k < 18; ++k) {
     L.off[k] = off;
     off += (sizes[k] + 255) / 256 * 256;
   }
@@ -1279,6 +1283,8 @@ size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* bas
     buf->iters_done = (int*)(base + L.off[14]);
     buf->trace = (double*)(base + L.off[15]);
     buf->ctr = (T*)(base + L.off[16]);
+    buf->packA = s.pack_w > 0 ? (uint32_t*)(base + L.off[17]) : nullptr;
+    buf->packB = s.pack_w > 0 ? buf->packA + (size_t)s.B * s.total_n * s.pack_w : nullptr;
   }
   return L.total;
 }
@@ -1416,6 +1422,8 @@ struct Engine {
     s.S = std::max(sA, sB);
     if (d.nranks > 1 && d.nccl_comm == nullptr) s.S = std::max(s.S, d.nranks);
     s.nblk = (int)ceil_div(std::max(d.n, d.m), TAIL_THREADS);
+    if constexpr (std::is_same<P, SqE32TC>::value)
+      s.pack_w = std::getenv("UOT_TC_NOPACK") == nullptr ? tc_pack_words(d.d) : 0;
     return s;
   }
 
@@ -1462,6 +1470,8 @@ struct Engine {
     a.g.ctr_bstride = d.d;
     a.g.ascale = (T)tc_ascale((double)(float)L);
     a.g.tc_full = 2.0 * (double)(float)L > 128.0 ? 1 : 0;
+    a.g.tc_pack = to_target ? bf.packB : bf.packA;
+    a.g.tc_pack_bstride = (long)(to_target ? d.m : d.n) * tc_pack_words(d.d);
     a.nred = nred;
     a.red_offset = red_offset;
     a.part_m = bf.part_m;
@@ -1632,6 +1642,12 @@ struct Engine {
       tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y,
                                            (const float*)bf.ctr, (long)d.d, d.batch, d.m,
                                            d.d, tc_kp(d.d), Lr, Sa);
+      if (bf.packA != nullptr) {
+        tc_pack_out<<<1024, 256, 0, st>>>(bf.packA, (const float*)d.x, (const float*)bf.ctr,
+                                          (long)d.d, d.batch, d.n, d.d, (float)Sa);
+        tc_pack_out<<<1024, 256, 0, st>>>(bf.packB, (const float*)d.y, (const float*)bf.ctr,
+                                          (long)d.d, d.batch, d.m, d.d, (float)Sa);
+      }
       UOT_CHECK_LAUNCH();
     }
     const long nm = std::max(d.n, d.m);
@@ -1778,6 +1794,12 @@ struct Engine {
       tc_init_static<<<1024, 256, 0, st>>>(bf.recB, s.recB, (const float*)d.y,
                                            (const float*)bf.ctr, (long)d.d, d.batch, d.m,
                                            d.d, tc_kp(d.d), Lr, Sa);
+      if (bf.packA != nullptr) {
+        tc_pack_out<<<1024, 256, 0, st>>>(bf.packA, (const float*)d.x, (const float*)bf.ctr,
+                                          (long)d.d, d.batch, d.n, d.d, (float)Sa);
+        tc_pack_out<<<1024, 256, 0, st>>>(bf.packB, (const float*)d.y, (const float*)bf.ctr,
+                                          (long)d.d, d.batch, d.m, d.d, (float)Sa);
+      }
       UOT_CHECK_LAUNCH();
     }
     sk_zero<T><<<256, 256, 0, st>>>((long)d.batch * s.n, bf.shiftA);
@@ -2195,7 +2217,7 @@ extern "C" int uot_sinkhorn_time_main(const uot_sinkhorn_desc* desc, void* works
 #ifdef UOT_TC_TIMING
 // scripts/tc_timeline.py (timing build only)
 extern "C" int uot_debug_tc_stamps(unsigned long long* out, int n) {
-  cudaMemcpyFromSymbol(out, uot::g_tc_stamps, sizeof(unsigned long long) * 5 * (size_t)n);
+  cudaMemcpyFromSymbol(out, uot::g_tc_stamps, sizeof(unsigned long long) * 8 * (size_t)n);
   return 0;
 }
 #endif

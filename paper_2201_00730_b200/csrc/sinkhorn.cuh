@@ -47,6 +47,8 @@ struct DirGeo {
   long ctr_bstride;
   T ascale;             // tcgen05 path: power-of-two scale of the A operand (B gets 2L/ascale)
   int tc_full;          // tcgen05 path: also the Yl*Xl product (2L > 128, i.e. eps < ~0.0225)
+  const uint32_t* tc_pack;  // tcgen05 path: precomputed A rows of the output side (tc_pack_out)
+  long tc_pack_bstride;     // words per problem
 };
 
 template <typename T>

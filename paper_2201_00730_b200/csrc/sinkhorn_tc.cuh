@@ -86,6 +86,11 @@ __device__ __forceinline__ long tc_cidx(int rl, int c, int d) {
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(tc::tf32_rna(x)); }
 
+// Precomputed A row of an output point (tc_pack_out, once per solve: the
+// points do not change across iterations): [Yh pairs (dp/2 words) | Yl pairs
+// (dp/2 words) | |y'|^2 as an fp64 (2 words) | 2 pad words], 16-byte rows.
+__host__ __device__ constexpr int tc_pack_words(int d) { return tc_dp(d) + 4; }
+
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);  // .x (low 16 bits) = a
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -119,7 +124,7 @@ __device__ __forceinline__ void tc_slice_mmas(int kh, int dp, uint32_t dcol, uin
 #ifdef UOT_TC_TIMING
 // timing build only (scripts/tc_timeline.py): per-CTA %globaltimer stamps
 // (start, A ready, first tile, last tile, end)
-__device__ unsigned long long g_tc_stamps[1 << 16][5];
+__device__ unsigned long long g_tc_stamps[1 << 16][8];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -153,6 +158,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int nst = nxs + 1;
   const bool full4 = A.g.tc_full != 0;
   (void)KP;
+  // Precomputed A row of this epilogue thread (compile-time d): its loads are
+  // issued before the TMEM allocation and barrier set-up, so their latency
+  // overlaps the prologue.
+  constexpr int PG = DT > 0 ? tc_dp(DT) / 16 : 1;  // 16-wide K groups
+  uint4 pre[DT > 0 ? 4 * PG + 1 : 1];
+  const bool packed = A.g.tc_pack != nullptr;
+  const int row0 = blockIdx.x * (TC_NB * TC_TILE);
+  const int blk = warp >= 2 ? (warp - 2) >> 2 : 0;
+  const int lane_base = 32 * (warp & 3);
+  const int row = lane_base + lane;
+  const int o = row0 + blk * TC_TILE + row;
+  // the stale shift of this output, also loaded up front
+  const float m_pre = (warp >= 2 && o < A.nout) ? __ldg(A.shift_in + (long)b * A.nout + o) : 0.f;
+  if constexpr (DT > 0) {
+    if (packed && warp >= 2) {
+      const uint4 zz = make_uint4(0u, 0u, 0u, 0u);
+      const bool live = o < A.nout;
+      const uint4* pr = reinterpret_cast<const uint4*>(A.g.tc_pack + b * A.g.tc_pack_bstride +
+                                                       (long)(live ? o : 0) * tc_pack_words(DT));
+#pragma unroll
+      for (int i = 0; i < 4 * PG + 1; ++i) pre[i] = live ? __ldg(pr + i) : zz;
+    }
+  }
 
   if (warp == 1) tc::tmem_alloc2(&tbase_s, 512);
   if (tid == 0) {
@@ -170,15 +198,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  TC_STAMP(5);
   const uint32_t tbase = tbase_s;
 
   // Epilogue threads own one output row of one block each (TMEM lane
-  // restriction: warp w reaches lanes 32*(w%4) .. +31).
-  const int blk = warp >= 2 ? (warp - 2) >> 2 : 0;
-  const int lane_base = 32 * (warp & 3);
-  const int row = lane_base + lane;
-  const int row0 = blockIdx.x * (TC_NB * TC_TILE);
-  const int o = row0 + blk * TC_TILE + row;
+  // restriction: warp w reaches lanes 32*(w%4) .. +31): blk, row, o above.
   float m_o = 0.f;
   // Prologue: the producer warp arrives at the cluster barrier and starts
   // streaming B stages at once (they depend on nothing else); the other
@@ -189,7 +213,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   const int YS = tc_ystride(d);
   if (warp == 0) {
     tc::cluster_arrive();
-  } else {
+  } else if (!packed) {
     const int nrows = max(0, min(TC_NB * TC_TILE, A.nout - row0));
     const float4* src =
         reinterpret_cast<const float4*>(A.g.out_pts + b * A.g.out_pts_bstride + (long)row0 * d);
@@ -202,8 +226,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
           make_float4(v.x - cv.x, v.y - cv.y, v.z - cv.z, v.w - cv.w);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(TC_THREADS - 32) : "memory");
+    TC_STAMP(6);
   }
-  if (warp >= 2) {
+  if (warp >= 2 && packed) {
+    // the precomputed row: 16-byte loads, no staging, no fp64 / fp16 work
+    const uint32_t ta = tbase + ((uint32_t)lane_base << 16) + blk * ka;
+    const int W = tc_pack_words(d);
+    // (tcgen05.st is warp-collective: every lane stores, rows past nout zeros)
+    const bool live = o < A.nout;
+    const uint4* pr = reinterpret_cast<const uint4*>(A.g.tc_pack + b * A.g.tc_pack_bstride +
+                                                     (long)(live ? o : 0) * W);
+    const uint4 zz = make_uint4(0u, 0u, 0u, 0u);
+    double s2 = 0.0;
+    if constexpr (DT > 0) {  // rows preloaded at kernel entry
+#pragma unroll
+      for (int g = 0; g < PG; ++g) {
+        const uint4 h0 = pre[2 * g], h1 = pre[2 * g + 1];
+        const uint4 l0 = pre[2 * PG + 2 * g], l1 = pre[2 * PG + 2 * g + 1];
+        const uint32_t vh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const uint32_t vl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        tc::tmem_st8(ta + 8 * g, vh);
+        tc::tmem_st8(ta + dp / 2 + 8 * g, vl);
+      }
+      if (live) s2 = __hiloint2double((int)pre[4 * PG].y, (int)pre[4 * PG].x);
+    } else {
+      for (int g = 0; g < dp / 16; ++g) {
+        const uint4 h0 = live ? __ldg(pr + 2 * g) : zz, h1 = live ? __ldg(pr + 2 * g + 1) : zz;
+        const uint4 l0 = live ? __ldg(pr + dp / 8 + 2 * g) : zz;
+        const uint4 l1 = live ? __ldg(pr + dp / 8 + 2 * g + 1) : zz;
+        const uint32_t vh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const uint32_t vl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        tc::tmem_st8(ta + 8 * g, vh);
+        tc::tmem_st8(ta + dp / 2 + 8 * g, vl);
+      }
+      if (live) {
+        const uint4 q = __ldg(pr + dp / 4);
+        s2 = __hiloint2double((int)q.y, (int)q.x);
+      }
+    }
+    m_o = m_pre;
+    const double c = -s2 * (double)A.g.L - (double)m_o;
+    const float ch = tf32_hi((float)c);
+    const double c1 = c - (double)ch;
+    const float cm = tf32_hi((float)c1);
+    const float cl = (float)(c1 - (double)cm);
+    {
+      const uint32_t vt[8] = {__float_as_uint(1.f), __float_as_uint(1.f), __float_as_uint(1.f),
+                              __float_as_uint(ch),  __float_as_uint(cm),  __float_as_uint(cl),
+                              0u,                   0u};
+      tc::tmem_st8(ta + dp, vt);
+    }
+    tc::wait_st();
+    TC_STAMP(7);
+  } else if (warp >= 2) {
     const float* y = ys + (blk * TC_TILE + row) * YS;
     double s2 = 0.0;
     if (o < A.nout) {
@@ -255,6 +330,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       tc::tmem_st8(ta + dp, vt);
     }
     tc::wait_st();
+    TC_STAMP(7);
   }
   // both CTAs' A rows and barriers ready before any MMA / remote arrive
   if (warp != 0) {
@@ -454,6 +530,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
   tc::cluster_sync_all();  // both CTAs done with TMEM and remote barriers
   TC_STAMP(4);
   if (warp == 1) tc::tmem_free2(tbase, 512);
+}
+
+// A rows of the output side, once per solve: y' = y - centre, |y'|^2 by the
+// prologue's four fp64 chains, and the fp16 hi/lo splits of ascale y' --
+// bit for bit what sk_main_tc's unpacked prologue builds.
+__global__ void tc_pack_out(uint32_t* out, const float* pts, const float* ctr, long ctr_bstride,
+                            int batch, int nrows, int d, float ascale) {
+  const int dp = tc_dp(d), W = tc_pack_words(d);
+  const long total = (long)batch * nrows;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / nrows);
+    const float* y = pts + i * d;
+    const float* c = ctr + b * ctr_bstride;
+    uint32_t* row = out + i * W;
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+    for (int k = 0; k < d; k += 4) {
+      const float v0 = y[k] - c[k], v1 = y[k + 1] - c[k + 1], v2 = y[k + 2] - c[k + 2],
+                  v3 = y[k + 3] - c[k + 3];
+      q0 = fma((double)v0, (double)v0, q0);
+      q1 = fma((double)v1, (double)v1, q1);
+      q2 = fma((double)v2, (double)v2, q2);
+      q3 = fma((double)v3, (double)v3, q3);
+    }
+    const double s2 = (q0 + q1) + (q2 + q3);
+    for (int cc = 0; cc < dp / 2; ++cc) {
+      const int k = 2 * cc;
+      const float y0 = k < d ? y[k] - c[k] : 0.f, y1 = k + 1 < d ? y[k + 1] - c[k + 1] : 0.f;
+      const float a0 = ascale * y0, a1 = ascale * y1;
+      const float h0 = __half2float(__float2half_rn(a0)), h1 = __half2float(__float2half_rn(a1));
+      row[cc] = pack_h2(h0, h1);
+      row[dp / 2 + cc] = pack_h2(a0 - h0, a1 - h1);
+    }
+    row[dp] = (uint32_t)__double2loint(s2);
+    row[dp + 1] = (uint32_t)__double2hiint(s2);
+    row[dp + 2] = 0u;
+    row[dp + 3] = 0u;
+  }
 }
 
 // Dead-row fill of a record buffer: X = 0 and U = -1e30 (exp2 -> 0) with

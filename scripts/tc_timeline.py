@@ -15,9 +15,11 @@ P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, 1, precis
 torch.cuda.synchronize()
 lib = _lib.load()
 n = B * 16  # CTAs of one launch (two 128-row blocks per CTA, 4096 outputs)
-buf = (ctypes.c_ulonglong * (5 * n))()
+buf = (ctypes.c_ulonglong * (8 * n))()
 lib.uot_debug_tc_stamps(buf, n)
-t = np.array(buf, dtype=np.float64).reshape(n, 5)
+t8 = np.array(buf, dtype=np.float64).reshape(n, 8)
+t8 = t8[t8[:, 0] > 0]
+t = t8[:, :5]
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 d = np.diff(t, axis=1) / 1e3
@@ -26,3 +28,7 @@ for k, name in enumerate(["prologue", "fill (first tile)", "tiles", "drain"]):
     print(f"{name:18s} mean {d[:, k].mean():7.2f} us  p10 {np.percentile(d[:, k], 10):7.2f}  p90 {np.percentile(d[:, k], 90):7.2f}")
 life = (t[:, 4] - t[:, 0]) / 1e3
 print(f"lifetime mean {life.mean():.2f} us; concurrent CTAs ~ {life.sum() / ((t[:, 4].max() - t0) / 1e3):.1f}")
+sub = t8[:, [0, 5, 6, 7, 1]]
+for k, name in enumerate(["alloc + barrier init", "stage outputs", "build A in TMEM", "cluster sync"]):
+    dd = np.diff(sub, axis=1)[:, k] / 1e3
+    print(f"  prologue: {name:22s} mean {dd.mean():7.2f} us")
