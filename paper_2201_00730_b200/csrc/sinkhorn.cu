@@ -464,11 +464,12 @@ __global__ void __launch_bounds__(THREADS) sk_main(MainArgs<typename P::T> A) {
 
   typename P::Out out[COLS];
   T cc[COLS], mm[COLS], acc[COLS];
-  const int obase = blockIdx.x * THREADS * COLS + threadIdx.x;
+  const int ohi = A.out_hi > 0 ? A.out_hi : A.nout;
+  const int obase = A.out_lo + blockIdx.x * THREADS * COLS + threadIdx.x;
 #pragma unroll
   for (int c = 0; c < COLS; ++c) {
     const int o = obase + c * THREADS;
-    const bool ok = o < A.nout;
+    const bool ok = o < ohi;
     P::load(out[c], A.g, b, ok ? o : 0);
     mm[c] = ok ? A.shift_in[(long)b * A.nout + o] : T(0);
     cc[c] = out[c].bias - mm[c];
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(THREADS) sk_main(MainArgs<typename P::T> A) {
 #pragma unroll
   for (int c = 0; c < COLS; ++c) {
     const int o = obase + c * THREADS;
-    if (o < A.nout) {
+    if (o < ohi) {
       const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
       A.part_m[idx] = mm[c];
       A.part_a[idx] = acc[c];
@@ -682,7 +683,8 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
   constexpr int COLS = 2 * CP;
   u64 y0[CP], y1[CP], cc[CP], acc[CP];
   float mm[COLS];
-  const int obase = blockIdx.x * THREADS * COLS + threadIdx.x;
+  const int ohi = A.out_hi > 0 ? A.out_hi : A.nout;
+  const int obase = A.out_lo + blockIdx.x * THREADS * COLS + threadIdx.x;
   const float L = A.g.L;
   const float* pts = A.g.out_pts + b * A.g.out_pts_bstride;
   const float cen0 = A.g.ctr[b * A.g.ctr_bstride], cen1 = A.g.ctr[b * A.g.ctr_bstride + 1];
@@ -692,7 +694,7 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int o = obase + (2 * j + h) * THREADS;
-      const bool ok = o < A.nout;
+      const bool ok = o < ohi;
       const float q0 = ok ? pts[(long)o * 2] - cen0 : 0.f;
       const float q1 = ok ? pts[(long)o * 2 + 1] - cen1 : 0.f;
       ya0[h] = q0;
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int o = obase + (2 * j + h) * THREADS;
-      if (o < A.nout) {
+      if (o < ohi) {
         const long idx = ((long)b * A.splits_total + A.split_base + split) * A.nout + o;
         A.part_m[idx] = mm[2 * j + h];
         A.part_a[idx] = a2[h];
@@ -1134,11 +1136,12 @@ __global__ void sk_finalize(int n, int m, const T* hatA0, const T* hatA1, const 
 // Row sharding, phase 1: fold this rank's split partials into one
 // (shift, sum) pair per output (the payload of the all-gather).
 template <typename T>
-__global__ void sk_combine(int nout, int S, const T* part_m, const T* part_a, T* out_m, T* out_a) {
+__global__ void sk_combine(int nout, int S, const T* part_m, const T* part_a, T* out_m, T* out_a,
+                           int o_lo, int o_hi) {
   using D = Dom<T>;
   const int b = blockIdx.y;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nout) return;
+  const int o = o_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= o_hi) return;
   const long pb = (long)b * S * nout + o;
   double M = -CUDART_INF;
   for (int s = 0; s < S; ++s)
@@ -1436,8 +1439,10 @@ struct Engine {
 
   static int launch_main(const uot_sinkhorn_desc& d, const Buffers<T>& bf, cudaStream_t st,
                          bool to_target, int splits, int red_offset, int nred, int split_base,
-                         int splits_total) {
+                         int splits_total, int out_lo = 0, int out_hi = 0) {
     MainArgs<T> a{};
+    a.out_lo = out_lo;
+    a.out_hi = out_hi;
     const double L = 1.0 / (d.eps * Dom<T>::unit);
     a.g.rw = P::rw(d.d);
     a.g.d = d.d;
@@ -1480,7 +1485,7 @@ struct Engine {
     a.chunk = chunk_for(a.g.rw);
     a.split_base = split_base;
     a.splits_total = splits_total;
-    dim3 grid(ceil_div(a.nout, OUT_PER_BLOCK), splits, d.batch);
+    dim3 grid(ceil_div((out_hi > 0 ? out_hi : a.nout) - out_lo, OUT_PER_BLOCK), splits, d.batch);
     const size_t smem = (size_t)a.chunk * a.g.rw * sizeof(T);
     if constexpr (std::is_same<P, SqE32TC>::value) {
       const size_t tsm = tc_smem_bytes(d.d);
@@ -1913,6 +1918,68 @@ struct Engine {
     return L.total;
   }
 
+  static int shard_chunks(int m, int nranks) {
+    const char* e = std::getenv("UOT_SHARD_CHUNKS");
+    int c = e ? std::atoi(e) : (nranks > 1 ? 4 : 1);
+    c = std::max(1, std::min(c, 16));
+    const int min_cols = e ? 1 : 1024;  // default: chunks of >= 1024 columns
+    while (c > 1 && m / c < min_cols) --c;
+    return c;
+  }
+
+  // Exchange of the g-update's pairs for columns [c0, c1) (and, with the
+  // first chunk, the published scalars) into the same gathered layout as
+  // exchange(): grouped NCCL sends / receives with every peer over
+  // NVLink, or device copies between the emulated rank contexts.
+  static int exchange_cols(const uot_sinkhorn_desc& d, const ShardLayout& L, char* base,
+                           char* recv, int c0, int c1, bool scalars, cudaStream_t st) {
+    const size_t scal_bytes = sizeof(double) * 4 * d.batch;
+    const size_t arr = sizeof(T) * (size_t)d.batch * d.m;  // bytes of one pair array
+    const size_t lo = sizeof(T) * (size_t)c0, len = sizeof(T) * (size_t)(c1 - c0);
+    // pieces of a rank's slot: (offset, bytes); batch == 1 on the sharded path
+    const size_t off[3] = {0, scal_bytes + lo, scal_bytes + arr + lo};
+    const size_t sz[3] = {scalars ? scal_bytes : 0, len, len};
+#if defined(UOT_WITH_NCCL)
+    if (d.nccl_comm != nullptr) {
+      ncclComm_t comm = (ncclComm_t)d.nccl_comm;
+      const int me = d.rank, npeer = d.nranks;
+      char* mine = base + L.xbuf_off;
+      ncclResult_t rc = ncclGroupStart();
+      for (int k = 0; k < 3 && rc == ncclSuccess; ++k) {
+        if (sz[k] == 0) continue;
+        for (int p = 0; p < npeer && rc == ncclSuccess; ++p) {
+          if (p == me) continue;
+          rc = ncclSend(mine + off[k], sz[k], ncclChar, p, comm, st);
+          if (rc == ncclSuccess)
+            rc = ncclRecv(recv + L.stride * p + off[k], sz[k], ncclChar, p, comm, st);
+        }
+      }
+      const ncclResult_t re = ncclGroupEnd();
+      if (rc != ncclSuccess || re != ncclSuccess) {
+        set_error("chunked exchange failed: %s",
+                  ncclGetErrorString(rc != ncclSuccess ? rc : re));
+        return UOT_NCCL;
+      }
+      for (int k = 0; k < 3; ++k)
+        if (sz[k] > 0)
+          UOT_CUDA_TRY(cudaMemcpyAsync(recv + L.stride * me + off[k], mine + off[k], sz[k],
+                                       cudaMemcpyDeviceToDevice, st));
+      return UOT_OK;
+    }
+#endif
+    if (d.nccl_comm != nullptr) {
+      set_error("built without NCCL");
+      return UOT_NCCL;
+    }
+    for (int r = 0; r < L.R; ++r)
+      for (int k = 0; k < 3; ++k)
+        if (sz[k] > 0)
+          UOT_CUDA_TRY(cudaMemcpyAsync(recv + L.stride * r + off[k],
+                                       base + L.xbuf_off + L.stride * r + off[k], sz[k],
+                                       cudaMemcpyDeviceToDevice, st));
+    return UOT_OK;
+  }
+
   static int exchange(const uot_sinkhorn_desc& d, const ShardLayout& L, char* base, size_t bytes,
                       char* recv, size_t recv_stride, cudaStream_t st) {
 #if defined(UOT_WITH_NCCL)
@@ -1989,17 +2056,52 @@ struct Engine {
                           trace_len, &so));
     }
     double* trace = d.trace_delta != nullptr ? d.trace_delta : bf[0].trace;
-    for (int t = 0; t < d.iters; ++t) {
-      for (int r = 0; r < L.R; ++r) {
-        UOT_TRY(launch_main(dr[r], bf[r], st, true, sB[r], 0, L.nl[r], 0, sB[r]));
-        char* xb = base + L.xbuf_off + L.stride * r;
-        T* pm = (T*)(xb + scal_bytes);
-        T* pa = pm + (size_t)d.batch * d.m;
-        sk_combine<T><<<dim3(ceil_div(d.m, 256), d.batch), 256, 0, st>>>(d.m, sB[r], bf[r].part_m,
-                                                                         bf[r].part_a, pm, pa);
-        UOT_CHECK_LAUNCH();
+    // The g-update's exchange runs in column chunks on a second stream: chunk
+    // c's (shift, sum) pairs travel while the main kernel computes chunk c+1
+    // (SURVEY.md §8e).  UOT_SHARD_CHUNKS overrides the count (1: no overlap).
+    const int nchunk = shard_chunks(d.m, NR);
+    cudaStream_t cs = st;
+    std::vector<cudaEvent_t> ev;
+    if (nchunk > 1) {
+      UOT_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      ev.resize(nchunk + 1);
+      for (auto& e : ev) UOT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    struct StreamGuard {
+      cudaStream_t s, main;
+      std::vector<cudaEvent_t>* ev;
+      ~StreamGuard() {
+        if (s != main) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+          for (auto& e : *ev) cudaEventDestroy(e);
+        }
       }
-      UOT_TRY(exchange(d, L, base, L.stride, xall, L.stride, st));
+    } guard{cs, st, &ev};
+    for (int t = 0; t < d.iters; ++t) {
+      for (int c = 0; c < nchunk; ++c) {
+        const int c0 = (int)((long)d.m * c / nchunk), c1 = (int)((long)d.m * (c + 1) / nchunk);
+        for (int r = 0; r < L.R; ++r) {
+          UOT_TRY(launch_main(dr[r], bf[r], st, true, sB[r], 0, L.nl[r], 0, sB[r], c0, c1));
+          char* xb = base + L.xbuf_off + L.stride * r;
+          T* pm = (T*)(xb + scal_bytes);
+          T* pa = pm + (size_t)d.batch * d.m;
+          sk_combine<T><<<dim3(ceil_div(c1 - c0, 256), d.batch), 256, 0, st>>>(
+              d.m, sB[r], bf[r].part_m, bf[r].part_a, pm, pa, c0, c1);
+          UOT_CHECK_LAUNCH();
+        }
+        if (nchunk == 1) {
+          UOT_TRY(exchange(d, L, base, L.stride, xall, L.stride, st));
+        } else {
+          UOT_CUDA_TRY(cudaEventRecord(ev[c], st));
+          UOT_CUDA_TRY(cudaStreamWaitEvent(cs, ev[c], 0));
+          UOT_TRY(exchange_cols(d, L, base, xall, c0, c1, c == 0, cs));
+        }
+      }
+      if (nchunk > 1) {  // the g-tail needs every chunk
+        UOT_CUDA_TRY(cudaEventRecord(ev[nchunk], cs));
+        UOT_CUDA_TRY(cudaStreamWaitEvent(st, ev[nchunk], 0));
+      }
       for (int r = 0; r < L.R; ++r) {
         const T* pm = (const T*)(xall + scal_bytes);
         const T* pa = pm + (size_t)d.batch * d.m;

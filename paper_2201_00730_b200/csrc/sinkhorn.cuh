@@ -63,6 +63,7 @@ struct MainArgs {
   int red_offset;     // reduced range handled by this launch: [red_offset, red_offset+nred)
   int split_base;     // first split index written by this launch
   int splits_total;   // S of the partial buffer layout
+  int out_lo, out_hi; // output range of this launch (out_hi == 0: all nout outputs)
 };
 
 template <typename T>

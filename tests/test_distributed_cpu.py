@@ -35,7 +35,7 @@ def _merge(ms, ss):
     return M, acc
 
 
-def _sharded_h_sinkhorn(rank, world, x, y, a, b, eps, rho, iters):
+def _sharded_h_sinkhorn(rank, world, x, y, a, b, eps, rho, iters, chunks=1):
     n = len(x)
     rows = shard_rows(n, world)
     off = row_offset(n, world, rank)
@@ -65,9 +65,31 @@ def _sharded_h_sinkhorn(rank, world, x, y, a, b, eps, rho, iters):
     hat_g = tau_b = shat_b = None
     deltas = []
     for t in range(iters):
-        m, s = _lse_pairs((hat_a[:, None] - C) / eps, al[:, None], 0)
-        allp = gather(np.concatenate([my_scal, m, s]))
-        sc, pm, ps = allp[:, :4], allp[:, 4:4 + len(y)], allp[:, 4 + len(y):]
+        if chunks == 1:
+            m, s = _lse_pairs((hat_a[:, None] - C) / eps, al[:, None], 0)
+            allp = gather(np.concatenate([my_scal, m, s]))
+            sc, pm, ps = allp[:, :4], allp[:, 4:4 + len(y)], allp[:, 4 + len(y):]
+        else:
+            # column chunks: chunk c's gather is in flight (async) while chunk
+            # c+1 is reduced, as run_sharded overlaps them on a second stream;
+            # the scalars travel with chunk 0
+            pend = []
+            for c in range(chunks):
+                c0, c1 = len(y) * c // chunks, len(y) * (c + 1) // chunks
+                m, s = _lse_pairs((hat_a[:, None] - C[:, c0:c1]) / eps, al[:, None], 0)
+                pay = np.concatenate([my_scal, m, s]) if c == 0 else np.concatenate([m, s])
+                tt = torch.as_tensor(pay)
+                out = [torch.empty_like(tt) for _ in range(world)]
+                pend.append((c0, c1, out, dist.all_gather(out, tt, async_op=True)))
+            pm = np.empty((world, len(y)))
+            ps = np.empty((world, len(y)))
+            for c, (c0, c1, out, work) in enumerate(pend):
+                work.wait()
+                arr = np.stack([o.numpy() for o in out])
+                if c == 0:
+                    sc, arr = arr[:, :4], arr[:, 4:]
+                w = c1 - c0
+                pm[:, c0:c1], ps[:, c0:c1] = arr[:, :w], arr[:, w:]
         qm, qs = _merge(sc[:, 0:1], sc[:, 1:2])
         shat_a = -r1 * (qm[0] + np.log(qs[0]))
         new_tau_a = 0.0 if t == 0 else facA * shat_a
@@ -90,7 +112,7 @@ def _sharded_h_sinkhorn(rank, world, x, y, a, b, eps, rho, iters):
     return hat_a + tau_a, hat_g + tau_b, np.array(deltas)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, chunks=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -101,7 +123,7 @@ def _worker(rank, world, port, q):
         y = np.sort(rng.uniform(0, 1, m))
         a = rng.uniform(0.1, 1.0, n)
         b = rng.uniform(0.1, 1.0, m) * 1.3
-        f_loc, g, dl = _sharded_h_sinkhorn(rank, world, x, y, a, b, 0.05, 1.0, 30)
+        f_loc, g, dl = _sharded_h_sinkhorn(rank, world, x, y, a, b, 0.05, 1.0, 30, chunks)
         parts = [None] * world
         dist.all_gather_object(parts, f_loc)
         if rank == 0:
@@ -131,11 +153,12 @@ def test_partitions():
 
 
 @pytest.mark.timeout(300)
-def test_sharded_protocol_gloo_world2():
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_sharded_protocol_gloo_world2(chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

@@ -134,10 +134,16 @@ def test_full_cfg3_one_step_sampled_columns():
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("nshards", [2, 3])
-def test_row_sharded_protocol_emulated(precision, nshards):
-    """The NCCL row-sharding protocol (one all-gather per iteration), run for
-    all shards in one process, equals the unsharded solve."""
+@pytest.mark.parametrize("chunks", [None, "3"])
+def test_row_sharded_protocol_emulated(precision, nshards, chunks, monkeypatch):
+    """The NCCL row-sharding protocol (one all-gather per iteration, or the
+    exchange in column chunks on a second stream overlapping the next chunk's
+    main kernel), run for all shards in one process, equals the unsharded
+    solve."""
     from paper_2201_00730_b200.distributed import shard_rows
+
+    if chunks is not None:
+        monkeypatch.setenv("UOT_SHARD_CHUNKS", chunks)
 
     c = S.cfg3_inputs(n=1536, m=1280, seed=11)
     rows = shard_rows(len(c.x), nshards)
@@ -284,12 +290,17 @@ def test_h_rejects_berg():
                            variant="h", cost="power", precision="fp64", ent1="berg", ent2="kl")
 
 
-def test_row_sharded_real_nccl_single_rank():
+@pytest.mark.parametrize("chunks", [None, "4"])
+def test_row_sharded_real_nccl_single_rank(chunks, monkeypatch):
     """The real NCCL branch of the row-sharded path (communicator built in the
     extension from a unique id broadcast by torch.distributed, ncclAllGather
-    per iteration, the scalar all-gather at the end) with one rank: equals
+    per iteration -- or grouped ncclSend / ncclRecv per column chunk on a
+    second stream --, the scalar all-gather at the end) with one rank: equals
     the unsharded solve.  Multi-rank runs need more than one GPU."""
     import os
+
+    if chunks is not None:
+        monkeypatch.setenv("UOT_SHARD_CHUNKS", chunks)
 
     import torch.distributed as dist
 
