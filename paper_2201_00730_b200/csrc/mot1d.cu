@@ -52,7 +52,7 @@ constexpr int BT = UOT_BT;  // threads of the bucket CTAs
 #define UOT_BT2 256
 #endif
 constexpr int BT2 = UOT_BT2;  // threads of the cost-increment bucket CTAs (mot_bucket)
-constexpr int KMAX = 16;          // cluster size limit (non-portable clusters)
+constexpr int KMAX = 32;          // lists per problem (16-CTA clusters of two lists each)
 constexpr int ST = 1024;          // threads of the per-problem splitter CTA
 constexpr int SMAX = 192;         // buckets per problem
 
@@ -635,8 +635,8 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
       A.scal[b * 4 + 1] = mnm;  // common total (min)
       bad_s = bad && A.done != nullptr;
     }
-    if (lane <= K) rb[lane] = lane * SS;
   }
+  for (int i = threadIdx.x; i <= K; i += ST) rb[i] = i * SS;
   int* sp = A.split + (long)b * (S + 1) * K;
   if (S == 1) {
     for (int q = threadIdx.x; q < K; q += ST) {
@@ -1391,6 +1391,14 @@ struct Swz {
   }
   // global row (16-byte aligned, nq valid entries) -> swizzled shared row, async
   __device__ static __forceinline__ void fill(double* srow, const double* grow, int nq) {
+    if ((reinterpret_cast<uintptr_t>(grow) & 15) != 0) {  // odd row stride: 8-byte copies
+      for (int i = threadIdx.x; i < MT * EPT; i += MT) {
+        const int t = i / EPT, e = i - t * EPT;
+        double* dst = reinterpret_cast<double*>(at(srow, t, e >> 1)) + (e & 1);
+        *dst = i < nq ? grow[i] : 0.0;
+      }
+      return;
+    }
     for (int j = threadIdx.x; j < MT * PAIRS; j += MT) {
       const int t = j / PAIRS, c = j - t * PAIRS;
       const int rem = nq - 2 * j;
@@ -1403,6 +1411,13 @@ struct Swz {
   }
   // swizzled shared row -> global row (coalesced)
   __device__ static __forceinline__ void drain(const double* srow, double* grow, int nq) {
+    if ((reinterpret_cast<uintptr_t>(grow) & 15) != 0) {
+      for (int i = threadIdx.x; i < nq; i += MT) {
+        const int t = i / EPT, e = i - t * EPT;
+        grow[i] = reinterpret_cast<const double*>(at(srow, t, e >> 1))[e & 1];
+      }
+      return;
+    }
     for (int j = threadIdx.x; j < MT * PAIRS && 2 * j < nq; j += MT) {
       const int t = j / PAIRS, c = j - t * PAIRS;
       const double2 v = *at(srow, t, c);
@@ -1555,10 +1570,12 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   __shared__ int iscr[MNW];
   __shared__ double vscr[MNW];
   const int c = (int)cl.block_rank();
-  const int qa = 2 * c, qb = 2 * c + 1;
   const int b = blockIdx.y;
   const int K = A.k, n = A.n;
-  const int na = list_len(A, qa), nb = list_len(A, qb);
+  const int qa = 2 * c;
+  const bool hasB = 2 * c + 1 < K;  // odd K: the last CTA holds one list
+  const int qb = hasB ? 2 * c + 1 : qa;
+  const int na = list_len(A, qa), nb = hasB ? list_len(A, qb) : 0;
   const int tid = threadIdx.x, i0 = tid * EPT;
   int parity = 0;
   bops::Ping<RBUF> ping{red, 0};
@@ -1628,6 +1645,8 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   const double rqa = A.omega[qa] * A.rho, rqb = A.omega[qb] * A.rho;
   const double irqa = 1.0 / rqa, irqb = 1.0 / rqb;
   const double lama = A.lam[(long)b * K + qa], lamb = A.lam[(long)b * K + qb];
+  // (without a list B, qb aliases qa: its rows are empty (nb = 0), its
+  // sums zero, its slot past lane K - 1 never read, and nothing is stored)
   // gap sums (barycenter.py:376-381), plan cost by complementary slackness,
   // KL terms, masses, second moment of d under the current tilt (its first
   // moment is the gap term); shift bounds.  One block reduction per list
@@ -1687,7 +1706,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
     }
   }
   bops::block_red<MNW, 6, 2>(acc, mxs, ping.next());
-  const double cqb = acc[0] / acc[3];
+  const double cqb = hasB ? acc[0] / acc[3] : 0.0;
   const double csb[4] = {acc[0], acc[1] + rqb * (acc[2] - acc[3] + acc[4]), cqb,
                          fmax(acc[5] / acc[3] - cqb * cqb, 0.0) / rqb};
   const double mass_b = acc[4];
@@ -1830,8 +1849,10 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   if (tid == 0) {
     A.lse[((long)b * K + qa) * 2 + 0] = m2[0];
     A.lse[((long)b * K + qa) * 2 + 1] = qka;
-    A.lse[((long)b * K + qb) * 2 + 0] = m2[1];
-    A.lse[((long)b * K + qb) * 2 + 1] = qkb;
+    if (hasB) {
+      A.lse[((long)b * K + qb) * 2 + 0] = m2[1];
+      A.lse[((long)b * K + qb) * 2 + 1] = qkb;
+    }
   }
   Swz<EPT>::drain(fB, A.f + baseb, nb);
   MOT_STAMP(5);
@@ -1845,18 +1866,57 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
     const double lam1b = rqb * qkb - (rqb / ex[2]) * ex[0];
     if (tid == 0) {
       A.lam[(long)b * K + qa] = lam1a;
-      A.lam[(long)b * K + qb] = lam1b;
+      if (hasB) A.lam[(long)b * K + qb] = lam1b;
       if (c == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
     }
     const double sca = exp(m2[0] - lam1a * irqa), scb = exp(m2[1] - lam1b * irqb);
 #pragma unroll
     for (int e = 0; e < EPT; ++e) tv[e] *= sca;
     tilt_tail<EPT>(A, b, qa, na, tv, ping.next(), iscr, vscr, nullptr, false);
-    tilt_tail_smem<EPT>(A, b, qb, nb, rB, scb, ping.next(), iscr, vscr);
+    if (hasB) tilt_tail_smem<EPT>(A, b, qb, nb, rB, scb, ping.next(), iscr, vscr);
   }
   MOT_STAMP(6);
   cl.sync();  // slots stay valid until every CTA read them
   MOT_STAMP(7);
+}
+
+// Balanced sweep (solve_mot_1d, mode 1): the duals are prefix sums of the
+// cost increments, f_1[0] = Cc(first tuple), f_k[0] = 0 (barycenter.py:206-229);
+// no cross-list reduction, so one plain CTA per list (any K).
+template <int EPT>
+__global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
+  __shared__ double scr[32];
+  __shared__ double cc0_s;
+  const int q = blockIdx.x, b = blockIdx.y;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  const long base = ((long)b * K + q) * n;
+  double rv[EPT];
+  load_run<EPT>(A.dcc + base, threadIdx.x * EPT, nq, rv);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double c = 0.0;
+    if (q == 0) {
+      const double x0 = lane < K ? A.x[((long)b * K + lane) * n] : 0.0;
+      const double om = lane < K ? A.omega[lane] : 0.0;
+      const double bb = warp_sum(om * x0);
+      c = warp_sum(om * ((x0 - bb) * (x0 - bb)));
+    }
+    if (lane == 0) cc0_s = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) rv[0] = 0.0;  // dcc[0] is not an event
+  double loc = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    loc += rv[e];
+    rv[e] = loc;
+  }
+  double tot;
+  const double off = bscan1(loc, tot, scr) + cc0_s;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) rv[e] += off;
+  store_run<EPT>(A.out_f + base, threadIdx.x * EPT, nq, rv);
 }
 
 // Final translation by the optimal zero-sum lambda (barycenter.py:413-414),
@@ -2137,6 +2197,7 @@ MotPlan plan_for(int k, int n) {
   // (K SS <= 8192 keeps mot_split's sample merge in shared memory)
   p.SS = (p.S > 1) ? std::max(1, std::min({16 * p.S, n - 1, 8192 / k})) : 1;
   p.ept = ept_for(n);
+  if (k > 16 && p.ept == 1) p.ept = 2;  // mot_update2 needs whole 16-byte pairs
   p.cap = (int)std::min(bucket_bound(k, std::max(n - 1, 0), p.S, p.SS), 60000L);
   p.tilt_smem = sizeof(double) * (size_t)n;
   p.split_smem = (sizeof(double) + 3 * sizeof(uint16_t)) * (size_t)k * p.SS;
@@ -2152,9 +2213,14 @@ bool env_flag(const char* name) {
   return e != nullptr && e[0] == '1';
 }
 
+// Two lists per CTA (mot_update2, EPT 2..16): whenever K > 16 (clusters of
+// up to 16 CTAs), and by default for even K <= 16 with 16-byte rows (the
+// faster choice at cfg5 scale); UOT_MOT_UPDATE1=1 forces the one-list kernel
+// where it applies (K <= 16).
 bool use_update2(const MotArgs& a) {
-  return !env_flag("UOT_MOT_UPDATE1") && a.mode == 0 && a.k % 2 == 0 && a.k / 2 <= 8 &&
-         a.n % 2 == 0;
+  if (a.mode != 0) return false;
+  if (a.k > 16) return true;
+  return !env_flag("UOT_MOT_UPDATE1") && a.k % 2 == 0 && a.n % 2 == 0;
 }
 
 template <class Kern>
@@ -2204,11 +2270,20 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
     mot_plan<false, true><<<dim3(p.S, a.batch), BT, p.plan_smem, st>>>(a);
     UOT_CHECK_LAUNCH();
   }
-  if constexpr (EPT == 8 || EPT == 16) {
+  if (a.mode == 1) {
+    mot_duals<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
+    UOT_CHECK_LAUNCH();
+    return UOT_OK;
+  }
+  if constexpr (EPT >= 2 && EPT <= 16) {
     if (use_update2(a)) {
-      UOT_TRY(launch_cluster(mot_update2<EPT>, a.k / 2, a.batch, upd2_smem<EPT>(), st, a));
+      UOT_TRY(launch_cluster(mot_update2<EPT>, (a.k + 1) / 2, a.batch, upd2_smem<EPT>(), st, a));
       return UOT_OK;
     }
+  }
+  if (a.k > 16) {
+    set_error("barycenter FW with more than 16 inputs needs lists of at most %d atoms", 16 * MT);
+    return UOT_INVALID;
   }
   UOT_TRY(launch_cluster(mot_update<EPT>, a.k, a.batch,
                          StageRun<EPT>::ON ? 2 * StageRun<EPT>::BYTES : 0, st, a));
@@ -2356,7 +2431,7 @@ int check_sizes(int batch, int k, int n) {
     return UOT_INVALID;
   }
   if (k > KMAX) {
-    set_error("at most %d input measures per barycenter on the cluster path", KMAX);
+    set_error("at most %d input measures per problem", KMAX);
     return UOT_INVALID;
   }
   if (ept_for(n) < 0) {
@@ -2429,6 +2504,10 @@ extern "C" int uot_bary_run(const uot_bary_desc* d, void* workspace, size_t work
   UOT_TRY(check_sizes(d->batch, d->k, d->n));
   if (!(d->rho > 0.0) || d->max_iters < 1) {
     set_error("uot_bary_run: need rho > 0 and max_iters >= 1");
+    return UOT_INVALID;
+  }
+  if (d->k > 16 && plan_for(d->k, d->n).ept > 16) {
+    set_error("barycenter FW with more than 16 inputs needs lists of at most %d atoms", 16 * MT);
     return UOT_INVALID;
   }
   MotPlan p = plan_for(d->k, d->n);

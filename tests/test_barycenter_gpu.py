@@ -201,15 +201,20 @@ def test_sweep_variants_agree(monkeypatch, env):
     xs[2, 5] = xs[2, 4]              # two identical lists: cross-list ties
     ws[2, 5] = ws[2, 4]
     w = np.full(16, 1 / 16)
-    base = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, "linesearch", trace_support=True)
+    # the two update kernels associate their block / cluster sums differently:
+    # compared on harmonic steps (a fixed gamma schedule); the merge fallback
+    # orders the same keys, compared on line-search runs
+    step = "harmonic" if env == "UOT_MOT_UPDATE1" else "linesearch"
+    base = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
     monkeypatch.setenv(env, "1")
-    alt = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, "linesearch", trace_support=True)
+    alt = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
     monkeypatch.delenv(env)
     assert (D.to_np(base.status) == 0).all() and (D.to_np(alt.status) == 0).all()
     np.testing.assert_array_equal(D.to_np(base.supp_hash), D.to_np(alt.supp_hash))
     f0, f1 = D.to_np(base.f), D.to_np(alt.f)
-    assert np.abs(f0 - f1).max() <= 1e-12 * np.abs(f0).max()
-    np.testing.assert_allclose(D.to_np(alt.h0), D.to_np(base.h0), rtol=1e-13)
+    tol = 1e-14 if env == "UOT_MOT_NOBIN" else 1e-13
+    assert np.abs(f0 - f1).max() <= tol * np.abs(f0).max()
+    np.testing.assert_allclose(D.to_np(alt.h0), D.to_np(base.h0), rtol=max(tol, 1e-13))
     c = D.to_np(base.count)
     for p in range(3):
         np.testing.assert_array_equal(D.to_np(alt.idx[p, :c[p]]), D.to_np(base.idx[p, :c[p]]))
@@ -223,3 +228,46 @@ def test_sweep_variants_agree(monkeypatch, env):
         monkeypatch.delenv(env)
         c0 = int(r0[3][0].item())
         np.testing.assert_array_equal(D.to_np(r0[1][0, :c0]), D.to_np(r1[1][0, :c0]))
+
+
+# ---------------------------------------------------------------------------
+# More than 16 input measures (the reference has no limit, barycenter.py:169-233):
+# 16 < K <= 32 runs on clusters of ceil(K/2) CTAs holding two lists each
+# (odd K: the last CTA holds one); the balanced sweep needs no cluster at all.
+@pytest.mark.parametrize("k,n", [(21, 300), (32, 1000), (24, 129)])
+def test_barycenter_many_inputs_vs_oracle(k, n):
+    xs, ws = S.cfg5_batch(batch=2, k=k, n=n, count=2)
+    w = np.full(k, 1.0 / k)
+    rh = P.fw_barycenter_batched(xs, ws, w, 1.0, 10, "harmonic")
+    assert (D.to_np(rh.status) == 0).all()
+    for p in range(2):
+        out = O.fw_barycenter_fixed(list(xs[p]), list(ws[p]), w, 1.0, 10, step="harmonic")
+        np.testing.assert_allclose(D.to_np(rh.h0[p]), out["h0"], rtol=1e-9)
+        f = D.to_np(rh.f[p])
+        scale = max(np.abs(v).max() for v in out["pots"])
+        assert max(np.abs(f[q] - out["pots"][q]).max() for q in range(k)) <= 1e-9 * scale
+        c = int(rh.count[p].item())
+        np.testing.assert_array_equal(D.to_np(rh.idx[p, :c]), out["plan"][0])
+    rl = P.fw_barycenter_batched(xs, ws, w, 1.0, 6, "linesearch")
+    out = O.fw_barycenter_fixed(list(xs[0]), list(ws[0]), w, 1.0, 6)
+    np.testing.assert_allclose(D.to_np(rl.h0[0]), out["h0"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("k,n", [(24, 300), (32, 2049)])
+def test_mot_many_inputs_vs_oracle(k, n):
+    xs, ws = S.cfg5_batch(batch=1, k=k, n=n, count=1)
+    ws = ws / ws.sum(axis=2, keepdims=True)
+    w = np.full(k, 1.0 / k)
+    f, idx, mass, count, st = P.solve_mot_1d_batched(xs, ws, w)
+    ii, mm, pots = O.solve_mot_1d(list(xs[0]), list(ws[0]), w)
+    c = int(count[0].item())
+    np.testing.assert_array_equal(D.to_np(idx[0, :c]), ii)
+    np.testing.assert_allclose(D.to_np(mass[0, :c]), mm, rtol=0, atol=1e-13)
+    fd = D.to_np(f[0])
+    assert max(np.abs(fd[q] - pots[q]).max() for q in range(k)) <= 1e-10
+
+
+def test_too_many_inputs_raise_like_a_limit():
+    xs, ws = S.cfg5_batch(batch=1, k=33, n=64, count=1)
+    with pytest.raises(ValueError):
+        P.fw_barycenter_batched(xs, ws, np.full(33, 1 / 33), 1.0, 2, "harmonic")

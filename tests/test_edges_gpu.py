@@ -124,7 +124,8 @@ def test_mot_max_list_length_and_k2():
 def test_mot_limits_raise():
     one = P.DiscreteMeasure([0.5], [1.0])
     with pytest.raises(ValueError):
-        P.solve_mot_1d([one] * 17, np.full(17, 1 / 17))  # K > 16 (cluster size)
+        P.solve_mot_1d([one] * 33, np.full(33, 1 / 33))  # K > 32 (two lists per CTA, 16-CTA clusters)
+    P.solve_mot_1d([one] * 17, np.full(17, 1 / 17))  # 16 < K <= 32 runs
     big = P.DiscreteMeasure(np.linspace(0, 1, 16385), np.full(16385, 1 / 16385))
     with pytest.raises(ValueError):
         P.solve_mot_1d([big, big], np.array([0.5, 0.5]))
