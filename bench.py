@@ -447,8 +447,24 @@ def run_cfg2(rank, world, dev, peaks):
     assert int(r.status.max().item()) == 0
     it_s = iters / (ms * 1e-3)
     gbs = CFG2_BYTES_PER_ITER * it_s / 1e9
+    # the bound that applies (the state is on chip): SM issue slots, from the
+    # committed instruction count of the same workload (profiles/r2_cfg2_issue.json)
+    issue = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_cfg2_issue.json")) as fh:
+            ipi = json.load(fh)["warp_instr_per_problem_iteration"]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_i = sms * 4 * 1.965e9 / 1e9  # G warp-instructions/s at the max SM clock
+        ach_i = ipi * (hi - lo) * it_s / 1e9
+        issue = {"bound": "issue", "achieved": ach_i, "peak": peak_i, "unit": "Gwarp-instr/s",
+                 "frac": ach_i / peak_i,
+                 "work_per_iteration": f"{ipi} warp-instructions per problem-iteration (ncu, "
+                                       "500 line-search iterations)"}
+    except (OSError, KeyError, ValueError):
+        pass
     return {"workload": "cfg2: batched 1-D FW, B=4096, N=M=1024, KL rho=1, |x-y|^2, fp64, "
                         "500 line-search iterations (fixed count)",
+            "issue": issue,
             "value": it_s, "unit": "iter/s (batched FW iterations over all 4096 problems)",
             "ms_total": ms, "dtype": "f64", "scaling": "weak-by-problem" if world > 1 else None,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -718,7 +734,7 @@ def compact(entry):
             "mean_active_atoms", "res_f", "res_g")
     out = {k: entry[k] for k in keep if k in entry}
     for sub in ("roofline", "tensor", "issue"):
-        if sub in entry:
+        if entry.get(sub):
             out[sub] = {k: v for k, v in entry[sub].items()
                         if k in ("bound", "achieved", "peak", "unit", "frac", "achieved_tflops",
                                  "peak_tflops", "peak_sustained_tflops", "frac_sustained",
