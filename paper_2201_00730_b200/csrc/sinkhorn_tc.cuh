@@ -500,20 +500,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) sk_main_tc(MainArgs<float> A, i
       tc::mbar_wait(&dfull[blk], i & 1);
       if (i == 0) TC_STAMP(2);
       tc::fence_after();
-      uint32_t v0[32], v1[32];
+      uint32_t v0[32], v1[32], w0[32], w1[32];
       tc::tmem_ld32(tl, v0);
       tc::tmem_ld32(tl + 32, v1);
       tc::wait_ld();
+      // the second half is read while the first half's exponentials run
+      tc::tmem_ld32(tl + 64, w0);
+      tc::tmem_ld32(tl + 96, w1);
       chunk(v0, v1);
-      tc::tmem_ld32(tl + 64, v0);
-      tc::tmem_ld32(tl + 96, v1);
       tc::wait_ld();
       // No TMEM read is outstanding, so a relaxed arrive suffices (a
       // release.cluster arrive per warp and tile costs ~1.5x the kernel time).
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_remote_relaxed(dempty_leader);
-      chunk(v0, v1);
+      chunk(w0, w1);
     }
     TC_STAMP(3);
     if (o < A.nout) {
