@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "../../include/uot_b200.h"
 #include "blockops.cuh"
@@ -96,6 +97,7 @@ struct MotArgs {
   double* samp;           // [B][K][SS] regular samples (values)
   int* sampt;             // [B][K][SS] (indices)
   int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
+  int b0;                 // first problem of this launch (problem groups on streams)
   int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1, parity tests)
   // parity / trace mode (optional)
   const double* step_in;  // [B][max_iters] replayed gamma_t
@@ -311,7 +313,7 @@ template <int EPT>
 __global__ void __launch_bounds__(MT) mot_lse(MotArgs A) {
   __shared__ __align__(16) double red[2 * MBUF];
   __shared__ double tab[32];
-  const int q = blockIdx.x, b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   bops::load_exp_table(tab);
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(MT) mot_tilt(MotArgs A) {
   __shared__ double tab[32];
   __shared__ int iscr[MNW];
   __shared__ double vscr[MNW];
-  const int q = blockIdx.x, b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   if (A.done != nullptr && A.done[b]) return;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(ST) mot_split(MotArgs A) {
   __shared__ int splc[SMAX + 1], splr[SMAX + 1];
   __shared__ int rb[KMAX + 1];
   __shared__ int bad_s;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x + A.b0;
   const int K = A.k, n = A.n, S = A.S, SS = A.SS, KSS = K * SS;
   if (A.done != nullptr && A.done[b]) return;
   if (threadIdx.x < 32) {
@@ -1026,7 +1028,7 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   __shared__ double bstart_s;
   __shared__ int done_s;
   BKT_STAMP(0);
-  const int s = blockIdx.x, b = blockIdx.y;
+  const int s = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n, cap = A.cap;
   const int* sp = A.split + (long)b * (A.S + 1) * K;
   if (threadIdx.x < 32) {  // lane q: list q's range, offsets by a warp scan (one latency)
@@ -1141,7 +1143,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   __shared__ int iscr[MNW];
   __shared__ double vscr[MNW];
   const int q = (int)cl.block_rank();
-  const int b = blockIdx.y;
+  const int b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   int parity = 0;
@@ -1570,7 +1572,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   __shared__ int iscr[MNW];
   __shared__ double vscr[MNW];
   const int c = (int)cl.block_rank();
-  const int b = blockIdx.y;
+  const int b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int qa = 2 * c;
   const bool hasB = 2 * c + 1 < K;  // odd K: the last CTA holds one list
@@ -1887,7 +1889,7 @@ template <int EPT>
 __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
   __shared__ double scr[32];
   __shared__ double cc0_s;
-  const int q = blockIdx.x, b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   const long base = ((long)b * K + q) * n;
@@ -1923,7 +1925,7 @@ __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
 // from the log-sum-exps the last update stored for the final iterate.
 template <int EPT>
 __global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
-  const int q = blockIdx.x, b = blockIdx.y;
+  const int q = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   const int nq = list_len(A, q);
   const long base = ((long)b * K + q) * n;
@@ -1962,7 +1964,7 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
   __shared__ int lo_s[KMAX + 1], cnt_s[KMAX + 1];
   __shared__ int scan_s[BT / 32];
   __shared__ int kept_s;
-  const int s = blockIdx.x, b = blockIdx.y;
+  const int s = blockIdx.x, b = blockIdx.y + A.b0;
   const int K = A.k, n = A.n;
   double* key;
   int* code;
@@ -2302,23 +2304,64 @@ int run_plan(const MotArgs& a, const MotPlan& p, cudaStream_t st) {
   return UOT_OK;
 }
 
+// Problem groups: the batch runs as G independent groups on their own
+// streams (their iterations interleave on the device, so one group's bucket
+// sorts fill the SMs another group's last update wave leaves idle).
+int mot_groups(int batch) {
+  const char* e = getenv("UOT_MOT_GROUPS");
+  const int g = e ? atoi(e) : std::min(8, std::max(1, batch / 8));
+  return std::max(1, std::min(g, std::min(batch, 16)));
+}
+
 template <int EPT>
 int run_all(MotArgs a, const MotPlan& p, cudaStream_t st, bool fw) {
   if (fw) {
-    mot_lse<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
-    UOT_CHECK_LAUNCH();
-    for (int t = 0; t < a.max_iters; ++t) {
-      a.t = t;
-      UOT_TRY(run_sweep<EPT>(a, p, st, t == 0));
+    const int G = mot_groups(a.batch);
+    std::vector<MotArgs> ga(G, a);
+    std::vector<cudaStream_t> gs(G, st);
+    cudaEvent_t fork = nullptr;
+    std::vector<cudaEvent_t> join(G, nullptr);
+    if (G > 1) {
+      UOT_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      UOT_CUDA_TRY(cudaEventRecord(fork, st));
+      for (int g = 0; g < G; ++g) {
+        ga[g].b0 = (int)((long)a.batch * g / G);
+        ga[g].batch = (int)((long)a.batch * (g + 1) / G) - ga[g].b0;
+        UOT_CUDA_TRY(cudaStreamCreateWithFlags(&gs[g], cudaStreamNonBlocking));
+        UOT_CUDA_TRY(cudaEventCreateWithFlags(&join[g], cudaEventDisableTiming));
+        UOT_CUDA_TRY(cudaStreamWaitEvent(gs[g], fork, 0));
+      }
     }
-    // plan of the last recorded iteration: its breakpoints are still in A.
-    // (Converged problems stopped before updating; the others updated f
-    // after the last oracle call, exactly like the reference loop.)
-    MotArgs ap = a;
-    ap.done = nullptr;
-    UOT_TRY(run_plan(ap, p, st));
-    mot_finalize<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
-    UOT_CHECK_LAUNCH();
+    for (int g = 0; g < G; ++g) {
+      mot_lse<EPT><<<dim3(a.k, ga[g].batch), MT, 0, gs[g]>>>(ga[g]);
+      UOT_CHECK_LAUNCH();
+    }
+    for (int t = 0; t < a.max_iters; ++t)
+      for (int g = 0; g < G; ++g) {
+        ga[g].t = t;
+        UOT_TRY(run_sweep<EPT>(ga[g], p, gs[g], t == 0));
+      }
+    for (int g = 0; g < G; ++g) {
+      // plan of the last recorded iteration: its breakpoints are still in A.
+      // (Converged problems stopped before updating; the others updated f
+      // after the last oracle call, exactly like the reference loop.)
+      MotArgs ap = ga[g];
+      ap.done = nullptr;
+      UOT_TRY(run_plan(ap, p, gs[g]));
+      mot_finalize<EPT><<<dim3(a.k, ga[g].batch), MT, 0, gs[g]>>>(ga[g]);
+      UOT_CHECK_LAUNCH();
+    }
+    if (G > 1) {
+      for (int g = 0; g < G; ++g) {
+        UOT_CUDA_TRY(cudaEventRecord(join[g], gs[g]));
+        UOT_CUDA_TRY(cudaStreamWaitEvent(st, join[g], 0));
+      }
+      for (int g = 0; g < G; ++g) {
+        cudaStreamDestroy(gs[g]);  // released once its work completes
+        cudaEventDestroy(join[g]);
+      }
+      cudaEventDestroy(fork);
+    }
   } else {
     a.mode = 1;
     UOT_TRY(run_sweep<EPT>(a, p, st, true));
