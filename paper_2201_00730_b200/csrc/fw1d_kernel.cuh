@@ -1056,8 +1056,10 @@ inline int ept_for(int nm) {
   return -1;
 }
 
-// Large-problem path: elements per thread at FW_THREADS_BIG threads.
-constexpr int FW_EPT_BIG_MAX = 16;  // n, m <= 16384 per problem
+// Large-problem path: elements per thread at FW_THREADS_BIG threads (EPT 8 /
+// 16 in fw1d_big.cu; 32 -- arrays beyond the register budget live in local
+// memory: a correctness path -- in fw1d_huge.cu).
+constexpr int FW_EPT_BIG_MAX = 32;  // n, m <= 32768 per problem
 inline int ept_for_big(int nm) {
   const int per = (nm + FW_THREADS_BIG - 1) / FW_THREADS_BIG;
   for (int e = 8; e <= FW_EPT_BIG_MAX; e *= 2)
@@ -1097,14 +1099,28 @@ int launch_fw_big(const FwArgs& a, int batch, cudaStream_t st, int ept) {
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }
+template <bool PW, int PK>
+int launch_fw_huge(const FwArgs& a, int batch, cudaStream_t st, int ept) {
+  (void)ept;  // 32
+  fw1d_kernel<32, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
 #define UOT_FW_BIG(EXT, PW)                                                          \
   EXT template int launch_fw_big<PW, 0>(const FwArgs&, int, cudaStream_t, int);     \
   EXT template int launch_fw_big<PW, 1>(const FwArgs&, int, cudaStream_t, int);     \
   EXT template int launch_fw_big<PW, 2>(const FwArgs&, int, cudaStream_t, int);     \
   EXT template int launch_fw_big<PW, 3>(const FwArgs&, int, cudaStream_t, int);
+#define UOT_FW_HUGE(EXT, PW)                                                         \
+  EXT template int launch_fw_huge<PW, 0>(const FwArgs&, int, cudaStream_t, int);    \
+  EXT template int launch_fw_huge<PW, 1>(const FwArgs&, int, cudaStream_t, int);    \
+  EXT template int launch_fw_huge<PW, 2>(const FwArgs&, int, cudaStream_t, int);    \
+  EXT template int launch_fw_huge<PW, 3>(const FwArgs&, int, cudaStream_t, int);
 #ifndef UOT_FW_BIG_TU
 UOT_FW_BIG(extern, false)
 UOT_FW_BIG(extern, true)
+UOT_FW_HUGE(extern, false)
+UOT_FW_HUGE(extern, true)
 #endif
 
 template <bool PW>
@@ -1137,7 +1153,9 @@ int launch_fw_impl(const FwArgs& a0, int batch, cudaStream_t st) {
   };
   auto by_ept = [&](auto pk) -> int {
     constexpr int PK = decltype(pk)::value;
-    if (big) return launch_fw_big<PW, PK>(a, batch, st, eptb);
+    if (big)
+      return eptb <= 16 ? launch_fw_big<PW, PK>(a, batch, st, eptb)
+                        : launch_fw_huge<PW, PK>(a, batch, st, eptb);
     switch (ept) {
       case 1: return go(fw1d_kernel<1, PK, PW>, FW_THREADS, smem);
       case 2: return go(fw1d_kernel<2, PK, PW>, FW_THREADS, smem);

@@ -130,3 +130,26 @@ def test_large_pairwise_replay():
     assert (hs == z["pfw_hash"]).all() and (nz == z["pfw_nnz"]).all()
     np.testing.assert_array_equal(D.to_np(r.natoms[0]), z["pfw_natoms"])
     assert rel_err(D.to_np(r.f[0]), D.to_np(r.g[0]), z["pfw_f"], z["pfw_g"]) <= TOL
+
+
+def test_huge_ot1d_and_fw_vs_oracle():
+    """n, m > 16384 (up to 32768): the EPT-32 instantiation of the large kernel
+    (per-thread arrays past the register budget in local memory).  The oracle is
+    pinned to the reference (test_oracle_golden.py)."""
+    n, m = 30000, 24577
+    x, y, wa, wb = O.large_ot_inputs(n, m, 91)
+    f, g, ei, ej, em, count, status = P.solve_ot_1d_batched(x, y, wa, wb, 2.0)
+    assert int(status[0].item()) == 0
+    ii, jj, mm, fo, go = O.solve_ot_1d(x, y, wa, wb, 2.0)
+    c = int(count[0].item())
+    np.testing.assert_array_equal(D.to_np(ei[0, :c]), ii)
+    np.testing.assert_array_equal(D.to_np(ej[0, :c]), jj)
+    np.testing.assert_allclose(D.to_np(em[0, :c]), mm, rtol=0, atol=1e-13)
+    assert rel_err(D.to_np(f[0]), D.to_np(g[0]), fo, go) <= TOL
+    # FW on cfg2-style inputs (sorted uniform supports, Exp(1) weights); the
+    # mixture generator's near-zero tails make near-ties that flip supports
+    x2, y2, a2, b2 = S.cfg2_batch(batch=1, n=20000, m=18000, seed=77)
+    r = P.fw_solve_batched(x2, y2, a2, b2, 1.0, 1.0, 2.0, 6, "harmonic")
+    out = O.fw_fixed(x2[0], y2[0], a2[0], b2[0], 1.0, 1.0, 6, step="harmonic")
+    assert rel_err(D.to_np(r.f[0]), D.to_np(r.g[0]), out["f"], out["g"]) <= 1e-9
+    np.testing.assert_allclose(D.to_np(r.h0[0]), out["h0"], rtol=1e-9)
