@@ -398,6 +398,36 @@ int uot_mot_certify(int32_t batch, int32_t k, int32_t n, const int32_t* lens, co
                     const double* a, const double* omega_host, const double* f,
                     const int32_t* idx, const double* mass, const int32_t* count, double* out,
                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Custom tuple costs: `solve_mot_1d(inputs, costfn=...)`, `plan_cost`,
+ * `dual_feasibility_exhaustive`, `mot_certificate(..., costfn)`
+ * (src/barycenter.py:169-233, 236-295).  The sweep order depends only on the
+ * weights, so a caller-supplied costfn (a host callable) is evaluated by the
+ * caller on the tuples the device returns:
+ *   1. uot_mot1d_states: every state the sweep visits, zero-mass ones
+ *      included, idx [batch][K*(n-1)+1][K], mass, count = 1 + sum_q (len_q-1)
+ *      (barycenter.py:209-229: the initial tuple, then one per advance);
+ *      status as uot_mot1d_batched (1 = unequal masses).  Workspace of
+ *      uot_mot1d_workspace_size.
+ *   2. the caller evaluates cost[b][t] = costfn(points of state t);
+ *   3. uot_mot1d_cost_duals: f [batch][K][n] with f_1[0] = cost[0], f_k[0] = 0
+ *      and f_p[i] = f_p[i-1] + cost[t] - cost[t-1] for the state t advancing
+ *      list p to i (:224-228).
+ * uot_mot_certify_costs: uot_mot_certify with ecost [batch][K*(n-1)+1] =
+ * costfn at the plan entries and, for grids of at most 1e5 tuples, gcost
+ * [batch][grid] = costfn over the index grid in C order (NULL skips the
+ * exhaustive sweep). */
+int uot_mot1d_states(int32_t batch, int32_t k, int32_t n, const int32_t* lens, const double* a,
+                     int32_t* idx, double* mass, int32_t* count, int32_t* status,
+                     void* workspace, size_t workspace_bytes, void* stream);
+int uot_mot1d_cost_duals(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                         const int32_t* idx, const int32_t* count, const double* cost, double* f,
+                         void* workspace, size_t workspace_bytes, void* stream);
+int uot_mot_certify_costs(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                          const double* a, const double* f, const int32_t* idx,
+                          const double* mass, const int32_t* count, const double* ecost,
+                          const double* gcost, double* out, void* workspace,
+                          size_t workspace_bytes, void* stream);
 int uot_bary_workspace_size(const uot_bary_desc* desc, size_t* bytes);
 int uot_bary_run(const uot_bary_desc* desc, void* workspace, size_t workspace_bytes,
                  void* stream);

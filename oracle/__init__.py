@@ -784,6 +784,43 @@ def solve_mot_1d(xs, ws, w):
     return idx[:e].copy(), mass[:e].copy(), [pots[off[q]:off[q] + lens[q]].copy() for q in range(k)]
 
 
+def solve_mot_1d_custom(xs, ws, costfn):
+    """barycenter.py:169-233 with a caller costfn (pure-Python restatement of
+    the sweep loop :209-229; small cases only).  Returns (indices, mass,
+    potentials list)."""
+    k = len(xs)
+    last = np.array([len(a) - 1 for a in xs], dtype=np.int64)
+    idx = np.zeros(k, dtype=np.int64)
+    rem = np.array([float(w[0]) for w in ws])
+    pots = [np.zeros(len(a)) for a in xs]
+    cur = np.array([float(x[0]) for x in xs])
+    pots[0][0] = costfn(cur)
+    pot_sum = pots[0][0]
+    ent_i, ent_m = [], []
+    while True:
+        can = idx < last
+        if not can.any():
+            step = float(rem.min())
+            if step > 0:
+                ent_i.append(idx.copy())
+                ent_m.append(step)
+            break
+        p = int(np.argmin(np.where(can, rem, np.inf)))
+        step = float(rem[p])
+        if step > 0:
+            ent_i.append(idx.copy())
+            ent_m.append(step)
+        rem = np.maximum(rem - step, 0.0)
+        idx[p] += 1
+        cur[p] = xs[p][idx[p]]
+        old = pots[p][idx[p] - 1]
+        new = costfn(cur) - (pot_sum - old)
+        pots[p][idx[p]] = new
+        pot_sum += new - old
+        rem[p] = ws[p][idx[p]]
+    return np.array(ent_i, dtype=np.int64).reshape(-1, k), np.array(ent_m), pots
+
+
 def large_ot_inputs(n, m, seed):
     """Seeded balanced 1-D OT inputs for the large-size goldens (test
     fixture generator): sorted uniform supports with a run of duplicated

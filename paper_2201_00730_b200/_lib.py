@@ -78,6 +78,7 @@ EXPORTS = (
     "uot_ot1d_workspace_size", "uot_ot1d_batched", "uot_fw1d_workspace_size", "uot_fw1d_run", "uot_feasibility_1d",
     "uot_feasibility_explicit", "uot_translation",
     "uot_mot1d_workspace_size", "uot_mot1d_batched", "uot_mot_certify", "uot_bary_workspace_size", "uot_bary_run",
+    "uot_mot1d_states", "uot_mot1d_cost_duals", "uot_mot_certify_costs",
     "uot_nccl_unique_id", "uot_nccl_comm_init", "uot_nccl_comm_destroy",
 )
 

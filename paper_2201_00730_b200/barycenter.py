@@ -179,11 +179,90 @@ def solve_mot_1d_batched(x, a, omega, lens=None, stream=None):
     return f, idx, mass, count, status
 
 
+def mot_states_batched(a, lens=None, stream=None):
+    """Every state of the balanced sweep (zero-mass ones included), in sweep
+    order: (idx [B, E, K], mass [B, E], count [B], status [B]) on the device
+    (uot_mot1d_states; src/barycenter.py:209-229 visits them in this order)."""
+    t = D.torch()
+    lib = _lib.load()
+    a = D.to_dev(a, t.float64)
+    B, K, n = a.shape
+    cap = K * (n - 1) + 1
+    idx = D.empty((B, cap, K), t.int32)
+    mass = D.empty((B, cap), t.float64)
+    count = D.empty((B,), t.int32)
+    status = D.empty((B,), t.int32)
+    ln = None if lens is None else np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_mot1d_workspace_size(B, K, n, ctypes.byref(size)))
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_mot1d_states(
+        B, K, n, ln.ctypes.data_as(ctypes.c_void_p) if ln is not None else None, _lib.ptr(a),
+        _lib.ptr(idx), _lib.ptr(mass), _lib.ptr(count), _lib.ptr(status), _lib.ptr(ws),
+        ctypes.c_size_t(size.value), _lib.stream_handle(stream)), "uot_mot1d_states")
+    return idx, mass, count, status
+
+
+def mot_cost_duals_batched(idx, count, cost, k, n, lens=None, stream=None):
+    """Duals of the sweep from caller-evaluated state costs cost [B, E]
+    (uot_mot1d_cost_duals; src/barycenter.py:224-228).  Returns f [B, K, n]."""
+    t = D.torch()
+    lib = _lib.load()
+    idx = D.to_dev(idx, t.int32)
+    count = D.to_dev(count, t.int32)
+    cost = D.to_dev(cost, t.float64)
+    B = idx.shape[0]
+    f = t.zeros((B, k, n), dtype=t.float64, device=idx.device)
+    ln = None if lens is None else np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.uot_mot1d_workspace_size(B, k, n, ctypes.byref(size)))
+    ws = D.workspace(size.value)
+    _lib.check(lib.uot_mot1d_cost_duals(
+        B, k, n, ln.ctypes.data_as(ctypes.c_void_p) if ln is not None else None, _lib.ptr(idx),
+        _lib.ptr(count), _lib.ptr(cost), _lib.ptr(f), _lib.ptr(ws), ctypes.c_size_t(size.value),
+        _lib.stream_handle(stream)), "uot_mot1d_cost_duals")
+    return f
+
+
+def _tuple_costs(inputs, rows, costfn):
+    """costfn on each index tuple (the caller's host callable, evaluated on a
+    length-K point vector exactly as src/barycenter.py:217-227 does)."""
+    pts = [np.asarray(m.points, dtype=np.float64) for m in inputs]
+    out = np.empty(len(rows))
+    cur = np.empty(len(inputs))
+    for t, row in enumerate(rows):
+        for q, i in enumerate(row):
+            cur[q] = pts[q][i]
+        out[t] = float(costfn(cur.copy()))
+    return out
+
+
+def _custom_sweep(inputs, costfn):
+    x, a, _, lens = _pack(inputs)
+    K, n = a.shape[1], a.shape[2]
+    idx, mass, count, status = mot_states_batched(a, lens)
+    D.torch().cuda.current_stream().synchronize()
+    if int(status[0].item()) == 1:
+        raise MassBalanceError("multimarginal sweep needs equal masses")
+    c = int(count[0].item())
+    rows = D.to_np(idx[0, :c]).astype(np.int64)
+    cost = np.zeros((1, idx.shape[1]))
+    cost[0, :c] = _tuple_costs(inputs, rows, costfn)
+    f = mot_cost_duals_batched(idx, count, cost, K, n, lens)
+    fd = D.to_np(f[0])
+    m = D.to_np(mass[0, :c])
+    keep = m > 0.0
+    plan = MultiPlan(rows[keep], m[keep])
+    return plan, MultiDual(tuple(fd[q, :lens[q]] for q in range(K)))
+
+
 def solve_mot_1d(inputs, w=None, costfn=None):
     """Balanced 1-D multimarginal transport (src/barycenter.py:169-233).
 
-    Only the barycentric squared-Euclidean tuple cost runs on the B200 path;
-    a custom ``costfn`` raises."""
+    The barycentric squared-Euclidean cost is fused into the sweep kernels; a
+    custom ``costfn`` (any host callable on a length-K point vector) is
+    evaluated on the tuples of the device sweep (uot_mot1d_states) and the
+    duals are formed from those costs on the device (uot_mot1d_cost_duals)."""
     inputs = tuple(inputs)
     if len(inputs) < 2:
         raise ValueError("need at least two measures")
@@ -191,9 +270,10 @@ def solve_mot_1d(inputs, w=None, costfn=None):
     if float(masses.max() - masses.min()) > MASS_TOL * float(masses.max()):
         raise MassBalanceError(f"multimarginal sweep needs equal masses, got {masses.tolist()}")
     if costfn is not None:
-        from .exceptions import UnsupportedEntropyError
-
-        raise UnsupportedEntropyError("custom tuple costs are not on the B200 path")
+        wf = getattr(costfn, "weights", None)
+        if wf is None:
+            return _custom_sweep(inputs, costfn)
+        w = wf
     if w is None:
         raise ValueError("need barycentric weights when costfn is omitted")
     x, a, _, lens = _pack(inputs)
@@ -243,7 +323,10 @@ def mot_certify_batched(x, a, omega, f, idx, mass, count, lens=None, stream=None
     return out
 
 
-def _certify_inputs(inputs, w, plan, duals):
+def _certify_inputs(inputs, w, plan, duals, costfn=None, grid=True):
+    """uot_mot_certify (barycentric cost, weights w) or, for a custom costfn,
+    uot_mot_certify_costs with costfn evaluated on the plan tuples and (grid)
+    on the whole index grid when it holds at most EXHAUSTIVE_LIMIT tuples."""
     inputs = tuple(inputs)
     x, a, f, lens = _pack(inputs, extra=tuple(duals))
     K, n = x.shape[1], x.shape[2]
@@ -255,21 +338,44 @@ def _certify_inputs(inputs, w, plan, duals):
         raise ValueError("plan has more entries than a monotone sweep can produce")
     idx[0, :e] = plan.indices
     mass[0, :e] = plan.mass
-    out = mot_certify_batched(x, a, w, f, idx, mass, np.array([e], dtype=np.int32), lens)
+    if costfn is None:
+        out = mot_certify_batched(x, a, w, f, idx, mass, np.array([e], dtype=np.int32), lens)
+        return D.to_np(out[0], readonly=False)
+    t = D.torch()
+    lib = _lib.load()
+    ecost = np.zeros((1, cap))
+    ecost[0, :e] = _tuple_costs(inputs, np.asarray(plan.indices, dtype=np.int64), costfn)
+    gsize = int(np.prod([len(m) for m in inputs], dtype=np.float64))
+    gcost = None
+    if grid and gsize <= EXHAUSTIVE_LIMIT:
+        rows = np.array(list(np.ndindex(*[len(m) for m in inputs])), dtype=np.int64)
+        gcost = D.to_dev(_tuple_costs(inputs, rows, costfn)[None], t.float64)
+    ad, fd = D.to_dev(a, t.float64), D.to_dev(f, t.float64)
+    idd, md = D.to_dev(idx, t.int32), D.to_dev(mass, t.float64)
+    cnt = D.to_dev(np.array([e], dtype=np.int32), t.int32)
+    ed = D.to_dev(ecost, t.float64)
+    out = t.zeros((1, 6), dtype=t.float64, device=ad.device)
+    ws = D.workspace(64 * K + 512)
+    _lib.check(lib.uot_mot_certify_costs(
+        1, K, n, lens.ctypes.data_as(ctypes.c_void_p), _lib.ptr(ad), _lib.ptr(fd), _lib.ptr(idd),
+        _lib.ptr(md), _lib.ptr(cnt), _lib.ptr(ed), _lib.ptr(gcost) if gcost is not None else None,
+        _lib.ptr(out), _lib.ptr(ws), ctypes.c_size_t(64 * K + 512), None),
+        "uot_mot_certify_costs")
+    t.cuda.current_stream().synchronize()
     return D.to_np(out[0], readonly=False)
 
 
 def _weights_of(costfn, w):
+    """Barycentric weights of a built-in cost, or None for a custom costfn."""
     if costfn is None:
         if w is None:
             raise ValueError("need barycentric weights when costfn is omitted")
         return np.asarray(w, dtype=np.float64)
-    wf = getattr(costfn, "weights", None)
-    if wf is None:
-        from .exceptions import UnsupportedEntropyError
+    return getattr(costfn, "weights", None)
 
-        raise UnsupportedEntropyError("custom tuple costs are not on the B200 path")
-    return wf
+
+def _custom(costfn, w):
+    return costfn if (costfn is not None and w is None) else None
 
 
 def plan_cost(plan, inputs, costfn):
@@ -277,7 +383,7 @@ def plan_cost(plan, inputs, costfn):
     inputs = tuple(inputs)
     w = _weights_of(costfn, None)
     duals = MultiDual(tuple(np.zeros(len(m)) for m in inputs))
-    return float(_certify_inputs(inputs, w, plan, duals)[0])
+    return float(_certify_inputs(inputs, w, plan, duals, _custom(costfn, w), grid=False)[0])
 
 
 def dual_feasibility_exhaustive(inputs, duals, costfn):
@@ -288,7 +394,7 @@ def dual_feasibility_exhaustive(inputs, duals, costfn):
         raise ValueError("grid too large for the exhaustive check")
     w = _weights_of(costfn, None)
     plan = MultiPlan(np.zeros((1, len(inputs)), dtype=np.int64), np.array([1.0]))
-    v = _certify_inputs(inputs, w, plan, duals)
+    v = _certify_inputs(inputs, w, plan, duals, _custom(costfn, w))
     return float(v[4])
 
 
@@ -299,7 +405,7 @@ def mot_certificate(inputs, w, plan, duals, costfn=None, rel_tol=1e-9):
     has at most 1e5 tuples), tolerance rel_tol (1 + |primal|)."""
     inputs = tuple(inputs)
     wv = _weights_of(costfn, w)
-    v = _certify_inputs(inputs, wv, plan, duals)
+    v = _certify_inputs(inputs, wv, plan, duals, _custom(costfn, wv))
     primal, dual = float(v[0]), float(v[1])
     violation = max(float(v[2]), float(v[3]), float(v[4]))
     return assemble_certificate(primal, dual, violation, rel_tol * (1.0 + abs(primal)))

@@ -60,8 +60,13 @@ def build(verbose=False, force=False):
                     "-I" + inc, "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
     flags += os.environ.get("UOT_NVCC_EXTRA", "").split()
 
+    hdr_time = max(os.path.getmtime(p) for p in hdrs + [__file__])
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_time)):
+            return obj  # up to date (headers are shared, so any header change rebuilds all)
         cmd = [nvcc, "-c", src, "-o", obj] + flags
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -99,6 +99,9 @@ struct MotArgs {
   int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
   int b0;                 // first problem of this launch (problem groups on streams)
   int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1, parity tests)
+  int all_states;         // 1: mot_plan keeps every state (zero-mass ones too) and the
+                          //    balanced sweep skips its duals (custom tuple costs)
+  int cost_given;         // 1: mot_duals takes dcc[q][0] as given (custom tuple costs)
   // parity / trace mode (optional)
   const double* step_in;  // [B][max_iters] replayed gamma_t
   unsigned long long* supp_hash;  // [B][max_iters] plan-support hash
@@ -1898,7 +1901,7 @@ __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double c = 0.0;
-    if (q == 0) {
+    if (q == 0 && !A.cost_given) {
       const double x0 = lane < K ? A.x[((long)b * K + lane) * n] : 0.0;
       const double om = lane < K ? A.omega[lane] : 0.0;
       const double bb = warp_sum(om * x0);
@@ -1907,7 +1910,8 @@ __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
     if (lane == 0) cc0_s = c;
   }
   __syncthreads();
-  if (threadIdx.x == 0) rv[0] = 0.0;  // dcc[0] is not an event
+  // dcc[0] is not an event (custom costs: it holds f_q[0] = Cc(first tuple) or 0)
+  if (threadIdx.x == 0 && !A.cost_given) rv[0] = 0.0;
   double loc = 0.0;
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
@@ -1919,6 +1923,34 @@ __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
 #pragma unroll
   for (int e = 0; e < EPT; ++e) rv[e] += off;
   store_run<EPT>(A.out_f + base, threadIdx.x * EPT, nq, rv);
+}
+
+// Custom tuple costs (solve_mot_1d with costfn, barycenter.py:195-229): the
+// sweep's state sequence is cost-independent, so the caller evaluates its
+// costfn on the visited tuples and the duals follow from the increments:
+// state t advances exactly one list p to index i, and
+// f_p[i] = f_p[i-1] + cost[t] - cost[t-1]  (new = cost - (pot_sum - old), :225-228),
+// f_1[0] = cost[0], f_k[0] = 0.  This kernel scatters the increments into dcc
+// at (p, i); mot_duals (cost_given) turns them into prefix sums.
+__global__ void mot_cost_dcc(MotArgs A, const double* cost) {
+  const int b = blockIdx.y, K = A.k, n = A.n;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cnt = A.pcount[b];
+  const int* ib = A.pidx + (long)b * A.cap_e * K;
+  const double* cb = cost + (long)b * A.cap_e;
+  double* db = A.dcc + (long)b * K * n;
+  if (t == 0) {
+    for (int q = 0; q < K; ++q) db[(long)q * n] = (q == 0) ? cb[0] : 0.0;
+    return;
+  }
+  if (t >= cnt) return;
+  for (int q = 0; q < K; ++q) {
+    const int i = ib[(long)t * K + q];
+    if (i != ib[(long)(t - 1) * K + q]) {
+      db[(long)q * n + i] = cb[t] - cb[t - 1];
+      return;
+    }
+  }
 }
 
 // Final translation by the optimal zero-sum lambda (barycenter.py:413-414),
@@ -1991,7 +2023,7 @@ __global__ void __launch_bounds__(BT) mot_plan(MotArgs A) {
       hi = fmin(hi, tot_mass);
       mass = hi - lo;
     }
-    const int keep = (c < nst && mass > 0.0) ? 1 : 0;
+    const int keep = (c < nst && (mass > 0.0 || A.all_states)) ? 1 : 0;
     // block exclusive scan of keep
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int incl = keep;
@@ -2079,7 +2111,10 @@ __global__ void __launch_bounds__(CT) mot_certify_kernel(int K, int n, const int
                                                          const double* a, const double* f,
                                                          const int* idx, const double* mass,
                                                          const int* count, int cap_e,
-                                                         int exhaustive, double* out) {
+                                                         int exhaustive, double* out,
+                                                         const double* ecost = nullptr,
+                                                         const double* gcost = nullptr,
+                                                         long gstride = 0) {
   __shared__ double scr[32];
   const int b = blockIdx.x;
   const int cnt = count[b];
@@ -2093,13 +2128,17 @@ __global__ void __launch_bounds__(CT) mot_certify_kernel(int K, int n, const int
     double bc = 0.0, fs = 0.0;
     for (int q = 0; q < K; ++q) {
       const int i = ib[(long)e * K + q];
-      bc += omega[q] * xb[(long)q * n + i];
+      if (ecost == nullptr) bc += omega[q] * xb[(long)q * n + i];
       fs += fb[(long)q * n + i];
     }
     double cc = 0.0;
-    for (int q = 0; q < K; ++q) {
-      const double dx = xb[(long)q * n + ib[(long)e * K + q]] - bc;
-      cc += omega[q] * (dx * dx);
+    if (ecost != nullptr) {  // caller-evaluated tuple cost (custom costfn)
+      cc = ecost[(long)b * cap_e + e];
+    } else {
+      for (int q = 0; q < K; ++q) {
+        const double dx = xb[(long)q * n + ib[(long)e * K + q]] - bc;
+        cc += omega[q] * (dx * dx);
+      }
     }
     primal += mb[e] * cc;
     sup = fmax(sup, fabs(fs - cc));
@@ -2127,17 +2166,21 @@ __global__ void __launch_bounds__(CT) mot_certify_kernel(int K, int n, const int
         const int nq = lens != nullptr ? lens[q] : n;
         const int i = (int)(r % nq);
         r /= nq;
-        bc += omega[q] * xb[(long)q * n + i];
+        if (gcost == nullptr) bc += omega[q] * xb[(long)q * n + i];
         fs += fb[(long)q * n + i];
       }
       r = t;
       double cc = 0.0;
-      for (int q = K - 1; q >= 0; --q) {
-        const int nq = lens != nullptr ? lens[q] : n;
-        const int i = (int)(r % nq);
-        r /= nq;
-        const double dx = xb[(long)q * n + i] - bc;
-        cc += omega[q] * (dx * dx);
+      if (gcost != nullptr) {
+        cc = gcost[(long)b * gstride + t];
+      } else {
+        for (int q = K - 1; q >= 0; --q) {
+          const int nq = lens != nullptr ? lens[q] : n;
+          const int i = (int)(r % nq);
+          r /= nq;
+          const double dx = xb[(long)q * n + i] - bc;
+          cc += omega[q] * (dx * dx);
+        }
       }
       worst = fmax(worst, fs - cc);
     }
@@ -2273,8 +2316,10 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
     UOT_CHECK_LAUNCH();
   }
   if (a.mode == 1) {
-    mot_duals<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
-    UOT_CHECK_LAUNCH();
+    if (!a.all_states) {
+      mot_duals<EPT><<<dim3(a.k, a.batch), MT, 0, st>>>(a);
+      UOT_CHECK_LAUNCH();
+    }
     return UOT_OK;
   }
   if constexpr (EPT >= 2 && EPT <= 16) {
@@ -2627,6 +2672,116 @@ extern "C" int uot_mot_certify(int32_t batch, int32_t k, int32_t n, const int32_
   mot_certify_kernel<<<batch, CT, 0, st>>>(k, n, lens != nullptr ? ld : nullptr, om, x, a, f, idx,
                                            mass, count, cap_e, grid <= 100000 ? 1 : 0, out);
   UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+
+// Custom tuple costs (solve_mot_1d / plan_cost / mot_certificate with a
+// caller costfn).  States: the sweep of uot_mot1d_batched with every visited
+// tuple kept (zero-mass states included), count[b] = 1 + sum_q (len_q - 1).
+extern "C" int uot_mot1d_states(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                                const double* a, int32_t* idx, double* mass, int32_t* count,
+                                int32_t* status, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  UOT_TRY(check_sizes(batch, k, n));
+  MotPlan p = plan_for(k, n);
+  if (workspace_bytes < ws_layout(batch, k, n, p.S, p.SS).total) {
+    set_error("uot_mot1d_states: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> om(k, 1.0 / k);  // the cost increments of the sweep are discarded
+  int rc;
+  MotArgs A = make_args(batch, k, n, p, (char*)workspace, om.data(), lens, 1.0, st, &rc);
+  UOT_TRY(rc);
+  A.mode = 1;
+  A.all_states = 1;
+  A.x = a;  // positions do not enter the state sequence
+  A.a = a;
+  A.status = status;
+  A.pidx = idx;
+  A.pmass = mass;
+  A.pcount = count;
+  A.cap_e = k * (n - 1) + 1;
+  A.max_iters = 1;
+  UOT_TRY(dispatch(A, p, st, false));
+  // make_args staged om/lens from host memory that dies with this frame
+  UOT_CUDA_TRY(cudaStreamSynchronize(st));
+  return UOT_OK;
+}
+
+// Duals of the custom-cost sweep from the caller's state costs cost [batch][cap]
+// (cap = k (n-1) + 1, the states of uot_mot1d_states in order).
+extern "C" int uot_mot1d_cost_duals(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                                    const int32_t* idx, const int32_t* count, const double* cost,
+                                    double* f, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+  UOT_TRY(check_sizes(batch, k, n));
+  MotPlan p = plan_for(k, n);
+  if (workspace_bytes < ws_layout(batch, k, n, p.S, p.SS).total) {
+    set_error("uot_mot1d_cost_duals: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> om(k, 1.0 / k);
+  int rc;
+  MotArgs A = make_args(batch, k, n, p, (char*)workspace, om.data(), lens, 1.0, st, &rc);
+  UOT_TRY(rc);
+  A.mode = 1;
+  A.cost_given = 1;
+  A.pidx = const_cast<int32_t*>(idx);
+  A.pcount = const_cast<int32_t*>(count);
+  A.cap_e = k * (n - 1) + 1;
+  A.out_f = f;
+  mot_cost_dcc<<<dim3((A.cap_e + 255) / 256, batch), 256, 0, st>>>(A, cost);
+  UOT_CHECK_LAUNCH();
+  switch (p.ept) {
+    case 1: mot_duals<1><<<dim3(k, batch), MT, 0, st>>>(A); break;
+    case 2: mot_duals<2><<<dim3(k, batch), MT, 0, st>>>(A); break;
+    case 4: mot_duals<4><<<dim3(k, batch), MT, 0, st>>>(A); break;
+    case 8: mot_duals<8><<<dim3(k, batch), MT, 0, st>>>(A); break;
+    case 16: mot_duals<16><<<dim3(k, batch), MT, 0, st>>>(A); break;
+    default: mot_duals<32><<<dim3(k, batch), MT, 0, st>>>(A); break;
+  }
+  UOT_CHECK_LAUNCH();
+  UOT_CUDA_TRY(cudaStreamSynchronize(st));
+  return UOT_OK;
+}
+
+// Certificate with caller-evaluated tuple costs: ecost [batch][cap] at the plan
+// entries, gcost [batch][grid] over the whole index grid (C order) when the
+// grid holds at most 1e5 tuples (else may be NULL; the sweep is skipped).
+extern "C" int uot_mot_certify_costs(int32_t batch, int32_t k, int32_t n, const int32_t* lens,
+                                     const double* a, const double* f, const int32_t* idx,
+                                     const double* mass, const int32_t* count,
+                                     const double* ecost, const double* gcost, double* out,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+  UOT_TRY(check_sizes(batch, k, n));
+  if (ecost == nullptr) {
+    set_error("uot_mot_certify_costs: ecost is required");
+    return UOT_INVALID;
+  }
+  if (workspace_bytes < sizeof(double) * (size_t)k + sizeof(int) * (size_t)k + 256) {
+    set_error("uot_mot_certify_costs: workspace too small");
+    return UOT_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* om = (double*)workspace;
+  int* ld = (int*)((char*)workspace + (sizeof(double) * (size_t)k + 15) / 16 * 16);
+  long grid = 1;
+  for (int q = 0; q < k; ++q) {
+    grid *= (lens != nullptr ? lens[q] : n);
+    if (grid > 100000) break;
+  }
+  const int exhaustive = (grid <= 100000 && gcost != nullptr) ? 1 : 0;
+  UOT_CUDA_TRY(cudaMemsetAsync(om, 0, sizeof(double) * k, st));
+  if (lens != nullptr)
+    UOT_CUDA_TRY(cudaMemcpyAsync(ld, lens, sizeof(int) * k, cudaMemcpyHostToDevice, st));
+  const int cap_e = k * (n - 1) + 1;
+  mot_certify_kernel<<<batch, CT, 0, st>>>(k, n, lens != nullptr ? ld : nullptr, om, a, a, f, idx,
+                                           mass, count, cap_e, exhaustive, out, ecost, gcost,
+                                           exhaustive ? grid : 0);
+  UOT_CHECK_LAUNCH();
+  if (lens != nullptr) UOT_CUDA_TRY(cudaStreamSynchronize(st));
   return UOT_OK;
 }
 

@@ -1326,10 +1326,62 @@ def gen_large():
         out[f"tie_{kk}"] = v
     save("large.npz", **out)
 
+def gen_mot_custom():
+    """solve_mot_1d / plan_cost / dual_feasibility_exhaustive / mot_certificate
+    with custom tuple costs (barycenter.py:169-295, costfn given)."""
+    from custom_costs import COSTS
+
+    rng = np.random.default_rng(23)
+    out = {}
+    cases = []
+    names = sorted(COSTS)
+    for c in range(18):
+        kk = int(rng.integers(2, 6)) if c < 15 else 8
+        inputs = []
+        for _q in range(kk):
+            n = int(rng.integers(1, 25)) if c < 15 else 6
+            wq = rng.uniform(0.1, 1.0, n)
+            if n > 2 and c % 3 == 0:
+                # zero-weight atom (tests/test_barycenter.py:95-105); not the last one: lists
+                # ending in zero weights tie at their total masses, which differ in the last
+                # ulp, and the reference breaks that tie on its clipped remainders
+                # (barycenter.py:216-221) -- the structural near tie of DESIGN.md §2
+                wq[rng.integers(0, n - 1)] = 0.0
+            wq *= 1.7 / wq.sum()
+            inputs.append(U.DiscreteMeasure(np.sort(rng.uniform(-1, 1, n)), wq))
+        w = rng.uniform(0.2, 1.0, kk)
+        w /= w.sum()
+        name = names[c % len(names)]
+        costfn = COSTS[name](w)
+        plan, duals = UB.solve_mot_1d(inputs, costfn=costfn)
+        out[f"c{c}_k"] = np.array(kk)
+        out[f"c{c}_cost"] = np.array(name)
+        out[f"c{c}_w"] = w
+        for q, mq in enumerate(inputs):
+            out[f"c{c}_x{q}"], out[f"c{c}_a{q}"] = mq.points, mq.weights
+            out[f"c{c}_f{q}"] = duals.potentials[q]
+        out[f"c{c}_idx"], out[f"c{c}_m"] = plan.indices, plan.mass
+        out[f"c{c}_pc"] = np.array(UB.plan_cost(plan, inputs, costfn))
+        cert = UB.mot_certificate(inputs, None, plan, duals, costfn=costfn)
+        out[f"c{c}_cert"] = np.array([cert.primal, cert.dual, cert.gap,
+                                      cert.feasibility_violation, 1.0 if cert.passed else 0.0])
+        bad = UB.MultiDual(tuple(p + (0.01 if q == 0 else 0.0)
+                                 for q, p in enumerate(duals.potentials)))
+        cb = UB.mot_certificate(inputs, None, plan, bad, costfn=costfn)
+        out[f"c{c}_bad"] = np.array([cb.primal, cb.dual, cb.gap, cb.feasibility_violation,
+                                     1.0 if cb.passed else 0.0])
+        grid = int(np.prod([len(m) for m in inputs], dtype=np.float64))
+        out[f"c{c}_dfe"] = np.array(UB.dual_feasibility_exhaustive(inputs, bad, costfn)
+                                    if grid <= 10**5 else np.nan)
+        cases.append(c)
+    out["cases"] = np.array(cases)
+    save("mot_custom.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "sinkhorn_small", "cfg3_small", "cfg4_small", "ot1d", "fw",
                              "mot", "barycenter", "duality", "pfw", "sinkhorn_g", "mot_cert",
-                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw", "replay", "large"]
+                             "sinkhorn_ent", "anderson", "formats", "dense", "entropy_api", "explicit", "bary_api", "berg", "sk_trace", "berg_pfw", "replay", "large", "mot_custom"]
     for w in which:
         t0 = time.time()
         globals()[f"gen_{w}"]()

@@ -1,6 +1,9 @@
 """Pin the CPU oracle (oracle/) against golden vectors produced by the
 reference itself (tests/golden/make_golden.py).  CPU only."""
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -173,6 +176,25 @@ def test_mot_sweep():
         np.testing.assert_allclose(mass, z[f"c{k}_m"], rtol=1e-12, atol=1e-16)
         for q in range(kk):
             np.testing.assert_allclose(pots[q], z[f"c{k}_f{q}"], rtol=1e-11, atol=1e-12)
+
+
+def test_mot_sweep_custom_cost():
+    """Custom tuple costs (barycenter.py:169-233 with costfn): the oracle's
+    restatement against the reference's own outputs."""
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from custom_costs import COSTS
+
+    z = golden("mot_custom.npz")
+    for c in cases(z):
+        kk = int(z[f"c{c}_k"])
+        xs = [z[f"c{c}_x{q}"] for q in range(kk)]
+        ws = [z[f"c{c}_a{q}"] for q in range(kk)]
+        costfn = COSTS[str(z[f"c{c}_cost"])](z[f"c{c}_w"])
+        idx, mass, pots = O.solve_mot_1d_custom(xs, ws, costfn)
+        np.testing.assert_array_equal(idx, z[f"c{c}_idx"])
+        np.testing.assert_array_equal(mass, z[f"c{c}_m"])
+        for q in range(kk):
+            np.testing.assert_array_equal(pots[q], z[f"c{c}_f{q}"])
 
 
 def test_barycenter_fw():
