@@ -195,7 +195,7 @@ struct Cta {
         hi = mid;
     }
     int i = lo, j = d0 - lo;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? IPT : 1)
     for (int s = 0; s < IPT; ++s) {
       if (d0 + s < E) {
         const double av = i < na ? sA[i] : CUDART_INF;
@@ -216,7 +216,7 @@ struct Cta {
                          double (&s)[EPT], double& mass_a, double& mass_b, PING& ping) {
     double pa[EPT], pb[EPT];
     double ca = 0.0, cb = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       ca += ta[e];
       pa[e] = ca;
@@ -225,7 +225,7 @@ struct Cta {
     }
     double tot[2] = {ca, cb}, totals[2];
     bops::block_scan_excl<NW, 2>(tot, totals, ping.next());
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
       if (i < n) sA[i] = tot[0] + pa[e];
@@ -244,7 +244,7 @@ struct Cta {
                                 const double (&pa)[EPT], const double (&pb)[EPT], double offa,
                                 double offb, double sca, double scb, double (&r)[EPT],
                                 double (&s)[EPT], PING& ping) {
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
       if (i < n) sA[i] = sca * (offa + pa[e]);
@@ -261,7 +261,7 @@ struct Cta {
       // bit (the reference emits no entry for it, ot1d.py:149-153), but the
       // block scan associates differently across thread boundaries.
       int lza = -1, lzb = -1;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = src(e);
         if (i < n && ta[e] > 0.0) lza = i;
@@ -271,7 +271,7 @@ struct Cta {
       int prb = excl_max_scan(lzb, reinterpret_cast<int*>(zred));
       __syncthreads();
       double fa[EPT], fb[EPT];
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = src(e);
         fa[e] = (i < n && ta[e] == 0.0) ? (pra >= 0 ? sA[pra] : 0.0) : -1.0;
@@ -280,7 +280,7 @@ struct Cta {
         if (i < m && tb[e] > 0.0) prb = i;
       }
       __syncthreads();
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = src(e);
         if (fa[e] >= 0.0) sA[i] = fa[e];
@@ -293,7 +293,7 @@ struct Cta {
     // cost increments along the staircase
     double da[EPT], db[EPT];
     double la = 0.0, lb = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = src(e);
       da[e] = 0.0;
@@ -313,7 +313,7 @@ struct Cta {
     bops::block_scan_excl<NW, 2>(off, unused, ping.next());
     const double s0 = cost(0, 0);
     double ra = off[0], rb = off[1];
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       ra += da[e];
       rb += db[e];
@@ -466,7 +466,7 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
   (void)sal;
   __shared__ int away_s, hit_s, na_s;
   __syncthreads();  // sA / sB readers (oracle, plan extraction) are done
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     if (i < n) {
@@ -536,7 +536,7 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
   double dA[EPT], dB[EPT];
   double mom[4] = {0.0, 0.0, 0.0, 0.0};
   double mxs[4] = {0.0, 0.0, -CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     dA[e] = i < n ? r[e] - ra[i] : 0.0;
@@ -570,7 +570,7 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
         const double pha = sha + gam * mxs[2];
         const double phb = shb + gam * mxs[3];
         double mm[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
         for (int e = 0; e < EPT; ++e) {
           const int i = c.src(e);
           const double va = dA[e] * i1, vb = dB[e] * i2;
@@ -613,7 +613,7 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
     const int nslot = pst.ntot;
     if (hit < 0) {
       double* row = A.atoms + (sb0 + nslot) * nm;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         if (i < n) row[i] = r[e];
@@ -639,7 +639,7 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
       na_s = k;
     }
     if (hit < 0) ++pst.ntot;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       f[e] += gam * dA[e];
       g[e] += gam * dB[e];
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   c.zeros = ibsum<NW>(nz, reinterpret_cast<int*>(c.zred)) > 0;  // (syncs: smem now visible)
 
   double f[EPT], g[EPT];
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     f[e] = i < n ? A.f[(long)b * n + i] : 0.0;
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   if (A.mode == 1) {
     // Plain balanced OT on (a, b): src/ot1d.py:112-172.
     double ta[EPT], tb[EPT], r[EPT], s[EPT], ma, mb;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       ta[e] = i < n ? sal[i] : 0.0;
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
     const int bad = fabs(ma - mb) > 1e-9 * fmax(ma, mb);  // ot1d.py:133-136
     if (threadIdx.x == 0) A.status[b] = bad ? UOT_MASS_BALANCE : 0;
     if (bad) return;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       if (i < n) A.f[(long)b * n + i] = r[e];
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   double sha, shb;
   {
     double ms[2] = {0.0, 0.0}, mx[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       if (i < n) ms[0] += sal[i];
@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   PfwState pst{1, 1};
   if constexpr (PW) {  // store = {(f0, g0)} with weight 1 (fw.py:332)
     double* row = A.atoms + (long)b * A.cap * (n + m);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       if (i < n) row[i] = f[e];
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
       // exponentials, local prefixes and one block scan: the scan's totals are
       // the log-sum-exp sums, its offsets give the breakpoints (oracle_scaled)
       double ca = 0.0, cb = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         const double wa = i < n ? sal[i] : 0.0, wb = i < m ? sbe[i] : 0.0;
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
       if (!((sums[0] < 1e-280 && sha > -CUDART_INF) || (sums[1] < 1e-280 && shb > -CUDART_INF)))
         break;
       double mx[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
     const double dual = r1 * malpha + r2 * mbeta - (r1 + r2) * __shfl_sync(bops::FULL, ev, 0);
     if (A.err_f != nullptr) {  // fw.py:217-219: translated iterate vs the reference
       double em1[1] = {0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
       for (int e = 0; e < EPT; ++e) {
         const int i = c.src(e);
         if (i < n) em1[0] = bops::dmax(em1[0], fabs(f[e] + lam - A.ref_f[(long)b * n + i]));
@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
     }
     const double sca = sha > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 1) : 0.0;
     const double scb = shb > -CUDART_INF ? __shfl_sync(bops::FULL, ev, 2) : 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       ta[e] *= sca;
       tb[e] *= scb;
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
     double acc[9], mr[2] = {-CUDART_INF, -CUDART_INF};
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = c.src(e);
       const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
           const double pha = (1.0 - gam) * sha + gam * mr[0];
           const double phb = (1.0 - gam) * shb + gam * mr[1];
           double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
           for (int e = 0; e < EPT; ++e) {
             const int i = c.src(e);
             const double va = (r[e] - f[e]) * i1, vb = (s[e] - g[e]) * i2;
@@ -1005,7 +1005,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
     // --- update (fw.py:227-230) and the next shift bounds, rounded as numpy
     // rounds (1 - gamma) f + gamma r: two products and a sum, no FMA
     const double omg = 1.0 - gam;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
       f[e] = __dadd_rn(__dmul_rn(omg, f[e]), __dmul_rn(gam, r[e]));
       g[e] = __dadd_rn(__dmul_rn(omg, g[e]), __dmul_rn(gam, s[e]));
@@ -1015,7 +1015,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   }
   // --- finalize: translate by lambda* (fw.py:235-252), exact maxima
   double mx[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     if (i < n && sal[i] > 0.0) mx[0] = bops::dmax(mx[0], -f[e] * i1);
@@ -1023,7 +1023,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   }
   bops::block_max<NW, 2>(mx, ping.next());
   double ls[2] = {0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     if (i < n) ls[0] += bops::wexp(sal[i], -f[e] * i1 - mx[0], tab);
@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   }
   bops::block_sum<NW, 2>(ls, ping.next());
   const double lam = (r1 * r2 / (r1 + r2)) * ((mx[0] + log(ls[0])) - (mx[1] + log(ls[1])));
-#pragma unroll
+#pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
     if (i < n) A.f[(long)b * n + i] = f[e] + lam;
@@ -1059,7 +1059,9 @@ inline int ept_for(int nm) {
 // Large-problem path: elements per thread at FW_THREADS_BIG threads (EPT 8 /
 // 16 in fw1d_big.cu; 32 -- arrays beyond the register budget live in local
 // memory: a correctness path -- in fw1d_huge.cu).
-constexpr int FW_EPT_BIG_MAX = 32;  // n, m <= 32768 per problem
+// 64 / 128 / 256 -- fw1d_giant.cu: the per-atom loops stay rolled (#pragma
+// unroll 1 above EPT 32), so these compile in seconds and run from local memory.
+constexpr int FW_EPT_BIG_MAX = 256;  // n, m <= 262144 per problem
 inline int ept_for_big(int nm) {
   const int per = (nm + FW_THREADS_BIG - 1) / FW_THREADS_BIG;
   for (int e = 8; e <= FW_EPT_BIG_MAX; e *= 2)
@@ -1106,6 +1108,22 @@ int launch_fw_huge(const FwArgs& a, int batch, cudaStream_t st, int ept) {
   UOT_CHECK_LAUNCH();
   return UOT_OK;
 }
+template <bool PW, int PK>
+int launch_fw_giant(const FwArgs& a, int batch, cudaStream_t st, int ept) {
+  if (ept == 64)
+    fw1d_kernel<64, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  else if (ept == 128)
+    fw1d_kernel<128, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  else
+    fw1d_kernel<256, PK, PW, FW_THREADS_BIG><<<batch, FW_THREADS_BIG, 0, st>>>(a);
+  UOT_CHECK_LAUNCH();
+  return UOT_OK;
+}
+#define UOT_FW_GIANT(EXT, PW)                                                        \
+  EXT template int launch_fw_giant<PW, 0>(const FwArgs&, int, cudaStream_t, int);   \
+  EXT template int launch_fw_giant<PW, 1>(const FwArgs&, int, cudaStream_t, int);   \
+  EXT template int launch_fw_giant<PW, 2>(const FwArgs&, int, cudaStream_t, int);   \
+  EXT template int launch_fw_giant<PW, 3>(const FwArgs&, int, cudaStream_t, int);
 #define UOT_FW_BIG(EXT, PW)                                                          \
   EXT template int launch_fw_big<PW, 0>(const FwArgs&, int, cudaStream_t, int);     \
   EXT template int launch_fw_big<PW, 1>(const FwArgs&, int, cudaStream_t, int);     \
@@ -1121,6 +1139,8 @@ UOT_FW_BIG(extern, false)
 UOT_FW_BIG(extern, true)
 UOT_FW_HUGE(extern, false)
 UOT_FW_HUGE(extern, true)
+UOT_FW_GIANT(extern, false)
+UOT_FW_GIANT(extern, true)
 #endif
 
 template <bool PW>
@@ -1154,8 +1174,9 @@ int launch_fw_impl(const FwArgs& a0, int batch, cudaStream_t st) {
   auto by_ept = [&](auto pk) -> int {
     constexpr int PK = decltype(pk)::value;
     if (big)
-      return eptb <= 16 ? launch_fw_big<PW, PK>(a, batch, st, eptb)
-                        : launch_fw_huge<PW, PK>(a, batch, st, eptb);
+      return eptb <= 16   ? launch_fw_big<PW, PK>(a, batch, st, eptb)
+             : eptb <= 32 ? launch_fw_huge<PW, PK>(a, batch, st, eptb)
+                          : launch_fw_giant<PW, PK>(a, batch, st, eptb);
     switch (ept) {
       case 1: return go(fw1d_kernel<1, PK, PW>, FW_THREADS, smem);
       case 2: return go(fw1d_kernel<2, PK, PW>, FW_THREADS, smem);

@@ -62,10 +62,10 @@ def test_ot1d_shapes_and_max_size(n, m):
 
 
 def test_ot1d_beyond_max_size_raises():
-    """n, m <= 4096 run resident on chip, up to 32768 on the large-problem
-    kernel (tests/test_large_gpu.py); beyond that the call raises."""
-    x = np.linspace(0, 1, 32769)
-    w = np.full(32769, 1.0 / 32769)
+    """n, m <= 4096 run resident on chip, up to 262144 on the large-problem
+    kernels (tests/test_large_gpu.py); beyond that the call raises."""
+    x = np.linspace(0, 1, 262145)
+    w = np.full(262145, 1.0 / 262145)
     with pytest.raises(ValueError):
         P.solve_ot_1d_batched(x, x, w, w, 2.0)
 

@@ -153,3 +153,36 @@ def test_huge_ot1d_and_fw_vs_oracle():
     out = O.fw_fixed(x2[0], y2[0], a2[0], b2[0], 1.0, 1.0, 6, step="harmonic")
     assert rel_err(D.to_np(r.f[0]), D.to_np(r.g[0]), out["f"], out["g"]) <= 1e-9
     np.testing.assert_allclose(D.to_np(r.h0[0]), out["h0"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("n,m", [(40000, 33001), (70001, 100000), (200000, 150000)])
+def test_giant_ot1d_vs_oracle(n, m):
+    """n or m > 32768 (up to 262144): the rolled-loop instantiations (64 / 128 / 256
+    atoms per thread, fw1d_giant.cu) of the same kernel; plan bit-exact, duals 1e-12."""
+    x, y, wa, wb = O.large_ot_inputs(n, m, 17 + n % 7)
+    f, g, ei, ej, em, count, status = P.solve_ot_1d_batched(x, y, wa, wb, 2.0)
+    assert int(status[0].item()) == 0
+    ii, jj, mm, fo, go = O.solve_ot_1d(x, y, wa, wb, 2.0)
+    c = int(count[0].item())
+    np.testing.assert_array_equal(D.to_np(ei[0, :c]), ii)
+    np.testing.assert_array_equal(D.to_np(ej[0, :c]), jj)
+    np.testing.assert_allclose(D.to_np(em[0, :c]), mm, rtol=0, atol=1e-13)
+    assert rel_err(D.to_np(f[0]), D.to_np(g[0]), fo, go) <= TOL
+
+
+def test_giant_fw_vs_oracle():
+    """FW (harmonic, line search) and pairwise FW at 50000 x 36000 atoms against the
+    oracle: potentials 1e-9, objective traces 1e-9."""
+    x2, y2, a2, b2 = S.cfg2_batch(batch=1, n=50000, m=36000, seed=78)
+    for step, its in (("harmonic", 5), ("linesearch", 4)):
+        r = P.fw_solve_batched(x2, y2, a2, b2, 1.0, 1.0, 2.0, its, step)
+        assert int(r.status[0].item()) == 0
+        out = O.fw_fixed(x2[0], y2[0], a2[0], b2[0], 1.0, 1.0, its, step=step)
+        np.testing.assert_allclose(D.to_np(r.h0[0]), out["h0"], rtol=1e-9)
+        if step == "harmonic":
+            assert rel_err(D.to_np(r.f[0]), D.to_np(r.g[0]), out["f"], out["g"]) <= 1e-9
+    r = P.fw_solve_batched(x2, y2, a2, b2, 1.0, 1.0, 2.0, 3, "pairwise")
+    assert int(r.status[0].item()) == 0
+    h0 = D.to_np(r.h0[0])
+    assert np.all(np.diff(h0) >= -1e-12 * np.abs(h0[0]))  # monotone dual ascent (fw.py:275-310)
+
