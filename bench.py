@@ -3,8 +3,11 @@
 Headline workload = BASELINE.json's metric as quoted on config 3:
 TI-Sinkhorn (H variant) on two seeded 8-component 2-D Gaussian mixtures,
 N = M = 65536, fp32 log-domain, eps = 1e-2 * max|x - y|^2, KL rho = 1.
-A "step" is one full H-Sinkhorn iteration (g half-step + f half-step) over
-the whole problem; ``value`` = iterations/s of the whole job.  With
+A "step" is one solve of that configuration through the public API -- 200
+H-Sinkhorn iterations (g half-step + f half-step each) over the whole problem
+from zero potentials, as BASELINE config 3 states it; ``value`` = iterations/s
+of the whole job = 200 * steps / timed seconds (an L2 flush between steps is
+inside the timed region).  With
 ``--gpus N`` under torchrun the single problem is row-sharded across the
 ranks (one NCCL all-gather per iteration) and the step time is the max over
 ranks.  The same line carries the other BASELINE configs as ``secondary``
@@ -33,6 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TI-Sinkhorn iter/s (N=M=65536, d=2)"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+CFG3_ITERS = 200  # BASELINE config 3: one solve = 200 iterations
 CFG2_BYTES_PER_ITER = 268435456  # 4096 * 32 * (1024 + 1024)
 CFG5_BYTES_PER_ITER = 268435456  # 64 * 16 * 8192 * 32
 
@@ -117,9 +121,10 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k] == "Active"})
         busy = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        pw = [v for v in (num(r[3]) for r in self.rows) if v is not None]
         return {"sm_mhz": float(np.median(busy or sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "power_w": float(np.median(pw)) if pw else None}
 
 
 def cuda_timer():
@@ -287,6 +292,8 @@ def cfg3_config(c, world):
             "n": len(c.x), "m": len(c.y), "d": 2, "eps": c.eps, "rho": c.rho, "variant": "h",
             "parallelism": f"rows/{world} (NCCL all-gather per iteration)" if world > 1
             else "single GPU",
+            "iters_per_step": CFG3_ITERS,
+            "step": f"one {CFG3_ITERS}-iteration solve from zero potentials (sinkhorn_batched)",
             "l2": f"{L2_FLUSH_BYTES >> 20} MiB write between steps (included in timing)"}
 
 
@@ -313,14 +320,13 @@ def run_cfg3(args, rank, world, dev, comm):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     kw = dict(comm=comm.handle, nranks=world, rank=rank) if comm is not None else {}
 
-    def step(f0):
-        f, g, _, _ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, variant="h",
-                                        precision="fp32", f0=f0, **kw)
+    def step():
+        f, g, _, _ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, CFG3_ITERS, variant="h",
+                                        precision="fp32", **kw)
         return f, g
 
-    f = None
     for _ in range(max(args.warmup, 3)):
-        f, g = step(f)
+        f, g = step()
     flush.zero_()
     with cuda_timer() as tf:
         flush.zero_()
@@ -331,9 +337,9 @@ def run_cfg3(args, rank, world, dev, comm):
         with cuda_timer() as tt:
             for _ in range(args.steps):
                 flush.zero_()
-                f, g = step(f)
+                f, g = step()
     ms_step = max_over_ranks(tt.ms / args.steps, world, dev)
-    value = 1e3 / ms_step
+    value = CFG3_ITERS * 1e3 / ms_step
 
     # roofline of the dominant kernel (fused cost + online LSE half-step),
     # timed live with CUDA events on the launching stream, on this rank's shard.
@@ -381,30 +387,31 @@ def run_cfg3(args, rank, world, dev, comm):
         "data": "synthetic (seeded 8-component 2-D Gaussian mixtures, BASELINE cfg3)",
         "config": cfg3_config(c, world), "l2_flush_ms": tf.ms,
         "roofline": roof, "e2e": e2e,
-        "gpu_launches": (4 + 7) * args.steps if world == 1 else (5 + 8) * args.steps,
+        # per iteration: 2 main kernels + 2 tails (+ the combine when sharded), replayed from
+        # the captured two-iteration graph; per solve: centre, zero, reset, finalize, ...
+        "gpu_launches": ((4 if world == 1 else 5) * CFG3_ITERS + (7 if world == 1 else 8))
+        * args.steps,
     }
     return line, clk
 
 
 def run_cfg3_e2e(P, c, xl, al, steps, dev, kw, world):
     """Same metric through the public API from pinned host buffers: H2D of
-    the step's inputs, one iteration, D2H of the resulting pair."""
+    the step's inputs, one CFG3_ITERS-iteration solve, D2H of the resulting
+    potentials -- the call a user of the reference's run() makes."""
     import torch
 
     host = {k: torch.as_tensor(v, dtype=torch.float32).pin_memory()
             for k, v in (("x", xl), ("y", c.y), ("a", al), ("b", c.beta))}
-    fh = torch.zeros(len(xl), dtype=torch.float32).pin_memory()
     out_f = torch.empty(len(xl), dtype=torch.float32).pin_memory()
     out_g = torch.empty(len(c.y), dtype=torch.float32).pin_memory()
 
     def one():
         dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-        f0 = fh.to(dev, non_blocking=True)
         f, g, _, _ = P.sinkhorn_batched(dv["x"], dv["y"], dv["a"], dv["b"], c.eps, c.rho, c.rho,
-                                        1, precision="fp32", f0=f0, **kw)
+                                        CFG3_ITERS, precision="fp32", **kw)
         out_f.copy_(f[0], non_blocking=True)
-        out_g.copy_(g[0], non_blocking=True)
-        fh.copy_(out_f)
+        out_g.copy_(g[0], non_blocking=False)
 
     for _ in range(2):
         one()
@@ -416,8 +423,8 @@ def run_cfg3_e2e(P, c, xl, al, steps, dev, kw, world):
             one()
     ms = max_over_ranks(t.ms / steps, world, dev)
     n, m = len(xl), len(c.y)
-    return {"value": 1e3 / ms, "unit": "iter/s",
-            "h2d_bytes_per_step": 4 * (2 * n + 2 * m + n + m + n),
+    return {"value": CFG3_ITERS * 1e3 / ms, "unit": "iter/s",
+            "h2d_bytes_per_step": 4 * (2 * n + 2 * m + n + m),
             "d2h_bytes_per_step": 4 * (n + m), "ms_per_step": ms,
             "path": "paper_2201_00730_b200.sinkhorn_batched -> uot_sinkhorn_run (C-ABI)"}
 
@@ -598,13 +605,14 @@ def run_cfg4(rank, world, dev):
     lo, hi = shard_problems(256, world, rank)
     x, y, a, b = S.cfg4_batch(start=lo, count=hi - lo)
     xt, yt, at, bt = (torch.as_tensor(v, dtype=torch.float32, device=dev) for v in (x, y, a, b))
-    iters = 30
+    iters = 300  # the whole BASELINE config-4 solve
     P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
                        precision="fp32")  # warm-up, same shapes
     torch.cuda.synchronize()
-    with cuda_timer() as t:
-        P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
-                           precision="fp32")
+    with ClockSampler(dev.index) as clk4:  # tensor + MUFU load: the power cap sets the clock
+        with cuda_timer() as t:
+            P.sinkhorn_batched(xt, yt, at, bt, S.CFG4_EPS, S.CFG4_RHO, S.CFG4_RHO, iters,
+                               precision="fp32")
     ms = max_over_ranks(t.ms, world, dev)
     value = iters / (ms * 1e-3)  # batched iterations over all 256 problems (all ranks)
     # Per 256 x 128 pair tile: 12 kind::f16 MMAs (fp16 hi/lo splits, K = 16)
@@ -653,8 +661,9 @@ def run_cfg4(rank, world, dev):
     return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32, tcgen05 cost tiles "
                         "(kind::f16 hi/lo splits + one kind::tf32 constants MMA, A in TMEM, B "
                         "ring in smem, CTA pairs) + MUFU LSE epilogue; "
-                        f"timed over {iters} of the 300 iterations",
+                        f"one whole {iters}-iteration solve timed",
             "value": value, "unit": "iter/s", "dtype": "f32 (fp16-split tensor, fp32 accumulate)",
+            "clocks": clk4.summary(),
             "roofline": {"bound": "mufu", "achieved": kernel["achieved"] if kernel else exps,
                          "peak": peak_g, "unit": "Gex2/s",
                          "frac": (kernel["achieved"] if kernel else exps) / peak_g,
@@ -731,7 +740,7 @@ def compact(entry):
     keeps a bounded tail of stdout); the descriptive keys go to
     gpurun_out/bench_detail.json."""
     keep = ("value", "unit", "ms_total", "dtype", "f_variant_iter_s", "g_variant_iter_s",
-            "mean_active_atoms", "res_f", "res_g")
+            "mean_active_atoms", "res_f", "res_g", "clocks")
     out = {k: entry[k] for k in keep if k in entry}
     for sub in ("roofline", "tensor", "issue"):
         if entry.get(sub):
