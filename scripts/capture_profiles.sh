@@ -8,9 +8,10 @@ O=gpurun_out
 part=${1:-all}
 if [ "$part" = 1 ] || [ "$part" = all ]; then
 # cfg3 headline: launch list of a short bench run + full capture of the main kernel
-timeout 300 python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_cfg3_launches.csv python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:sk_main -s 4 -c 1 -f -o $O/prof_cfg3_full python bench.py --no-secondary --steps 3 --warmup 3 > /dev/null 2>&1
+# (a step is a whole 200-iteration solve: 1 timed + 3 warm-up solves and the e2e leg's 3)
+timeout 300 python bench.py --no-secondary --steps 1 --warmup 3 > /dev/null && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_cfg3_launches.csv python bench.py --no-secondary --steps 1 --warmup 3 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sk_main -s 40 -c 1 -f -o $O/prof_cfg3_full python bench.py --no-secondary --steps 1 --warmup 3 > /dev/null 2>&1
 # cfg2 FW: 296 problems x 20 iterations
 timeout 300 python scripts/prof_fw.py 296 20 linesearch && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prof_fw_launches.csv python scripts/prof_fw.py 296 20 linesearch > /dev/null 2>&1

@@ -3,11 +3,11 @@
 cd "$(dirname "$0")/.."
 S=scripts/summarize_ncu.py
 R=${1:-r2}
-{ echo "# ${R} — cfg3 TI-Sinkhorn (N=M=65536, d=2, fp32), \`python bench.py --no-secondary --steps 3 --warmup 3\`"; echo;
+{ echo "# ${R} — cfg3 TI-Sinkhorn (N=M=65536, d=2, fp32), \`python bench.py --no-secondary --steps 1 --warmup 3\` (a step = one 200-iteration solve)"; echo;
   echo "## Launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised — compare shares)"; echo;
   python $S launches gpurun_out/prof_cfg3_launches.csv; echo;
   echo "probe_ex2 is the MUFU peak microbenchmark bench.py runs live beside the fixed denominator (not part of a step)."; echo;
-  echo "## Full capture of the dominant kernel (ncu --set full --clock-control none, -k regex:sk_main -s 4 -c 1)"; echo;
+  echo "## Full capture of the dominant kernel (ncu --set full --clock-control none, -k regex:sk_main -s 40 -c 1)"; echo;
   python $S full gpurun_out/prof_cfg3_full.ncu-rep; echo;
   echo "Reading: XU (MUFU) pipe ~93% busy; DRAM traffic per launch is the row records and column data only (no re-reads). Bound = MUFU ex2 throughput."; } > profiles/${R}_cfg3_sinkhorn.md
 cp gpurun_out/prof_cfg3_launches.csv profiles/${R}_cfg3_launches.csv
