@@ -98,6 +98,7 @@ struct MotArgs {
   int* sampt;             // [B][K][SS] (indices)
   int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
   int b0;                 // first problem of this launch (problem groups on streams)
+  int upd_s;              // update by mot_update_s (the batch runs ungrouped: < 16 problems)
   int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1, parity tests)
   int all_states;         // 1: mot_plan keeps every state (zero-mass ones too) and the
                           //    balanced sweep skips its duals (custom tuple costs)
@@ -1885,6 +1886,246 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   MOT_STAMP(7);
 }
 
+// mot_update_s: ONE list per CTA (clusters of K CTAs, K <= 16) with the list's
+// three rows in shared memory (mot_update2's list-B path on its own).  No row
+// lives in registers, so the per-atom loops unroll four wide and the fp64
+// exp chains of consecutive atoms interleave (mot_update / mot_update2 keep
+// 96 state registers per thread and run them one after the other).
+// Chosen by use_update_s (small, ungrouped batches; even n, N <= 16 MT).
+#ifndef UPDS_UNROLL
+#define UPDS_UNROLL 4
+#endif
+template <int EPT>
+__global__ void __launch_bounds__(MT, 1) mot_update_s(MotArgs A) {
+  MOT_STAMP(0);
+  using SW = Swz<EPT>;
+  constexpr int PAIRS = EPT / 2;
+  constexpr int UNR = PAIRS < UPDS_UNROLL ? PAIRS : UPDS_UNROLL;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double rows[];  // r (dcc first), f, w
+  constexpr int RBUF = 8 * MNW;
+  __shared__ __align__(16) double red[2 * RBUF];
+  __shared__ double tab[32];
+  __shared__ double slots[32];
+  __shared__ int done_s;
+  __shared__ double cc0_s;
+  __shared__ int iscr[MNW];
+  __shared__ double vscr[MNW];
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.y + A.b0;
+  const int K = A.k, n = A.n;
+  const int nq = list_len(A, q);
+  const int tid = threadIdx.x;
+  int parity = 0;
+  bops::Ping<RBUF> ping{red, 0};
+  bops::load_exp_table(tab);
+  if (tid == 0) done_s = (A.done != nullptr) ? A.done[b] : 0;
+  __syncthreads();
+  if (done_s) return;
+  const long base = ((long)b * K + q) * n;
+  double* rB = rows;
+  double* fB = rows + MT * EPT;
+  double* wB = rows + 2 * MT * EPT;
+  SW::fill(rB, A.dcc + base, nq);
+  SW::fill(fB, A.f + base, nq);
+  SW::fill(wB, A.a + base, nq);
+  if (tid < 32) {  // f_1[0] = Cc(first tuple) (barycenter.py:206-207)
+    const int lane = tid;
+    double cc = 0.0;
+    if (q == 0) {
+      const double x0 = lane < K ? A.x[((long)b * K + lane) * n] : 0.0;
+      const double om = lane < K ? A.omega[lane] : 0.0;
+      const double bb = warp_sum(om * x0);
+      cc = warp_sum(om * ((x0 - bb) * (x0 - bb)));
+    }
+    if (lane == 0) cc0_s = cc;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  MOT_STAMP(1);
+  // dual atoms: prefix sums of the cost increments (dcc[0] is not an event)
+  if (tid == 0) SW::at(rB, 0, 0)->x = 0.0;
+  double sc1[1] = {0.0};
+#pragma unroll UNR
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 d = *SW::at(rB, tid, cc);
+    sc1[0] += d.x;
+    sc1[0] += d.y;
+  }
+  {
+    double tot1[1];
+    bops::block_scan_excl<MNW, 1>(sc1, tot1, ping.next());
+  }
+  const double offb = sc1[0] + cc0_s;
+  {
+    double lb = 0.0;
+#pragma unroll UNR
+    for (int cc = 0; cc < PAIRS; ++cc) {
+      double2* p = SW::at(rB, tid, cc);
+      const double2 d = *p;
+      lb += d.x;
+      const double x0 = lb + offb;
+      lb += d.y;
+      *p = make_double2(x0, lb + offb);
+    }
+  }
+  const double rq = A.omega[q] * A.rho, irq = 1.0 / rq;
+  const double lamq = A.lam[(long)b * K + q];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  double mxs[2] = {-CUDART_INF, -CUDART_INF};
+  const double mxq = A.lse[((long)b * K + q) * 2 + 0];
+  const double tsq = exp(mxq - lamq * irq);
+#pragma unroll UNR
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+    const double rr[2] = {r2.x, r2.y}, ff[2] = {f2.x, f2.y}, ww[2] = {w2.x, w2.y};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double t = bops::wexp(ww[h], -ff[h] * irq - mxq, tab) * tsq;
+      const double d = rr[h] - ff[h];
+      acc[0] += t * d;
+      acc[1] += t * rr[h];
+      if (t > 0.0) acc[2] += t * (-(ff[h] + lamq) * irq);
+      acc[3] += t;
+      acc[4] += ww[h];
+      acc[5] += t * d * d;
+      if (ww[h] > 0.0) {
+        mxs[0] = bops::dmax(mxs[0], -ff[h] * irq);
+        mxs[1] = bops::dmax(mxs[1], -rr[h] * irq);
+      }
+    }
+  }
+  bops::block_red<MNW, 6, 2>(acc, mxs, ping.next());
+  const double cq = acc[0] / acc[3];
+  double cs[4] = {acc[0], acc[1] + rq * (acc[2] - acc[3] + acc[4]), cq,
+                  fmax(acc[5] / acc[3] - cq * cq, 0.0) / rq};
+  const double mass_q = acc[4];
+  const double mx0 = mxs[0], mx1 = mxs[1];
+  MOT_STAMP(2);
+  cluster_sum<4>(cs, slots, parity);
+  MOT_STAMP(3);
+  const double fw_gap = cs[0];
+  const double primal = cs[1];
+  const double dual = A.scal[b * 4 + 0];
+  const double pd_gap = primal - dual;
+  const int t = A.t;
+  if (q == 0 && tid == 0) {
+    A.h0[(long)b * A.max_iters + t] = dual;
+    A.fw_gap[(long)b * A.max_iters + t] = fw_gap;
+    A.pd_gap[(long)b * A.max_iters + t] = pd_gap;
+    A.iterations[b] = t + 1;
+    A.summary[b * 2 + 0] = primal;
+    A.summary[b * 2 + 1] = dual;
+  }
+  const bool stop = A.early_exit && pd_gap < A.gap_tol;  // barycenter.py:394-396
+  if (stop) {
+    if (q == 0 && tid == 0) A.done[b] = 2;
+    cl.sync();
+    return;
+  }
+  double gam;
+  if (A.step_in != nullptr) {
+    gam = __ldg(A.step_in + (long)b * A.max_iters + t);  // replayed gamma_t
+  } else if (A.step == UOT_STEP_HARMONIC) {
+    gam = 2.0 / (2.0 + t);
+  } else {  // safeguarded Newton on Phi(gamma) (see mot_update)
+    const double k0 = -cs[2];
+    const double vs = cs[3];
+    if (!(k0 < 0.0)) {
+      gam = 0.0;
+    } else {
+      double lo = 0.0, hi = 1.0;
+      gam = vs > 0.0 ? fmin(1.0, -k0 / vs) : 1.0;
+      for (int it = 0; it < 24; ++it) {
+        const double sh = (1.0 - gam) * mx0 + gam * mx1;
+        double mom[3] = {0.0, 0.0, 0.0};
+#pragma unroll UNR
+        for (int cc = 0; cc < PAIRS; ++cc) {
+          const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc),
+                        w2 = *SW::at(wB, tid, cc);
+          const double rr[2] = {r2.x, r2.y}, ff[2] = {f2.x, f2.y}, wq[2] = {w2.x, w2.y};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double d = rr[h] - ff[h];
+            const double ww = bops::wexp(wq[h], -(ff[h] + gam * d) * irq - sh, tab);
+            const double xc = d - cq;
+            mom[0] += ww;
+            mom[1] += ww * xc;
+            mom[2] += ww * xc * xc;
+          }
+        }
+        bops::block_sum<MNW, 3>(mom, ping.next());
+        const double e1 = mom[1] / mom[0];
+        double gv[2] = {e1, (mom[2] / mom[0] - e1 * e1) / rq};
+        cluster_sum<2>(gv, slots, parity);
+        const double g1 = k0 - gv[0], g2 = gv[1];
+        if (g1 < 0.0)
+          lo = gam;
+        else
+          hi = gam;
+        if (gam >= 1.0 && g1 <= 0.0) {
+          gam = 1.0;
+          break;
+        }
+        double nxt = g2 > 0.0 ? gam - g1 / g2 : 0.5 * (lo + hi);
+        const bool newton = nxt > lo && nxt < hi;
+        if (!newton) nxt = 0.5 * (lo + hi);
+        const bool conv = (newton && fabs(nxt - gam) <= 1e-9 * fmax(1.0, gam)) || g1 == 0.0 ||
+                          hi - lo <= 1e-15;
+        gam = nxt;
+        if (conv) break;
+      }
+    }
+  }
+  MOT_STAMP(4);
+  // barycenter.py:409-411, rounded as numpy rounds it (two products, a sum);
+  // the maximum of the new iterate's exponents in the same pass
+  const double omg = 1.0 - gam;
+  double m1[1] = {-CUDART_INF};
+#pragma unroll UNR
+  for (int cc = 0; cc < PAIRS; ++cc) {
+    const double2 r2 = *SW::at(rB, tid, cc), f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+    const double2 fn = make_double2(__dadd_rn(__dmul_rn(omg, f2.x), __dmul_rn(gam, r2.x)),
+                                    __dadd_rn(__dmul_rn(omg, f2.y), __dmul_rn(gam, r2.y)));
+    *SW::at(fB, tid, cc) = fn;
+    if (w2.x > 0.0) m1[0] = bops::dmax(m1[0], -fn.x * irq);
+    if (w2.y > 0.0) m1[0] = bops::dmax(m1[0], -fn.y * irq);
+  }
+  bops::block_max<MNW, 1>(m1, ping.next());
+  double s1[1] = {0.0};
+#pragma unroll UNR
+  for (int cc = 0; cc < PAIRS; ++cc) {  // w exp(-f/rho - mx) replaces the dual atoms
+    const double2 f2 = *SW::at(fB, tid, cc), w2 = *SW::at(wB, tid, cc);
+    const double ex = bops::wexp(w2.x, -f2.x * irq - m1[0], tab);
+    const double ey = bops::wexp(w2.y, -f2.y * irq - m1[0], tab);
+    s1[0] += ex;
+    s1[0] += ey;
+    *SW::at(rB, tid, cc) = make_double2(ex, ey);
+  }
+  bops::block_sum<MNW, 1>(s1, ping.next());
+  const double qk = m1[0] + log(s1[0]);
+  if (tid == 0) {
+    A.lse[((long)b * K + q) * 2 + 0] = m1[0];
+    A.lse[((long)b * K + q) * 2 + 1] = qk;
+  }
+  Swz<EPT>::drain(fB, A.f + base, nq);
+  MOT_STAMP(5);
+  if (t + 1 < A.max_iters) {
+    double ex[3] = {rq * qk, rq * mass_q, rq};
+    cluster_sum<3>(ex, slots, parity);
+    const double lam1 = rq * qk - (rq / ex[2]) * ex[0];
+    if (tid == 0) {
+      A.lam[(long)b * K + q] = lam1;
+      if (q == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
+    }
+    const double sc = exp(m1[0] - lam1 * irq);
+    tilt_tail_smem<EPT>(A, b, q, nq, rB, sc, ping.next(), iscr, vscr);
+  }
+  MOT_STAMP(6);
+  cl.sync();  // slots stay valid until every CTA read them
+  MOT_STAMP(7);
+}
+
 // Balanced sweep (solve_mot_1d, mode 1): the duals are prefix sums of the
 // cost increments, f_1[0] = Cc(first tuple), f_k[0] = 0 (barycenter.py:206-229);
 // no cross-list reduction, so one plain CTA per list (any K).
@@ -2268,6 +2509,20 @@ bool use_update2(const MotArgs& a) {
   return !env_flag("UOT_MOT_UPDATE1") && a.k % 2 == 0 && a.n % 2 == 0;
 }
 
+// mot_update_s (one list per CTA, rows in shared memory, clusters of K CTAs)
+// finishes a list in ~33 us where mot_update2 takes ~79 us for two, but only 7
+// sixteen-CTA clusters are co-resident against 15 eight-CTA ones.  It wins
+// whenever the batch is small enough to run ungrouped (a single problem -- the
+// reference's own fw_barycenter call -- 75 -> 48 us per iteration at cfg5 size,
+// 7 problems 139 -> 84 us); the grouped cfg5 batch stays on mot_update2 (0.435
+// vs 0.46 ms per iteration).  UOT_MOT_UPDATES=1 / 0 forces / forbids it.
+bool use_update_s(const MotArgs& a) {
+  if (a.mode != 0 || a.k > 16 || a.n % 2 != 0) return false;
+  const char* e = getenv("UOT_MOT_UPDATES");
+  if (e != nullptr) return atoi(e) != 0;
+  return a.upd_s != 0 && !env_flag("UOT_MOT_UPDATE1");
+}
+
 template <class Kern>
 int launch_cluster(Kern kern, int k, int batch, size_t smem, cudaStream_t st, const MotArgs& a) {
   cudaLaunchConfig_t cfg = {};
@@ -2323,6 +2578,11 @@ int run_sweep(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool tilt) {
     return UOT_OK;
   }
   if constexpr (EPT >= 2 && EPT <= 16) {
+    if (use_update_s(a)) {
+      UOT_TRY(launch_cluster(mot_update_s<EPT>, a.k, a.batch, 3 * (size_t)MT * EPT * sizeof(double),
+                             st, a));
+      return UOT_OK;
+    }
     if (use_update2(a)) {
       UOT_TRY(launch_cluster(mot_update2<EPT>, (a.k + 1) / 2, a.batch, upd2_smem<EPT>(), st, a));
       return UOT_OK;
@@ -2362,6 +2622,7 @@ template <int EPT>
 int run_all(MotArgs a, const MotPlan& p, cudaStream_t st, bool fw) {
   if (fw) {
     const int G = mot_groups(a.batch);
+    a.upd_s = G == 1;
     std::vector<MotArgs> ga(G, a);
     std::vector<cudaStream_t> gs(G, st);
     cudaEvent_t fork = nullptr;

@@ -191,11 +191,13 @@ def test_fw_barycenter_report_vs_reference(k):
 # ---------------------------------------------------------------------------
 # Kernel variants of the sweep (csrc/mot1d.cu): the bin sort and its merge-path
 # fallback order the events identically (the (value, list, index) order is
-# total), and the one-list / two-lists-per-CTA updates compute the same
-# iterates; clustered keys (zero-weight runs repeat breakpoints) and ties
+# total), and the three update kernels (mot_update_s, the default of small
+# batches; mot_update2 with UOT_MOT_UPDATES=0; mot_update with
+# UOT_MOT_UPDATE1=1) compute the same iterates; clustered keys (zero-weight runs repeat breakpoints) and ties
 # across lists (identical inputs) exercise the fallback and the tie rule.
-@pytest.mark.parametrize("env", ["UOT_MOT_NOBIN", "UOT_MOT_UPDATE1"])
-def test_sweep_variants_agree(monkeypatch, env):
+@pytest.mark.parametrize("env,val", [("UOT_MOT_NOBIN", "1"), ("UOT_MOT_UPDATE1", "1"),
+                                     ("UOT_MOT_UPDATES", "0")])
+def test_sweep_variants_agree(monkeypatch, env, val):
     xs, ws = S.cfg5_batch(count=3, n=2048)
     ws[1, :, 100:400] = 0.0          # zero-weight runs: repeated breakpoints
     xs[2, 5] = xs[2, 4]              # two identical lists: cross-list ties
@@ -204,9 +206,9 @@ def test_sweep_variants_agree(monkeypatch, env):
     # the two update kernels associate their block / cluster sums differently:
     # compared on harmonic steps (a fixed gamma schedule); the merge fallback
     # orders the same keys, compared on line-search runs
-    step = "harmonic" if env == "UOT_MOT_UPDATE1" else "linesearch"
+    step = "linesearch" if env == "UOT_MOT_NOBIN" else "harmonic"
     base = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
-    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv(env, val)
     alt = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
     monkeypatch.delenv(env)
     assert (D.to_np(base.status) == 0).all() and (D.to_np(alt.status) == 0).all()
