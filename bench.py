@@ -658,12 +658,13 @@ def run_cfg4(rank, world, dev):
         kernel = {"kernel": "sk_main_tc", "kernel_ms": kms, "achieved": kach,
                   "frac": kach / peak_g,
                   "share_of_iteration": 2.0 * kms / (1e3 / value)}
+    c4 = clk4.summary()
     return {"workload": "cfg4: batched H-Sinkhorn B=256 N=M=4096 d=64 fp32, tcgen05 cost tiles "
                         "(kind::f16 hi/lo splits + one kind::tf32 constants MMA, A in TMEM, B "
                         "ring in smem, CTA pairs) + MUFU LSE epilogue; "
                         f"one whole {iters}-iteration solve timed",
             "value": value, "unit": "iter/s", "dtype": "f32 (fp16-split tensor, fp32 accumulate)",
-            "clocks": clk4.summary(),
+            "clocks": c4,
             "roofline": {"bound": "mufu", "achieved": kernel["achieved"] if kernel else exps,
                          "peak": peak_g, "unit": "Gex2/s",
                          "frac": (kernel["achieved"] if kernel else exps) / peak_g,
@@ -671,6 +672,11 @@ def run_cfg4(rank, world, dev):
                          "kernel_ms": kernel["kernel_ms"] if kernel else None,
                          "work_per_launch": "B*N*M = 4.29e9 ex2",
                          "iteration_frac": exps / peak_g,
+                         # the MUFU peak scales with the SM clock; under this kernel's
+                         # tensor + MUFU load the power cap holds the clock below its maximum
+                         "iteration_frac_at_sampled_clock": (
+                             exps / peak_g * c4["sm_max_mhz"] / c4["sm_mhz"]
+                             if c4.get("sm_mhz") and c4.get("sm_max_mhz") else None),
                          "kernel_share_of_iteration": kernel["share_of_iteration"] if kernel
                          else None,
                          "peak_source": probes["source"]},
@@ -747,7 +753,7 @@ def compact(entry):
             out[sub] = {k: v for k, v in entry[sub].items()
                         if k in ("bound", "achieved", "peak", "unit", "frac", "achieved_tflops",
                                  "peak_tflops", "peak_sustained_tflops", "frac_sustained",
-                                 "iteration_frac", "kernel")}
+                                 "iteration_frac", "iteration_frac_at_sampled_clock", "kernel")}
     if "cpu_baseline" in entry:
         cb = entry["cpu_baseline"]
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind")}
