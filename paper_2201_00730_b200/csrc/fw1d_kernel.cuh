@@ -438,7 +438,13 @@ struct Cta {
 // slots used so far (identical in every thread).
 struct PfwState {
   int na, ntot;
+  double* wts;  // weight of each slot: shared memory when cap <= PFW_CAP_S, else the workspace
+  int* act;     // active slots in insertion order (likewise)
 };
+constexpr int PFW_CAP_S = 1024;
+#ifndef PFW_CH
+#define PFW_CH 2  // atoms scored per block reduction
+#endif
 
 // One pairwise step (fw.py:275-310) after the LMO of iteration t: scores of
 // the active atoms against the tilted marginals (one warp per atom, coalesced
@@ -448,8 +454,9 @@ struct PfwState {
 // 295-297 runs a ternary search + endpoint check on the same concave H0);
 // weight transfer, merge into an atom closer than 1e-12 (:260-272), drop of
 // zero weights, and the iterate update d += gamma ((r, s) - away).  Returns
-// gamma.  The shared breakpoint arrays sA / sB are free after the oracle and
-// hold ta / tb here; the new atom is staged after them.
+// gamma.  Slot weights and the active list live in shared memory (up to
+// PFW_CAP_S slots, i.e. max_iters < 1024; the workspace beyond that); the atom
+// rows in the workspace, each element read back by the thread that wrote it.
 template <int EPT, int PK, int NT, typename PING>
 __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, double (&f)[EPT],
                            double (&g)[EPT], const double (&r)[EPT], const double (&s)[EPT],
@@ -458,84 +465,71 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
                            double t2, const double* sal, const double* sbe, const double* tab,
                            PING& ping, PfwState& pst) {
   const int n = c.n, m = c.m, nm = n + m;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* ta_s = c.sA;  // [n]
-  double* tb_s = c.sB;  // [m]
-  double* nr_s = c.pfw;  // [n] new atom staging (pairwise only)
-  double* ns_s = nr_s + n;  // [m]
+  using CT = Cta<EPT, PK, NT>;
   (void)sal;
-  __shared__ int away_s, hit_s, na_s;
-  __syncthreads();  // sA / sB readers (oracle, plan extraction) are done
-#pragma unroll (EPT <= 32 ? EPT : 1)
-  for (int e = 0; e < EPT; ++e) {
-    const int i = c.src(e);
-    if (i < n) {
-      ta_s[i] = ta[e];
-      nr_s[i] = r[e];
-    }
-    if (i < m) {
-      tb_s[i] = tb[e];
-      ns_s[i] = s[e];
-    }
-  }
-  __syncthreads();
+  __shared__ int na_s;
   const long sb0 = (long)b * A.cap;
   const double* AT = A.atoms + sb0 * nm;
-  for (int pos = warp; pos < pst.na; pos += Cta<EPT, PK, NT>::NW) {
-    const double* row = AT + (long)__ldcg(A.act + sb0 + pos) * nm;
-    double sc = 0.0, dd = 0.0;
-    for (int i = lane; i < nm; i += 32) {
-      const double v = row[i];
-      const bool src = i < n;
-      const double tw = src ? ta_s[i] : tb_s[i - n];
-      const double nv = src ? nr_s[i] : ns_s[i - n];
-      sc = fma(v, tw, sc);
-      dd = bops::dmax(dd, fabs(v - nv));
-    }
-    sc = warp_sum(sc);
-    dd = bops::warp_dmax(dd);
-    if (lane == 0) {
-      A.scs[sb0 + pos] = sc;
-      A.dis[sb0 + pos] = dd;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    double best = CUDART_INF;
-    int bp = 0x7fffffff, hp = 0x7fffffff;
-    for (int pos = lane; pos < pst.na; pos += 32) {
-      const double sc = __ldcg(A.scs + sb0 + pos);
-      if (sc < best) {  // positions ascend per lane: first minimum kept
-        best = sc;
-        bp = pos;
-      }
-      if (hp == 0x7fffffff && __ldcg(A.dis + sb0 + pos) < 1e-12) hp = pos;
-    }
+  double* wts = pst.wts;
+  int* act = pst.act;
+  // Scores <atom, (ta, tb)> and sup-norm distances to the new atom, all
+  // threads sharing each stored row: a thread reads exactly the elements it
+  // wrote (same ownership as the registers), PFW_CH atoms per block reduction
+  // (sums only: the sup-norm test |atom - new| < 1e-12 is a count of the
+  // elements that fail it), and every thread tracks the away atom (lowest
+  // score, lowest position on ties) and the first atom within 1e-12 of the
+  // new one from the bit-identical reduced values.
+  constexpr int CH = PFW_CH;
+  double best = CUDART_INF;
+  int bp = 0x7fffffff, hp = 0x7fffffff;
+  for (int p0 = 0; p0 < pst.na; p0 += CH) {
+    double sd[2 * CH];  // scores, then counts of elements farther than 1e-12
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (ob < best || (ob == best && op < bp)) {
-        best = ob;
-        bp = op;
+    for (int k = 0; k < CH; ++k) {
+      double sck = 0.0;
+      int far = 0;
+      if (p0 + k < pst.na) {
+        const double* row = AT + (long)act[p0 + k] * nm;
+#pragma unroll (EPT <= 32 ? EPT : 1)
+        for (int e = 0; e < EPT; ++e) {
+          const int i = c.src(e);
+          if (i < n) {
+            const double v = row[i];
+            sck = fma(v, ta[e], sck);
+            far += !(fabs(v - r[e]) < 1e-12);
+          }
+          if (i < m) {
+            const double v = row[n + i];
+            sck = fma(v, tb[e], sck);
+            far += !(fabs(v - s[e]) < 1e-12);
+          }
+        }
       }
-      hp = min(hp, __shfl_xor_sync(0xffffffffu, hp, o));
+      sd[k] = sck;
+      sd[CH + k] = (double)far;
     }
-    if (lane == 0) {
-      away_s = bp;
-      hit_s = hp == 0x7fffffff ? -1 : hp;
+    bops::block_sum<CT::NW, 2 * CH>(sd, ping.next());
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      if (p0 + k < pst.na) {
+        if (sd[k] < best) {  // positions ascend: the first minimum is kept
+          best = sd[k];
+          bp = p0 + k;
+        }
+        if (hp == 0x7fffffff && sd[CH + k] == 0.0) hp = p0 + k;
+      }
     }
   }
-  __syncthreads();
   const long tix = (long)b * A.max_iters + t;
   const bool replay = A.away_in != nullptr && A.step_in != nullptr;
-  const int away = replay ? max(__ldg(A.away_in + tix), 0) : away_s;
-  const int hit = hit_s;
-  const int aslot = __ldcg(A.act + sb0 + away);
+  const int away = replay ? max(__ldg(A.away_in + tix), 0) : bp;
+  const int hit = hp == 0x7fffffff ? -1 : hp;
+  const int aslot = act[away];
   const double* ra = AT + (long)aslot * nm;
   double dA[EPT], dB[EPT];
-  double mom[4] = {0.0, 0.0, 0.0, 0.0};
-  double mxs[4] = {0.0, 0.0, -CUDART_INF, -CUDART_INF};
+  double mom[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // [4]: elements of the direction above 1e-12
+  double mxs[2] = {-CUDART_INF, -CUDART_INF};
+  int farn = 0;
 #pragma unroll (EPT <= 32 ? EPT : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = c.src(e);
@@ -546,17 +540,18 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
     mom[1] += ta[e] * va * va;
     mom[2] += tb[e] * vb;
     mom[3] += tb[e] * vb * vb;
-    mxs[0] = bops::dmax(mxs[0], fabs(dA[e]));
-    mxs[1] = bops::dmax(mxs[1], fabs(dB[e]));
-    if (i < n && sal[i] > 0.0) mxs[2] = bops::dmax(mxs[2], -va);
-    if (i < m && sbe[i] > 0.0) mxs[3] = bops::dmax(mxs[3], -vb);
+    farn += !(fabs(dA[e]) < 1e-12);
+    farn += !(fabs(dB[e]) < 1e-12);
+    if (i < n && sal[i] > 0.0) mxs[0] = bops::dmax(mxs[0], -va);
+    if (i < m && sbe[i] > 0.0) mxs[1] = bops::dmax(mxs[1], -vb);
   }
-  bops::block_red<Cta<EPT, PK, NT>::NW, 4, 4>(mom, mxs, ping.next());
-  const double gmax = __ldcg(A.wts + sb0 + aslot);
+  mom[4] = (double)farn;
+  bops::block_red<Cta<EPT, PK, NT>::NW, 5, 2>(mom, mxs, ping.next());
+  const double gmax = wts[aslot];
   double gam = 0.0;
   if (replay) {  // the reference's away atom and transfer (no step: away < 0)
     gam = __ldg(A.away_in + tix) < 0 ? 0.0 : __ldg(A.step_in + tix);
-  } else if (!(gmax <= 0.0 || (mxs[0] < 1e-12 && mxs[1] < 1e-12))) {  // fw.py:291-293
+  } else if (!(gmax <= 0.0 || mom[4] == 0.0)) {  // fw.py:291-293
     // minimise phi(gamma) = t1 LSE_a(u - gamma va) + t2 LSE_b(u' - gamma vb)
     // on [0, gmax]; centred moments as in the FW line search
     const double ca = mom[0] / mta, cb = mom[2] / mtb;
@@ -567,8 +562,8 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
       double lo = 0.0, hi = gmax;
       gam = (d2 > 0.0) ? fmin(gmax, -k0 / d2) : gmax;
       for (int it = 0; it < 32; ++it) {
-        const double pha = sha + gam * mxs[2];
-        const double phb = shb + gam * mxs[3];
+        const double pha = sha + gam * mxs[0];
+        const double phb = shb + gam * mxs[1];
         double mm[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll (EPT <= 32 ? EPT : 1)
         for (int e = 0; e < EPT; ++e) {
@@ -621,8 +616,8 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
       }
     }
     if (threadIdx.x == 0) {
-      double* w = A.wts + sb0;
-      int* ac = A.act + sb0;
+      double* w = wts;
+      int* ac = act;
       w[aslot] = fmax(w[aslot] - gam, 0.0);
       int na = pst.na;
       if (hit >= 0) {
@@ -644,8 +639,8 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
       f[e] += gam * dA[e];
       g[e] += gam * dB[e];
     }
-    if (sha > -CUDART_INF) sha += gam * mxs[2];
-    if (shb > -CUDART_INF) shb += gam * mxs[3];
+    if (sha > -CUDART_INF) sha += gam * mxs[0];
+    if (shb > -CUDART_INF) shb += gam * mxs[1];
     __syncthreads();
     pst.na = na_s;
   }
@@ -767,8 +762,13 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   int status = 0;
   int iters = 0;
   double last_primal = 0.0, last_dual = 0.0;
-  PfwState pst{1, 1};
+  __shared__ double pfw_wts_s[PW ? PFW_CAP_S : 1];
+  __shared__ int pfw_act_s[PW ? PFW_CAP_S : 1];
+  PfwState pst{1, 1, nullptr, nullptr};
   if constexpr (PW) {  // store = {(f0, g0)} with weight 1 (fw.py:332)
+    const bool ins = A.cap <= PFW_CAP_S;
+    pst.wts = ins ? pfw_wts_s : A.wts + (long)b * A.cap;
+    pst.act = ins ? pfw_act_s : A.act + (long)b * A.cap;
     double* row = A.atoms + (long)b * A.cap * (n + m);
 #pragma unroll (EPT <= 32 ? EPT : 1)
     for (int e = 0; e < EPT; ++e) {
@@ -777,8 +777,8 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
       if (i < m) row[n + i] = g[e];
     }
     if (threadIdx.x == 0) {
-      A.act[(long)b * A.cap] = 0;
-      A.wts[(long)b * A.cap] = 1.0;
+      pst.act[0] = 0;
+      pst.wts[0] = 1.0;
     }
     __syncthreads();
   }
@@ -1070,11 +1070,12 @@ inline int ept_for_big(int nm) {
 }
 
 // Per-problem array bytes: supports, cumulative masses, weights (3 (n + m)
-// doubles), merge ranks (rk_bytes each) and, for pairwise, the new atom's
-// staging (n + m doubles).
+// doubles) and merge ranks (rk_bytes each).  (At n = m = 4096 that is 213,008 B
+// of dynamic shared memory; with the kernels' static 3.3 KB -- 15.6 KB for
+// pairwise, whose slot weights and active list sit there -- still under 227 KB.)
 inline size_t fw_smem(int n, int m, bool pairwise, size_t rk_bytes = 2) {
-  return sizeof(double) * 3 * (size_t)(n + m) + rk_bytes * (size_t)(n + m) +
-         (pairwise ? 16 + sizeof(double) * (size_t)(n + m) : 0);
+  (void)pairwise;  // (the pairwise step no longer stages the new atom on chip)
+  return sizeof(double) * 3 * (size_t)(n + m) + rk_bytes * (size_t)(n + m) + 16;
 }
 
 constexpr size_t FW_SMEM_MAX = 227 * 1024;
