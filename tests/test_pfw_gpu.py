@@ -76,3 +76,18 @@ def test_pfw_reaches_fw_optimum():
     # both duals sit below the common optimum by at most their own pd gap
     assert abs(hp - hl) <= max(gp, gl) + 1e-12 * abs(hl)
     assert gp <= gl  # pairwise converges linearly, FW sublinearly
+
+
+def test_pfw_store_in_workspace_equals_shared():
+    """Slot weights and the active list sit in shared memory up to 1024 slots
+    (max_iters < 1024) and in the workspace beyond (fw1d_kernel.cuh: PFW_CAP_S);
+    the arithmetic is the same, so the first 1000 iterations of a 1100-iteration
+    run are bit-identical to a 1000-iteration run."""
+    z = golden("pfw.npz")
+    x, y, a, b, r1, r2, p, _ = _case(z, 2)
+    rs = F.fw_solve_batched(x, y, a, b, r1, r2, p, 1000, "pairwise")
+    rw = F.fw_solve_batched(x, y, a, b, r1, r2, p, 1100, "pairwise")
+    assert int(rs.status[0].item()) == 0 and int(rw.status[0].item()) == 0
+    np.testing.assert_array_equal(D.to_np(rw.h0[0])[:1000], D.to_np(rs.h0[0]))
+    np.testing.assert_array_equal(D.to_np(rw.natoms[0])[:1000], D.to_np(rs.natoms[0]))
+    np.testing.assert_array_equal(D.to_np(rw.step_size[0])[:1000], D.to_np(rs.step_size[0]))
