@@ -99,7 +99,8 @@ struct MotArgs {
   int cap;                // events per bucket: the regular-sampling bound (bucket_bound)
   int b0;                 // first problem of this launch (problem groups on streams)
   int upd_s;              // update by mot_update_s (the batch runs ungrouped: < 16 problems)
-  int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1, parity tests)
+  int no_bin;             // 1: merge path only (UOT_MOT_NOBIN=1), 2: coarse bins only
+                          // (UOT_MOT_COARSEBIN=1) -- parity tests
   int all_states;         // 1: mot_plan keeps every state (zero-mass ones too) and the
                           //    balanced sweep skips its duals (custom tuple costs)
   int cost_given;         // 1: mot_duals takes dcc[q][0] as given (custom tuple costs)
@@ -915,8 +916,98 @@ __device__ int merge_runs16(const double* key, uint16_t* code0, uint16_t* code1,
 // (heavily tied or clustered keys): the caller then merges instead.
 constexpr int BINMAX = 64;
 
+// Fast path (total <= BIN_EV events per thread, the cfg5 regime): one bin per
+// event on average, two 16-bit counters packed per word (same buffer as the
+// coarse path); the counting atomic's return value is the event's arrival
+// rank in its bin, so the scatter needs no second atomic pass, and most bins
+// hold one event, so little is left for the insertion sort.
+constexpr int BIN_EV = 8;
+
+__device__ __forceinline__ int bin_get(const int* binc, int i) {
+  return (binc[i >> 1] >> ((i & 1) * 16)) & 0xffff;
+}
+
+__device__ int bin_sort_fine(const double* key0, uint16_t* code1, int* binc, int total, double kmin,
+                             double span, int* over_s, int* wsum) {
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int NB = total;
+  for (int i = tid; i < ((NB + 1) >> 1); i += bd) binc[i] = 0;
+  __syncthreads();
+  const double scale = (double)NB / span;
+  int bi_r[BIN_EV], rk_r[BIN_EV];
+#pragma unroll
+  for (int u = 0; u < BIN_EV; ++u) {
+    const int e = tid + u * bd;
+    bi_r[u] = 0;
+    rk_r[u] = 0;
+    if (e < total) {
+      const int bi = min(NB - 1, (int)((key0[e] - kmin) * scale));
+      const int sh = (bi & 1) * 16;
+      const int old = atomicAdd(&binc[bi >> 1], 1 << sh);
+      bi_r[u] = bi;
+      rk_r[u] = (old >> sh) & 0xffff;
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the bin counts: an even number of bins per thread, so no
+  // two threads share a packed word
+  const int per = (((NB + bd - 1) / bd) + 1) & ~1;
+  const int b0 = min(NB, tid * per), b1 = min(NB, b0 + per);
+  int loc = 0, big = 0;
+  for (int i = b0; i < b1; ++i) {
+    const int c = bin_get(binc, i);
+    loc += c;
+    big = max(big, c);
+  }
+  if (big > BINMAX) *over_s = 1;
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (*over_s) return 0;
+  int off = incl - loc;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  for (int i = b0; i < b1; i += 2) {  // counts -> starts, a packed word at a time
+    const int wv = binc[i >> 1];
+    const int c0 = wv & 0xffff, c1 = (wv >> 16) & 0xffff;
+    binc[i >> 1] = off | ((off + c0) << 16);
+    off += c0 + c1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < BIN_EV; ++u) {
+    const int e = tid + u * bd;
+    if (e < total) code1[bin_get(binc, bi_r[u]) + rk_r[u]] = (uint16_t)e;
+  }
+  __syncthreads();
+  // insertion sort of every bin by (key, gather position)
+  for (int i = tid; i < NB; i += bd) {
+    const int st = bin_get(binc, i), en = i + 1 < NB ? bin_get(binc, i + 1) : total;
+    for (int a = st + 1; a < en; ++a) {
+      const uint16_t c = code1[a];
+      const double k = key0[c];
+      int j = a - 1;
+      while (j >= st) {
+        const uint16_t cj = code1[j];
+        const double kj = key0[cj];
+        if (!(kj > k || (kj == k && cj > c))) break;
+        code1[j + 1] = cj;
+        --j;
+      }
+      code1[j + 1] = c;
+    }
+  }
+  __syncthreads();
+  return 1;
+}
+
 __device__ int bin_sort(const double* key0, uint16_t* code1, int* binc, const int* rb, int K,
-                        int total) {
+                        int total, bool bin_coarse) {
   __shared__ double kmin_s, kmax_s;
   __shared__ int over_s;
   const int tid = threadIdx.x;
@@ -933,6 +1024,13 @@ __device__ int bin_sort(const double* key0, uint16_t* code1, int* binc, const in
       kmax_s = mx;
       over_s = 0;
     }
+  }
+  __shared__ int wsum[32];
+  if (total <= BIN_EV * (int)blockDim.x && total < 65536 && !bin_coarse) {
+    __syncthreads();
+    const double kmin = kmin_s, span = kmax_s - kmin_s;
+    if (!(span > 0.0)) return 0;
+    return bin_sort_fine(key0, code1, binc, total, kmin, span, &over_s, wsum);
   }
   const int NB = max(1, total >> 1);
   for (int i = tid; i < NB; i += blockDim.x) binc[i] = 0;
@@ -954,7 +1052,6 @@ __device__ int bin_sort(const double* key0, uint16_t* code1, int* binc, const in
     big = max(big, binc[i]);
   }
   if (big > BINMAX) over_s = 1;
-  __shared__ int wsum[32];
   const int lane = tid & 31, warp = tid >> 5;
   int incl = loc;
 #pragma unroll
@@ -1098,7 +1195,7 @@ __global__ void __launch_bounds__(BT2) mot_bucket(MotArgs A) {
   int* binc = reinterpret_cast<int*>(
       (reinterpret_cast<uintptr_t>(qt + cap) + 15) & ~static_cast<uintptr_t>(15));
   const uint16_t* code = c1;
-  if (A.no_bin || !bin_sort(key0, c1, binc, cnt_s, K, total))
+  if (A.no_bin == 1 || !bin_sort(key0, c1, binc, cnt_s, K, total, A.no_bin == 2))
     code = merge_runs16(key0, c0, c1, cnt_s, K, total) ? c1 : c0;
   BKT_STAMP(2);
   const int per = (total + BT2 - 1) / BT2;
@@ -2738,7 +2835,7 @@ MotArgs make_args(int batch, int k, int n, const MotPlan& p, char* ws, const dou
   a.S = p.S;
   a.SS = p.SS;
   a.cap = p.cap;
-  a.no_bin = env_flag("UOT_MOT_NOBIN") ? 1 : 0;
+  a.no_bin = env_flag("UOT_MOT_NOBIN") ? 1 : env_flag("UOT_MOT_COARSEBIN") ? 2 : 0;
   a.ta = (double*)(ws + L.off[0]);
   a.A = (double*)(ws + L.off[1]);
   a.dcc = (double*)(ws + L.off[2]);

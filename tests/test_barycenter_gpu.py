@@ -189,14 +189,15 @@ def test_fw_barycenter_report_vs_reference(k):
 
 
 # ---------------------------------------------------------------------------
-# Kernel variants of the sweep (csrc/mot1d.cu): the bin sort and its merge-path
-# fallback order the events identically (the (value, list, index) order is
+# Kernel variants of the sweep (csrc/mot1d.cu): the fine bin sort (default), the
+# coarse one (UOT_MOT_COARSEBIN=1, also the path of buckets above 8 events per
+# thread) and the merge-path fallback order the events identically (the (value, list, index) order is
 # total), and the three update kernels (mot_update_s, the default of small
 # batches; mot_update2 with UOT_MOT_UPDATES=0; mot_update with
 # UOT_MOT_UPDATE1=1) compute the same iterates; clustered keys (zero-weight runs repeat breakpoints) and ties
 # across lists (identical inputs) exercise the fallback and the tie rule.
-@pytest.mark.parametrize("env,val", [("UOT_MOT_NOBIN", "1"), ("UOT_MOT_UPDATE1", "1"),
-                                     ("UOT_MOT_UPDATES", "0")])
+@pytest.mark.parametrize("env,val", [("UOT_MOT_NOBIN", "1"), ("UOT_MOT_COARSEBIN", "1"),
+                                     ("UOT_MOT_UPDATE1", "1"), ("UOT_MOT_UPDATES", "0")])
 def test_sweep_variants_agree(monkeypatch, env, val):
     xs, ws = S.cfg5_batch(count=3, n=2048)
     ws[1, :, 100:400] = 0.0          # zero-weight runs: repeated breakpoints
@@ -206,7 +207,7 @@ def test_sweep_variants_agree(monkeypatch, env, val):
     # the two update kernels associate their block / cluster sums differently:
     # compared on harmonic steps (a fixed gamma schedule); the merge fallback
     # orders the same keys, compared on line-search runs
-    step = "linesearch" if env == "UOT_MOT_NOBIN" else "harmonic"
+    step = "linesearch" if env in ("UOT_MOT_NOBIN", "UOT_MOT_COARSEBIN") else "harmonic"
     base = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
     monkeypatch.setenv(env, val)
     alt = P.fw_barycenter_batched(xs, ws, w, 1.0, 15, step, trace_support=True)
@@ -214,7 +215,7 @@ def test_sweep_variants_agree(monkeypatch, env, val):
     assert (D.to_np(base.status) == 0).all() and (D.to_np(alt.status) == 0).all()
     np.testing.assert_array_equal(D.to_np(base.supp_hash), D.to_np(alt.supp_hash))
     f0, f1 = D.to_np(base.f), D.to_np(alt.f)
-    tol = 1e-14 if env == "UOT_MOT_NOBIN" else 1e-13
+    tol = 1e-14 if env in ("UOT_MOT_NOBIN", "UOT_MOT_COARSEBIN") else 1e-13
     assert np.abs(f0 - f1).max() <= tol * np.abs(f0).max()
     np.testing.assert_allclose(D.to_np(alt.h0), D.to_np(base.h0), rtol=max(tol, 1e-13))
     c = D.to_np(base.count)
