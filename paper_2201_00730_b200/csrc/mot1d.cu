@@ -1116,6 +1116,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+// all but the most recent committed group have landed
+__device__ __forceinline__ void cp_async_wait_but_last() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
@@ -1691,8 +1699,10 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   double* fB = rows + MT * EPT;
   double* wB = rows + 2 * MT * EPT;
   SW::fill(rB, A.dcc + baseb, nb);
+  cp_async_commit();  // the increments first: the prefix scan starts while f and w are in flight
   SW::fill(fB, A.f + baseb, nb);
   SW::fill(wB, A.a + baseb, nb);
+  cp_async_commit();
   double rv[EPT], fv[EPT], wv[EPT];
   load_run<EPT>(A.dcc + basea, i0, na, rv);
   load_run<EPT>(A.f + basea, i0, na, fv);
@@ -1708,7 +1718,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
     }
     if (lane == 0) cc0_s = cc;
   }
-  cp_async_wait_all();
+  cp_async_wait_but_last();
   __syncthreads();
   MOT_STAMP(1);
   // dual atoms: prefix sums of the cost increments (dcc[0] is not an event)
@@ -1745,6 +1755,8 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
       *p = make_double2(x0, lb + offb);
     }
   }
+  cp_async_wait_all();  // f and w rows
+  __syncthreads();
   const double rqa = A.omega[qa] * A.rho, rqb = A.omega[qb] * A.rho;
   const double irqa = 1.0 / rqa, irqb = 1.0 / rqb;
   const double lama = A.lam[(long)b * K + qa], lamb = A.lam[(long)b * K + qb];
@@ -2024,8 +2036,10 @@ __global__ void __launch_bounds__(MT, 1) mot_update_s(MotArgs A) {
   double* fB = rows + MT * EPT;
   double* wB = rows + 2 * MT * EPT;
   SW::fill(rB, A.dcc + base, nq);
+  cp_async_commit();  // the increments first: the prefix scan starts while f and w are in flight
   SW::fill(fB, A.f + base, nq);
   SW::fill(wB, A.a + base, nq);
+  cp_async_commit();
   if (tid < 32) {  // f_1[0] = Cc(first tuple) (barycenter.py:206-207)
     const int lane = tid;
     double cc = 0.0;
@@ -2037,7 +2051,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update_s(MotArgs A) {
     }
     if (lane == 0) cc0_s = cc;
   }
-  cp_async_wait_all();
+  cp_async_wait_but_last();
   __syncthreads();
   MOT_STAMP(1);
   // dual atoms: prefix sums of the cost increments (dcc[0] is not an event)
@@ -2066,6 +2080,8 @@ __global__ void __launch_bounds__(MT, 1) mot_update_s(MotArgs A) {
       *p = make_double2(x0, lb + offb);
     }
   }
+  cp_async_wait_all();  // f and w rows
+  __syncthreads();
   const double rq = A.omega[q] * A.rho, irq = 1.0 / rq;
   const double lamq = A.lam[(long)b * K + q];
   double acc[6] = {0, 0, 0, 0, 0, 0};
