@@ -55,7 +55,7 @@ constexpr int BT = UOT_BT;  // threads of the bucket CTAs
 constexpr int BT2 = UOT_BT2;  // threads of the cost-increment bucket CTAs (mot_bucket)
 constexpr int KMAX = 32;          // lists per problem (16-CTA clusters of two lists each)
 constexpr int ST = 1024;          // threads of the per-problem splitter CTA
-constexpr int SMAX = 192;         // buckets per problem
+constexpr int SMAX = 768;         // buckets per problem
 
 struct MotArgs {
   int batch, k, n;        // n = row stride (max list length)
@@ -126,14 +126,14 @@ template <int EPT>
 __device__ __forceinline__ void load_run(const double* row, int i0, int nq, double (&v)[EPT]) {
   if (EPT % 2 == 0 && i0 + EPT <= nq && ((reinterpret_cast<uintptr_t>(row + i0) & 15) == 0)) {
     const double2* p = reinterpret_cast<const double2*>(row + i0);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT / 2) : 1)
     for (int e = 0; e < EPT / 2; ++e) {
       const double2 u = p[e];
       v[2 * e] = u.x;
       v[2 * e + 1] = u.y;
     }
   } else {
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) v[e] = i0 + e < nq ? row[i0 + e] : 0.0;
   }
 }
@@ -142,10 +142,10 @@ template <int EPT>
 __device__ __forceinline__ void store_run(double* row, int i0, int nq, const double (&v)[EPT]) {
   if (EPT % 2 == 0 && i0 + EPT <= nq && ((reinterpret_cast<uintptr_t>(row + i0) & 15) == 0)) {
     double2* p = reinterpret_cast<double2*>(row + i0);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT / 2) : 1)
     for (int e = 0; e < EPT / 2; ++e) p[e] = make_double2(v[2 * e], v[2 * e + 1]);
   } else {
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e)
       if (i0 + e < nq) row[i0 + e] = v[e];
   }
@@ -299,12 +299,12 @@ __device__ __forceinline__ void list_lse(const double (&w)[EPT], const double (&
                                          const double* tab, double* red0, double* red1, double& mx,
                                          double& qk, double (&ew)[EPT]) {
   double m1[1] = {-CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e)
     if (w[e] > 0.0) m1[0] = bops::dmax(m1[0], -fv[e] * irq);
   bops::block_max<MNW, 1>(m1, red0);
   double s1[1] = {0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     ew[e] = bops::wexp(w[e], -fv[e] * irq - m1[0], tab);
     s1[0] += ew[e];
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(MT) mot_lse(MotArgs A) {
   load_run<EPT>(A.a + base, threadIdx.x * EPT, nq, w);
   load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
   double ms[1] = {0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) ms[0] += w[e];
   double mx, qk;
   list_lse<EPT>(w, fv, irq, tab, red, red + MBUF, mx, qk, fv);
@@ -438,7 +438,7 @@ template <int EPT>
 __device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v)[EPT]) {
   constexpr int RUN = StageRun<EPT>::RUN;
   const double2* p = reinterpret_cast<const double2*>(buf + threadIdx.x * RUN);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT / 2) : 1)
   for (int e = 0; e < EPT / 2; ++e) {
     const double2 u = p[e];
     v[2 * e] = u.x;
@@ -446,7 +446,7 @@ __device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v
   }
   const int i0 = threadIdx.x * EPT;
   if (i0 + EPT > nq) {
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e)
       if (i0 + e >= nq) v[e] = 0.0;
   }
@@ -457,7 +457,7 @@ __device__ __forceinline__ void stage_load(const double* buf, int nq, double (&v
 template <int EPT>
 __device__ __forceinline__ void stage_put(double* buf, const double (&v)[EPT]) {
   double2* p = reinterpret_cast<double2*>(buf + threadIdx.x * StageRun<EPT>::RUN);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT / 2) : 1)
   for (int e = 0; e < EPT / 2; ++e) p[e] = make_double2(v[2 * e], v[2 * e + 1]);
 }
 
@@ -502,18 +502,18 @@ __device__ __forceinline__ void tilt_tail(const MotArgs& A, int b, int q, int nq
     store_run<EPT>(A.ta + base, i0, nq, ta);
   double av[EPT];
   double loc = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     loc += ta[e];
     av[e] = loc;
   }
   double v[1] = {loc}, tot[1];
   bops::block_scan_excl<MNW, 1>(v, tot, buf);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) av[e] = v[0] + av[e];
   int any0 = 0, lz = -1;
   double lzv = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     const int i = i0 + e;
     if (i < nq && ta[e] == 0.0) any0 = 1;
@@ -526,7 +526,7 @@ __device__ __forceinline__ void tilt_tail(const MotArgs& A, int b, int q, int nq
     int pi = lz;
     double pv = lzv;
     excl_last_pos(pi, pv, iscr, vscr);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = i0 + e;
       if (i < nq && ta[e] == 0.0) av[e] = pi >= 0 ? pv : 0.0;
@@ -562,7 +562,7 @@ __device__ __forceinline__ void tilt_tail(const MotArgs& A, int b, int q, int nq
     if (t >= i0 + EPT) break;
     if (t >= i0) {
       double val = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
       for (int e = 0; e < EPT; ++e)
         if (i0 + e == t) val = av[e];
       sv[j] = val;
@@ -602,10 +602,10 @@ __global__ void __launch_bounds__(MT) mot_tilt(MotArgs A) {
       if (q == 0) A.scal[b * 4 + 0] = ex1 - rtot * exp(ex0 / rtot);  // H_0, :320-327
     }
     const double sc = exp(mx - lamq * irq);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) ta[e] = bops::wexp(w[e], -fv[e] * irq - mx, tab) * sc;
   } else {
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) ta[e] = w[e];
   }
   tilt_tail<EPT>(A, b, q, nq, ta, red, iscr, vscr);
@@ -1306,18 +1306,18 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   }
   __syncthreads();
   if (threadIdx.x == 0) rv[0] = 0.0;  // dcc[0] is not an event
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     loc += rv[e];
     rv[e] = loc;
   }
   double tot;
   const double off = bscan1(loc, tot, scr) + cc0_s;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) rv[e] += off;
 
   if (A.mode == 1) {  // balanced sweep: the duals are the output
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) {
       const int i = threadIdx.x * EPT + e;
       if (i < nq) A.out_f[base + i] = rv[e];
@@ -1329,7 +1329,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   const double irq = 1.0 / rq;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   double mxs[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     const double d = rv[e] - fv[e];
     acc[0] += tv[e] * d;                 // fw_gap part (barycenter.py:376-381)
@@ -1395,7 +1395,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
       for (int it = 0; it < 24; ++it) {
         const double sh = (1.0 - gam) * mxs[0] + gam * mxs[1];
         double mom[3] = {0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
         for (int e = 0; e < EPT; ++e) {
           const double d = rv[e] - fv[e];
           const double ww = bops::wexp(wv[e], -(fv[e] + gam * d) * irq - sh, tab);
@@ -1432,7 +1432,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
   }
   // barycenter.py:409-411, rounded as numpy rounds it (two products, a sum)
   const double omg = 1.0 - gam;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) fv[e] = __dadd_rn(__dmul_rn(omg, fv[e]), __dmul_rn(gam, rv[e]));
   MOT_STAMP(4);
   if constexpr (StageRun<EPT>::ON) {  // coalesced: the stage buffer is free here
@@ -1463,7 +1463,7 @@ __global__ void __launch_bounds__(MT) mot_update(MotArgs A) {
         if (q == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
       }
       const double sc = exp(mx - lam1 * irq);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
       for (int e = 0; e < EPT; ++e) tv[e] *= sc;
       tilt_tail<EPT>(A, b, q, nq, tv, ping.next(), iscr, vscr,
                      StageRun<EPT>::ON ? stg : nullptr);
@@ -1724,7 +1724,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   // dual atoms: prefix sums of the cost increments (dcc[0] is not an event)
   if (tid == 0) rv[0] = 0.0;
   double sc2[2] = {0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     sc2[0] += rv[e];
     rv[e] = sc2[0];
@@ -1741,7 +1741,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
     bops::block_scan_excl<MNW, 2>(sc2, tot2, ping.next());
   }
   const double offa = sc2[0] + cc0_s, offb = sc2[1];
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) rv[e] += offa;
   {
     double lb = 0.0;  // list B: local inclusive prefix + offset, in place
@@ -1773,7 +1773,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   // lambda (bit-identical; no row round trip through HBM).
   const double mxa = A.lse[((long)b * K + qa) * 2 + 0], mxb = A.lse[((long)b * K + qb) * 2 + 0];
   const double tsa = exp(mxa - lama * irqa), tsb = exp(mxb - lamb * irqb);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     const double r = rv[e], f = fv[e], w = wv[e];
     const double tv = bops::wexp(w, -f * irqa - mxa, tab) * tsa;
@@ -1868,7 +1868,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
         const double sha = (1.0 - gam) * mxa0 + gam * mxa1;
         const double shb = (1.0 - gam) * mxb0 + gam * mxb1;
         double mom[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
         for (int e = 0; e < EPT; ++e) {
           const double d = rv[e] - fv[e];
           const double ww = bops::wexp(wv[e], -(fv[e] + gam * d) * irqa - sha, tab);
@@ -1922,7 +1922,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   MOT_STAMP(4);
   // barycenter.py:409-411, rounded as numpy rounds it (two products, a sum)
   const double omg = 1.0 - gam;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) fv[e] = __dadd_rn(__dmul_rn(omg, fv[e]), __dmul_rn(gam, rv[e]));
   store_run<EPT>(A.f + basea, i0, na, fv);
 #pragma unroll 2
@@ -1933,7 +1933,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   }
   // log-sum-exps of the new iterate (both lists; list_lse's arithmetic)
   double m2[2] = {-CUDART_INF, -CUDART_INF};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e)
     if (wv[e] > 0.0) m2[0] = bops::dmax(m2[0], -fv[e] * irqa);
 #pragma unroll 2
@@ -1945,7 +1945,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
   bops::block_max<MNW, 2>(m2, ping.next());
   double tv[EPT];
   double s2[2] = {0.0, 0.0};
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     tv[e] = bops::wexp(wv[e], -fv[e] * irqa - m2[0], tab);
     s2[0] += tv[e];
@@ -1985,7 +1985,7 @@ __global__ void __launch_bounds__(MT, 1) mot_update2(MotArgs A) {
       if (c == 0) A.scal[b * 4 + 0] = ex[1] - ex[2] * exp(ex[0] / ex[2]);
     }
     const double sca = exp(m2[0] - lam1a * irqa), scb = exp(m2[1] - lam1b * irqb);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
     for (int e = 0; e < EPT; ++e) tv[e] *= sca;
     tilt_tail<EPT>(A, b, qa, na, tv, ping.next(), iscr, vscr, nullptr, false);
     if (hasB) tilt_tail_smem<EPT>(A, b, qb, nb, rB, scb, ping.next(), iscr, vscr);
@@ -2267,14 +2267,14 @@ __global__ void __launch_bounds__(MT) mot_duals(MotArgs A) {
   // dcc[0] is not an event (custom costs: it holds f_q[0] = Cc(first tuple) or 0)
   if (threadIdx.x == 0 && !A.cost_given) rv[0] = 0.0;
   double loc = 0.0;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) {
     loc += rv[e];
     rv[e] = loc;
   }
   double tot;
   const double off = bscan1(loc, tot, scr) + cc0_s;
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) rv[e] += off;
   store_run<EPT>(A.out_f + base, threadIdx.x * EPT, nq, rv);
 }
@@ -2319,7 +2319,7 @@ __global__ void __launch_bounds__(MT) mot_finalize(MotArgs A) {
   const double lamq = problem_lambda(A, b, q, ex0, ex1, rtot);
   double fv[EPT];
   load_run<EPT>(A.f + base, threadIdx.x * EPT, nq, fv);
-#pragma unroll
+#pragma unroll (EPT <= 32 ? (EPT) : 1)
   for (int e = 0; e < EPT; ++e) fv[e] += lamq;
   store_run<EPT>(A.out_f + base, threadIdx.x * EPT, nq, fv);
 }
@@ -2571,8 +2571,14 @@ int ept_for(int n) {
   if (per <= 8) return 8;
   if (per <= 16) return 16;
   if (per <= 32) return 32;
+  // beyond 32 atoms per thread the per-atom loops stay rolled and the per-thread
+  // arrays live in local memory (a correctness path; K <= 16 only)
+  if (per <= 64) return 64;
+  if (per <= 128) return 128;
+  if (per <= 256) return 256;
   return -1;
 }
+constexpr int EPT_MAX = 256;
 
 // Largest possible bucket under regular sampling: list q has
 // SS samples at t_j = floor((j+1) ne / (SS+1)), consecutive samples (and the
@@ -2797,8 +2803,11 @@ int dispatch(const MotArgs& a, const MotPlan& p, cudaStream_t st, bool fw) {
     case 8: return run_all<8>(a, p, st, fw);
     case 16: return run_all<16>(a, p, st, fw);
     case 32: return run_all<32>(a, p, st, fw);
+    case 64: return run_all<64>(a, p, st, fw);
+    case 128: return run_all<128>(a, p, st, fw);
+    case 256: return run_all<256>(a, p, st, fw);
   }
-  set_error("lists longer than %d atoms are not supported", 32 * MT);
+  set_error("lists longer than %d atoms are not supported", EPT_MAX * MT);
   return UOT_INVALID;
 }
 
@@ -2897,7 +2906,7 @@ int check_sizes(int batch, int k, int n) {
     return UOT_INVALID;
   }
   if (ept_for(n) < 0) {
-    set_error("lists longer than %d atoms are not supported", 32 * MT);
+    set_error("lists longer than %d atoms are not supported", EPT_MAX * MT);
     return UOT_INVALID;
   }
   const MotPlan p = plan_for(k, n);

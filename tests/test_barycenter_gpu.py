@@ -274,3 +274,39 @@ def test_too_many_inputs_raise_like_a_limit():
     xs, ws = S.cfg5_batch(batch=1, k=33, n=64, count=1)
     with pytest.raises(ValueError):
         P.fw_barycenter_batched(xs, ws, np.full(33, 1 / 33), 1.0, 2, "harmonic")
+
+
+# ---------------------------------------------------------------------------
+# Lists beyond 16384 atoms (K <= 16): 64 / 128 / 256 atoms per thread with the
+# per-atom loops rolled (csrc/mot1d.cu: ept_for), up to 768 buckets per problem.
+@pytest.mark.parametrize("k,n", [(4, 20000), (3, 70001), (16, 40000)])
+def test_long_lists_vs_oracle(k, n):
+    xs, ws = S.cfg5_batch(batch=1, k=k, n=n, count=1, floor=1e-3)
+    w = np.full(k, 1.0 / k)
+    wb = ws / ws.sum(axis=2, keepdims=True)
+    f, idx, mass, count, st = P.solve_mot_1d_batched(xs, wb, w)
+    assert int(st[0].item()) == 0
+    ii, mm, pots = O.solve_mot_1d(list(xs[0]), list(wb[0]), w)
+    c = int(count[0].item())
+    np.testing.assert_array_equal(D.to_np(idx[0, :c]), ii)
+    np.testing.assert_allclose(D.to_np(mass[0, :c]), mm, rtol=0, atol=1e-13)
+    fd = D.to_np(f[0])
+    assert max(np.abs(fd[q] - pots[q]).max() for q in range(k)) <= 1e-10
+    its = 4
+    rh = P.fw_barycenter_batched(xs, ws, w, 1.0, its, "harmonic")
+    assert int(rh.status[0].item()) == 0
+    out = O.fw_barycenter_fixed(list(xs[0]), list(ws[0]), w, 1.0, its, step="harmonic")
+    np.testing.assert_allclose(D.to_np(rh.h0[0]), out["h0"], rtol=1e-9)
+    fh = D.to_np(rh.f[0])
+    scale = max(np.abs(v).max() for v in out["pots"])
+    assert max(np.abs(fh[q] - out["pots"][q]).max() for q in range(k)) <= 1e-9 * scale
+    rl = P.fw_barycenter_batched(xs, ws, w, 1.0, 3, "linesearch")
+    outl = O.fw_barycenter_fixed(list(xs[0]), list(ws[0]), w, 1.0, 3)
+    np.testing.assert_allclose(D.to_np(rl.h0[0]), outl["h0"], rtol=1e-9)
+
+
+def test_list_length_limit_message():
+    xs = np.sort(np.random.default_rng(0).uniform(size=(1, 2, 131073)), axis=2)
+    ws = np.full((1, 2, 131073), 1.0 / 131073)
+    with pytest.raises(ValueError, match="131072"):
+        P.solve_mot_1d_batched(xs, ws, np.full(2, 0.5))
