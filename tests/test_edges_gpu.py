@@ -127,8 +127,10 @@ def test_mot_limits_raise():
         P.solve_mot_1d([one] * 33, np.full(33, 1 / 33))  # K > 32 (two lists per CTA, 16-CTA clusters)
     P.solve_mot_1d([one] * 17, np.full(17, 1 / 17))  # 16 < K <= 32 runs
     big = P.DiscreteMeasure(np.linspace(0, 1, 16385), np.full(16385, 1 / 16385))
+    P.solve_mot_1d([big, big], np.array([0.5, 0.5]))  # up to 131072 atoms per list (K <= 16)
+    huge = P.DiscreteMeasure(np.linspace(0, 1, 131073), np.full(131073, 1 / 131073))
     with pytest.raises(ValueError):
-        P.solve_mot_1d([big, big], np.array([0.5, 0.5]))
+        P.solve_mot_1d([huge, huge], np.array([0.5, 0.5]))
 
 
 def test_barycenter_ragged_vs_oracle():
