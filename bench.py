@@ -340,6 +340,15 @@ def run_cfg3(args, rank, world, dev, comm):
                 f, g = step()
     ms_step = max_over_ranks(tt.ms / args.steps, world, dev)
     value = CFG3_ITERS * 1e3 / ms_step
+    # the same workload as one-iteration calls with a flush before every iteration (the
+    # step definition used until round 2's last session), for comparison only
+    fi = f
+    with cuda_timer() as t1:
+        for _ in range(20):
+            flush.zero_()
+            fi, _g, _, _ = P.sinkhorn_batched(x, y, a, b, c.eps, c.rho, c.rho, 1, variant="h",
+                                              precision="fp32", f0=fi, **kw)
+    ms_call = max_over_ranks(t1.ms / 20, world, dev)
 
     # roofline of the dominant kernel (fused cost + online LSE half-step),
     # timed live with CUDA events on the launching stream, on this rank's shard.
@@ -386,6 +395,8 @@ def run_cfg3(args, rank, world, dev, comm):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded 8-component 2-D Gaussian mixtures, BASELINE cfg3)",
         "config": cfg3_config(c, world), "l2_flush_ms": tf.ms,
+        "single_iteration_calls": {"value": 1e3 / ms_call, "unit": "iter/s", "ms_per_call": ms_call,
+                                   "note": "20 one-iteration calls, L2 flush before each"},
         "roofline": roof, "e2e": e2e,
         # per iteration: 2 main kernels + 2 tails (+ the combine when sharded), replayed from
         # the captured two-iteration graph; per solve: centre, zero, reset, finalize, ...
