@@ -652,7 +652,10 @@ __device__ double pfw_step(Cta<EPT, PK, NT>& c, const FwArgs& A, int b, int t, d
 // CTAs per SM).  NT = FW_THREADS_BIG: large problems -- the same arrays in the
 // global workspace (L2-resident per problem), 32-bit merge ranks, one CTA of
 // 1024 threads per problem.
-template <int EPT, int PK, bool PW, int NT = FW_THREADS>
+// FULL: n = m = NT * EPT exactly (cfg2: 1024 = 256 x 4) -- the sizes are
+// compile-time constants, so every bounds test on an owned element folds away
+// and the shared-memory sub-array offsets are immediates.
+template <int EPT, int PK, bool PW, int NT = FW_THREADS, bool FULL = false>
 __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kernel(FwArgs A) {
   constexpr int NW = NT / 32;
   constexpr int BUF = 16 * NW;  // one reduction buffer (doubles)
@@ -661,7 +664,8 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   __shared__ __align__(16) double red[3 * BUF];
   __shared__ double tab[32];
   const int b = blockIdx.x;
-  const int n = A.n, m = A.m;
+  const int n = FULL ? NT * EPT : A.n, m = FULL ? NT * EPT : A.m;
+  if constexpr (FULL) __builtin_assume(threadIdx.x < NT);
   double* base = smem;
   if constexpr (NT != FW_THREADS) base = reinterpret_cast<double*>(A.big + (size_t)b * A.big_stride);
   double* sx = base;
@@ -1178,6 +1182,14 @@ int launch_fw_impl(const FwArgs& a0, int batch, cudaStream_t st) {
       return eptb <= 16   ? launch_fw_big<PW, PK>(a, batch, st, eptb)
              : eptb <= 32 ? launch_fw_huge<PW, PK>(a, batch, st, eptb)
                           : launch_fw_giant<PW, PK>(a, batch, st, eptb);
+    if constexpr (PK == 0) {  // exact power-of-two sizes: constant-size instantiations
+      if (a.n == a.m && a.n == FW_THREADS * ept && !std::getenv("UOT_FW_NOFULL")) {
+        if (ept == 4) return go(fw1d_kernel<4, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
+        if (ept == 8) return go(fw1d_kernel<8, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
+        if constexpr (!PW)
+          if (ept == 16) return go(fw1d_kernel<16, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
+      }
+    }
     switch (ept) {
       case 1: return go(fw1d_kernel<1, PK, PW>, FW_THREADS, smem);
       case 2: return go(fw1d_kernel<2, PK, PW>, FW_THREADS, smem);

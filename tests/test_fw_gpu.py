@@ -150,3 +150,23 @@ def test_fw_solve_api_matches_oracle_with_early_exit():
     assert rel_err(rep.final.f, rep.final.g, out["f"], out["g"]) < 1e-9
     feas = float(P.feasibility_violation(a.points, b.points, rep.final.f, rep.final.g)[0].item())
     assert feas <= 1e-9 or rep.certificate.feasibility_violation <= 1e-9
+
+
+@pytest.mark.parametrize("step", ["linesearch", "harmonic", "pairwise"])
+def test_constant_size_instantiation_is_bit_identical(monkeypatch, step):
+    """n = m = 256 x EPT problems (cfg2: 1024) run on kernels instantiated with the
+    sizes as compile-time constants (fw1d_kernel.cuh: FULL); only bounds tests fold
+    away, so the results equal the general kernel's bit for bit."""
+    for n in (1024, 2048):
+        x, y, a, b = S.cfg2_batch(batch=3, n=n, m=n, count=3, seed=11)
+        a[1, 5:40] = 0.0  # zero-weight atoms too
+        r0 = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 25, step)
+        monkeypatch.setenv("UOT_FW_NOFULL", "1")
+        r1 = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 25, step)
+        monkeypatch.delenv("UOT_FW_NOFULL")
+        for k in ("f", "g", "h0", "fw_gap", "pd_gap"):
+            np.testing.assert_array_equal(D.to_np(getattr(r0, k)), D.to_np(getattr(r1, k)))
+        c = D.to_np(r0.count)
+        np.testing.assert_array_equal(c, D.to_np(r1.count))
+        for p in range(3):
+            np.testing.assert_array_equal(D.to_np(r0.ei[p, :c[p]]), D.to_np(r1.ei[p, :c[p]]))
