@@ -55,8 +55,9 @@ int launch_fw(const FwArgs& a0, int batch, cudaStream_t st) {
   return launch_fw_impl<false>(a, batch, st);
 }
 
-// pairwise atom store: atoms [batch][cap][n+m], wts / scs / dis [batch][cap]
-// doubles, act [batch][cap] ints; cap = max_iters + 1
+// pairwise atom store: atoms [batch][cap][n+m] doubles; beyond PFW_CAP_S slots
+// also the slot weights [batch][cap] (doubles) and the active list [batch][cap]
+// (ints), which otherwise live in shared memory; cap = max_iters + 1
 size_t pfw_store_bytes(int batch, int n, int m, int max_iters) {
   const size_t cap = (size_t)max_iters + 1;
   return sizeof(double) * (size_t)batch * cap * (n + m) +
@@ -183,9 +184,7 @@ extern "C" int uot_fw1d_run(const uot_fw_desc* d, void* ws, size_t ws_bytes, voi
     a.atoms = (double*)p;
     p += sizeof(double) * bc * (d->n + d->m);
     a.wts = (double*)p;
-    a.scs = a.wts + bc;
-    a.dis = a.scs + bc;
-    a.act = (int*)(a.dis + bc);
+    a.act = (int*)(a.wts + bc);
   }
   return launch_fw(a, d->batch, (cudaStream_t)stream);
 }

@@ -73,8 +73,6 @@ struct FwArgs {
   double* atoms;  // [batch][cap][n+m] (r | s) rows
   double* wts;    // [batch][cap] weight of each slot
   int* act;       // [batch][cap] active slots in insertion order
-  double* scs;    // [batch][cap] scores of the active atoms (per position)
-  double* dis;    // [batch][cap] sup-norm distance to the new atom
   int* natoms;    // optional [batch][max_iters] trace
   const double* ref_f;  // optional [batch][n]: reference potential
   double* err_f;        // optional [batch][max_iters]: sup error of the translated iterate
@@ -167,7 +165,6 @@ struct Cta {
   RK* rkB;  // rkB[l] = #source events before target event l
   double* zred;  // scratch of the zero-weight fix (own syncs)
   bool zeros;  // the problem has zero-weight atoms (exact-repeat fix needed)
-  double* pfw;   // pairwise FW staging (n + m doubles) or nullptr
   const double* cm = nullptr;  // PK == 3: this problem's [n][m] cost matrix
 
   // C(i, j): the cost at source i, target j (src/ot1d.py:92-109)
@@ -676,10 +673,7 @@ __global__ void __launch_bounds__(NT, NT == FW_THREADS ? FW_MINB : 1) fw1d_kerne
   double* sbe = sal + n;
   RK* rkA = reinterpret_cast<RK*>(sbe + m);
   RK* rkB = rkA + n;
-  double* pfwbuf = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(rkB + m) + 15) & ~static_cast<uintptr_t>(15));
-  Cta<EPT, PK, NT> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * BUF, false,
-                     PW ? pfwbuf : nullptr};
+  Cta<EPT, PK, NT> c{n, m, A.p, sx, sy, sA, sB, rkA, rkB, red + 2 * BUF, false};
   if constexpr (PK == 3) c.cm = A.C + (long)b * n * m;
   bops::Ping<BUF> ping{red, 0};
   bops::load_exp_table(tab);
