@@ -62,3 +62,38 @@ def test_eval_primal_sparse_dense_balanced_and_inf():
     A = P.DiscreteMeasure(x, [0.2, 0.0, 0.3, 0.2, 0.3])
     prob = P.UotProblem(A, A, P.PowerDistance(2.0), P.KL(1.0), P.KL(1.0), eps=0.0)
     assert P.eval_primal(prob, np.diag([0.2, 0.1, 0.3, 0.2, 0.2])) == float(z["inf_primal"])
+
+
+def test_eval_primal_large_dense_plan():
+    """Dense plans with many entries take the grid-parallel path (csrc/dense.cu:
+    eval_primal_entries, marginals by fp64 atomics); checked against the formula
+    of src/duality.py:320-344 written out in numpy, and timed loosely: the one-CTA
+    kernel needed ~1 s at 2048 x 2048."""
+    import time
+
+    rng = np.random.default_rng(4)
+    n, m, eps, r1, r2 = 900, 1300, 0.07, 0.8, 1.7
+    x, y = np.sort(rng.uniform(0, 1, n)), np.sort(rng.uniform(0, 1, m))
+    a, b = rng.exponential(1.0, n), rng.exponential(1.0, m)
+    C = (x[:, None] - y[None, :]) ** 2
+    plan = np.outer(a, b) * np.exp(-C / eps) * rng.uniform(0.5, 1.5, (n, m))
+    prob = P.UotProblem(P.DiscreteMeasure(x, a), P.DiscreteMeasure(y, b), P.PowerDistance(2.0),
+                        P.KL(r1), P.KL(r2), eps)
+
+    def kl(p, q):
+        return float(np.sum(p * np.log(p / q) - p + q))
+
+    want = (float(np.sum(plan * C)) + eps * kl(plan, np.outer(a, b)) + r1 * kl(plan.sum(1), a)
+            + r2 * kl(plan.sum(0), b))
+    got = P.eval_primal(prob, plan)
+    assert abs(got - want) <= 1e-11 * abs(want)
+    big = np.ones((2048, 2048)) / 2048.0 ** 2
+    u = np.linspace(0, 1, 2048)
+    pb = P.UotProblem(P.DiscreteMeasure(u, np.full(2048, 1 / 2048)),
+                      P.DiscreteMeasure(u, np.full(2048, 1 / 2048)), P.PowerDistance(2.0),
+                      P.KL(1.0), P.KL(1.0), 0.0)
+    P.eval_primal(pb, big)
+    t0 = time.perf_counter()
+    v = P.eval_primal(pb, big)
+    assert time.perf_counter() - t0 < 0.5
+    assert v == pytest.approx(float(np.sum(big * (u[:, None] - u[None, :]) ** 2)), rel=1e-11)
