@@ -1178,6 +1178,10 @@ int launch_fw_impl(const FwArgs& a0, int batch, cudaStream_t st) {
                           : launch_fw_giant<PW, PK>(a, batch, st, eptb);
     if constexpr (PK == 0) {  // exact power-of-two sizes: constant-size instantiations
       if (a.n == a.m && a.n == FW_THREADS * ept && !std::getenv("UOT_FW_NOFULL")) {
+        if constexpr (!PW) {
+          if (ept == 1) return go(fw1d_kernel<1, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
+          if (ept == 2) return go(fw1d_kernel<2, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
+        }
         if (ept == 4) return go(fw1d_kernel<4, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
         if (ept == 8) return go(fw1d_kernel<8, 0, PW, FW_THREADS, true>, FW_THREADS, smem);
         if constexpr (!PW)

@@ -157,7 +157,7 @@ def test_constant_size_instantiation_is_bit_identical(monkeypatch, step):
     """n = m = 256 x EPT problems (cfg2: 1024) run on kernels instantiated with the
     sizes as compile-time constants (fw1d_kernel.cuh: FULL); only bounds tests fold
     away, so the results equal the general kernel's bit for bit."""
-    for n in (1024, 2048):
+    for n in ((1024, 2048) if step == "pairwise" else (256, 512, 1024, 2048, 4096)):
         x, y, a, b = S.cfg2_batch(batch=3, n=n, m=n, count=3, seed=11)
         a[1, 5:40] = 0.0  # zero-weight atoms too
         r0 = P.fw_solve_batched(x, y, a, b, 1.0, 1.0, 2.0, 25, step)
