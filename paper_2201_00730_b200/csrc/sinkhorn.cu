@@ -671,8 +671,12 @@ __device__ __forceinline__ void tile_sq2(const float* srec, int rr, int clen, co
   }
 }
 
+#ifndef SQ2_MINB
+#define SQ2_MINB 8  // resident CTAs per SM asked of the compiler: 64 registers (44 B of spills) and 32
+                    // warps per SM -- measured 7 / 8 / 9 / 10 CTAs: 488.0 / 496.8 / 492.0 / 488.5 iter/s at cfg3
+#endif
 template <int THREADS, int CP, int RT>
-__global__ void __launch_bounds__(THREADS) sk_main_sq2(MainArgs<float> A) {
+__global__ void __launch_bounds__(THREADS, SQ2_MINB) sk_main_sq2(MainArgs<float> A) {
   const int b = blockIdx.z;
   if (A.done != nullptr && A.done[b]) return;
   const int split = blockIdx.y, S = gridDim.y;
