@@ -1335,9 +1335,15 @@ size_t layout(const Shape& s, int iters, WsLayout& L, Buffers<T>* buf, char* bas
 
 template <class P>
 struct Cfg;
+#ifndef SQ2_THREADS
+#define SQ2_THREADS 128
+#endif
+#ifndef SQ2_RT
+#define SQ2_RT 8
+#endif
 template <int D>
 struct Cfg<SqE32<D>> {
-  static constexpr int THREADS = 128, COLS = 4, RT = 8;
+  static constexpr int THREADS = SQ2_THREADS, COLS = 4, RT = SQ2_RT;
 };
 template <>
 struct Cfg<SqE32N> {
